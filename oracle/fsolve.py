@@ -1,0 +1,100 @@
+"""Oracle F-solves (TEST INFRASTRUCTURE ONLY — see oracle/__init__.py).
+
+F = [−H Aᵀ; A 0]  (eq. f-def) is nonsingular for SPD H
+and full-row-rank A; its inertia is (n negative, m1 positive)
+(Haynsworth).
+
+Two independent ways to apply F⁻¹:
+
+* ``DenseF``  — the explicit block inverse of P:L757–773 (eq. f-inv)
+      F⁻¹ = [ −H⁻¹ + H⁻¹AᵀF_H⁻¹AH⁻¹ ,  H⁻¹AᵀF_H⁻¹ ]
+            [        F_H⁻¹AH⁻¹        ,     F_H⁻¹   ],   F_H = AH⁻¹Aᵀ,
+  applied with LAPACK Cholesky factors of H and of F_H (no LDLᵀ at all).
+* ``SparseF`` — SuperLU LU of F permuted to the x-block order ``x_perm``
+  with the λ block last, NATURAL column order and no pivoting
+  (diag_pivot_thresh = 0), for the sparse configs.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+
+def assemble_F(H, A) -> sp.csr_matrix:
+    """F = [−H Aᵀ; A 0]."""
+    m1 = A.shape[0]
+    if m1 == 0:
+        return sp.csr_matrix(-H)
+    return sp.bmat([[-H, A.T], [A, sp.csr_matrix((m1, m1))]], format="csr")
+
+
+class DenseF:
+    """F⁻¹ through the block-inverse formula f-inv."""
+
+    def __init__(self, H, A):
+        Hd = H.toarray() if sp.issparse(H) else np.asarray(H, dtype=float)
+        Ad = A.toarray() if sp.issparse(A) else np.asarray(A, dtype=float)
+        self.n, self.m1 = Hd.shape[0], Ad.shape[0]
+        self.A = Ad
+        self.cH = sla.cho_factor(Hd, lower=True)           # H = L Lᵀ (H SPD)
+        if self.m1:
+            HiAt = sla.cho_solve(self.cH, Ad.T)              # H⁻¹Aᵀ
+            FH = Ad @ HiAt                                   # F_H = A H⁻¹ Aᵀ (SPD)
+            self.cFH = sla.cho_factor(FH, lower=True)
+        else:
+            self.cFH = None
+
+    def Hinv(self, v):
+        return sla.cho_solve(self.cH, v)
+
+    def solve(self, r1, r2=None):
+        """Return (y, z) = F⁻¹ (r1; r2), block by block as in f-inv."""
+        t = self.Hinv(r1)                                    # H⁻¹ r1
+        if self.m1 == 0:
+            return -t, np.zeros((0,) + np.shape(r1)[1:])
+        if r2 is None:
+            r2 = np.zeros((self.m1,) + np.shape(r1)[1:])
+        # row 2 of f-inv:  z = F_H⁻¹ A H⁻¹ r1 + F_H⁻¹ r2
+        z = sla.cho_solve(self.cFH, self.A @ t) + sla.cho_solve(self.cFH, r2)
+        # row 1 of f-inv:  y = (−H⁻¹ + H⁻¹AᵀF_H⁻¹AH⁻¹) r1 + H⁻¹AᵀF_H⁻¹ r2
+        #                    = −t + H⁻¹Aᵀ z
+        y = -t + self.Hinv(self.A.T @ z)
+        return y, z
+
+
+class SparseF:
+    """F⁻¹ through SuperLU on P F Pᵀ (x block by ``x_perm``, λ block last).
+
+    NATURAL ordering and diag_pivot_thresh=0 keep the given order and static
+    diagonal pivots.
+    """
+
+    def __init__(self, H, A, x_perm=None):
+        n, m1 = H.shape[0], A.shape[0]
+        self.n, self.m1 = n, m1
+        if x_perm is None:
+            x_perm = np.arange(n)
+        self.perm = np.concatenate([np.asarray(x_perm, dtype=np.int64), n + np.arange(m1)])
+        F = assemble_F(H, A).tocsr()
+        Fp = F[self.perm][:, self.perm].tocsc()
+        self.lu = spla.splu(Fp, permc_spec="NATURAL", diag_pivot_thresh=0.0,
+                            options=dict(SymmetricMode=True))
+
+    def solve(self, r1, r2=None):
+        n, m1 = self.n, self.m1
+        if r2 is None:
+            r2 = np.zeros((m1,) + np.shape(r1)[1:])
+        rhs = np.concatenate([r1, r2])
+        sol_p = self.lu.solve(rhs[self.perm])
+        sol = np.empty_like(sol_p)
+        sol[self.perm] = sol_p
+        return sol[:n], sol[n:]
+
+
+def make_fsolver(H, A, x_perm=None, dense_limit=30000):
+    """Dense block formula up to ``dense_limit`` unknowns, SuperLU beyond."""
+    if H.shape[0] + A.shape[0] <= dense_limit and x_perm is None:
+        return DenseF(H, A)
+    return SparseF(H, A, x_perm)

@@ -1,0 +1,120 @@
+"""Oracle KKT pieces of one IPM iteration (TEST INFRASTRUCTURE ONLY).
+
+Notation of PAPER.md §2/§4: slacks s, multipliers ν (inequalities) and λ
+(equalities); S = diag(s), V = diag(ν).
+
+* residuals            r_g, r_e, r_i, r_c (the rhs of eq. augmented,
+                       P:L486–505), with the sign reading r_g = −(Hx+g−Aᵀλ−Cᵀν)
+                       (reading R1) and r_a = r_i + V⁻¹r_c (R2)
+* diag_D               D = V⁻¹S
+* r_nu                 r_ν = −r_a + [C 0]F⁻¹(r_g; r_e)
+* KF_apply             K_F p = D p − [C 0]F⁻¹[Cᵀp; 0]
+* recover              F(Δx;Δλ) = −(r_g + CᵀΔν; r_e)
+* delta_s              Δs = −V⁻¹r_c − DΔν
+* P_L / P_H            P_L = D; P_H = D + C·diag(H)⁻¹·Cᵀ
+                       and the exact form D + CH⁻¹Cᵀ (Theorem 2)
+* step_length          fraction-to-boundary α = min(1, τ·α_max) (reading R3)
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+
+def residuals(qp, x, lam, nu, s, sigma):
+    """Return dict with r_g, r_e, r_i, r_c, r_a, mu and the KKT gradient."""
+    m2 = qp.C.shape[0]
+    mu = float(s @ nu) / m2                                   # μ = sᵀν/m2
+    grad = qp.H @ x + qp.g - qp.A.T @ lam - qp.C.T @ nu       # ∇ₓ Lagrangian
+    r_g = -grad                                              # reading R1 (§0.3 of SURVEY)
+    r_e = qp.A @ x - qp.b
+    r_i = qp.C @ x - s - qp.d
+    r_c = s * nu - sigma * mu
+    r_a = r_i + r_c / nu
+    return dict(r_g=r_g, r_e=r_e, r_i=r_i, r_c=r_c, r_a=r_a, mu=mu, grad=grad)
+
+
+def diag_D(s, nu):
+    """D = V⁻¹S."""
+    return s / nu
+
+
+def r_nu(qp, fs, res):
+    """r_ν = −r_a + [C 0] F⁻¹ (r_g; r_e)."""
+    y, _ = fs.solve(res["r_g"], res["r_e"])
+    return -res["r_a"] + qp.C @ y
+
+
+def KF_apply(qp, fs, D, p):
+    """K_F p = D∘p − [C 0] F⁻¹ [Cᵀp; 0], never forming K_F."""
+    u = qp.C.T @ p
+    w, _ = fs.solve(u, None)
+    return D * p - qp.C @ w
+
+
+def recover(qp, fs, res, dnu):
+    """(Δx, Δλ) from F(Δx;Δλ) = −(r_g + CᵀΔν; r_e)."""
+    return fs.solve(-(res["r_g"] + qp.C.T @ dnu), -res["r_e"])
+
+
+def delta_s(res, D, nu, dnu):
+    """Δs = −V⁻¹r_c − DΔν."""
+    return -res["r_c"] / nu - D * dnu
+
+
+def step_length(s, ds, nu, dnu, tau):
+    """Common step α = min(1, τ·α_max), α_max = sup{α : s+αΔs ≥ 0, ν+αΔν ≥ 0} (reading R3)."""
+    amax = np.inf
+    neg = ds < 0
+    if neg.any():
+        amax = min(amax, float(np.min(-s[neg] / ds[neg])))
+    neg = dnu < 0
+    if neg.any():
+        amax = min(amax, float(np.min(-nu[neg] / dnu[neg])))
+    return min(1.0, tau * amax), amax
+
+
+class PrecondL:
+    """P_L = D (eq. prec-mat-1): z = r / D."""
+
+    def __init__(self, D):
+        self.D = D
+
+    def __call__(self, r):
+        return r / self.D
+
+
+class PrecondNone:
+    """U-KF: no preconditioner."""
+
+    def __call__(self, r):
+        return r.copy()
+
+
+def T_matrix(qp):
+    """T = C·diag(H)⁻¹·Cᵀ, formed once in the setup phase."""
+    dH = qp.H.diagonal()
+    return (qp.C @ sp.diags(1.0 / dH) @ qp.C.T).tocsr()
+
+
+class PrecondH:
+    """P_H = D + T with T = C diag(H)⁻¹ Cᵀ, Cholesky-factored per IPM iteration.
+
+    ``exact=True`` uses the theoretical form P_H = D + C H⁻¹ Cᵀ of Theorem 2
+     — dense, tiny problems only.
+    """
+
+    def __init__(self, qp, D, T=None, exact=False):
+        if exact:
+            Hd = qp.H.toarray()
+            Cd = qp.C.toarray()
+            M = Cd @ np.linalg.solve(Hd, Cd.T)
+        else:
+            M = (T if T is not None else T_matrix(qp)).toarray()
+        P = M + np.diag(D)
+        self.c = sla.cho_factor(P, lower=True)
+        self.P = P
+
+    def __call__(self, r):
+        return sla.cho_solve(self.c, r)

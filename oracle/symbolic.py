@@ -1,0 +1,125 @@
+"""Oracle symbolic structures of the LDLᵀ factor of F (TEST INFRASTRUCTURE ONLY).
+
+The paper factors F once with an LDLᵀ whose factor L_F has
+nz(L_F[:,j]) entries per column.  The structures here
+are what the library's symbolic phase must reproduce bit-exactly, given the
+same x-block permutation:
+
+* ordering: x block by ``x_perm``, then the λ block last in row order;
+* elimination tree and column structures by the definition of symbolic
+  elimination: struct(L[:,j]) = {j} ∪ {i>j : F_ij ≠ 0}
+  ∪ ⋃_{c : parent(c)=j} struct(L[:,c]) \\ {c},   parent(j) = min(struct(j) \\ {j});
+* column counts cc(j) = |struct(L[:,j])| (diagonal included);
+* supernodes: column j joins j−1's supernode iff parent(j−1) = j and
+  cc(j−1) = cc(j) + 1 (then struct(j−1) = {j−1} ∪ struct(j));
+* supernodal tree: parent of supernode J = supernode of parent(last col of J);
+  level(J) = 0 for leaves, else 1 + max level(children);
+* row levels: lev(i) = 1 + max{lev(j) : j < i, L_ij ≠ 0}, 0 for rows with no
+  off-diagonal entry.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import scipy.sparse as sp
+
+
+def permuted_lower_pattern(H, A, x_perm=None):
+    """Column lists of the strictly-lower pattern of P F Pᵀ, F = [−H Aᵀ; A 0]."""
+    n, m1 = H.shape[0], A.shape[0]
+    if x_perm is None:
+        x_perm = np.arange(n)
+    x_perm = np.asarray(x_perm, dtype=np.int64)
+    pinv = np.empty(n, dtype=np.int64)
+    pinv[x_perm] = np.arange(n)
+    N = n + m1
+    Hc = sp.coo_matrix(H)
+    Ac = sp.coo_matrix(A)
+    rows = np.concatenate([pinv[Hc.row], n + Ac.row])
+    cols = np.concatenate([pinv[Hc.col], pinv[Ac.col]])
+    lo = rows > cols
+    P = sp.csc_matrix((np.ones(int(lo.sum())), (rows[lo], cols[lo])), shape=(N, N))
+    P.sum_duplicates()
+    P.sort_indices()
+    return N, [P.indices[P.indptr[j]:P.indptr[j + 1]].astype(np.int64) for j in range(N)]
+
+
+def symbolic_factor(N, lower_cols):
+    """Elimination tree and full column structures (definition, in column order)."""
+    parent = np.full(N, -1, dtype=np.int64)
+    children = [[] for _ in range(N)]
+    struct = [None] * N
+    for j in range(N):
+        parts = [np.array([j], dtype=np.int64), lower_cols[j]]
+        for c in children[j]:
+            sc = struct[c]
+            parts.append(sc[sc != c])
+        sj = np.unique(np.concatenate(parts))
+        struct[j] = sj
+        if len(sj) > 1:
+            parent[j] = int(sj[1])
+            children[int(sj[1])].append(j)
+    return parent, struct
+
+
+def supernodes(parent, cc):
+    """Supernode start columns (with a final sentinel N)."""
+    N = len(parent)
+    starts = [0]
+    for j in range(1, N):
+        if not (parent[j - 1] == j and cc[j - 1] == cc[j] + 1):
+            starts.append(j)
+    starts.append(N)
+    return np.asarray(starts, dtype=np.int64)
+
+
+def supernode_tree(parent, sn_start):
+    ns = len(sn_start) - 1
+    col2sn = np.empty(sn_start[-1], dtype=np.int64)
+    for J in range(ns):
+        col2sn[sn_start[J]:sn_start[J + 1]] = J
+    sparent = np.full(ns, -1, dtype=np.int64)
+    for J in range(ns):
+        p = parent[sn_start[J + 1] - 1]
+        if p >= 0:
+            sparent[J] = col2sn[p]
+    level = np.zeros(ns, dtype=np.int64)
+    for J in range(ns):               # children have smaller indices than parents
+        if sparent[J] >= 0:
+            level[sparent[J]] = max(level[sparent[J]], level[J] + 1)
+    return sparent, level
+
+
+def row_levels(N, struct):
+    lev = np.zeros(N, dtype=np.int64)
+    for j in range(N):
+        sj = struct[j]
+        below = sj[sj > j]
+        if len(below):
+            lev[below] = np.maximum(lev[below], lev[j] + 1)
+    return lev
+
+
+def analyse(H, A, x_perm=None):
+    """All structures, as a dict of int64 arrays."""
+    N, lower = permuted_lower_pattern(H, A, x_perm)
+    parent, struct = symbolic_factor(N, lower)
+    cc = np.array([len(s) for s in struct], dtype=np.int64)
+    sn = supernodes(parent, cc)
+    sparent, slevel = supernode_tree(parent, sn)
+    sn_rows = np.concatenate([struct[sn[J]] for J in range(len(sn) - 1)]) if N else np.zeros(0, np.int64)
+    sn_rowptr = np.concatenate([[0], np.cumsum([cc[sn[J]] for J in range(len(sn) - 1)])]).astype(np.int64)
+    rlev = row_levels(N, struct)
+    return dict(N=N, parent=parent, colcount=cc, sn_start=sn, sn_parent=sparent,
+                sn_level=slevel, sn_rowptr=sn_rowptr, sn_rows=sn_rows, row_level=rlev,
+                nnz_L=int(cc.sum()), struct=struct)
+
+
+def struct_hash(arr) -> str:
+    """64-bit hash of an int64 array together with its length."""
+    a = np.ascontiguousarray(np.asarray(arr, dtype=np.int64))
+    h = hashlib.blake2b(digest_size=8)
+    h.update(np.int64(len(a)).tobytes())
+    h.update(a.tobytes())
+    return h.hexdigest()

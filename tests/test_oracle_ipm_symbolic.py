@@ -1,0 +1,189 @@
+"""Pins for oracle/ipm.py, oracle/symbolic.py, oracle/costs.py and qpgen (CPU only)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+import qpgen
+from oracle import costs, symbolic
+from oracle.fsolve import assemble_F
+from oracle.ipm import ipm_solve
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ----------------------------------------------------------------------------- qpgen
+def test_generator_deterministic_and_feasible():
+    a, b = qpgen.make("c0"), qpgen.make("c0")
+    for M1, M2 in ((a.H, b.H), (a.A, b.A), (a.C, b.C)):
+        assert (M1 != M2).nnz == 0
+    assert np.array_equal(a.g, b.g)
+    assert (a.n, a.m1, a.m2) == (200, 50, 300)
+    assert np.diff(a.A.indptr).tolist() == [3] * 50 and np.diff(a.C.indptr).tolist() == [4] * 300
+    assert np.allclose(a.A @ a.x0, a.b) and np.all(a.C @ a.x0 - a.d > 0)
+    assert np.allclose((a.H - a.H.T).toarray(), 0)
+    assert np.linalg.eigvalsh(a.H.toarray()).min() > 0.09     # GᵀG + 0.1 I
+
+
+def test_grid_nd_perm_is_permutation():
+    p = qpgen.grid_nd_perm(37)
+    assert sorted(p.tolist()) == list(range(37 * 37))
+
+
+# ----------------------------------------------------------------------------- IPM
+def brute_force_active_set(qp, s, tol=1e-6):
+    """Solve the equality QP on the active set {i : s_i < tol} densely."""
+    act = np.nonzero(s < tol)[0]
+    H, A, C = qp.H.toarray(), qp.A.toarray(), qp.C.toarray()[act]
+    n, m1, ma = qp.n, qp.m1, len(act)
+    K = np.zeros((n + m1 + ma,) * 2)
+    K[:n, :n] = H
+    K[:n, n:n + m1] = A.T
+    K[:n, n + m1:] = C.T
+    K[n:n + m1, :n] = A
+    K[n + m1:, :n] = C
+    rhs = np.concatenate([-qp.g, qp.b, qp.d[act]])
+    sol = np.linalg.solve(K, rhs)
+    x = sol[:n]
+    # multipliers: Hx + g = Aᵀλ + Cᵀν with the sign convention of the KKT system
+    nu_act = -sol[n + m1:]
+    return x, nu_act, act
+
+
+def test_ipm_direct_converges_and_matches_brute_force():
+    qp = qpgen.make("c0")
+    r = ipm_solve(qp, direct=True, ipm_tol=1e-10)
+    assert r.converged and r.n_ipm < 40
+    assert r.s.min() > 0 and r.nu.min() > 0
+    x, nu_act, act = brute_force_active_set(qp, r.s)
+    assert np.all(nu_act >= -1e-8)
+    inact = np.setdiff1d(np.arange(qp.m2), act)
+    assert np.all((qp.C @ x - qp.d)[inact] > 0)
+    obj = 0.5 * x @ (qp.H @ x) + qp.g @ x
+    assert abs(obj - r.objective) <= 1e-9 * abs(obj)
+
+
+@pytest.mark.parametrize("pc", ["low", "high"])
+def test_ipm_inexact_converges_to_direct_objective(pc):
+    qp = qpgen.make("c0")
+    ref = ipm_solve(qp, direct=True, ipm_tol=1e-10)
+    r = ipm_solve(qp, precond=pc, ipm_tol=1e-10)
+    assert r.converged
+    assert abs(r.objective - ref.objective) <= 1e-8 * abs(ref.objective)   # north_star gate
+    # KKT at convergence
+    grad = qp.H @ r.x + qp.g - qp.A.T @ r.lam - qp.C.T @ r.nu
+    assert np.abs(grad).max() <= 1e-10 * (1 + np.abs(qp.g).max())
+    assert np.abs(qp.C @ r.x - r.s - qp.d).max() <= 1e-10 * (1 + np.abs(qp.d).max())
+
+
+def test_ipm_fixed_eps_stalls_on_ri_but_objective_accurate():
+    """Reading R4 evidence: fixed ε = 1e-3 keeps ‖r_i‖ ≈ ε-level (never meets 1e-8),
+    while the objective loss stays below the paper's 6e-7."""
+    qp = qpgen.make("c0")
+    ref = ipm_solve(qp, direct=True, ipm_tol=1e-10)
+    r = ipm_solve(qp, precond="high", forcing=False, max_ipm=30)
+    assert not r.converged
+    assert r.trace[-1]["ri"] > 1e-6
+    assert abs(r.objective - ref.objective) <= 6e-7 * abs(ref.objective)
+
+
+def test_syqp_family_ipm():
+    for m1 in (1, 16, 32):
+        qp = qpgen.make_syqp(32, m1)
+        r = ipm_solve(qp, precond="high")
+        ref = ipm_solve(qp, direct=True)
+        assert r.converged and ref.converged
+        assert abs(r.objective - ref.objective) <= 1e-7 * max(1.0, abs(ref.objective))
+
+
+# ----------------------------------------------------------------------------- symbolic
+def _pattern_matrix(kind, n):
+    if kind == "diagonal":
+        return sp.identity(n, format="csr")
+    if kind == "tridiagonal":
+        return sp.diags([np.ones(n - 1), 4 * np.ones(n), np.ones(n - 1)], [-1, 0, 1], format="csr")
+    if kind == "arrowhead":
+        M = np.eye(n) * 4
+        M[-1, :] = 1
+        M[:, -1] = 1
+        M[-1, -1] = n + 4
+        return sp.csr_matrix(M)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("ex", GOLD["symbolic_cholesky"], ids=lambda e: e["kind"])
+def test_symbolic_spec_examples(ex):
+    """column counts / nnz(L) of small patterns (m1 = 0, F = −H)."""
+    H = _pattern_matrix(ex["kind"], ex["n"])
+    st = symbolic.analyse(H, sp.csr_matrix((0, ex["n"])))
+    assert st["nnz_L"] == ex["nnz_L"]
+    if "colcounts" in ex:
+        assert st["colcount"].tolist() == ex["colcounts"]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_symbolic_matches_numeric_ldlt_pattern(seed):
+    """Symbolic structure = pattern of the numeric LDLᵀ of P F Pᵀ (static pivots,
+    random values ⇒ no cancellation), etree parent = first sub-diagonal nonzero."""
+    qp = qpgen.scaled_random_qp(25, 6, 10, seed=seed, g_nnz=2, a_nnz=2, c_nnz=2)
+    perm = np.random.default_rng(seed).permutation(qp.n)
+    st = symbolic.analyse(qp.H, qp.A, perm)
+    P = np.concatenate([perm, qp.n + np.arange(qp.m1)])
+    F = assemble_F(qp.H, qp.A).toarray()[np.ix_(P, P)]
+    # random values on the pattern of P F Pᵀ with a dominant diagonal: no cancellation
+    rng = np.random.default_rng(100 + seed)
+    R = np.where(F != 0, rng.uniform(0.5, 1.0, F.shape), 0.0)
+    N = F.shape[0]
+    A = np.tril(R, -1) + np.tril(R, -1).T
+    A += np.diag(np.abs(A).sum(axis=1) + 1.0)
+    Lm = np.eye(N)
+    for j in range(N):
+        d = A[j, j]
+        Lm[j + 1:, j] = A[j + 1:, j] / d
+        A[j + 1:, j + 1:] -= np.outer(Lm[j + 1:, j], A[j, j + 1:])
+    pattern = [set(np.nonzero(Lm[:, j] != 0)[0].tolist()) | {j} for j in range(N)]
+    for j in range(N):
+        assert set(st["struct"][j].tolist()) == pattern[j]
+        below = sorted(pattern[j] - {j})
+        assert st["parent"][j] == (below[0] if below else -1)
+    # supernode property: struct(j−1) = {j−1} ∪ struct(j) inside a supernode
+    sn = st["sn_start"]
+    for J in range(len(sn) - 1):
+        for j in range(sn[J] + 1, sn[J + 1]):
+            assert pattern[j - 1] == {j - 1} | pattern[j]
+    # row levels by longest dependency path
+    lev = np.zeros(N, dtype=int)
+    for i in range(N):
+        deps = [j for j in range(i) if i in pattern[j]]
+        lev[i] = 1 + max(lev[j] for j in deps) if deps else 0
+    assert lev.tolist() == st["row_level"].tolist()
+
+
+# ----------------------------------------------------------------------------- costs
+@pytest.mark.parametrize("ex", GOLD["kernel_costs"], ids=lambda e: e["kind"])
+def test_kernel_cost_spec_examples(ex):
+    H = _pattern_matrix(ex["kind"], ex["n"])
+    st = symbolic.analyse(H, sp.csr_matrix((0, ex["n"])))
+    assert costs.c_fact(st["colcount"]) == ex["c_fact"]
+    assert costs.c_trsv(st["nnz_L"]) == ex["c_trsv"]
+
+
+@pytest.mark.parametrize("ex", GOLD["spmv"], ids=lambda e: e["cite"])
+def test_spmv_spec_examples(ex):
+    B = sp.csr_matrix(np.array(ex["B_dense"], dtype=float))
+    assert np.allclose(B @ np.array(ex["v"], dtype=float), ex["out"])
+    assert costs.c_spmv(B) == ex["flops"]
+
+
+def test_cost_model_hand_cases():
+    qp = qpgen.make("c0")
+    assert costs.c_spmm_BDBt(sp.identity(9, format="csr")) == 9              # C = I → n
+    assert costs.pl_kf(qp, 123, 45, []) == 123                                # N_I = 0 → c_fact(F)
+    t, s, tp = 2 * 45, 2 * qp.C.nnz, 2 * 7
+    rhs = 2 * qp.H.nnz + 4 * qp.A.nnz + 4 * qp.C.nnz
+    hand = 123 + costs.c_spmm_BDBt(qp.C) + sum(4 * t + 2 * s + 2 * k * t + 2 * k * s + 11 + 2 * k * tp
+                                               for k in (3, 4)) + 2 * rhs
+    assert costs.ph_kf(qp, 123, 45, 11, 7, [3, 4]) == hand
