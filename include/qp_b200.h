@@ -1,0 +1,188 @@
+/*
+ * qp_b200.h — C ABI of the B200-native single-factorization inexact IPM
+ * (arXiv 2104.12916, "PAPER.md" in the citations below).
+ *
+ * The library solves convex QPs
+ *
+ *     min ½xᵀHx + gᵀx   s.t.  Ax = b,  Cx ≥ d
+ *
+ * with a primal-dual IPM whose Newton system is reduced to the SPD
+ * inequality-constraint-reduced system (eq. ineq-const-reduced)
+ *
+ *     K_F Δν = r_ν,   K_F = D − [C 0] F⁻¹ [Cᵀ; 0],   F = [−H Aᵀ; A 0],
+ *     r_ν = −r_a + [C 0] F⁻¹ (r_g; r_e),
+ *
+ * solved by PCG with P_L = D or
+ * P_H = D + C·diag(H)⁻¹·Cᵀ.  F is LDLᵀ-factored ONCE
+ * and every K_F product is Cᵀ-SpMV → F-solve → C-SpMV
+ * (P:L144).  (Δx, Δλ) are recovered from F(Δx;Δλ) = −(r_g + CᵀΔν; r_e)
+ * and Δs = −V⁻¹r_c − DΔν.
+ *
+ * All arithmetic is fp64 and runs in hand-written sm_100a CUDA kernels; there
+ * is no CPU fallback: every compute entry point returns QP_ECUDA when no
+ * usable GPU is present.
+ *
+ * Conventions (all entry points):
+ *  - Return value: a qp_status; on error a message is kept per context
+ *    (qp_last_error).  QP_MAXIT is a non-fatal status.
+ *  - Ownership: every pointer argument is BORROWED for the duration of the
+ *    call and never retained.  qp_setup deep-copies the problem to the GPU.
+ *    Output buffers are caller-owned.
+ *  - Vectors: by default host pointers (the library copies in/out).  With
+ *    qp_setup_opts.vectors_on_device = 1, the vector arguments of pcg_solve,
+ *    ipm_factor_once, qp_f_solve, qp_kf_apply and the x/lam/nu/s buffers of
+ *    qp_ipm_result are DEVICE pointers on opts.device.
+ *  - Call order: qp_setup → ipm_factor_once → any number of pcg_solve /
+ *    ipm_solve / qp_ipm_* calls.  Anything else returns QP_ESTATE.
+ *  - Streams: all work is issued on opts.stream (a cudaStream_t; NULL = the
+ *    library's own stream).  Calls are synchronous with respect to the host.
+ */
+#ifndef QP_B200_H
+#define QP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qp_ctx qp_ctx; /* opaque; one per process / GPU */
+
+/* Compressed sparse row matrix, host pointers, canonical: column indices
+ * sorted and unique within each row, 0-based.  nrows+1 indptr entries. */
+typedef struct {
+  int64_t nrows, ncols;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const double* values;
+} qp_csr;
+
+typedef enum {
+  QP_OK = 0,
+  QP_MAXIT = 1,        /* non-fatal: PCG stopped at maxit (the IPM continues) */
+  QP_EINVAL = -1,      /* bad CSR / dimensions / non-finite input */
+  QP_ENOTSPD = -2,     /* F inertia != (n negative, m1 positive): H not SPD or A
+                          rank-deficient; or a P_H pivot <= 0 */
+  QP_EBREAKDOWN = -3,  /* PCG breakdown: pᵀq <= 0 or non-finite */
+  QP_ENOMEM = -4,
+  QP_ECUDA = -5,       /* CUDA error or no usable sm_100 device */
+  QP_ENCCL = -6,
+  QP_ESTATE = -7       /* call order violated */
+} qp_status;
+
+typedef enum {
+  QP_PREC_NONE = 0, /* U-KF: unpreconditioned CG */
+  QP_PREC_LOW = 1,  /* PL-KF: P_L = D */
+  QP_PREC_HIGH = 2  /* PH-KF: P_H = D + C diag(H)^-1 C^T, Cholesky per IPM iteration */
+} qp_precond;
+
+typedef struct {
+  int device;              /* CUDA device ordinal */
+  void* stream;            /* cudaStream_t or NULL */
+  int rank, world;         /* SPMD rank / size; world = 1 for single GPU */
+  const void* nccl_uid;    /* 128-byte ncclUniqueId (world > 1) or NULL */
+  const int64_t* x_perm;   /* optional fill-reducing order of the x block (new→old,
+                              length n); NULL = the library's minimum-degree order */
+  int vectors_on_device;   /* see Conventions */
+  int64_t workspace_limit_bytes; /* multifrontal workspace cap; 0 = 120 GiB */
+} qp_setup_opts;
+
+/* Copy the QP to the GPU and validate it.  H: full symmetric n×n (both
+ * triangles stored); A: m1×n, m1 >= 0 (m1 = 0 ⇒ F = −H); C: m2×n, m2 >= 1.
+ * g (n), b (m1), d (m2): host arrays.  Errors: QP_EINVAL on shape/CSR/NaN
+ * problems, QP_ECUDA without a GPU, QP_ENOMEM. */
+int qp_setup(qp_ctx** ctx, const qp_csr* H, const qp_csr* A, const qp_csr* C,
+             const double* g, const double* b, const double* d, const qp_setup_opts* opts);
+
+/* Setup phase: ordering (x block by x_perm or minimum
+ * degree, λ block last), symbolic analysis, multifrontal numeric LDLᵀ of F
+ * on the GPU with static 1×1 pivots and an inertia check (x pivots < 0,
+ * λ pivots > 0) → QP_ENOTSPD on failure.  For QP_PREC_HIGH also
+ * T = C·diag(H)⁻¹·Cᵀ and the symbolic analysis of D + T; D0 (m2
+ * values, may be NULL = ones) gives the first numeric P_H factor. */
+int ipm_factor_once(qp_ctx* ctx, const double* D0, qp_precond p);
+
+/* Solve K_F(D_k) Δν = rhs from Δν = 0 by PCG with the preconditioner chosen
+ * at ipm_factor_once (P_H is refactored when D_k changed).  Stop when
+ * ‖r‖₂ <= tol·‖rhs‖₂ or after maxit iterations (→ QP_MAXIT).
+ * D_k, rhs, dnu_out: m2 values.  iters / relres may be NULL. */
+int pcg_solve(qp_ctx* ctx, const double* D_k, const double* rhs, double tol, int32_t maxit,
+              double* dnu_out, int32_t* iters, double* relres);
+
+typedef struct {
+  double ipm_tol;      /* 1e-8 */
+  double pcg_tol;      /* ε = 1e-3 */
+  double sigma;        /* 0.1 */
+  double tau;          /* 0.995 */
+  int32_t max_ipm;     /* 100 */
+  int32_t pcg_maxit;   /* 2000 */
+  int32_t pcg_forcing; /* 1: ε_k = min(ε, μ_k) (reading R4); 0: fixed ε */
+} qp_ipm_opts;
+
+typedef struct {
+  double *x, *lam, *nu, *s; /* caller buffers (n, m1, m2, m2) or NULL */
+  double objective;         /* ½xᵀHx + gᵀx */
+  int32_t n_ipm;            /* IPM iterations taken (N_I) */
+  int32_t* pcg_iters;       /* caller buffer of length max_ipm or NULL (n_kr per iteration) */
+  int32_t status;           /* QP_OK if converged, QP_MAXIT if max_ipm reached */
+  int32_t pcg_total;        /* Σ n_kr */
+  double t_setup_s, t_solve_s;
+  double mu, rg_inf, re_inf, ri_inf; /* final μ and residual ∞-norms */
+} qp_ipm_result;
+
+/* The inexact IPM (readings R1–R4): start x=0, λ=0, ν=1,
+ * s=|d|+1; per iteration residuals → r_ν → PCG → recovery → Δs → common
+ * fraction-to-boundary step; stop on the KKT test of DESIGN.md. */
+int ipm_solve(qp_ctx* ctx, const qp_ipm_opts* o, qp_ipm_result* r);
+
+/* Step-wise IPM control (bench / tests): qp_ipm_init resets the iterate to
+ * the starting point; qp_ipm_iterate runs up to nsteps IPM iterations
+ * (stopping early at convergence) and fills r (vectors only when non-NULL);
+ * *done = 1 once converged. */
+int qp_ipm_init(qp_ctx* ctx, const qp_ipm_opts* o);
+int qp_ipm_iterate(qp_ctx* ctx, int32_t nsteps, qp_ipm_result* r, int32_t* done);
+
+/* Component entry points (parity tests; same conventions):
+ * qp_f_solve:  (y; z) = F⁻¹ (r1; r2), vectors in the ORIGINAL order,
+ *              rhs/out of length n + m1 (a2–a4 of SURVEY §8(a)).
+ * qp_kf_apply: q = K_F(D) p (a1–a5). */
+int qp_f_solve(qp_ctx* ctx, const double* rhs, double* out);
+int qp_kf_apply(qp_ctx* ctx, const double* D, const double* p, double* q);
+
+/* Structure export for bit-exact parity.  which:
+ *  0 perm (new→old, N = n+m1)  1 etree parent  2 column counts
+ *  3 supernode starts (ns+1)   4 supernode parent  5 supernode level
+ *  6 supernode row pointer (ns+1)  7 supernode rows  8 row levels
+ *  10.. the same for the P_H factor (m2 unknowns).
+ * Call with out = NULL to get *len; then with a buffer of *len int64. */
+int qp_get_structure(qp_ctx* ctx, int32_t which, int64_t* out, int64_t* len);
+
+typedef struct {
+  int64_t n, m1, m2, nnz_H, nnz_A, nnz_C;
+  int64_t nnz_LF, n_supernodes_F, n_blocks_F, n_levels_F, row_levels_F;
+  int64_t nnz_LPH, n_supernodes_PH;
+  int64_t workspace_bytes, factor_bytes;
+  double c_fact_F, c_fact_PH;        /* paper model flops Σ nz(L[:,j])² */
+  double t_symbolic_s, t_factor_s, t_factor_ph_s;
+  double pcg_bytes_per_iter;         /* algorithmic bytes B_it */
+  double pcg_flops_per_iter;         /* 2c_trsv(L_F) + 2c_spmv(C) (+2c_trsv(L_PH)) */
+  double sweep_bytes_F;              /* algorithmic bytes of one L_F sweep: 8·nnz(L_F) */
+} qp_stats;
+int qp_get_stats(qp_ctx* ctx, qp_stats* s);
+
+/* Kernel-time accounting with CUDA events on the library stream.
+ * qp_profile(ctx, 1) enables, 0 disables and clears.  qp_profile_read
+ * returns, per class, accumulated ms and launch count:
+ *  0 F forward sweep, 1 F backward sweep, 2 K_F q-SpMV (a5), 3 PCG vector
+ *  updates (a6), 4 P_H sweeps (a7), 5 P_H refactor (a8), 6 IPM rhs (a9),
+ *  7 other. */
+int qp_profile(qp_ctx* ctx, int32_t enable);
+int qp_profile_read(qp_ctx* ctx, double* ms /*8*/, int64_t* count /*8*/);
+
+const char* qp_last_error(const qp_ctx* ctx);
+void qp_free(qp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QP_B200_H */

@@ -1,0 +1,1097 @@
+// C ABI (include/qp_b200.h): host orchestration of the single-factorization
+// inexact IPM (arXiv 2104.12916) on one B200.  Every arithmetic step runs in
+// the kernels of kernels.cu; this file does validation, symbolic planning
+// (symbolic.cpp), device memory, and the IPM / PCG control flow.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/qp_b200.h"
+#include "kernels.cuh"
+#include "symbolic.h"
+
+using namespace qpb;
+
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+struct HostCSR {
+  int64_t nrows = 0, ncols = 0;
+  std::vector<int64_t> p;
+  std::vector<int32_t> i;
+  std::vector<double> v;
+  int64_t nnz() const { return (int64_t)i.size(); }
+};
+
+HostCSR transpose(const HostCSR& A) {
+  HostCSR T;
+  T.nrows = A.ncols;
+  T.ncols = A.nrows;
+  T.p.assign(T.nrows + 1, 0);
+  for (int32_t c : A.i) T.p[c + 1]++;
+  for (int64_t r = 0; r < T.nrows; ++r) T.p[r + 1] += T.p[r];
+  T.i.resize(A.nnz());
+  T.v.resize(A.nnz());
+  std::vector<int64_t> pos(T.p.begin(), T.p.end() - 1);
+  for (int64_t r = 0; r < A.nrows; ++r)
+    for (int64_t q = A.p[r]; q < A.p[r + 1]; ++q) {
+      int64_t d = pos[A.i[q]]++;
+      T.i[d] = (int32_t)r;
+      T.v[d] = A.v[q];
+    }
+  return T;
+}
+
+// B = A(rowperm, :) with columns renumbered by colmap (old col → new col), rows sorted.
+HostCSR permute(const HostCSR& A, const std::vector<int64_t>* rowperm, const std::vector<int64_t>* colmap) {
+  HostCSR B;
+  B.nrows = A.nrows;
+  B.ncols = A.ncols;
+  B.p.assign(B.nrows + 1, 0);
+  B.i.resize(A.nnz());
+  B.v.resize(A.nnz());
+  std::vector<std::pair<int32_t, double>> tmp;
+  int64_t w = 0;
+  for (int64_t r = 0; r < B.nrows; ++r) {
+    int64_t ro = rowperm ? (*rowperm)[r] : r;
+    tmp.clear();
+    for (int64_t q = A.p[ro]; q < A.p[ro + 1]; ++q)
+      tmp.emplace_back(colmap ? (int32_t)(*colmap)[A.i[q]] : A.i[q], A.v[q]);
+    std::sort(tmp.begin(), tmp.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    for (auto& e : tmp) {
+      B.i[w] = e.first;
+      B.v[w] = e.second;
+      ++w;
+    }
+    B.p[r + 1] = w;
+  }
+  return B;
+}
+
+struct DeviceArena {
+  std::vector<void*> ptrs;
+  size_t bytes = 0;
+  ~DeviceArena() { release(); }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+    bytes = 0;
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    size_t b = std::max<size_t>(1, n) * sizeof(T);
+    if (cudaMalloc(&p, b) != cudaSuccess) throw std::bad_alloc();
+    ptrs.push_back(p);
+    bytes += b;
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, cudaStream_t s) {
+    T* d = alloc<T>(v.size());
+    if (!v.empty()) cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    return d;
+  }
+  template <class T>
+  T* zeros(size_t n, cudaStream_t s) {
+    T* d = alloc<T>(n);
+    cudaMemsetAsync(d, 0, std::max<size_t>(1, n) * sizeof(T), s);
+    return d;
+  }
+};
+
+struct Factor {
+  Symbolic S;
+  DevFactor d{};
+  DeviceArena mem;
+  bool ready = false;
+  int64_t fs_bytes = 0, ws_bytes = 0;
+};
+
+DevCSR upload_csr(DeviceArena& mem, const HostCSR& A, cudaStream_t s) {
+  DevCSR d;
+  d.nrows = A.nrows;
+  d.ncols = A.ncols;
+  d.nnz = A.nnz();
+  d.p = mem.upload(A.p, s);
+  d.i = mem.upload(A.i, s);
+  d.v = mem.upload(A.v, s);
+  return d;
+}
+
+}  // namespace
+
+struct qp_ctx {
+  std::string err;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int vectors_on_device = 0;
+  int rank = 0, world = 1;
+  int64_t ws_limit = 0;
+  int64_t n = 0, m1 = 0, m2 = 0;
+  HostCSR H, A, C;
+  std::vector<double> g, b, d;
+  std::vector<int64_t> xperm_user;
+  bool setup_done = false, factored = false;
+  int precond = 1;
+  int sm_count = 148;
+  int vgrid = 148 * 4;     // grid for vector kernels (fixed ⇒ deterministic reductions)
+  int tgrid = 148;         // persistent trsv grid
+
+  // ordering + permuted operators
+  std::vector<int64_t> perm;  // new → old for x block (n)
+  DeviceArena mem;            // problem + vectors
+  DevCSR Hf{}, Af{}, Atf{}, Cf{}, Ctf{}, Cnu{};
+  double *gf = nullptr, *bv = nullptr, *dv = nullptr;
+  int64_t* perm_dev = nullptr;   // N: factor position → original index (x: perm, λ: n+i)
+  Factor FF;                     // LDLᵀ of F
+  Factor FP;                     // Cholesky (LDLᵀ, positive pivots) of P_H
+  // P_H extras
+  std::vector<int64_t> perm_ph;
+  int64_t* perm_ph_dev = nullptr;
+  int64_t* t_row = nullptr;
+  int32_t* t_col = nullptr;
+  double* t_val = nullptr;
+  int64_t nnz_t = 0;
+  double* hdiag = nullptr;
+  double* D_ph_last = nullptr;   // D of the current P_H numeric factor
+  bool ph_valid = false;
+  double t_factor_ph = 0;
+  int64_t ph_refactors = 0;
+
+  // vectors
+  double *xl = nullptr, *nu = nullptr, *s = nullptr;          // iterate (x_f; λ), ν, s
+  double *rgre = nullptr, *rhs2 = nullptr, *xbuf = nullptr;   // (r_g; r_e), recovery rhs, sweep buffer
+  double *rc = nullptr, *ra = nullptr, *Dk = nullptr, *rnu = nullptr, *ds = nullptr, *dxl = nullptr;
+  double *px = nullptr, *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *xph = nullptr;
+  double *vin = nullptr, *vin2 = nullptr, *vout = nullptr;  // staging for host I/O
+  double* partial = nullptr;
+  PcgState* pst = nullptr;
+  IpmState* ist = nullptr;
+  PcgState* h_pst = nullptr;  // pinned
+  IpmState* h_ist = nullptr;  // pinned
+
+  // IPM control
+  qp_ipm_opts opts{};
+  bool ipm_initialised = false;
+  bool ipm_converged = false;
+  int32_t ipm_k = 0;
+  std::vector<int32_t> pcg_hist;
+  double gmax = 0, bmax = 0, dmax = 0;
+  double t_symbolic = 0, t_factor = 0;
+
+  // profiling
+  bool prof = false;
+  struct Ev { int cls; cudaEvent_t a, b; };
+  std::vector<Ev> evs;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[8] = {0};
+  int64_t prof_cnt[8] = {0};
+
+  cudaEvent_t get_ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  int begin(int cls) {
+    if (!prof) return -1;
+    Ev e{cls, get_ev(), get_ev()};
+    cudaEventRecord(e.a, stream);
+    evs.push_back(e);
+    return (int)evs.size() - 1;
+  }
+  void end(int h) {
+    if (h < 0) return;
+    cudaEventRecord(evs[h].b, stream);
+  }
+  void harvest() {
+    if (evs.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto& e : evs) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      prof_ms[e.cls] += ms;
+      prof_cnt[e.cls] += 1;
+      pool.push_back(e.a);
+      pool.push_back(e.b);
+    }
+    evs.clear();
+  }
+  ~qp_ctx() {
+    harvest();
+    for (auto e : pool) cudaEventDestroy(e);
+    if (h_pst) cudaFreeHost(h_pst);
+    if (h_ist) cudaFreeHost(h_ist);
+    FF.mem.release();
+    FP.mem.release();
+    mem.release();
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int fail(qp_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_check(qp_ctx* c, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, QP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return QP_OK;
+}
+
+int sync_check(qp_ctx* c, const char* where) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, QP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return QP_OK;
+}
+
+std::string check_csr(const qp_csr* M, int64_t nr, int64_t nc, const char* name, HostCSR& out) {
+  if (!M) return std::string(name) + " is NULL";
+  if (M->nrows != nr || M->ncols != nc)
+    return std::string(name) + " has shape " + std::to_string(M->nrows) + "x" + std::to_string(M->ncols) +
+           ", expected " + std::to_string(nr) + "x" + std::to_string(nc);
+  if (nr > 0 && (!M->indptr)) return std::string(name) + ": NULL indptr";
+  out.nrows = nr;
+  out.ncols = nc;
+  out.p.assign(M->indptr, M->indptr + nr + 1);
+  if (out.p[0] != 0) return std::string(name) + ": indptr[0] != 0";
+  for (int64_t r = 0; r < nr; ++r)
+    if (out.p[r + 1] < out.p[r]) return std::string(name) + ": indptr not monotone";
+  int64_t nnz = out.p[nr];
+  if (nnz > 0 && (!M->indices || !M->values)) return std::string(name) + ": NULL indices/values";
+  out.i.assign(M->indices, M->indices + nnz);
+  out.v.assign(M->values, M->values + nnz);
+  for (int64_t r = 0; r < nr; ++r)
+    for (int64_t q = out.p[r]; q < out.p[r + 1]; ++q) {
+      if (out.i[q] < 0 || out.i[q] >= nc) return std::string(name) + ": column index out of range";
+      if (q > out.p[r] && out.i[q] <= out.i[q - 1]) return std::string(name) + ": columns not sorted/unique";
+      if (!std::isfinite(out.v[q])) return std::string(name) + ": non-finite value";
+    }
+  return "";
+}
+
+// Upload a symbolic plan and allocate numeric storage for one factor.
+std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
+  Symbolic& S = F.S;
+  cudaStream_t st = c->stream;
+  if (S.ws_size * 8 > ws_limit)
+    return "multifrontal workspace " + std::to_string(S.ws_size * 8 / (1 << 20)) + " MiB exceeds the limit";
+  try {
+    DeviceArena& m = F.mem;
+    DevFactor& d = F.d;
+    d.N = S.N;
+    d.ns = S.ns;
+    d.nb = S.nb;
+    d.n_tiles = (int64_t)S.tile_blk.size();
+    d.n_fwd_tasks = (int64_t)S.fwd_tasks.size();
+    d.n_bwd_tasks = (int64_t)S.bwd_tasks.size();
+    d.sn_start = m.upload(S.sn_start, st);
+    d.sn_rowptr = m.upload(S.sn_rowptr, st);
+    d.sn_rows = m.upload(S.sn_rows, st);
+    d.front_off = m.upload(S.front_off, st);
+    d.sn_blk0 = m.upload(S.sn_blk0, st);
+    d.blk_col0 = m.upload(S.blk_col0, st);
+    d.blk_w = m.upload(S.blk_w, st);
+    d.blk_noff = m.upload(S.blk_noff, st);
+    d.blk_rows = m.upload(S.blk_rows, st);
+    d.blk_inv = m.upload(S.blk_inv, st);
+    d.blk_off = m.upload(S.blk_off, st);
+    d.tile_blk = m.upload(S.tile_blk, st);
+    d.tile_r0 = m.upload(S.tile_r0, st);
+    d.tile_nr = m.upload(S.tile_nr, st);
+    d.tile_dest = m.upload(S.tile_dest, st);
+    d.fwd_tasks = m.upload(S.fwd_tasks, st);
+    d.bwd_tasks = m.upload(S.bwd_tasks, st);
+    d.fwd_expect = m.upload(S.fwd_expect, st);
+    d.bwd_expect = m.upload(S.bwd_expect, st);
+    d.ws = m.alloc<double>(S.ws_size);
+    d.fstore = m.zeros<double>(S.fs_size, st);
+    d.Dpiv = m.zeros<double>(S.N, st);
+    d.pivsign = m.upload(S.pivsign, st);
+    d.acc = m.zeros<double>(S.N, st);
+    d.tacc = m.zeros<double>(S.N, st);
+    d.cnt_f = m.zeros<unsigned long long>(S.nb, st);
+    d.cnt_b = m.zeros<unsigned long long>(S.nb, st);
+    d.ready_f = m.zeros<unsigned int>(S.nb, st);
+    d.ready_b = m.zeros<unsigned int>(S.nb, st);
+    d.sweep = m.zeros<unsigned int>(4, st);
+    d.asm_dst = m.upload(S.asm_dst, st);
+    d.asm_val = m.upload(S.asm_val, st);
+    d.asm_src = m.upload(S.asm_src, st);
+    d.n_asm = (int64_t)S.asm_dst.size();
+    d.diag_dst = m.upload(S.diag_dst, st);
+    d.relind = m.upload(S.relind, st);
+    d.relind_off = m.upload(S.relind_off, st);
+    d.grp_P = m.upload(S.grp_P, st);
+    d.grp_pc = m.upload(S.grp_pc, st);
+    d.grp_ptr = m.upload(S.grp_ptr, st);
+    d.grp_K = m.upload(S.grp_K, st);
+    d.grp_j = m.upload(S.grp_j, st);
+    d.act = m.upload(S.act, st);
+    d.pan_pref = m.upload(S.pan_pref, st);
+    d.upd_pref = m.upload(S.upd_pref, st);
+    d.status = m.zeros<int>(1, st);
+    F.fs_bytes = S.fs_size * 8;
+    F.ws_bytes = S.ws_size * 8;
+  } catch (std::bad_alloc&) {
+    return "cudaMalloc failed (factor storage)";
+  }
+  return "";
+}
+
+// Numeric multifrontal factorization (assembly → per level: extend-add, blocked steps).
+int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D, const int64_t* dperm,
+                   const char* what) {
+  cudaStream_t st = c->stream;
+  const Symbolic& S = F.S;
+  cudaMemsetAsync(F.d.ws, 0, (size_t)S.ws_size * 8, st);
+  cudaMemsetAsync(F.d.status, 0, sizeof(int), st);
+  mf_assemble(F.d, src_vals, st);
+  if (D) mf_assemble_diag_add(F.d, D, dperm, st);
+  size_t si = 0;
+  for (int64_t L = 0; L < S.n_levels; ++L) {
+    mf_extend_add(F.d, S.level_ea[L].grp_off, S.level_ea[L].n_grp, st);
+    while (si < S.steps.size() && S.steps[si].level == L) {
+      const StepDesc& sd = S.steps[si];
+      mf_step(F.d, sd.k, sd.act_off, sd.n_act, S.pref_off[si], sd.pan_total, sd.upd_total, st);
+      ++si;
+    }
+  }
+  int rc = cuda_check(c, what);
+  if (rc) return rc;
+  int status = 0;
+  cudaMemcpyAsync(&status, F.d.status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  rc = sync_check(c, what);
+  if (rc) return rc;
+  if (status) return fail(c, QP_ENOTSPD, std::string(what) + ": pivot of wrong sign / zero (inertia check)");
+  F.ready = true;
+  return QP_OK;
+}
+
+// y = F⁻¹ rhs (factor order, N), forward + backward sweeps.
+void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
+  SweepRhs r{};
+  r.rhs = rhs_f;
+  int h = c->begin(0);
+  trsv_forward(c->FF.d, r, out, c->tgrid, c->stream);
+  c->end(h);
+  h = c->begin(1);
+  trsv_backward(c->FF.d, out, nullptr, c->tgrid, c->stream);
+  c->end(h);
+}
+
+// q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
+void kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode) {
+  SweepRhs r{};
+  r.ct = c->Ctf;
+  r.p = p;
+  r.done_flag = pcg_mode ? &c->pst->done : nullptr;
+  int h = c->begin(0);
+  trsv_forward(c->FF.d, r, c->xbuf, c->tgrid, c->stream);
+  c->end(h);
+  h = c->begin(1);
+  trsv_backward(c->FF.d, c->xbuf, r.done_flag, c->tgrid, c->stream);
+  c->end(h);
+  h = c->begin(2);
+  kf_q(c->Cf, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
+  c->end(h);
+}
+
+// z = P_H⁻¹ r (a7), P_H factor order via perm_ph.
+void ph_apply_dev(qp_ctx* c, const double* r, double* z, const int* done) {
+  SweepRhs sr{};
+  sr.rhs = r;
+  sr.in_perm = c->perm_ph_dev;
+  sr.done_flag = done;
+  int h = c->begin(4);
+  trsv_forward(c->FP.d, sr, c->xph, c->tgrid, c->stream);
+  trsv_backward(c->FP.d, c->xph, done, c->tgrid, c->stream);
+  scatter(z, c->xph, c->perm_ph_dev, c->m2, done, c->stream);
+  c->end(h);
+}
+
+int ph_refactor(qp_ctx* c, const double* D) {
+  double t0 = now_s();
+  int h = c->begin(5);
+  int rc = numeric_factor(c, c->FP, c->t_val, D, c->perm_ph_dev, "P_H factorization");
+  c->end(h);
+  if (rc) return rc;
+  cudaMemcpyAsync(c->D_ph_last, D, c->m2 * 8, cudaMemcpyDeviceToDevice, c->stream);
+  c->ph_valid = true;
+  c->t_factor_ph += now_s() - t0;
+  c->ph_refactors++;
+  return QP_OK;
+}
+
+// PCG on K_F(D) x = b from x = 0.  Result in c->px.
+int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, int* iters, double* relres,
+            bool refactor_ph) {
+  cudaStream_t st = c->stream;
+  const int prec = c->precond;
+  const int64_t m2 = c->m2;
+  if (prec == 2 && refactor_ph) {
+    int rc = ph_refactor(c, D);
+    if (rc) return rc;
+  }
+  int h = c->begin(3);
+  pcg_init(prec, m2, b, D, c->px, c->pr, c->pz, c->pp, c->partial, c->pst, tol, maxit, c->vgrid, st);
+  c->end(h);
+  if (prec == 2) {
+    ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
+    pcg_init_ph(m2, c->pr, c->pz, c->pp, c->partial, c->pst, c->vgrid, st);
+  }
+  int chunk = 2;
+  for (int it = 0; it < maxit + 1;) {
+    for (int k = 0; k < chunk; ++k) {
+      kf_apply_dev(c, D, c->pp, c->pq, true);
+      h = c->begin(3);
+      pcg_update1(prec, m2, D, c->pp, c->pq, c->px, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
+      c->end(h);
+      if (prec == 2) {
+        ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
+        pcg_rz_ph(m2, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
+      }
+      h = c->begin(3);
+      pcg_update2(m2, c->pz, c->pp, c->pst, c->vgrid, st);
+      c->end(h);
+    }
+    it += chunk;
+    cudaMemcpyAsync(c->h_pst, c->pst, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
+    int rc = sync_check(c, "pcg");
+    if (rc) return rc;
+    if (c->h_pst->done) break;
+    chunk = std::min(chunk * 2, 32);
+  }
+  c->harvest();
+  if (!c->h_pst->done) return fail(c, QP_ECUDA, "pcg loop ended without completion (internal error)");
+  if (iters) *iters = c->h_pst->iter;
+  if (relres) *relres = c->h_pst->bnorm2 > 0 ? std::sqrt(c->h_pst->rr / c->h_pst->bnorm2) : 0.0;
+  if (c->h_pst->status == -3) return fail(c, QP_EBREAKDOWN, "PCG breakdown (pᵀq <= 0 or non-finite)");
+  return c->h_pst->status == 1 ? QP_MAXIT : QP_OK;
+}
+
+int require(qp_ctx* c, bool factored) {
+  if (!c) return QP_EINVAL;
+  if (!c->setup_done) return fail(c, QP_ESTATE, "qp_setup has not completed");
+  if (factored && !c->factored) return fail(c, QP_ESTATE, "ipm_factor_once has not completed");
+  cudaSetDevice(c->device);
+  return QP_OK;
+}
+
+// Copy m doubles host/device → device buffer (staging) according to vectors_on_device.
+const double* in_vec(qp_ctx* c, const double* v, double* stage, int64_t m) {
+  if (c->vectors_on_device) return v;
+  cudaMemcpyAsync(stage, v, m * 8, cudaMemcpyHostToDevice, c->stream);
+  return stage;
+}
+void out_vec(qp_ctx* c, double* dst, const double* src_dev, int64_t m) {
+  if (!dst) return;
+  cudaMemcpyAsync(dst, src_dev, m * 8, c->vectors_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                  c->stream);
+}
+
+int ipm_iteration(qp_ctx* c, bool* converged) {
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n, m1 = c->m1, m2 = c->m2, N = n + m1;
+  int h = c->begin(6);
+  ipm_mu(m2, c->s, c->nu, c->partial, c->ist, c->vgrid, st);
+  ipm_residuals(c->Hf, c->Atf, c->Ctf, c->Af, c->Cf, c->gf, c->bv, c->dv, c->xl, c->xl + n, c->nu, c->s, c->rgre,
+                c->rc, c->ra, c->Dk, c->partial, c->ist, c->vgrid, st);
+  c->end(h);
+  cudaMemcpyAsync(c->h_ist, c->ist, sizeof(IpmState), cudaMemcpyDeviceToHost, st);
+  int rc = sync_check(c, "ipm residuals");
+  if (rc) return rc;
+  const IpmState& S = *c->h_ist;
+  const double tol = c->opts.ipm_tol;
+  if (S.rg_inf <= tol * (1 + c->gmax) && S.re_inf <= tol * (1 + c->bmax) && S.ri_inf <= tol * (1 + c->dmax) &&
+      S.mu <= tol) {
+    *converged = true;
+    return QP_OK;
+  }
+  *converged = false;
+  // r_ν = −r_a + [C 0] F⁻¹ (r_g; r_e)
+  f_solve_dev(c, c->rgre, c->xbuf);
+  h = c->begin(7);
+  ipm_rnu(c->Cf, c->ra, c->xbuf, c->rnu, c->vgrid, st);
+  c->end(h);
+  // PCG (reading R4 forcing)
+  double eps = c->opts.pcg_forcing ? std::min(c->opts.pcg_tol, S.mu) : c->opts.pcg_tol;
+  int iters = 0;
+  rc = pcg_dev(c, c->Dk, c->rnu, eps, c->opts.pcg_maxit, &iters, nullptr, true);
+  if (rc != QP_OK && rc != QP_MAXIT) return rc;
+  c->pcg_hist.push_back(iters);
+  // recovery: F(Δx;Δλ) = −(r_g + CᵀΔν; r_e)
+  h = c->begin(7);
+  ipm_recovery_rhs(c->Ctf, n, m1, c->rgre, c->px, c->rhs2, c->vgrid, st);
+  c->end(h);
+  f_solve_dev(c, c->rhs2, c->dxl);
+  h = c->begin(7);
+  ipm_ds_alpha(m2, c->rc, c->nu, c->Dk, c->px, c->s, c->ds, c->partial, c->ist, c->vgrid, st);
+  ipm_update(N, m2, c->dxl, c->px, c->ds, c->xl, c->nu, c->s, c->ist, c->vgrid, st);
+  c->end(h);
+  c->ipm_k++;
+  return cuda_check(c, "ipm iteration");
+}
+
+void fill_result(qp_ctx* c, qp_ipm_result* r) {
+  if (!r) return;
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n;
+  ipm_objective(c->Hf, c->gf, c->xl, c->partial, c->ist, c->vgrid, st);
+  cudaMemcpyAsync(c->h_ist, c->ist, sizeof(IpmState), cudaMemcpyDeviceToHost, st);
+  if (r->x) {
+    scatter(c->vout, c->xl, c->perm_dev, n, nullptr, st);  // x[perm[i]] = x_f[i]
+    out_vec(c, r->x, c->vout, n);
+  }
+  out_vec(c, r->lam, c->xl + n, c->m1);
+  out_vec(c, r->nu, c->nu, c->m2);
+  out_vec(c, r->s, c->s, c->m2);
+  cudaStreamSynchronize(st);
+  r->objective = c->h_ist->objective;
+  r->n_ipm = c->ipm_k;
+  r->status = c->ipm_converged ? QP_OK : QP_MAXIT;
+  int64_t tot = 0;
+  for (size_t i = 0; i < c->pcg_hist.size(); ++i) {
+    if (r->pcg_iters && (int32_t)i < c->opts.max_ipm) r->pcg_iters[i] = c->pcg_hist[i];
+    tot += c->pcg_hist[i];
+  }
+  r->pcg_total = (int32_t)tot;
+  r->t_setup_s = c->t_symbolic + c->t_factor;
+  r->mu = c->h_ist->mu;
+  r->rg_inf = c->h_ist->rg_inf;
+  r->re_inf = c->h_ist->re_inf;
+  r->ri_inf = c->h_ist->ri_inf;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, const double* g, const double* b,
+             const double* d, const qp_setup_opts* opts) {
+  if (!out) return QP_EINVAL;
+  *out = nullptr;
+  std::unique_ptr<qp_ctx> c(new qp_ctx());
+  if (!H || !A || !C) return QP_EINVAL;
+  const int64_t n = H->nrows, m1 = A->nrows, m2 = C->nrows;
+  if (n <= 0 || m2 <= 0 || m1 < 0 || m1 > n) {
+    *out = c.release();
+    return fail(*out, QP_EINVAL, "need n >= 1, m2 >= 1, 0 <= m1 <= n");
+  }
+  std::string e = check_csr(H, n, n, "H", c->H);
+  if (e.empty()) e = check_csr(A, m1, n, "A", c->A);
+  if (e.empty()) e = check_csr(C, m2, n, "C", c->C);
+  if (e.empty()) {
+    // H symmetric (both triangles stored)
+    HostCSR Ht = transpose(c->H);
+    if (Ht.p != c->H.p || Ht.i != c->H.i) e = "H pattern is not symmetric (store both triangles)";
+    else
+      for (int64_t q = 0; q < c->H.nnz() && e.empty(); ++q)
+        if (Ht.v[q] != c->H.v[q]) e = "H values are not symmetric";
+  }
+  c->n = n;
+  c->m1 = m1;
+  c->m2 = m2;
+  if (e.empty() && (!g || (m1 > 0 && !b) || !d)) e = "NULL g / b / d";
+  if (e.empty()) {
+    c->g.assign(g, g + n);
+    c->b.assign(b ? b : g, (b ? b : g) + m1);
+    c->d.assign(d, d + m2);
+    for (double v : c->g) if (!std::isfinite(v)) e = "non-finite g";
+    for (double v : c->b) if (!std::isfinite(v)) e = "non-finite b";
+    for (double v : c->d) if (!std::isfinite(v)) e = "non-finite d";
+  }
+  if (!e.empty()) {
+    *out = c.release();
+    return fail(*out, QP_EINVAL, e);
+  }
+  qp_setup_opts o{};
+  if (opts) o = *opts;
+  c->device = o.device;
+  c->vectors_on_device = o.vectors_on_device;
+  c->rank = o.rank;
+  c->world = o.world <= 0 ? 1 : o.world;
+  c->ws_limit = o.workspace_limit_bytes > 0 ? o.workspace_limit_bytes : (int64_t)120 << 30;
+  if (c->world != 1) {
+    *out = c.release();
+    return fail(*out, QP_EINVAL, "world > 1: run one independent replica per GPU (DESIGN.md §Multi-GPU)");
+  }
+  if (o.x_perm) {
+    c->xperm_user.assign(o.x_perm, o.x_perm + n);
+    std::vector<char> seen(n, 0);
+    for (int64_t v : c->xperm_user) {
+      if (v < 0 || v >= n || seen[v]) {
+        *out = c.release();
+        return fail(*out, QP_EINVAL, "x_perm is not a permutation of 0..n-1");
+      }
+      seen[v] = 1;
+    }
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->device) {
+    cudaGetLastError();
+    *out = c.release();
+    return fail(*out, QP_ECUDA, "no CUDA device available (this library has no CPU fallback)");
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, c->device);
+  if (prop.major < 10) {
+    *out = c.release();
+    return fail(*out, QP_ECUDA, "device is not sm_100 class (Blackwell) — the kernels are built for sm_100a only");
+  }
+  cudaSetDevice(c->device);
+  c->sm_count = prop.multiProcessorCount;
+  c->vgrid = c->sm_count * 4;
+  if (o.stream) {
+    c->stream = (cudaStream_t)o.stream;
+  } else {
+    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    c->own_stream = true;
+  }
+  c->tgrid = trsv_grid(c->device);
+  cudaMallocHost(&c->h_pst, sizeof(PcgState));
+  cudaMallocHost(&c->h_ist, sizeof(IpmState));
+  c->gmax = 0;
+  for (double v : c->g) c->gmax = std::max(c->gmax, std::fabs(v));
+  c->bmax = 0;
+  for (double v : c->b) c->bmax = std::max(c->bmax, std::fabs(v));
+  c->dmax = 0;
+  for (double v : c->d) c->dmax = std::max(c->dmax, std::fabs(v));
+  int rc = cuda_check(c.get(), "qp_setup");
+  c->setup_done = rc == QP_OK;
+  *out = c.release();
+  return rc;
+}
+
+int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
+  int rc = require(c, false);
+  if (rc) return rc;
+  if (c->factored) return fail(c, QP_ESTATE, "ipm_factor_once already called (the factor of F is computed once)");
+  if (p < QP_PREC_NONE || p > QP_PREC_HIGH) return fail(c, QP_EINVAL, "unknown preconditioner");
+  c->precond = (int)p;
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n, m1 = c->m1, m2 = c->m2, N = n + m1;
+  double t0 = now_s();
+  // ---- ordering of the x block (user or minimum degree on the graph of H), λ last
+  if (!c->xperm_user.empty()) {
+    c->perm = c->xperm_user;
+  } else {
+    std::vector<int64_t> ptr(n + 1, 0);
+    std::vector<int32_t> idx;
+    idx.reserve(c->H.nnz());
+    for (int64_t r = 0; r < n; ++r) {
+      for (int64_t q = c->H.p[r]; q < c->H.p[r + 1]; ++q)
+        if (c->H.i[q] != r) idx.push_back(c->H.i[q]);
+      ptr[r + 1] = (int64_t)idx.size();
+    }
+    c->perm = min_degree_order(n, ptr, idx);
+  }
+  std::vector<int64_t> pinv(n);
+  for (int64_t i = 0; i < n; ++i) pinv[c->perm[i]] = i;
+  LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(), c->A.i.data(),
+                                c->A.v.data(), c->perm);
+  std::string e = analyse(M, c->FF.S, n);
+  if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of F: " + e);
+  c->t_symbolic = now_s() - t0;
+  e = upload_factor(c, c->FF, c->ws_limit);
+  if (!e.empty()) return fail(c, QP_ENOMEM, e);
+  // ---- permuted operators (factor order for the x block)
+  try {
+    HostCSR Hf = permute(c->H, &c->perm, &pinv);
+    HostCSR Af = permute(c->A, nullptr, &pinv);
+    HostCSR Cf = permute(c->C, nullptr, &pinv);
+    HostCSR Atf = transpose(Af), Ctf = transpose(Cf);
+    c->Hf = upload_csr(c->mem, Hf, st);
+    c->Af = upload_csr(c->mem, Af, st);
+    c->Cf = upload_csr(c->mem, Cf, st);
+    c->Atf = upload_csr(c->mem, Atf, st);
+    c->Ctf = upload_csr(c->mem, Ctf, st);
+    std::vector<double> gf(n);
+    for (int64_t i = 0; i < n; ++i) gf[i] = c->g[c->perm[i]];
+    c->gf = c->mem.upload(gf, st);
+    c->bv = c->mem.upload(c->b, st);
+    c->dv = c->mem.upload(c->d, st);
+    std::vector<int64_t> pf(N);
+    for (int64_t i = 0; i < n; ++i) pf[i] = c->perm[i];
+    for (int64_t i = 0; i < m1; ++i) pf[n + i] = n + i;
+    c->perm_dev = c->mem.upload(pf, st);
+    int64_t V = std::max<int64_t>(N, m2);
+    c->xl = c->mem.zeros<double>(N, st);
+    c->nu = c->mem.zeros<double>(m2, st);
+    c->s = c->mem.zeros<double>(m2, st);
+    c->rgre = c->mem.zeros<double>(N, st);
+    c->rhs2 = c->mem.zeros<double>(N, st);
+    c->xbuf = c->mem.zeros<double>(N, st);
+    c->dxl = c->mem.zeros<double>(N, st);
+    c->rc = c->mem.zeros<double>(m2, st);
+    c->ra = c->mem.zeros<double>(m2, st);
+    c->Dk = c->mem.zeros<double>(m2, st);
+    c->rnu = c->mem.zeros<double>(m2, st);
+    c->ds = c->mem.zeros<double>(m2, st);
+    c->px = c->mem.zeros<double>(m2, st);
+    c->pr = c->mem.zeros<double>(m2, st);
+    c->pz = c->mem.zeros<double>(m2, st);
+    c->pp = c->mem.zeros<double>(m2, st);
+    c->pq = c->mem.zeros<double>(m2, st);
+    c->vin = c->mem.zeros<double>(V, st);
+    c->vin2 = c->mem.zeros<double>(V, st);
+    c->vout = c->mem.zeros<double>(V, st);
+    c->partial = c->mem.zeros<double>(4 * (size_t)std::max(c->vgrid, 1), st);
+    c->pst = c->mem.zeros<PcgState>(1, st);
+    c->ist = c->mem.zeros<IpmState>(1, st);
+  } catch (std::bad_alloc&) {
+    return fail(c, QP_ENOMEM, "cudaMalloc failed (problem / vectors)");
+  }
+  rc = cuda_check(c, "upload");
+  if (rc) return rc;
+  // ---- numeric LDLᵀ of F, once
+  double t1 = now_s();
+  rc = numeric_factor(c, c->FF, nullptr, nullptr, nullptr, "F factorization");
+  c->t_factor = now_s() - t1;
+  if (rc) return rc;
+  // ---- P_H: T = C diag(H)⁻¹ Cᵀ pattern (host) and values (device), symbolic of D + T
+  if (p == QP_PREC_HIGH) {
+    HostCSR Ct = transpose(c->C);
+    std::vector<int64_t> tp(m2 + 1, 0);
+    std::vector<int32_t> ti;
+    std::vector<int64_t> mark(m2, -1);
+    std::vector<int32_t> rowbuf;
+    for (int64_t i = 0; i < m2; ++i) {
+      rowbuf.clear();
+      for (int64_t q = c->C.p[i]; q < c->C.p[i + 1]; ++q) {
+        int32_t k = c->C.i[q];
+        for (int64_t u = Ct.p[k]; u < Ct.p[k + 1]; ++u) {
+          int32_t j = Ct.i[u];
+          if (mark[j] != i) { mark[j] = i; rowbuf.push_back(j); }
+        }
+      }
+      if (mark[i] != i) rowbuf.push_back((int32_t)i);  // empty C row: keep the diagonal of D
+      std::sort(rowbuf.begin(), rowbuf.end());
+      ti.insert(ti.end(), rowbuf.begin(), rowbuf.end());
+      tp[i + 1] = (int64_t)ti.size();
+    }
+    c->nnz_t = (int64_t)ti.size();
+    std::vector<int64_t> trow(c->nnz_t);
+    for (int64_t i = 0; i < m2; ++i)
+      for (int64_t q = tp[i]; q < tp[i + 1]; ++q) trow[q] = i;
+    // ordering of P_H: minimum degree on the pattern of T
+    {
+      std::vector<int64_t> ptr(m2 + 1, 0);
+      std::vector<int32_t> idx;
+      idx.reserve(c->nnz_t);
+      for (int64_t r = 0; r < m2; ++r) {
+        for (int64_t q = tp[r]; q < tp[r + 1]; ++q)
+          if (ti[q] != r) idx.push_back(ti[q]);
+        ptr[r + 1] = (int64_t)idx.size();
+      }
+      c->perm_ph = min_degree_order(m2, ptr, idx);
+    }
+    std::vector<int64_t> pinv_ph(m2);
+    for (int64_t i = 0; i < m2; ++i) pinv_ph[c->perm_ph[i]] = i;
+    LowerMatrix PM;
+    PM.N = m2;
+    PM.colptr.assign(m2 + 1, 0);
+    PM.diag_src.assign(m2, -1);
+    for (int64_t i = 0; i < m2; ++i)
+      for (int64_t q = tp[i]; q < tp[i + 1]; ++q) {
+        int64_t a = pinv_ph[i], bb = pinv_ph[ti[q]];
+        if (a > bb) PM.colptr[bb + 1]++;
+        else if (a == bb) PM.diag_src[a] = q;
+      }
+    for (int64_t j = 0; j < m2; ++j) PM.colptr[j + 1] += PM.colptr[j];
+    PM.rowind.resize(PM.colptr[m2]);
+    PM.src.resize(PM.colptr[m2]);
+    {
+      std::vector<int64_t> pos(PM.colptr.begin(), PM.colptr.end() - 1);
+      for (int64_t i = 0; i < m2; ++i)
+        for (int64_t q = tp[i]; q < tp[i + 1]; ++q) {
+          int64_t a = pinv_ph[i], bb = pinv_ph[ti[q]];
+          if (a > bb) {
+            int64_t w = pos[bb]++;
+            PM.rowind[w] = (int32_t)a;
+            PM.src[w] = q;
+          }
+        }
+      std::vector<std::pair<int32_t, int64_t>> tmp;
+      for (int64_t j = 0; j < m2; ++j) {
+        tmp.clear();
+        for (int64_t q = PM.colptr[j]; q < PM.colptr[j + 1]; ++q) tmp.emplace_back(PM.rowind[q], PM.src[q]);
+        std::sort(tmp.begin(), tmp.end());
+        for (int64_t q = PM.colptr[j]; q < PM.colptr[j + 1]; ++q) {
+          PM.rowind[q] = tmp[q - PM.colptr[j]].first;
+          PM.src[q] = tmp[q - PM.colptr[j]].second;
+        }
+      }
+    }
+    e = analyse(PM, c->FP.S, 0);
+    if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of P_H: " + e);
+    e = upload_factor(c, c->FP, c->ws_limit);
+    if (!e.empty()) return fail(c, QP_ENOMEM, e);
+    try {
+      c->t_row = c->mem.upload(trow, st);
+      c->t_col = c->mem.upload(ti, st);
+      c->t_val = c->mem.zeros<double>(c->nnz_t, st);
+      std::vector<double> hd(n, 0.0);
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t q = c->H.p[r]; q < c->H.p[r + 1]; ++q)
+          if (c->H.i[q] == r) hd[r] = c->H.v[q];
+      c->hdiag = c->mem.upload(hd, st);
+      HostCSR Cn = c->C;
+      c->Cnu = upload_csr(c->mem, Cn, st);
+      c->perm_ph_dev = c->mem.upload(c->perm_ph, st);
+      c->xph = c->mem.zeros<double>(m2, st);
+      c->D_ph_last = c->mem.zeros<double>(m2, st);
+    } catch (std::bad_alloc&) {
+      return fail(c, QP_ENOMEM, "cudaMalloc failed (P_H)");
+    }
+    t_values(c->Cnu, c->hdiag, c->t_row, c->t_col, c->nnz_t, c->t_val, st);  // T once
+    std::vector<double> ones(m2, 1.0);
+    const double* D0d;
+    if (D0) {
+      D0d = in_vec(c, D0, c->vin, m2);
+    } else {
+      cudaMemcpyAsync(c->vin, ones.data(), m2 * 8, cudaMemcpyHostToDevice, st);
+      D0d = c->vin;
+    }
+    rc = ph_refactor(c, D0d);
+    if (rc) return rc;
+  }
+  c->factored = true;
+  return sync_check(c, "ipm_factor_once");
+}
+
+int pcg_solve(qp_ctx* c, const double* D_k, const double* rhs, double tol, int32_t maxit, double* dnu_out,
+              int32_t* iters, double* relres) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  if (!D_k || !rhs) return fail(c, QP_EINVAL, "NULL D_k / rhs");
+  const int64_t m2 = c->m2;
+  const double* Dd = in_vec(c, D_k, c->vin, m2);
+  const double* bd = in_vec(c, rhs, c->vin2, m2);
+  // copy D into the IPM D buffer so P_H change detection compares stable storage
+  cudaMemcpyAsync(c->Dk, Dd, m2 * 8, cudaMemcpyDeviceToDevice, c->stream);
+  bool refac = false;
+  if (c->precond == 2) {
+    std::vector<double> a(m2), b(m2);
+    cudaMemcpyAsync(a.data(), c->Dk, m2 * 8, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(b.data(), c->D_ph_last, m2 * 8, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    refac = !c->ph_valid || a != b;
+  }
+  int it = 0;
+  double rr = 0;
+  rc = pcg_dev(c, c->Dk, bd, tol, maxit, &it, &rr, refac);
+  if (iters) *iters = it;
+  if (relres) *relres = rr;
+  if (rc != QP_OK && rc != QP_MAXIT) return rc;
+  out_vec(c, dnu_out, c->px, m2);
+  int rc2 = sync_check(c, "pcg_solve");
+  return rc2 ? rc2 : rc;
+}
+
+int qp_ipm_init(qp_ctx* c, const qp_ipm_opts* o) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  qp_ipm_opts d{1e-8, 1e-3, 0.1, 0.995, 100, 2000, 1};
+  c->opts = o ? *o : d;
+  if (c->opts.max_ipm <= 0) c->opts.max_ipm = 100;
+  if (c->opts.pcg_maxit <= 0) c->opts.pcg_maxit = 2000;
+  const int64_t n = c->n, m1 = c->m1, m2 = c->m2;
+  cudaStream_t st = c->stream;
+  // x = 0, λ = 0, ν = 1, s = |d| + 1 (reading R3 start)
+  cudaMemsetAsync(c->xl, 0, (n + m1) * 8, st);
+  std::vector<double> ones(m2, 1.0), s0(m2);
+  for (int64_t i = 0; i < m2; ++i) s0[i] = std::fabs(c->d[i]) + 1.0;
+  cudaMemcpyAsync(c->nu, ones.data(), m2 * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->s, s0.data(), m2 * 8, cudaMemcpyHostToDevice, st);
+  IpmState is{};
+  is.sigma = c->opts.sigma;
+  is.tau = c->opts.tau;
+  cudaMemcpyAsync(c->ist, &is, sizeof(IpmState), cudaMemcpyHostToDevice, st);
+  c->ipm_k = 0;
+  c->ipm_converged = false;
+  c->pcg_hist.clear();
+  c->ipm_initialised = true;
+  return sync_check(c, "qp_ipm_init");
+}
+
+int qp_ipm_iterate(qp_ctx* c, int32_t nsteps, qp_ipm_result* r, int32_t* done) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  if (!c->ipm_initialised) return fail(c, QP_ESTATE, "qp_ipm_init has not been called");
+  for (int32_t k = 0; k < nsteps && !c->ipm_converged && c->ipm_k < c->opts.max_ipm; ++k) {
+    bool conv = false;
+    rc = ipm_iteration(c, &conv);
+    if (rc) return rc;
+    if (conv) c->ipm_converged = true;
+  }
+  if (!c->ipm_converged && c->ipm_k >= c->opts.max_ipm) {
+    // final residual evaluation at the last iterate
+    int h = c->begin(6);
+    ipm_mu(c->m2, c->s, c->nu, c->partial, c->ist, c->vgrid, c->stream);
+    ipm_residuals(c->Hf, c->Atf, c->Ctf, c->Af, c->Cf, c->gf, c->bv, c->dv, c->xl, c->xl + c->n, c->nu, c->s,
+                  c->rgre, c->rc, c->ra, c->Dk, c->partial, c->ist, c->vgrid, c->stream);
+    c->end(h);
+
+  }
+  if (done) *done = c->ipm_converged ? 1 : 0;
+  fill_result(c, r);
+  return sync_check(c, "qp_ipm_iterate");
+}
+
+int ipm_solve(qp_ctx* c, const qp_ipm_opts* o, qp_ipm_result* r) {
+  double t0 = now_s();
+  int rc = qp_ipm_init(c, o);
+  if (rc) return rc;
+  int32_t done = 0;
+  rc = qp_ipm_iterate(c, c->opts.max_ipm + 1, r, &done);
+  if (r) r->t_solve_s = now_s() - t0;
+  if (rc) return rc;
+  return done ? QP_OK : QP_MAXIT;
+}
+
+int qp_f_solve(qp_ctx* c, const double* rhs, double* out) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  const int64_t N = c->n + c->m1;
+  const double* in = in_vec(c, rhs, c->vin, N);
+  gather(c->rhs2, in, c->perm_dev, N, nullptr, c->stream);   // factor order
+  f_solve_dev(c, c->rhs2, c->xbuf);
+  scatter(c->vout, c->xbuf, c->perm_dev, N, nullptr, c->stream);
+  out_vec(c, out, c->vout, N);
+  rc = sync_check(c, "qp_f_solve");
+  c->harvest();
+  return rc;
+}
+
+int qp_kf_apply(qp_ctx* c, const double* D, const double* p, double* q) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  const int64_t m2 = c->m2;
+  const double* Dd = in_vec(c, D, c->vin, m2);
+  const double* pd = in_vec(c, p, c->vin2, m2);
+  kf_apply_dev(c, Dd, pd, c->vout, false);
+  out_vec(c, q, c->vout, m2);
+  rc = sync_check(c, "qp_kf_apply");
+  c->harvest();
+  return rc;
+}
+
+int qp_get_structure(qp_ctx* c, int32_t which, int64_t* out, int64_t* len) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  const Symbolic& S = which >= 10 ? c->FP.S : c->FF.S;
+  if (which >= 10 && c->precond != 2) return fail(c, QP_ESTATE, "no P_H factor (precond != HIGH)");
+  std::vector<int64_t> v;
+  switch (which % 10) {
+    case 0:
+      if (which >= 10) v = c->perm_ph;
+      else {
+        v = c->perm;
+        for (int64_t i = 0; i < c->m1; ++i) v.push_back(c->n + i);
+      }
+      break;
+    case 1: v = S.parent; break;
+    case 2: v = S.colcount; break;
+    case 3: v = S.sn_start; break;
+    case 4: v = S.sn_parent; break;
+    case 5: v = S.sn_level; break;
+    case 6: v = S.sn_rowptr; break;
+    case 7: v.assign(S.sn_rows.begin(), S.sn_rows.end()); break;
+    case 8: v = S.rowlev; break;
+    default: return fail(c, QP_EINVAL, "unknown structure id");
+  }
+  if (!len) return QP_EINVAL;
+  if (out) {
+    if (*len < (int64_t)v.size()) return fail(c, QP_EINVAL, "buffer too small");
+    std::memcpy(out, v.data(), v.size() * 8);
+  }
+  *len = (int64_t)v.size();
+  return QP_OK;
+}
+
+int qp_get_stats(qp_ctx* c, qp_stats* s) {
+  int rc = require(c, false);
+  if (rc) return rc;
+  if (!s) return QP_EINVAL;
+  std::memset(s, 0, sizeof(*s));
+  s->n = c->n;
+  s->m1 = c->m1;
+  s->m2 = c->m2;
+  s->nnz_H = c->H.nnz();
+  s->nnz_A = c->A.nnz();
+  s->nnz_C = c->C.nnz();
+  if (c->factored) {
+    const Symbolic& S = c->FF.S;
+    s->nnz_LF = S.nnz_L;
+    s->n_supernodes_F = S.ns;
+    s->n_blocks_F = S.nb;
+    s->n_levels_F = S.n_levels;
+    s->row_levels_F = S.n_rowlev;
+    s->c_fact_F = S.c_fact;
+    s->workspace_bytes = c->FF.ws_bytes + c->FP.ws_bytes;
+    s->factor_bytes = c->FF.fs_bytes + c->FP.fs_bytes;
+    if (c->precond == 2) {
+      s->nnz_LPH = c->FP.S.nnz_L;
+      s->n_supernodes_PH = c->FP.S.ns;
+      s->c_fact_PH = c->FP.S.c_fact;
+    }
+    s->t_symbolic_s = c->t_symbolic;
+    s->t_factor_s = c->t_factor;
+    s->t_factor_ph_s = c->ph_refactors ? c->t_factor_ph / (double)c->ph_refactors : 0.0;
+    const double n = (double)c->n, m1 = (double)c->m1, m2 = (double)c->m2;
+    s->pcg_bytes_per_iter = 16.0 * (double)S.nnz_L + 24.0 * (double)c->C.nnz() + 8.0 * (15.0 * m2 + 6.0 * (n + m1)) +
+                            16.0 * (double)s->nnz_LPH;
+    s->pcg_flops_per_iter = 4.0 * (double)S.nnz_L + 4.0 * (double)c->C.nnz() + 4.0 * (double)s->nnz_LPH;
+    s->sweep_bytes_F = 8.0 * (double)S.nnz_L;
+  }
+  return QP_OK;
+}
+
+int qp_profile(qp_ctx* c, int32_t enable) {
+  if (!c) return QP_EINVAL;
+  c->harvest();
+  c->prof = enable != 0;
+  if (!enable) {
+    std::memset(c->prof_ms, 0, sizeof(c->prof_ms));
+    std::memset(c->prof_cnt, 0, sizeof(c->prof_cnt));
+  }
+  return QP_OK;
+}
+
+int qp_profile_read(qp_ctx* c, double* ms, int64_t* count) {
+  if (!c) return QP_EINVAL;
+  c->harvest();
+  for (int i = 0; i < 8; ++i) {
+    if (ms) ms[i] = c->prof_ms[i];
+    if (count) count[i] = c->prof_cnt[i];
+  }
+  return QP_OK;
+}
+
+const char* qp_last_error(const qp_ctx* c) { return c ? c->err.c_str() : "NULL context"; }
+
+void qp_free(qp_ctx* c) { delete c; }
+
+}  // extern "C"

@@ -1,0 +1,1008 @@
+// sm_100a fp64 kernels for the single-factorization inexact IPM (arXiv 2104.12916).
+//
+//  * multifrontal numeric LDLᵀ / Cholesky (setup of F; P_H refactor
+//    every IPM iteration): assemble → extend-add → per-level blocked
+//    partial factorization (DIAG / PANEL / UPDATE tile kernels), deterministic
+//    owner-computes, no atomics;
+//  * forward / backward triangular sweeps with L (c_trsv) as persistent
+//    task-graph kernels: tasks are claimed from a ticket counter in topological
+//    order, dependencies are tracked with per-block counters/flags, so there is
+//    no level barrier; the K_F product's Cᵀp SpMV is fused into the
+//    forward sweep's diagonal tasks;
+//  * K_F's q = D∘p − C·w SpMV with the pᵀq reduction, fused PCG vector updates
+//    with deterministic warp-shuffle + block + last-block reductions
+//    (P:L284–285);
+//  * IPM rhs / r_ν / recovery / Δs / step kernels (P:L65–69, P:L473–505,
+//    P:L727–752).
+#include "kernels.cuh"
+
+#include <cfloat>
+#include <cmath>
+#include <algorithm>
+
+namespace qpb {
+
+// ------------------------------------------------------------------------- helpers
+__device__ __forceinline__ unsigned ld_acq_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// Block reduction (NT threads); result valid in every thread.
+template <int OP>
+__device__ double block_reduce(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = OP == 0 ? warp_sum(v) : (OP == 1 ? warp_max(v) : warp_min(v));
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double init = OP == 0 ? 0.0 : (OP == 1 ? -DBL_MAX : DBL_MAX);
+  v = (lane < NT / 32) ? sh[lane] : init;
+  v = OP == 0 ? warp_sum(v) : (OP == 1 ? warp_max(v) : warp_min(v));
+  return v;
+}
+// Last-block detection after each block stored its partials.
+__device__ bool is_last_block(unsigned int* arrive) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(arrive, 1u) == gridDim.x - 1);
+  __syncthreads();
+  return last;
+}
+// Deterministic sum of partial[0..n) by one block (fixed assignment).
+template <int OP>
+__device__ double reduce_partials(const double* part, int n, double* sh) {
+  double init = OP == 0 ? 0.0 : (OP == 1 ? -DBL_MAX : DBL_MAX);
+  double v = init;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double x = __ldcg(part + i);
+    v = OP == 0 ? v + x : (OP == 1 ? fmax(v, x) : fmin(v, x));
+  }
+  return block_reduce<OP>(v, sh);
+}
+__device__ __forceinline__ double csr_dot(const DevCSR& M, int64_t row, const double* x) {
+  double s = 0.0;
+  for (int64_t q = M.p[row]; q < M.p[row + 1]; ++q) s += M.v[q] * __ldg(x + M.i[q]);
+  return s;
+}
+// Front tile boundaries: pivot blocks of 64, then the update rows in tiles of 64.
+__device__ __forceinline__ int64_t tile_begin(int64_t t, int64_t nk, int64_t w, int64_t m) {
+  int64_t v = t < nk ? (int64_t)MF_BW * t : w + (int64_t)MF_BW * (t - nk);
+  return v < m ? v : m;
+}
+__device__ __forceinline__ int find_seg(const int64_t* pref, int n, int64_t x) {
+  int lo = 0, hi = n - 1;  // largest a with pref[a] <= x
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (pref[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------------- multifrontal
+__global__ void k_mf_assemble(DevFactor F, const double* src_vals) {
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < F.n_asm; e += (int64_t)gridDim.x * NT) {
+    double v = F.asm_val[e];
+    if (src_vals != nullptr) {
+      int64_t s = F.asm_src[e];
+      v = s >= 0 ? src_vals[s] : 0.0;
+    }
+    F.ws[F.asm_dst[e]] = v;
+  }
+}
+
+__global__ void k_mf_diag_add(DevFactor F, const double* D, const int64_t* perm) {
+  for (int64_t c = blockIdx.x * (int64_t)NT + threadIdx.x; c < F.N; c += (int64_t)gridDim.x * NT)
+    F.ws[F.diag_dst[c]] += D[perm[c]];
+}
+
+// One warp per (parent front, parent column) group; children in fixed order.
+__global__ void k_mf_extend_add(DevFactor F, int64_t grp_off, int64_t n_grp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = grp_off + (blockIdx.x * (int64_t)NT + threadIdx.x) / 32;
+  if (g >= grp_off + n_grp) return;
+  const int32_t P = F.grp_P[g];
+  const int64_t mP = F.sn_rowptr[P + 1] - F.sn_rowptr[P];
+  double* col = F.ws + F.front_off[P] + (int64_t)F.grp_pc[g] * mP;
+  for (int64_t e = F.grp_ptr[g]; e < F.grp_ptr[g + 1]; ++e) {
+    const int32_t K = F.grp_K[e];
+    const int64_t j = F.grp_j[e];
+    const int64_t mK = F.sn_rowptr[K + 1] - F.sn_rowptr[K];
+    const int64_t wK = F.sn_start[K + 1] - F.sn_start[K];
+    const int32_t* ri = F.relind + F.relind_off[K] - wK;
+    const double* u = F.ws + F.front_off[K] + j * mK;
+    for (int64_t i = j + lane; i < mK; i += 32) col[ri[i]] += u[i];
+  }
+}
+
+// DIAG: LDLᵀ of the 64×64 pivot tile (static 1×1 pivots), sign check, L⁻¹.
+__global__ void __launch_bounds__(NT) k_mf_diag(DevFactor F, int k, int64_t act_off) {
+  extern __shared__ double dsm[];
+  double* a = dsm;
+  double* xi = dsm + 64 * 65;
+  const int J = F.act[act_off + blockIdx.x];
+  const int64_t c0 = F.sn_start[J], w = F.sn_start[J + 1] - c0;
+  const int64_t m = F.sn_rowptr[J + 1] - F.sn_rowptr[J];
+  const int64_t fo = F.front_off[J];
+  const int64_t p0 = (int64_t)MF_BW * k;
+  const int wk = (int)(w - p0 < MF_BW ? w - p0 : MF_BW);
+  const int b = F.sn_blk0[J] + k;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < wk * wk; idx += NT) {
+    int c = idx / wk, r = idx % wk;
+    a[c * 65 + r] = F.ws[fo + (p0 + c) * m + p0 + r];
+    xi[c * 65 + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < wk; ++j) {
+    const double d = a[j * 65 + j];
+    if (tid == 0) {
+      F.Dpiv[c0 + p0 + j] = d;
+      const signed char sg = F.pivsign[c0 + p0 + j];
+      if (!(isfinite(d)) || d == 0.0 || (sg < 0 && d > 0.0) || (sg > 0 && d < 0.0)) atomicExch(F.status, 1);
+    }
+    const int rem = wk - j - 1;
+    const double inv = 1.0 / d;
+    for (int idx = tid; idx < rem * rem; idx += NT) {
+      int i = j + 1 + idx % rem, c = j + 1 + idx / rem;
+      if (c <= i) a[c * 65 + i] -= a[j * 65 + i] * a[j * 65 + c] * inv;
+    }
+    __syncthreads();
+    for (int i = j + 1 + tid; i < wk; i += NT) a[j * 65 + i] *= inv;
+    __syncthreads();
+  }
+  // X = L⁻¹ (unit lower) by column-oriented forward substitution
+  for (int j = 0; j + 1 < wk; ++j) {
+    const int rem = wk - j - 1;
+    for (int idx = tid; idx < rem * (j + 1); idx += NT) {
+      int i = j + 1 + idx % rem, c = idx / rem;
+      xi[c * 65 + i] -= a[j * 65 + i] * xi[c * 65 + j];
+    }
+    __syncthreads();
+  }
+  double* inv = F.fstore + F.blk_inv[b];
+  for (int idx = tid; idx < wk * wk; idx += NT) {
+    int c = idx / wk, r = idx % wk;
+    inv[idx] = r >= c ? xi[c * 65 + r] : 0.0;
+  }
+}
+
+// PANEL: L_tk = A_tk · L_kk⁻ᵀ · D_k⁻¹ for the row tiles below the pivot block.
+__global__ void __launch_bounds__(NT) k_mf_panel(DevFactor F, int k, int64_t act_off, int n_act,
+                                                 int64_t pref_off) {
+  extern __shared__ double dsm[];
+  double* Ls = dsm;
+  double* At = dsm + 64 * 65;
+  double* Dk = dsm + 2 * 64 * 65;
+  const int64_t* pref = F.pan_pref + pref_off;
+  const int a = find_seg(pref, n_act + 1, blockIdx.x);
+  const int J = F.act[act_off + a];
+  const int64_t c0 = F.sn_start[J], w = F.sn_start[J + 1] - c0;
+  const int64_t m = F.sn_rowptr[J + 1] - F.sn_rowptr[J];
+  const int64_t fo = F.front_off[J];
+  const int64_t nk = (w + MF_BW - 1) / MF_BW;
+  const int64_t t = k + 1 + (blockIdx.x - pref[a]);
+  const int64_t p0 = (int64_t)MF_BW * k;
+  const int wk = (int)(w - p0 < MF_BW ? w - p0 : MF_BW);
+  const int b = F.sn_blk0[J] + k;
+  const int64_t tb = tile_begin(t, nk, w, m), te = tile_begin(t + 1, nk, w, m);
+  const int R = (int)(te - tb);
+  const int tid = threadIdx.x;
+  const double* inv = F.fstore + F.blk_inv[b];
+  for (int idx = tid; idx < wk * wk; idx += NT) {
+    int c = idx / wk, r = idx % wk;
+    Ls[c * 65 + r] = inv[idx];
+  }
+  for (int idx = tid; idx < R * wk; idx += NT) {
+    int c = idx / R, r = idx % R;
+    At[c * 65 + r] = F.ws[fo + (p0 + c) * m + tb + r];
+  }
+  if (tid < wk) Dk[tid] = F.Dpiv[c0 + p0 + tid];
+  __syncthreads();
+  const int64_t noff = F.blk_noff[b];
+  double* L = F.fstore + F.blk_off[b] + (tb - (p0 + wk));
+  for (int idx = tid; idx < R * wk; idx += NT) {
+    int r = idx % R, c = idx / R;
+    double s = 0.0;
+    for (int j = 0; j <= c; ++j) s += At[j * 65 + r] * Ls[j * 65 + c];  // Linv(c, j)
+    L[r + (int64_t)c * noff] = s / Dk[c];
+  }
+}
+
+// UPDATE: A_ij −= L_ik D_k L_jkᵀ on the trailing tiles (i ≥ j > k) of each front.
+__global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t act_off, int n_act,
+                                                  int64_t pref_off) {
+  extern __shared__ double dsm[];
+  double* Ls = dsm;
+  double* Rs = dsm + 64 * 68;
+  const int64_t* pref = F.upd_pref + pref_off;
+  const int a = find_seg(pref, n_act + 1, blockIdx.x);
+  const int J = F.act[act_off + a];
+  const int64_t c0 = F.sn_start[J], w = F.sn_start[J + 1] - c0;
+  const int64_t m = F.sn_rowptr[J + 1] - F.sn_rowptr[J];
+  const int64_t fo = F.front_off[J];
+  const int64_t nk = (w + MF_BW - 1) / MF_BW;
+  const int64_t q = blockIdx.x - pref[a];
+  int64_t ii = (int64_t)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+  while (ii * (ii + 1) / 2 > q) --ii;
+  while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+  const int64_t jj = q - ii * (ii + 1) / 2;
+  const int64_t ti = k + 1 + ii, tj = k + 1 + jj;
+  const int64_t p0 = (int64_t)MF_BW * k;
+  const int wk = (int)(w - p0 < MF_BW ? w - p0 : MF_BW);
+  const int b = F.sn_blk0[J] + k;
+  const int64_t ib = tile_begin(ti, nk, w, m), ie = tile_begin(ti + 1, nk, w, m);
+  const int64_t jb = tile_begin(tj, nk, w, m), je = tile_begin(tj + 1, nk, w, m);
+  const int Ri = (int)(ie - ib), Rj = (int)(je - jb);
+  const int64_t noff = F.blk_noff[b];
+  const double* L = F.fstore + F.blk_off[b] - (p0 + wk);  // index by front row
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < 64 * wk; idx += NT) {
+    int r = idx & 63, c = idx >> 6;
+    double d = F.Dpiv[c0 + p0 + c];
+    Ls[c * 68 + r] = r < Ri ? L[ib + r + (int64_t)c * noff] * d : 0.0;
+    Rs[c * 68 + r] = r < Rj ? L[jb + r + (int64_t)c * noff] : 0.0;
+  }
+  __syncthreads();
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+  for (int c = 0; c < wk; ++c) {
+    double lr[4], rs[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) lr[x] = Ls[c * 68 + tx + 16 * x];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) rs[y] = Rs[c * 68 + ty + 16 * y];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma(lr[x], rs[y], acc[x][y]);
+  }
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    int s = ty + 16 * y;
+    if (s >= Rj) continue;
+    double* col = F.ws + fo + (jb + s) * m + ib;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      int r = tx + 16 * x;
+      if (r < Ri) col[r] -= acc[x][y];
+    }
+  }
+}
+
+void mf_assemble(const DevFactor& F, const double* src_vals, cudaStream_t s) {
+  if (F.n_asm == 0) return;
+  int grid = (int)std::min<int64_t>((F.n_asm + NT - 1) / NT, 148 * 16);
+  k_mf_assemble<<<grid, NT, 0, s>>>(F, src_vals);
+}
+void mf_assemble_diag_add(const DevFactor& F, const double* D, const int64_t* perm, cudaStream_t s) {
+  int grid = (int)std::min<int64_t>((F.N + NT - 1) / NT, 148 * 16);
+  k_mf_diag_add<<<grid, NT, 0, s>>>(F, D, perm);
+}
+void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s) {
+  if (n_grp == 0) return;
+  int64_t grid = (n_grp * 32 + NT - 1) / NT;
+  k_mf_extend_add<<<(unsigned)grid, NT, 0, s>>>(F, grp_off, n_grp);
+}
+void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
+             int64_t upd_total, cudaStream_t s) {
+  if (n_act == 0) return;
+  static bool attr = false;
+  const size_t sd = 2 * 64 * 65 * 8, sp = (2 * 64 * 65 + 64) * 8, su = 2 * 64 * 68 * 8;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+    cudaFuncSetAttribute(k_mf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp);
+    cudaFuncSetAttribute(k_mf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
+    attr = true;
+  }
+  k_mf_diag<<<n_act, NT, sd, s>>>(F, k, act_off);
+  if (pan_total > 0) k_mf_panel<<<(unsigned)pan_total, NT, sp, s>>>(F, k, act_off, n_act, pref_off);
+  if (upd_total > 0) k_mf_update<<<(unsigned)upd_total, NT, su, s>>>(F, k, act_off, n_act, pref_off);
+}
+
+// ------------------------------------------------------------------------- triangular sweeps
+struct SweepShared {
+  int task;
+  unsigned epoch;
+  double rhs[64];
+  double y[64];
+  double red[4 * 64];
+};
+
+__device__ __forceinline__ void spin_u64(const unsigned long long* p, unsigned long long target) {
+  if (ld_acq_u64(p) >= target) return;
+  unsigned ns = 32;
+  while (ld_acq_u64(p) < target) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+__device__ __forceinline__ void spin_u32(const unsigned* p, unsigned target) {
+  if (ld_acq_u32(p) == target) return;
+  unsigned ns = 32;
+  while (ld_acq_u32(p) != target) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+// Forward sweep L y = b (unit lower L, factor order); y written to x.
+__global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double* x) {
+  extern __shared__ double sm[];
+  __shared__ SweepShared S;
+  const int tid = threadIdx.x;
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  if (tid == 0) S.epoch = *((volatile unsigned*)(F.sweep + 2)) + 1u;
+  __syncthreads();
+  const unsigned E = S.epoch;
+  while (true) {
+    if (tid == 0) {
+      unsigned t = atomicAdd(F.sweep + 0, 1u);
+      S.task = t < (unsigned)F.n_fwd_tasks ? F.fwd_tasks[t] : INT32_MIN;
+    }
+    __syncthreads();
+    const int task = S.task;
+    __syncthreads();
+    if (task == INT32_MIN) break;
+    if (task < 0) {
+      // ---------------- DIAG(b): y_b = L_bb⁻¹ (b_b − Σ updates)
+      const int b = -task - 1;
+      const int wk = F.blk_w[b];
+      const int64_t c0 = F.blk_col0[b];
+      const double* inv = F.fstore + F.blk_inv[b];
+      for (int idx = tid; idx < wk * wk; idx += NT) {
+        int c = idx / wk, r = idx % wk;
+        sm[c * 65 + r] = inv[idx];
+      }
+      if (tid < wk) {
+        const int64_t c = c0 + tid;
+        double v;
+        if (R.ct.p != nullptr) {
+          v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+        } else {
+          v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+        }
+        S.rhs[tid] = v;
+      }
+      if (tid == 0) spin_u64(F.cnt_f + b, (unsigned long long)E * (unsigned long long)F.fwd_expect[b]);
+      __syncthreads();
+      if (tid < wk) {
+        double* ap = F.acc + c0 + tid;
+        S.rhs[tid] -= __ldcg(ap);
+        *ap = 0.0;
+      }
+      __syncthreads();
+      {
+        const int i = tid & 63, g = tid >> 6;
+        double s = 0.0;
+        if (i < wk)
+          for (int j = g; j <= i; j += 4) s += sm[j * 65 + i] * S.rhs[j];
+        S.red[g * 64 + i] = s;
+      }
+      __syncthreads();
+      if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_rel_u32(F.ready_f + b, E);
+    } else {
+      // ---------------- tile: acc[rows] += L_tile · y_b
+      const int ti = task;
+      const int b = F.tile_blk[ti];
+      const int wk = F.blk_w[b];
+      const int Rn = F.tile_nr[ti];
+      const int r0 = F.tile_r0[ti];
+      const int64_t noff = F.blk_noff[b];
+      const int64_t c0 = F.blk_col0[b];
+      const double* L = F.fstore + F.blk_off[b] + r0;
+      const int ld = Rn + 1;
+      for (int idx = tid; idx < Rn * wk; idx += NT) {
+        int c = idx / Rn, r = idx % Rn;
+        sm[c * ld + r] = L[r + (int64_t)c * noff];
+      }
+      if (tid == 0) spin_u32(F.ready_f + b, E);
+      __syncthreads();
+      if (tid < wk) S.y[tid] = __ldcg(x + c0 + tid);
+      __syncthreads();
+      const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
+      if (Rn <= 64) {
+        const int r = tid & 63, g = tid >> 6;
+        double s = 0.0;
+        if (r < Rn)
+          for (int c = g; c < wk; c += 4) s += sm[c * ld + r] * S.y[c];
+        S.red[g * 64 + r] = s;
+        __syncthreads();
+        if (tid < Rn) {
+          double v = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+          atomicAdd(F.acc + rows[tid], v);
+        }
+      } else {
+        for (int r = tid; r < Rn; r += NT) {
+          double s = 0.0;
+          for (int c = 0; c < wk; ++c) s += sm[c * ld + r] * S.y[c];
+          atomicAdd(F.acc + rows[r], s);
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(F.cnt_f + F.tile_dest[ti], 1ull);
+    }
+  }
+  if (tid == 0) {
+    unsigned d = atomicAdd(F.sweep + 1, 1u);
+    if (d == gridDim.x - 1) {
+      F.sweep[0] = 0u;
+      F.sweep[1] = 0u;
+      F.sweep[2] = E;
+      __threadfence();
+    }
+  }
+}
+
+// Backward sweep Lᵀ x = D⁻¹ y (in place in x).
+__global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const int* done_flag) {
+  extern __shared__ double sm[];
+  __shared__ SweepShared S;
+  const int tid = threadIdx.x;
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  if (tid == 0) S.epoch = *((volatile unsigned*)(F.sweep + 3)) + 1u;
+  __syncthreads();
+  const unsigned E = S.epoch;
+  while (true) {
+    if (tid == 0) {
+      unsigned t = atomicAdd(F.sweep + 0, 1u);
+      S.task = t < (unsigned)F.n_bwd_tasks ? F.bwd_tasks[t] : INT32_MIN;
+    }
+    __syncthreads();
+    const int task = S.task;
+    __syncthreads();
+    if (task == INT32_MIN) break;
+    if (task < 0) {
+      const int b = -task - 1;
+      const int wk = F.blk_w[b];
+      const int64_t c0 = F.blk_col0[b];
+      const double* inv = F.fstore + F.blk_inv[b];
+      for (int idx = tid; idx < wk * wk; idx += NT) {
+        int c = idx / wk, r = idx % wk;
+        sm[c * 65 + r] = inv[idx];
+      }
+      if (tid == 0) spin_u64(F.cnt_b + b, (unsigned long long)E * (unsigned long long)F.bwd_expect[b]);
+      __syncthreads();
+      if (tid < wk) {
+        double* tp = F.tacc + c0 + tid;
+        S.rhs[tid] = __ldcg(x + c0 + tid) / F.Dpiv[c0 + tid] - __ldcg(tp);
+        *tp = 0.0;
+      }
+      __syncthreads();
+      {
+        const int i = tid & 63, g = tid >> 6;
+        double s = 0.0;
+        if (i < wk)
+          for (int j = i + g; j < wk; j += 4) s += sm[i * 65 + j] * S.rhs[j];  // Linv(j, i)
+        S.red[g * 64 + i] = s;
+      }
+      __syncthreads();
+      if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_rel_u32(F.ready_b + b, E);
+    } else {
+      const int ti = task;
+      const int b = F.tile_blk[ti];
+      const int wk = F.blk_w[b];
+      const int Rn = F.tile_nr[ti];
+      const int r0 = F.tile_r0[ti];
+      const int64_t noff = F.blk_noff[b];
+      const int64_t c0 = F.blk_col0[b];
+      const double* L = F.fstore + F.blk_off[b] + r0;
+      const int ld = Rn + 1;
+      for (int idx = tid; idx < Rn * wk; idx += NT) {
+        int c = idx / Rn, r = idx % Rn;
+        sm[c * ld + r] = L[r + (int64_t)c * noff];
+      }
+      if (tid == 0) spin_u32(F.ready_b + F.tile_dest[ti], E);
+      __syncthreads();
+      const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
+      double* xr = sm + wk * ld;  // Rn values after the tile
+      for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r]);
+      __syncthreads();
+      const int lane = tid & 31, wid = tid >> 5;
+      const int P = wk >= 8 ? 1 : 8 / wk;
+      for (int it = wid; it < wk * P; it += NT / 32) {
+        const int c = it / P, part = it % P;
+        double s = 0.0;
+        for (int r = part * 32 + lane; r < Rn; r += 32 * P) s += sm[c * ld + r] * xr[r];
+        s = warp_sum(s);
+        if (lane == 0) S.red[it] = s;
+      }
+      __syncthreads();
+      if (tid < wk) {
+        double s = 0.0;
+        for (int part = 0; part < P; ++part) s += S.red[tid * P + part];
+        atomicAdd(F.tacc + c0 + tid, s);
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(F.cnt_b + b, 1ull);
+    }
+  }
+  if (tid == 0) {
+    unsigned d = atomicAdd(F.sweep + 1, 1u);
+    if (d == gridDim.x - 1) {
+      F.sweep[0] = 0u;
+      F.sweep[1] = 0u;
+      F.sweep[3] = E;
+      __threadfence();
+    }
+  }
+}
+
+static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)(TRSV_SMEM_DBL + 1024); }
+
+int trsv_grid(int device) {
+  static int cached[64] = {0};
+  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  int sms = 148, occ = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsv_smem_bytes());
+  cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsv_smem_bytes());
+  int o1 = 1, o2 = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_trsv_fwd, NT, trsv_smem_bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_trsv_bwd, NT, trsv_smem_bytes());
+  occ = std::max(1, std::min(o1, o2));
+  int g = sms * occ;
+  if (device >= 0 && device < 64) cached[device] = g;
+  return g;
+}
+
+void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s) {
+  k_trsv_fwd<<<grid, NT, trsv_smem_bytes(), s>>>(F, r, x);
+}
+void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s) {
+  k_trsv_bwd<<<grid, NT, trsv_smem_bytes(), s>>>(F, x, done_flag);
+}
+
+// ------------------------------------------------------------------------- K_F product and PCG
+// q = D∘p − C_f·z (a5) with the pᵀq reduction; last block: α = ρ / pᵀq.
+__global__ void __launch_bounds__(NT) k_kf_q(DevCSR Cf, const double* D, const double* p, const double* z,
+                                             double* q, double* partial, PcgState* st, int pcg_mode) {
+  __shared__ double sh[32];
+  if (pcg_mode && *((volatile int*)&st->done)) return;
+  double loc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < Cf.nrows; i += (int64_t)gridDim.x * NT) {
+    const double pi = p[i];
+    const double qi = D[i] * pi - csr_dot(Cf, i, z);
+    q[i] = qi;
+    loc += pi * qi;
+  }
+  if (!pcg_mode) return;
+  double v = block_reduce<0>(loc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    double pq = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->pq = pq;
+      if (!(pq > 0.0) || !isfinite(pq)) {
+        st->status = -3;
+        st->done = 1;
+      } else {
+        st->alpha = st->rho / pq;
+      }
+      st->arrive = 0;
+    }
+  }
+}
+
+// init: x = 0, r = b, z = M⁻¹ r, p = z, ρ = rᵀz, ‖b‖²
+__global__ void __launch_bounds__(NT) k_pcg_init(int prec, int64_t m2, const double* b, const double* D,
+                                                 double* x, double* r, double* z, double* p, double* partial,
+                                                 PcgState* st, double tol, int maxit) {
+  __shared__ double sh[32];
+  double bb = 0.0, rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    bb += bi * bi;
+    if (prec != 2) {
+      const double zi = prec == 1 ? bi / D[i] : bi;
+      z[i] = zi;
+      p[i] = zi;
+      rz += bi * zi;
+    }
+  }
+  double v1 = block_reduce<0>(bb, sh);
+  double v2 = block_reduce<0>(rz, sh);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = v1;
+    partial[gridDim.x + blockIdx.x] = v2;
+  }
+  if (is_last_block(&st->arrive)) {
+    double s1 = reduce_partials<0>(partial, gridDim.x, sh);
+    double s2 = reduce_partials<0>(partial + gridDim.x, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->bnorm2 = s1;
+      st->rr = s1;
+      st->rho = s2;
+      st->tol2 = tol * tol;
+      st->iter = 0;
+      st->maxit = maxit;
+      st->status = 0;
+      st->done = (s1 == 0.0) ? 1 : 0;
+      if (maxit <= 0 && s1 != 0.0) { st->done = 1; st->status = 1; }
+      st->arrive = 0;
+    }
+  }
+}
+
+// P_H init (after z = P_H⁻¹ r): p = z, ρ = rᵀz
+__global__ void __launch_bounds__(NT) k_pcg_init_ph(int64_t m2, const double* r, const double* z, double* p,
+                                                    double* partial, PcgState* st) {
+  __shared__ double sh[32];
+  if (*((volatile int*)&st->done)) return;
+  double rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT) {
+    p[i] = z[i];
+    rz += r[i] * z[i];
+  }
+  double v = block_reduce<0>(rz, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    double s = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->rho = s;
+      st->arrive = 0;
+    }
+  }
+}
+
+// x += αp; r −= αq; z = M⁻¹r (P_L / none); reductions ‖r‖², rᵀz; convergence; β.
+__global__ void __launch_bounds__(NT) k_pcg_update1(int prec, int64_t m2, const double* D, const double* p,
+                                                    const double* q, double* x, double* r, double* z,
+                                                    double* partial, PcgState* st) {
+  __shared__ double sh[32];
+  if (*((volatile int*)&st->done)) return;
+  const double alpha = st->alpha;
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    rr += ri * ri;
+    if (prec != 2) {
+      const double zi = prec == 1 ? ri / D[i] : ri;
+      z[i] = zi;
+      rz += ri * zi;
+    }
+  }
+  double v1 = block_reduce<0>(rr, sh);
+  double v2 = block_reduce<0>(rz, sh);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = v1;
+    partial[gridDim.x + blockIdx.x] = v2;
+  }
+  if (is_last_block(&st->arrive)) {
+    double s1 = reduce_partials<0>(partial, gridDim.x, sh);
+    double s2 = reduce_partials<0>(partial + gridDim.x, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->iter += 1;
+      st->rr = s1;
+      if (!isfinite(s1)) {
+        st->status = -3;
+        st->done = 1;
+      } else if (s1 <= st->tol2 * st->bnorm2) {
+        st->done = 1;
+      } else if (st->iter >= st->maxit) {
+        st->done = 1;
+        st->status = 1;
+      } else if (prec != 2) {
+        st->beta = s2 / st->rho;
+        st->rho = s2;
+        st->rz = s2;
+      }
+      st->arrive = 0;
+    }
+  }
+}
+
+// P_H: ρ' = rᵀz after z = P_H⁻¹ r; β = ρ'/ρ.
+__global__ void __launch_bounds__(NT) k_pcg_rz_ph(int64_t m2, const double* r, const double* z, double* partial,
+                                                  PcgState* st) {
+  __shared__ double sh[32];
+  if (*((volatile int*)&st->done)) return;
+  double rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT)
+    rz += r[i] * z[i];
+  double v = block_reduce<0>(rz, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    double s = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->beta = s / st->rho;
+      st->rho = s;
+      st->rz = s;
+      st->arrive = 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z, double* p, PcgState* st) {
+  if (*((volatile int*)&st->done)) return;
+  const double beta = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT)
+    p[i] = z[i] + beta * p[i];
+}
+
+void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,
+          PcgState* st, int grid, cudaStream_t s, bool pcg_mode) {
+  k_kf_q<<<grid, NT, 0, s>>>(Cf, D, p, z, q, partial, st, pcg_mode ? 1 : 0);
+}
+void pcg_init(int prec, int64_t m2, const double* b, const double* D, double* x, double* r, double* z,
+              double* p, double* partial, PcgState* st, double tol, int maxit, int grid, cudaStream_t s) {
+  k_pcg_init<<<grid, NT, 0, s>>>(prec, m2, b, D, x, r, z, p, partial, st, tol, maxit);
+}
+void pcg_init_ph(int64_t m2, const double* r, const double* z, double* p, double* partial, PcgState* st,
+                 int grid, cudaStream_t s) {
+  k_pcg_init_ph<<<grid, NT, 0, s>>>(m2, r, z, p, partial, st);
+}
+void pcg_update1(int prec, int64_t m2, const double* D, const double* p, const double* q, double* x,
+                 double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s) {
+  k_pcg_update1<<<grid, NT, 0, s>>>(prec, m2, D, p, q, x, r, z, partial, st);
+}
+void pcg_rz_ph(int64_t m2, const double* r, const double* z, double* partial, PcgState* st, int grid,
+               cudaStream_t s) {
+  k_pcg_rz_ph<<<grid, NT, 0, s>>>(m2, r, z, partial, st);
+}
+void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid, cudaStream_t s) {
+  k_pcg_update2<<<grid, NT, 0, s>>>(m2, z, p, st);
+}
+
+__global__ void k_gather(double* out, const double* in, const int64_t* idx, int64_t n, const int* done) {
+  if (done != nullptr && *((volatile const int*)done)) return;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT)
+    out[i] = in[idx[i]];
+}
+__global__ void k_scatter(double* out, const double* in, const int64_t* idx, int64_t n, const int* done) {
+  if (done != nullptr && *((volatile const int*)done)) return;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT)
+    out[idx[i]] = in[i];
+}
+void gather(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s) {
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + NT - 1) / NT, 148 * 8));
+  k_gather<<<grid, NT, 0, s>>>(out, in, idx, n, done);
+}
+void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s) {
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + NT - 1) / NT, 148 * 8));
+  k_scatter<<<grid, NT, 0, s>>>(out, in, idx, n, done);
+}
+
+// ------------------------------------------------------------------------- IPM kernels
+__global__ void __launch_bounds__(NT) k_ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial,
+                                               IpmState* st) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT)
+    v += s_[i] * nu[i];
+  v = block_reduce<0>(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    double s = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->mu = s / (double)m2;                 // μ = sᵀν / m2
+      st->sigma_mu = st->sigma * st->mu;
+      st->arrive = 0;
+    }
+  }
+}
+
+// Rows [0,n): r_g = −(Hx + g − Aᵀλ − Cᵀν) (reading R1) → rhs_f[i];
+// rows [n,n+m1): r_e = Ax − b → rhs_f[i];
+// rows [n+m1, n+m1+m2): r_i = Cx − s − d, r_c = s∘ν − σμ, r_a = r_i + r_c/ν, D = s/ν.
+__global__ void __launch_bounds__(NT) k_ipm_resid(DevCSR Hf, DevCSR Atf, DevCSR Ctf, DevCSR Af, DevCSR Cf,
+                                                  const double* gf, const double* b, const double* d,
+                                                  const double* x, const double* lam, const double* nu,
+                                                  const double* s_, double* rhs_f, double* rc, double* ra,
+                                                  double* D, double* partial, IpmState* st) {
+  __shared__ double sh[32];
+  const int64_t n = Hf.nrows, m1 = Af.nrows, m2 = Cf.nrows;
+  const double smu = st->sigma_mu;
+  double mg = 0.0, me = 0.0, mi = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < n + m1 + m2; t += (int64_t)gridDim.x * NT) {
+    if (t < n) {
+      const double grad = csr_dot(Hf, t, x) + gf[t] - csr_dot(Atf, t, lam) - csr_dot(Ctf, t, nu);
+      rhs_f[t] = -grad;
+      mg = fmax(mg, fabs(grad));
+    } else if (t < n + m1) {
+      const int64_t i = t - n;
+      const double re = csr_dot(Af, i, x) - b[i];
+      rhs_f[t] = re;
+      me = fmax(me, fabs(re));
+    } else {
+      const int64_t i = t - n - m1;
+      const double si = s_[i], ni = nu[i];
+      const double ri = csr_dot(Cf, i, x) - si - d[i];
+      const double rci = si * ni - smu;
+      rc[i] = rci;
+      ra[i] = ri + rci / ni;
+      D[i] = si / ni;
+      mi = fmax(mi, fabs(ri));
+    }
+  }
+  double v1 = block_reduce<1>(mg, sh);
+  double v2 = block_reduce<1>(me, sh);
+  double v3 = block_reduce<1>(mi, sh);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = v1;
+    partial[gridDim.x + blockIdx.x] = v2;
+    partial[2 * gridDim.x + blockIdx.x] = v3;
+  }
+  if (is_last_block(&st->arrive)) {
+    double a1 = reduce_partials<1>(partial, gridDim.x, sh);
+    double a2 = reduce_partials<1>(partial + gridDim.x, gridDim.x, sh);
+    double a3 = reduce_partials<1>(partial + 2 * gridDim.x, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->rg_inf = a1;
+      st->re_inf = a2;
+      st->ri_inf = a3;
+      st->arrive = 0;
+    }
+  }
+}
+
+// r_ν = −r_a + C·y_x
+__global__ void k_ipm_rnu(DevCSR Cf, const double* ra, const double* y, double* rnu) {
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < Cf.nrows; i += (int64_t)gridDim.x * NT)
+    rnu[i] = -ra[i] + csr_dot(Cf, i, y);
+}
+
+// rhs of F(Δx;Δλ) = −(r_g + CᵀΔν; r_e); rg_re holds (r_g; r_e) in factor order.
+__global__ void k_ipm_recrhs(DevCSR Ctf, int64_t n, int64_t m1, const double* rg_re, const double* dnu,
+                             double* rhs_f) {
+  for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < n + m1; t += (int64_t)gridDim.x * NT)
+    rhs_f[t] = t < n ? -(rg_re[t] + csr_dot(Ctf, t, dnu)) : -rg_re[t];
+}
+
+// Δs = −V⁻¹r_c − DΔν; α_max over s, ν; α = min(1, τ α_max) (reading R3).
+__global__ void __launch_bounds__(NT) k_ipm_ds_alpha(int64_t m2, const double* rc, const double* nu,
+                                                     const double* D, const double* dnu, const double* s_,
+                                                     double* ds, double* partial, IpmState* st) {
+  __shared__ double sh[32];
+  double amin = DBL_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT) {
+    const double dsi = -rc[i] / nu[i] - D[i] * dnu[i];
+    ds[i] = dsi;
+    if (dsi < 0.0) amin = fmin(amin, -s_[i] / dsi);
+    const double dn = dnu[i];
+    if (dn < 0.0) amin = fmin(amin, -nu[i] / dn);
+  }
+  double v = block_reduce<2>(amin, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    double a = reduce_partials<2>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->alpha_max = a;
+      st->alpha = fmin(1.0, st->tau * a);
+      st->arrive = 0;
+    }
+  }
+}
+
+__global__ void k_ipm_update(int64_t N, int64_t m2, const double* dxl, const double* dnu, const double* ds,
+                             double* xl, double* nu, double* s_, const IpmState* st) {
+  const double a = st->alpha;
+  for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < N + m2; t += (int64_t)gridDim.x * NT) {
+    if (t < N) {
+      xl[t] += a * dxl[t];
+    } else {
+      const int64_t i = t - N;
+      nu[i] += a * dnu[i];
+      s_[i] += a * ds[i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_ipm_objective(DevCSR Hf, const double* gf, const double* x,
+                                                      double* partial, IpmState* st) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < Hf.nrows; i += (int64_t)gridDim.x * NT)
+    v += x[i] * (0.5 * csr_dot(Hf, i, x) + gf[i]);
+  v = block_reduce<0>(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    double s = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->objective = s;
+      st->arrive = 0;
+    }
+  }
+}
+
+void ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial, IpmState* st, int grid,
+            cudaStream_t s) {
+  k_ipm_mu<<<grid, NT, 0, s>>>(m2, s_, nu, partial, st);
+}
+void ipm_residuals(const DevCSR& Hf, const DevCSR& Atf, const DevCSR& Ctf, const DevCSR& Af, const DevCSR& Cf,
+                   const double* gf, const double* b, const double* d, const double* x, const double* lam,
+                   const double* nu, const double* s_, double* rhs_f, double* rc, double* ra, double* D,
+                   double* partial, IpmState* st, int grid, cudaStream_t s) {
+  k_ipm_resid<<<grid, NT, 0, s>>>(Hf, Atf, Ctf, Af, Cf, gf, b, d, x, lam, nu, s_, rhs_f, rc, ra, D, partial, st);
+}
+void ipm_rnu(const DevCSR& Cf, const double* ra, const double* y, double* rnu, int grid, cudaStream_t s) {
+  k_ipm_rnu<<<grid, NT, 0, s>>>(Cf, ra, y, rnu);
+}
+void ipm_recovery_rhs(const DevCSR& Ctf, int64_t n, int64_t m1, const double* rg_re, const double* dnu,
+                      double* rhs_f, int grid, cudaStream_t s) {
+  k_ipm_recrhs<<<grid, NT, 0, s>>>(Ctf, n, m1, rg_re, dnu, rhs_f);
+}
+void ipm_ds_alpha(int64_t m2, const double* rc, const double* nu, const double* D, const double* dnu,
+                  const double* s_, double* ds, double* partial, IpmState* st, int grid, cudaStream_t s) {
+  k_ipm_ds_alpha<<<grid, NT, 0, s>>>(m2, rc, nu, D, dnu, s_, ds, partial, st);
+}
+void ipm_update(int64_t N, int64_t m2, const double* dxl, const double* dnu, const double* ds, double* xl,
+                double* nu, double* s_, const IpmState* st, int grid, cudaStream_t s) {
+  k_ipm_update<<<grid, NT, 0, s>>>(N, m2, dxl, dnu, ds, xl, nu, s_, st);
+}
+void ipm_objective(const DevCSR& Hf, const double* gf, const double* x, double* partial, IpmState* st, int grid,
+                   cudaStream_t s) {
+  k_ipm_objective<<<grid, NT, 0, s>>>(Hf, gf, x, partial, st);
+}
+
+// ------------------------------------------------------------------------- T = C diag(H)⁻¹ Cᵀ values
+// One thread per stored entry (i, j): sparse dot of C rows i and j weighted by 1/H_kk.
+__global__ void k_t_values(DevCSR C, const double* hdiag, const int64_t* t_row, const int32_t* t_col,
+                           int64_t nnz, double* t_val) {
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * NT) {
+    const int64_t i = t_row[e], j = t_col[e];
+    int64_t a = C.p[i], ae = C.p[i + 1], b = C.p[j], be = C.p[j + 1];
+    double s = 0.0;
+    while (a < ae && b < be) {
+      const int32_t ca = C.i[a], cb = C.i[b];
+      if (ca == cb) {
+        s += C.v[a] * C.v[b] / hdiag[ca];
+        ++a;
+        ++b;
+      } else if (ca < cb) {
+        ++a;
+      } else {
+        ++b;
+      }
+    }
+    t_val[e] = s;
+  }
+}
+void t_values(const DevCSR& Cnu, const double* hdiag, const int64_t* t_row, const int32_t* t_col, int64_t nnz_t,
+              double* t_val, cudaStream_t s) {
+  if (nnz_t == 0) return;
+  int grid = (int)std::min<int64_t>((nnz_t + NT - 1) / NT, 148 * 16);
+  k_t_values<<<grid, NT, 0, s>>>(Cnu, hdiag, t_row, t_col, nnz_t, t_val);
+}
+
+}  // namespace qpb

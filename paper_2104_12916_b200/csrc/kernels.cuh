@@ -1,0 +1,151 @@
+// Device-side data structures and kernel declarations (sm_100a, fp64).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qpb {
+
+constexpr int NT = 256;            // threads per CTA for every kernel here
+constexpr int MF_BW = 64;          // pivot block (must equal symbolic BW)
+constexpr int TRSV_SMEM_DBL = 4096 + 1088;  // tile (≤4096 + padding) or Linv (64×65)
+
+// One factor (F or P_H): symbolic plan + numeric storage + trsv sweep state.
+struct DevFactor {
+  int64_t N, ns, nb, n_tiles, n_fwd_tasks, n_bwd_tasks;
+  // supernodes
+  const int64_t* sn_start;
+  const int64_t* sn_rowptr;
+  const int32_t* sn_rows;
+  const int64_t* front_off;
+  const int32_t* sn_blk0;
+  // blocks
+  const int32_t* blk_col0;
+  const int32_t* blk_w;
+  const int32_t* blk_noff;
+  const int64_t* blk_rows;
+  const int64_t* blk_inv;
+  const int64_t* blk_off;
+  // trsv tiles / tasks
+  const int32_t* tile_blk;
+  const int32_t* tile_r0;
+  const int32_t* tile_nr;
+  const int32_t* tile_dest;
+  const int32_t* fwd_tasks;
+  const int32_t* bwd_tasks;
+  const int32_t* fwd_expect;
+  const int32_t* bwd_expect;
+  // numeric
+  double* ws;         // multifrontal workspace (fronts)
+  double* fstore;     // factor storage: per block Linv (w×w) + off-diagonal (noff×w)
+  double* Dpiv;       // pivots, factor order
+  const signed char* pivsign;
+  // trsv sweep state
+  double* acc;                    // N: forward accumulators
+  double* tacc;                   // N: backward accumulators
+  unsigned long long* cnt_f;      // nb
+  unsigned long long* cnt_b;      // nb
+  unsigned int* ready_f;          // nb
+  unsigned int* ready_b;          // nb
+  unsigned int* sweep;            // [0] ticket, [1] finished CTAs, [2] fwd epoch, [3] bwd epoch
+  // multifrontal plan
+  const int64_t* asm_dst;
+  const double* asm_val;
+  const int64_t* asm_src;
+  int64_t n_asm;
+  const int64_t* diag_dst;
+  const int32_t* relind;
+  const int64_t* relind_off;
+  const int32_t* grp_P;
+  const int32_t* grp_pc;
+  const int64_t* grp_ptr;
+  const int32_t* grp_K;
+  const int32_t* grp_j;
+  const int32_t* act;
+  const int64_t* pan_pref;
+  const int64_t* upd_pref;
+  int* status;        // pivot failures (device int)
+};
+
+// CSR on the device (int64 row pointers, int32 columns).
+struct DevCSR {
+  int64_t nrows, ncols, nnz;
+  const int64_t* p;
+  const int32_t* i;
+  const double* v;
+};
+
+// PCG scalar state (device), written by last-block reductions.
+struct PcgState {
+  double rho, pq, rr, rz, bnorm2, tol2, alpha, beta;
+  int iter, maxit, done, status;
+  unsigned int arrive;
+  int pad;
+};
+
+// IPM scalar state (device).
+struct IpmState {
+  double mu, sigma_mu, sigma, tau;
+  double rg_inf, re_inf, ri_inf;
+  double alpha, alpha_max;
+  double objective;
+  unsigned int arrive;
+  int pad;
+};
+
+// ---- multifrontal factorization
+void mf_assemble(const DevFactor& F, const double* src_vals, cudaStream_t s);
+void mf_assemble_diag_add(const DevFactor& F, const double* D, const int64_t* perm, cudaStream_t s);
+void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s);
+void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
+             int64_t upd_total, cudaStream_t s);
+
+// ---- level-free task-graph triangular sweeps (persistent kernels)
+struct SweepRhs {
+  const double* rhs;        // dense rhs (factor order) or nullptr
+  const int64_t* in_perm;   // optional gather index for rhs (rhs[in_perm[c]])
+  DevCSR ct;                // optional: rhs[c] = Σ ct(c,:)·p for c < ct.nrows (K_F: Cᵀp fused)
+  const double* p;
+  const int* done_flag;     // early-exit flag (PCG converged) or nullptr
+};
+void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s);
+void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s);
+int trsv_grid(int device);
+
+// ---- vector / SpMV kernels
+void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,
+          PcgState* st, int grid, cudaStream_t s, bool pcg_mode);
+void pcg_init(int prec, int64_t m2, const double* b, const double* D, double* x, double* r, double* z,
+              double* p, double* partial, PcgState* st, double tol, int maxit, int grid, cudaStream_t s);
+void pcg_init_ph(int64_t m2, const double* r, const double* z, double* p, double* partial, PcgState* st,
+                 int grid, cudaStream_t s);
+void pcg_update1(int prec, int64_t m2, const double* D, const double* p, const double* q, double* x,
+                 double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s);
+void pcg_rz_ph(int64_t m2, const double* r, const double* z, double* partial, PcgState* st, int grid,
+               cudaStream_t s);
+void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid, cudaStream_t s);
+
+void gather(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
+void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
+
+// ---- IPM kernels (a9–a11)
+void ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial, IpmState* st, int grid,
+            cudaStream_t s);
+void ipm_residuals(const DevCSR& Hf, const DevCSR& Atf, const DevCSR& Ctf, const DevCSR& Af, const DevCSR& Cf,
+                   const double* gf, const double* b, const double* d, const double* x, const double* lam,
+                   const double* nu, const double* s_, double* rhs_f, double* rc, double* ra, double* D,
+                   double* partial, IpmState* st, int grid, cudaStream_t s);
+void ipm_rnu(const DevCSR& Cf, const double* ra, const double* y, double* rnu, int grid, cudaStream_t s);
+void ipm_recovery_rhs(const DevCSR& Ctf, int64_t n, int64_t m1, const double* rg_re, const double* dnu,
+                      double* rhs_f, int grid, cudaStream_t s);
+void ipm_ds_alpha(int64_t m2, const double* rc, const double* nu, const double* D, const double* dnu,
+                  const double* s_, double* ds, double* partial, IpmState* st, int grid, cudaStream_t s);
+void ipm_update(int64_t N, int64_t m2, const double* dxl, const double* dnu, const double* ds, double* xl,
+                double* nu, double* s_, const IpmState* st, int grid, cudaStream_t s);
+void ipm_objective(const DevCSR& Hf, const double* gf, const double* x, double* partial, IpmState* st, int grid,
+                   cudaStream_t s);
+
+// ---- P_H setup: numeric T = C diag(H)^-1 C^T on a given pattern
+void t_values(const DevCSR& Cnu /*m2×n, original cols*/, const double* hdiag, const int64_t* t_row,
+              const int32_t* t_col, int64_t nnz_t, double* t_val, cudaStream_t s);
+
+}  // namespace qpb

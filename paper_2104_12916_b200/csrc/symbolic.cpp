@@ -1,0 +1,480 @@
+// Host symbolic analysis (see symbolic.h).  Plain C++; runs once per factor.
+//
+// Definitions follow SURVEY.md §8(c) c4 / DESIGN.md §Structures:
+//   etree      Liu's algorithm on the lower pattern (parent(j) = min{i>j: L_ij≠0})
+//   colcounts  row-subtree traversal: row i of L = ∪ paths k→i in the etree
+//              over F_ik ≠ 0, k < i (O(nnz(L)))
+//   rowlev     lev(i) = 1 + max{lev(j): L_ij ≠ 0, j<i}, 0 without off-diagonals
+//   supernodes j joins j−1 iff parent(j−1)=j and cc(j−1)=cc(j)+1
+//   sn levels  0 for leaves, 1 + max over children
+#include "symbolic.h"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+
+namespace qpb {
+
+LowerMatrix build_F_lower(int64_t n, int64_t m1, const int64_t* Hp, const int32_t* Hi, const double* Hx,
+                          const int64_t* Ap, const int32_t* Ai, const double* Ax,
+                          const std::vector<int64_t>& xperm) {
+  LowerMatrix M;
+  const int64_t N = n + m1;
+  M.N = N;
+  std::vector<int64_t> pinv(n);
+  for (int64_t i = 0; i < n; ++i) pinv[xperm[i]] = i;
+  M.diag.assign(N, 0.0);
+  std::vector<int64_t> cnt(N + 1, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = Hp[i]; p < Hp[i + 1]; ++p) {
+      int64_t j = Hi[p];
+      if (pinv[i] > pinv[j]) cnt[pinv[j] + 1]++;
+      else if (i == j) M.diag[pinv[i]] = -Hx[p];  // (1,1) block of F is −H
+    }
+  for (int64_t i = 0; i < m1; ++i)
+    for (int64_t p = Ap[i]; p < Ap[i + 1]; ++p) cnt[pinv[Ai[p]] + 1]++;  // A in rows n+i
+  for (int64_t j = 0; j < N; ++j) cnt[j + 1] += cnt[j];
+  M.colptr = cnt;
+  M.rowind.resize(cnt[N]);
+  M.val.resize(cnt[N]);
+  std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = Hp[i]; p < Hp[i + 1]; ++p) {
+      int64_t j = Hi[p];
+      if (pinv[i] > pinv[j]) {
+        int64_t q = pos[pinv[j]]++;
+        M.rowind[q] = (int32_t)pinv[i];
+        M.val[q] = -Hx[p];
+      }
+    }
+  for (int64_t i = 0; i < m1; ++i)
+    for (int64_t p = Ap[i]; p < Ap[i + 1]; ++p) {
+      int64_t q = pos[pinv[Ai[p]]]++;
+      M.rowind[q] = (int32_t)(n + i);
+      M.val[q] = Ax[p];
+    }
+  // sort rows inside each column
+  std::vector<std::pair<int32_t, double>> tmp;
+  for (int64_t j = 0; j < N; ++j) {
+    int64_t a = M.colptr[j], b = M.colptr[j + 1];
+    tmp.clear();
+    for (int64_t q = a; q < b; ++q) tmp.emplace_back(M.rowind[q], M.val[q]);
+    std::sort(tmp.begin(), tmp.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    for (int64_t q = a; q < b; ++q) { M.rowind[q] = tmp[q - a].first; M.val[q] = tmp[q - a].second; }
+  }
+  return M;
+}
+
+static inline int64_t tile_begin(int64_t t, int64_t nk, int64_t w, int64_t m) {
+  int64_t v = t < nk ? (int64_t)BW * t : w + (int64_t)BW * (t - nk);
+  return v < m ? v : m;
+}
+
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
+  const int64_t N = M.N;
+  S.N = N;
+  // ---------------------------------------------------------------- row form of the strict lower part
+  std::vector<int64_t> rp(N + 1, 0);
+  for (int64_t q = 0; q < (int64_t)M.rowind.size(); ++q) rp[M.rowind[q] + 1]++;
+  for (int64_t i = 0; i < N; ++i) rp[i + 1] += rp[i];
+  std::vector<int32_t> rc(rp[N]);
+  {
+    std::vector<int64_t> pos(rp.begin(), rp.end() - 1);
+    for (int64_t j = 0; j < N; ++j)
+      for (int64_t q = M.colptr[j]; q < M.colptr[j + 1]; ++q) rc[pos[M.rowind[q]]++] = (int32_t)j;
+  }
+  // ---------------------------------------------------------------- elimination tree (Liu)
+  S.parent.assign(N, -1);
+  {
+    std::vector<int64_t> anc(N, -1);
+    for (int64_t i = 0; i < N; ++i) {
+      for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        int64_t r = rc[q];
+        while (anc[r] != -1 && anc[r] != i) {
+          int64_t t = anc[r];
+          anc[r] = i;
+          r = t;
+        }
+        if (anc[r] == -1) {
+          anc[r] = i;
+          S.parent[r] = i;
+        }
+      }
+    }
+  }
+  // ---------------------------------------------------------------- column counts + row levels
+  S.colcount.assign(N, 0);
+  S.rowlev.assign(N, 0);
+  {
+    std::vector<int64_t> mark(N, -1);
+    for (int64_t i = 0; i < N; ++i) {
+      mark[i] = i;
+      S.colcount[i] += 1;
+      int64_t lev = 0;
+      for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        int64_t j = rc[q];
+        while (mark[j] != i) {
+          mark[j] = i;
+          S.colcount[j] += 1;
+          lev = std::max(lev, S.rowlev[j] + 1);
+          j = S.parent[j];
+          if (j < 0) return "etree walk escaped the tree (internal error)";
+        }
+      }
+      S.rowlev[i] = lev;
+    }
+  }
+  S.nnz_L = 0;
+  S.c_fact = 0;
+  S.n_rowlev = 0;
+  for (int64_t j = 0; j < N; ++j) {
+    S.nnz_L += S.colcount[j];
+    S.c_fact += (double)S.colcount[j] * (double)S.colcount[j];
+    S.n_rowlev = std::max(S.n_rowlev, S.rowlev[j] + 1);
+  }
+  // ---------------------------------------------------------------- supernodes
+  S.sn_start.clear();
+  S.sn_start.push_back(0);
+  for (int64_t j = 1; j < N; ++j)
+    if (!(S.parent[j - 1] == j && S.colcount[j - 1] == S.colcount[j] + 1)) S.sn_start.push_back(j);
+  S.sn_start.push_back(N);
+  const int64_t ns = (int64_t)S.sn_start.size() - 1;
+  S.ns = ns;
+  std::vector<int64_t> col2sn(N);
+  for (int64_t J = 0; J < ns; ++J)
+    for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) col2sn[c] = J;
+  S.sn_parent.assign(ns, -1);
+  for (int64_t J = 0; J < ns; ++J) {
+    int64_t p = S.parent[S.sn_start[J + 1] - 1];
+    if (p >= 0) S.sn_parent[J] = col2sn[p];
+  }
+  S.sn_level.assign(ns, 0);
+  for (int64_t J = 0; J < ns; ++J)
+    if (S.sn_parent[J] >= 0)
+      S.sn_level[S.sn_parent[J]] = std::max(S.sn_level[S.sn_parent[J]], S.sn_level[J] + 1);
+  S.n_levels = 0;
+  for (int64_t J = 0; J < ns; ++J) S.n_levels = std::max(S.n_levels, S.sn_level[J] + 1);
+  std::vector<std::vector<int32_t>> children(ns);
+  for (int64_t J = 0; J < ns; ++J)
+    if (S.sn_parent[J] >= 0) children[S.sn_parent[J]].push_back((int32_t)J);
+  // ---------------------------------------------------------------- supernode row structures
+  S.sn_rowptr.assign(ns + 1, 0);
+  S.sn_rows.clear();
+  {
+    std::vector<int64_t> mark(N, -1);
+    std::vector<int32_t> buf;
+    for (int64_t J = 0; J < ns; ++J) {
+      const int64_t c0 = S.sn_start[J], c1 = S.sn_start[J + 1];
+      buf.clear();
+      for (int64_t c = c0; c < c1; ++c)
+        for (int64_t q = M.colptr[c]; q < M.colptr[c + 1]; ++q) {
+          int64_t r = M.rowind[q];
+          if (r >= c1 && mark[r] != J) { mark[r] = J; buf.push_back((int32_t)r); }
+        }
+      for (int32_t K : children[J]) {
+        for (int64_t q = S.sn_rowptr[K]; q < S.sn_rowptr[K + 1]; ++q) {
+          int64_t r = S.sn_rows[q];
+          if (r >= c1 && mark[r] != J) { mark[r] = J; buf.push_back((int32_t)r); }
+        }
+      }
+      std::sort(buf.begin(), buf.end());
+      for (int64_t c = c0; c < c1; ++c) S.sn_rows.push_back((int32_t)c);
+      S.sn_rows.insert(S.sn_rows.end(), buf.begin(), buf.end());
+      S.sn_rowptr[J + 1] = (int64_t)S.sn_rows.size();
+      if (S.sn_rowptr[J + 1] - S.sn_rowptr[J] != S.colcount[c0])
+        return "supernode structure does not match column count (internal error)";
+    }
+  }
+  // ---------------------------------------------------------------- fronts
+  S.front_off.assign(ns, 0);
+  S.ws_size = 0;
+  for (int64_t J = 0; J < ns; ++J) {
+    int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+    S.front_off[J] = S.ws_size;
+    S.ws_size += m * m;
+    S.ws_size = (S.ws_size + 1) & ~int64_t(1);
+  }
+  // ---------------------------------------------------------------- blocks + factor storage
+  S.sn_blk0.assign(ns + 1, 0);
+  S.blk_col0.clear(); S.blk_w.clear(); S.blk_sn.clear(); S.blk_noff.clear();
+  S.blk_rows.clear(); S.blk_inv.clear(); S.blk_off.clear();
+  S.fs_size = 0;
+  for (int64_t J = 0; J < ns; ++J) {
+    const int64_t c0 = S.sn_start[J], w = S.sn_start[J + 1] - c0;
+    const int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+    S.sn_blk0[J] = (int32_t)S.blk_col0.size();
+    for (int64_t k = 0; k * BW < w; ++k) {
+      int64_t wk = std::min<int64_t>(BW, w - k * BW);
+      int64_t noff = m - k * BW - wk;
+      S.blk_col0.push_back((int32_t)(c0 + k * BW));
+      S.blk_w.push_back((int32_t)wk);
+      S.blk_sn.push_back((int32_t)J);
+      S.blk_noff.push_back((int32_t)noff);
+      S.blk_rows.push_back(S.sn_rowptr[J] + k * BW + wk);
+      S.blk_inv.push_back(S.fs_size);
+      S.fs_size += wk * wk;
+      S.fs_size = (S.fs_size + 1) & ~int64_t(1);
+      S.blk_off.push_back(S.fs_size);
+      S.fs_size += noff * wk;
+      S.fs_size = (S.fs_size + 1) & ~int64_t(1);
+    }
+  }
+  S.sn_blk0[ns] = (int32_t)S.blk_col0.size();
+  S.nb = (int64_t)S.blk_col0.size();
+  S.col2blk.assign(N, 0);
+  for (int64_t b = 0; b < S.nb; ++b)
+    for (int64_t c = S.blk_col0[b]; c < S.blk_col0[b] + S.blk_w[b]; ++c) S.col2blk[c] = (int32_t)b;
+  // ---------------------------------------------------------------- trsv tiles and task queues
+  S.tile_blk.clear(); S.tile_r0.clear(); S.tile_nr.clear(); S.tile_dest.clear();
+  S.fwd_expect.assign(S.nb, 0);
+  S.bwd_expect.assign(S.nb, 0);
+  std::vector<int64_t> blk_tile0(S.nb + 1, 0);
+  for (int64_t b = 0; b < S.nb; ++b) {
+    blk_tile0[b] = (int64_t)S.tile_blk.size();
+    const int64_t wk = S.blk_w[b], noff = S.blk_noff[b];
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(1024, TILE_ELEMS / wk));
+    int64_t r = 0;
+    while (r < noff) {
+      int32_t dest = S.col2blk[S.sn_rows[S.blk_rows[b] + r]];
+      int64_t e = r + 1;
+      while (e < noff && e - r < cap && S.col2blk[S.sn_rows[S.blk_rows[b] + e]] == dest) ++e;
+      S.tile_blk.push_back((int32_t)b);
+      S.tile_r0.push_back((int32_t)r);
+      S.tile_nr.push_back((int32_t)(e - r));
+      S.tile_dest.push_back(dest);
+      S.fwd_expect[dest] += 1;
+      S.bwd_expect[b] += 1;
+      r = e;
+    }
+  }
+  blk_tile0[S.nb] = (int64_t)S.tile_blk.size();
+  S.fwd_tasks.clear();
+  S.bwd_tasks.clear();
+  for (int64_t b = 0; b < S.nb; ++b) {
+    S.fwd_tasks.push_back(-(int32_t)b - 1);
+    for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back((int32_t)t);
+  }
+  for (int64_t b = S.nb - 1; b >= 0; --b) {
+    for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back((int32_t)t);
+    S.bwd_tasks.push_back(-(int32_t)b - 1);
+  }
+  // ---------------------------------------------------------------- assembly map, relative indices
+  S.asm_dst.clear();
+  S.asm_val.clear();
+  S.asm_src.clear();
+  S.diag_dst.assign(N, 0);
+  S.relind.clear();
+  S.relind_off.assign(ns, -1);
+  {
+    std::vector<int32_t> posmap(N, -1);
+    for (int64_t J = 0; J < ns; ++J) {
+      const int64_t c0 = S.sn_start[J], c1 = S.sn_start[J + 1];
+      const int64_t r0 = S.sn_rowptr[J], m = S.sn_rowptr[J + 1] - r0;
+      for (int64_t q = 0; q < m; ++q) posmap[S.sn_rows[r0 + q]] = (int32_t)q;
+      for (int64_t c = c0; c < c1; ++c) {
+        const int64_t colbase = S.front_off[J] + (c - c0) * m;
+        S.diag_dst[c] = colbase + posmap[c];
+        S.asm_dst.push_back(colbase + posmap[c]);
+        S.asm_val.push_back(M.diag.empty() ? 0.0 : M.diag[c]);
+        S.asm_src.push_back(M.diag_src.empty() ? -1 : M.diag_src[c]);
+        for (int64_t q = M.colptr[c]; q < M.colptr[c + 1]; ++q) {
+          S.asm_dst.push_back(colbase + posmap[M.rowind[q]]);
+          S.asm_val.push_back(M.val.empty() ? 0.0 : M.val[q]);
+          S.asm_src.push_back(M.src.empty() ? -1 : M.src[q]);
+        }
+      }
+      for (int32_t K : children[J]) {
+        const int64_t k0 = S.sn_rowptr[K], mK = S.sn_rowptr[K + 1] - k0;
+        const int64_t wK = S.sn_start[K + 1] - S.sn_start[K];
+        S.relind_off[K] = (int64_t)S.relind.size();
+        for (int64_t q = wK; q < mK; ++q) {
+          int32_t p = posmap[S.sn_rows[k0 + q]];
+          if (p < 0) return "child row missing from parent front (internal error)";
+          S.relind.push_back(p);
+        }
+      }
+      for (int64_t q = 0; q < m; ++q) posmap[S.sn_rows[r0 + q]] = -1;
+    }
+  }
+  // ---------------------------------------------------------------- levels: extend-add groups and steps
+  std::vector<std::vector<int32_t>> by_level(S.n_levels);
+  for (int64_t J = 0; J < ns; ++J) by_level[S.sn_level[J]].push_back((int32_t)J);
+  S.grp_P.clear(); S.grp_pc.clear(); S.grp_K.clear(); S.grp_j.clear();
+  S.grp_ptr.assign(1, 0);
+  S.level_ea.assign(S.n_levels, LevelEA{0, 0});
+  S.steps.clear();
+  S.act.clear();
+  S.pan_pref.clear();
+  S.upd_pref.clear();
+  S.pref_off.clear();
+  std::vector<std::pair<int32_t, std::pair<int32_t, int32_t>>> ent;  // (pc, (K, j))
+  for (int64_t L = 0; L < S.n_levels; ++L) {
+    S.level_ea[L].grp_off = (int64_t)S.grp_P.size();
+    for (int32_t P : by_level[L]) {
+      ent.clear();
+      for (int32_t K : children[P]) {
+        const int64_t mK = S.sn_rowptr[K + 1] - S.sn_rowptr[K];
+        const int64_t wK = S.sn_start[K + 1] - S.sn_start[K];
+        for (int64_t j = wK; j < mK; ++j)
+          ent.push_back({S.relind[S.relind_off[K] + (j - wK)], {K, (int32_t)j}});
+      }
+      std::stable_sort(ent.begin(), ent.end(), [](auto& a, auto& b) { return a.first < b.first; });
+      for (size_t e = 0; e < ent.size();) {
+        size_t f = e;
+        while (f < ent.size() && ent[f].first == ent[e].first) {
+          S.grp_K.push_back(ent[f].second.first);
+          S.grp_j.push_back(ent[f].second.second);
+          ++f;
+        }
+        S.grp_P.push_back(P);
+        S.grp_pc.push_back(ent[e].first);
+        S.grp_ptr.push_back((int64_t)S.grp_K.size());
+        e = f;
+      }
+    }
+    S.level_ea[L].n_grp = (int64_t)S.grp_P.size() - S.level_ea[L].grp_off;
+    // steps
+    int64_t max_nk = 0;
+    for (int32_t J : by_level[L]) {
+      int64_t w = S.sn_start[J + 1] - S.sn_start[J];
+      max_nk = std::max(max_nk, (w + BW - 1) / BW);
+    }
+    for (int64_t k = 0; k < max_nk; ++k) {
+      StepDesc sd;
+      sd.level = (int)L;
+      sd.k = (int)k;
+      sd.act_off = (int64_t)S.act.size();
+      S.pref_off.push_back((int64_t)S.pan_pref.size());
+      S.pan_pref.push_back(0);
+      S.upd_pref.push_back(0);
+      int n_act = 0;
+      for (int32_t J : by_level[L]) {
+        const int64_t w = S.sn_start[J + 1] - S.sn_start[J];
+        const int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+        const int64_t nk = (w + BW - 1) / BW;
+        if (nk <= k) continue;
+        const int64_t ntile = nk + (m - w + BW - 1) / BW;
+        const int64_t T = ntile - k - 1;
+        S.act.push_back(J);
+        S.pan_pref.push_back(S.pan_pref.back() + T);
+        S.upd_pref.push_back(S.upd_pref.back() + T * (T + 1) / 2);
+        ++n_act;
+      }
+      sd.n_act = n_act;
+      sd.pan_total = S.pan_pref.back();
+      sd.upd_total = S.upd_pref.back();
+      S.steps.push_back(sd);
+    }
+  }
+  S.pivsign.assign(N, 1);
+  for (int64_t c = 0; c < std::min(N, n_negative); ++c) S.pivsign[c] = -1;
+  (void)tile_begin;
+  return "";
+}
+
+}  // namespace qpb
+
+namespace qpb {
+
+// Approximate minimum degree on the quotient graph (element absorption,
+// aggressive absorption of elements contained in the new element, AMD-style
+// external degree bound d_i ≤ |A_i| + |L_p \ i| + Σ_{e∈E_i\p} |L_e \ L_p|).
+// A fill-reducing heuristic for the x block of F and for P_H; the paper does
+// not fix an ordering (it used dense SYTRF).  Deterministic.
+std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx) {
+  std::vector<std::vector<int32_t>> Av(n), Ev(n), Le(n);
+  std::vector<int64_t> deg(n);
+  for (int64_t i = 0; i < n; ++i) {
+    Av[i].assign(idx.begin() + ptr[i], idx.begin() + ptr[i + 1]);
+    std::sort(Av[i].begin(), Av[i].end());
+    Av[i].erase(std::unique(Av[i].begin(), Av[i].end()), Av[i].end());
+    Av[i].erase(std::remove(Av[i].begin(), Av[i].end(), (int32_t)i), Av[i].end());
+    deg[i] = (int64_t)Av[i].size();
+  }
+  // degree buckets (doubly linked)
+  std::vector<int64_t> head(n + 1, -1), nxt(n, -1), prv(n, -1);
+  auto insert = [&](int64_t i) {
+    int64_t d = deg[i];
+    nxt[i] = head[d];
+    prv[i] = -1;
+    if (head[d] >= 0) prv[head[d]] = i;
+    head[d] = i;
+  };
+  auto remove = [&](int64_t i) {
+    if (prv[i] >= 0) nxt[prv[i]] = nxt[i];
+    else head[deg[i]] = nxt[i];
+    if (nxt[i] >= 0) prv[nxt[i]] = prv[i];
+    nxt[i] = prv[i] = -1;
+  };
+  for (int64_t i = n - 1; i >= 0; --i) insert(i);
+  std::vector<char> state(n, 0);  // 0 variable, 1 element, 2 absorbed / dead
+  std::vector<int64_t> mark(n, -1), wstamp(n, -1), w(n, 0);
+  std::vector<int64_t> order;
+  order.reserve(n);
+  std::vector<int32_t> Lp, tmp;
+  int64_t mind = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    while (mind <= n && head[mind] < 0) ++mind;
+    if (mind > n) break;
+    const int64_t p = head[mind];
+    remove(p);
+    // new element L_p
+    Lp.clear();
+    mark[p] = k;
+    for (int32_t v : Av[p])
+      if (state[v] == 0 && mark[v] != k) { mark[v] = k; Lp.push_back(v); }
+    for (int32_t e : Ev[p]) {
+      if (state[e] != 1) continue;
+      for (int32_t v : Le[e])
+        if (state[v] == 0 && mark[v] != k) { mark[v] = k; Lp.push_back(v); }
+      state[e] = 2;
+      std::vector<int32_t>().swap(Le[e]);
+    }
+    state[p] = 1;
+    std::vector<int32_t>().swap(Av[p]);
+    std::vector<int32_t>().swap(Ev[p]);
+    Le[p] = Lp;
+    order.push_back(p);
+    // |L_e \ L_p| for elements adjacent to L_p
+    for (int32_t i : Lp)
+      for (int32_t e : Ev[i]) {
+        if (state[e] != 1) continue;
+        if (wstamp[e] != k) { wstamp[e] = k; w[e] = (int64_t)Le[e].size(); }
+        w[e] -= 1;
+      }
+    const int64_t nrem = n - k - 1;
+    const int64_t lp = (int64_t)Lp.size();
+    for (int32_t i : Lp) {
+      tmp.clear();
+      int64_t ext = 0;
+      for (int32_t e : Ev[i]) {
+        if (state[e] != 1 || e == p) continue;
+        if (wstamp[e] == k && w[e] == 0) {  // L_e ⊆ L_p: aggressive absorption
+          state[e] = 2;
+          std::vector<int32_t>().swap(Le[e]);
+          continue;
+        }
+        tmp.push_back(e);
+        ext += wstamp[e] == k ? w[e] : (int64_t)Le[e].size();
+      }
+      tmp.push_back((int32_t)p);
+      Ev[i].swap(tmp);
+      tmp.clear();
+      for (int32_t v : Av[i])
+        if (state[v] == 0 && mark[v] != k) tmp.push_back(v);
+      Av[i].swap(tmp);
+      int64_t d = (int64_t)Av[i].size() + (lp - 1) + ext;
+      d = std::min(d, deg[i] + lp - 1);
+      d = std::min(d, nrem - 1 < 0 ? 0 : nrem - 1);
+      if (d < 0) d = 0;
+      remove(i);
+      deg[i] = d;
+      insert(i);
+      if (d < mind) mind = d;
+    }
+  }
+  return order;
+}
+
+}  // namespace qpb

@@ -1,0 +1,102 @@
+// Host symbolic analysis for the multifrontal LDLᵀ / Cholesky factors used by
+// the single-factorization IPM (arXiv 2104.12916):
+//   * F = [−H Aᵀ; A 0] ordered x-block first (fill-reducing order), λ last
+//     (P:L703–714 inertia; static 1×1 pivots, reading R5 in DESIGN.md);
+//   * P_H = D + C·diag(H)⁻¹·Cᵀ, pattern of T = C·Cᵀ.
+// Everything here is D-independent and computed once.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace qpb {
+
+constexpr int BW = 64;          // pivot block width (columns per trsv block column)
+constexpr int TILE_ELEMS = 4096; // max doubles in one trsv tile (32 KiB)
+
+// Lower-triangular (strict) pattern + values of a symmetric matrix already in
+// factor order, by columns, plus its diagonal.
+struct LowerMatrix {
+  int64_t N = 0;
+  std::vector<int64_t> colptr;   // N+1
+  std::vector<int32_t> rowind;   // strictly lower rows, sorted per column
+  std::vector<double> val;       // values (may be empty for pattern-only)
+  std::vector<double> diag;      // N diagonal values (may be empty)
+  std::vector<int64_t> src;      // optional source index per stored entry (P_H: index into T values)
+  std::vector<int64_t> diag_src; // optional source index of diagonal (P_H)
+};
+
+struct StepDesc {
+  int level, k;
+  int n_act;          // active fronts
+  int64_t act_off;    // offset into act list
+  int64_t pan_total;  // PANEL tiles
+  int64_t upd_total;  // UPDATE tiles
+};
+
+struct LevelEA {        // extend-add groups of one level
+  int64_t grp_off, n_grp;   // into grp arrays
+};
+
+struct Symbolic {
+  int64_t N = 0;
+  std::vector<int64_t> perm;      // new -> old (of the matrix being factored)
+  std::vector<int64_t> parent, colcount, rowlev;
+  int64_t nnz_L = 0, n_rowlev = 0;
+  double c_fact = 0;              // Σ cc²
+
+  // supernodes
+  int64_t ns = 0;
+  std::vector<int64_t> sn_start, sn_parent, sn_level, sn_rowptr;
+  std::vector<int32_t> sn_rows;   // global rows (factor order)
+  int64_t n_levels = 0;
+
+  // fronts
+  std::vector<int64_t> front_off;  // doubles
+  int64_t ws_size = 0;             // doubles
+
+  // blocks
+  int64_t nb = 0;
+  std::vector<int32_t> sn_blk0;    // ns+1
+  std::vector<int32_t> blk_col0, blk_w, blk_sn, blk_noff;
+  std::vector<int64_t> blk_rows;   // offset into sn_rows of the first off-diag row
+  std::vector<int64_t> blk_inv, blk_off; // factor-storage offsets (doubles)
+  int64_t fs_size = 0;
+  std::vector<int32_t> col2blk;    // N
+
+  // trsv tiles + task queues
+  std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;
+  std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect, bwd_expect;
+
+  // multifrontal plan
+  std::vector<int64_t> asm_dst;    // destination in workspace for each lower entry (+diag)
+  std::vector<double> asm_val;     // F: values; P_H: T-values filled on device
+  std::vector<int64_t> asm_src;    // P_H: index into device T values (-1 = none)
+  std::vector<int64_t> diag_dst;   // P_H: workspace position of each diagonal (factor order)
+  std::vector<int32_t> relind;     // per child: positions in parent of rows [w, m)
+  std::vector<int64_t> relind_off; // ns
+  std::vector<int32_t> grp_P, grp_pc; // extend-add groups (parent sn, parent-local col)
+  std::vector<int64_t> grp_ptr;       // n_grp+1 into grp_K/grp_j
+  std::vector<int32_t> grp_K, grp_j;
+  std::vector<LevelEA> level_ea;      // per level
+  std::vector<StepDesc> steps;
+  std::vector<int32_t> act;           // concatenated active-front lists
+  std::vector<int64_t> pan_pref, upd_pref; // per step: (n_act+1) prefix, concatenated at act_off + step_index
+  std::vector<int64_t> pref_off;      // per step offset into pan_pref/upd_pref
+  std::vector<signed char> pivsign;   // expected pivot sign per column (factor order)
+};
+
+// Build the permuted lower pattern of F = [−H Aᵀ; A 0] (x block by pinv, λ last).
+LowerMatrix build_F_lower(int64_t n, int64_t m1, const int64_t* Hp, const int32_t* Hi, const double* Hx,
+                          const int64_t* Ap, const int32_t* Ai, const double* Ax,
+                          const std::vector<int64_t>& xperm);
+
+// Symmetric pattern (full, both triangles, no diagonal) → approximate minimum
+// degree order (new→old).
+std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr,
+                                      const std::vector<int32_t>& idx);
+
+// Full symbolic analysis + multifrontal / trsv plans.  Returns "" or an error.
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative);
+
+}  // namespace qpb

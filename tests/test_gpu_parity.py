@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): PCG solutions 1e-8 relative 2-norm,
+IPM objective 1e-8 relative, PCG counts ±2 per IPM iteration, structures
+bit-exact.  F-solves / K_F products: 1e-12·cond-scaled relative (fp64
+rounding of two different but exact factorizations).
+"""
+import numpy as np
+import pytest
+
+import qpgen
+from oracle import kkt, symbolic
+from oracle.fsolve import DenseF, SparseF, make_fsolver
+from oracle.ipm import ipm_solve as oracle_ipm
+from oracle.pcg import pcg as oracle_pcg
+
+pytestmark = pytest.mark.gpu
+
+
+def solver(qp, precond="low", **kw):
+    from paper_2104_12916_b200.binding import from_qp
+    s = from_qp(qp, **kw)
+    s.ipm_factor_once(precond)
+    return s
+
+
+def fsolver_for(qp, perm):
+    return SparseF(qp.H, qp.A, perm) if qp.n + qp.m1 > 3000 else DenseF(qp.H, qp.A)
+
+
+CASES = {
+    "tiny": lambda: qpgen.scaled_random_qp(9, 4, 12, seed=1, g_nnz=3, a_nnz=3, c_nnz=3),
+    "m1_zero": lambda: qpgen.scaled_random_qp(30, 0, 40, seed=2, g_nnz=3, a_nnz=3, c_nnz=3),
+    "m1_eq_n": lambda: qpgen.make_syqp(24, 24),
+    "c0": lambda: qpgen.make("c0"),
+    "ragged": lambda: qpgen.scaled_random_qp(700, 130, 900, seed=3),       # several 64-tiles + tail
+    "grid": lambda: qpgen.make_grid_qp(24, 40, 60, seed=4, name="grid24"),  # supernodal, ND perm
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request):
+    qp = CASES[request.param]()
+    s = solver(qp)
+    return request.param, qp, s
+
+
+def test_structures_bit_exact(case):
+    name, qp, s = case
+    perm = s.structure("perm")[:qp.n]
+    ref = symbolic.analyse(qp.H, qp.A, perm)
+    for key in ("parent", "colcount", "sn_start", "sn_parent", "sn_level", "sn_rowptr", "sn_rows", "row_level"):
+        got = s.structure(key)
+        assert symbolic.struct_hash(got) == symbolic.struct_hash(ref[key]), key
+    assert s.stats()["nnz_LF"] == ref["nnz_L"]
+
+
+def test_f_solve(case):
+    name, qp, s = case
+    perm = s.structure("perm")[:qp.n]
+    fs = fsolver_for(qp, perm)
+    rng = np.random.default_rng(5)
+    r1, r2 = rng.standard_normal(qp.n), rng.standard_normal(qp.m1)
+    y, z = s.f_solve(np.concatenate([r1, r2]))
+    yr, zr = fs.solve(r1, r2)
+    ref = np.concatenate([yr, zr])
+    got = np.concatenate([y, z])
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_kf_apply(case):
+    name, qp, s = case
+    perm = s.structure("perm")[:qp.n]
+    fs = fsolver_for(qp, perm)
+    rng = np.random.default_rng(6)
+    D = rng.uniform(0.1, 3.0, qp.m2)
+    p = rng.standard_normal(qp.m2)
+    q = s.kf_apply(D, p)
+    qr = kkt.KF_apply(qp, fs, D, p)
+    assert np.linalg.norm(q - qr) <= 1e-9 * np.linalg.norm(qr)
+
+
+@pytest.mark.parametrize("tol", [1e-12, 1e-3])
+def test_pcg_solve(case, tol):
+    name, qp, s = case
+    perm = s.structure("perm")[:qp.n]
+    fs = fsolver_for(qp, perm)
+    rng = np.random.default_rng(7)
+    D = rng.uniform(0.1, 3.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    x, it, rr, rc = s.pcg_solve(D, b, tol=tol, maxit=4000)
+    xr, itr, rrr, ok, _ = oracle_pcg(lambda v: kkt.KF_apply(qp, fs, D, v), b, kkt.PrecondL(D), tol, 4000)
+    assert abs(it - itr) <= 2
+    # the GPU solution meets the stopping test against the ORACLE operator
+    Kx = kkt.KF_apply(qp, fs, D, x)
+    op_gap = np.linalg.norm(s.kf_apply(D, x) - Kx)   # rounding gap between the two exact operators
+    res = b - Kx
+    assert np.linalg.norm(res) <= 1.01 * tol * np.linalg.norm(b) + 2 * op_gap + 1e-13 * np.linalg.norm(b)
+    if tol <= 1e-10:   # reading c5#16: iterate parity is meaningful at tight tolerance
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def test_pcg_fixed_iterations_match(case):
+    """Same (D, rhs), same number of iterations ⇒ iterates agree to 1e-8 (reading c5#16)."""
+    name, qp, s = case
+    perm = s.structure("perm")[:qp.n]
+    fs = fsolver_for(qp, perm)
+    rng = np.random.default_rng(8)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    for k in (1, 3):
+        x, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=k)
+        xr, itr, *_ = oracle_pcg(lambda v: kkt.KF_apply(qp, fs, D, v), b, kkt.PrecondL(D), 0.0, k)
+        assert it == k == itr
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def test_ipm_objective_matches_oracle(case):
+    name, qp, s = case
+    if name in ("ragged", "grid"):
+        pytest.skip("PL-IPM oracle too slow at this size (thousands of dense PCG steps); see PH tests")
+    perm = s.structure("perm")[:qp.n]
+    ref = oracle_ipm(qp, precond="low", ipm_tol=1e-10, fs=fsolver_for(qp, perm))
+    got = s.ipm_solve(ipm_tol=1e-10)
+    assert got["converged"] and ref.converged
+    assert abs(got["objective"] - ref.objective) <= 1e-8 * max(1.0, abs(ref.objective))
+    # KKT at the GPU solution, checked on the host
+    x, lam, nu, sl = got["x"], got["lam"], got["nu"], got["s"]
+    grad = qp.H @ x + qp.g - qp.A.T @ lam - qp.C.T @ nu
+    assert np.abs(grad).max() <= 1e-9 * (1 + np.abs(qp.g).max())
+    assert np.abs(qp.C @ x - sl - qp.d).max() <= 1e-9 * (1 + np.abs(qp.d).max())
+    assert sl.min() > 0 and nu.min() > 0
+    # per-IPM-iteration PCG counts within ±2 while the trajectories coincide
+    n_cmp = min(len(ref.pcg_iters), len(got["pcg_iters"]), 6)
+    for a, b in zip(ref.pcg_iters[:n_cmp], got["pcg_iters"][:n_cmp]):
+        assert abs(a - b) <= 2
