@@ -149,6 +149,12 @@ int qp_ipm_iterate(qp_ctx* ctx, int32_t nsteps, qp_ipm_result* r, int32_t* done)
 int qp_f_solve(qp_ctx* ctx, const double* rhs, double* out);
 int qp_kf_apply(qp_ctx* ctx, const double* D, const double* p, double* q);
 
+/* Host-only symbolic analysis (no GPU needed): ordering of the x block
+ * (x_perm or minimum degree), λ last, elimination tree, column counts,
+ * supernodes, levels of the LDLᵀ factor of F.  The returned context
+ * supports qp_get_structure / qp_get_stats / qp_free only. */
+int qp_analyse(qp_ctx** ctx, const qp_csr* H, const qp_csr* A, const int64_t* x_perm);
+
 /* Structure export for bit-exact parity.  which:
  *  0 perm (new→old, N = n+m1)  1 etree parent  2 column counts
  *  3 supernode starts (ns+1)   4 supernode parent  5 supernode level
@@ -162,6 +168,7 @@ typedef struct {
   int64_t nnz_LF, n_supernodes_F, n_blocks_F, n_levels_F, row_levels_F;
   int64_t nnz_LPH, n_supernodes_PH;
   int64_t workspace_bytes, factor_bytes;
+  int64_t nnz_LF_stored;             /* entries stored by the relaxed supernodes (explicit zeros incl.) */
   double c_fact_F, c_fact_PH;        /* paper model flops Σ nz(L[:,j])² */
   double t_symbolic_s, t_factor_s, t_factor_ph_s;
   double pcg_bytes_per_iter;         /* algorithmic bytes B_it */
@@ -178,6 +185,11 @@ int qp_get_stats(qp_ctx* ctx, qp_stats* s);
  *  7 other. */
 int qp_profile(qp_ctx* ctx, int32_t enable);
 int qp_profile_read(qp_ctx* ctx, double* ms /*8*/, int64_t* count /*8*/);
+
+/* Debug instrumentation of the L_F sweeps: enable = 1 resets and enables;
+ * enable = 0 disables and copies 50 int64 = [fwd, bwd] × [DIAG, TILE, PREP,
+ * XCHUNK, SNF] × [count, wait ns, busy ns, first start ns, last end ns] into out. */
+int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
 
 const char* qp_last_error(const qp_ctx* ctx);
 void qp_free(qp_ctx* ctx);

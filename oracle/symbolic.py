@@ -10,8 +10,15 @@ same x-block permutation:
   elimination: struct(L[:,j]) = {j} ∪ {i>j : F_ij ≠ 0}
   ∪ ⋃_{c : parent(c)=j} struct(L[:,c]) \\ {c},   parent(j) = min(struct(j) \\ {j});
 * column counts cc(j) = |struct(L[:,j])| (diagonal included);
-* supernodes: column j joins j−1's supernode iff parent(j−1) = j and
-  cc(j−1) = cc(j) + 1 (then struct(j−1) = {j−1} ∪ struct(j));
+* fundamental supernodes: column j joins j−1's supernode iff
+  parent(j−1) = j and cc(j−1) = cc(j) + 1 (then struct(j−1) = {j−1} ∪ struct(j));
+* relaxed amalgamation, in increasing supernode
+  order: merge J into its parent P when J's columns end right before P's and
+  the merged block's explicit zeros are small — merged width w ≤ 4, or
+  w ≤ 16 and zeros ≤ 80 %, or w ≤ 48 and zeros ≤ 10 %, or zeros ≤ 5 % of
+  the stored w·m − w(w−1)/2 entries (m = w_J + m_P rows);  a relaxed
+  supernode's rows are its columns followed by the rows below its topmost
+  fundamental supernode;
 * supernodal tree: parent of supernode J = supernode of parent(last col of J);
   level(J) = 0 for leaves, else 1 + max level(children);
 * row levels: lev(i) = 1 + max{lev(j) : j < i, L_ij ≠ 0}, 0 for rows with no
@@ -64,7 +71,7 @@ def symbolic_factor(N, lower_cols):
 
 
 def supernodes(parent, cc):
-    """Supernode start columns (with a final sentinel N)."""
+    """Fundamental supernode start columns (with a final sentinel N)."""
     N = len(parent)
     starts = [0]
     for j in range(1, N):
@@ -72,6 +79,43 @@ def supernodes(parent, cc):
             starts.append(j)
     starts.append(N)
     return np.asarray(starts, dtype=np.int64)
+
+
+def _col2sn(starts, N):
+    col2sn = np.empty(N, dtype=np.int64)
+    for J in range(len(starts) - 1):
+        col2sn[starts[J]:starts[J + 1]] = J
+    return col2sn
+
+
+def relax(parent, cc, struct, fstart):
+    """Relaxed amalgamation of the fundamental supernodes; returns (starts, rows-per-supernode)."""
+    N = len(parent)
+    nf = len(fstart) - 1
+    col2f = _col2sn(fstart, N)
+    fpar = [int(col2f[parent[fstart[J + 1] - 1]]) if parent[fstart[J + 1] - 1] >= 0 else -1 for J in range(nf)]
+    below = [struct[fstart[J]][fstart[J + 1] - fstart[J]:] for J in range(nf)]
+    c0 = [int(fstart[J]) for J in range(nf)]
+    w = [int(fstart[J + 1] - fstart[J]) for J in range(nf)]
+    m = [w[J] + len(below[J]) for J in range(nf)]
+    true = [int(cc[fstart[J]:fstart[J + 1]].sum()) for J in range(nf)]
+    alive = [True] * nf
+    for J in range(nf):
+        P = fpar[J]
+        if P < 0 or c0[J] + w[J] != c0[P]:
+            continue
+        ww = w[J] + w[P]
+        mm = w[J] + m[P]
+        stored = ww * mm - ww * (ww - 1) // 2
+        zeros = stored - (true[J] + true[P])
+        if ww <= 4 or (ww <= 16 and 100 * zeros <= 80 * stored) or (ww <= 48 and 100 * zeros <= 10 * stored) \
+                or 100 * zeros <= 5 * stored:
+            c0[P], w[P], m[P], true[P] = c0[J], ww, mm, true[P] + true[J]
+            alive[J] = False
+    starts = [c0[J] for J in range(nf) if alive[J]] + [N]
+    rows = [np.concatenate([np.arange(c0[J], c0[J] + w[J]), below[J]]).astype(np.int64)
+            for J in range(nf) if alive[J]]
+    return np.asarray(starts, dtype=np.int64), rows
 
 
 def supernode_tree(parent, sn_start):
@@ -106,12 +150,17 @@ def analyse(H, A, x_perm=None):
     N, lower = permuted_lower_pattern(H, A, x_perm)
     parent, struct = symbolic_factor(N, lower)
     cc = np.array([len(s) for s in struct], dtype=np.int64)
-    sn = supernodes(parent, cc)
+    fsn = supernodes(parent, cc)
+    sn, rows = relax(parent, cc, struct, fsn)
     sparent, slevel = supernode_tree(parent, sn)
-    sn_rows = np.concatenate([struct[sn[J]] for J in range(len(sn) - 1)]) if N else np.zeros(0, np.int64)
-    sn_rowptr = np.concatenate([[0], np.cumsum([cc[sn[J]] for J in range(len(sn) - 1)])]).astype(np.int64)
+    sn_rows = np.concatenate(rows) if N else np.zeros(0, np.int64)
+    sn_rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
     rlev = row_levels(N, struct)
-    return dict(N=N, parent=parent, colcount=cc, sn_start=sn, sn_parent=sparent,
+    w = np.diff(sn)
+    m = np.diff(sn_rowptr)
+    nnz_stored = int(np.sum(w * m - w * (w - 1) // 2))
+    return dict(N=N, parent=parent, colcount=cc, sn_start=sn, fsn_start=fsn, nnz_stored=nnz_stored,
+                sn_parent=sparent,
                 sn_level=slevel, sn_rowptr=sn_rowptr, sn_rows=sn_rows, row_level=rlev,
                 nnz_L=int(cc.sum()), struct=struct)
 

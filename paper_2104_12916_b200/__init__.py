@@ -6,8 +6,8 @@ thin ctypes binding with the same names (argument marshalling only); there
 is no CPU fallback — on a machine without the built library or without a
 Blackwell GPU every compute call raises.
 """
-from .binding import (QPSolver, QPError, load_library, PREC, STRUCTURES,  # noqa: F401
+from .binding import (Analysis, QPSolver, QPError, load_library, PREC, STRUCTURES,  # noqa: F401
                       exported_symbols, header_functions)
 
-__all__ = ["QPSolver", "QPError", "load_library", "PREC", "STRUCTURES", "exported_symbols",
+__all__ = ["Analysis", "QPSolver", "QPError", "load_library", "PREC", "STRUCTURES", "exported_symbols",
            "header_functions"]

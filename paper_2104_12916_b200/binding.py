@@ -61,7 +61,8 @@ class _IpmResult(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("n", "m1", "m2", "nnz_H", "nnz_A", "nnz_C", "nnz_LF",
                                          "n_supernodes_F", "n_blocks_F", "n_levels_F", "row_levels_F",
-                                         "nnz_LPH", "n_supernodes_PH", "workspace_bytes", "factor_bytes")] + \
+                                         "nnz_LPH", "n_supernodes_PH", "workspace_bytes", "factor_bytes",
+                                         "nnz_LF_stored")] + \
                [(k, C.c_double) for k in ("c_fact_F", "c_fact_PH", "t_symbolic_s", "t_factor_s",
                                           "t_factor_ph_s", "pcg_bytes_per_iter", "pcg_flops_per_iter",
                                           "sweep_bytes_F")]
@@ -96,10 +97,12 @@ def load_library(build: bool = True):
     lib.qp_ipm_iterate.argtypes = [vp, i32, C.POINTER(_IpmResult), C.POINTER(i32)]
     lib.qp_f_solve.argtypes = [vp, vp, vp]
     lib.qp_kf_apply.argtypes = [vp, vp, vp, vp]
+    lib.qp_analyse.argtypes = [C.POINTER(vp), C.POINTER(_CSR), C.POINTER(_CSR), vp]
     lib.qp_get_structure.argtypes = [vp, i32, vp, C.POINTER(i64)]
     lib.qp_get_stats.argtypes = [vp, C.POINTER(_Stats)]
     lib.qp_profile.argtypes = [vp, i32]
     lib.qp_profile_read.argtypes = [vp, vp, vp]
+    lib.qp_debug_sweep_profile.argtypes = [vp, i32, vp]
     lib.qp_last_error.argtypes = [vp]
     lib.qp_last_error.restype = C.c_char_p
     lib.qp_free.argtypes = [vp]
@@ -268,6 +271,11 @@ class QPSolver:
         self._check(self.lib.qp_get_structure(self.ctx, which, buf.ctypes.data, C.byref(n)))
         return buf
 
+    def debug_sweep_profile(self, enable):
+        out = np.zeros(50, dtype=np.int64)
+        self._check(self.lib.qp_debug_sweep_profile(self.ctx, 1 if enable else 0, out.ctypes.data))
+        return out.reshape(2, 5, 5)
+
     def stats(self):
         s = _Stats()
         self._check(self.lib.qp_get_stats(self.ctx, C.byref(s)))
@@ -282,6 +290,34 @@ class QPSolver:
         self._check(self.lib.qp_profile_read(self.ctx, ms.ctypes.data, cnt.ctypes.data))
         names = ["f_fwd", "f_bwd", "kf_q", "pcg_vec", "ph_sweeps", "ph_refactor", "ipm_rhs", "other"]
         return {nm: (float(m), int(c)) for nm, m, c in zip(names, ms, cnt)}
+
+
+class Analysis(QPSolver):
+    """Host-only symbolic analysis context (``qp_analyse``): structures and stats, no GPU."""
+
+    def __init__(self, H, A, x_perm=None):
+        import scipy.sparse as sp
+        self.lib = load_library()
+        self.vectors_on_device = False
+        keep = []
+
+        def csr(M):
+            M = sp.csr_matrix(M)
+            ip = np.ascontiguousarray(M.indptr, dtype=np.int64)
+            ix = np.ascontiguousarray(M.indices, dtype=np.int32)
+            vv = np.ascontiguousarray(M.data, dtype=np.float64)
+            keep.extend([ip, ix, vv])
+            return _CSR(M.shape[0], M.shape[1], ip.ctypes.data, ix.ctypes.data, vv.ctypes.data)
+
+        self.n, self.m1, self.m2 = H.shape[0], A.shape[0], 0
+        cH, cA = csr(H), csr(A)
+        xp = None
+        if x_perm is not None:
+            xp = np.ascontiguousarray(x_perm, dtype=np.int64)
+        self.ctx = C.c_void_p()
+        rc = self.lib.qp_analyse(C.byref(self.ctx), C.byref(cH), C.byref(cA),
+                                 xp.ctypes.data if xp is not None else None)
+        self._check(rc)
 
 
 def from_qp(qp, **kw):

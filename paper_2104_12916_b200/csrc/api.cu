@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -116,6 +117,19 @@ struct Factor {
   DeviceArena mem;
   bool ready = false;
   int64_t fs_bytes = 0, ws_bytes = 0;
+  // partitioned inverse of big supernodes
+  double* xtmp = nullptr;
+  int32_t* big = nullptr;
+  std::vector<int32_t> big_host;
+  int n_big = 0;
+  int64_t max_w2 = 0;
+  std::vector<std::vector<GemmProb>> inv_plan;   // per height: [T1 problems..., X21 problems...]
+  std::vector<int> inv_split;                    // per height: number of T1 problems
+  GemmProb* inv_dev = nullptr;
+  int64_t* inv_pref_dev = nullptr;
+  std::vector<int64_t> inv_off;                  // per (height, phase) offsets into inv_dev / inv_pref_dev
+  std::vector<int64_t> inv_total;
+  unsigned long long* tprof_buf = nullptr;
 };
 
 DevCSR upload_csr(DeviceArena& mem, const HostCSR& A, cudaStream_t s) {
@@ -143,7 +157,7 @@ struct qp_ctx {
   HostCSR H, A, C;
   std::vector<double> g, b, d;
   std::vector<int64_t> xperm_user;
-  bool setup_done = false, factored = false;
+  bool setup_done = false, factored = false, analysed = false;
   int precond = 1;
   int sm_count = 148;
   int vgrid = 148 * 4;     // grid for vector kernels (fixed ⇒ deterministic reductions)
@@ -330,11 +344,49 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.pivsign = m.upload(S.pivsign, st);
     d.acc = m.zeros<double>(S.N, st);
     d.tacc = m.zeros<double>(S.N, st);
-    d.cnt_f = m.zeros<unsigned long long>(S.nb, st);
+    d.cnt_f = m.zeros<unsigned long long>(S.ns, st);
     d.cnt_b = m.zeros<unsigned long long>(S.nb, st);
     d.ready_f = m.zeros<unsigned int>(S.nb, st);
     d.ready_b = m.zeros<unsigned int>(S.nb, st);
     d.sweep = m.zeros<unsigned int>(4, st);
+    d.blk_sn = m.upload(S.blk_sn, st);
+    d.sn_xinv = m.upload(S.sn_xinv, st);
+    d.xt_bI = m.upload(S.xt_bI, st);
+    d.xt_bK = m.upload(S.xt_bK, st);
+    d.xt_nK = m.upload(S.xt_nK, st);
+    d.xb_bK = m.upload(S.xb_bK, st);
+    d.xb_bI = m.upload(S.xb_bI, st);
+    d.xb_nI = m.upload(S.xb_nI, st);
+    d.sn_xtr = m.upload(S.sn_xtr, st);
+    d.sn_ldx = m.upload(S.sn_ldx, st);
+    d.sn_nblk = m.upload(S.sn_nblk, st);
+    d.blk_dptr = m.upload(S.blk_dptr, st);
+    d.blk_dest = m.upload(S.blk_dest, st);
+    d.ready_sb = m.zeros<unsigned int>(S.ns, st);
+    d.sn_done_b = m.zeros<unsigned long long>(S.ns, st);
+    d.xexp_f = m.upload(S.xexp_f, st);
+    d.xexp_b = m.upload(S.xexp_b, st);
+    d.xinv = m.alloc<double>(S.x_size);
+    d.vbuf = m.zeros<double>(S.N, st);
+    d.cntx_f = m.zeros<unsigned long long>(S.nb, st);
+    d.cntx_b = m.zeros<unsigned long long>(S.nb, st);
+    d.vready_f = m.zeros<unsigned int>(S.nb, st);
+    d.vready_b = m.zeros<unsigned int>(S.nb, st);
+    F.xtmp = m.alloc<double>(S.xtmp_size);
+    {
+      std::vector<int32_t> big;
+      int64_t mw2 = 0;
+      for (int64_t J = 0; J < S.ns; ++J)
+        if (S.sn_xinv[J] >= 0) {
+          big.push_back((int32_t)J);
+          int64_t w = S.sn_start[J + 1] - S.sn_start[J];
+          mw2 = std::max(mw2, w * S.sn_ldx[J]);
+        }
+      F.n_big = (int)big.size();
+      F.max_w2 = mw2;
+      F.big = m.upload(big, st);
+      F.big_host = big;
+    }
     d.asm_dst = m.upload(S.asm_dst, st);
     d.asm_val = m.upload(S.asm_val, st);
     d.asm_src = m.upload(S.asm_src, st);
@@ -351,12 +403,83 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.pan_pref = m.upload(S.pan_pref, st);
     d.upd_pref = m.upload(S.upd_pref, st);
     d.status = m.zeros<int>(1, st);
+    d.tprof = nullptr;
+    F.tprof_buf = m.alloc<unsigned long long>(50);
     F.fs_bytes = S.fs_size * 8;
     F.ws_bytes = S.ws_size * 8;
   } catch (std::bad_alloc&) {
     return "cudaMalloc failed (factor storage)";
   }
   return "";
+}
+
+// Plan of the recursive blocked inversion X_J = L_JJ⁻¹ for every big supernode:
+// split the tile range [lo, hi) at mid; X21 = −X22 · (L21 · X11), bottom-up by height.
+void plan_inverse(qp_ctx* c, Factor& F) {
+  const Symbolic& S = F.S;
+  F.inv_plan.clear();
+  F.inv_split.clear();
+  std::vector<std::vector<GemmProb>> t1, x21;
+  for (int32_t J : F.big_host) {
+    const int64_t w = S.sn_start[J + 1] - S.sn_start[J];
+    const int64_t T = S.sn_blk0[J + 1] - S.sn_blk0[J];
+    const int64_t ldx = S.sn_ldx[J];
+    double* X = F.d.xinv + S.sn_xinv[J];
+    double* tmp = F.xtmp + S.sn_xtmp[J];
+    std::vector<int64_t> tmp_used(64, 0);
+    auto tb = [&](int64_t t) { return std::min<int64_t>(t * BW, w); };
+    std::function<int(int64_t, int64_t)> gen = [&](int64_t lo, int64_t hi) -> int {
+      if (hi - lo <= 1) return 0;
+      const int64_t mid = lo + (hi - lo) / 2;
+      const int h = 1 + std::max(gen(lo, mid), gen(mid, hi));
+      if ((int)t1.size() < h) { t1.resize(h); x21.resize(h); }
+      if ((int)tmp_used.size() <= h) tmp_used.resize(h + 1, 0);
+      const int64_t a = tb(lo), m = tb(mid), e = tb(hi);
+      const int M2 = (int)(e - m), M1 = (int)(m - a);
+      double* T1 = tmp + tmp_used[h];
+      tmp_used[h] += (int64_t)M2 * M1;
+      GemmProb p1{X + m + a * ldx, X + a + a * ldx, T1, M2, M1, M1, (int)ldx, (int)ldx, M2, 1.0, 0.0, 2, 0};
+      GemmProb p2{X + m + m * ldx, T1, X + m + a * ldx, M2, M1, M2, (int)ldx, M2, (int)ldx, -1.0, 0.0, 1, 0};
+      t1[h - 1].push_back(p1);
+      x21[h - 1].push_back(p2);
+      return h;
+    };
+    gen(0, T);
+  }
+  std::vector<GemmProb> all;
+  std::vector<int64_t> pref;
+  F.inv_off.clear();
+  F.inv_total.clear();
+  for (size_t h = 0; h < t1.size(); ++h)
+    for (int phase = 0; phase < 2; ++phase) {
+      const auto& v = phase == 0 ? t1[h] : x21[h];
+      F.inv_off.push_back((int64_t)all.size());
+      int64_t acc = 0;
+      for (const GemmProb& p : v) {
+        pref.push_back(acc);
+        acc += (int64_t)((p.M + 63) / 64) * ((p.N + 63) / 64);
+        all.push_back(p);
+      }
+      pref.push_back(acc);
+      all.push_back(GemmProb{});  // keeps all[] aligned with pref[] (one sentinel per group)
+      F.inv_total.push_back(acc);
+    }
+  F.inv_dev = F.mem.upload(all, c->stream);
+  F.inv_pref_dev = F.mem.upload(pref, c->stream);
+  F.inv_split.assign(t1.size(), 0);
+  for (size_t h = 0; h < t1.size(); ++h) F.inv_split[h] = (int)t1[h].size();
+}
+
+void run_inverse(qp_ctx* c, Factor& F) {
+  if (F.n_big == 0) return;
+  build_xinv(F.d, F.big, F.n_big, F.max_w2, c->stream);
+  for (size_t h = 0; h < F.inv_split.size(); ++h)
+    for (int phase = 0; phase < 2; ++phase) {
+      const size_t g = 2 * h + phase;
+      const int64_t off = F.inv_off[g];
+      gemm_batched(F.inv_dev + off, F.inv_pref_dev + off, F.inv_split[h], F.inv_total[g], c->stream);
+    }
+  transpose_xinv(F.d, F.big, F.n_big, F.max_w2, c->stream);
 }
 
 // Numeric multifrontal factorization (assembly → per level: extend-add, blocked steps).
@@ -377,6 +500,7 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
       ++si;
     }
   }
+  run_inverse(c, F);   // partitioned inverse of the big supernodes' diagonal blocks
   int rc = cuda_check(c, what);
   if (rc) return rc;
   int status = 0;
@@ -490,6 +614,31 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   return c->h_pst->status == 1 ? QP_MAXIT : QP_OK;
 }
 
+// Ordering (x block by x_perm or minimum degree on the graph of H, λ last) + symbolic analysis of F.
+std::string analyse_F(qp_ctx* c) {
+  const int64_t n = c->n, m1 = c->m1;
+  double t0 = now_s();
+  if (!c->xperm_user.empty()) {
+    c->perm = c->xperm_user;
+  } else {
+    std::vector<int64_t> ptr(n + 1, 0);
+    std::vector<int32_t> idx;
+    idx.reserve(c->H.nnz());
+    for (int64_t r = 0; r < n; ++r) {
+      for (int64_t q = c->H.p[r]; q < c->H.p[r + 1]; ++q)
+        if (c->H.i[q] != r) idx.push_back(c->H.i[q]);
+      ptr[r + 1] = (int64_t)idx.size();
+    }
+    c->perm = min_degree_order(n, ptr, idx);
+  }
+  LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(), c->A.i.data(),
+                                c->A.v.data(), c->perm);
+  std::string e = analyse(M, c->FF.S, n);
+  c->t_symbolic = now_s() - t0;
+  if (e.empty()) c->analysed = true;
+  return e;
+}
+
 int require(qp_ctx* c, bool factored) {
   if (!c) return QP_EINVAL;
   if (!c->setup_done) return fail(c, QP_ESTATE, "qp_setup has not completed");
@@ -587,6 +736,21 @@ void fill_result(qp_ctx* c, qp_ipm_result* r) {
 
 // ============================================================================ C ABI
 extern "C" {
+
+int qp_analyse(qp_ctx** out, const qp_csr* H, const qp_csr* A, const int64_t* x_perm) {
+  if (!out || !H || !A) return QP_EINVAL;
+  std::unique_ptr<qp_ctx> c(new qp_ctx());
+  const int64_t n = H->nrows, m1 = A->nrows;
+  std::string e = n > 0 && m1 >= 0 && m1 <= n ? "" : "need n >= 1 and 0 <= m1 <= n";
+  if (e.empty()) e = check_csr(H, n, n, "H", c->H);
+  if (e.empty()) e = check_csr(A, m1, n, "A", c->A);
+  c->n = n;
+  c->m1 = m1;
+  if (e.empty() && x_perm) c->xperm_user.assign(x_perm, x_perm + n);
+  if (e.empty()) e = analyse_F(c.get());
+  *out = c.release();
+  return e.empty() ? QP_OK : fail(*out, QP_EINVAL, e);
+}
 
 int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, const double* g, const double* b,
              const double* d, const qp_setup_opts* opts) {
@@ -693,29 +857,13 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
   cudaStream_t st = c->stream;
   const int64_t n = c->n, m1 = c->m1, m2 = c->m2, N = n + m1;
   double t0 = now_s();
-  // ---- ordering of the x block (user or minimum degree on the graph of H), λ last
-  if (!c->xperm_user.empty()) {
-    c->perm = c->xperm_user;
-  } else {
-    std::vector<int64_t> ptr(n + 1, 0);
-    std::vector<int32_t> idx;
-    idx.reserve(c->H.nnz());
-    for (int64_t r = 0; r < n; ++r) {
-      for (int64_t q = c->H.p[r]; q < c->H.p[r + 1]; ++q)
-        if (c->H.i[q] != r) idx.push_back(c->H.i[q]);
-      ptr[r + 1] = (int64_t)idx.size();
-    }
-    c->perm = min_degree_order(n, ptr, idx);
-  }
+  std::string e = analyse_F(c);
+  if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of F: " + e);
   std::vector<int64_t> pinv(n);
   for (int64_t i = 0; i < n; ++i) pinv[c->perm[i]] = i;
-  LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(), c->A.i.data(),
-                                c->A.v.data(), c->perm);
-  std::string e = analyse(M, c->FF.S, n);
-  if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of F: " + e);
-  c->t_symbolic = now_s() - t0;
   e = upload_factor(c, c->FF, c->ws_limit);
   if (!e.empty()) return fail(c, QP_ENOMEM, e);
+  plan_inverse(c, c->FF);
   // ---- permuted operators (factor order for the x block)
   try {
     HostCSR Hf = permute(c->H, &c->perm, &pinv);
@@ -848,6 +996,7 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of P_H: " + e);
     e = upload_factor(c, c->FP, c->ws_limit);
     if (!e.empty()) return fail(c, QP_ENOMEM, e);
+    plan_inverse(c, c->FP);
     try {
       c->t_row = c->mem.upload(trow, st);
       c->t_col = c->mem.upload(ti, st);
@@ -999,8 +1148,8 @@ int qp_kf_apply(qp_ctx* c, const double* D, const double* p, double* q) {
 }
 
 int qp_get_structure(qp_ctx* c, int32_t which, int64_t* out, int64_t* len) {
-  int rc = require(c, true);
-  if (rc) return rc;
+  if (!c) return QP_EINVAL;
+  if (!c->analysed) return fail(c, QP_ESTATE, "no symbolic analysis yet (qp_analyse or ipm_factor_once)");
   const Symbolic& S = which >= 10 ? c->FP.S : c->FF.S;
   if (which >= 10 && c->precond != 2) return fail(c, QP_ESTATE, "no P_H factor (precond != HIGH)");
   std::vector<int64_t> v;
@@ -1032,9 +1181,7 @@ int qp_get_structure(qp_ctx* c, int32_t which, int64_t* out, int64_t* len) {
 }
 
 int qp_get_stats(qp_ctx* c, qp_stats* s) {
-  int rc = require(c, false);
-  if (rc) return rc;
-  if (!s) return QP_EINVAL;
+  if (!c || !s) return QP_EINVAL;
   std::memset(s, 0, sizeof(*s));
   s->n = c->n;
   s->m1 = c->m1;
@@ -1042,16 +1189,19 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
   s->nnz_H = c->H.nnz();
   s->nnz_A = c->A.nnz();
   s->nnz_C = c->C.nnz();
-  if (c->factored) {
+  if (c->analysed) {
     const Symbolic& S = c->FF.S;
     s->nnz_LF = S.nnz_L;
+    s->nnz_LF_stored = S.nnz_stored;
+    s->workspace_bytes = S.ws_size * 8;
+    s->factor_bytes = S.fs_size * 8;
     s->n_supernodes_F = S.ns;
     s->n_blocks_F = S.nb;
     s->n_levels_F = S.n_levels;
     s->row_levels_F = S.n_rowlev;
     s->c_fact_F = S.c_fact;
-    s->workspace_bytes = c->FF.ws_bytes + c->FP.ws_bytes;
-    s->factor_bytes = c->FF.fs_bytes + c->FP.fs_bytes;
+    s->workspace_bytes = S.ws_size * 8 + c->FP.S.ws_size * 8;
+    s->factor_bytes = S.fs_size * 8 + c->FP.S.fs_size * 8;
     if (c->precond == 2) {
       s->nnz_LPH = c->FP.S.nnz_L;
       s->n_supernodes_PH = c->FP.S.ns;
@@ -1088,6 +1238,23 @@ int qp_profile_read(qp_ctx* c, double* ms, int64_t* count) {
     if (count) count[i] = c->prof_cnt[i];
   }
   return QP_OK;
+}
+
+// Debug: sweep instrumentation of the F factor. enable=1 resets and turns it on;
+// enable=0 copies [2 sweeps][4 task types][count, wait ns, busy ns, first, last] into out (40 int64).
+int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
+  if (!c || !c->factored) return QP_ESTATE;
+  Factor& F = c->FF;
+  if (enable) {
+    std::vector<unsigned long long> init(50, 0);
+    for (int i = 0; i < 10; ++i) init[i * 5 + 3] = ~0ull;
+    cudaMemcpyAsync(F.tprof_buf, init.data(), 50 * 8, cudaMemcpyHostToDevice, c->stream);
+    F.d.tprof = F.tprof_buf;
+  } else {
+    if (out) cudaMemcpyAsync(out, F.tprof_buf, 50 * 8, cudaMemcpyDeviceToHost, c->stream);
+    F.d.tprof = nullptr;
+  }
+  return sync_check(c, "qp_debug_sweep_profile");
 }
 
 const char* qp_last_error(const qp_ctx* c) { return c ? c->err.c_str() : "NULL context"; }

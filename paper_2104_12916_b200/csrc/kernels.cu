@@ -329,6 +329,7 @@ void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref
 }
 
 // ------------------------------------------------------------------------- triangular sweeps
+// Task types (symbolic.h): 0 DIAG(b), 1 TILE(t), 2 PREP(b), 3 XTILE(x); index in the low 29 bits.
 struct SweepShared {
   int task;
   unsigned epoch;
@@ -339,19 +340,131 @@ struct SweepShared {
 
 __device__ __forceinline__ void spin_u64(const unsigned long long* p, unsigned long long target) {
   if (ld_acq_u64(p) >= target) return;
-  unsigned ns = 32;
+  unsigned ns = 16;
   while (ld_acq_u64(p) < target) {
     __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+    if (ns < 128) ns <<= 1;
   }
 }
 __device__ __forceinline__ void spin_u32(const unsigned* p, unsigned target) {
   if (ld_acq_u32(p) == target) return;
-  unsigned ns = 32;
+  unsigned ns = 16;
   while (ld_acq_u32(p) != target) {
     __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+    if (ns < 128) ns <<= 1;
   }
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// instrumentation: per sweep (0 fwd, 1 bwd) and task type: count, wait ns, busy ns, first start, last end
+__device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int type, unsigned long long t0,
+                                          unsigned long long t1, unsigned long long t2) {
+  if (tp == nullptr || threadIdx.x != 0) return;
+  unsigned long long* q = tp + (sweep * 5 + type) * 5;
+  atomicAdd(q + 0, 1ull);
+  atomicAdd(q + 1, t1 - t0);
+  atomicAdd(q + 2, t2 - t1);
+  atomicMin(q + 3, t0);
+  atomicMax(q + 4, t2);
+}
+
+// Load a R×W column-major tile (leading dimension ld) into smem with padding R+1.
+__device__ __forceinline__ void load_tile(double* sm, const double* g, int R, int W, int64_t ld) {
+  const int ldp = R + 1;
+  for (int idx = threadIdx.x; idx < R * W; idx += NT) {
+    int c = idx / R, r = idx - c * R;
+    sm[c * ldp + r] = __ldg(g + r + (int64_t)c * ld);
+  }
+}
+// out[r] = Σ_c T(r,c) v[c]   (T in smem, R×W, ld R+1); result for r < R in S.red[r] (after sync)
+__device__ __forceinline__ void tile_gemv(const double* sm, int R, int W, const double* v, double* red) {
+  const int ldp = R + 1;
+  if (R <= 64) {
+    const int r = threadIdx.x & 63, g = threadIdx.x >> 6;
+    double s = 0.0;
+    if (r < R)
+      for (int c = g; c < W; c += 4) s += sm[c * ldp + r] * v[c];
+    red[g * 64 + r] = s;
+    __syncthreads();
+    if (threadIdx.x < R) red[threadIdx.x] = red[threadIdx.x] + red[64 + threadIdx.x] + red[128 + threadIdx.x] +
+                                            red[192 + threadIdx.x];
+  } else {
+    // caller handles R > 64 inline (rows per thread); not used with red
+  }
+  __syncthreads();
+}
+// out[c] = Σ_r T(r,c) v[r]   (transpose), result in red[c] for c < W (after sync)
+__device__ __forceinline__ void tile_gemv_t(const double* sm, int R, int W, const double* v, double* red) {
+  const int ldp = R + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int P = W >= 8 ? 1 : 8 / W;
+  __shared__ double part[64 * 8];
+  for (int it = wid; it < W * P; it += NT / 32) {
+    const int c = it / P, pr = it % P;
+    double s = 0.0;
+    for (int r = pr * 32 + lane; r < R; r += 32 * P) s += sm[c * ldp + r] * v[r];
+    s = warp_sum(s);
+    if (lane == 0) part[it] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < W) {
+    double s = 0.0;
+    for (int pr = 0; pr < P; ++pr) s += part[threadIdx.x * P + pr];
+    red[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Spin (by threads 0..n-1, one flag each) until every flag equals E; then barrier.
+__device__ __forceinline__ void wait_flags(const unsigned* flags, int n, unsigned E) {
+  if (threadIdx.x < n) spin_u32(flags + threadIdx.x, E);
+}
+
+// Streaming GEMV over a chunk of a big supernode's X_J (or X_Jᵀ): R ≤ 64 rows,
+// ncol columns, leading dimension ld (multiple of 8, zero padding rows):
+// red[512 + r] = Σ_c M(r, c)·v[c].  Lane l owns rows 2l, 2l+1 (128-bit loads);
+// the 8 warps split the columns; 8 columns of loads in flight per thread.
+__device__ __forceinline__ void xchunk_gemv(const double* __restrict__ M, int64_t ld, int R, int ncol,
+                                            const double* v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool ok = 2 * lane < R;
+  const double2* base = reinterpret_cast<const double2*>(M + 2 * lane);
+  const int64_t ld2 = ld >> 1;
+  double a0 = 0.0, a1 = 0.0;
+  int c = wid;
+  if (ok) {
+    for (; c + 56 < ncol; c += 64) {
+      double2 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = __ldg(base + (int64_t)(c + 8 * u) * ld2);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double vc = v[c + 8 * u];
+        a0 = fma(q[u].x, vc, a0);
+        a1 = fma(q[u].y, vc, a1);
+      }
+    }
+    for (; c < ncol; c += 8) {
+      const double2 q = __ldg(base + (int64_t)c * ld2);
+      const double vc = v[c];
+      a0 = fma(q.x, vc, a0);
+      a1 = fma(q.y, vc, a1);
+    }
+  }
+  red[wid * 64 + 2 * lane] = a0;
+  red[wid * 64 + 2 * lane + 1] = a1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k * 64 + threadIdx.x];
+    red[512 + threadIdx.x] = s;
+  }
+  __syncthreads();
 }
 
 // Forward sweep L y = b (unit lower L, factor order); y written to x.
@@ -366,33 +479,88 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
   while (true) {
     if (tid == 0) {
       unsigned t = atomicAdd(F.sweep + 0, 1u);
-      S.task = t < (unsigned)F.n_fwd_tasks ? F.fwd_tasks[t] : INT32_MIN;
+      S.task = t < (unsigned)F.n_fwd_tasks ? F.fwd_tasks[t] : -1;
     }
     __syncthreads();
     const int task = S.task;
     __syncthreads();
-    if (task == INT32_MIN) break;
-    if (task < 0) {
-      // ---------------- DIAG(b): y_b = L_bb⁻¹ (b_b − Σ updates)
-      const int b = -task - 1;
+    if (task < 0) break;
+    const int type = task >> 28, idx = task & ((1 << 28) - 1);
+    const unsigned long long t0 = F.tprof ? gtime() : 0ull;
+    unsigned long long t1 = t0;
+    if (type == 0 || type == 2) {
+      // ---------------- DIAG(b) / PREP(b): v = b_b − Σ updates into supernode J
+      const int b = idx;
+      const int J = F.blk_sn[b];
       const int wk = F.blk_w[b];
       const int64_t c0 = F.blk_col0[b];
-      const double* inv = F.fstore + F.blk_inv[b];
-      for (int idx = tid; idx < wk * wk; idx += NT) {
-        int c = idx / wk, r = idx % wk;
-        sm[c * 65 + r] = inv[idx];
+      if (type == 0) {
+        const double* inv = F.fstore + F.blk_inv[b];
+        for (int i2 = tid; i2 < wk * wk; i2 += NT) {
+          int c = i2 / wk, r = i2 - c * wk;
+          sm[c * 65 + r] = __ldg(inv + i2);
+        }
       }
       if (tid < wk) {
         const int64_t c = c0 + tid;
         double v;
-        if (R.ct.p != nullptr) {
-          v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
-        } else {
-          v = R.rhs[R.in_perm ? R.in_perm[c] : c];
-        }
+        if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+        else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
         S.rhs[tid] = v;
       }
-      if (tid == 0) spin_u64(F.cnt_f + b, (unsigned long long)E * (unsigned long long)F.fwd_expect[b]);
+      if (tid == 0) {
+        spin_u64(F.cnt_f + J, (unsigned long long)E * (unsigned long long)F.fwd_expect[J]);
+        if (F.tprof) t1 = gtime();
+      }
+      __syncthreads();
+      if (tid < wk) {
+        double* ap = F.acc + c0 + tid;
+        S.rhs[tid] -= __ldcg(ap);
+        *ap = 0.0;
+      }
+      __syncthreads();
+      if (type == 0) {
+        const int i = tid & 63, g = tid >> 6;
+        double s = 0.0;
+        if (i < wk)
+          for (int j = g; j <= i; j += 4) s += sm[j * 65 + i] * S.rhs[j];
+        S.red[g * 64 + i] = s;
+        __syncthreads();
+        if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_rel_u32(F.ready_f + b, E);
+      } else {
+        if (tid < wk) {
+          F.vbuf[c0 + tid] = S.rhs[tid];
+          x[c0 + tid] = 0.0;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_rel_u32(F.vready_f + b, E);
+      }
+    } else if (type == 4) {
+      // ---------------- SNF(b): small supernode in one task — y_b = L_bb⁻¹ v, then acc[rows] += L_rows·y_b
+      const int b = idx;
+      const int J = F.blk_sn[b];
+      const int wk = F.blk_w[b];
+      const int64_t c0 = F.blk_col0[b];
+      const double* inv = F.fstore + F.blk_inv[b];
+      for (int i2 = tid; i2 < wk * wk; i2 += NT) {
+        int c = i2 / wk, r = i2 - c * wk;
+        sm[c * 65 + r] = __ldg(inv + i2);
+      }
+      if (tid < wk) {
+        const int64_t c = c0 + tid;
+        double v;
+        if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+        else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+        S.rhs[tid] = v;
+      }
+      if (tid == 0) {
+        spin_u64(F.cnt_f + J, (unsigned long long)E * (unsigned long long)F.fwd_expect[J]);
+        if (F.tprof) t1 = gtime();
+      }
       __syncthreads();
       if (tid < wk) {
         double* ap = F.acc + c0 + tid;
@@ -408,42 +576,73 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         S.red[g * 64 + i] = s;
       }
       __syncthreads();
-      if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+      if (tid < wk) {
+        const double yv = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+        S.y[tid] = yv;
+        x[c0 + tid] = yv;
+      }
+      __syncthreads();
+      const int64_t noff = F.blk_noff[b];
+      const double* L = F.fstore + F.blk_off[b];
+      const int32_t* rows = F.sn_rows + F.blk_rows[b];
+      for (int64_t r = tid; r < noff; r += NT) {
+        double s = 0.0;
+        for (int c = 0; c < wk; ++c) s += __ldg(L + r + (int64_t)c * noff) * S.y[c];
+        atomicAdd(F.acc + rows[r], s);
+      }
       __threadfence();
       __syncthreads();
-      if (tid == 0) st_rel_u32(F.ready_f + b, E);
+      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) atomicAdd(F.cnt_f + F.blk_dest[k], 1ull);
+    } else if (type == 3) {
+      // ---------------- XCHUNK: x[I] += X_{I,K0..K0+nK} · v[K0..]
+      const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
+      const int J = F.blk_sn[bI];
+      const int64_t cJ = F.sn_start[J];
+      const int64_t rI = F.blk_col0[bI], cK = F.blk_col0[bK];
+      const int Rn = F.blk_w[bI];
+      const int ncol = (int)(F.blk_col0[bK + nK - 1] + F.blk_w[bK + nK - 1] - cK);
+      if (tid < nK) spin_u32(F.vready_f + bK + tid, E);
+      if (tid == 64) spin_u32(F.vready_f + bI, E);
+      if (F.tprof && tid == 0) t1 = gtime();
+      __syncthreads();
+      for (int c = tid; c < ncol; c += NT) sm[c] = __ldcg(F.vbuf + cK + c);
+      __syncthreads();
+      double* red = sm + 512;
+      const int64_t ldx = F.sn_ldx[J];
+      xchunk_gemv(F.xinv + F.sn_xinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, sm, red);
+      if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long old = atomicAdd(F.cntx_f + bI, 1ull);
+        if (old + 1 == (unsigned long long)E * (unsigned long long)F.xexp_f[bI]) {
+          __threadfence();
+          st_rel_u32(F.ready_f + bI, E);
+        }
+      }
     } else {
-      // ---------------- tile: acc[rows] += L_tile · y_b
-      const int ti = task;
+      // ---------------- TILE: acc[rows] += L_tile · y_b  (rows all in supernode tile_dest)
+      const int ti = idx;
       const int b = F.tile_blk[ti];
       const int wk = F.blk_w[b];
       const int Rn = F.tile_nr[ti];
       const int r0 = F.tile_r0[ti];
       const int64_t noff = F.blk_noff[b];
       const int64_t c0 = F.blk_col0[b];
-      const double* L = F.fstore + F.blk_off[b] + r0;
-      const int ld = Rn + 1;
-      for (int idx = tid; idx < Rn * wk; idx += NT) {
-        int c = idx / Rn, r = idx % Rn;
-        sm[c * ld + r] = L[r + (int64_t)c * noff];
+      load_tile(sm, F.fstore + F.blk_off[b] + r0, Rn, wk, noff);
+      if (tid == 0) {
+        spin_u32(F.ready_f + b, E);
+        if (F.tprof) t1 = gtime();
       }
-      if (tid == 0) spin_u32(F.ready_f + b, E);
       __syncthreads();
       if (tid < wk) S.y[tid] = __ldcg(x + c0 + tid);
       __syncthreads();
       const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
       if (Rn <= 64) {
-        const int r = tid & 63, g = tid >> 6;
-        double s = 0.0;
-        if (r < Rn)
-          for (int c = g; c < wk; c += 4) s += sm[c * ld + r] * S.y[c];
-        S.red[g * 64 + r] = s;
-        __syncthreads();
-        if (tid < Rn) {
-          double v = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
-          atomicAdd(F.acc + rows[tid], v);
-        }
+        tile_gemv(sm, Rn, wk, S.y, S.red);
+        if (tid < Rn) atomicAdd(F.acc + rows[tid], S.red[tid]);
       } else {
+        const int ld = Rn + 1;
         for (int r = tid; r < Rn; r += NT) {
           double s = 0.0;
           for (int c = 0; c < wk; ++c) s += sm[c * ld + r] * S.y[c];
@@ -454,6 +653,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       __syncthreads();
       if (tid == 0) atomicAdd(F.cnt_f + F.tile_dest[ti], 1ull);
     }
+    if (F.tprof) tprof_add(F.tprof, 0, type, t0, t1, gtime());
   }
   if (tid == 0) {
     unsigned d = atomicAdd(F.sweep + 1, 1u);
@@ -478,80 +678,160 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
   while (true) {
     if (tid == 0) {
       unsigned t = atomicAdd(F.sweep + 0, 1u);
-      S.task = t < (unsigned)F.n_bwd_tasks ? F.bwd_tasks[t] : INT32_MIN;
+      S.task = t < (unsigned)F.n_bwd_tasks ? F.bwd_tasks[t] : -1;
     }
     __syncthreads();
     const int task = S.task;
     __syncthreads();
-    if (task == INT32_MIN) break;
-    if (task < 0) {
-      const int b = -task - 1;
+    if (task < 0) break;
+    const int type = task >> 28, idx = task & ((1 << 28) - 1);
+    const unsigned long long t0 = F.tprof ? gtime() : 0ull;
+    unsigned long long t1 = t0;
+    if (type == 0 || type == 2) {
+      const int b = idx;
       const int wk = F.blk_w[b];
       const int64_t c0 = F.blk_col0[b];
-      const double* inv = F.fstore + F.blk_inv[b];
-      for (int idx = tid; idx < wk * wk; idx += NT) {
-        int c = idx / wk, r = idx % wk;
-        sm[c * 65 + r] = inv[idx];
+      if (type == 0) {
+        const double* inv = F.fstore + F.blk_inv[b];
+        for (int i2 = tid; i2 < wk * wk; i2 += NT) {
+          int c = i2 / wk, r = i2 - c * wk;
+          sm[c * 65 + r] = __ldg(inv + i2);
+        }
       }
-      if (tid == 0) spin_u64(F.cnt_b + b, (unsigned long long)E * (unsigned long long)F.bwd_expect[b]);
+      double dinv = 0.0;
+      if (tid < wk) dinv = 1.0 / F.Dpiv[c0 + tid];
+      if (tid == 0) {
+        spin_u64(F.cnt_b + b, (unsigned long long)E * (unsigned long long)F.bwd_expect[b]);
+        if (F.tprof) t1 = gtime();
+      }
       __syncthreads();
       if (tid < wk) {
         double* tp = F.tacc + c0 + tid;
-        S.rhs[tid] = __ldcg(x + c0 + tid) / F.Dpiv[c0 + tid] - __ldcg(tp);
+        S.rhs[tid] = __ldcg(x + c0 + tid) * dinv - __ldcg(tp);
         *tp = 0.0;
       }
+      __syncthreads();
+      if (type == 0) {
+        const int i = tid & 63, g = tid >> 6;
+        double s = 0.0;
+        if (i < wk)
+          for (int j = i + g; j < wk; j += 4) s += sm[i * 65 + j] * S.rhs[j];  // Linv(j, i)
+        S.red[g * 64 + i] = s;
+        __syncthreads();
+        if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_rel_u32(F.ready_sb + F.blk_sn[b], E);
+      } else {
+        if (tid < wk) {
+          F.vbuf[c0 + tid] = S.rhs[tid];
+          x[c0 + tid] = 0.0;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_rel_u32(F.vready_b + b, E);
+      }
+    } else if (type == 4) {
+      // ---------------- SNF(b) backward: t = L_rowsᵀ x_rows (gather), x_b = L_bb⁻ᵀ (D⁻¹ y_b − t)
+      const int b = idx;
+      const int J = F.blk_sn[b];
+      const int wk = F.blk_w[b];
+      const int64_t c0 = F.blk_col0[b];
+      double dinv = 0.0;
+      if (tid < wk) dinv = 1.0 / F.Dpiv[c0 + tid];
+      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) spin_u32(F.ready_sb + F.blk_dest[k], E);
+      if (F.tprof && tid == 0) t1 = gtime();
+      __syncthreads();
+      const int64_t noff = F.blk_noff[b];
+      const double* L = F.fstore + F.blk_off[b];
+      const int32_t* rows = F.sn_rows + F.blk_rows[b];
+      const int Rc = wk > 4 ? 4096 / wk : 1024;
+      double tsum = 0.0;
+      for (int64_t r0 = 0; r0 < noff; r0 += Rc) {
+        const int Rn = (int)(noff - r0 < Rc ? noff - r0 : Rc);
+        load_tile(sm, L + r0, Rn, wk, noff);
+        double* xr = sm + wk * (Rn + 1);
+        for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r0 + r]);
+        __syncthreads();
+        tile_gemv_t(sm, Rn, wk, xr, S.red);
+        if (tid < wk) tsum += S.red[tid];
+        __syncthreads();
+      }
+      const double* inv = F.fstore + F.blk_inv[b];
+      for (int i2 = tid; i2 < wk * wk; i2 += NT) {
+        int c = i2 / wk, r = i2 - c * wk;
+        sm[c * 65 + r] = __ldg(inv + i2);
+      }
+      if (tid < wk) S.rhs[tid] = __ldcg(x + c0 + tid) * dinv - tsum;
       __syncthreads();
       {
         const int i = tid & 63, g = tid >> 6;
         double s = 0.0;
         if (i < wk)
-          for (int j = i + g; j < wk; j += 4) s += sm[i * 65 + j] * S.rhs[j];  // Linv(j, i)
+          for (int j = i + g; j < wk; j += 4) s += sm[i * 65 + j] * S.rhs[j];
         S.red[g * 64 + i] = s;
       }
       __syncthreads();
       if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
       __threadfence();
       __syncthreads();
-      if (tid == 0) st_rel_u32(F.ready_b + b, E);
+      if (tid == 0) st_rel_u32(F.ready_sb + J, E);
+    } else if (type == 3) {
+      // ---------------- XCHUNK (backward): x[K] += (X_Jᵀ)_{K, I0..I0+nI} · v[I0..]
+      const int bK = F.xb_bK[idx], bI = F.xb_bI[idx], nI = F.xb_nI[idx];
+      const int J = F.blk_sn[bK];
+      const int64_t cJ = F.sn_start[J];
+      const int64_t rK = F.blk_col0[bK], cI = F.blk_col0[bI];
+      const int Rn = F.blk_w[bK];
+      const int ncol = (int)(F.blk_col0[bI + nI - 1] + F.blk_w[bI + nI - 1] - cI);
+      if (tid < nI) spin_u32(F.vready_b + bI + tid, E);
+      if (tid == 64) spin_u32(F.vready_b + bK, E);
+      if (F.tprof && tid == 0) t1 = gtime();
+      __syncthreads();
+      for (int c = tid; c < ncol; c += NT) sm[c] = __ldcg(F.vbuf + cI + c);
+      __syncthreads();
+      double* red = sm + 512;
+      const int64_t ldx = F.sn_ldx[J];
+      xchunk_gemv(F.xinv + F.sn_xtr[J] + (rK - cJ) + (cI - cJ) * ldx, ldx, Rn, ncol, sm, red);
+      if (tid < Rn) atomicAdd(x + rK + tid, red[512 + tid]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long old = atomicAdd(F.cntx_b + bK, 1ull);
+        if (old + 1 == (unsigned long long)E * (unsigned long long)F.xexp_b[bK]) {
+          __threadfence();
+          unsigned long long d = atomicAdd(F.sn_done_b + J, 1ull);
+          if (d + 1 == (unsigned long long)E * (unsigned long long)F.sn_nblk[J]) {
+            __threadfence();
+            st_rel_u32(F.ready_sb + J, E);
+          }
+        }
+      }
     } else {
-      const int ti = task;
+      const int ti = idx;
       const int b = F.tile_blk[ti];
       const int wk = F.blk_w[b];
       const int Rn = F.tile_nr[ti];
       const int r0 = F.tile_r0[ti];
       const int64_t noff = F.blk_noff[b];
       const int64_t c0 = F.blk_col0[b];
-      const double* L = F.fstore + F.blk_off[b] + r0;
-      const int ld = Rn + 1;
-      for (int idx = tid; idx < Rn * wk; idx += NT) {
-        int c = idx / Rn, r = idx % Rn;
-        sm[c * ld + r] = L[r + (int64_t)c * noff];
+      load_tile(sm, F.fstore + F.blk_off[b] + r0, Rn, wk, noff);
+      if (tid == 0) {
+        spin_u32(F.ready_sb + F.tile_dest[ti], E);
+        if (F.tprof) t1 = gtime();
       }
-      if (tid == 0) spin_u32(F.ready_b + F.tile_dest[ti], E);
       __syncthreads();
       const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
-      double* xr = sm + wk * ld;  // Rn values after the tile
+      double* xr = sm + wk * (Rn + 1);
       for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r]);
       __syncthreads();
-      const int lane = tid & 31, wid = tid >> 5;
-      const int P = wk >= 8 ? 1 : 8 / wk;
-      for (int it = wid; it < wk * P; it += NT / 32) {
-        const int c = it / P, part = it % P;
-        double s = 0.0;
-        for (int r = part * 32 + lane; r < Rn; r += 32 * P) s += sm[c * ld + r] * xr[r];
-        s = warp_sum(s);
-        if (lane == 0) S.red[it] = s;
-      }
-      __syncthreads();
-      if (tid < wk) {
-        double s = 0.0;
-        for (int part = 0; part < P; ++part) s += S.red[tid * P + part];
-        atomicAdd(F.tacc + c0 + tid, s);
-      }
+      tile_gemv_t(sm, Rn, wk, xr, S.red);
+      if (tid < wk) atomicAdd(F.tacc + c0 + tid, S.red[tid]);
       __threadfence();
       __syncthreads();
       if (tid == 0) atomicAdd(F.cnt_b + b, 1ull);
     }
+    if (F.tprof) tprof_add(F.tprof, 1, type, t0, t1, gtime());
   }
   if (tid == 0) {
     unsigned d = atomicAdd(F.sweep + 1, 1u);
@@ -562,6 +842,129 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       __threadfence();
     }
   }
+}
+
+// ------------------------------------------------------------------------- partitioned inverse
+// Batched C = α·A·B + β·C (column-major), 64×64 C tile per CTA, K in chunks of 32.
+__global__ void __launch_bounds__(NT) k_gemm_batched(const GemmProb* probs, const int64_t* pref, int nprob) {
+  __shared__ double As[32 * 64];
+  __shared__ double Bs[32 * 64];
+  const int p = find_seg(pref, nprob + 1, blockIdx.x);
+  const GemmProb P = probs[p];
+  const int64_t t = blockIdx.x - pref[p];
+  const int tilesM = (P.M + 63) / 64;
+  const int ti = (int)(t % tilesM), tj = (int)(t / tilesM);
+  const int r0 = ti * 64, c0 = tj * 64;
+  int kmin = (P.flags & 2) ? c0 : 0;
+  int kmax = (P.flags & 1) ? min(P.K, r0 + 64) : P.K;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = kmin; k0 < kmax; k0 += 32) {
+    const int kc = min(32, kmax - k0);
+    for (int idx = tid; idx < 32 * 64; idx += NT) {
+      int r = idx & 63, k = idx >> 6;
+      As[k * 64 + r] = (k < kc && r0 + r < P.M) ? P.A[(r0 + r) + (int64_t)(k0 + k) * P.lda] : 0.0;
+      int kk = idx & 31, c = idx >> 5;
+      Bs[kk * 64 + c] = (kk < kc && c0 + c < P.N) ? P.B[(k0 + kk) + (int64_t)(c0 + c) * P.ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = As[k * 64 + tx + 16 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = Bs[k * 64 + ty + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const int c = c0 + ty + 16 * y;
+    if (c >= P.N) continue;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int r = r0 + tx + 16 * x;
+      if (r >= P.M) continue;
+      double* cp = P.C + r + (int64_t)c * P.ldc;
+      *cp = P.alpha * acc[x][y] + (P.beta != 0.0 ? P.beta * *cp : 0.0);
+    }
+  }
+}
+
+void gemm_batched(const GemmProb* probs, const int64_t* tile_pref, int nprob, int64_t total_tiles,
+                  cudaStream_t s) {
+  if (total_tiles <= 0) return;
+  k_gemm_batched<<<(unsigned)total_tiles, NT, 0, s>>>(probs, tile_pref, nprob);
+}
+
+// X_J := unit-lower L_JJ below the diagonal tiles, L_kk⁻¹ on the 64×64 diagonal tiles, 0 above.
+__global__ void k_build_xinv(DevFactor F, const int32_t* big, int n_big) {
+  const int J = big[blockIdx.y];
+  const int64_t cJ = F.sn_start[J], w = F.sn_start[J + 1] - cJ, ldx = F.sn_ldx[J];
+  double* X = F.xinv + F.sn_xinv[J];
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < ldx * w; e += (int64_t)gridDim.x * NT) {
+    const int64_t c = e / ldx, r = e - c * ldx;
+    if (r >= w) {
+      X[e] = 0.0;
+      continue;
+    }
+    double v = 0.0;
+    const int64_t kc = c / MF_BW, kr = r / MF_BW;
+    const int b = F.sn_blk0[J] + (int)kc;
+    const int wk = F.blk_w[b];
+    if (kr == kc) {
+      if (r >= c) v = F.fstore[F.blk_inv[b] + (c - kc * MF_BW) * wk + (r - kc * MF_BW)];
+    } else if (r > c) {
+      const int64_t noff = F.blk_noff[b];
+      v = F.fstore[F.blk_off[b] + (r - (kc * MF_BW + wk)) + (c - kc * MF_BW) * noff];
+    }
+    X[e] = v;
+  }
+}
+
+// X_Jᵀ (same padded layout) by 32×32 smem tiles; padding rows of X_Jᵀ are zero.
+__global__ void k_transpose_xinv(DevFactor F, const int32_t* big) {
+  __shared__ double t[32][33];
+  const int J = big[blockIdx.z];
+  const int64_t w = F.sn_start[J + 1] - F.sn_start[J], ldx = F.sn_ldx[J];
+  const double* X = F.xinv + F.sn_xinv[J];
+  double* XT = F.xinv + F.sn_xtr[J];
+  const int64_t nt = (ldx + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < nt * nt; tile += gridDim.x) {
+    const int64_t bi = tile % nt, bj = tile / nt;   // X rows bi*32.., cols bj*32..
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 × 8
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t r = bi * 32 + tx, c = bj * 32 + k;
+      t[k][tx] = (r < ldx && c < w) ? X[r + c * ldx] : 0.0;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t r = bj * 32 + tx, c = bi * 32 + k;   // XT(r, c) = X(c, r)
+      if (r < ldx && c < w) XT[r + c * ldx] = r < w ? t[tx][k] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+void transpose_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s) {
+  if (n_big == 0) return;
+  dim3 grid((unsigned)std::min<int64_t>((max_w2 + 1023) / 1024 + 1, 148 * 8), 1, (unsigned)n_big);
+  k_transpose_xinv<<<grid, NT, 0, s>>>(F, big_sns);
+}
+
+void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s) {
+  if (n_big == 0) return;
+  dim3 grid((unsigned)std::min<int64_t>((max_w2 + NT - 1) / NT, 148 * 8), (unsigned)n_big);
+  k_build_xinv<<<grid, NT, 0, s>>>(F, big_sns, n_big);
 }
 
 static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)(TRSV_SMEM_DBL + 1024); }

@@ -42,11 +42,35 @@ struct DevFactor {
   // trsv sweep state
   double* acc;                    // N: forward accumulators
   double* tacc;                   // N: backward accumulators
-  unsigned long long* cnt_f;      // nb
+  unsigned long long* cnt_f;      // per SUPERNODE: forward contributions received
   unsigned long long* cnt_b;      // nb
   unsigned int* ready_f;          // nb
   unsigned int* ready_b;          // nb
   unsigned int* sweep;            // [0] ticket, [1] finished CTAs, [2] fwd epoch, [3] bwd epoch
+  // partitioned inverse of big supernodes
+  const int32_t* blk_sn;
+  const int64_t* sn_xinv;
+  const int32_t* xt_bI;
+  const int32_t* xt_bK;
+  const int32_t* xt_nK;
+  const int32_t* xb_bK;
+  const int32_t* xb_bI;
+  const int32_t* xb_nI;
+  const int64_t* sn_xtr;
+  const int64_t* sn_ldx;
+  const int32_t* sn_nblk;
+  const int64_t* blk_dptr;        // fused small supernodes: destination supernode lists
+  const int32_t* blk_dest;
+  unsigned int* ready_sb;         // ns: backward — all of supernode J final
+  unsigned long long* sn_done_b;  // ns: backward — completed column blocks of a big supernode
+  const int32_t* xexp_f;
+  const int32_t* xexp_b;
+  double* xinv;                   // X_J storage
+  double* vbuf;                   // N: staged right-hand sides of big supernodes
+  unsigned long long* cntx_f;     // nb
+  unsigned long long* cntx_b;     // nb
+  unsigned int* vready_f;         // nb
+  unsigned int* vready_b;         // nb
   // multifrontal plan
   const int64_t* asm_dst;
   const double* asm_val;
@@ -64,6 +88,7 @@ struct DevFactor {
   const int64_t* pan_pref;
   const int64_t* upd_pref;
   int* status;        // pivot failures (device int)
+  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][4 types][5]
 };
 
 // CSR on the device (int64 row pointers, int32 columns).
@@ -98,6 +123,21 @@ void mf_assemble_diag_add(const DevFactor& F, const double* D, const int64_t* pe
 void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s);
 void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
              int64_t upd_total, cudaStream_t s);
+
+// ---- partitioned inverse X_J = L_JJ⁻¹ of big supernodes (factor time)
+struct GemmProb {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, lda, ldb, ldc;
+  double alpha, beta;
+  int flags;  // 1: A lower-triangular (k <= row), 2: B lower-triangular (k >= col)
+  int pad;
+};
+void gemm_batched(const GemmProb* probs, const int64_t* tile_pref, int nprob, int64_t total_tiles,
+                  cudaStream_t s);
+void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
+void transpose_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
 
 // ---- level-free task-graph triangular sweeps (persistent kernels)
 struct SweepRhs {

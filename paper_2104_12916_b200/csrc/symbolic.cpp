@@ -133,15 +133,91 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
     S.c_fact += (double)S.colcount[j] * (double)S.colcount[j];
     S.n_rowlev = std::max(S.n_rowlev, S.rowlev[j] + 1);
   }
-  // ---------------------------------------------------------------- supernodes
-  S.sn_start.clear();
-  S.sn_start.push_back(0);
+  // ---------------------------------------------------------------- fundamental supernodes
+  std::vector<int64_t> fs_start;
+  fs_start.push_back(0);
   for (int64_t j = 1; j < N; ++j)
-    if (!(S.parent[j - 1] == j && S.colcount[j - 1] == S.colcount[j] + 1)) S.sn_start.push_back(j);
+    if (!(S.parent[j - 1] == j && S.colcount[j - 1] == S.colcount[j] + 1)) fs_start.push_back(j);
+  fs_start.push_back(N);
+  const int64_t nf = (int64_t)fs_start.size() - 1;
+  std::vector<int64_t> col2sn(N);
+  for (int64_t J = 0; J < nf; ++J)
+    for (int64_t c = fs_start[J]; c < fs_start[J + 1]; ++c) col2sn[c] = J;
+  std::vector<int64_t> fparent(nf, -1);
+  for (int64_t J = 0; J < nf; ++J) {
+    int64_t p = S.parent[fs_start[J + 1] - 1];
+    if (p >= 0) fparent[J] = col2sn[p];
+  }
+  std::vector<std::vector<int32_t>> fchildren(nf);
+  for (int64_t J = 0; J < nf; ++J)
+    if (fparent[J] >= 0) fchildren[fparent[J]].push_back((int32_t)J);
+  // rows strictly below each fundamental supernode's columns
+  std::vector<int64_t> fb_ptr(nf + 1, 0);
+  std::vector<int32_t> fb_rows;
+  {
+    std::vector<int64_t> mark(N, -1);
+    std::vector<int32_t> buf;
+    for (int64_t J = 0; J < nf; ++J) {
+      const int64_t c0 = fs_start[J], c1 = fs_start[J + 1];
+      buf.clear();
+      for (int64_t c = c0; c < c1; ++c)
+        for (int64_t q = M.colptr[c]; q < M.colptr[c + 1]; ++q) {
+          int64_t r = M.rowind[q];
+          if (r >= c1 && mark[r] != J) { mark[r] = J; buf.push_back((int32_t)r); }
+        }
+      for (int32_t K : fchildren[J])
+        for (int64_t q = fb_ptr[K]; q < fb_ptr[K + 1]; ++q) {
+          int64_t r = fb_rows[q];
+          if (r >= c1 && mark[r] != J) { mark[r] = J; buf.push_back((int32_t)r); }
+        }
+      std::sort(buf.begin(), buf.end());
+      fb_rows.insert(fb_rows.end(), buf.begin(), buf.end());
+      fb_ptr[J + 1] = (int64_t)fb_rows.size();
+      if ((c1 - c0) + (int64_t)buf.size() != S.colcount[c0])
+        return "supernode structure does not match column count (internal error)";
+    }
+  }
+  // ---------------------------------------------------------------- relaxed amalgamation
+  // Merge supernode J into its parent P when J's columns immediately precede
+  // P's and the explicit zeros stay small (thresholds of DESIGN.md §Structures:
+  // width ≤ 4 always; ≤ 16 if zeros ≤ 80%; ≤ 48 if ≤ 10%; else ≤ 5%).
+  std::vector<int64_t> rc0(nf), rw(nf), rm(nf), rtrue(nf);
+  std::vector<char> alive(nf, 1);
+  for (int64_t J = 0; J < nf; ++J) {
+    rc0[J] = fs_start[J];
+    rw[J] = fs_start[J + 1] - fs_start[J];
+    rm[J] = rw[J] + (fb_ptr[J + 1] - fb_ptr[J]);
+    int64_t t = 0;
+    for (int64_t c = fs_start[J]; c < fs_start[J + 1]; ++c) t += S.colcount[c];
+    rtrue[J] = t;
+  }
+  for (int64_t J = 0; J < nf; ++J) {
+    const int64_t P = fparent[J];
+    if (P < 0 || rc0[J] + rw[J] != rc0[P]) continue;
+    const int64_t w = rw[J] + rw[P];
+    const int64_t m = rw[J] + rm[P];
+    const int64_t stored = w * m - w * (w - 1) / 2;
+    const int64_t zeros = stored - (rtrue[J] + rtrue[P]);
+    bool merge = w <= 4 || (w <= 16 && 100 * zeros <= 80 * stored) || (w <= 48 && 100 * zeros <= 10 * stored) ||
+                 (100 * zeros <= 5 * stored);
+    if (!merge) continue;
+    rc0[P] = rc0[J];
+    rw[P] = w;
+    rm[P] = m;
+    rtrue[P] += rtrue[J];
+    alive[J] = 0;
+  }
+  // relaxed partition (alive supernodes, in column order)
+  S.sn_start.clear();
+  std::vector<int64_t> rep;  // fundamental id that carries each relaxed supernode's below-rows
+  for (int64_t J = 0; J < nf; ++J)
+    if (alive[J]) {
+      S.sn_start.push_back(rc0[J]);
+      rep.push_back(J);
+    }
   S.sn_start.push_back(N);
   const int64_t ns = (int64_t)S.sn_start.size() - 1;
   S.ns = ns;
-  std::vector<int64_t> col2sn(N);
   for (int64_t J = 0; J < ns; ++J)
     for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) col2sn[c] = J;
   S.sn_parent.assign(ns, -1);
@@ -158,33 +234,19 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
   std::vector<std::vector<int32_t>> children(ns);
   for (int64_t J = 0; J < ns; ++J)
     if (S.sn_parent[J] >= 0) children[S.sn_parent[J]].push_back((int32_t)J);
-  // ---------------------------------------------------------------- supernode row structures
+  // ---------------------------------------------------------------- relaxed supernode row structures
   S.sn_rowptr.assign(ns + 1, 0);
   S.sn_rows.clear();
-  {
-    std::vector<int64_t> mark(N, -1);
-    std::vector<int32_t> buf;
-    for (int64_t J = 0; J < ns; ++J) {
-      const int64_t c0 = S.sn_start[J], c1 = S.sn_start[J + 1];
-      buf.clear();
-      for (int64_t c = c0; c < c1; ++c)
-        for (int64_t q = M.colptr[c]; q < M.colptr[c + 1]; ++q) {
-          int64_t r = M.rowind[q];
-          if (r >= c1 && mark[r] != J) { mark[r] = J; buf.push_back((int32_t)r); }
-        }
-      for (int32_t K : children[J]) {
-        for (int64_t q = S.sn_rowptr[K]; q < S.sn_rowptr[K + 1]; ++q) {
-          int64_t r = S.sn_rows[q];
-          if (r >= c1 && mark[r] != J) { mark[r] = J; buf.push_back((int32_t)r); }
-        }
-      }
-      std::sort(buf.begin(), buf.end());
-      for (int64_t c = c0; c < c1; ++c) S.sn_rows.push_back((int32_t)c);
-      S.sn_rows.insert(S.sn_rows.end(), buf.begin(), buf.end());
-      S.sn_rowptr[J + 1] = (int64_t)S.sn_rows.size();
-      if (S.sn_rowptr[J + 1] - S.sn_rowptr[J] != S.colcount[c0])
-        return "supernode structure does not match column count (internal error)";
-    }
+  for (int64_t J = 0; J < ns; ++J) {
+    for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) S.sn_rows.push_back((int32_t)c);
+    const int64_t F0 = rep[J];
+    S.sn_rows.insert(S.sn_rows.end(), fb_rows.begin() + fb_ptr[F0], fb_rows.begin() + fb_ptr[F0 + 1]);
+    S.sn_rowptr[J + 1] = (int64_t)S.sn_rows.size();
+  }
+  S.nnz_stored = 0;
+  for (int64_t J = 0; J < ns; ++J) {
+    const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+    S.nnz_stored += w * m - w * (w - 1) / 2;
   }
   // ---------------------------------------------------------------- fronts
   S.front_off.assign(ns, 0);
@@ -226,19 +288,62 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
   for (int64_t b = 0; b < S.nb; ++b)
     for (int64_t c = S.blk_col0[b]; c < S.blk_col0[b] + S.blk_w[b]; ++c) S.col2blk[c] = (int32_t)b;
   // ---------------------------------------------------------------- trsv tiles and task queues
+  // Big supernodes (more than one 64-column block) are swept through X_J = L_JJ⁻¹
+  // (partitioned inverse): their intra-supernode rows are not tiled.
   S.tile_blk.clear(); S.tile_r0.clear(); S.tile_nr.clear(); S.tile_dest.clear();
-  S.fwd_expect.assign(S.nb, 0);
+  S.fwd_expect.assign(ns, 0);
   S.bwd_expect.assign(S.nb, 0);
+  S.blk_big.assign(S.nb, 0);
+  S.sn_xinv.assign(ns, -1);
+  S.sn_xtr.assign(ns, -1);
+  S.sn_ldx.assign(ns, 0);
+  S.sn_xtmp.assign(ns, -1);
+  S.x_size = 0;
+  S.xtmp_size = 0;
+  for (int64_t J = 0; J < ns; ++J) {
+    const int64_t w = S.sn_start[J + 1] - S.sn_start[J];
+    if (w > BW) {
+      const int64_t ldx = (w + 7) & ~int64_t(7);
+      S.sn_ldx[J] = ldx;
+      S.sn_xinv[J] = S.x_size;
+      S.x_size += ldx * w;
+      S.sn_xtr[J] = S.x_size;
+      S.x_size += ldx * w;
+      S.sn_xtmp[J] = S.xtmp_size;
+      S.xtmp_size += (w / 2 + BW) * (w / 2 + BW);
+      for (int64_t b = S.sn_blk0[J]; b < S.sn_blk0[J + 1]; ++b) S.blk_big[b] = 1;
+    }
+  }
   std::vector<int64_t> blk_tile0(S.nb + 1, 0);
+  std::vector<char> fused(S.nb, 0);
+  S.blk_dptr.assign(S.nb + 1, 0);
+  S.blk_dest.clear();
   for (int64_t b = 0; b < S.nb; ++b) {
     blk_tile0[b] = (int64_t)S.tile_blk.size();
+    const int64_t J = S.blk_sn[b];
     const int64_t wk = S.blk_w[b], noff = S.blk_noff[b];
+    if (!S.blk_big[b] && wk * noff <= FUSE_ELEMS) {
+      fused[b] = 1;
+      int64_t last = -1;
+      for (int64_t r = 0; r < noff; ++r) {
+        int64_t dsn = col2sn[S.sn_rows[S.blk_rows[b] + r]];
+        if (dsn != last) {   // rows are sorted, so destination supernodes are non-decreasing
+          S.blk_dest.push_back((int32_t)dsn);
+          S.fwd_expect[dsn] += 1;
+          last = dsn;
+        }
+      }
+      S.blk_dptr[b + 1] = (int64_t)S.blk_dest.size();
+      continue;
+    }
+    S.blk_dptr[b + 1] = (int64_t)S.blk_dest.size();
     const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(1024, TILE_ELEMS / wk));
-    int64_t r = 0;
+    // first off-diagonal row below the supernode's own columns
+    int64_t r = S.blk_big[b] ? (S.sn_start[J + 1] - (S.blk_col0[b] + wk)) : 0;
     while (r < noff) {
-      int32_t dest = S.col2blk[S.sn_rows[S.blk_rows[b] + r]];
+      int32_t dest = (int32_t)col2sn[S.sn_rows[S.blk_rows[b] + r]];
       int64_t e = r + 1;
-      while (e < noff && e - r < cap && S.col2blk[S.sn_rows[S.blk_rows[b] + e]] == dest) ++e;
+      while (e < noff && e - r < cap && col2sn[S.sn_rows[S.blk_rows[b] + e]] == dest) ++e;
       S.tile_blk.push_back((int32_t)b);
       S.tile_r0.push_back((int32_t)r);
       S.tile_nr.push_back((int32_t)(e - r));
@@ -249,15 +354,74 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
     }
   }
   blk_tile0[S.nb] = (int64_t)S.tile_blk.size();
+  auto enc = [](int type, int64_t idx) { return (int32_t)(((int64_t)type << TASK_SHIFT) | idx); };
+  S.xt_bI.clear();
+  S.xt_bK.clear();
+  S.xt_nK.clear();
+  S.xb_bK.clear();
+  S.xb_bI.clear();
+  S.xb_nI.clear();
+  std::vector<int64_t> sn_xb0(ns + 1, 0);
+  S.xexp_f.assign(S.nb, 0);
+  S.xexp_b.assign(S.nb, 0);
+  S.sn_nblk.assign(ns, 0);
+  std::vector<int64_t> sn_xt0(ns + 1, 0);
+  for (int64_t J = 0; J < ns; ++J) {
+    sn_xt0[J] = (int64_t)S.xt_bI.size();
+    sn_xb0[J] = (int64_t)S.xb_bK.size();
+    S.sn_nblk[J] = S.sn_blk0[J + 1] - S.sn_blk0[J];
+    if (S.sn_xinv[J] < 0) continue;
+    const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1], T = b1 - b0;
+    for (int64_t I = 0; I < T; ++I)
+      for (int64_t K = 0; K <= I; K += XCH) {
+        S.xt_bI.push_back((int32_t)(b0 + I));
+        S.xt_bK.push_back((int32_t)(b0 + K));
+        S.xt_nK.push_back((int32_t)std::min<int64_t>(XCH, I + 1 - K));
+      }
+    for (int64_t K = 0; K < T; ++K)
+      for (int64_t I = K; I < T; I += XCH) {
+        S.xb_bK.push_back((int32_t)(b0 + K));
+        S.xb_bI.push_back((int32_t)(b0 + I));
+        S.xb_nI.push_back((int32_t)std::min<int64_t>(XCH, T - I));
+      }
+    for (int64_t I = 0; I < T; ++I) {
+      S.xexp_f[b0 + I] = (int32_t)((I + XCH) / XCH);           // forward chunks covering row-block I
+      S.xexp_b[b0 + I] = (int32_t)((T - I + XCH - 1) / XCH);   // backward chunks of output block K = I
+    }
+  }
+  sn_xt0[ns] = (int64_t)S.xt_bI.size();
+  sn_xb0[ns] = (int64_t)S.xb_bK.size();
+  if ((int64_t)S.xt_bI.size() >= (int64_t(1) << TASK_SHIFT) || (int64_t)S.tile_blk.size() >= (int64_t(1) << TASK_SHIFT))
+    return "too many sweep tasks for the 28-bit task encoding";
   S.fwd_tasks.clear();
   S.bwd_tasks.clear();
-  for (int64_t b = 0; b < S.nb; ++b) {
-    S.fwd_tasks.push_back(-(int32_t)b - 1);
-    for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back((int32_t)t);
+  for (int64_t J = 0; J < ns; ++J) {
+    const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
+    if (S.sn_xinv[J] < 0) {
+      for (int64_t b = b0; b < b1; ++b) {
+        S.fwd_tasks.push_back(enc(fused[b] ? 4 : 0, b));
+        for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back(enc(1, t));
+      }
+    } else {
+      for (int64_t b = b0; b < b1; ++b) S.fwd_tasks.push_back(enc(2, b));
+      for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) S.fwd_tasks.push_back(enc(3, x));
+      for (int64_t b = b0; b < b1; ++b)
+        for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back(enc(1, t));
+    }
   }
-  for (int64_t b = S.nb - 1; b >= 0; --b) {
-    for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back((int32_t)t);
-    S.bwd_tasks.push_back(-(int32_t)b - 1);
+  for (int64_t J = ns - 1; J >= 0; --J) {
+    const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
+    if (S.sn_xinv[J] < 0) {
+      for (int64_t b = b1 - 1; b >= b0; --b) {
+        for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back(enc(1, t));
+        S.bwd_tasks.push_back(enc(fused[b] ? 4 : 0, b));
+      }
+    } else {
+      for (int64_t b = b1 - 1; b >= b0; --b)
+        for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back(enc(1, t));
+      for (int64_t b = b0; b < b1; ++b) S.bwd_tasks.push_back(enc(2, b));
+      for (int64_t x = sn_xb0[J]; x < sn_xb0[J + 1]; ++x) S.bwd_tasks.push_back(enc(3, x));
+    }
   }
   // ---------------------------------------------------------------- assembly map, relative indices
   S.asm_dst.clear();

@@ -13,6 +13,9 @@ namespace qpb {
 
 constexpr int BW = 64;          // pivot block width (columns per trsv block column)
 constexpr int TILE_ELEMS = 4096; // max doubles in one trsv tile (32 KiB)
+constexpr int XCH = 8;           // column blocks per X chunk of a big supernode
+constexpr int FUSE_ELEMS = 32768; // small supernodes with w·noff ≤ this are swept as one task
+constexpr int TASK_SHIFT = 28;   // task = (type << TASK_SHIFT) | index
 
 // Lower-triangular (strict) pattern + values of a symmetric matrix already in
 // factor order, by columns, plus its diagonal.
@@ -43,6 +46,7 @@ struct Symbolic {
   std::vector<int64_t> perm;      // new -> old (of the matrix being factored)
   std::vector<int64_t> parent, colcount, rowlev;
   int64_t nnz_L = 0, n_rowlev = 0;
+  int64_t nnz_stored = 0;          // entries stored by the relaxed supernodes (≥ nnz_L)
   double c_fact = 0;              // Σ cc²
 
   // supernodes
@@ -64,9 +68,26 @@ struct Symbolic {
   int64_t fs_size = 0;
   std::vector<int32_t> col2blk;    // N
 
-  // trsv tiles + task queues
-  std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;
-  std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect, bwd_expect;
+  // trsv tiles + task queues.  Task encoding: (type << 28) | index with
+  // type 0 DIAG(block), 1 TILE(off-diagonal tile), 2 PREP(block of a big
+  // supernode), 3 XCHUNK(chunk of the inverse diagonal block of a big
+  // supernode), 4 SNF(small supernode swept in one task: diagonal + all rows).
+  std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;   // tile_dest: destination SUPERNODE
+  std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect /*per supernode*/, bwd_expect /*per block*/;
+  // partitioned inverse of multi-block ("big") supernodes
+  std::vector<int64_t> sn_xinv;          // offset of X_J = L_JJ⁻¹ (w×w col-major, ld sn_ldx) or -1
+  std::vector<int64_t> sn_xtr;           // offset of X_Jᵀ (same layout)
+  std::vector<int64_t> sn_ldx;           // leading dimension (w rounded up to 8)
+  std::vector<int32_t> xb_bK, xb_bI, xb_nI; // backward chunks: output block K, first row-block I, #blocks
+  std::vector<int32_t> xt_bI, xt_bK, xt_nK; // X chunks: row-block, first column-block, #column-blocks
+  std::vector<int32_t> xexp_f, xexp_b;   // per block: X chunks covering the row-block / column-block
+  std::vector<int32_t> sn_nblk;          // blocks per supernode
+  std::vector<int64_t> blk_dptr;         // per block: fused destination-supernode list (nb+1)
+  std::vector<int32_t> blk_dest;
+  std::vector<int32_t> blk_big;          // 1 if the block belongs to a big supernode
+  int64_t x_size = 0;                    // doubles of all X_J
+  int64_t xtmp_size = 0;                 // doubles of the inversion scratch
+  std::vector<int64_t> sn_xtmp;          // scratch offset per big supernode
 
   // multifrontal plan
   std::vector<int64_t> asm_dst;    // destination in workspace for each lower entry (+diag)

@@ -1,0 +1,17 @@
+"""Factor c1 (or another config) and apply K_F a few times — a short command for ncu."""
+import sys
+import numpy as np
+sys.path.insert(0, '.')
+import qpgen
+from paper_2104_12916_b200.binding import from_qp
+name = sys.argv[1] if len(sys.argv) > 1 else 'c1'
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+qp = qpgen.make(name)
+s = from_qp(qp)
+s.ipm_factor_once('low')
+rng = np.random.default_rng(0)
+D = rng.uniform(0.5, 2.0, qp.m2)
+p = rng.standard_normal(qp.m2)
+for _ in range(reps):
+    q = s.kf_apply(D, p)
+print('ok', float(np.linalg.norm(q)))

@@ -131,6 +131,23 @@ def test_ipm_objective_matches_oracle(case):
     assert np.abs(qp.C @ x - sl - qp.d).max() <= 1e-9 * (1 + np.abs(qp.d).max())
     assert sl.min() > 0 and nu.min() > 0
     # per-IPM-iteration PCG counts within ±2 while the trajectories coincide
-    n_cmp = min(len(ref.pcg_iters), len(got["pcg_iters"]), 6)
+    n_cmp = min(len(ref.pcg_iters), len(got["pcg_iters"]), 3)
     for a, b in zip(ref.pcg_iters[:n_cmp], got["pcg_iters"][:n_cmp]):
         assert abs(a - b) <= 2
+
+
+def test_pcg_counts_along_oracle_trajectory(case):
+    """For every IPM iteration of the oracle run, the GPU PCG on the SAME (D_k, r_ν, ε_k)
+    takes the oracle's iteration count ±2 (north_star gate), isolating PCG parity from
+    trajectory drift."""
+    name, qp, s = case
+    if name in ("ragged", "grid"):
+        pytest.skip("PL-IPM oracle too slow at this size")
+    perm = s.structure("perm")[:qp.n]
+    ref = oracle_ipm(qp, precond="low", ipm_tol=1e-8, fs=fsolver_for(qp, perm), record=True)
+    bad = []
+    for t in ref.trace:
+        _, it, _, _ = s.pcg_solve(t["D"], t["rnu"], tol=t["eps"], maxit=2000)
+        if abs(it - t["pcg"]) > 2:
+            bad.append((t["k"], it, t["pcg"]))
+    assert not bad, bad

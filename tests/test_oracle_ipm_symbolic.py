@@ -149,11 +149,17 @@ def test_symbolic_matches_numeric_ldlt_pattern(seed):
         assert set(st["struct"][j].tolist()) == pattern[j]
         below = sorted(pattern[j] - {j})
         assert st["parent"][j] == (below[0] if below else -1)
-    # supernode property: struct(j−1) = {j−1} ∪ struct(j) inside a supernode
-    sn = st["sn_start"]
+    # fundamental supernode property: struct(j−1) = {j−1} ∪ struct(j)
+    sn = st["fsn_start"]
     for J in range(len(sn) - 1):
         for j in range(sn[J] + 1, sn[J + 1]):
             assert pattern[j - 1] == {j - 1} | pattern[j]
+    # relaxed supernodes cover every column's structure (explicit zeros allowed)
+    rs, rp, rr = st["sn_start"], st["sn_rowptr"], st["sn_rows"]
+    for J in range(len(rs) - 1):
+        rows = set(rr[rp[J]:rp[J + 1]].tolist())
+        for j in range(rs[J], rs[J + 1]):
+            assert pattern[j] <= rows
     # row levels by longest dependency path
     lev = np.zeros(N, dtype=int)
     for i in range(N):
