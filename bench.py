@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py — PCG iterations/s of the single-factorization inexact IPM (arXiv 2104.12916) on B200.
+
+Workload (BASELINE.json configs[1], "c1"): random sparse convex QP, n = 20 000,
+m1 = 5 000, m2 = 40 000, H = GᵀG + 0.1 I (G 8 nnz/row), A 4 / C 6 nnz/row,
+seed 0, fp64, preconditioner P_L (PL-KF).  A *step* is one IPM iteration of
+the hot path — residuals (a9), r_ν F-solve (a10), PCG on K_F to ε_k (a1–a6),
+recovery F-solve + Δs + step (a11) — on the device-resident iterate.  The
+one-time F factorization (a12) is setup, timed and reported separately.
+
+  value      PCG iterations / s over the K timed IPM steps (after W warm-up
+             steps), CUDA events on the library's stream, max over ranks.
+  e2e        the same metric through the public C ABI from pinned HOST
+             buffers: pcg_solve(D_k, r_ν) replayed for the same K steps, with
+             the host→device copy of (D_k, r_ν) and device→host copy of Δν in
+             the timed region.
+  roofline   the L_F triangular sweeps (forward + backward; ≥ 95 % of the
+             step): algorithmic bytes 8·nnz(L_F) per sweep
+             ÷ their CUDA-event durations inside the timed region, against
+             MEASURED_PEAKS.json's HBM copy bandwidth.
+  cpu_baseline  the CPU oracle (oracle/, NumPy/SciPy fp64) on the box's host
+             cores: PCG iterations of IPM step 0 on the same c1 problem.
+
+Multi-GPU (torchrun, N > 1): one independent replica per GPU (DESIGN.md
+§Multi-GPU: the F-solve, ≥ 95 % of the bytes, is replicated, so the path is
+run as weak-scaling replicas), value = Σ PCG iterations / max-over-ranks time.
+
+``--impl reference`` times the CPU oracle as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG iterations/s (fp64, K_F = D - [C 0] F^-1 [C^T; 0], IPM hot path)"
+UNIT = "PCG iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--precond", default="low", choices=["none", "low", "high"])
+    ap.add_argument("--cpu-iters", type=int, default=6, help="oracle PCG iterations per sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-traffic", default=os.path.join(ROOT, "profiles", "traffic.json"))
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def dist_init(world, local):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world > 1
+
+
+def barrier(use_dist):
+    if use_dist:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce(vals, op, use_dist):
+    if not use_dist:
+        return vals
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return t.cpu().tolist()
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in open(self.path):
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def cpu_oracle_sample(qp, iters, x_perm=None):
+    """Time `iters` oracle PCG iterations on IPM step 0's reduced system (oracle as it stands)."""
+    import numpy as np
+    from oracle import kkt
+    from oracle.fsolve import make_fsolver
+    from oracle.pcg import pcg
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    t0 = time.perf_counter()
+    fs = make_fsolver(qp.H, qp.A, x_perm)
+    t_setup = time.perf_counter() - t0
+    x = np.zeros(qp.n)
+    lam = np.zeros(qp.m1)
+    nu = np.ones(qp.m2)
+    s = np.abs(qp.d) + 1.0
+    res = kkt.residuals(qp, x, lam, nu, s, 0.1)
+    D = kkt.diag_D(s, nu)
+    rnu = kkt.r_nu(qp, fs, res)
+    t1 = time.perf_counter()
+    _, it, _, _, _ = pcg(lambda p: kkt.KF_apply(qp, fs, D, p), rnu, kkt.PrecondL(D), 0.0, iters)
+    dt = time.perf_counter() - t1
+    return it, dt, t_setup, cores
+
+
+def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle, timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import qpgen
+    qp = qpgen.make(args.config)
+    # warm-up samples are folded into the setup (the oracle has no GPU warm-up)
+    its, dts = 0, 0.0
+    setup = None
+    cores = None
+    for k in range(args.steps):
+        it, dt, t_setup, cores = cpu_oracle_sample(qp, args.cpu_iters, qp.x_perm)
+        setup = t_setup if setup is None else setup
+        its += it
+        dts += dt
+    value = its / dts if dts > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dts / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} PL-KF (CPU oracle: dense block-inverse F-solve, textbook PCG)",
+                   "n": qp.n, "m1": qp.m1, "m2": qp.m2},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} x {args.cpu_iters} PCG iterations of IPM step 0 on {args.config} "
+                                   f"(oracle F setup {setup:.1f} s excluded)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local, use_dist):
+    import numpy as np
+    import torch
+    import qpgen
+    from paper_2104_12916_b200.binding import from_qp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    qp = qpgen.make(args.config)
+    stream = torch.cuda.Stream(device=dev)
+    s = from_qp(qp, device=local, stream=stream.cuda_stream)
+    t0 = time.perf_counter()
+    s.ipm_factor_once(args.precond)
+    t_setup = time.perf_counter() - t0
+    st = s.stats()
+    W, K = args.warmup, args.steps
+
+    # ---------------------------------------------------------------- device-resident value run
+    s.ipm_init()
+    s.ipm_iterate(W)
+    torch.cuda.synchronize(dev)
+    s.profile(True)
+    s.profile_read()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = s.launch_count()
+    barrier(use_dist)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    r = s.ipm_iterate(K)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(use_dist)
+    ck = clocks.stop()
+    launches = s.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    prof = s.profile_read()
+    s.profile(False)
+    hist = r["pcg_iters"]
+    pcg_timed = int(sum(hist[W:W + K]))
+    steps_done = max(0, min(K, r["n_ipm"] - W))
+
+    # ---------------------------------------------------------------- e2e replay through the C ABI
+    e2e = None
+    if not args.no_e2e:
+        systems = []
+        s.ipm_init()
+        for k in range(W + K):
+            rr = s.ipm_iterate(1)
+            if rr["converged"]:
+                break
+            if k >= W:
+                D, rnu, eps = s.ipm_last_system()
+                Dp = torch.from_numpy(D).pin_memory()
+                rp = torch.from_numpy(rnu).pin_memory()
+                systems.append((Dp, rp, eps))
+        outp = torch.empty(qp.m2, dtype=torch.float64).pin_memory()
+        for (Dp, rp, eps) in systems[:1]:   # warm the host path
+            s.pcg_solve(Dp.numpy(), rp.numpy(), tol=eps, maxit=2000)
+        barrier(use_dist)
+        torch.cuda.synchronize(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        its = 0
+        f0.record(stream)
+        for (Dp, rp, eps) in systems:
+            x, it, rel, rc = s.pcg_solve(Dp.numpy(), rp.numpy(), tol=eps, maxit=2000)
+            outp.numpy()[:] = x
+            its += it
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier(use_dist)
+        ms_e2e = f0.elapsed_time(f1)
+        its_all, ms_max = allreduce([float(its)], None, False)[0], ms_e2e
+        if use_dist:
+            import torch.distributed as dist
+            its_all = allreduce([float(its)], dist.ReduceOp.SUM, True)[0]
+            ms_max = allreduce([ms_e2e], dist.ReduceOp.MAX, True)[0]
+        e2e = {"value": its_all / (ms_max / 1e3) if ms_max > 0 else 0.0, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * 8 * qp.m2, "d2h_bytes_per_step": 8 * qp.m2 + 16,
+               "steps": len(systems), "pcg_iters": its}
+
+    # ---------------------------------------------------------------- aggregate over ranks
+    tot_pcg, ms_max = float(pcg_timed), ms
+    if use_dist:
+        import torch.distributed as dist
+        tot_pcg = allreduce([float(pcg_timed)], dist.ReduceOp.SUM, True)[0]
+        ms_max = allreduce([ms], dist.ReduceOp.MAX, True)[0]
+    value = tot_pcg / (ms_max / 1e3) if ms_max > 0 else 0.0
+
+    # ---------------------------------------------------------------- roofline of the L_F sweeps
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        try:
+            peak = float(json.load(open(peaks_path))["hbm_gbs"])
+            peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    fwd_ms, fwd_n = prof["f_fwd"]
+    bwd_ms, bwd_n = prof["f_bwd"]
+    n_ipm_timed = steps_done
+    real_sweeps = 2 * pcg_timed + 2 * n_ipm_timed          # K_F products + r_ν and recovery F-solves
+    sweep_bytes = 8.0 * st["nnz_LF"]
+    achieved = (real_sweeps / 2) * sweep_bytes * 2 / ((fwd_ms + bwd_ms) / 1e3) / 1e9 if fwd_ms + bwd_ms > 0 else 0
+    traffic = None
+    if os.path.exists(args.profile_traffic):
+        try:
+            traffic = json.load(open(args.profile_traffic)).get(args.config, {}).get("dram_bytes_per_sweep")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "k_trsv_fwd + k_trsv_bwd (L_F sweeps)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src, "algorithmic_bytes_per_sweep": sweep_bytes,
+                "sweep_ms_avg": (fwd_ms + bwd_ms) / max(1, real_sweeps),
+                "sweep_share_of_step": (fwd_ms + bwd_ms) / ms if ms > 0 else None}
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        it, dt, t_or, cores = cpu_oracle_sample(qp, args.cpu_iters, s.structure("perm")[:qp.n]
+                                                if qp.n + qp.m1 > 30000 else None)
+        cpu = {"value": it / dt if dt > 0 else 0.0, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{it} PCG iterations of IPM step 0 on {args.config} (oracle F setup {t_or:.1f} s excluded)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / max(1, steps_done), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} PL-KF: one IPM iteration per step (residuals, r_nu F-solve, "
+                               f"PCG to eps_k, recovery, step)" if args.precond == "low" else
+                   f"{args.config} {args.precond.upper()}-KF IPM iteration per step",
+                   "n": qp.n, "m1": qp.m1, "m2": qp.m2, "nnz_LF": st["nnz_LF"], "precond": args.precond,
+                   "ipm_steps_timed": steps_done, "pcg_iters_timed": pcg_timed,
+                   "l2": "no flush: the factor read every sweep (%.2f GB) exceeds L2" % (st["factor_bytes"] / 1e9),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
+        "setup_s": {"symbolic": st["t_symbolic_s"], "factor": st["t_factor_s"], "factor_once_total": t_setup},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_info()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    use_dist = dist_init(world, local)
+    run_ours(args, rank, world, local, use_dist)
+    if use_dist:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -142,6 +142,14 @@ int ipm_solve(qp_ctx* ctx, const qp_ipm_opts* o, qp_ipm_result* r);
 int qp_ipm_init(qp_ctx* ctx, const qp_ipm_opts* o);
 int qp_ipm_iterate(qp_ctx* ctx, int32_t nsteps, qp_ipm_result* r, int32_t* done);
 
+/* The reduced system of the last IPM iteration run by qp_ipm_iterate:
+ * D_k (m2), r_ν (m2) and the PCG tolerance ε_k it was solved to (bench e2e
+ * replay; vector conventions as above, eps a host pointer). */
+int qp_ipm_last_system(qp_ctx* ctx, double* D, double* rnu, double* eps);
+
+/* Number of CUDA kernel launches this context has issued so far. */
+int64_t qp_launch_count(const qp_ctx* ctx);
+
 /* Component entry points (parity tests; same conventions):
  * qp_f_solve:  (y; z) = F⁻¹ (r1; r2), vectors in the ORIGINAL order,
  *              rhs/out of length n + m1 (a2–a4 of SURVEY §8(a)).

@@ -75,7 +75,7 @@ def header_functions():
     """Function names declared in include/qp_b200.h."""
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(\w+)\s*\(", txt, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(\w+)\s*\(", txt, flags=re.M)))
 
 
 def load_library(build: bool = True):
@@ -103,6 +103,9 @@ def load_library(build: bool = True):
     lib.qp_profile.argtypes = [vp, i32]
     lib.qp_profile_read.argtypes = [vp, vp, vp]
     lib.qp_debug_sweep_profile.argtypes = [vp, i32, vp]
+    lib.qp_ipm_last_system.argtypes = [vp, vp, vp, C.POINTER(dbl)]
+    lib.qp_launch_count.argtypes = [vp]
+    lib.qp_launch_count.restype = i64
     lib.qp_last_error.argtypes = [vp]
     lib.qp_last_error.restype = C.c_char_p
     lib.qp_free.argtypes = [vp]
@@ -275,6 +278,15 @@ class QPSolver:
         out = np.zeros(50, dtype=np.int64)
         self._check(self.lib.qp_debug_sweep_profile(self.ctx, 1 if enable else 0, out.ctypes.data))
         return out.reshape(2, 5, 5)
+
+    def ipm_last_system(self):
+        D, r = np.zeros(self.m2), np.zeros(self.m2)
+        eps = C.c_double()
+        self._check(self.lib.qp_ipm_last_system(self.ctx, D.ctypes.data, r.ctypes.data, C.byref(eps)))
+        return D, r, float(eps.value)
+
+    def launch_count(self):
+        return int(self.lib.qp_launch_count(self.ctx))
 
     def stats(self):
         s = _Stats()

@@ -183,6 +183,8 @@ struct qp_ctx {
   bool ph_valid = false;
   double t_factor_ph = 0;
   int64_t ph_refactors = 0;
+  int64_t launches = 0;           // kernel launches issued by this context
+  double last_eps = 0;            // PCG tolerance of the last IPM iteration
 
   // vectors
   double *xl = nullptr, *nu = nullptr, *s = nullptr;          // iterate (x_f; λ), ν, s
@@ -514,6 +516,7 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
 
 // y = F⁻¹ rhs (factor order, N), forward + backward sweeps.
 void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
+  c->launches += 2;
   SweepRhs r{};
   r.rhs = rhs_f;
   int h = c->begin(0);
@@ -526,6 +529,7 @@ void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
 
 // q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
 void kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode) {
+  c->launches += 3;
   SweepRhs r{};
   r.ct = c->Ctf;
   r.p = p;
@@ -543,6 +547,7 @@ void kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool p
 
 // z = P_H⁻¹ r (a7), P_H factor order via perm_ph.
 void ph_apply_dev(qp_ctx* c, const double* r, double* z, const int* done) {
+  c->launches += 3;
   SweepRhs sr{};
   sr.rhs = r;
   sr.in_perm = c->perm_ph_dev;
@@ -580,9 +585,11 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   int h = c->begin(3);
   pcg_init(prec, m2, b, D, c->px, c->pr, c->pz, c->pp, c->partial, c->pst, tol, maxit, c->vgrid, st);
   c->end(h);
+  c->launches += 1;
   if (prec == 2) {
     ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
     pcg_init_ph(m2, c->pr, c->pz, c->pp, c->partial, c->pst, c->vgrid, st);
+    c->launches += 1;
   }
   int chunk = 2;
   for (int it = 0; it < maxit + 1;) {
@@ -598,6 +605,7 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
       h = c->begin(3);
       pcg_update2(m2, c->pz, c->pp, c->pst, c->vgrid, st);
       c->end(h);
+      c->launches += prec == 2 ? 3 : 2;
     }
     it += chunk;
     cudaMemcpyAsync(c->h_pst, c->pst, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
@@ -629,7 +637,7 @@ std::string analyse_F(qp_ctx* c) {
         if (c->H.i[q] != r) idx.push_back(c->H.i[q]);
       ptr[r + 1] = (int64_t)idx.size();
     }
-    c->perm = min_degree_order(n, ptr, idx);
+    c->perm = etree_postorder(n, ptr, idx, min_degree_order(n, ptr, idx));
   }
   LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(), c->A.i.data(),
                                 c->A.v.data(), c->perm);
@@ -667,6 +675,7 @@ int ipm_iteration(qp_ctx* c, bool* converged) {
   ipm_residuals(c->Hf, c->Atf, c->Ctf, c->Af, c->Cf, c->gf, c->bv, c->dv, c->xl, c->xl + n, c->nu, c->s, c->rgre,
                 c->rc, c->ra, c->Dk, c->partial, c->ist, c->vgrid, st);
   c->end(h);
+  c->launches += 2;
   cudaMemcpyAsync(c->h_ist, c->ist, sizeof(IpmState), cudaMemcpyDeviceToHost, st);
   int rc = sync_check(c, "ipm residuals");
   if (rc) return rc;
@@ -685,6 +694,8 @@ int ipm_iteration(qp_ctx* c, bool* converged) {
   c->end(h);
   // PCG (reading R4 forcing)
   double eps = c->opts.pcg_forcing ? std::min(c->opts.pcg_tol, S.mu) : c->opts.pcg_tol;
+  c->last_eps = eps;
+  c->launches += 1 + 1 + 2;   // r_nu, recovery rhs, ds/alpha + update
   int iters = 0;
   rc = pcg_dev(c, c->Dk, c->rnu, eps, c->opts.pcg_maxit, &iters, nullptr, true);
   if (rc != QP_OK && rc != QP_MAXIT) return rc;
@@ -953,7 +964,7 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
           if (ti[q] != r) idx.push_back(ti[q]);
         ptr[r + 1] = (int64_t)idx.size();
       }
-      c->perm_ph = min_degree_order(m2, ptr, idx);
+      c->perm_ph = etree_postorder(m2, ptr, idx, min_degree_order(m2, ptr, idx));
     }
     std::vector<int64_t> pinv_ph(m2);
     for (int64_t i = 0; i < m2; ++i) pinv_ph[c->perm_ph[i]] = i;
@@ -1218,6 +1229,18 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
   }
   return QP_OK;
 }
+
+int qp_ipm_last_system(qp_ctx* c, double* D, double* rnu, double* eps) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  if (c->ipm_k == 0) return fail(c, QP_ESTATE, "no IPM iteration has run");
+  out_vec(c, D, c->Dk, c->m2);
+  out_vec(c, rnu, c->rnu, c->m2);
+  if (eps) *eps = c->last_eps;
+  return sync_check(c, "qp_ipm_last_system");
+}
+
+int64_t qp_launch_count(const qp_ctx* c) { return c ? c->launches : -1; }
 
 int qp_profile(qp_ctx* c, int32_t enable) {
   if (!c) return QP_EINVAL;

@@ -642,3 +642,72 @@ std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr
 }
 
 }  // namespace qpb
+
+namespace qpb {
+
+// Postorder the elimination tree of the symmetric pattern (ptr, idx) under the
+// ordering `order` (new→old): an equivalent reordering (same fill) that makes
+// every last child contiguous with its parent, so chains of supernodes can be
+// amalgamated.  Returns the composed order (new→old).
+std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
+                                     const std::vector<int64_t>& order) {
+  std::vector<int64_t> pinv(n);
+  for (int64_t i = 0; i < n; ++i) pinv[order[i]] = i;
+  std::vector<int64_t> parent(n, -1), anc(n, -1);
+  // Liu's algorithm over rows of the permuted lower triangle
+  std::vector<int64_t> rp(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q)
+      if (pinv[idx[q]] < pinv[i]) rp[pinv[i] + 1]++;
+  for (int64_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
+  std::vector<int64_t> rc(rp[n]);
+  {
+    std::vector<int64_t> pos(rp.begin(), rp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q)
+        if (pinv[idx[q]] < pinv[i]) rc[pos[pinv[i]]++] = pinv[idx[q]];
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+      int64_t r = rc[q];
+      while (anc[r] != -1 && anc[r] != i) {
+        int64_t t = anc[r];
+        anc[r] = i;
+        r = t;
+      }
+      if (anc[r] == -1) {
+        anc[r] = i;
+        parent[r] = i;
+      }
+    }
+  // children lists (increasing), iterative DFS from roots in increasing order
+  std::vector<int64_t> head(n, -1), next(n, -1);
+  for (int64_t j = n - 1; j >= 0; --j)
+    if (parent[j] >= 0) {
+      next[j] = head[parent[j]];
+      head[parent[j]] = j;
+    }
+  std::vector<int64_t> post;
+  post.reserve(n);
+  std::vector<int64_t> stack;
+  for (int64_t r = 0; r < n; ++r) {
+    if (parent[r] >= 0) continue;
+    stack.push_back(r);
+    while (!stack.empty()) {
+      int64_t p = stack.back();
+      int64_t c = head[p];
+      if (c >= 0) {
+        head[p] = next[c];
+        stack.push_back(c);
+      } else {
+        stack.pop_back();
+        post.push_back(p);
+      }
+    }
+  }
+  std::vector<int64_t> out(n);
+  for (int64_t k = 0; k < n; ++k) out[k] = order[post[k]];
+  return out;
+}
+
+}  // namespace qpb

@@ -117,6 +117,10 @@ LowerMatrix build_F_lower(int64_t n, int64_t m1, const int64_t* Hp, const int32_
 std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr,
                                       const std::vector<int32_t>& idx);
 
+// Equivalent reordering by an elimination-tree postorder (same fill), composed with `order`.
+std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
+                                     const std::vector<int64_t>& order);
+
 // Full symbolic analysis + multifrontal / trsv plans.  Returns "" or an error.
 std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative);
 
