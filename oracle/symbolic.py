@@ -12,8 +12,8 @@ same x-block permutation:
 * column counts cc(j) = |struct(L[:,j])| (diagonal included);
 * fundamental supernodes: column j joins j−1's supernode iff
   parent(j−1) = j and cc(j−1) = cc(j) + 1 (then struct(j−1) = {j−1} ∪ struct(j));
-* relaxed amalgamation, in increasing supernode
-  order: merge J into its parent P when J's columns end right before P's and
+* relaxed amalgamation, repeated passes in increasing
+  supernode order until no merge happens: merge J into its parent P when J's columns end right before P's and
   the merged block's explicit zeros are small — merged width w ≤ 4, or
   w ≤ 16 and zeros ≤ 80 %, or w ≤ 48 and zeros ≤ 10 %, or zeros ≤ 5 % of
   the stored w·m − w(w−1)/2 entries (m = w_J + m_P rows);  a relaxed
@@ -100,18 +100,34 @@ def relax(parent, cc, struct, fstart):
     m = [w[J] + len(below[J]) for J in range(nf)]
     true = [int(cc[fstart[J]:fstart[J + 1]].sum()) for J in range(nf)]
     alive = [True] * nf
-    for J in range(nf):
-        P = fpar[J]
-        if P < 0 or c0[J] + w[J] != c0[P]:
-            continue
-        ww = w[J] + w[P]
-        mm = w[J] + m[P]
-        stored = ww * mm - ww * (ww - 1) // 2
-        zeros = stored - (true[J] + true[P])
-        if ww <= 4 or (ww <= 16 and 100 * zeros <= 80 * stored) or (ww <= 48 and 100 * zeros <= 10 * stored) \
-                or 100 * zeros <= 5 * stored:
-            c0[P], w[P], m[P], true[P] = c0[J], ww, mm, true[P] + true[J]
-            alive[J] = False
+    # passes over the current partition until no merge happens
+    while True:
+        own = np.empty(N, dtype=np.int64)
+        for J in range(nf):
+            if alive[J]:
+                own[c0[J]:c0[J] + w[J]] = J
+        merged = 0
+        for J in range(nf):
+            if not alive[J]:
+                continue
+            pc = parent[c0[J] + w[J] - 1]
+            if pc < 0:
+                continue
+            P = int(own[pc])
+            if not alive[P] or c0[J] + w[J] != c0[P]:
+                continue
+            ww = w[J] + w[P]
+            mm = w[J] + m[P]
+            stored = ww * mm - ww * (ww - 1) // 2
+            zeros = stored - (true[J] + true[P])
+            if ww <= 4 or (ww <= 16 and 100 * zeros <= 80 * stored) or (ww <= 48 and 100 * zeros <= 10 * stored) \
+                    or 100 * zeros <= 5 * stored:
+                c0[P], w[P], m[P], true[P] = c0[J], ww, mm, true[P] + true[J]
+                alive[J] = False
+                own[c0[P]:c0[P] + w[P]] = P
+                merged += 1
+        if merged == 0:
+            break
     starts = [c0[J] for J in range(nf) if alive[J]] + [N]
     rows = [np.concatenate([np.arange(c0[J], c0[J] + w[J]), below[J]]).astype(np.int64)
             for J in range(nf) if alive[J]]

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <functional>
 #include <memory>
 #include <string>
@@ -637,7 +638,8 @@ std::string analyse_F(qp_ctx* c) {
         if (c->H.i[q] != r) idx.push_back(c->H.i[q]);
       ptr[r + 1] = (int64_t)idx.size();
     }
-    c->perm = etree_postorder(n, ptr, idx, min_degree_order(n, ptr, idx));
+    c->perm = min_degree_order(n, ptr, idx);
+    if (!std::getenv("QPB_NO_POSTORDER")) c->perm = etree_postorder(n, ptr, idx, c->perm);
   }
   LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(), c->A.i.data(),
                                 c->A.v.data(), c->perm);
@@ -845,6 +847,7 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
     c->own_stream = true;
   }
   c->tgrid = trsv_grid(c->device);
+  if (std::getenv("QPB_VERBOSE")) std::fprintf(stderr, "qpb: trsv grid %d CTAs on %d SMs\n", c->tgrid, c->sm_count);
   cudaMallocHost(&c->h_pst, sizeof(PcgState));
   cudaMallocHost(&c->h_ist, sizeof(IpmState));
   c->gmax = 0;

@@ -36,6 +36,17 @@ __device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long lon
 __device__ __forceinline__ void st_rel_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_acqrel_add_u64(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -336,6 +347,8 @@ struct SweepShared {
   double rhs[64];
   double y[64];
   double red[4 * 64];
+  int rows[512];
+  double xr[512];
 };
 
 __device__ __forceinline__ void spin_u64(const unsigned long long* p, unsigned long long target) {
@@ -372,12 +385,22 @@ __device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int
   atomicMax(q + 4, t2);
 }
 
-// Load a R×W column-major tile (leading dimension ld) into smem with padding R+1.
+// Load a R×W column-major tile (leading dimension ld, R·W ≤ 4096) into smem with padding R+1.
 __device__ __forceinline__ void load_tile(double* sm, const double* g, int R, int W, int64_t ld) {
   const int ldp = R + 1;
-  for (int idx = threadIdx.x; idx < R * W; idx += NT) {
-    int c = idx / R, r = idx - c * R;
+  const int n = R * W;
+#pragma unroll 4
+  for (int idx = threadIdx.x; idx < n; idx += NT) {
+    const int c = idx / R, r = idx - c * R;
     sm[c * ldp + r] = __ldg(g + r + (int64_t)c * ld);
+  }
+}
+// Prefetch the lines of a R×W column-major block into L2 (fire and forget).
+__device__ __forceinline__ void prefetch_block(const double* g, int64_t R, int W, int64_t ld) {
+  const int64_t lines = (R + 15) / 16;  // 128-byte lines per column
+  for (int64_t e = threadIdx.x; e < lines * W; e += NT) {
+    const int64_t c = e / lines, l = e - c * lines;
+    prefetch_l2(g + l * 16 + c * ld);
   }
 }
 // out[r] = Σ_c T(r,c) v[c]   (T in smem, R×W, ld R+1); result for r < R in S.red[r] (after sync)
@@ -402,7 +425,7 @@ __device__ __forceinline__ void tile_gemv_t(const double* sm, int R, int W, cons
   const int ldp = R + 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int P = W >= 8 ? 1 : 8 / W;
-  __shared__ double part[64 * 8];
+  __shared__ double part[64];
   for (int it = wid; it < W * P; it += NT / 32) {
     const int c = it / P, pr = it % P;
     double s = 0.0;
@@ -545,10 +568,29 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       const int J = F.blk_sn[b];
       const int wk = F.blk_w[b];
       const int64_t c0 = F.blk_col0[b];
+      const int64_t noff = F.blk_noff[b];
+      const double* L = F.fstore + F.blk_off[b];
+      const int32_t* rows = F.sn_rows + F.blk_rows[b];
+      const int Rc = wk > 4 ? 4096 / wk : 1024;
+      // independent of the dependency: L_bb⁻¹ → smem[0, 4160); a first L chunk (≤ 2048 doubles,
+      // ≤ 512 rows) and its row indices → smem; otherwise the whole L block is prefetched into L2
+      double* Ls = sm + 4160;
       const double* inv = F.fstore + F.blk_inv[b];
       for (int i2 = tid; i2 < wk * wk; i2 += NT) {
         int c = i2 / wk, r = i2 - c * wk;
         sm[c * 65 + r] = __ldg(inv + i2);
+      }
+      const int R0 = (int)(noff < Rc ? noff : Rc);
+      const bool one_chunk = noff <= 512 && wk * (noff + 1) <= 1024;
+      if (one_chunk) {
+        for (int i2 = tid; i2 < wk * R0; i2 += NT) {
+          int c = i2 / R0, r = i2 - c * R0;
+          Ls[c * (R0 + 1) + r] = __ldg(L + r + (int64_t)c * noff);
+        }
+        for (int r = tid; r < R0; r += NT) S.rows[r] = __ldg(rows + r);
+      } else {
+        prefetch_block(L, noff, wk, noff);
+        for (int64_t r = (int64_t)tid * 32; r < noff; r += (int64_t)NT * 32) prefetch_l2(rows + r);
       }
       if (tid < wk) {
         const int64_t c = c0 + tid;
@@ -582,17 +624,29 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         x[c0 + tid] = yv;
       }
       __syncthreads();
-      const int64_t noff = F.blk_noff[b];
-      const double* L = F.fstore + F.blk_off[b];
-      const int32_t* rows = F.sn_rows + F.blk_rows[b];
-      for (int64_t r = tid; r < noff; r += NT) {
-        double s = 0.0;
-        for (int c = 0; c < wk; ++c) s += __ldg(L + r + (int64_t)c * noff) * S.y[c];
-        atomicAdd(F.acc + rows[r], s);
+      if (one_chunk) {
+        for (int r = tid; r < R0; r += NT) {
+          double s = 0.0;
+          for (int c = 0; c < wk; ++c) s += Ls[c * (R0 + 1) + r] * S.y[c];
+          atomicAdd(F.acc + S.rows[r], s);
+        }
+      } else {
+        for (int64_t r0 = 0; r0 < noff; r0 += Rc) {
+          const int Rn = (int)(noff - r0 < Rc ? noff - r0 : Rc);
+          __syncthreads();
+          load_tile(sm, L + r0, Rn, wk, noff);
+          __syncthreads();
+          for (int r = tid; r < Rn; r += NT) {
+            double s = 0.0;
+            for (int c = 0; c < wk; ++c) s += sm[c * (Rn + 1) + r] * S.y[c];
+            atomicAdd(F.acc + __ldg(rows + r0 + r), s);
+          }
+        }
       }
       __threadfence();
       __syncthreads();
-      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) atomicAdd(F.cnt_f + F.blk_dest[k], 1ull);
+      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT)
+        red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
     } else if (type == 3) {
       // ---------------- XCHUNK: x[I] += X_{I,K0..K0+nK} · v[K0..]
       const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
@@ -737,30 +791,59 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       const int J = F.blk_sn[b];
       const int wk = F.blk_w[b];
       const int64_t c0 = F.blk_col0[b];
-      double dinv = 0.0;
-      if (tid < wk) dinv = 1.0 / F.Dpiv[c0 + tid];
-      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) spin_u32(F.ready_sb + F.blk_dest[k], E);
-      if (F.tprof && tid == 0) t1 = gtime();
-      __syncthreads();
       const int64_t noff = F.blk_noff[b];
       const double* L = F.fstore + F.blk_off[b];
       const int32_t* rows = F.sn_rows + F.blk_rows[b];
-      const int Rc = wk > 4 ? 4096 / wk : 1024;
-      double tsum = 0.0;
-      for (int64_t r0 = 0; r0 < noff; r0 += Rc) {
-        const int Rn = (int)(noff - r0 < Rc ? noff - r0 : Rc);
-        load_tile(sm, L + r0, Rn, wk, noff);
-        double* xr = sm + wk * (Rn + 1);
-        for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r0 + r]);
-        __syncthreads();
-        tile_gemv_t(sm, Rn, wk, xr, S.red);
-        if (tid < wk) tsum += S.red[tid];
-        __syncthreads();
-      }
+      double dinv = 0.0;
+      if (tid < wk) dinv = 1.0 / F.Dpiv[c0 + tid];
+      // independent of the dependencies: L_bb⁻¹, a single L chunk and its row indices → smem
+      const bool one_chunk = noff <= 512 && wk * (noff + 1) <= 1024;
+      const int R0 = (int)noff;
+      double* Ls = sm + 4160;
       const double* inv = F.fstore + F.blk_inv[b];
       for (int i2 = tid; i2 < wk * wk; i2 += NT) {
         int c = i2 / wk, r = i2 - c * wk;
         sm[c * 65 + r] = __ldg(inv + i2);
+      }
+      if (one_chunk) {
+        for (int i2 = tid; i2 < wk * R0; i2 += NT) {
+          int c = i2 / R0, r = i2 - c * R0;
+          Ls[c * (R0 + 1) + r] = __ldg(L + r + (int64_t)c * noff);
+        }
+        for (int r = tid; r < R0; r += NT) S.rows[r] = __ldg(rows + r);
+      } else {
+        prefetch_block(L, noff, wk, noff);
+        for (int64_t r = (int64_t)tid * 32; r < noff; r += (int64_t)NT * 32) prefetch_l2(rows + r);
+      }
+      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) spin_u32(F.ready_sb + F.blk_dest[k], E);
+      if (F.tprof && tid == 0) t1 = gtime();
+      __syncthreads();
+      double tsum = 0.0;
+      if (one_chunk) {
+        for (int r = tid; r < R0; r += NT) S.xr[r] = __ldcg(x + S.rows[r]);
+        __syncthreads();
+        tile_gemv_t(Ls, R0, wk, S.xr, S.red);
+        if (tid < wk) tsum = S.red[tid];
+        __syncthreads();
+      } else {
+        double* Lc = sm + 4160;   // chunk tiles must not overwrite L_bb⁻¹: use a second pass below
+        (void)Lc;
+        const int Rc = wk > 4 ? 4096 / wk : 1024;
+        for (int64_t r0 = 0; r0 < noff; r0 += Rc) {
+          const int Rn = (int)(noff - r0 < Rc ? noff - r0 : Rc);
+          __syncthreads();
+          load_tile(sm, L + r0, Rn, wk, noff);
+          double* xr = sm + wk * (Rn + 1);
+          for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + __ldg(rows + r0 + r));
+          __syncthreads();
+          tile_gemv_t(sm, Rn, wk, xr, S.red);
+          if (tid < wk) tsum += S.red[tid];
+        }
+        __syncthreads();
+        for (int i2 = tid; i2 < wk * wk; i2 += NT) {
+          int c = i2 / wk, r = i2 - c * wk;
+          sm[c * 65 + r] = __ldg(inv + i2);
+        }
       }
       if (tid < wk) S.rhs[tid] = __ldcg(x + c0 + tid) * dinv - tsum;
       __syncthreads();
@@ -967,7 +1050,7 @@ void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t m
   k_build_xinv<<<grid, NT, 0, s>>>(F, big_sns, n_big);
 }
 
-static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)(TRSV_SMEM_DBL + 1024); }
+static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)TRSV_SMEM_DBL; }
 
 int trsv_grid(int device) {
   static int cached[64] = {0};

@@ -7,7 +7,7 @@ namespace qpb {
 
 constexpr int NT = 256;            // threads per CTA for every kernel here
 constexpr int MF_BW = 64;          // pivot block (must equal symbolic BW)
-constexpr int TRSV_SMEM_DBL = 4096 + 1088;  // tile (≤4096 + padding) or Linv (64×65)
+constexpr int TRSV_SMEM_DBL = 4096 + 64 + 1024;  // tile R×W ≤ 4096 with R+1 padding + gathered x (≤1024); Linv 64×65 + 1024
 
 // One factor (F or P_H): symbolic plan + numeric storage + trsv sweep state.
 struct DevFactor {

@@ -191,21 +191,38 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
     for (int64_t c = fs_start[J]; c < fs_start[J + 1]; ++c) t += S.colcount[c];
     rtrue[J] = t;
   }
-  for (int64_t J = 0; J < nf; ++J) {
-    const int64_t P = fparent[J];
-    if (P < 0 || rc0[J] + rw[J] != rc0[P]) continue;
-    const int64_t w = rw[J] + rw[P];
-    const int64_t m = rw[J] + rm[P];
-    const int64_t stored = w * m - w * (w - 1) / 2;
-    const int64_t zeros = stored - (rtrue[J] + rtrue[P]);
-    bool merge = w <= 4 || (w <= 16 && 100 * zeros <= 80 * stored) || (w <= 48 && 100 * zeros <= 10 * stored) ||
-                 (100 * zeros <= 5 * stored);
-    if (!merge) continue;
-    rc0[P] = rc0[J];
-    rw[P] = w;
-    rm[P] = m;
-    rtrue[P] += rtrue[J];
-    alive[J] = 0;
+  // passes over the current partition until no merge happens (a merged parent may now be
+  // contiguous with, and cheap enough for, its own parent)
+  {
+    std::vector<int64_t> colown(N);
+    while (true) {
+      for (int64_t J = 0; J < nf; ++J)
+        if (alive[J])
+          for (int64_t c = rc0[J]; c < rc0[J] + rw[J]; ++c) colown[c] = J;
+      int64_t merged = 0;
+      for (int64_t J = 0; J < nf; ++J) {
+        if (!alive[J]) continue;
+        const int64_t pc = S.parent[rc0[J] + rw[J] - 1];
+        if (pc < 0) continue;
+        const int64_t P = colown[pc];
+        if (!alive[P] || rc0[J] + rw[J] != rc0[P]) continue;
+        const int64_t w = rw[J] + rw[P];
+        const int64_t m = rw[J] + rm[P];
+        const int64_t stored = w * m - w * (w - 1) / 2;
+        const int64_t zeros = stored - (rtrue[J] + rtrue[P]);
+        bool merge = w <= 4 || (w <= 16 && 100 * zeros <= 80 * stored) || (w <= 48 && 100 * zeros <= 10 * stored) ||
+                     (100 * zeros <= 5 * stored);
+        if (!merge) continue;
+        rc0[P] = rc0[J];
+        rw[P] = w;
+        rm[P] = m;
+        rtrue[P] += rtrue[J];
+        alive[J] = 0;
+        for (int64_t c = rc0[J]; c < rc0[J] + rw[J]; ++c) colown[c] = P;
+        ++merged;
+      }
+      if (merged == 0) break;
+    }
   }
   // relaxed partition (alive supernodes, in column order)
   S.sn_start.clear();
