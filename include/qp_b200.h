@@ -128,6 +128,7 @@ typedef struct {
   int32_t pcg_total;        /* Σ n_kr */
   double t_setup_s, t_solve_s;
   double mu, rg_inf, re_inf, ri_inf; /* final μ and residual ∞-norms */
+  double alpha;             /* step length of the last IPM iteration */
 } qp_ipm_result;
 
 /* The inexact IPM (readings R1–R4): start x=0, λ=0, ν=1,

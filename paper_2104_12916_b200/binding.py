@@ -55,7 +55,7 @@ class _IpmResult(C.Structure):
                 ("objective", C.c_double), ("n_ipm", C.c_int32), ("pcg_iters", C.c_void_p),
                 ("status", C.c_int32), ("pcg_total", C.c_int32), ("t_setup_s", C.c_double),
                 ("t_solve_s", C.c_double), ("mu", C.c_double), ("rg_inf", C.c_double),
-                ("re_inf", C.c_double), ("ri_inf", C.c_double)]
+                ("re_inf", C.c_double), ("ri_inf", C.c_double), ("alpha", C.c_double)]
 
 
 class _Stats(C.Structure):
@@ -228,7 +228,8 @@ class QPSolver:
     def _pack(r, bufs, it):
         out = dict(objective=r.objective, n_ipm=r.n_ipm, status=r.status, pcg_total=r.pcg_total,
                    t_setup_s=r.t_setup_s, t_solve_s=r.t_solve_s, mu=r.mu, rg_inf=r.rg_inf,
-                   re_inf=r.re_inf, ri_inf=r.ri_inf, pcg_iters=it[:min(r.n_ipm, len(it))].tolist())
+                   re_inf=r.re_inf, ri_inf=r.ri_inf, alpha=r.alpha,
+                   pcg_iters=it[:min(r.n_ipm, len(it))].tolist())
         out.update(bufs)
         return out
 

@@ -743,6 +743,7 @@ void fill_result(qp_ctx* c, qp_ipm_result* r) {
   r->rg_inf = c->h_ist->rg_inf;
   r->re_inf = c->h_ist->re_inf;
   r->ri_inf = c->h_ist->ri_inf;
+  r->alpha = c->h_ist->alpha;
 }
 
 }  // namespace
