@@ -395,6 +395,9 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.asm_src = m.upload(S.asm_src, st);
     d.n_asm = (int64_t)S.asm_dst.size();
     d.diag_dst = m.upload(S.diag_dst, st);
+    d.asm_diag = m.upload(S.asm_diag, st);
+    d.lev_fronts = m.upload(S.lev_fronts, st);
+    d.lev_zpref = m.upload(S.lev_zpref, st);
     d.relind = m.upload(S.relind, st);
     d.relind_off = m.upload(S.relind_off, st);
     d.grp_P = m.upload(S.grp_P, st);
@@ -490,12 +493,12 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
                    const char* what) {
   cudaStream_t st = c->stream;
   const Symbolic& S = F.S;
-  cudaMemsetAsync(F.d.ws, 0, (size_t)S.ws_size * 8, st);
   cudaMemsetAsync(F.d.status, 0, sizeof(int), st);
-  mf_assemble(F.d, src_vals, st);
-  if (D) mf_assemble_diag_add(F.d, D, dperm, st);
   size_t si = 0;
   for (int64_t L = 0; L < S.n_levels; ++L) {
+    const LevelEA& le = S.level_ea[L];
+    mf_assemble_level(F.d, le.fr_off, le.n_fr, S.lev_zpref[le.fr_off + le.n_fr], le.asm_off, le.n_asm, src_vals, D,
+                      dperm, st);
     mf_extend_add(F.d, S.level_ea[L].grp_off, S.level_ea[L].n_grp, st);
     while (si < S.steps.size() && S.steps[si].level == L) {
       const StepDesc& sd = S.steps[si];

@@ -115,20 +115,29 @@ __device__ __forceinline__ int find_seg(const int64_t* pref, int n, int64_t x) {
 }
 
 // ------------------------------------------------------------------------- multifrontal
-__global__ void k_mf_assemble(DevFactor F, const double* src_vals) {
-  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < F.n_asm; e += (int64_t)gridDim.x * NT) {
+__global__ void k_mf_zero_fronts(DevFactor F, int64_t fr_off, int n_fr, int64_t total) {
+  const int32_t* fr = F.lev_fronts + fr_off;
+  const int64_t* zp = F.lev_zpref + fr_off;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int a = find_seg(zp, n_fr + 1, e);
+    F.ws[F.front_off[fr[a]] + (e - zp[a])] = 0.0;
+  }
+}
+
+__global__ void k_mf_assemble(DevFactor F, int64_t off, int64_t n, const double* src_vals, const double* D,
+                              const int64_t* perm) {
+  for (int64_t e = off + blockIdx.x * (int64_t)NT + threadIdx.x; e < off + n; e += (int64_t)gridDim.x * NT) {
     double v = F.asm_val[e];
     if (src_vals != nullptr) {
       int64_t s = F.asm_src[e];
       v = s >= 0 ? src_vals[s] : 0.0;
     }
+    if (D != nullptr) {
+      const int32_t c = F.asm_diag[e];
+      if (c >= 0) v += D[perm[c]];
+    }
     F.ws[F.asm_dst[e]] = v;
   }
-}
-
-__global__ void k_mf_diag_add(DevFactor F, const double* D, const int64_t* perm) {
-  for (int64_t c = blockIdx.x * (int64_t)NT + threadIdx.x; c < F.N; c += (int64_t)gridDim.x * NT)
-    F.ws[F.diag_dst[c]] += D[perm[c]];
 }
 
 // One warp per (parent front, parent column) group; children in fixed order.
@@ -309,14 +318,16 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t ac
   }
 }
 
-void mf_assemble(const DevFactor& F, const double* src_vals, cudaStream_t s) {
-  if (F.n_asm == 0) return;
-  int grid = (int)std::min<int64_t>((F.n_asm + NT - 1) / NT, 148 * 16);
-  k_mf_assemble<<<grid, NT, 0, s>>>(F, src_vals);
-}
-void mf_assemble_diag_add(const DevFactor& F, const double* D, const int64_t* perm, cudaStream_t s) {
-  int grid = (int)std::min<int64_t>((F.N + NT - 1) / NT, 148 * 16);
-  k_mf_diag_add<<<grid, NT, 0, s>>>(F, D, perm);
+void mf_assemble_level(const DevFactor& F, int64_t fr_off, int64_t n_fr, int64_t zero_total, int64_t asm_off,
+                       int64_t n_asm, const double* src_vals, const double* D, const int64_t* perm, cudaStream_t s) {
+  if (zero_total > 0) {
+    int grid = (int)std::min<int64_t>((zero_total + NT - 1) / NT, 148 * 16);
+    k_mf_zero_fronts<<<grid, NT, 0, s>>>(F, fr_off, (int)n_fr, zero_total);
+  }
+  if (n_asm > 0) {
+    int grid = (int)std::min<int64_t>((n_asm + NT - 1) / NT, 148 * 16);
+    k_mf_assemble<<<grid, NT, 0, s>>>(F, asm_off, n_asm, src_vals, D, perm);
+  }
 }
 void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s) {
   if (n_grp == 0) return;

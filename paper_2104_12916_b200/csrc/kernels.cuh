@@ -77,6 +77,9 @@ struct DevFactor {
   const int64_t* asm_src;
   int64_t n_asm;
   const int64_t* diag_dst;
+  const int32_t* asm_diag;
+  const int32_t* lev_fronts;
+  const int64_t* lev_zpref;
   const int32_t* relind;
   const int64_t* relind_off;
   const int32_t* grp_P;
@@ -118,8 +121,9 @@ struct IpmState {
 };
 
 // ---- multifrontal factorization
-void mf_assemble(const DevFactor& F, const double* src_vals, cudaStream_t s);
-void mf_assemble_diag_add(const DevFactor& F, const double* D, const int64_t* perm, cudaStream_t s);
+// zero the fronts of one level, then scatter its original entries (+ D on the diagonal for P_H)
+void mf_assemble_level(const DevFactor& F, int64_t fr_off, int64_t n_fr, int64_t zero_total, int64_t asm_off,
+                       int64_t n_asm, const double* src_vals, const double* D, const int64_t* perm, cudaStream_t s);
 void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s);
 void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
              int64_t upd_total, cudaStream_t s);

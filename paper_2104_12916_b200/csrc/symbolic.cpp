@@ -265,14 +265,60 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
     const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
     S.nnz_stored += w * m - w * (w - 1) / 2;
   }
-  // ---------------------------------------------------------------- fronts
+  // ---------------------------------------------------------------- fronts: liveness-based memory plan
+  // Levels are factored bottom-up; the fronts of level L are allocated before level L
+  // (first fit), and a front is released once its parent's level has extend-added it.
+  std::vector<std::vector<int32_t>> by_level(S.n_levels);
+  for (int64_t J = 0; J < ns; ++J) by_level[S.sn_level[J]].push_back((int32_t)J);
   S.front_off.assign(ns, 0);
   S.ws_size = 0;
-  for (int64_t J = 0; J < ns; ++J) {
-    int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
-    S.front_off[J] = S.ws_size;
-    S.ws_size += m * m;
-    S.ws_size = (S.ws_size + 1) & ~int64_t(1);
+  S.ws_naive = 0;
+  {
+    std::vector<std::pair<int64_t, int64_t>> freel;  // (offset, size), sorted by offset
+    int64_t top = 0;
+    auto alloc = [&](int64_t sz) -> int64_t {
+      for (size_t i = 0; i < freel.size(); ++i)
+        if (freel[i].second >= sz) {
+          int64_t off = freel[i].first;
+          freel[i].first += sz;
+          freel[i].second -= sz;
+          if (freel[i].second == 0) freel.erase(freel.begin() + i);
+          return off;
+        }
+      int64_t off = top;
+      top += sz;
+      return off;
+    };
+    auto release = [&](int64_t off, int64_t sz) {
+      auto it = std::lower_bound(freel.begin(), freel.end(), std::make_pair(off, (int64_t)0));
+      it = freel.insert(it, {off, sz});
+      size_t i = it - freel.begin();
+      if (i + 1 < freel.size() && freel[i].first + freel[i].second == freel[i + 1].first) {
+        freel[i].second += freel[i + 1].second;
+        freel.erase(freel.begin() + i + 1);
+      }
+      if (i > 0 && freel[i - 1].first + freel[i - 1].second == freel[i].first) {
+        freel[i - 1].second += freel[i].second;
+        freel.erase(freel.begin() + i);
+      }
+      if (!freel.empty() && freel.back().first + freel.back().second == top) {
+        top = freel.back().first;
+        freel.pop_back();
+      }
+    };
+    auto fsize = [&](int64_t J) {
+      const int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+      return (m * m + 1) & ~int64_t(1);
+    };
+    for (int64_t L = 0; L < S.n_levels; ++L) {
+      for (int32_t J : by_level[L]) {
+        S.front_off[J] = alloc(fsize(J));
+        S.ws_size = std::max(S.ws_size, top);
+        S.ws_naive += fsize(J);
+      }
+      for (int32_t J : by_level[L])
+        for (int32_t K : children[J]) release(S.front_off[K], fsize(K));
+    }
   }
   // ---------------------------------------------------------------- blocks + factor storage
   S.sn_blk0.assign(ns + 1, 0);
@@ -440,50 +486,68 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
       for (int64_t x = sn_xb0[J]; x < sn_xb0[J + 1]; ++x) S.bwd_tasks.push_back(enc(3, x));
     }
   }
-  // ---------------------------------------------------------------- assembly map, relative indices
+  // ---------------------------------------------------------------- assembly map (grouped by level), relative indices
   S.asm_dst.clear();
   S.asm_val.clear();
   S.asm_src.clear();
+  S.asm_diag.clear();
   S.diag_dst.assign(N, 0);
   S.relind.clear();
   S.relind_off.assign(ns, -1);
+  S.level_ea.assign(S.n_levels, LevelEA{0, 0, 0, 0, 0, 0});
+  S.lev_fronts.clear();
+  S.lev_zpref.clear();
   {
     std::vector<int32_t> posmap(N, -1);
-    for (int64_t J = 0; J < ns; ++J) {
-      const int64_t c0 = S.sn_start[J], c1 = S.sn_start[J + 1];
-      const int64_t r0 = S.sn_rowptr[J], m = S.sn_rowptr[J + 1] - r0;
-      for (int64_t q = 0; q < m; ++q) posmap[S.sn_rows[r0 + q]] = (int32_t)q;
-      for (int64_t c = c0; c < c1; ++c) {
-        const int64_t colbase = S.front_off[J] + (c - c0) * m;
-        S.diag_dst[c] = colbase + posmap[c];
-        S.asm_dst.push_back(colbase + posmap[c]);
-        S.asm_val.push_back(M.diag.empty() ? 0.0 : M.diag[c]);
-        S.asm_src.push_back(M.diag_src.empty() ? -1 : M.diag_src[c]);
-        for (int64_t q = M.colptr[c]; q < M.colptr[c + 1]; ++q) {
-          S.asm_dst.push_back(colbase + posmap[M.rowind[q]]);
-          S.asm_val.push_back(M.val.empty() ? 0.0 : M.val[q]);
-          S.asm_src.push_back(M.src.empty() ? -1 : M.src[q]);
-        }
+    for (int64_t L = 0; L < S.n_levels; ++L) {
+      S.level_ea[L].asm_off = (int64_t)S.asm_dst.size();
+      S.level_ea[L].fr_off = (int64_t)S.lev_zpref.size();
+      S.level_ea[L].n_fr = (int64_t)by_level[L].size();
+      int64_t zacc = 0;
+      for (int32_t J : by_level[L]) {
+        S.lev_fronts.push_back(J);
+        S.lev_zpref.push_back(zacc);
+        const int64_t mJ = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+        zacc += mJ * mJ;
       }
-      for (int32_t K : children[J]) {
-        const int64_t k0 = S.sn_rowptr[K], mK = S.sn_rowptr[K + 1] - k0;
-        const int64_t wK = S.sn_start[K + 1] - S.sn_start[K];
-        S.relind_off[K] = (int64_t)S.relind.size();
-        for (int64_t q = wK; q < mK; ++q) {
-          int32_t p = posmap[S.sn_rows[k0 + q]];
-          if (p < 0) return "child row missing from parent front (internal error)";
-          S.relind.push_back(p);
+      S.lev_fronts.push_back(-1);   // keeps lev_fronts aligned with lev_zpref
+      S.lev_zpref.push_back(zacc);
+      for (int32_t J : by_level[L]) {
+        const int64_t c0 = S.sn_start[J], c1 = S.sn_start[J + 1];
+        const int64_t r0 = S.sn_rowptr[J], m = S.sn_rowptr[J + 1] - r0;
+        for (int64_t q = 0; q < m; ++q) posmap[S.sn_rows[r0 + q]] = (int32_t)q;
+        for (int64_t c = c0; c < c1; ++c) {
+          const int64_t colbase = S.front_off[J] + (c - c0) * m;
+          S.diag_dst[c] = colbase + posmap[c];
+          S.asm_dst.push_back(colbase + posmap[c]);
+          S.asm_val.push_back(M.diag.empty() ? 0.0 : M.diag[c]);
+          S.asm_src.push_back(M.diag_src.empty() ? -1 : M.diag_src[c]);
+          S.asm_diag.push_back((int32_t)c);
+          for (int64_t q = M.colptr[c]; q < M.colptr[c + 1]; ++q) {
+            S.asm_dst.push_back(colbase + posmap[M.rowind[q]]);
+            S.asm_val.push_back(M.val.empty() ? 0.0 : M.val[q]);
+            S.asm_src.push_back(M.src.empty() ? -1 : M.src[q]);
+            S.asm_diag.push_back(-1);
+          }
         }
+        for (int32_t K : children[J]) {
+          const int64_t k0 = S.sn_rowptr[K], mK = S.sn_rowptr[K + 1] - k0;
+          const int64_t wK = S.sn_start[K + 1] - S.sn_start[K];
+          S.relind_off[K] = (int64_t)S.relind.size();
+          for (int64_t q = wK; q < mK; ++q) {
+            int32_t p = posmap[S.sn_rows[k0 + q]];
+            if (p < 0) return "child row missing from parent front (internal error)";
+            S.relind.push_back(p);
+          }
+        }
+        for (int64_t q = 0; q < m; ++q) posmap[S.sn_rows[r0 + q]] = -1;
       }
-      for (int64_t q = 0; q < m; ++q) posmap[S.sn_rows[r0 + q]] = -1;
+      S.level_ea[L].n_asm = (int64_t)S.asm_dst.size() - S.level_ea[L].asm_off;
     }
   }
   // ---------------------------------------------------------------- levels: extend-add groups and steps
-  std::vector<std::vector<int32_t>> by_level(S.n_levels);
-  for (int64_t J = 0; J < ns; ++J) by_level[S.sn_level[J]].push_back((int32_t)J);
   S.grp_P.clear(); S.grp_pc.clear(); S.grp_K.clear(); S.grp_j.clear();
   S.grp_ptr.assign(1, 0);
-  S.level_ea.assign(S.n_levels, LevelEA{0, 0});
   S.steps.clear();
   S.act.clear();
   S.pan_pref.clear();
@@ -598,6 +662,13 @@ std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr
   for (int64_t k = 0; k < n; ++k) {
     while (mind <= n && head[mind] < 0) ++mind;
     if (mind > n) break;
+    if (mind >= n - k - 1 && n - k > 64) {
+      // every remaining variable has (approximate) external degree n-k-1: the rest is a
+      // clique, its internal order does not change the fill — append in index order
+      for (int64_t i = 0; i < n; ++i)
+        if (state[i] == 0) order.push_back(i);
+      break;
+    }
     const int64_t p = head[mind];
     remove(p);
     // new element L_p

@@ -39,6 +39,8 @@ struct StepDesc {
 
 struct LevelEA {        // extend-add groups of one level
   int64_t grp_off, n_grp;   // into grp arrays
+  int64_t asm_off, n_asm;   // assembly entries of the level's fronts
+  int64_t fr_off, n_fr;     // the level's fronts (into lev_fronts / lev_zpref)
 };
 
 struct Symbolic {
@@ -56,8 +58,11 @@ struct Symbolic {
   int64_t n_levels = 0;
 
   // fronts
-  std::vector<int64_t> front_off;  // doubles
-  int64_t ws_size = 0;             // doubles
+  std::vector<int64_t> front_off;  // doubles; fronts share memory by liveness (level schedule)
+  int64_t ws_size = 0;             // doubles (peak of the liveness plan)
+  int64_t ws_naive = 0;            // doubles if every front were allocated at once
+  std::vector<int32_t> lev_fronts; // fronts grouped by level
+  std::vector<int64_t> lev_zpref;  // per level: prefix of m² (n_fr+1 entries per level, concatenated)
 
   // blocks
   int64_t nb = 0;
@@ -94,6 +99,7 @@ struct Symbolic {
   std::vector<double> asm_val;     // F: values; P_H: T-values filled on device
   std::vector<int64_t> asm_src;    // P_H: index into device T values (-1 = none)
   std::vector<int64_t> diag_dst;   // P_H: workspace position of each diagonal (factor order)
+  std::vector<int32_t> asm_diag;   // per assembly entry: factor column if it is a diagonal entry, else -1
   std::vector<int32_t> relind;     // per child: positions in parent of rows [w, m)
   std::vector<int64_t> relind_off; // ns
   std::vector<int32_t> grp_P, grp_pc; // extend-add groups (parent sn, parent-local col)
