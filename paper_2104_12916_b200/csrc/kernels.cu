@@ -364,18 +364,18 @@ struct SweepShared {
 
 __device__ __forceinline__ void spin_u64(const unsigned long long* p, unsigned long long target) {
   if (ld_acq_u64(p) >= target) return;
-  unsigned ns = 16;
+  unsigned ns = 8;
   while (ld_acq_u64(p) < target) {
     __nanosleep(ns);
-    if (ns < 128) ns <<= 1;
+    if (ns < 64) ns <<= 1;
   }
 }
 __device__ __forceinline__ void spin_u32(const unsigned* p, unsigned target) {
   if (ld_acq_u32(p) == target) return;
-  unsigned ns = 16;
+  unsigned ns = 8;
   while (ld_acq_u32(p) != target) {
     __nanosleep(ns);
-    if (ns < 128) ns <<= 1;
+    if (ns < 64) ns <<= 1;
   }
 }
 

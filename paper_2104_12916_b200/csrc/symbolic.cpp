@@ -13,6 +13,7 @@
 #include <cmath>
 #include <numeric>
 #include <stdexcept>
+#include <cstdlib>
 
 namespace qpb {
 
@@ -379,13 +380,14 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
   }
   std::vector<int64_t> blk_tile0(S.nb + 1, 0);
   std::vector<char> fused(S.nb, 0);
+  const int64_t fuse_elems = std::getenv("QPB_FUSE_ELEMS") ? std::atoll(std::getenv("QPB_FUSE_ELEMS")) : FUSE_ELEMS;
   S.blk_dptr.assign(S.nb + 1, 0);
   S.blk_dest.clear();
   for (int64_t b = 0; b < S.nb; ++b) {
     blk_tile0[b] = (int64_t)S.tile_blk.size();
     const int64_t J = S.blk_sn[b];
     const int64_t wk = S.blk_w[b], noff = S.blk_noff[b];
-    if (!S.blk_big[b] && wk * noff <= FUSE_ELEMS) {
+    if (!S.blk_big[b] && wk * noff <= fuse_elems) {
       fused[b] = 1;
       int64_t last = -1;
       for (int64_t r = 0; r < noff; ++r) {

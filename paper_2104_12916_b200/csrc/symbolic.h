@@ -14,7 +14,7 @@ namespace qpb {
 constexpr int BW = 64;          // pivot block width (columns per trsv block column)
 constexpr int TILE_ELEMS = 4096; // max doubles in one trsv tile (32 KiB)
 constexpr int XCH = 8;           // column blocks per X chunk of a big supernode
-constexpr int FUSE_ELEMS = 32768; // small supernodes with w·noff ≤ this are swept as one task
+constexpr int FUSE_ELEMS = 2048;  // small supernodes with w·noff ≤ this are swept as one task
 constexpr int TASK_SHIFT = 28;   // task = (type << TASK_SHIFT) | index
 
 // Lower-triangular (strict) pattern + values of a symmetric matrix already in
