@@ -14,10 +14,12 @@ one-time F factorization (a12) is setup, timed and reported separately.
              buffers: pcg_solve(D_k, r_ν) replayed for the same K steps, with
              the host→device copy of (D_k, r_ν) and device→host copy of Δν in
              the timed region.
-  roofline   the L_F triangular sweeps (forward + backward; ≥ 95 % of the
-             step): algorithmic bytes 8·nnz(L_F) per sweep
-             ÷ their CUDA-event durations inside the timed region, against
-             MEASURED_PEAKS.json's HBM copy bandwidth.
+  roofline   the F-solve (forward + backward sweep kernels, ~90 % of the step):
+             the bytes one F-solve must read in this formulation — L_F outside
+             the symmetric root twice, the root's S⁻¹ lower triangle once
+              — ÷ the CUDA-event durations inside the timed
+             region, against MEASURED_PEAKS.json's HBM copy bandwidth; the
+             survey's 2·8·nnz(L_F) per F-solve is reported beside it.
   cpu_baseline  the CPU oracle (oracle/, NumPy/SciPy fp64) on the box's host
              cores: PCG iterations of IPM step 0 on the same c1 problem.
 
@@ -141,31 +143,41 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
+class OracleSampler:
+    """The CPU oracle as it stands: F factorization once, then PCG samples on IPM step 0's system."""
+
+    def __init__(self, qp, x_perm=None):
+        import numpy as np
+        from oracle import kkt
+        from oracle.fsolve import make_fsolver
+        try:
+            from threadpoolctl import threadpool_info
+            self.cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+        except Exception:
+            self.cores = os.cpu_count()
+        t0 = time.perf_counter()
+        self.qp = qp
+        self.fs = make_fsolver(qp.H, qp.A, x_perm)
+        self.t_setup = time.perf_counter() - t0
+        x, lam, nu = np.zeros(qp.n), np.zeros(qp.m1), np.ones(qp.m2)
+        s = np.abs(qp.d) + 1.0
+        res = kkt.residuals(qp, x, lam, nu, s, 0.1)
+        self.D = kkt.diag_D(s, nu)
+        self.rnu = kkt.r_nu(qp, self.fs, res)
+
+    def sample(self, iters):
+        from oracle import kkt
+        from oracle.pcg import pcg
+        t1 = time.perf_counter()
+        _, it, _, _, _ = pcg(lambda p: kkt.KF_apply(self.qp, self.fs, self.D, p), self.rnu, kkt.PrecondL(self.D),
+                             0.0, iters)
+        return it, time.perf_counter() - t1
+
+
 def cpu_oracle_sample(qp, iters, x_perm=None):
-    """Time `iters` oracle PCG iterations on IPM step 0's reduced system (oracle as it stands)."""
-    import numpy as np
-    from oracle import kkt
-    from oracle.fsolve import make_fsolver
-    from oracle.pcg import pcg
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
-    t0 = time.perf_counter()
-    fs = make_fsolver(qp.H, qp.A, x_perm)
-    t_setup = time.perf_counter() - t0
-    x = np.zeros(qp.n)
-    lam = np.zeros(qp.m1)
-    nu = np.ones(qp.m2)
-    s = np.abs(qp.d) + 1.0
-    res = kkt.residuals(qp, x, lam, nu, s, 0.1)
-    D = kkt.diag_D(s, nu)
-    rnu = kkt.r_nu(qp, fs, res)
-    t1 = time.perf_counter()
-    _, it, _, _, _ = pcg(lambda p: kkt.KF_apply(qp, fs, D, p), rnu, kkt.PrecondL(D), 0.0, iters)
-    dt = time.perf_counter() - t1
-    return it, dt, t_setup, cores
+    o = OracleSampler(qp, x_perm)
+    it, dt = o.sample(iters)
+    return it, dt, o.t_setup, o.cores
 
 
 def run_reference(args, rank, world):
@@ -174,13 +186,11 @@ def run_reference(args, rank, world):
         return
     import qpgen
     qp = qpgen.make(args.config)
-    # warm-up samples are folded into the setup (the oracle has no GPU warm-up)
+    o = OracleSampler(qp, qp.x_perm)
+    o.sample(1)                                   # warm-up
     its, dts = 0, 0.0
-    setup = None
-    cores = None
     for k in range(args.steps):
-        it, dt, t_setup, cores = cpu_oracle_sample(qp, args.cpu_iters, qp.x_perm)
-        setup = t_setup if setup is None else setup
+        it, dt = o.sample(args.cpu_iters)
         its += it
         dts += dt
     value = its / dts if dts > 0 else 0.0
@@ -190,9 +200,9 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} PL-KF (CPU oracle: dense block-inverse F-solve, textbook PCG)",
                    "n": qp.n, "m1": qp.m1, "m2": qp.m2},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": o.cores, "kind": "oracle",
                          "sample": f"{args.steps} x {args.cpu_iters} PCG iterations of IPM step 0 on {args.config} "
-                                   f"(oracle F setup {setup:.1f} s excluded)"},
+                                   f"(oracle F setup {o.t_setup:.1f} s excluded)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -301,20 +311,27 @@ def run_ours(args, rank, world, local, use_dist):
     fwd_ms, fwd_n = prof["f_fwd"]
     bwd_ms, bwd_n = prof["f_bwd"]
     n_ipm_timed = steps_done
-    real_sweeps = 2 * pcg_timed + 2 * n_ipm_timed          # K_F products + r_ν and recovery F-solves
-    sweep_bytes = 8.0 * st["nnz_LF"]
-    achieved = (real_sweeps / 2) * sweep_bytes * 2 / ((fwd_ms + bwd_ms) / 1e3) / 1e9 if fwd_ms + bwd_ms > 0 else 0
+    real_solves = pcg_timed + 2 * n_ipm_timed          # K_F products + r_ν and recovery F-solves
+    solve_ms = fwd_ms + bwd_ms
+    fsolve_bytes = st["fsolve_bytes_F"]
+    achieved = real_solves * fsolve_bytes / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0.0
+    paper_bytes = 2 * 8.0 * st["nnz_LF"]                # L_F values read twice per F-solve
     traffic = None
     if os.path.exists(args.profile_traffic):
         try:
-            traffic = json.load(open(args.profile_traffic)).get(args.config, {}).get("dram_bytes_per_sweep")
+            traffic = json.load(open(args.profile_traffic)).get(args.config, {}).get("dram_bytes_per_fsolve")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_trsv_fwd + k_trsv_bwd (L_F sweeps)", "achieved": achieved,
+    roofline = {"bound": "hbm", "kernel": "F-solve = k_trsv_fwd + k_trsv_bwd", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": peak_src, "algorithmic_bytes_per_sweep": sweep_bytes,
-                "sweep_ms_avg": (fwd_ms + bwd_ms) / max(1, real_sweeps),
-                "sweep_share_of_step": (fwd_ms + bwd_ms) / ms if ms > 0 else None}
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_fsolve": fsolve_bytes,
+                "algorithmic_bytes_note": "8*(2*nnz(L_F) outside the symmetric root + w(w+1)/2 of the root's "
+                                          "S^-1, read once per F-solve)",
+                "paper_bytes_per_fsolve": paper_bytes,
+                "paper_formulation_GBps": real_solves * paper_bytes / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0,
+                "fsolve_ms_avg": solve_ms / max(1, real_solves),
+                "fsolve_share_of_step": solve_ms / ms if ms > 0 else None}
 
     # ---------------------------------------------------------------- CPU baseline (rank 0)
     cpu = None

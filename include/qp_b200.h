@@ -183,6 +183,8 @@ typedef struct {
   double pcg_bytes_per_iter;         /* algorithmic bytes B_it */
   double pcg_flops_per_iter;         /* 2c_trsv(L_F) + 2c_spmv(C) (+2c_trsv(L_PH)) */
   double sweep_bytes_F;              /* algorithmic bytes of one L_F sweep: 8·nnz(L_F) */
+  double fsolve_bytes_F;             /* bytes one F-solve must read in this implementation: 8·(2·nnz of L_F
+                                        outside symmetric roots + w(w+1)/2 of each root's S⁻¹) */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 

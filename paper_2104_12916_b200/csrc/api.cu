@@ -123,6 +123,13 @@ struct Factor {
   int32_t* big = nullptr;
   std::vector<int32_t> big_host;
   int n_big = 0;
+  int32_t* sym = nullptr;            // symmetric roots (S⁻¹ stored)
+  std::vector<int32_t> sym_host;
+  int n_sym = 0;
+  std::vector<GemmProb> sym_plan;
+  GemmProb* sym_dev = nullptr;
+  int64_t* sym_pref_dev = nullptr;
+  int64_t sym_total = 0;
   int64_t max_w2 = 0;
   std::vector<std::vector<GemmProb>> inv_plan;   // per height: [T1 problems..., X21 problems...]
   std::vector<int> inv_split;                    // per height: number of T1 problems
@@ -362,6 +369,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.xb_nI = m.upload(S.xb_nI, st);
     d.sn_xtr = m.upload(S.sn_xtr, st);
     d.sn_ldx = m.upload(S.sn_ldx, st);
+    d.sn_sinv = m.upload(S.sn_sinv, st);
     d.sn_nblk = m.upload(S.sn_nblk, st);
     d.blk_dptr = m.upload(S.blk_dptr, st);
     d.blk_dest = m.upload(S.blk_dest, st);
@@ -389,6 +397,12 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
       F.max_w2 = mw2;
       F.big = m.upload(big, st);
       F.big_host = big;
+      std::vector<int32_t> sym;
+      for (int32_t J : big)
+        if (S.sn_sinv[J] >= 0) sym.push_back(J);
+      F.n_sym = (int)sym.size();
+      F.sym = m.upload(sym, st);
+      F.sym_host = sym;
     }
     d.asm_dst = m.upload(S.asm_dst, st);
     d.asm_val = m.upload(S.asm_val, st);
@@ -474,6 +488,23 @@ void plan_inverse(qp_ctx* c, Factor& F) {
   F.inv_pref_dev = F.mem.upload(pref, c->stream);
   F.inv_split.assign(t1.size(), 0);
   for (size_t h = 0; h < t1.size(); ++h) F.inv_split[h] = (int)t1[h].size();
+  // S_J⁻¹ = X_Jᵀ (D_J⁻¹ X_J) for the symmetric roots: lower tiles, diagonal tiles full
+  std::vector<GemmProb> sp;
+  std::vector<int64_t> spref;
+  int64_t acc = 0;
+  for (int32_t J : F.sym_host) {
+    const int64_t w = S.sn_start[J + 1] - S.sn_start[J], ldx = S.sn_ldx[J];
+    GemmProb g{F.d.xinv + S.sn_xtr[J], F.d.xinv + S.sn_xinv[J], F.d.xinv + S.sn_sinv[J], (int)w, (int)w, (int)w,
+               (int)ldx, (int)ldx, (int)ldx, 1.0, 0.0, 2 | 4 | 8, 0};
+    spref.push_back(acc);
+    acc += ((w + 63) / 64) * ((w + 63) / 64);
+    sp.push_back(g);
+  }
+  spref.push_back(acc);
+  sp.push_back(GemmProb{});
+  F.sym_total = acc;
+  F.sym_dev = F.mem.upload(sp, c->stream);
+  F.sym_pref_dev = F.mem.upload(spref, c->stream);
 }
 
 void run_inverse(qp_ctx* c, Factor& F) {
@@ -486,6 +517,10 @@ void run_inverse(qp_ctx* c, Factor& F) {
       gemm_batched(F.inv_dev + off, F.inv_pref_dev + off, F.inv_split[h], F.inv_total[g], c->stream);
     }
   transpose_xinv(F.d, F.big, F.n_big, F.max_w2, c->stream);
+  if (F.n_sym > 0) {
+    scale_xinv_rows(F.d, F.sym, F.n_sym, F.max_w2, c->stream);   // X ← D⁻¹X (X no longer needed)
+    gemm_batched(F.sym_dev, F.sym_pref_dev, F.n_sym, F.sym_total, c->stream);
+  }
 }
 
 // Numeric multifrontal factorization (assembly → per level: extend-add, blocked steps).
@@ -1233,6 +1268,7 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
                             16.0 * (double)s->nnz_LPH;
     s->pcg_flops_per_iter = 4.0 * (double)S.nnz_L + 4.0 * (double)c->C.nnz() + 4.0 * (double)s->nnz_LPH;
     s->sweep_bytes_F = 8.0 * (double)S.nnz_L;
+    s->fsolve_bytes_F = 8.0 * (2.0 * (double)(S.nnz_L - S.sym_true) + (double)S.sym_lower);
   }
   return QP_OK;
 }

@@ -501,6 +501,59 @@ __device__ __forceinline__ void xchunk_gemv(const double* __restrict__ M, int64_
   __syncthreads();
 }
 
+// Symmetric-root chunk: rows R ≤ 64 of block I, ncol columns of blocks K0..;
+// red[512 + r] = Σ_c S(r,c)·vK[c] (all columns) and colv[c] = Σ_r S(r,c)·vI[r] for c < ncol_t
+// (the columns strictly before block I).  One read of the chunk serves both products.
+__device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_t ld, int R, int ncol, int ncol_t,
+                                            const double* vK, const double* vI, double* red, double* colv) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool ok = 2 * lane < R;
+  const double2* base = reinterpret_cast<const double2*>(M + 2 * lane);
+  const int64_t ld2 = ld >> 1;
+  const double vi0 = ok ? vI[2 * lane] : 0.0, vi1 = (2 * lane + 1 < R) ? vI[2 * lane + 1] : 0.0;
+  double a0 = 0.0, a1 = 0.0;
+  int c = wid;
+  for (; c + 56 < ncol; c += 64) {
+    double2 q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = ok ? __ldg(base + (int64_t)(c + 8 * u) * ld2) : make_double2(0.0, 0.0);
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double vc = vK[c + 8 * u];
+      a0 = fma(q[u].x, vc, a0);
+      a1 = fma(q[u].y, vc, a1);
+      t[u] = q[u].x * vi0 + q[u].y * vi1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o);
+    if (lane == 0)
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c + 8 * u < ncol_t) colv[c + 8 * u] = t[u];
+  }
+  for (; c < ncol; c += 8) {
+    const double2 q = ok ? __ldg(base + (int64_t)c * ld2) : make_double2(0.0, 0.0);
+    const double vc = vK[c];
+    a0 = fma(q.x, vc, a0);
+    a1 = fma(q.y, vc, a1);
+    double t = warp_sum(q.x * vi0 + q.y * vi1);
+    if (lane == 0 && c < ncol_t) colv[c] = t;
+  }
+  red[wid * 64 + 2 * lane] = a0;
+  red[wid * 64 + 2 * lane + 1] = a1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k * 64 + threadIdx.x];
+    red[512 + threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
 // Forward sweep L y = b (unit lower L, factor order); y written to x.
 __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double* x) {
   extern __shared__ double sm[];
@@ -658,6 +711,30 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       __syncthreads();
       for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT)
         red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
+    } else if (type == 5) {
+      // ---------------- SCHUNK: symmetric root — x_I += S_IK v_K, x_K += S_IKᵀ v_I (K < I)
+      const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
+      const int J = F.blk_sn[bI];
+      const int64_t cJ = F.sn_start[J];
+      const int64_t rI = F.blk_col0[bI], cK = F.blk_col0[bK];
+      const int Rn = F.blk_w[bI];
+      const int ncol = (int)(F.blk_col0[bK + nK - 1] + F.blk_w[bK + nK - 1] - cK);
+      const int ncol_t = (int)((rI < cK + ncol ? rI : cK + ncol) - cK);   // columns before block I
+      if (tid < nK) spin_u32(F.vready_f + bK + tid, E);
+      if (tid == 64) spin_u32(F.vready_f + bI, E);
+      if (F.tprof && tid == 0) t1 = gtime();
+      __syncthreads();
+      double* vK = sm;              // ≤ 512
+      double* vI = sm + 512;        // 64
+      double* red = sm + 576;       // 8·64 + 64
+      double* colv = sm + 576 + 576;  // ≤ 512
+      for (int c = tid; c < ncol; c += NT) vK[c] = __ldcg(F.vbuf + cK + c);
+      if (tid < Rn) vI[tid] = __ldcg(F.vbuf + rI + tid);
+      __syncthreads();
+      const int64_t ldx = F.sn_ldx[J];
+      schunk_gemv(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
+      if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
+      for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
     } else if (type == 3) {
       // ---------------- XCHUNK: x[I] += X_{I,K0..K0+nK} · v[K0..]
       const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
@@ -870,6 +947,9 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       __threadfence();
       __syncthreads();
       if (tid == 0) st_rel_u32(F.ready_sb + J, E);
+    } else if (type == 6) {
+      // ---------------- ROOTB: the symmetric root's x = S⁻¹ v was completed by the forward sweep
+      if (tid == 0) st_rel_u32(F.ready_sb + idx, E);
     } else if (type == 3) {
       // ---------------- XCHUNK (backward): x[K] += (X_Jᵀ)_{K, I0..I0+nI} · v[I0..]
       const int bK = F.xb_bK[idx], bI = F.xb_bI[idx], nI = F.xb_nI[idx];
@@ -949,7 +1029,9 @@ __global__ void __launch_bounds__(NT) k_gemm_batched(const GemmProb* probs, cons
   const int tilesM = (P.M + 63) / 64;
   const int ti = (int)(t % tilesM), tj = (int)(t / tilesM);
   const int r0 = ti * 64, c0 = tj * 64;
+  if ((P.flags & 8) && tj > ti) return;
   int kmin = (P.flags & 2) ? c0 : 0;
+  if (P.flags & 4) kmin = max(kmin, r0);
   int kmax = (P.flags & 1) ? min(P.K, r0 + 64) : P.K;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   double acc[4][4];
@@ -1047,6 +1129,22 @@ __global__ void k_transpose_xinv(DevFactor F, const int32_t* big) {
     }
     __syncthreads();
   }
+}
+
+__global__ void k_scale_xinv_rows(DevFactor F, const int32_t* sns) {
+  const int J = sns[blockIdx.y];
+  const int64_t cJ = F.sn_start[J], w = F.sn_start[J + 1] - cJ, ldx = F.sn_ldx[J];
+  double* X = F.xinv + F.sn_xinv[J];
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < ldx * w; e += (int64_t)gridDim.x * NT) {
+    const int64_t r = e % ldx;
+    if (r < w) X[e] /= F.Dpiv[cJ + r];
+  }
+}
+
+void scale_xinv_rows(const DevFactor& F, const int32_t* sns, int n, int64_t max_w2, cudaStream_t s) {
+  if (n == 0) return;
+  dim3 grid((unsigned)std::min<int64_t>((max_w2 + NT - 1) / NT, 148 * 8), (unsigned)n);
+  k_scale_xinv_rows<<<grid, NT, 0, s>>>(F, sns);
 }
 
 void transpose_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s) {

@@ -58,6 +58,7 @@ struct DevFactor {
   const int32_t* xb_nI;
   const int64_t* sn_xtr;
   const int64_t* sn_ldx;
+  const int64_t* sn_sinv;
   const int32_t* sn_nblk;
   const int64_t* blk_dptr;        // fused small supernodes: destination supernode lists
   const int32_t* blk_dest;
@@ -135,13 +136,16 @@ struct GemmProb {
   double* C;
   int M, N, K, lda, ldb, ldc;
   double alpha, beta;
-  int flags;  // 1: A lower-triangular (k <= row), 2: B lower-triangular (k >= col)
+  int flags;  // 1: A lower-triangular (k <= row), 2: B lower-triangular (k >= col),
+              // 4: A upper-triangular (k >= row), 8: only tiles with tj <= ti (lower half, diagonal tiles full)
   int pad;
 };
 void gemm_batched(const GemmProb* probs, const int64_t* tile_pref, int nprob, int64_t total_tiles,
                   cudaStream_t s);
 void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
 void transpose_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
+// Y = D_J⁻¹ X_J (rows scaled by the pivots), in place, for the listed supernodes
+void scale_xinv_rows(const DevFactor& F, const int32_t* sns, int n, int64_t max_w2, cudaStream_t s);
 
 // ---- level-free task-graph triangular sweeps (persistent kernels)
 struct SweepRhs {

@@ -359,6 +359,9 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
   S.bwd_expect.assign(S.nb, 0);
   S.blk_big.assign(S.nb, 0);
   S.sn_xinv.assign(ns, -1);
+  S.sn_sinv.assign(ns, -1);
+  S.sym_true = 0;
+  S.sym_lower = 0;
   S.sn_xtr.assign(ns, -1);
   S.sn_ldx.assign(ns, 0);
   S.sn_xtmp.assign(ns, -1);
@@ -373,6 +376,13 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
       S.x_size += ldx * w;
       S.sn_xtr[J] = S.x_size;
       S.x_size += ldx * w;
+      const int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+      if (S.sn_parent[J] < 0 && m == w && !std::getenv("QPB_NO_SYMROOT")) {
+        S.sn_sinv[J] = S.x_size;
+        S.x_size += ldx * w;
+        for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) S.sym_true += S.colcount[c];
+        S.sym_lower += w * (w + 1) / 2;
+      }
       S.sn_xtmp[J] = S.xtmp_size;
       S.xtmp_size += (w / 2 + BW) * (w / 2 + BW);
       for (int64_t b = S.sn_blk0[J]; b < S.sn_blk0[J + 1]; ++b) S.blk_big[b] = 1;
@@ -429,6 +439,7 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
   std::vector<int64_t> sn_xb0(ns + 1, 0);
   S.xexp_f.assign(S.nb, 0);
   S.xexp_b.assign(S.nb, 0);
+  S.sexp.assign(S.nb, 0);
   S.sn_nblk.assign(ns, 0);
   std::vector<int64_t> sn_xt0(ns + 1, 0);
   for (int64_t J = 0; J < ns; ++J) {
@@ -452,6 +463,7 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
     for (int64_t I = 0; I < T; ++I) {
       S.xexp_f[b0 + I] = (int32_t)((I + XCH) / XCH);           // forward chunks covering row-block I
       S.xexp_b[b0 + I] = (int32_t)((T - I + XCH - 1) / XCH);   // backward chunks of output block K = I
+      if (S.sn_sinv[J] >= 0) S.sexp[b0 + I] = (int32_t)((I + XCH) / XCH + (T - 1 - I));
     }
   }
   sn_xt0[ns] = (int64_t)S.xt_bI.size();
@@ -469,7 +481,7 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
       }
     } else {
       for (int64_t b = b0; b < b1; ++b) S.fwd_tasks.push_back(enc(2, b));
-      for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) S.fwd_tasks.push_back(enc(3, x));
+      for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) S.fwd_tasks.push_back(enc(S.sn_sinv[J] >= 0 ? 5 : 3, x));
       for (int64_t b = b0; b < b1; ++b)
         for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back(enc(1, t));
     }
@@ -482,6 +494,10 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
         S.bwd_tasks.push_back(enc(fused[b] ? 4 : 0, b));
       }
     } else {
+      if (S.sn_sinv[J] >= 0) {
+        S.bwd_tasks.push_back(enc(6, J));
+        continue;
+      }
       for (int64_t b = b1 - 1; b >= b0; --b)
         for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back(enc(1, t));
       for (int64_t b = b0; b < b1; ++b) S.bwd_tasks.push_back(enc(2, b));

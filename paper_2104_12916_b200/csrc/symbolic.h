@@ -49,6 +49,8 @@ struct Symbolic {
   std::vector<int64_t> parent, colcount, rowlev;
   int64_t nnz_L = 0, n_rowlev = 0;
   int64_t nnz_stored = 0;          // entries stored by the relaxed supernodes (≥ nnz_L)
+  int64_t sym_true = 0;            // true nnz(L) in the columns of symmetric roots
+  int64_t sym_lower = 0;           // w(w+1)/2 summed over symmetric roots (entries of S⁻¹ read per solve)
   double c_fact = 0;              // Σ cc²
 
   // supernodes
@@ -76,7 +78,9 @@ struct Symbolic {
   // trsv tiles + task queues.  Task encoding: (type << 28) | index with
   // type 0 DIAG(block), 1 TILE(off-diagonal tile), 2 PREP(block of a big
   // supernode), 3 XCHUNK(chunk of the inverse diagonal block of a big
-  // supernode), 4 SNF(small supernode swept in one task: diagonal + all rows).
+  // supernode), 4 SNF(small supernode swept in one task: diagonal + all rows),
+  // 5 SCHUNK(chunk of S_J⁻¹ of a symmetric root: x_I += S_IK v_K and x_K += S_IKᵀ v_I),
+  // 6 ROOTB(backward: the symmetric root's x is already final — publish it).
   std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;   // tile_dest: destination SUPERNODE
   std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect /*per supernode*/, bwd_expect /*per block*/;
   // partitioned inverse of multi-block ("big") supernodes
@@ -84,6 +88,8 @@ struct Symbolic {
   std::vector<int64_t> sn_xtr;           // offset of X_Jᵀ (same layout)
   std::vector<int64_t> sn_ldx;           // leading dimension (w rounded up to 8)
   std::vector<int32_t> xb_bK, xb_bI, xb_nI; // backward chunks: output block K, first row-block I, #blocks
+  std::vector<int64_t> sn_sinv;          // symmetric root: offset of S_J⁻¹ = X_Jᵀ D_J⁻¹ X_J (lower + full diagonal tiles) or -1
+  std::vector<int32_t> sexp;             // per block of a symmetric root: contributions to x_I expected
   std::vector<int32_t> xt_bI, xt_bK, xt_nK; // X chunks: row-block, first column-block, #column-blocks
   std::vector<int32_t> xexp_f, xexp_b;   // per block: X chunks covering the row-block / column-block
   std::vector<int32_t> sn_nblk;          // blocks per supernode
