@@ -185,6 +185,8 @@ typedef struct {
   double sweep_bytes_F;              /* algorithmic bytes of one L_F sweep: 8·nnz(L_F) */
   double fsolve_bytes_F;             /* bytes one F-solve must read in this implementation: 8·(2·nnz of L_F
                                         outside symmetric roots + w(w+1)/2 of each root's S⁻¹) */
+  double sym_discrepancy;            /* ‖y_S⁻¹ − y_X‖/‖y_X‖ of the factor-time accuracy guard */
+  double sym_enabled;                /* 1 if the symmetric-root S⁻¹ shortcut is in use (guard ≤ 1e-10) */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 

@@ -65,7 +65,7 @@ class _Stats(C.Structure):
                                          "nnz_LF_stored")] + \
                [(k, C.c_double) for k in ("c_fact_F", "c_fact_PH", "t_symbolic_s", "t_factor_s",
                                           "t_factor_ph_s", "pcg_bytes_per_iter", "pcg_flops_per_iter",
-                                          "sweep_bytes_F", "fsolve_bytes_F")]
+                                          "sweep_bytes_F", "fsolve_bytes_F", "sym_discrepancy", "sym_enabled")]
 
 
 _LIB = None

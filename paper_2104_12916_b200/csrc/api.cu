@@ -138,6 +138,21 @@ struct Factor {
   std::vector<int64_t> inv_off;                  // per (height, phase) offsets into inv_dev / inv_pref_dev
   std::vector<int64_t> inv_total;
   unsigned long long* tprof_buf = nullptr;
+  int32_t* fwd_x = nullptr;      // task queues without the symmetric-root shortcut
+  int32_t* bwd_x = nullptr;
+  double sym_discrepancy = 0.0;  // ‖y_sym − y_X‖ / ‖y_X‖ measured at factor time
+  bool sym_enabled = false;
+  const int32_t* fwd_sym = nullptr;
+  const int32_t* bwd_sym = nullptr;
+  int64_t n_fwd_sym = 0, n_bwd_sym = 0, n_fwd_x = 0, n_bwd_x = 0;
+  void use_symmetric_roots(bool on) {
+    d.use_sym = on ? 1 : 0;
+    d.fwd_tasks = on ? fwd_sym : fwd_x;
+    d.bwd_tasks = on ? bwd_sym : bwd_x;
+    d.n_fwd_tasks = on ? n_fwd_sym : n_fwd_x;
+    d.n_bwd_tasks = on ? n_bwd_sym : n_bwd_x;
+    sym_enabled = on;
+  }
 };
 
 DevCSR upload_csr(DeviceArena& mem, const HostCSR& A, cudaStream_t s) {
@@ -346,6 +361,8 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.tile_dest = m.upload(S.tile_dest, st);
     d.fwd_tasks = m.upload(S.fwd_tasks, st);
     d.bwd_tasks = m.upload(S.bwd_tasks, st);
+    F.fwd_x = m.upload(S.fwd_tasks_x, st);
+    F.bwd_x = m.upload(S.bwd_tasks_x, st);
     d.fwd_expect = m.upload(S.fwd_expect, st);
     d.bwd_expect = m.upload(S.bwd_expect, st);
     d.ws = m.alloc<double>(S.ws_size);
@@ -424,6 +441,13 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.upd_pref = m.upload(S.upd_pref, st);
     d.status = m.zeros<int>(1, st);
     d.tprof = nullptr;
+    d.use_sym = 0;
+    F.fwd_sym = d.fwd_tasks;
+    F.bwd_sym = d.bwd_tasks;
+    F.n_fwd_sym = d.n_fwd_tasks;
+    F.n_bwd_sym = d.n_bwd_tasks;
+    F.n_fwd_x = (int64_t)S.fwd_tasks_x.size();
+    F.n_bwd_x = (int64_t)S.bwd_tasks_x.size();
     F.tprof_buf = m.alloc<unsigned long long>(50);
     F.fs_bytes = S.fs_size * 8;
     F.ws_bytes = S.ws_size * 8;
@@ -518,8 +542,9 @@ void run_inverse(qp_ctx* c, Factor& F) {
     }
   transpose_xinv(F.d, F.big, F.n_big, F.max_w2, c->stream);
   if (F.n_sym > 0) {
-    scale_xinv_rows(F.d, F.sym, F.n_sym, F.max_w2, c->stream);   // X ← D⁻¹X (X no longer needed)
+    scale_xinv_rows(F.d, F.sym, F.n_sym, F.max_w2, false, c->stream);   // X ← D⁻¹X
     gemm_batched(F.sym_dev, F.sym_pref_dev, F.n_sym, F.sym_total, c->stream);
+    scale_xinv_rows(F.d, F.sym, F.n_sym, F.max_w2, true, c->stream);    // X restored (X/Xᵀ fallback path)
   }
 }
 
@@ -971,6 +996,32 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
   rc = numeric_factor(c, c->FF, nullptr, nullptr, nullptr, "F factorization");
   c->t_factor = now_s() - t1;
   if (rc) return rc;
+  c->FF.use_symmetric_roots(false);
+  if (c->FF.n_sym > 0) {
+    // accuracy guard for the symmetric-root shortcut: one F-solve through S⁻¹ vs through X/Xᵀ
+    std::vector<double> r(N), y1(N), y2(N);
+    uint64_t st64 = 0x9E3779B97F4A7C15ull;
+    for (int64_t i = 0; i < N; ++i) {
+      st64 = st64 * 6364136223846793005ull + 1442695040888963407ull;
+      r[i] = (double)((st64 >> 11) & ((1ull << 52) - 1)) / (double)(1ull << 52) - 0.5;
+    }
+    cudaMemcpyAsync(c->rhs2, r.data(), N * 8, cudaMemcpyHostToDevice, st);
+    c->FF.use_symmetric_roots(true);
+    f_solve_dev(c, c->rhs2, c->xbuf);
+    cudaMemcpyAsync(y1.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+    c->FF.use_symmetric_roots(false);
+    f_solve_dev(c, c->rhs2, c->xbuf);
+    cudaMemcpyAsync(y2.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+    rc = sync_check(c, "symmetric-root guard");
+    if (rc) return rc;
+    double dn = 0, nn = 0;
+    for (int64_t i = 0; i < N; ++i) {
+      dn += (y1[i] - y2[i]) * (y1[i] - y2[i]);
+      nn += y2[i] * y2[i];
+    }
+    c->FF.sym_discrepancy = nn > 0 ? std::sqrt(dn / nn) : 0.0;
+    c->FF.use_symmetric_roots(c->FF.sym_discrepancy <= 1e-10 && std::isfinite(c->FF.sym_discrepancy));
+  }
   // ---- P_H: T = C diag(H)⁻¹ Cᵀ pattern (host) and values (device), symbolic of D + T
   if (p == QP_PREC_HIGH) {
     HostCSR Ct = transpose(c->C);
@@ -1045,7 +1096,7 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
         }
       }
     }
-    e = analyse(PM, c->FP.S, 0);
+    e = analyse(PM, c->FP.S, 0, /*allow_symroot=*/false);   // P_H is refactored at every D: keep L-based sweeps
     if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of P_H: " + e);
     e = upload_factor(c, c->FP, c->ws_limit);
     if (!e.empty()) return fail(c, QP_ENOMEM, e);
@@ -1268,7 +1319,11 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
                             16.0 * (double)s->nnz_LPH;
     s->pcg_flops_per_iter = 4.0 * (double)S.nnz_L + 4.0 * (double)c->C.nnz() + 4.0 * (double)s->nnz_LPH;
     s->sweep_bytes_F = 8.0 * (double)S.nnz_L;
-    s->fsolve_bytes_F = 8.0 * (2.0 * (double)(S.nnz_L - S.sym_true) + (double)S.sym_lower);
+    s->fsolve_bytes_F = c->FF.sym_enabled || !c->factored
+                            ? 8.0 * (2.0 * (double)(S.nnz_L - S.sym_true) + (double)S.sym_lower)
+                            : 16.0 * (double)S.nnz_L;
+    s->sym_discrepancy = c->FF.sym_discrepancy;
+    s->sym_enabled = c->FF.sym_enabled ? 1.0 : 0.0;
   }
   return QP_OK;
 }

@@ -624,7 +624,11 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         }
         __threadfence();
         __syncthreads();
-        if (tid == 0) st_rel_u32(F.vready_f + b, E);
+        if (tid == 0) {
+          // keep the X-path counters in step when the symmetric root bypasses them
+          if (F.use_sym && F.sn_sinv[J] >= 0) atomicAdd(F.cntx_f + b, (unsigned long long)F.xexp_f[b]);
+          st_rel_u32(F.vready_f + b, E);
+        }
       }
     } else if (type == 4) {
       // ---------------- SNF(b): small supernode in one task — y_b = L_bb⁻¹ v, then acc[rows] += L_rows·y_b
@@ -949,7 +953,14 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       if (tid == 0) st_rel_u32(F.ready_sb + J, E);
     } else if (type == 6) {
       // ---------------- ROOTB: the symmetric root's x = S⁻¹ v was completed by the forward sweep
-      if (tid == 0) st_rel_u32(F.ready_sb + idx, E);
+      const int J = idx;
+      for (int b = F.sn_blk0[J] + tid; b < F.sn_blk0[J + 1]; b += NT)
+        atomicAdd(F.cntx_b + b, (unsigned long long)F.xexp_b[b]);   // keep X-path counters in step
+      __syncthreads();
+      if (tid == 0) {
+        atomicAdd(F.sn_done_b + J, (unsigned long long)F.sn_nblk[J]);
+        st_rel_u32(F.ready_sb + J, E);
+      }
     } else if (type == 3) {
       // ---------------- XCHUNK (backward): x[K] += (X_Jᵀ)_{K, I0..I0+nI} · v[I0..]
       const int bK = F.xb_bK[idx], bI = F.xb_bI[idx], nI = F.xb_nI[idx];
@@ -1131,20 +1142,20 @@ __global__ void k_transpose_xinv(DevFactor F, const int32_t* big) {
   }
 }
 
-__global__ void k_scale_xinv_rows(DevFactor F, const int32_t* sns) {
+__global__ void k_scale_xinv_rows(DevFactor F, const int32_t* sns, int multiply) {
   const int J = sns[blockIdx.y];
   const int64_t cJ = F.sn_start[J], w = F.sn_start[J + 1] - cJ, ldx = F.sn_ldx[J];
   double* X = F.xinv + F.sn_xinv[J];
   for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < ldx * w; e += (int64_t)gridDim.x * NT) {
     const int64_t r = e % ldx;
-    if (r < w) X[e] /= F.Dpiv[cJ + r];
+    if (r < w) X[e] = multiply ? X[e] * F.Dpiv[cJ + r] : X[e] / F.Dpiv[cJ + r];
   }
 }
 
-void scale_xinv_rows(const DevFactor& F, const int32_t* sns, int n, int64_t max_w2, cudaStream_t s) {
+void scale_xinv_rows(const DevFactor& F, const int32_t* sns, int n, int64_t max_w2, bool multiply, cudaStream_t s) {
   if (n == 0) return;
   dim3 grid((unsigned)std::min<int64_t>((max_w2 + NT - 1) / NT, 148 * 8), (unsigned)n);
-  k_scale_xinv_rows<<<grid, NT, 0, s>>>(F, sns);
+  k_scale_xinv_rows<<<grid, NT, 0, s>>>(F, sns, multiply ? 1 : 0);
 }
 
 void transpose_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s) {

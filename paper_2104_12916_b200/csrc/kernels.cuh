@@ -92,7 +92,8 @@ struct DevFactor {
   const int64_t* pan_pref;
   const int64_t* upd_pref;
   int* status;        // pivot failures (device int)
-  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][4 types][5]
+  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][5 types][5]
+  int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
 };
 
 // CSR on the device (int64 row pointers, int32 columns).
@@ -145,7 +146,7 @@ void gemm_batched(const GemmProb* probs, const int64_t* tile_pref, int nprob, in
 void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
 void transpose_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
 // Y = D_J⁻¹ X_J (rows scaled by the pivots), in place, for the listed supernodes
-void scale_xinv_rows(const DevFactor& F, const int32_t* sns, int n, int64_t max_w2, cudaStream_t s);
+void scale_xinv_rows(const DevFactor& F, const int32_t* sns, int n, int64_t max_w2, bool multiply, cudaStream_t s);
 
 // ---- level-free task-graph triangular sweeps (persistent kernels)
 struct SweepRhs {

@@ -72,7 +72,7 @@ static inline int64_t tile_begin(int64_t t, int64_t nk, int64_t w, int64_t m) {
   return v < m ? v : m;
 }
 
-std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot) {
   const int64_t N = M.N;
   S.N = N;
   // ---------------------------------------------------------------- row form of the strict lower part
@@ -377,7 +377,7 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
       S.sn_xtr[J] = S.x_size;
       S.x_size += ldx * w;
       const int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
-      if (S.sn_parent[J] < 0 && m == w && !std::getenv("QPB_NO_SYMROOT")) {
+      if (allow_symroot && S.sn_parent[J] < 0 && m == w && !std::getenv("QPB_NO_SYMROOT")) {
         S.sn_sinv[J] = S.x_size;
         S.x_size += ldx * w;
         for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) S.sym_true += S.colcount[c];
@@ -470,40 +470,46 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative) {
   sn_xb0[ns] = (int64_t)S.xb_bK.size();
   if ((int64_t)S.xt_bI.size() >= (int64_t(1) << TASK_SHIFT) || (int64_t)S.tile_blk.size() >= (int64_t(1) << TASK_SHIFT))
     return "too many sweep tasks for the 28-bit task encoding";
-  S.fwd_tasks.clear();
-  S.bwd_tasks.clear();
-  for (int64_t J = 0; J < ns; ++J) {
-    const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
-    if (S.sn_xinv[J] < 0) {
-      for (int64_t b = b0; b < b1; ++b) {
-        S.fwd_tasks.push_back(enc(fused[b] ? 4 : 0, b));
-        for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back(enc(1, t));
+  auto build_queues = [&](bool use_sym, std::vector<int32_t>& fq, std::vector<int32_t>& bq) {
+    fq.clear();
+    bq.clear();
+    for (int64_t J = 0; J < ns; ++J) {
+      const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
+      const bool sym = use_sym && S.sn_sinv[J] >= 0;
+      if (S.sn_xinv[J] < 0) {
+        for (int64_t b = b0; b < b1; ++b) {
+          fq.push_back(enc(fused[b] ? 4 : 0, b));
+          for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) fq.push_back(enc(1, t));
+        }
+      } else {
+        for (int64_t b = b0; b < b1; ++b) fq.push_back(enc(2, b));
+        for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) fq.push_back(enc(sym ? 5 : 3, x));
+        for (int64_t b = b0; b < b1; ++b)
+          for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) fq.push_back(enc(1, t));
       }
-    } else {
-      for (int64_t b = b0; b < b1; ++b) S.fwd_tasks.push_back(enc(2, b));
-      for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) S.fwd_tasks.push_back(enc(S.sn_sinv[J] >= 0 ? 5 : 3, x));
-      for (int64_t b = b0; b < b1; ++b)
-        for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) S.fwd_tasks.push_back(enc(1, t));
     }
-  }
-  for (int64_t J = ns - 1; J >= 0; --J) {
-    const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
-    if (S.sn_xinv[J] < 0) {
-      for (int64_t b = b1 - 1; b >= b0; --b) {
-        for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back(enc(1, t));
-        S.bwd_tasks.push_back(enc(fused[b] ? 4 : 0, b));
+    for (int64_t J = ns - 1; J >= 0; --J) {
+      const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
+      const bool sym = use_sym && S.sn_sinv[J] >= 0;
+      if (S.sn_xinv[J] < 0) {
+        for (int64_t b = b1 - 1; b >= b0; --b) {
+          for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) bq.push_back(enc(1, t));
+          bq.push_back(enc(fused[b] ? 4 : 0, b));
+        }
+      } else {
+        if (sym) {
+          bq.push_back(enc(6, J));
+          continue;
+        }
+        for (int64_t b = b1 - 1; b >= b0; --b)
+          for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) bq.push_back(enc(1, t));
+        for (int64_t b = b0; b < b1; ++b) bq.push_back(enc(2, b));
+        for (int64_t x = sn_xb0[J]; x < sn_xb0[J + 1]; ++x) bq.push_back(enc(3, x));
       }
-    } else {
-      if (S.sn_sinv[J] >= 0) {
-        S.bwd_tasks.push_back(enc(6, J));
-        continue;
-      }
-      for (int64_t b = b1 - 1; b >= b0; --b)
-        for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) S.bwd_tasks.push_back(enc(1, t));
-      for (int64_t b = b0; b < b1; ++b) S.bwd_tasks.push_back(enc(2, b));
-      for (int64_t x = sn_xb0[J]; x < sn_xb0[J + 1]; ++x) S.bwd_tasks.push_back(enc(3, x));
     }
-  }
+  };
+  build_queues(true, S.fwd_tasks, S.bwd_tasks);
+  build_queues(false, S.fwd_tasks_x, S.bwd_tasks_x);
   // ---------------------------------------------------------------- assembly map (grouped by level), relative indices
   S.asm_dst.clear();
   S.asm_val.clear();

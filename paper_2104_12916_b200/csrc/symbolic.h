@@ -83,6 +83,7 @@ struct Symbolic {
   // 6 ROOTB(backward: the symmetric root's x is already final — publish it).
   std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;   // tile_dest: destination SUPERNODE
   std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect /*per supernode*/, bwd_expect /*per block*/;
+  std::vector<int32_t> fwd_tasks_x, bwd_tasks_x;   // same queues with symmetric roots swept through X/Xᵀ (fallback)
   // partitioned inverse of multi-block ("big") supernodes
   std::vector<int64_t> sn_xinv;          // offset of X_J = L_JJ⁻¹ (w×w col-major, ld sn_ldx) or -1
   std::vector<int64_t> sn_xtr;           // offset of X_Jᵀ (same layout)
@@ -134,6 +135,6 @@ std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr,
                                      const std::vector<int64_t>& order);
 
 // Full symbolic analysis + multifrontal / trsv plans.  Returns "" or an error.
-std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative);
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot = true);
 
 }  // namespace qpb
