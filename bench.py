@@ -97,6 +97,16 @@ def allreduce(vals, op, use_dist):
     return t.cpu().tolist()
 
 
+def aggregate(pcg_iters, ms, use_dist):
+    """Whole-job throughput: Σ PCG iterations over ranks ÷ the slowest rank's time (max over ranks)."""
+    tot, mx = float(pcg_iters), float(ms)
+    if use_dist:
+        import torch.distributed as dist
+        tot = allreduce([tot], dist.ReduceOp.SUM, True)[0]
+        mx = allreduce([mx], dist.ReduceOp.MAX, True)[0]
+    return (tot / (mx / 1e3) if mx > 0 else 0.0), tot, mx
+
+
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -282,22 +292,13 @@ def run_ours(args, rank, world, local, use_dist):
         torch.cuda.synchronize(dev)
         barrier(use_dist)
         ms_e2e = f0.elapsed_time(f1)
-        its_all, ms_max = allreduce([float(its)], None, False)[0], ms_e2e
-        if use_dist:
-            import torch.distributed as dist
-            its_all = allreduce([float(its)], dist.ReduceOp.SUM, True)[0]
-            ms_max = allreduce([ms_e2e], dist.ReduceOp.MAX, True)[0]
-        e2e = {"value": its_all / (ms_max / 1e3) if ms_max > 0 else 0.0, "unit": UNIT,
+        e2e_value, _, _ = aggregate(its, ms_e2e, use_dist)
+        e2e = {"value": e2e_value, "unit": UNIT,
                "h2d_bytes_per_step": 2 * 8 * qp.m2, "d2h_bytes_per_step": 8 * qp.m2 + 16,
                "steps": len(systems), "pcg_iters": its}
 
     # ---------------------------------------------------------------- aggregate over ranks
-    tot_pcg, ms_max = float(pcg_timed), ms
-    if use_dist:
-        import torch.distributed as dist
-        tot_pcg = allreduce([float(pcg_timed)], dist.ReduceOp.SUM, True)[0]
-        ms_max = allreduce([ms], dist.ReduceOp.MAX, True)[0]
-    value = tot_pcg / (ms_max / 1e3) if ms_max > 0 else 0.0
+    value, tot_pcg, ms_max = aggregate(pcg_timed, ms, use_dist)
 
     # ---------------------------------------------------------------- roofline of the L_F sweeps
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")

@@ -276,9 +276,9 @@ class QPSolver:
         return buf
 
     def debug_sweep_profile(self, enable):
-        out = np.zeros(50, dtype=np.int64)
+        out = np.zeros(70, dtype=np.int64)
         self._check(self.lib.qp_debug_sweep_profile(self.ctx, 1 if enable else 0, out.ctypes.data))
-        return out.reshape(2, 5, 5)
+        return out.reshape(2, 7, 5)
 
     def ipm_last_system(self):
         D, r = np.zeros(self.m2), np.zeros(self.m2)

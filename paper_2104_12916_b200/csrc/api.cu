@@ -448,7 +448,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     F.n_bwd_sym = d.n_bwd_tasks;
     F.n_fwd_x = (int64_t)S.fwd_tasks_x.size();
     F.n_bwd_x = (int64_t)S.bwd_tasks_x.size();
-    F.tprof_buf = m.alloc<unsigned long long>(50);
+    F.tprof_buf = m.alloc<unsigned long long>(70);
     F.fs_bytes = S.fs_size * 8;
     F.ws_bytes = S.ws_size * 8;
   } catch (std::bad_alloc&) {
@@ -1367,12 +1367,12 @@ int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
   if (!c || !c->factored) return QP_ESTATE;
   Factor& F = c->FF;
   if (enable) {
-    std::vector<unsigned long long> init(50, 0);
-    for (int i = 0; i < 10; ++i) init[i * 5 + 3] = ~0ull;
-    cudaMemcpyAsync(F.tprof_buf, init.data(), 50 * 8, cudaMemcpyHostToDevice, c->stream);
+    std::vector<unsigned long long> init(70, 0);
+    for (int i = 0; i < 14; ++i) init[i * 5 + 3] = ~0ull;
+    cudaMemcpyAsync(F.tprof_buf, init.data(), 70 * 8, cudaMemcpyHostToDevice, c->stream);
     F.d.tprof = F.tprof_buf;
   } else {
-    if (out) cudaMemcpyAsync(out, F.tprof_buf, 50 * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (out) cudaMemcpyAsync(out, F.tprof_buf, 70 * 8, cudaMemcpyDeviceToHost, c->stream);
     F.d.tprof = nullptr;
   }
   return sync_check(c, "qp_debug_sweep_profile");

@@ -388,7 +388,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int type, unsigned long long t0,
                                           unsigned long long t1, unsigned long long t2) {
   if (tp == nullptr || threadIdx.x != 0) return;
-  unsigned long long* q = tp + (sweep * 5 + type) * 5;
+  unsigned long long* q = tp + (sweep * 7 + type) * 5;
   atomicAdd(q + 0, 1ull);
   atomicAdd(q + 1, t1 - t0);
   atomicAdd(q + 2, t2 - t1);
