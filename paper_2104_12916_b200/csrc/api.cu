@@ -579,12 +579,19 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
 }
 
 // y = F⁻¹ rhs (factor order, N), forward + backward sweeps.
+void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
+  if (!F.sym_enabled) return;
+  c->launches += 1;
+  symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, done, c->sm_count * 3, c->stream);
+}
+
 void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
   c->launches += 2;
   SweepRhs r{};
   r.rhs = rhs_f;
   int h = c->begin(0);
   trsv_forward(c->FF.d, r, out, c->tgrid, c->stream);
+  sym_gemv(c, c->FF, out, nullptr);
   c->end(h);
   h = c->begin(1);
   trsv_backward(c->FF.d, out, nullptr, c->tgrid, c->stream);
@@ -600,6 +607,7 @@ void kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool p
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
   int h = c->begin(0);
   trsv_forward(c->FF.d, r, c->xbuf, c->tgrid, c->stream);
+  sym_gemv(c, c->FF, c->xbuf, r.done_flag);
   c->end(h);
   h = c->begin(1);
   trsv_backward(c->FF.d, c->xbuf, r.done_flag, c->tgrid, c->stream);

@@ -1170,6 +1170,41 @@ void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t m
   k_build_xinv<<<grid, NT, 0, s>>>(F, big_sns, n_big);
 }
 
+// Symmetric-root GEMV as its own kernel (between the forward and backward sparse sweeps):
+// x_J += S_J⁻¹ v_J over the chunks (I, K0..K0+nK) of every symmetric root, grid-stride, no flags.
+__global__ void __launch_bounds__(NT, 3) k_symroot_gemv(DevFactor F, double* x, int64_t c_begin, int64_t c_end,
+                                                         const int* done_flag) {
+  __shared__ double vK[512];
+  __shared__ double vI[64];
+  __shared__ double red[576];
+  __shared__ double colv[512];
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const int tid = threadIdx.x;
+  for (int64_t idx = c_begin + blockIdx.x; idx < c_end; idx += gridDim.x) {
+    const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
+    const int J = F.blk_sn[bI];
+    const int64_t cJ = F.sn_start[J];
+    const int64_t rI = F.blk_col0[bI], cK = F.blk_col0[bK];
+    const int Rn = F.blk_w[bI];
+    const int ncol = (int)(F.blk_col0[bK + nK - 1] + F.blk_w[bK + nK - 1] - cK);
+    const int ncol_t = (int)((rI < cK + ncol ? rI : cK + ncol) - cK);
+    __syncthreads();
+    for (int c = tid; c < ncol; c += NT) vK[c] = F.vbuf[cK + c];
+    if (tid < Rn) vI[tid] = F.vbuf[rI + tid];
+    __syncthreads();
+    const int64_t ldx = F.sn_ldx[J];
+    schunk_gemv(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
+    if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
+    for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
+  }
+}
+
+void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
+                  cudaStream_t s) {
+  if (c_end <= c_begin) return;
+  k_symroot_gemv<<<grid, NT, 0, s>>>(F, x, c_begin, c_end, done_flag);
+}
+
 static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)TRSV_SMEM_DBL; }
 
 int trsv_grid(int device) {

@@ -159,6 +159,9 @@ struct SweepRhs {
 void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s);
 void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s);
 int trsv_grid(int device);
+// x_J += S_J⁻¹ v_J for the symmetric-root chunks [c_begin, c_end) (dedicated kernel)
+void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
+                  cudaStream_t s);
 
 // ---- vector / SpMV kernels
 void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,

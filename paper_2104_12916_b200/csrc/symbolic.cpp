@@ -483,7 +483,8 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
         }
       } else {
         for (int64_t b = b0; b < b1; ++b) fq.push_back(enc(2, b));
-        for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) fq.push_back(enc(sym ? 5 : 3, x));
+        if (!sym)
+          for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) fq.push_back(enc(3, x));
         for (int64_t b = b0; b < b1; ++b)
           for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) fq.push_back(enc(1, t));
       }
@@ -509,6 +510,12 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     }
   };
   build_queues(true, S.fwd_tasks, S.bwd_tasks);
+  S.sym_c0 = S.sym_c1 = 0;
+  for (int64_t J = 0; J < ns; ++J)
+    if (S.sn_sinv[J] >= 0) {   // symmetric roots are etree roots: at most one chunk range per root, roots last
+      if (S.sym_c1 == 0) S.sym_c0 = sn_xt0[J];
+      S.sym_c1 = sn_xt0[J + 1];
+    }
   build_queues(false, S.fwd_tasks_x, S.bwd_tasks_x);
   // ---------------------------------------------------------------- assembly map (grouped by level), relative indices
   S.asm_dst.clear();

@@ -91,6 +91,7 @@ struct Symbolic {
   std::vector<int32_t> xb_bK, xb_bI, xb_nI; // backward chunks: output block K, first row-block I, #blocks
   std::vector<int64_t> sn_sinv;          // symmetric root: offset of S_J⁻¹ = X_Jᵀ D_J⁻¹ X_J (lower + full diagonal tiles) or -1
   std::vector<int32_t> sexp;             // per block of a symmetric root: contributions to x_I expected
+  int64_t sym_c0 = 0, sym_c1 = 0;        // chunk range [sym_c0, sym_c1) of the symmetric roots (separate GEMV kernel)
   std::vector<int32_t> xt_bI, xt_bK, xt_nK; // X chunks: row-block, first column-block, #column-blocks
   std::vector<int32_t> xexp_f, xexp_b;   // per block: X chunks covering the row-block / column-block
   std::vector<int32_t> sn_nblk;          // blocks per supernode
