@@ -168,6 +168,7 @@ int qp_analyse(qp_ctx** ctx, const qp_csr* H, const qp_csr* A, const int64_t* x_
  *  0 perm (new→old, N = n+m1)  1 etree parent  2 column counts
  *  3 supernode starts (ns+1)   4 supernode parent  5 supernode level
  *  6 supernode row pointer (ns+1)  7 supernode rows  8 row levels
+ *  9 trailing_from: first column of the forced dense trailing supernode (−1 if none)
  *  10.. the same for the P_H factor (m2 unknowns).
  * Call with out = NULL to get *len; then with a buffer of *len int64. */
 int qp_get_structure(qp_ctx* ctx, int32_t which, int64_t* out, int64_t* len);

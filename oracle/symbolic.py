@@ -19,6 +19,8 @@ same x-block permutation:
   the stored w·m − w(w−1)/2 entries (m = w_J + m_P rows);  a relaxed
   supernode's rows are its columns followed by the rows below its topmost
   fundamental supernode;
+* forced dense trailing supernode (input `trailing_from`, the library's choice like x_perm): after
+  amalgamation every supernode reaching that column merges with the last one;
 * supernodal tree: parent of supernode J = supernode of parent(last col of J);
   level(J) = 0 for leaves, else 1 + max level(children);
 * row levels: lev(i) = 1 + max{lev(j) : j < i, L_ij ≠ 0}, 0 for rows with no
@@ -88,7 +90,7 @@ def _col2sn(starts, N):
     return col2sn
 
 
-def relax(parent, cc, struct, fstart):
+def relax(parent, cc, struct, fstart, trailing_from=-1):
     """Relaxed amalgamation of the fundamental supernodes; returns (starts, rows-per-supernode)."""
     N = len(parent)
     nf = len(fstart) - 1
@@ -128,6 +130,19 @@ def relax(parent, cc, struct, fstart):
                 merged += 1
         if merged == 0:
             break
+    # forced dense trailing supernode: every supernode reaching column trailing_from merges with the last
+    if 0 <= trailing_from < N:
+        live = [J for J in range(nf) if alive[J]]
+        first = next(J for J in live if c0[J] + w[J] > trailing_from)
+        last = live[-1]
+        if first != last:
+            group = [J for J in live if J >= first]
+            wsum = sum(w[J] for J in group)
+            tsum = sum(true[J] for J in group)
+            for J in group[:-1]:
+                alive[J] = False
+            c0[last], w[last], m[last], true[last] = N - wsum, wsum, wsum, tsum
+            assert len(below[last]) == 0
     starts = [c0[J] for J in range(nf) if alive[J]] + [N]
     rows = [np.concatenate([np.arange(c0[J], c0[J] + w[J]), below[J]]).astype(np.int64)
             for J in range(nf) if alive[J]]
@@ -161,13 +176,14 @@ def row_levels(N, struct):
     return lev
 
 
-def analyse(H, A, x_perm=None):
-    """All structures, as a dict of int64 arrays."""
+def analyse(H, A, x_perm=None, trailing_from=-1):
+    """All structures, as a dict of int64 arrays.  trailing_from: first column of a forced dense
+    trailing supernode (the library's absorbed tree top, exported as structure 9), or -1."""
     N, lower = permuted_lower_pattern(H, A, x_perm)
     parent, struct = symbolic_factor(N, lower)
     cc = np.array([len(s) for s in struct], dtype=np.int64)
     fsn = supernodes(parent, cc)
-    sn, rows = relax(parent, cc, struct, fsn)
+    sn, rows = relax(parent, cc, struct, fsn, trailing_from)
     sparent, slevel = supernode_tree(parent, sn)
     sn_rows = np.concatenate(rows) if N else np.zeros(0, np.int64)
     sn_rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)

@@ -24,7 +24,7 @@ PREC = {"none": 0, "low": 1, "high": 2}
 STATUS = {0: "QP_OK", 1: "QP_MAXIT", -1: "QP_EINVAL", -2: "QP_ENOTSPD", -3: "QP_EBREAKDOWN",
           -4: "QP_ENOMEM", -5: "QP_ECUDA", -6: "QP_ENCCL", -7: "QP_ESTATE"}
 STRUCTURES = {"perm": 0, "parent": 1, "colcount": 2, "sn_start": 3, "sn_parent": 4, "sn_level": 5,
-              "sn_rowptr": 6, "sn_rows": 7, "row_level": 8}
+              "sn_rowptr": 6, "sn_rows": 7, "row_level": 8, "trailing_from": 9}
 
 
 class QPError(RuntimeError):

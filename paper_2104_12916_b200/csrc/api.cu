@@ -695,14 +695,19 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
 }
 
 // Ordering (x block by x_perm or minimum degree on the graph of H, λ last) + symbolic analysis of F.
+// When the factor ends in a dense root supernode, the top levels of the supernodal tree (an
+// ancestor-closed set) are moved next to it — an equivalent reordering with the same fill — so that
+// amalgamation absorbs them into the root: fewer dependent levels for the sweeps, at the price of a
+// bounded number of explicit zeros (≤ 2 % of the root's entries).
 std::string analyse_F(qp_ctx* c) {
   const int64_t n = c->n, m1 = c->m1;
   double t0 = now_s();
-  if (!c->xperm_user.empty()) {
+  const bool user = !c->xperm_user.empty();
+  std::vector<int64_t> ptr(n + 1, 0);
+  std::vector<int32_t> idx;
+  if (user) {
     c->perm = c->xperm_user;
   } else {
-    std::vector<int64_t> ptr(n + 1, 0);
-    std::vector<int32_t> idx;
     idx.reserve(c->H.nnz());
     for (int64_t r = 0; r < n; ++r) {
       for (int64_t q = c->H.p[r]; q < c->H.p[r + 1]; ++q)
@@ -712,9 +717,59 @@ std::string analyse_F(qp_ctx* c) {
     c->perm = min_degree_order(n, ptr, idx);
     if (!std::getenv("QPB_NO_POSTORDER")) c->perm = etree_postorder(n, ptr, idx, c->perm);
   }
-  LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(), c->A.i.data(),
-                                c->A.v.data(), c->perm);
-  std::string e = analyse(M, c->FF.S, n);
+  int64_t trailing = -1;
+  auto run = [&]() {
+    c->FF.S = Symbolic();
+    LowerMatrix M = build_F_lower(n, m1, c->H.p.data(), c->H.i.data(), c->H.v.data(), c->A.p.data(),
+                                  c->A.i.data(), c->A.v.data(), c->perm);
+    return analyse(M, c->FF.S, n, true, trailing);
+  };
+  std::string e = run();
+  if (e.empty() && !user && !std::getenv("QPB_NO_ABSORB")) {
+    const Symbolic& S = c->FF.S;
+    const int64_t ns = S.ns, root = ns - 1;
+    const int64_t wr = S.sn_start[ns] - S.sn_start[root];
+    const bool dense_root = ns > 1 && S.sn_parent[root] < 0 && wr > BW &&
+                            S.sn_rowptr[root + 1] - S.sn_rowptr[root] == wr;
+    if (dense_root && S.n_levels > 3) {
+      // choose the lowest cut level L (≥ 1) whose absorbed set costs ≤ 2 % of the root's entries
+      const double budget = 0.02 * (double)wr * (double)(wr + 1) / 2;
+      int64_t best = S.n_levels - 1;
+      for (int64_t L = S.n_levels - 2; L >= 1; --L) {
+        double zeros = 0;
+        int64_t wsum = 0;
+        for (int64_t J = 0; J < root; ++J)
+          if (S.sn_level[J] >= L) {
+            const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+            wsum += w;
+            zeros += (double)w * (double)(wr - (m - w));
+          }
+        zeros += (double)wsum * (double)wsum / 2;
+        if (zeros > budget) break;
+        best = L;
+      }
+      if (best < S.n_levels - 1) {
+        // new x order: columns of supernodes below the cut, then the absorbed ones, then the root
+        std::vector<int64_t> low, high;
+        for (int64_t J = 0; J < root; ++J)
+          for (int64_t col = S.sn_start[J]; col < S.sn_start[J + 1]; ++col)
+            if (col < n) (S.sn_level[J] >= best ? high : low).push_back(c->perm[col]);
+        for (int64_t col = S.sn_start[root]; col < n; ++col) high.push_back(c->perm[col]);
+        low.insert(low.end(), high.begin(), high.end());
+        if (std::getenv("QPB_VERBOSE"))
+          std::fprintf(stderr, "qpb: absorbing levels >= %lld into the root (%zu columns moved)\n", (long long)best,
+                       high.size());
+        if ((int64_t)low.size() == n) {
+          trailing = n - (int64_t)high.size();   // first column of the absorbed block
+          c->perm = low;
+          e = run();
+          if (std::getenv("QPB_VERBOSE"))
+            std::fprintf(stderr, "qpb: after absorption: %lld supernodes, %lld levels\n", (long long)c->FF.S.ns,
+                         (long long)c->FF.S.n_levels);
+        }
+      }
+    }
+  }
   c->t_symbolic = now_s() - t0;
   if (e.empty()) c->analysed = true;
   return e;
@@ -1281,6 +1336,7 @@ int qp_get_structure(qp_ctx* c, int32_t which, int64_t* out, int64_t* len) {
     case 6: v = S.sn_rowptr; break;
     case 7: v.assign(S.sn_rows.begin(), S.sn_rows.end()); break;
     case 8: v = S.rowlev; break;
+    case 9: v = {S.trailing_from}; break;
     default: return fail(c, QP_EINVAL, "unknown structure id");
   }
   if (!len) return QP_EINVAL;

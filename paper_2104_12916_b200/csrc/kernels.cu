@@ -19,6 +19,7 @@
 #include <cfloat>
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
 
 namespace qpb {
 
@@ -504,6 +505,7 @@ __device__ __forceinline__ void xchunk_gemv(const double* __restrict__ M, int64_
 // Symmetric-root chunk: rows R ≤ 64 of block I, ncol columns of blocks K0..;
 // red[512 + r] = Σ_c S(r,c)·vK[c] (all columns) and colv[c] = Σ_r S(r,c)·vI[r] for c < ncol_t
 // (the columns strictly before block I).  One read of the chunk serves both products.
+template <int U = 8>
 __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_t ld, int R, int ncol, int ncol_t,
                                             const double* vK, const double* vI, double* red, double* colv) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -513,13 +515,13 @@ __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_
   const double vi0 = ok ? vI[2 * lane] : 0.0, vi1 = (2 * lane + 1 < R) ? vI[2 * lane + 1] : 0.0;
   double a0 = 0.0, a1 = 0.0;
   int c = wid;
-  for (; c + 56 < ncol; c += 64) {
-    double2 q[8];
+  for (; c + 8 * (U - 1) < ncol; c += 8 * U) {
+    double2 q[U];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) q[u] = ok ? __ldg(base + (int64_t)(c + 8 * u) * ld2) : make_double2(0.0, 0.0);
-    double t[8];
+    for (int u = 0; u < U; ++u) q[u] = ok ? __ldg(base + (int64_t)(c + 8 * u) * ld2) : make_double2(0.0, 0.0);
+    double t[U];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < U; ++u) {
       const double vc = vK[c + 8 * u];
       a0 = fma(q[u].x, vc, a0);
       a1 = fma(q[u].y, vc, a1);
@@ -528,10 +530,10 @@ __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o);
+      for (int u = 0; u < U; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o);
     if (lane == 0)
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < U; ++u)
         if (c + 8 * u < ncol_t) colv[c + 8 * u] = t[u];
   }
   for (; c < ncol; c += 8) {
@@ -1172,8 +1174,9 @@ void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t m
 
 // Symmetric-root GEMV as its own kernel (between the forward and backward sparse sweeps):
 // x_J += S_J⁻¹ v_J over the chunks (I, K0..K0+nK) of every symmetric root, grid-stride, no flags.
-__global__ void __launch_bounds__(NT, 3) k_symroot_gemv(DevFactor F, double* x, int64_t c_begin, int64_t c_end,
-                                                         const int* done_flag) {
+template <int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* x, int64_t c_begin, int64_t c_end,
+                                                           const int* done_flag) {
   __shared__ double vK[512];
   __shared__ double vI[64];
   __shared__ double red[576];
@@ -1193,7 +1196,7 @@ __global__ void __launch_bounds__(NT, 3) k_symroot_gemv(DevFactor F, double* x, 
     if (tid < Rn) vI[tid] = F.vbuf[rI + tid];
     __syncthreads();
     const int64_t ldx = F.sn_ldx[J];
-    schunk_gemv(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
+    schunk_gemv<U>(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
     if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
     for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
   }
@@ -1202,7 +1205,17 @@ __global__ void __launch_bounds__(NT, 3) k_symroot_gemv(DevFactor F, double* x, 
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
                   cudaStream_t s) {
   if (c_end <= c_begin) return;
-  k_symroot_gemv<<<grid, NT, 0, s>>>(F, x, c_begin, c_end, done_flag);
+  static int variant = std::getenv("QPB_GEMV_VARIANT") ? std::atoi(std::getenv("QPB_GEMV_VARIANT")) : 1;
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  switch (variant) {
+    case 1: k_symroot_gemv<8, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
+    case 2: k_symroot_gemv<16, 2><<<sms * 2, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
+    case 3: k_symroot_gemv<16, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
+    case 4: k_symroot_gemv<4, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
+    default: k_symroot_gemv<8, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
+  }
+  (void)grid;
 }
 
 static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)TRSV_SMEM_DBL; }

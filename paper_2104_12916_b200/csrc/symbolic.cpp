@@ -72,7 +72,7 @@ static inline int64_t tile_begin(int64_t t, int64_t nk, int64_t w, int64_t m) {
   return v < m ? v : m;
 }
 
-std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot) {
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot, int64_t trailing_from) {
   const int64_t N = M.N;
   S.N = N;
   // ---------------------------------------------------------------- row form of the strict lower part
@@ -223,6 +223,30 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
         ++merged;
       }
       if (merged == 0) break;
+    }
+  }
+  // forced dense trailing supernode (absorbed top of the tree, see api.cu analyse_F)
+  S.trailing_from = trailing_from;
+  if (trailing_from >= 0 && trailing_from < N) {
+    int64_t last = -1, first = -1;
+    for (int64_t J = 0; J < nf; ++J)
+      if (alive[J]) {
+        if (rc0[J] + rw[J] > trailing_from && first < 0) first = J;
+        last = J;
+      }
+    if (first >= 0 && last >= 0 && first != last) {
+      int64_t t = 0, wsum = 0;
+      for (int64_t J = first; J <= last; ++J)
+        if (alive[J]) {
+          t += rtrue[J];
+          wsum += rw[J];
+          if (J != last) alive[J] = 0;
+        }
+      rc0[last] = N - wsum;
+      rw[last] = wsum;
+      rm[last] = wsum;
+      rtrue[last] = t;
+      if (fb_ptr[last + 1] != fb_ptr[last]) return "trailing merge: last supernode has rows below (internal error)";
     }
   }
   // relaxed partition (alive supernodes, in column order)

@@ -49,6 +49,7 @@ struct Symbolic {
   std::vector<int64_t> parent, colcount, rowlev;
   int64_t nnz_L = 0, n_rowlev = 0;
   int64_t nnz_stored = 0;          // entries stored by the relaxed supernodes (≥ nnz_L)
+  int64_t trailing_from = -1;       // see analyse()
   int64_t sym_true = 0;            // true nnz(L) in the columns of symmetric roots
   int64_t sym_lower = 0;           // w(w+1)/2 summed over symmetric roots (entries of S⁻¹ read per solve)
   double c_fact = 0;              // Σ cc²
@@ -136,6 +137,10 @@ std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr,
                                      const std::vector<int64_t>& order);
 
 // Full symbolic analysis + multifrontal / trsv plans.  Returns "" or an error.
-std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot = true);
+// trailing_from ≥ 0: after amalgamation, every supernode reaching column trailing_from or beyond is merged
+// with the last supernode into one dense trailing supernode (requires that block to be closed: the
+// ancestor-closed top of the tree reordered to the end).
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot = true,
+                    int64_t trailing_from = -1);
 
 }  // namespace qpb

@@ -45,7 +45,7 @@ def test_host_symbolic_matches_oracle(name):
     perm = a.structure("perm")
     assert sorted(perm[:qp.n].tolist()) == list(range(qp.n))
     assert perm[qp.n:].tolist() == list(range(qp.n, qp.n + qp.m1))      # λ block last, in row order
-    ref = symbolic.analyse(qp.H, qp.A, perm[:qp.n])
+    ref = symbolic.analyse(qp.H, qp.A, perm[:qp.n], trailing_from=int(a.structure("trailing_from")[0]))
     for k in KEYS:
         assert symbolic.struct_hash(a.structure(k)) == symbolic.struct_hash(ref[k]), k
     st = a.stats()

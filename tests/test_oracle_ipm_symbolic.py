@@ -193,3 +193,21 @@ def test_cost_model_hand_cases():
     hand = 123 + costs.c_spmm_BDBt(qp.C) + sum(4 * t + 2 * s + 2 * k * t + 2 * k * s + 11 + 2 * k * tp
                                                for k in (3, 4)) + 2 * rhs
     assert costs.ph_kf(qp, 123, 45, 11, 7, [3, 4]) == hand
+
+
+@pytest.mark.parametrize("k", [3, 9])
+def test_symbolic_trailing_merge(k):
+    """Forced dense trailing supernode: the last supernode starts at or before column N−k, its rows
+    are exactly its columns (a trailing block of a lower-triangular factor is closed), and every
+    column's true structure is covered."""
+    qp = qpgen.scaled_random_qp(40, 8, 20, seed=k, g_nnz=2, a_nnz=2, c_nnz=2)
+    base = symbolic.analyse(qp.H, qp.A)
+    N = base["N"]
+    st = symbolic.analyse(qp.H, qp.A, trailing_from=N - k)
+    s0 = st["sn_start"][-2]
+    assert s0 <= N - k
+    rows = st["sn_rows"][st["sn_rowptr"][-2]:st["sn_rowptr"][-1]]
+    assert rows.tolist() == list(range(s0, N))
+    for j in range(s0, N):
+        assert set(st["struct"][j].tolist()) <= set(rows.tolist())
+    assert st["nnz_L"] == base["nnz_L"] and st["colcount"].tolist() == base["colcount"].tolist()
