@@ -207,6 +207,9 @@ struct qp_ctx {
   double t_factor_ph = 0;
   int64_t ph_refactors = 0;
   int64_t launches = 0;           // kernel launches issued by this context
+  cudaGraphExec_t pcg_graph[3] = {nullptr, nullptr, nullptr};   // GCH PCG iterations per preconditioner
+  bool use_graphs = true;
+  int graph_launches_per_chunk = 0;
   double last_eps = 0;            // PCG tolerance of the last IPM iteration
 
   // vectors
@@ -274,6 +277,8 @@ struct qp_ctx {
   }
   ~qp_ctx() {
     harvest();
+    for (auto& g : pcg_graph)
+      if (g) cudaGraphExecDestroy(g);
     for (auto e : pool) cudaEventDestroy(e);
     if (h_pst) cudaFreeHost(h_pst);
     if (h_ist) cudaFreeHost(h_ist);
@@ -663,23 +668,48 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
     pcg_init_ph(m2, c->pr, c->pz, c->pp, c->partial, c->pst, c->vgrid, st);
     c->launches += 1;
   }
+  auto body = [&]() {
+    kf_apply_dev(c, D, c->pp, c->pq, true);
+    int hh = c->begin(3);
+    pcg_update1(prec, m2, D, c->pp, c->pq, c->px, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
+    c->end(hh);
+    if (prec == 2) {
+      ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
+      pcg_rz_ph(m2, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
+    }
+    hh = c->begin(3);
+    pcg_update2(m2, c->pz, c->pp, c->pst, c->vgrid, st);
+    c->end(hh);
+    c->launches += prec == 2 ? 3 : 2;
+  };
+  // CUDA graph of GCH iterations (kernels exit early once the device `done` flag is set); the
+  // operands are the context's fixed buffers, so one graph per preconditioner is reused.
+  constexpr int GCH = 8;
+  const bool graphs = c->use_graphs && !c->prof && D == c->Dk;
+  if (graphs && !c->pcg_graph[prec]) {
+    int64_t l0 = c->launches;
+    cudaGraph_t g;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      for (int k = 0; k < GCH; ++k) body();
+      if (cudaStreamEndCapture(st, &g) == cudaSuccess) {
+        if (cudaGraphInstantiate(&c->pcg_graph[prec], g, 0) != cudaSuccess) c->pcg_graph[prec] = nullptr;
+        cudaGraphDestroy(g);
+      }
+    }
+    cudaGetLastError();
+    c->launches = l0;
+    c->graph_launches_per_chunk = 0;
+  }
   int chunk = 2;
   for (int it = 0; it < maxit + 1;) {
-    for (int k = 0; k < chunk; ++k) {
-      kf_apply_dev(c, D, c->pp, c->pq, true);
-      h = c->begin(3);
-      pcg_update1(prec, m2, D, c->pp, c->pq, c->px, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
-      c->end(h);
-      if (prec == 2) {
-        ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
-        pcg_rz_ph(m2, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
-      }
-      h = c->begin(3);
-      pcg_update2(m2, c->pz, c->pp, c->pst, c->vgrid, st);
-      c->end(h);
-      c->launches += prec == 2 ? 3 : 2;
+    if (graphs && c->pcg_graph[prec] && it >= 2) {
+      cudaGraphLaunch(c->pcg_graph[prec], st);
+      c->launches += (prec == 2 ? 11 : 6) * GCH;
+      it += GCH;
+    } else {
+      for (int k = 0; k < chunk; ++k) body();
+      it += chunk;
     }
-    it += chunk;
     cudaMemcpyAsync(c->h_pst, c->pst, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
     int rc = sync_check(c, "pcg");
     if (rc) return rc;
@@ -974,6 +1004,7 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
     c->own_stream = true;
   }
   c->tgrid = trsv_grid(c->device);
+  c->use_graphs = std::getenv("QPB_NO_GRAPH") == nullptr;
   if (std::getenv("QPB_VERBOSE")) std::fprintf(stderr, "qpb: trsv grid %d CTAs on %d SMs\n", c->tgrid, c->sm_count);
   cudaMallocHost(&c->h_pst, sizeof(PcgState));
   cudaMallocHost(&c->h_ist, sizeof(IpmState));
