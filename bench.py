@@ -268,13 +268,13 @@ def run_ours(args, rank, world, local, use_dist):
     torch.cuda.synchronize(dev)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    rp = s.ipm_iterate(K)
+    r_prof = s.ipm_iterate(K)
     p1.record(stream)
     torch.cuda.synchronize(dev)
     ms_prof = p0.elapsed_time(p1)
     prof = s.profile_read()
     s.profile(False)
-    pcg_prof = int(sum(rp["pcg_iters"][W:W + K]))
+    pcg_prof = int(sum(r_prof["pcg_iters"][W:W + K]))
 
     # ---------------------------------------------------------------- e2e replay through the C ABI
     e2e = None
@@ -325,7 +325,7 @@ def run_ours(args, rank, world, local, use_dist):
             pass
     fwd_ms, fwd_n = prof["f_fwd"]
     bwd_ms, bwd_n = prof["f_bwd"]
-    n_ipm_timed = max(0, min(K, rp["n_ipm"] - W))
+    n_ipm_timed = max(0, min(K, r_prof["n_ipm"] - W))
     real_solves = pcg_prof + 2 * n_ipm_timed          # K_F products + r_ν and recovery F-solves (profiled pass)
     solve_ms = fwd_ms + bwd_ms
     fsolve_bytes = st["fsolve_bytes_F"]
