@@ -205,6 +205,13 @@ int qp_profile_read(qp_ctx* ctx, double* ms /*8*/, int64_t* count /*8*/);
  * XCHUNK, SNF, SCHUNK, ROOTB] × [count, wait ns, busy ns, first start ns, last end ns]. */
 int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
 
+/* Debug: per-task trace of the sweeps profiled by the last enable/disable pair of
+ * qp_debug_sweep_profile.  sweep 0 = forward, 1 = backward.  Writes min(cap, #tasks)
+ * records of 4 int64 to out (host, caller-owned), indexed by dispatch ticket:
+ * [task word | SM id << 32, start ns, dependency-met ns, end ns] (globaltimer).
+ * Returns the number of records, or a negative qp_status. */
+int64_t qp_debug_sweep_trace(qp_ctx* ctx, int32_t sweep, int64_t* out, int64_t cap);
+
 const char* qp_last_error(const qp_ctx* ctx);
 void qp_free(qp_ctx* ctx);
 

@@ -103,6 +103,8 @@ def load_library(build: bool = True):
     lib.qp_profile.argtypes = [vp, i32]
     lib.qp_profile_read.argtypes = [vp, vp, vp]
     lib.qp_debug_sweep_profile.argtypes = [vp, i32, vp]
+    lib.qp_debug_sweep_trace.argtypes = [vp, i32, vp, i64]
+    lib.qp_debug_sweep_trace.restype = i64
     lib.qp_ipm_last_system.argtypes = [vp, vp, vp, C.POINTER(dbl)]
     lib.qp_launch_count.argtypes = [vp]
     lib.qp_launch_count.restype = i64
@@ -279,6 +281,13 @@ class QPSolver:
         out = np.zeros(70, dtype=np.int64)
         self._check(self.lib.qp_debug_sweep_profile(self.ctx, 1 if enable else 0, out.ctypes.data))
         return out.reshape(2, 7, 5)
+
+    def debug_sweep_trace(self, sweep, cap=1 << 20):
+        out = np.zeros((cap, 4), dtype=np.int64)
+        n = int(self.lib.qp_debug_sweep_trace(self.ctx, int(sweep), out.ctypes.data, cap))
+        if n < 0:
+            self._check(n)
+        return out[:n]
 
     def ipm_last_system(self):
         D, r = np.zeros(self.m2), np.zeros(self.m2)

@@ -355,6 +355,7 @@ void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref
 // Task types (symbolic.h): 0 DIAG(b), 1 TILE(t), 2 PREP(b), 3 XTILE(x); index in the low 29 bits.
 struct SweepShared {
   int task;
+  unsigned ticket;
   unsigned epoch;
   double rhs[64];
   double y[64];
@@ -386,9 +387,22 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 // instrumentation: per sweep (0 fwd, 1 bwd) and task type: count, wait ns, busy ns, first start, last end
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int type, unsigned long long t0,
-                                          unsigned long long t1, unsigned long long t2) {
+                                          unsigned long long t1, unsigned long long t2, int task = 0,
+                                          unsigned ticket = 0, int64_t cap = 0) {
   if (tp == nullptr || threadIdx.x != 0) return;
+  if ((int64_t)ticket < cap) {  // per-task trace: [task | smid<<32, t0, t1, t2]
+    unsigned long long* r = tp + 70 + ((int64_t)sweep * cap + ticket) * 4;
+    r[0] = (unsigned long long)(unsigned)task | ((unsigned long long)smid() << 32);
+    r[1] = t0;
+    r[2] = t1;
+    r[3] = t2;
+  }
   unsigned long long* q = tp + (sweep * 7 + type) * 5;
   atomicAdd(q + 0, 1ull);
   atomicAdd(q + 1, t1 - t0);
@@ -556,6 +570,30 @@ __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_
   __syncthreads();
 }
 
+// Right-hand side of block columns c0..c0+wk-1 into rhs[] (visible after the caller's barrier):
+// either the given vector, or (Cᵀp)_c gathered warp-per-column so all the CTA's loads are in flight.
+__device__ __forceinline__ void sweep_rhs(const SweepRhs& R, int64_t c0, int wk, double* rhs) {
+  const int tid = threadIdx.x;
+  if (R.ct.p == nullptr) {
+    if (tid < wk) {
+      const int64_t c = c0 + tid;
+      rhs[tid] = R.rhs[R.in_perm ? R.in_perm[c] : c];
+    }
+    return;
+  }
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int j = wid; j < wk; j += NT / 32) {
+    const int64_t c = c0 + j;
+    double v = 0.0;
+    if (c < R.ct.nrows) {
+      const int64_t q0 = __ldg(R.ct.p + c), q1 = __ldg(R.ct.p + c + 1);
+      for (int64_t q = q0 + lane; q < q1; q += 32) v += __ldg(R.ct.v + q) * __ldg(R.p + __ldg(R.ct.i + q));
+      v = warp_sum(v);
+    }
+    if (lane == 0) rhs[j] = v;
+  }
+}
+
 // Forward sweep L y = b (unit lower L, factor order); y written to x.
 __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double* x) {
   extern __shared__ double sm[];
@@ -569,6 +607,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
     if (tid == 0) {
       unsigned t = atomicAdd(F.sweep + 0, 1u);
       S.task = t < (unsigned)F.n_fwd_tasks ? F.fwd_tasks[t] : -1;
+      S.ticket = t;
     }
     __syncthreads();
     const int task = S.task;
@@ -590,13 +629,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
           sm[c * 65 + r] = __ldg(inv + i2);
         }
       }
-      if (tid < wk) {
-        const int64_t c = c0 + tid;
-        double v;
-        if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
-        else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
-        S.rhs[tid] = v;
-      }
+      sweep_rhs(R, c0, wk, S.rhs);
       if (tid == 0) {
         spin_u64(F.cnt_f + J, (unsigned long long)E * (unsigned long long)F.fwd_expect[J]);
         if (F.tprof) t1 = gtime();
@@ -616,17 +649,19 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         S.red[g * 64 + i] = s;
         __syncthreads();
         if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
-        __threadfence();
         __syncthreads();
-        if (tid == 0) st_rel_u32(F.ready_f + b, E);
+        if (tid == 0) {
+          __threadfence();
+          st_rel_u32(F.ready_f + b, E);
+        }
       } else {
         if (tid < wk) {
           F.vbuf[c0 + tid] = S.rhs[tid];
           x[c0 + tid] = 0.0;
         }
-        __threadfence();
         __syncthreads();
         if (tid == 0) {
+          __threadfence();
           // keep the X-path counters in step when the symmetric root bypasses them
           if (F.use_sym && F.sn_sinv[J] >= 0) atomicAdd(F.cntx_f + b, (unsigned long long)F.xexp_f[b]);
           st_rel_u32(F.vready_f + b, E);
@@ -662,13 +697,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         prefetch_block(L, noff, wk, noff);
         for (int64_t r = (int64_t)tid * 32; r < noff; r += (int64_t)NT * 32) prefetch_l2(rows + r);
       }
-      if (tid < wk) {
-        const int64_t c = c0 + tid;
-        double v;
-        if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
-        else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
-        S.rhs[tid] = v;
-      }
+      sweep_rhs(R, c0, wk, S.rhs);
       if (tid == 0) {
         spin_u64(F.cnt_f + J, (unsigned long long)E * (unsigned long long)F.fwd_expect[J]);
         if (F.tprof) t1 = gtime();
@@ -713,10 +742,11 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
           }
         }
       }
-      __threadfence();
       __syncthreads();
-      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT)
+      for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) {
+        __threadfence();
         red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
+      }
     } else if (type == 5) {
       // ---------------- SCHUNK: symmetric root — x_I += S_IK v_K, x_K += S_IKᵀ v_I (K < I)
       const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
@@ -759,9 +789,9 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       const int64_t ldx = F.sn_ldx[J];
       xchunk_gemv(F.xinv + F.sn_xinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, sm, red);
       if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
-      __threadfence();
       __syncthreads();
       if (tid == 0) {
+        __threadfence();
         unsigned long long old = atomicAdd(F.cntx_f + bI, 1ull);
         if (old + 1 == (unsigned long long)E * (unsigned long long)F.xexp_f[bI]) {
           __threadfence();
@@ -797,11 +827,13 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
           atomicAdd(F.acc + rows[r], s);
         }
       }
-      __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(F.cnt_f + F.tile_dest[ti], 1ull);
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(F.cnt_f + F.tile_dest[ti], 1ull);
+      }
     }
-    if (F.tprof) tprof_add(F.tprof, 0, type, t0, t1, gtime());
+    if (F.tprof) tprof_add(F.tprof, 0, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap);
   }
   if (tid == 0) {
     unsigned d = atomicAdd(F.sweep + 1, 1u);
@@ -827,6 +859,7 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
     if (tid == 0) {
       unsigned t = atomicAdd(F.sweep + 0, 1u);
       S.task = t < (unsigned)F.n_bwd_tasks ? F.bwd_tasks[t] : -1;
+      S.ticket = t;
     }
     __syncthreads();
     const int task = S.task;
@@ -867,17 +900,21 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
         S.red[g * 64 + i] = s;
         __syncthreads();
         if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
-        __threadfence();
         __syncthreads();
-        if (tid == 0) st_rel_u32(F.ready_sb + F.blk_sn[b], E);
+        if (tid == 0) {
+          __threadfence();
+          st_rel_u32(F.ready_sb + F.blk_sn[b], E);
+        }
       } else {
         if (tid < wk) {
           F.vbuf[c0 + tid] = S.rhs[tid];
           x[c0 + tid] = 0.0;
         }
-        __threadfence();
         __syncthreads();
-        if (tid == 0) st_rel_u32(F.vready_b + b, E);
+        if (tid == 0) {
+          __threadfence();
+          st_rel_u32(F.vready_b + b, E);
+        }
       }
     } else if (type == 4) {
       // ---------------- SNF(b) backward: t = L_rowsᵀ x_rows (gather), x_b = L_bb⁻ᵀ (D⁻¹ y_b − t)
@@ -950,9 +987,11 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       }
       __syncthreads();
       if (tid < wk) x[c0 + tid] = S.red[tid] + S.red[64 + tid] + S.red[128 + tid] + S.red[192 + tid];
-      __threadfence();
       __syncthreads();
-      if (tid == 0) st_rel_u32(F.ready_sb + J, E);
+      if (tid == 0) {
+        __threadfence();
+        st_rel_u32(F.ready_sb + J, E);
+      }
     } else if (type == 6) {
       // ---------------- ROOTB: the symmetric root's x = S⁻¹ v was completed by the forward sweep
       const int J = idx;
@@ -981,9 +1020,9 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       const int64_t ldx = F.sn_ldx[J];
       xchunk_gemv(F.xinv + F.sn_xtr[J] + (rK - cJ) + (cI - cJ) * ldx, ldx, Rn, ncol, sm, red);
       if (tid < Rn) atomicAdd(x + rK + tid, red[512 + tid]);
-      __threadfence();
       __syncthreads();
       if (tid == 0) {
+        __threadfence();
         unsigned long long old = atomicAdd(F.cntx_b + bK, 1ull);
         if (old + 1 == (unsigned long long)E * (unsigned long long)F.xexp_b[bK]) {
           __threadfence();
@@ -1014,11 +1053,13 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       __syncthreads();
       tile_gemv_t(sm, Rn, wk, xr, S.red);
       if (tid < wk) atomicAdd(F.tacc + c0 + tid, S.red[tid]);
-      __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(F.cnt_b + b, 1ull);
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(F.cnt_b + b, 1ull);
+      }
     }
-    if (F.tprof) tprof_add(F.tprof, 1, type, t0, t1, gtime());
+    if (F.tprof) tprof_add(F.tprof, 1, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap);
   }
   if (tid == 0) {
     unsigned d = atomicAdd(F.sweep + 1, 1u);

@@ -92,7 +92,8 @@ struct DevFactor {
   const int64_t* pan_pref;
   const int64_t* upd_pref;
   int* status;        // pivot failures (device int)
-  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][5 types][5]
+  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][7 types][5] + per-task trace
+  int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
 };
 

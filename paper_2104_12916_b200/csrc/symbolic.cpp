@@ -494,10 +494,24 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   sn_xb0[ns] = (int64_t)S.xb_bK.size();
   if ((int64_t)S.xt_bI.size() >= (int64_t(1) << TASK_SHIFT) || (int64_t)S.tile_blk.size() >= (int64_t(1) << TASK_SHIFT))
     return "too many sweep tasks for the 28-bit task encoding";
+  // Level-major dispatch: the forward queue by height (leaves first), the backward queue by depth
+  // (root first), each stable in postorder.  Every dependency of a task is dispatched before it,
+  // and no CTA holding a waiting task blocks the dispatch of a task of an earlier wave.
+  std::vector<int32_t> fwd_order(ns), bwd_order(ns);
+  {
+    std::vector<int64_t> depth(ns, 0);
+    for (int64_t J = ns - 1; J >= 0; --J)
+      if (S.sn_parent[J] >= 0) depth[J] = depth[S.sn_parent[J]] + 1;
+    for (int64_t J = 0; J < ns; ++J) fwd_order[J] = bwd_order[J] = (int32_t)J;
+    std::stable_sort(fwd_order.begin(), fwd_order.end(),
+                     [&](int32_t a, int32_t b) { return S.sn_level[a] < S.sn_level[b]; });
+    std::stable_sort(bwd_order.begin(), bwd_order.end(),
+                     [&](int32_t a, int32_t b) { return depth[a] < depth[b]; });
+  }
   auto build_queues = [&](bool use_sym, std::vector<int32_t>& fq, std::vector<int32_t>& bq) {
     fq.clear();
     bq.clear();
-    for (int64_t J = 0; J < ns; ++J) {
+    for (int32_t J : fwd_order) {
       const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
       const bool sym = use_sym && S.sn_sinv[J] >= 0;
       if (S.sn_xinv[J] < 0) {
@@ -513,7 +527,7 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
           for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) fq.push_back(enc(1, t));
       }
     }
-    for (int64_t J = ns - 1; J >= 0; --J) {
+    for (int32_t J : bwd_order) {
       const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
       const bool sym = use_sym && S.sn_sinv[J] >= 0;
       if (S.sn_xinv[J] < 0) {

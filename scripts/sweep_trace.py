@@ -1,0 +1,43 @@
+"""Per-task timeline of the F-solve sweeps (debug): which level / task type is on the critical path."""
+import sys
+import numpy as np
+sys.path.insert(0, '.')
+import qpgen
+from paper_2104_12916_b200.binding import from_qp
+
+qp = qpgen.make(sys.argv[1] if len(sys.argv) > 1 else 'c1')
+s = from_qp(qp)
+s.ipm_factor_once('low')
+ss = s.structure('sn_start'); lev = s.structure('sn_level')
+w = np.diff(ss)
+nblk = (w + 63) // 64
+blk_sn = np.repeat(np.arange(len(w)), nblk)
+rng = np.random.default_rng(0)
+D = rng.uniform(0.5, 2, qp.m2); p = rng.standard_normal(qp.m2)
+for rep in range(3):
+    s.kf_apply(D, p)
+s.debug_sweep_profile(True); s.kf_apply(D, p); s.debug_sweep_profile(False)
+names = ['DIAG', 'TILE', 'PREP', 'XCHUNK', 'SNF', 'SCHUNK', 'ROOTB']
+for sw in range(2):
+    tr = s.debug_sweep_trace(sw)
+    task = tr[:, 0] & 0xffffffff
+    sm = tr[:, 0] >> 32
+    typ, idx = task >> 28, task & ((1 << 28) - 1)
+    t0 = tr[:, 1].min()
+    a, b, c = (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3, (tr[:, 3] - t0) / 1e3
+    L = np.where(np.isin(typ, [0, 2, 4]), lev[blk_sn[np.minimum(idx, len(blk_sn) - 1)]], -1)
+    print(['fwd', 'bwd'][sw], 'tasks', len(tr), 'span %.1f us' % c.max(), 'SMs used', len(np.unique(sm)))
+    for ty in np.unique(typ):
+        for lv in np.unique(L[typ == ty]):
+            k = (typ == ty) & (L == lv)
+            print('  %-6s lev %2d n %4d  start[min %.1f max %.1f]  dep-met[med %.1f max %.1f]  end[med %.1f max %.1f]  busy %.2f'
+                  % (names[ty], lv, k.sum(), a[k].min(), a[k].max(), np.median(b[k]), b[k].max(),
+                     np.median(c[k]), c[k].max(), np.mean(c[k] - b[k])))
+    order = np.argsort(b)
+    print('  tickets: first 5 types', [names[t] for t in typ[:5]], 'last 5', [names[t] for t in typ[-5:]])
+    st = a
+    print('  start time by ticket decile:', ['%.1f' % np.median(st[i:i + len(st) // 10]) for i in range(0, len(st), len(st) // 10)])
+    print('  setup (dep-met - start) by type:', {names[t]: '%.2f' % np.median((b - a)[typ == t]) for t in np.unique(typ)})
+    print('  tasks per SM: min %d max %d' % (np.bincount(sm).min(), np.bincount(sm).max()))
+    k = typ == 4
+    print('  SNF start quantiles', np.percentile(a[k], [10, 50, 90]).round(1), 'dep-start quantiles', np.percentile((b - a)[k], [10, 50, 90]).round(1))
