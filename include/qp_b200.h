@@ -76,16 +76,38 @@ typedef enum {
   QP_PREC_HIGH = 2  /* PH-KF: P_H = D + C diag(H)^-1 C^T, Cholesky per IPM iteration */
 } qp_precond;
 
+/* Cross-rank collective used by the sharded mode instead of NCCL (optional).
+ * In-place all-reduce of `count` doubles at DEVICE pointer buf, ordered on the
+ * cudaStream_t `stream` (the call may synchronise it); op: 0 sum, 1 max, 2 min.
+ * Every rank must produce bit-identical results.  Return 0 on success. */
+typedef int (*qp_allreduce_fn)(void* user, double* buf, int64_t count, int32_t op, void* stream);
+
 typedef struct {
   int device;              /* CUDA device ordinal */
   void* stream;            /* cudaStream_t or NULL */
   int rank, world;         /* SPMD rank / size; world = 1 for single GPU */
-  const void* nccl_uid;    /* 128-byte ncclUniqueId (world > 1) or NULL */
+  const void* nccl_uid;    /* 128-byte ncclUniqueId from qp_nccl_unique_id on rank 0,
+                              broadcast by the caller (sharded mode), or NULL */
   const int64_t* x_perm;   /* optional fill-reducing order of the x block (new→old,
                               length n); NULL = the library's minimum-degree order */
   int vectors_on_device;   /* see Conventions */
   int64_t workspace_limit_bytes; /* multifrontal workspace cap; 0 = 120 GiB */
+  qp_allreduce_fn allreduce;     /* optional collective provider (sharded mode), else NULL */
+  void* allreduce_user;          /* passed to allreduce */
 } qp_setup_opts;
+
+/* Sharded mode (enabled when world > 1, nccl_uid != NULL or
+ * allreduce != NULL).  Every rank calls every entry point collectively with the
+ * same GLOBAL H, A, C, g, b, d.  The m2 inequality rows are split into
+ * contiguous nnz-balanced slices (qp_partition_rows); rank r owns rows
+ * [row0, row1) (qp_get_partition): its slices of C, d, D, ν, s and of every
+ * PCG vector.  Per PCG iteration the partial products C_rᵀp_r are all-reduced
+ * (n doubles) before the replicated F-solve, and the three PCG reductions are
+ * all-reduced (the north_star's "dot products NCCL-allreduced"); the IPM
+ * all-reduces Cᵀν, CᵀΔν, μ, ‖r_i‖∞ and α_max.  The x-space (x, λ, F-solves)
+ * is replicated.  Then the m2-length arguments of pcg_solve, qp_kf_apply and
+ * the nu / s buffers of qp_ipm_result are the rank's (row1 − row0)-row slice;
+ * ipm_factor_once(QP_PREC_HIGH) returns QP_EINVAL (P_H couples all rows). */
 
 /* Copy the QP to the GPU and validate it.  H: full symmetric n×n (both
  * triangles stored); A: m1×n, m1 >= 0 (m1 = 0 ⇒ F = −H); C: m2×n, m2 >= 1.
@@ -211,6 +233,19 @@ int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
  * [task word | SM id << 32, start ns, dependency-met ns, end ns] (globaltimer).
  * Returns the number of records, or a negative qp_status. */
 int64_t qp_debug_sweep_trace(qp_ctx* ctx, int32_t sweep, int64_t* out, int64_t cap);
+
+/* Host-only: the contiguous split of m2 rows (CSR indptr, m2+1 entries) over
+ * `world` ranks balancing nnz+1 per row; bounds (caller-owned, world+1 entries)
+ * receives row offsets, bounds[0] = 0, bounds[world] = m2.  Deterministic. */
+int qp_partition_rows(const int64_t* indptr, int64_t m2, int32_t world, int64_t* bounds);
+
+/* This context's inequality-row slice [row0, row1) of m2_global rows (row0 = 0,
+ * row1 = m2_global when not sharded).  Any pointer may be NULL. */
+int qp_get_partition(qp_ctx* ctx, int64_t* row0, int64_t* row1, int64_t* m2_global);
+
+/* Host-only: a fresh ncclUniqueId (128 bytes into out) for qp_setup_opts.nccl_uid.
+ * NCCL is loaded on demand (dlopen libnccl.so.2); QP_ENCCL when unavailable. */
+int qp_nccl_unique_id(void* out);
 
 const char* qp_last_error(const qp_ctx* ctx);
 void qp_free(qp_ctx* ctx);

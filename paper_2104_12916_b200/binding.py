@@ -38,10 +38,15 @@ class _CSR(C.Structure):
                 ("indices", C.c_void_p), ("values", C.c_void_p)]
 
 
+# int (*)(void* user, double* buf, int64_t count, int32_t op, void* stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+
+
 class _SetupOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_uid", C.c_void_p), ("x_perm", C.c_void_p), ("vectors_on_device", C.c_int),
-                ("workspace_limit_bytes", C.c_int64)]
+                ("workspace_limit_bytes", C.c_int64), ("allreduce", ALLREDUCE_FN),
+                ("allreduce_user", C.c_void_p)]
 
 
 class _IpmOpts(C.Structure):
@@ -98,6 +103,9 @@ def load_library(build: bool = True):
     lib.qp_f_solve.argtypes = [vp, vp, vp]
     lib.qp_kf_apply.argtypes = [vp, vp, vp, vp]
     lib.qp_analyse.argtypes = [C.POINTER(vp), C.POINTER(_CSR), C.POINTER(_CSR), vp]
+    lib.qp_partition_rows.argtypes = [vp, i64, i32, vp]
+    lib.qp_get_partition.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+    lib.qp_nccl_unique_id.argtypes = [vp]
     lib.qp_get_structure.argtypes = [vp, i32, vp, C.POINTER(i64)]
     lib.qp_get_stats.argtypes = [vp, C.POINTER(_Stats)]
     lib.qp_profile.argtypes = [vp, i32]
@@ -123,6 +131,26 @@ def exported_symbols():
     return sorted({ln.split()[-1] for ln in out.splitlines() if " T " in ln})
 
 
+def partition_rows(indptr, m2, world):
+    """qp_partition_rows: contiguous nnz-balanced split of m2 rows over `world` ranks (host only)."""
+    lib = load_library()
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    out = np.zeros(world + 1, dtype=np.int64)
+    rc = lib.qp_partition_rows(ip.ctypes.data, int(m2), int(world), out.ctypes.data)
+    if rc != 0:
+        raise QPError(rc, "qp_partition_rows")
+    return out
+
+
+def nccl_unique_id():
+    """qp_nccl_unique_id: 128 bytes for QPSolver(nccl_uid=...) (rank 0 creates, caller broadcasts)."""
+    buf = C.create_string_buffer(128)
+    rc = load_library().qp_nccl_unique_id(buf)
+    if rc != 0:
+        raise QPError(rc, "qp_nccl_unique_id (NCCL unavailable)")
+    return buf.raw
+
+
 def _f64(a):
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
@@ -131,7 +159,11 @@ class QPSolver:
     """One qp_ctx: ``qp_setup`` on construction, ``qp_free`` on close."""
 
     def __init__(self, H, A, Cm, g, b, d, x_perm=None, device=0, stream=None, vectors_on_device=False,
-                 workspace_limit_bytes=0):
+                 workspace_limit_bytes=0, rank=0, world=1, nccl_uid=None, allreduce=None):
+        """rank / world / nccl_uid / allreduce select the sharded mode (qp_b200.h): every rank passes
+        the same global problem; m2-length vectors are then this rank's row slice
+        (``self.row0 : self.row0 + self.m2`` of ``self.m2_global``).  ``allreduce`` is a Python
+        callable ``f(buf_ptr, count, op, stream_ptr) -> int`` used instead of NCCL."""
         import scipy.sparse as sp
         self.lib = load_library()
         self.vectors_on_device = bool(vectors_on_device)
@@ -151,7 +183,15 @@ class QPSolver:
         opts = _SetupOpts()
         opts.device = device
         opts.stream = stream
-        opts.world = 1
+        opts.rank = rank
+        opts.world = world
+        if nccl_uid is not None:
+            uid = C.create_string_buffer(bytes(nccl_uid), 128)
+            self._keep.append(uid)
+            opts.nccl_uid = C.cast(uid, C.c_void_p)
+        if allreduce is not None:
+            self._ar = ALLREDUCE_FN(lambda user, buf, cnt, op, st: int(allreduce(buf, cnt, op, st)))
+            opts.allreduce = self._ar
         opts.vectors_on_device = 1 if vectors_on_device else 0
         opts.workspace_limit_bytes = workspace_limit_bytes
         if x_perm is not None:
@@ -163,6 +203,9 @@ class QPSolver:
                                b.ctypes.data if b.size else g.ctypes.data, d.ctypes.data, C.byref(opts))
         self._keep = []
         self._check(rc)
+        r0, r1, mg = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.lib.qp_get_partition(self.ctx, C.byref(r0), C.byref(r1), C.byref(mg)))
+        self.row0, self.m2, self.m2_global = int(r0.value), int(r1.value - r0.value), int(mg.value)
 
     # -------------------------------------------------------------- plumbing
     def _check(self, rc, ok=(0,)):

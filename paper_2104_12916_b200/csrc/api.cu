@@ -3,6 +3,8 @@
 // the kernels of kernels.cu; this file does validation, symbolic planning
 // (symbolic.cpp), device memory, and the IPM / PCG control flow.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -10,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <cstddef>
 #include <functional>
 #include <memory>
 #include <string>
@@ -25,6 +28,51 @@ namespace {
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// NCCL, loaded on first use (only sharded runs need it; single-GPU builds never touch it).
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    api.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return api;
+  }
+  api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
+  api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
+  api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
+  api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
+  api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+  api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy && api.error_string;
+  if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
+  return api;
+}
+
+// Contiguous split of the m2 inequality rows over `world` ranks, balancing nnz + 1 per row.
+void partition_rows(const int64_t* indptr, int64_t m2, int world, int64_t* bounds) {
+  const double total = (double)(indptr[m2] - indptr[0]) + (double)m2;
+  bounds[0] = 0;
+  int64_t i = 0;
+  for (int r = 1; r < world; ++r) {
+    const double target = total * r / world;
+    while (i < m2 && (double)(indptr[i] - indptr[0]) + (double)i < target) ++i;
+    bounds[r] = std::max<int64_t>(i, bounds[r - 1]);
+  }
+  bounds[world] = m2;
 }
 
 struct HostCSR {
@@ -175,6 +223,15 @@ struct qp_ctx {
   bool own_stream = false;
   int vectors_on_device = 0;
   int rank = 0, world = 1;
+  // sharded ν rows: this rank owns inequality rows [row0, row1) of m2_global;
+  // x-space work (F-solves, H, A) is replicated; Cᵀ(·) partial products and the PCG / IPM
+  // reductions are all-reduced (NCCL, or the caller's qp_allreduce_fn).
+  bool sharded = false;
+  int64_t m2_global = 0, row0 = 0, row1 = 0;
+  ncclComm_t nccl = nullptr;
+  qp_allreduce_fn ar_fn = nullptr;
+  void* ar_user = nullptr;
+  double* ubuf = nullptr;        // N: all-reduced Cᵀ(·) in factor order (λ part zero)
   int64_t ws_limit = 0;
   int64_t n = 0, m1 = 0, m2 = 0;
   HostCSR H, A, C;
@@ -275,8 +332,25 @@ struct qp_ctx {
     }
     evs.clear();
   }
+  // In-place all-reduce of cnt doubles on this context's stream (op: 0 sum, 1 max, 2 min).
+  int allreduce(double* buf, int64_t cnt, int op) {
+    if (!sharded || cnt <= 0) return 0;
+    if (ar_fn) {
+      int rc = ar_fn(ar_user, buf, cnt, op, (void*)stream);
+      if (rc != 0) err = "qp_allreduce_fn returned " + std::to_string(rc);
+      return rc != 0 ? QP_ENCCL : 0;
+    }
+    const ncclRedOp_t o = op == 0 ? ncclSum : (op == 1 ? ncclMax : ncclMin);
+    ncclResult_t r = nccl_api().all_reduce(buf, buf, (size_t)cnt, ncclFloat64, o, nccl, stream);
+    if (r != ncclSuccess) {
+      err = std::string("ncclAllReduce: ") + nccl_api().error_string(r);
+      return QP_ENCCL;
+    }
+    return 0;
+  }
   ~qp_ctx() {
     harvest();
+    if (nccl) nccl_api().comm_destroy(nccl);
     for (auto& g : pcg_graph)
       if (g) cudaGraphExecDestroy(g);
     for (auto e : pool) cudaEventDestroy(e);
@@ -585,6 +659,9 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
 }
 
 // y = F⁻¹ rhs (factor order, N), forward + backward sweeps.
+double* pst_red(qp_ctx* c) { return (double*)((char*)c->pst + offsetof(PcgState, red)); }
+double* ist_red(qp_ctx* c) { return (double*)((char*)c->ist + offsetof(IpmState, red)); }
+
 void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
   if (!F.sym_enabled) return;
   c->launches += 1;
@@ -605,12 +682,20 @@ void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
 }
 
 // q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
-void kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode) {
+int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode) {
   c->launches += 3;
   SweepRhs r{};
-  r.ct = c->Ctf;
-  r.p = p;
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
+  if (c->sharded) {
+    // u = Σ_ranks C_gᵀ p_g, then the replicated F-solve on [u; 0]
+    spmv(c->Ctf, p, c->ubuf, r.done_flag, c->vgrid, c->stream);
+    c->launches += 1;
+    if (int rc = c->allreduce(c->ubuf, c->n, 0)) return rc;
+    r.rhs = c->ubuf;
+  } else {
+    r.ct = c->Ctf;   // Cᵀp fused into the forward sweep (a1)
+    r.p = p;
+  }
   int h = c->begin(0);
   trsv_forward(c->FF.d, r, c->xbuf, c->tgrid, c->stream);
   sym_gemv(c, c->FF, c->xbuf, r.done_flag);
@@ -621,6 +706,12 @@ void kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool p
   h = c->begin(2);
   kf_q(c->Cf, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
   c->end(h);
+  if (c->sharded && pcg_mode) {
+    if (int rc = c->allreduce(pst_red(c), 1, 0)) return rc;
+    finalize(FIN_PCG_PQ, c->pst, c->ist, c->precond, c->stream);
+    c->launches += 1;
+  }
+  return 0;
 }
 
 // z = P_H⁻¹ r (a7), P_H factor order via perm_ph.
@@ -664,16 +755,26 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   pcg_init(prec, m2, b, D, c->px, c->pr, c->pz, c->pp, c->partial, c->pst, tol, maxit, c->vgrid, st);
   c->end(h);
   c->launches += 1;
+  if (c->sharded) {
+    if (int rc = c->allreduce(pst_red(c), 2, 0)) return rc;
+    finalize(FIN_PCG_INIT, c->pst, c->ist, prec, st);
+    c->launches += 1;
+  }
   if (prec == 2) {
     ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
     pcg_init_ph(m2, c->pr, c->pz, c->pp, c->partial, c->pst, c->vgrid, st);
     c->launches += 1;
   }
-  auto body = [&]() {
-    kf_apply_dev(c, D, c->pp, c->pq, true);
+  auto body = [&]() -> int {
+    if (int rc = kf_apply_dev(c, D, c->pp, c->pq, true)) return rc;
     int hh = c->begin(3);
     pcg_update1(prec, m2, D, c->pp, c->pq, c->px, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
     c->end(hh);
+    if (c->sharded) {
+      if (int rc = c->allreduce(pst_red(c), 2, 0)) return rc;
+      finalize(FIN_PCG_UPD1, c->pst, c->ist, prec, st);
+      c->launches += 1;
+    }
     if (prec == 2) {
       ph_apply_dev(c, c->pr, c->pz, &c->pst->done);
       pcg_rz_ph(m2, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);
@@ -682,11 +783,12 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
     pcg_update2(m2, c->pz, c->pp, c->pst, c->vgrid, st);
     c->end(hh);
     c->launches += prec == 2 ? 3 : 2;
+    return 0;
   };
   // CUDA graph of GCH iterations (kernels exit early once the device `done` flag is set); the
   // operands are the context's fixed buffers, so one graph per preconditioner is reused.
   constexpr int GCH = 8;
-  const bool graphs = c->use_graphs && !c->prof && D == c->Dk;
+  const bool graphs = c->use_graphs && !c->prof && D == c->Dk && !c->sharded;
   if (graphs && !c->pcg_graph[prec]) {
     int64_t l0 = c->launches;
     cudaGraph_t g;
@@ -708,7 +810,8 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
       c->launches += (prec == 2 ? 11 : 6) * GCH;
       it += GCH;
     } else {
-      for (int k = 0; k < chunk; ++k) body();
+      for (int k = 0; k < chunk; ++k)
+        if (int rc = body()) return rc;
       it += chunk;
     }
     cudaMemcpyAsync(c->h_pst, c->pst, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
@@ -826,15 +929,38 @@ void out_vec(qp_ctx* c, double* dst, const double* src_dev, int64_t m) {
                   c->stream);
 }
 
+// μ and the residuals (a9) at the current iterate; sharded: Cᵀν and the reductions all-reduced.
+int ipm_eval_residuals(qp_ctx* c) {
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n;
+  int h = c->begin(6);
+  ipm_mu(c->m2, c->s, c->nu, c->partial, c->ist, c->vgrid, st);
+  c->launches += 2;
+  const double* ctnu = nullptr;
+  if (c->sharded) {
+    if (int rc = c->allreduce(ist_red(c), 1, 0)) return rc;
+    finalize(FIN_IPM_MU, c->pst, c->ist, c->precond, st);
+    spmv(c->Ctf, c->nu, c->ubuf, nullptr, c->vgrid, st);
+    if (int rc = c->allreduce(c->ubuf, n, 0)) return rc;
+    ctnu = c->ubuf;
+    c->launches += 2;
+  }
+  ipm_residuals(c->Hf, c->Atf, c->Ctf, c->Af, c->Cf, c->gf, c->bv, c->dv, c->xl, c->xl + n, c->nu, c->s, c->rgre,
+                c->rc, c->ra, c->Dk, c->partial, c->ist, c->vgrid, st, ctnu);
+  if (c->sharded) {
+    if (int rc = c->allreduce(ist_red(c), 3, 1)) return rc;
+    finalize(FIN_IPM_RESID, c->pst, c->ist, c->precond, st);
+    c->launches += 1;
+  }
+  c->end(h);
+  return 0;
+}
+
 int ipm_iteration(qp_ctx* c, bool* converged) {
   cudaStream_t st = c->stream;
   const int64_t n = c->n, m1 = c->m1, m2 = c->m2, N = n + m1;
-  int h = c->begin(6);
-  ipm_mu(m2, c->s, c->nu, c->partial, c->ist, c->vgrid, st);
-  ipm_residuals(c->Hf, c->Atf, c->Ctf, c->Af, c->Cf, c->gf, c->bv, c->dv, c->xl, c->xl + n, c->nu, c->s, c->rgre,
-                c->rc, c->ra, c->Dk, c->partial, c->ist, c->vgrid, st);
-  c->end(h);
-  c->launches += 2;
+  int h;
+  if (int rc0 = ipm_eval_residuals(c)) return rc0;
   cudaMemcpyAsync(c->h_ist, c->ist, sizeof(IpmState), cudaMemcpyDeviceToHost, st);
   int rc = sync_check(c, "ipm residuals");
   if (rc) return rc;
@@ -861,11 +987,23 @@ int ipm_iteration(qp_ctx* c, bool* converged) {
   c->pcg_hist.push_back(iters);
   // recovery: F(Δx;Δλ) = −(r_g + CᵀΔν; r_e)
   h = c->begin(7);
-  ipm_recovery_rhs(c->Ctf, n, m1, c->rgre, c->px, c->rhs2, c->vgrid, st);
+  const double* ctdnu = nullptr;
+  if (c->sharded) {
+    spmv(c->Ctf, c->px, c->ubuf, nullptr, c->vgrid, st);
+    if ((rc = c->allreduce(c->ubuf, n, 0))) return rc;
+    ctdnu = c->ubuf;
+    c->launches += 1;
+  }
+  ipm_recovery_rhs(c->Ctf, n, m1, c->rgre, c->px, c->rhs2, c->vgrid, st, ctdnu);
   c->end(h);
   f_solve_dev(c, c->rhs2, c->dxl);
   h = c->begin(7);
   ipm_ds_alpha(m2, c->rc, c->nu, c->Dk, c->px, c->s, c->ds, c->partial, c->ist, c->vgrid, st);
+  if (c->sharded) {
+    if ((rc = c->allreduce(ist_red(c), 1, 2))) return rc;
+    finalize(FIN_IPM_ALPHA, c->pst, c->ist, c->precond, st);
+    c->launches += 1;
+  }
   ipm_update(N, m2, c->dxl, c->px, c->ds, c->xl, c->nu, c->s, c->ist, c->vgrid, st);
   c->end(h);
   c->ipm_k++;
@@ -968,9 +1106,37 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
   c->rank = o.rank;
   c->world = o.world <= 0 ? 1 : o.world;
   c->ws_limit = o.workspace_limit_bytes > 0 ? o.workspace_limit_bytes : (int64_t)120 << 30;
-  if (c->world != 1) {
-    *out = c.release();
-    return fail(*out, QP_EINVAL, "world > 1: run one independent replica per GPU (DESIGN.md §Multi-GPU)");
+  c->sharded = c->world > 1 || o.allreduce != nullptr || o.nccl_uid != nullptr;
+  c->m2_global = m2;
+  c->row0 = 0;
+  c->row1 = m2;
+  if (c->sharded) {
+    if (c->rank < 0 || c->rank >= c->world || m2 < c->world) {
+      *out = c.release();
+      return fail(*out, QP_EINVAL, "sharded setup needs 0 <= rank < world <= m2");
+    }
+    if (!o.allreduce && !o.nccl_uid) {
+      *out = c.release();
+      return fail(*out, QP_EINVAL, "world > 1 needs opts.nccl_uid (qp_nccl_unique_id) or opts.allreduce");
+    }
+    std::vector<int64_t> bounds(c->world + 1);
+    partition_rows(c->C.p.data(), m2, c->world, bounds.data());
+    c->row0 = bounds[c->rank];
+    c->row1 = bounds[c->rank + 1];
+    // keep only this rank's rows of C and d (global |d|max first: the stopping test is global)
+    c->dmax = 0;
+    for (double v : c->d) c->dmax = std::max(c->dmax, std::fabs(v));
+    HostCSR Cl;
+    Cl.nrows = c->row1 - c->row0;
+    Cl.ncols = n;
+    const int64_t q0 = c->C.p[c->row0], q1 = c->C.p[c->row1];
+    Cl.p.resize(Cl.nrows + 1);
+    for (int64_t i = 0; i <= Cl.nrows; ++i) Cl.p[i] = c->C.p[c->row0 + i] - q0;
+    Cl.i.assign(c->C.i.begin() + q0, c->C.i.begin() + q1);
+    Cl.v.assign(c->C.v.begin() + q0, c->C.v.begin() + q1);
+    c->C = std::move(Cl);
+    c->d = std::vector<double>(c->d.begin() + c->row0, c->d.begin() + c->row1);
+    c->m2 = c->row1 - c->row0;
   }
   if (o.x_perm) {
     c->xperm_user.assign(o.x_perm, o.x_perm + n);
@@ -1013,8 +1179,30 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
   for (double v : c->g) c->gmax = std::max(c->gmax, std::fabs(v));
   c->bmax = 0;
   for (double v : c->b) c->bmax = std::max(c->bmax, std::fabs(v));
-  c->dmax = 0;
-  for (double v : c->d) c->dmax = std::max(c->dmax, std::fabs(v));
+  if (!c->sharded) {
+    c->dmax = 0;
+    for (double v : c->d) c->dmax = std::max(c->dmax, std::fabs(v));
+  }
+  if (c->sharded) {
+    c->use_graphs = false;   // host-side collectives between the PCG kernels
+    if (!o.allreduce) {
+      NcclApi& api = nccl_api();
+      if (!api.ok) {
+        *out = c.release();
+        return fail(*out, QP_ENCCL, api.err);
+      }
+      ncclUniqueId uid;
+      std::memcpy(&uid, o.nccl_uid, sizeof(uid));
+      ncclResult_t r = api.comm_init_rank(&c->nccl, c->world, uid, c->rank);
+      if (r != ncclSuccess) {
+        *out = c.release();
+        return fail(*out, QP_ENCCL, std::string("ncclCommInitRank: ") + api.error_string(r));
+      }
+    } else {
+      c->ar_fn = o.allreduce;
+      c->ar_user = o.allreduce_user;
+    }
+  }
   int rc = cuda_check(c.get(), "qp_setup");
   c->setup_done = rc == QP_OK;
   *out = c.release();
@@ -1026,6 +1214,8 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
   if (rc) return rc;
   if (c->factored) return fail(c, QP_ESTATE, "ipm_factor_once already called (the factor of F is computed once)");
   if (p < QP_PREC_NONE || p > QP_PREC_HIGH) return fail(c, QP_EINVAL, "unknown preconditioner");
+  if (c->sharded && p == QP_PREC_HIGH)
+    return fail(c, QP_EINVAL, "P_H couples all inequality rows: not available with sharded rows (DESIGN.md §7)");
   c->precond = (int)p;
   cudaStream_t st = c->stream;
   const int64_t n = c->n, m1 = c->m1, m2 = c->m2, N = n + m1;
@@ -1081,6 +1271,11 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     c->partial = c->mem.zeros<double>(4 * (size_t)std::max(c->vgrid, 1), st);
     c->pst = c->mem.zeros<PcgState>(1, st);
     c->ist = c->mem.zeros<IpmState>(1, st);
+    c->ubuf = c->mem.zeros<double>(N, st);
+    PcgState ps{};
+    ps.defer = c->sharded ? 1 : 0;
+    cudaMemcpyAsync(c->pst, &ps, sizeof(PcgState), cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);   // ps is a stack object
   } catch (std::bad_alloc&) {
     return fail(c, QP_ENOMEM, "cudaMalloc failed (problem / vectors)");
   }
@@ -1276,6 +1471,8 @@ int qp_ipm_init(qp_ctx* c, const qp_ipm_opts* o) {
   IpmState is{};
   is.sigma = c->opts.sigma;
   is.tau = c->opts.tau;
+  is.defer = c->sharded ? 1 : 0;
+  is.m2_total = (double)c->m2_global;
   cudaMemcpyAsync(c->ist, &is, sizeof(IpmState), cudaMemcpyHostToDevice, st);
   c->ipm_k = 0;
   c->ipm_converged = false;
@@ -1296,11 +1493,7 @@ int qp_ipm_iterate(qp_ctx* c, int32_t nsteps, qp_ipm_result* r, int32_t* done) {
   }
   if (!c->ipm_converged && c->ipm_k >= c->opts.max_ipm) {
     // final residual evaluation at the last iterate
-    int h = c->begin(6);
-    ipm_mu(c->m2, c->s, c->nu, c->partial, c->ist, c->vgrid, c->stream);
-    ipm_residuals(c->Hf, c->Atf, c->Ctf, c->Af, c->Cf, c->gf, c->bv, c->dv, c->xl, c->xl + c->n, c->nu, c->s,
-                  c->rgre, c->rc, c->ra, c->Dk, c->partial, c->ist, c->vgrid, c->stream);
-    c->end(h);
+    if ((rc = ipm_eval_residuals(c))) return rc;
 
   }
   if (done) *done = c->ipm_converged ? 1 : 0;
@@ -1339,7 +1532,8 @@ int qp_kf_apply(qp_ctx* c, const double* D, const double* p, double* q) {
   const int64_t m2 = c->m2;
   const double* Dd = in_vec(c, D, c->vin, m2);
   const double* pd = in_vec(c, p, c->vin2, m2);
-  kf_apply_dev(c, Dd, pd, c->vout, false);
+  rc = kf_apply_dev(c, Dd, pd, c->vout, false);
+  if (rc) return rc;
   out_vec(c, q, c->vout, m2);
   rc = sync_check(c, "qp_kf_apply");
   c->harvest();
@@ -1485,6 +1679,30 @@ int64_t qp_debug_sweep_trace(qp_ctx* c, int32_t sweep, int64_t* out, int64_t cap
     cudaMemcpyAsync(out, F.tprof_buf + 70 + sweep * F.d.ttrace_cap * 4, n * 32, cudaMemcpyDeviceToHost, c->stream);
   int st = sync_check(c, "qp_debug_sweep_trace");
   return st != QP_OK ? st : n;
+}
+
+int qp_partition_rows(const int64_t* indptr, int64_t m2, int32_t world, int64_t* bounds) {
+  if (!indptr || !bounds || m2 < 0 || world < 1) return QP_EINVAL;
+  partition_rows(indptr, m2, world, bounds);
+  return QP_OK;
+}
+
+int qp_get_partition(qp_ctx* c, int64_t* row0, int64_t* row1, int64_t* m2_global) {
+  if (!c) return QP_EINVAL;
+  if (row0) *row0 = c->row0;
+  if (row1) *row1 = c->row1;
+  if (m2_global) *m2_global = c->m2_global;
+  return QP_OK;
+}
+
+int qp_nccl_unique_id(void* out) {
+  if (!out) return QP_EINVAL;
+  NcclApi& api = nccl_api();
+  if (!api.ok) return QP_ENCCL;
+  ncclUniqueId uid;
+  if (api.get_unique_id(&uid) != ncclSuccess) return QP_ENCCL;
+  std::memcpy(out, &uid, sizeof(uid));
+  return QP_OK;
 }
 
 const char* qp_last_error(const qp_ctx* c) { return c ? c->err.c_str() : "NULL context"; }

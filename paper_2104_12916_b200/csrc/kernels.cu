@@ -1284,6 +1284,90 @@ void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid
   k_trsv_bwd<<<grid, NT, trsv_smem_bytes(), s>>>(F, x, done_flag);
 }
 
+// ------------------------------------------------------------------------- reduction finalizers
+// Each takes the GLOBAL reduced values (local ones when not sharded) and updates the state.
+__device__ void fin_pcg_init(PcgState* st, double bb, double rz) {
+  st->bnorm2 = bb;
+  st->rr = bb;
+  st->rho = rz;
+  st->done = (bb == 0.0) ? 1 : 0;
+  if (st->maxit <= 0 && bb != 0.0) {
+    st->done = 1;
+    st->status = 1;
+  }
+}
+__device__ void fin_pcg_pq(PcgState* st, double pq) {
+  st->pq = pq;
+  if (!(pq > 0.0) || !isfinite(pq)) {
+    st->status = -3;
+    st->done = 1;
+  } else {
+    st->alpha = st->rho / pq;
+  }
+}
+__device__ void fin_pcg_upd1(PcgState* st, double rr, double rz, int prec) {
+  st->iter += 1;
+  st->rr = rr;
+  if (!isfinite(rr)) {
+    st->status = -3;
+    st->done = 1;
+  } else if (rr <= st->tol2 * st->bnorm2) {
+    st->done = 1;
+  } else if (st->iter >= st->maxit) {
+    st->done = 1;
+    st->status = 1;
+  } else if (prec != 2) {
+    st->beta = rz / st->rho;
+    st->rho = rz;
+    st->rz = rz;
+  }
+}
+__device__ void fin_pcg_rz_ph(PcgState* st, double rz) {
+  st->beta = rz / st->rho;
+  st->rho = rz;
+  st->rz = rz;
+}
+__device__ void fin_ipm_mu(IpmState* st, double smu) {
+  st->mu = smu / st->m2_total;   // μ = sᵀν / m2
+  st->sigma_mu = st->sigma * st->mu;
+}
+__device__ void fin_ipm_resid(IpmState* st, double a1, double a2, double a3) {
+  st->rg_inf = a1;
+  st->re_inf = a2;
+  st->ri_inf = a3;
+}
+__device__ void fin_ipm_alpha(IpmState* st, double a) {
+  st->alpha_max = a;
+  st->alpha = fmin(1.0, st->tau * a);
+}
+
+__global__ void k_finalize(int kind, PcgState* ps, IpmState* is, int prec) {
+  if (threadIdx.x != 0) return;
+  if (kind <= FIN_PCG_RZ_PH && *((volatile int*)&ps->done) && kind != FIN_PCG_INIT) return;
+  switch (kind) {
+    case FIN_PCG_INIT: fin_pcg_init(ps, ps->red[0], ps->red[1]); break;
+    case FIN_PCG_PQ: fin_pcg_pq(ps, ps->red[0]); break;
+    case FIN_PCG_UPD1: fin_pcg_upd1(ps, ps->red[0], ps->red[1], prec); break;
+    case FIN_PCG_INIT_PH: ps->rho = ps->red[0]; break;
+    case FIN_PCG_RZ_PH: fin_pcg_rz_ph(ps, ps->red[0]); break;
+    case FIN_IPM_MU: fin_ipm_mu(is, is->red[0]); break;
+    case FIN_IPM_RESID: fin_ipm_resid(is, is->red[0], is->red[1], is->red[2]); break;
+    case FIN_IPM_ALPHA: fin_ipm_alpha(is, is->red[0]); break;
+  }
+}
+void finalize(int kind, PcgState* ps, IpmState* is, int prec, cudaStream_t s) {
+  k_finalize<<<1, 32, 0, s>>>(kind, ps, is, prec);
+}
+
+__global__ void k_spmv(DevCSR M, const double* x, double* y, const int* done) {
+  if (done != nullptr && *((volatile const int*)done)) return;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < M.nrows; i += (int64_t)gridDim.x * NT)
+    y[i] = csr_dot(M, i, x);
+}
+void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid, cudaStream_t s) {
+  k_spmv<<<grid, NT, 0, s>>>(M, x, y, done);
+}
+
 // ------------------------------------------------------------------------- K_F product and PCG
 // q = D∘p − C_f·z (a5) with the pᵀq reduction; last block: α = ρ / pᵀq.
 __global__ void __launch_bounds__(NT) k_kf_q(DevCSR Cf, const double* D, const double* p, const double* z,
@@ -1303,13 +1387,8 @@ __global__ void __launch_bounds__(NT) k_kf_q(DevCSR Cf, const double* D, const d
   if (is_last_block(&st->arrive)) {
     double pq = reduce_partials<0>(partial, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->pq = pq;
-      if (!(pq > 0.0) || !isfinite(pq)) {
-        st->status = -3;
-        st->done = 1;
-      } else {
-        st->alpha = st->rho / pq;
-      }
+      if (st->defer) st->red[0] = pq;
+      else fin_pcg_pq(st, pq);
       st->arrive = 0;
     }
   }
@@ -1343,15 +1422,17 @@ __global__ void __launch_bounds__(NT) k_pcg_init(int prec, int64_t m2, const dou
     double s1 = reduce_partials<0>(partial, gridDim.x, sh);
     double s2 = reduce_partials<0>(partial + gridDim.x, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->bnorm2 = s1;
-      st->rr = s1;
-      st->rho = s2;
       st->tol2 = tol * tol;
       st->iter = 0;
       st->maxit = maxit;
       st->status = 0;
-      st->done = (s1 == 0.0) ? 1 : 0;
-      if (maxit <= 0 && s1 != 0.0) { st->done = 1; st->status = 1; }
+      if (st->defer) {
+        st->red[0] = s1;
+        st->red[1] = s2;
+        st->done = 0;
+      } else {
+        fin_pcg_init(st, s1, s2);
+      }
       st->arrive = 0;
     }
   }
@@ -1372,7 +1453,8 @@ __global__ void __launch_bounds__(NT) k_pcg_init_ph(int64_t m2, const double* r,
   if (is_last_block(&st->arrive)) {
     double s = reduce_partials<0>(partial, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->rho = s;
+      if (st->defer) st->red[0] = s;
+      else st->rho = s;
       st->arrive = 0;
     }
   }
@@ -1407,20 +1489,11 @@ __global__ void __launch_bounds__(NT) k_pcg_update1(int prec, int64_t m2, const 
     double s1 = reduce_partials<0>(partial, gridDim.x, sh);
     double s2 = reduce_partials<0>(partial + gridDim.x, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->iter += 1;
-      st->rr = s1;
-      if (!isfinite(s1)) {
-        st->status = -3;
-        st->done = 1;
-      } else if (s1 <= st->tol2 * st->bnorm2) {
-        st->done = 1;
-      } else if (st->iter >= st->maxit) {
-        st->done = 1;
-        st->status = 1;
-      } else if (prec != 2) {
-        st->beta = s2 / st->rho;
-        st->rho = s2;
-        st->rz = s2;
+      if (st->defer) {
+        st->red[0] = s1;
+        st->red[1] = s2;
+      } else {
+        fin_pcg_upd1(st, s1, s2, prec);
       }
       st->arrive = 0;
     }
@@ -1440,9 +1513,8 @@ __global__ void __launch_bounds__(NT) k_pcg_rz_ph(int64_t m2, const double* r, c
   if (is_last_block(&st->arrive)) {
     double s = reduce_partials<0>(partial, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->beta = s / st->rho;
-      st->rho = s;
-      st->rz = s;
+      if (st->defer) st->red[0] = s;
+      else fin_pcg_rz_ph(st, s);
       st->arrive = 0;
     }
   }
@@ -1510,8 +1582,8 @@ __global__ void __launch_bounds__(NT) k_ipm_mu(int64_t m2, const double* s_, con
   if (is_last_block(&st->arrive)) {
     double s = reduce_partials<0>(partial, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->mu = s / (double)m2;                 // μ = sᵀν / m2
-      st->sigma_mu = st->sigma * st->mu;
+      if (st->defer) st->red[0] = s;
+      else fin_ipm_mu(st, s);
       st->arrive = 0;
     }
   }
@@ -1524,14 +1596,15 @@ __global__ void __launch_bounds__(NT) k_ipm_resid(DevCSR Hf, DevCSR Atf, DevCSR 
                                                   const double* gf, const double* b, const double* d,
                                                   const double* x, const double* lam, const double* nu,
                                                   const double* s_, double* rhs_f, double* rc, double* ra,
-                                                  double* D, double* partial, IpmState* st) {
+                                                  double* D, double* partial, IpmState* st, const double* ctnu) {
   __shared__ double sh[32];
   const int64_t n = Hf.nrows, m1 = Af.nrows, m2 = Cf.nrows;
   const double smu = st->sigma_mu;
   double mg = 0.0, me = 0.0, mi = 0.0;
   for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < n + m1 + m2; t += (int64_t)gridDim.x * NT) {
     if (t < n) {
-      const double grad = csr_dot(Hf, t, x) + gf[t] - csr_dot(Atf, t, lam) - csr_dot(Ctf, t, nu);
+      const double grad = csr_dot(Hf, t, x) + gf[t] - csr_dot(Atf, t, lam) -
+                          (ctnu != nullptr ? ctnu[t] : csr_dot(Ctf, t, nu));
       rhs_f[t] = -grad;
       mg = fmax(mg, fabs(grad));
     } else if (t < n + m1) {
@@ -1563,9 +1636,13 @@ __global__ void __launch_bounds__(NT) k_ipm_resid(DevCSR Hf, DevCSR Atf, DevCSR 
     double a2 = reduce_partials<1>(partial + gridDim.x, gridDim.x, sh);
     double a3 = reduce_partials<1>(partial + 2 * gridDim.x, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->rg_inf = a1;
-      st->re_inf = a2;
-      st->ri_inf = a3;
+      if (st->defer) {
+        st->red[0] = a1;
+        st->red[1] = a2;
+        st->red[2] = a3;
+      } else {
+        fin_ipm_resid(st, a1, a2, a3);
+      }
       st->arrive = 0;
     }
   }
@@ -1579,9 +1656,9 @@ __global__ void k_ipm_rnu(DevCSR Cf, const double* ra, const double* y, double* 
 
 // rhs of F(Δx;Δλ) = −(r_g + CᵀΔν; r_e); rg_re holds (r_g; r_e) in factor order.
 __global__ void k_ipm_recrhs(DevCSR Ctf, int64_t n, int64_t m1, const double* rg_re, const double* dnu,
-                             double* rhs_f) {
+                             double* rhs_f, const double* ctdnu) {
   for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < n + m1; t += (int64_t)gridDim.x * NT)
-    rhs_f[t] = t < n ? -(rg_re[t] + csr_dot(Ctf, t, dnu)) : -rg_re[t];
+    rhs_f[t] = t < n ? -(rg_re[t] + (ctdnu != nullptr ? ctdnu[t] : csr_dot(Ctf, t, dnu))) : -rg_re[t];
 }
 
 // Δs = −V⁻¹r_c − DΔν; α_max over s, ν; α = min(1, τ α_max) (reading R3).
@@ -1602,8 +1679,8 @@ __global__ void __launch_bounds__(NT) k_ipm_ds_alpha(int64_t m2, const double* r
   if (is_last_block(&st->arrive)) {
     double a = reduce_partials<2>(partial, gridDim.x, sh);
     if (threadIdx.x == 0) {
-      st->alpha_max = a;
-      st->alpha = fmin(1.0, st->tau * a);
+      if (st->defer) st->red[0] = a;
+      else fin_ipm_alpha(st, a);
       st->arrive = 0;
     }
   }
@@ -1647,15 +1724,16 @@ void ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial, Ipm
 void ipm_residuals(const DevCSR& Hf, const DevCSR& Atf, const DevCSR& Ctf, const DevCSR& Af, const DevCSR& Cf,
                    const double* gf, const double* b, const double* d, const double* x, const double* lam,
                    const double* nu, const double* s_, double* rhs_f, double* rc, double* ra, double* D,
-                   double* partial, IpmState* st, int grid, cudaStream_t s) {
-  k_ipm_resid<<<grid, NT, 0, s>>>(Hf, Atf, Ctf, Af, Cf, gf, b, d, x, lam, nu, s_, rhs_f, rc, ra, D, partial, st);
+                   double* partial, IpmState* st, int grid, cudaStream_t s, const double* ctnu) {
+  k_ipm_resid<<<grid, NT, 0, s>>>(Hf, Atf, Ctf, Af, Cf, gf, b, d, x, lam, nu, s_, rhs_f, rc, ra, D, partial, st,
+                                  ctnu);
 }
 void ipm_rnu(const DevCSR& Cf, const double* ra, const double* y, double* rnu, int grid, cudaStream_t s) {
   k_ipm_rnu<<<grid, NT, 0, s>>>(Cf, ra, y, rnu);
 }
 void ipm_recovery_rhs(const DevCSR& Ctf, int64_t n, int64_t m1, const double* rg_re, const double* dnu,
-                      double* rhs_f, int grid, cudaStream_t s) {
-  k_ipm_recrhs<<<grid, NT, 0, s>>>(Ctf, n, m1, rg_re, dnu, rhs_f);
+                      double* rhs_f, int grid, cudaStream_t s, const double* ctdnu) {
+  k_ipm_recrhs<<<grid, NT, 0, s>>>(Ctf, n, m1, rg_re, dnu, rhs_f, ctdnu);
 }
 void ipm_ds_alpha(int64_t m2, const double* rc, const double* nu, const double* D, const double* dnu,
                   const double* s_, double* ds, double* partial, IpmState* st, int grid, cudaStream_t s) {

@@ -106,11 +106,14 @@ struct DevCSR {
 };
 
 // PCG scalar state (device), written by last-block reductions.
+// With `defer` set (ν rows sharded over ranks), the last block stores its LOCAL reductions in
+// red[] instead; the host all-reduces red[] across ranks and k_finalize applies the same update.
 struct PcgState {
   double rho, pq, rr, rz, bnorm2, tol2, alpha, beta;
   int iter, maxit, done, status;
   unsigned int arrive;
-  int pad;
+  int defer;
+  double red[4];
 };
 
 // IPM scalar state (device).
@@ -120,8 +123,17 @@ struct IpmState {
   double alpha, alpha_max;
   double objective;
   unsigned int arrive;
-  int pad;
+  int defer;          // see PcgState
+  double m2_total;    // global number of inequality rows (μ = sᵀν / m2_total)
+  double red[4];
 };
+
+// Finalization of a deferred reduction after the cross-rank all-reduce of red[] (one thread).
+enum FinKind { FIN_PCG_INIT = 0, FIN_PCG_PQ, FIN_PCG_UPD1, FIN_PCG_INIT_PH, FIN_PCG_RZ_PH, FIN_IPM_MU,
+               FIN_IPM_RESID, FIN_IPM_ALPHA };
+void finalize(int kind, PcgState* ps, IpmState* is, int prec, cudaStream_t s);
+// u[t] = Σ_k M(t,k)·x[k] for the rows of M (plain CSR SpMV; sharded Cᵀp / Cᵀν partial products)
+void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid, cudaStream_t s);
 
 // ---- multifrontal factorization
 // zero the fronts of one level, then scatter its original entries (+ D on the diagonal for P_H)
@@ -183,13 +195,15 @@ void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const
 // ---- IPM kernels (a9–a11)
 void ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial, IpmState* st, int grid,
             cudaStream_t s);
+// ctnu: optional precomputed Cᵀν (factor order, all ranks' rows summed); NULL = from Ctf
 void ipm_residuals(const DevCSR& Hf, const DevCSR& Atf, const DevCSR& Ctf, const DevCSR& Af, const DevCSR& Cf,
                    const double* gf, const double* b, const double* d, const double* x, const double* lam,
                    const double* nu, const double* s_, double* rhs_f, double* rc, double* ra, double* D,
-                   double* partial, IpmState* st, int grid, cudaStream_t s);
+                   double* partial, IpmState* st, int grid, cudaStream_t s, const double* ctnu = nullptr);
 void ipm_rnu(const DevCSR& Cf, const double* ra, const double* y, double* rnu, int grid, cudaStream_t s);
+// ctdnu: optional precomputed CᵀΔν (summed over ranks); NULL = from Ctf
 void ipm_recovery_rhs(const DevCSR& Ctf, int64_t n, int64_t m1, const double* rg_re, const double* dnu,
-                      double* rhs_f, int grid, cudaStream_t s);
+                      double* rhs_f, int grid, cudaStream_t s, const double* ctdnu = nullptr);
 void ipm_ds_alpha(int64_t m2, const double* rc, const double* nu, const double* D, const double* dnu,
                   const double* s_, double* ds, double* partial, IpmState* st, int grid, cudaStream_t s);
 void ipm_update(int64_t N, int64_t m2, const double* dxl, const double* dnu, const double* ds, double* xl,

@@ -1,0 +1,175 @@
+"""Sharded ν-row mode on one GPU (qp_b200.h "Sharded mode").
+
+The round's GPU budget is one device, so two ranks run as two threads of this process, each
+with its own qp_ctx (own stream, own replicated F factor) on cuda:0, and the collective is the
+C ABI's qp_allreduce_fn implemented here on the host: every call synchronises the rank's
+stream, copies the buffer out, sums in rank order (bit-identical on both ranks) and copies it
+back.  No kernel of one rank ever waits on the other's.  The NCCL path itself is exercised
+with world = 1 (a one-rank communicator: all-reduce is the identity, but every collective of
+the sharded code path is issued through NCCL).
+
+Checks: the concatenated sharded PCG solution equals the oracle's (1e-8 relative, reading
+R16 at fixed iterations) and the unsharded library's; the sharded IPM reaches the oracle's
+objective (1e-8 relative) with replicated x identical on both ranks and the KKT conditions.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import qpgen
+from oracle.fsolve import make_fsolver
+from oracle.kkt import KF_apply
+from oracle.pcg import pcg
+
+pytestmark = pytest.mark.gpu
+
+
+class ThreadComm:
+    """qp_allreduce_fn for `world` ranks living in threads of one process."""
+
+    def __init__(self, world):
+        self.world = world
+        self.slots = [None] * world
+        self.bar = threading.Barrier(world)
+
+    def fn(self, rank):
+        from cuda.bindings import runtime as rt
+
+        def allreduce(buf, count, op, stream):
+            (err,) = rt.cudaStreamSynchronize(stream)
+            assert int(err) == 0, err
+            host = np.empty(count)
+            (err,) = rt.cudaMemcpy(host.ctypes.data, buf, count * 8, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+            assert int(err) == 0, err
+            self.slots[rank] = host
+            self.bar.wait()
+            res = self.slots[0].copy()
+            for r in range(1, self.world):
+                res = res + self.slots[r] if op == 0 else (np.maximum(res, self.slots[r]) if op == 1
+                                                           else np.minimum(res, self.slots[r]))
+            self.bar.wait()
+            (err,) = rt.cudaMemcpy(buf, res.ctypes.data, count * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+            return int(err)
+        return allreduce
+
+
+def run_ranks(world, body):
+    """body(rank, comm) in `world` threads; returns the per-rank results (re-raises errors)."""
+    comm = ThreadComm(world)
+    out, errs = [None] * world, []
+
+    def run(r):
+        try:
+            out[r] = body(r, comm)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            comm.bar.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+def _solver(qp, rank, world, comm):
+    from paper_2104_12916_b200.binding import from_qp
+    s = from_qp(qp, rank=rank, world=world, allreduce=comm.fn(rank))
+    s.ipm_factor_once("low")
+    return s
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pcg_matches_oracle(world):
+    qp = qpgen.make("c0")
+    rng = np.random.default_rng(11)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    fs = make_fsolver(qp.H, qp.A)
+    for tol, maxit in ((0.0, 12), (1e-12, 300)):
+        def body(rank, comm):
+            s = _solver(qp, rank, world, comm)
+            sl = slice(s.row0, s.row0 + s.m2)
+            x, it, rr, rc = s.pcg_solve(D[sl], b[sl], tol=tol, maxit=maxit)
+            s.close()
+            return s.row0, x, it, rr
+        res = run_ranks(world, body)
+        assert [r[0] for r in res] == sorted(r[0] for r in res) and res[0][0] == 0
+        xs = np.concatenate([r[1] for r in res])
+        its = {r[2] for r in res}
+        assert len(its) == 1                                   # every rank took the same decisions
+        xo, ito, _, _, _ = pcg(lambda p: KF_apply(qp, fs, D, p), b, lambda r: r / D, tol, maxit)
+        if tol == 0.0:
+            assert its == {maxit} and ito == maxit
+        else:
+            assert abs(its.pop() - ito) <= 2
+        assert np.linalg.norm(xs - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_sharded_ipm_matches_oracle():
+    from oracle.ipm import ipm_solve as oracle_ipm
+    qp = qpgen.make("c0")
+    ref = oracle_ipm(qp, precond="low", ipm_tol=1e-10)
+
+    def body(rank, comm):
+        s = _solver(qp, rank, 2, comm)
+        r = s.ipm_solve(ipm_tol=1e-10, max_ipm=100)
+        r["row0"] = s.row0
+        s.close()
+        return r
+
+    res = run_ranks(2, body)
+    for r in res:
+        assert r["converged"]
+        assert abs(r["objective"] - ref.objective) <= 1e-8 * max(1.0, abs(ref.objective))
+    assert res[0]["n_ipm"] == res[1]["n_ipm"] and res[0]["pcg_iters"] == res[1]["pcg_iters"]
+    assert np.abs(res[0]["x"] - res[1]["x"]).max() <= 1e-12 * (1 + np.abs(res[0]["x"]).max())
+    x, lam = res[0]["x"], res[0]["lam"]
+    nu = np.concatenate([r["nu"] for r in res])
+    s_ = np.concatenate([r["s"] for r in res])
+    assert s_.min() > 0 and nu.min() > 0
+    tol = 1e-8
+    assert np.abs(qp.H @ x + qp.g - qp.A.T @ lam - qp.C.T @ nu).max() <= tol * (1 + np.abs(qp.g).max())
+    assert np.abs(qp.A @ x - qp.b).max() <= tol * (1 + np.abs(qp.b).max())
+    assert np.abs(qp.C @ x - s_ - qp.d).max() <= tol * (1 + np.abs(qp.d).max())
+
+
+def test_sharded_rejects_ph_and_bad_rank():
+    from paper_2104_12916_b200.binding import QPError, from_qp
+    qp = qpgen.make("c0")
+    with pytest.raises(QPError):
+        from_qp(qp, rank=2, world=2, allreduce=lambda *a: 0)
+
+    def body(rank, comm):
+        s = from_qp(qp, rank=rank, world=2, allreduce=comm.fn(rank))
+        with pytest.raises(QPError):
+            s.ipm_factor_once("high")
+        s.close()
+        return True
+
+    assert all(run_ranks(2, body))
+
+
+def test_nccl_world1_matches_unsharded():
+    """world = 1 through a real one-rank NCCL communicator: identical to the unsharded path up
+    to reduction order."""
+    from paper_2104_12916_b200.binding import from_qp, nccl_unique_id
+    qp = qpgen.make("c0")
+    rng = np.random.default_rng(5)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    s1 = from_qp(qp)
+    s1.ipm_factor_once("low")
+    s2 = from_qp(qp, rank=0, world=1, nccl_uid=nccl_unique_id())
+    s2.ipm_factor_once("low")
+    x1, it1, _, _ = s1.pcg_solve(D, b, tol=1e-12, maxit=300)
+    x2, it2, _, _ = s2.pcg_solve(D, b, tol=1e-12, maxit=300)
+    assert abs(it1 - it2) <= 1 and np.linalg.norm(x1 - x2) <= 1e-10 * np.linalg.norm(x1)
+    r1 = s1.ipm_solve(ipm_tol=1e-10)
+    r2 = s2.ipm_solve(ipm_tol=1e-10)
+    assert r1["converged"] and r2["converged"]
+    assert abs(r1["objective"] - r2["objective"]) <= 1e-10 * max(1.0, abs(r1["objective"]))

@@ -41,3 +41,61 @@ def test_replica_aggregation_two_ranks():
         value, tot, mx = out[r]
         assert tot == 2200 and mx == 800.0
         assert abs(value - 2200 / 0.8) < 1e-9      # Σ iterations / max-over-ranks seconds
+
+
+# ---------------------------------------------------------------- sharded ν rows
+def _sharded_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import qpgen
+    from oracle.fsolve import make_fsolver
+    from oracle.sharded import partition_rows, sharded_pcg
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def allreduce(a):
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    qp = qpgen.make("c0")
+    fs = make_fsolver(qp.H, qp.A)
+    C = qp.C.tocsr()
+    bounds = partition_rows(C.indptr, qp.m2, world)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    rng = np.random.default_rng(7)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    x_g, it, rr, conv = sharded_pcg(C[r0:r1], fs, D[r0:r1], b[r0:r1], lambda r: r / D[r0:r1], 1e-10, 500,
+                                    allreduce)
+    out[rank] = (r0, r1, x_g, it, rr, conv)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_sharded_pcg_two_ranks_matches_unsharded():
+    """Two gloo ranks, each owning a contiguous slice of the c0 inequality rows, run the sharded
+    PCG (Cᵀp all-reduced before the replicated F-solve, inner products all-reduced): the
+    concatenated solution and the iteration count equal the single-process PCG's."""
+    import numpy as np
+    import qpgen
+    from oracle.fsolve import make_fsolver
+    from oracle.kkt import KF_apply
+    from oracle.pcg import pcg
+    world = 2
+    port = 30500 + (os.getpid() % 1000)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sharded_worker, args=(world, port, out), nprocs=world, join=True)
+    qp = qpgen.make("c0")
+    fs = make_fsolver(qp.H, qp.A)
+    rng = np.random.default_rng(7)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    x, it, rr, conv, _ = pcg(lambda p: KF_apply(qp, fs, D, p), b, lambda r: r / D, 1e-10, 500)
+    assert out[0][1] == out[1][0] and out[0][0] == 0 and out[1][1] == qp.m2
+    xs = np.concatenate([out[0][2], out[1][2]])
+    assert out[0][3] == out[1][3] and abs(out[0][3] - it) <= 1
+    assert np.linalg.norm(xs - x) <= 1e-9 * np.linalg.norm(x)
