@@ -23,9 +23,12 @@ one-time F factorization (a12) is setup, timed and reported separately.
   cpu_baseline  the CPU oracle (oracle/, NumPy/SciPy fp64) on the box's host
              cores: PCG iterations of IPM step 0 on the same c1 problem.
 
-Multi-GPU (torchrun, N > 1): one independent replica per GPU (DESIGN.md
-§Multi-GPU: the F-solve, ≥ 95 % of the bytes, is replicated, so the path is
-run as weak-scaling replicas), value = Σ PCG iterations / max-over-ranks time.
+Multi-GPU (torchrun, N > 1), --mode replicas (default): one independent replica
+per GPU (the F-solve, ≥ 95 % of the bytes, is replicated, so the
+path scales as weak-scaling replicas), value = Σ PCG iterations / max-over-ranks
+time.  --mode sharded: ONE IPM with the inequality rows split over the ranks
+(NCCL all-reduce of Cᵀp and the PCG reductions, replicated F-solve; strong
+scaling), value = PCG iterations / max-over-ranks time.
 
 ``--impl reference`` times the CPU oracle as the reference arm (rank 0 only).
 """
@@ -57,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=6, help="oracle PCG iterations per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="N > 1: independent replicas (weak) or one IPM with sharded rows (strong)")
     ap.add_argument("--profile-traffic", default=os.path.join(ROOT, "profiles", "traffic.json"))
     return ap.parse_args()
 
@@ -97,12 +102,13 @@ def allreduce(vals, op, use_dist):
     return t.cpu().tolist()
 
 
-def aggregate(pcg_iters, ms, use_dist):
-    """Whole-job throughput: Σ PCG iterations over ranks ÷ the slowest rank's time (max over ranks)."""
+def aggregate(pcg_iters, ms, use_dist, shared=False):
+    """Whole-job throughput: Σ PCG iterations over ranks ÷ the slowest rank's time (max over ranks).
+    shared=True (sharded mode): the ranks run the SAME iterations, so they are counted once."""
     tot, mx = float(pcg_iters), float(ms)
     if use_dist:
         import torch.distributed as dist
-        tot = allreduce([tot], dist.ReduceOp.SUM, True)[0]
+        tot = allreduce([tot], dist.ReduceOp.MAX if shared else dist.ReduceOp.SUM, True)[0]
         mx = allreduce([mx], dist.ReduceOp.MAX, True)[0]
     return (tot / (mx / 1e3) if mx > 0 else 0.0), tot, mx
 
@@ -229,7 +235,16 @@ def run_ours(args, rank, world, local, use_dist):
     dev = torch.device("cuda", local)
     qp = qpgen.make(args.config)
     stream = torch.cuda.Stream(device=dev)
-    s = from_qp(qp, device=local, stream=stream.cuda_stream)
+    sharded = args.mode == "sharded"
+    if sharded:
+        from paper_2104_12916_b200.binding import nccl_unique_id
+        uid = [nccl_unique_id() if rank == 0 else None]
+        if use_dist:
+            import torch.distributed as dist
+            dist.broadcast_object_list(uid, src=0)
+        s = from_qp(qp, device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_uid=uid[0])
+    else:
+        s = from_qp(qp, device=local, stream=stream.cuda_stream)
     t0 = time.perf_counter()
     s.ipm_factor_once(args.precond)
     t_setup = time.perf_counter() - t0
@@ -290,7 +305,7 @@ def run_ours(args, rank, world, local, use_dist):
                 Dp = torch.from_numpy(D).pin_memory()
                 rp = torch.from_numpy(rnu).pin_memory()
                 systems.append((Dp, rp, eps))
-        outp = torch.empty(qp.m2, dtype=torch.float64).pin_memory()
+        outp = torch.empty(s.m2, dtype=torch.float64).pin_memory()
         for (Dp, rp, eps) in systems[:1]:   # warm the host path
             s.pcg_solve(Dp.numpy(), rp.numpy(), tol=eps, maxit=2000)
         barrier(use_dist)
@@ -306,13 +321,13 @@ def run_ours(args, rank, world, local, use_dist):
         torch.cuda.synchronize(dev)
         barrier(use_dist)
         ms_e2e = f0.elapsed_time(f1)
-        e2e_value, _, _ = aggregate(its, ms_e2e, use_dist)
+        e2e_value, _, _ = aggregate(its, ms_e2e, use_dist, sharded)
         e2e = {"value": e2e_value, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * 8 * qp.m2, "d2h_bytes_per_step": 8 * qp.m2 + 16,
+               "h2d_bytes_per_step": 2 * 8 * s.m2, "d2h_bytes_per_step": 8 * s.m2 + 16,
                "steps": len(systems), "pcg_iters": its}
 
     # ---------------------------------------------------------------- aggregate over ranks
-    value, tot_pcg, ms_max = aggregate(pcg_timed, ms, use_dist)
+    value, tot_pcg, ms_max = aggregate(pcg_timed, ms, use_dist, sharded)
 
     # ---------------------------------------------------------------- roofline of the L_F sweeps
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -337,7 +352,7 @@ def run_ours(args, rank, world, local, use_dist):
             traffic = json.load(open(args.profile_traffic)).get(args.config, {}).get("dram_bytes_per_fsolve")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "F-solve = k_trsv_fwd + k_trsv_bwd", "achieved": achieved,
+    roofline = {"bound": "hbm", "kernel": "F-solve = k_trsv_fwd + k_symroot_gemv + k_trsv_bwd", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_fsolve": fsolve_bytes,
@@ -360,7 +375,8 @@ def run_ours(args, rank, world, local, use_dist):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max / max(1, steps_done), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_max / max(1, steps_done), "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} PL-KF: one IPM iteration per step (residuals, r_nu F-solve, "
                                f"PCG to eps_k, recovery, step)" if args.precond == "low" else
@@ -368,7 +384,8 @@ def run_ours(args, rank, world, local, use_dist):
                    "n": qp.n, "m1": qp.m1, "m2": qp.m2, "nnz_LF": st["nnz_LF"], "precond": args.precond,
                    "ipm_steps_timed": steps_done, "pcg_iters_timed": pcg_timed,
                    "l2": "no flush: the factor read every sweep (%.2f GB) exceeds L2" % (st["factor_bytes"] / 1e9),
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"sharded inequality rows x{world} (NCCL all-reduce, replicated F-solve)"
+                                   if sharded else (f"replicas x{world}" if world > 1 else "single GPU"))},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         "setup_s": {"symbolic": st["t_symbolic_s"], "factor": st["t_factor_s"], "factor_once_total": t_setup},
     }

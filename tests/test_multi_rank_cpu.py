@@ -26,7 +26,8 @@ def _worker(rank, world, port, out):
     iters = [1000, 1200][rank]
     ms = [500.0, 800.0][rank]
     value, tot, mx = bench.aggregate(iters, ms, use)
-    out[rank] = (value, tot, mx)
+    shared = bench.aggregate(1000, ms, use, True)   # sharded mode: same iterations on every rank
+    out[rank] = (value, tot, mx, shared)
     dist.destroy_process_group()
 
 
@@ -38,9 +39,10 @@ def test_replica_aggregation_two_ranks():
     out = mgr.dict()
     mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
     for r in range(world):
-        value, tot, mx = out[r]
+        value, tot, mx, shared = out[r]
         assert tot == 2200 and mx == 800.0
         assert abs(value - 2200 / 0.8) < 1e-9      # Σ iterations / max-over-ranks seconds
+        assert shared[1] == 1000 and abs(shared[0] - 1000 / 0.8) < 1e-9   # counted once
 
 
 # ---------------------------------------------------------------- sharded ν rows
