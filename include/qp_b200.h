@@ -229,8 +229,9 @@ int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
 
 /* Debug: per-task trace of the sweeps profiled by the last enable/disable pair of
  * qp_debug_sweep_profile.  sweep 0 = forward, 1 = backward.  Writes min(cap, #tasks)
- * records of 4 int64 to out (host, caller-owned), indexed by dispatch ticket:
- * [task word | SM id << 32, start ns, dependency-met ns, end ns] (globaltimer).
+ * records of 6 int64 to out (host, caller-owned), indexed by dispatch ticket:
+ * [task word | SM id << 32, start, dependency met, marker a, marker b, end] in
+ * globaltimer ns; markers are task-type specific (0 = unused).
  * Returns the number of records, or a negative qp_status. */
 int64_t qp_debug_sweep_trace(qp_ctx* ctx, int32_t sweep, int64_t* out, int64_t cap);
 

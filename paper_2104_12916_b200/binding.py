@@ -326,7 +326,7 @@ class QPSolver:
         return out.reshape(2, 7, 5)
 
     def debug_sweep_trace(self, sweep, cap=1 << 20):
-        out = np.zeros((cap, 4), dtype=np.int64)
+        out = np.zeros((cap, 6), dtype=np.int64)
         n = int(self.lib.qp_debug_sweep_trace(self.ctx, int(sweep), out.ctypes.data, cap))
         if n < 0:
             self._check(n)

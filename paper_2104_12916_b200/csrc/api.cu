@@ -528,7 +528,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     F.n_fwd_x = (int64_t)S.fwd_tasks_x.size();
     F.n_bwd_x = (int64_t)S.bwd_tasks_x.size();
     d.ttrace_cap = std::max<int64_t>(std::max(F.n_fwd_sym, F.n_bwd_sym), std::max(F.n_fwd_x, F.n_bwd_x));
-    F.tprof_buf = m.alloc<unsigned long long>(70 + 8 * d.ttrace_cap);
+    F.tprof_buf = m.alloc<unsigned long long>(70 + 12 * d.ttrace_cap);
     F.fs_bytes = S.fs_size * 8;
     F.ws_bytes = S.ws_size * 8;
   } catch (std::bad_alloc&) {
@@ -1657,7 +1657,7 @@ int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
   if (!c || !c->factored) return QP_ESTATE;
   Factor& F = c->FF;
   if (enable) {
-    std::vector<unsigned long long> init(70 + 8 * F.d.ttrace_cap, 0);
+    std::vector<unsigned long long> init(70 + 12 * F.d.ttrace_cap, 0);
     for (int i = 0; i < 14; ++i) init[i * 5 + 3] = ~0ull;
     cudaMemcpyAsync(F.tprof_buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c->stream);
     F.d.tprof = F.tprof_buf;
@@ -1669,14 +1669,14 @@ int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
 }
 
 // Debug: per-task trace of the last profiled sweeps (after qp_debug_sweep_profile(…, 0)).
-// out[cap][4] = [task | smid << 32, start ns, dependency met ns, end ns] by ticket; returns the
+// out[cap][6] = [task | smid << 32, start, dependency met, marker a, marker b, end] (ns) by ticket; the
 // number of records written (the sweep's task count) or a negative status.
 int64_t qp_debug_sweep_trace(qp_ctx* c, int32_t sweep, int64_t* out, int64_t cap) {
   if (!c || !c->factored || sweep < 0 || sweep > 1) return QP_ESTATE;
   Factor& F = c->FF;
   const int64_t n = std::min<int64_t>(cap, sweep == 0 ? F.d.n_fwd_tasks : F.d.n_bwd_tasks);
   if (n > 0 && out)
-    cudaMemcpyAsync(out, F.tprof_buf + 70 + sweep * F.d.ttrace_cap * 4, n * 32, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(out, F.tprof_buf + 70 + sweep * F.d.ttrace_cap * 6, n * 48, cudaMemcpyDeviceToHost, c->stream);
   int st = sync_check(c, "qp_debug_sweep_trace");
   return st != QP_OK ? st : n;
 }

@@ -394,14 +394,17 @@ __device__ __forceinline__ unsigned smid() {
 }
 __device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int type, unsigned long long t0,
                                           unsigned long long t1, unsigned long long t2, int task = 0,
-                                          unsigned ticket = 0, int64_t cap = 0) {
+                                          unsigned ticket = 0, int64_t cap = 0, unsigned long long ta = 0,
+                                          unsigned long long tb = 0) {
   if (tp == nullptr || threadIdx.x != 0) return;
-  if ((int64_t)ticket < cap) {  // per-task trace: [task | smid<<32, t0, t1, t2]
-    unsigned long long* r = tp + 70 + ((int64_t)sweep * cap + ticket) * 4;
+  if ((int64_t)ticket < cap) {  // per-task trace: [task | smid<<32, t0, t1, ta, tb, t2]
+    unsigned long long* r = tp + 70 + ((int64_t)sweep * cap + ticket) * 6;
     r[0] = (unsigned long long)(unsigned)task | ((unsigned long long)smid() << 32);
     r[1] = t0;
     r[2] = t1;
-    r[3] = t2;
+    r[3] = ta;
+    r[4] = tb;
+    r[5] = t2;
   }
   unsigned long long* q = tp + (sweep * 7 + type) * 5;
   atomicAdd(q + 0, 1ull);
@@ -615,7 +618,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
     if (task < 0) break;
     const int type = task >> 28, idx = task & ((1 << 28) - 1);
     const unsigned long long t0 = F.tprof ? gtime() : 0ull;
-    unsigned long long t1 = t0;
+    unsigned long long t1 = t0, ta = 0, tb = 0;
     if (type == 0 || type == 2) {
       // ---------------- DIAG(b) / PREP(b): v = b_b − Σ updates into supernode J
       const int b = idx;
@@ -723,6 +726,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         x[c0 + tid] = yv;
       }
       __syncthreads();
+      if (F.tprof && tid == 0) ta = gtime();
       if (one_chunk) {
         for (int r = tid; r < R0; r += NT) {
           double s = 0.0;
@@ -743,6 +747,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         }
       }
       __syncthreads();
+      if (F.tprof && tid == 0) tb = gtime();
       for (int64_t k = F.blk_dptr[b] + tid; k < F.blk_dptr[b + 1]; k += NT) {
         __threadfence();
         red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
@@ -833,7 +838,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         atomicAdd(F.cnt_f + F.tile_dest[ti], 1ull);
       }
     }
-    if (F.tprof) tprof_add(F.tprof, 0, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap);
+    if (F.tprof) tprof_add(F.tprof, 0, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap, ta, tb);
   }
   if (tid == 0) {
     unsigned d = atomicAdd(F.sweep + 1, 1u);
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
     if (task < 0) break;
     const int type = task >> 28, idx = task & ((1 << 28) - 1);
     const unsigned long long t0 = F.tprof ? gtime() : 0ull;
-    unsigned long long t1 = t0;
+    unsigned long long t1 = t0, ta = 0, tb = 0;
     if (type == 0 || type == 2) {
       const int b = idx;
       const int wk = F.blk_w[b];
@@ -1059,7 +1064,7 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
         atomicAdd(F.cnt_b + b, 1ull);
       }
     }
-    if (F.tprof) tprof_add(F.tprof, 1, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap);
+    if (F.tprof) tprof_add(F.tprof, 1, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap, ta, tb);
   }
   if (tid == 0) {
     unsigned d = atomicAdd(F.sweep + 1, 1u);

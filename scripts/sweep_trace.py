@@ -24,7 +24,8 @@ for sw in range(2):
     sm = tr[:, 0] >> 32
     typ, idx = task >> 28, task & ((1 << 28) - 1)
     t0 = tr[:, 1].min()
-    a, b, c = (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3, (tr[:, 3] - t0) / 1e3
+    a, b, c = (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3, (tr[:, 5] - t0) / 1e3
+    ma, mb = (tr[:, 3] - t0) / 1e3, (tr[:, 4] - t0) / 1e3
     L = np.where(np.isin(typ, [0, 2, 4]), lev[blk_sn[np.minimum(idx, len(blk_sn) - 1)]], -1)
     print(['fwd', 'bwd'][sw], 'tasks', len(tr), 'span %.1f us' % c.max(), 'SMs used', len(np.unique(sm)))
     for ty in np.unique(typ):
@@ -40,4 +41,7 @@ for sw in range(2):
     print('  setup (dep-met - start) by type:', {names[t]: '%.2f' % np.median((b - a)[typ == t]) for t in np.unique(typ)})
     print('  tasks per SM: min %d max %d' % (np.bincount(sm).min(), np.bincount(sm).max()))
     k = typ == 4
+    if k.any() and (tr[k, 3] > 0).any():
+        print('  SNF phases (us, median): dep->solved %.2f  solved->atomics done %.2f  atomics->end %.2f' % (
+            np.median(ma[k] - b[k]), np.median(mb[k] - ma[k]), np.median(c[k] - mb[k])))
     print('  SNF start quantiles', np.percentile(a[k], [10, 50, 90]).round(1), 'dep-start quantiles', np.percentile((b - a)[k], [10, 50, 90]).round(1))
