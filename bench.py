@@ -340,9 +340,13 @@ def run_ours(args, rank, world, local, use_dist):
             pass
     fwd_ms, fwd_n = prof["f_fwd"]
     bwd_ms, bwd_n = prof["f_bwd"]
+    root_ms, root_n = prof["f_root"]
     n_ipm_timed = max(0, min(K, r_prof["n_ipm"] - W))
     real_solves = pcg_prof + 2 * n_ipm_timed          # K_F products + r_ν and recovery F-solves (profiled pass)
-    solve_ms = fwd_ms + bwd_ms
+    solve_ms = fwd_ms + root_ms + bwd_ms
+    ss = s.structure("sn_start")
+    w_root = int(ss[-1] - ss[-2]) if st["sym_enabled"] else 0
+    root_bytes = 8.0 * w_root * (w_root + 1) / 2           # lower triangle of S⁻¹, read once per F-solve
     fsolve_bytes = st["fsolve_bytes_F"]
     achieved = real_solves * fsolve_bytes / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0.0
     paper_bytes = 2 * 8.0 * st["nnz_LF"]                # L_F values read twice per F-solve
@@ -361,6 +365,12 @@ def run_ours(args, rank, world, local, use_dist):
                 "paper_bytes_per_fsolve": paper_bytes,
                 "paper_formulation_GBps": real_solves * paper_bytes / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0,
                 "fsolve_ms_avg": solve_ms / max(1, real_solves),
+                "fsolve_split_ms": {"forward": fwd_ms / max(1, real_solves), "root_gemv": root_ms / max(1, real_solves),
+                                    "backward": bwd_ms / max(1, real_solves)},
+                "root_gemv": {"kernel": "k_symroot_gemv", "bytes": root_bytes,
+                              "achieved": (root_n * root_bytes / (root_ms / 1e3) / 1e9) if root_ms > 0 else None,
+                              "frac": (root_n * root_bytes / (root_ms / 1e3) / 1e9 / peak) if root_ms > 0 else None},
+                "flattened_forest": bool(st.get("flat_enabled", 0)),
                 "fsolve_share_of_step": solve_ms / ms_prof if ms_prof > 0 else None,
                 "timing": "kernel durations from a second pass over the same IPM steps with CUDA events "
                           "around every launch (the headline pass runs without events)"}

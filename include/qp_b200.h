@@ -207,20 +207,25 @@ typedef struct {
   double pcg_flops_per_iter;         /* 2c_trsv(L_F) + 2c_spmv(C) (+2c_trsv(L_PH)) */
   double sweep_bytes_F;              /* algorithmic bytes of one L_F sweep: 8·nnz(L_F) */
   double fsolve_bytes_F;             /* bytes one F-solve must read in this implementation: 8·(2·nnz of L_F
-                                        outside symmetric roots + w(w+1)/2 of each root's S⁻¹) */
+                                        outside symmetric roots + w(w+1)/2 of each root's S⁻¹); with the
+                                        flattened forest 8·(w(w+1)/2 + 2·nnz(M) + 2·nnz(L11⁻¹)) */
   double sym_discrepancy;            /* ‖y_S⁻¹ − y_X‖/‖y_X‖ of the factor-time accuracy guard */
   double sym_enabled;                /* 1 if the symmetric-root S⁻¹ shortcut is in use (guard ≤ 1e-10) */
+  double flat_discrepancy;           /* ‖y_flat − y_sweeps‖/‖y_sweeps‖ of the flattened-forest guard (−1: n/a) */
+  double flat_enabled;               /* 1 if F-solves use the flattened forest (M = L21·L11⁻¹) */
+  double flat_nnz_M;                 /* stored entries of M */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 
 /* Kernel-time accounting with CUDA events on the library stream.
  * qp_profile(ctx, 1) enables, 0 disables and clears.  qp_profile_read
  * returns, per class, accumulated ms and launch count:
- *  0 F forward sweep, 1 F backward sweep, 2 K_F q-SpMV (a5), 3 PCG vector
- *  updates (a6), 4 P_H sweeps (a7), 5 P_H refactor (a8), 6 IPM rhs (a9),
- *  7 other. */
+ *  0 F forward sweep (or flattened forward product), 1 F backward sweep (or
+ *  flattened backward product), 2 K_F q-SpMV (a5), 3 PCG vector updates (a6),
+ *  4 P_H sweeps (a7), 5 P_H refactor (a8), 6 IPM rhs (a9), 7 other,
+ *  8 symmetric-root GEMV of the F-solve, 9 reserved (10 entries each). */
 int qp_profile(qp_ctx* ctx, int32_t enable);
-int qp_profile_read(qp_ctx* ctx, double* ms /*8*/, int64_t* count /*8*/);
+int qp_profile_read(qp_ctx* ctx, double* ms /*10*/, int64_t* count /*10*/);
 
 /* Debug instrumentation of the L_F sweeps: enable = 1 resets and enables;
  * enable = 0 disables and copies 70 int64 = [fwd, bwd] × [DIAG, TILE, PREP,

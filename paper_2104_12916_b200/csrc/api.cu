@@ -190,6 +190,7 @@ struct Factor {
   int32_t* bwd_x = nullptr;
   double sym_discrepancy = 0.0;  // ‖y_sym − y_X‖ / ‖y_X‖ measured at factor time
   bool sym_enabled = false;
+  double flat_discrepancy = -1.0;  // ‖y_flat − y_sweep‖ / ‖y_sweep‖ at factor time (−1: not tried)
   const int32_t* fwd_sym = nullptr;
   const int32_t* bwd_sym = nullptr;
   int64_t n_fwd_sym = 0, n_bwd_sym = 0, n_fwd_x = 0, n_bwd_x = 0;
@@ -295,8 +296,8 @@ struct qp_ctx {
   struct Ev { int cls; cudaEvent_t a, b; };
   std::vector<Ev> evs;
   std::vector<cudaEvent_t> pool;
-  double prof_ms[8] = {0};
-  int64_t prof_cnt[8] = {0};
+  double prof_ms[10] = {0};
+  int64_t prof_cnt[10] = {0};
 
   cudaEvent_t get_ev() {
     if (!pool.empty()) {
@@ -469,6 +470,28 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.sn_nblk = m.upload(S.sn_nblk, st);
     d.blk_dptr = m.upload(S.blk_dptr, st);
     d.blk_dest = m.upload(S.blk_dest, st);
+    d.flat = 0;
+    if (S.flat) {
+      d.fl_rc0 = S.fl_rc0;
+      d.fl_roff = m.upload(S.fl_roff, st);
+      d.fl_rows = m.upload(S.fl_rows, st);
+      d.fl_moff = m.upload(S.fl_moff, st);
+      d.fl_mval = m.zeros<double>(S.fl_msize, st);
+      d.fl_cp = m.upload(S.fl_cp, st);
+      d.fl_ci = m.upload(S.fl_ci, st);
+      d.fl_rp = m.upload(S.fl_rp, st);
+      d.fl_rj = m.upload(S.fl_rj, st);
+      d.fl_r2c = m.upload(S.fl_r2c, st);
+      d.fl_nval = m.zeros<double>(S.fl_ci.size(), st);
+      d.fl_col2sn = m.upload(S.fl_col2sn, st);
+      d.fl_mt_J = m.upload(S.fl_mt_J, st);
+      d.fl_mt_q0 = m.upload(S.fl_mt_q0, st);
+      d.fl_mt_nq = m.upload(S.fl_mt_nq, st);
+      d.fl_nmt = (int64_t)S.fl_mt_J.size();
+      d.fl_mr_ptr = m.upload(S.fl_mr_ptr, st);
+      d.fl_mr_col = m.upload(S.fl_mr_col, st);
+      d.fl_mr_val = m.zeros<double>(S.fl_mr_col.size(), st);
+    }
     d.ready_sb = m.zeros<unsigned int>(S.ns, st);
     d.sn_done_b = m.zeros<unsigned long long>(S.ns, st);
     d.xexp_f = m.upload(S.xexp_f, st);
@@ -668,22 +691,33 @@ void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
   symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, done, c->sm_count * 3, c->stream);
 }
 
-void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
-  c->launches += 2;
-  SweepRhs r{};
-  r.rhs = rhs_f;
+// One F-solve on the right-hand side described by r: the task-graph sweeps, or — flattened forest —
+// forward product, root GEMV, backward product (three dependency-free kernels).
+void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
+  Factor& F = c->FF;
+  c->launches += F.d.flat ? 3 : 2;
   int h = c->begin(0);
-  trsv_forward(c->FF.d, r, out, c->tgrid, c->stream);
-  sym_gemv(c, c->FF, out, nullptr);
+  if (F.d.flat) flat_forward(F.d, r, out, c->sm_count, c->stream);
+  else trsv_forward(F.d, r, out, c->tgrid, c->stream);
+  c->end(h);
+  h = c->begin(8);
+  sym_gemv(c, F, out, r.done_flag);
   c->end(h);
   h = c->begin(1);
-  trsv_backward(c->FF.d, out, nullptr, c->tgrid, c->stream);
+  if (F.d.flat) flat_backward(F.d, out, r.done_flag, c->sm_count, c->stream);
+  else trsv_backward(F.d, out, r.done_flag, c->tgrid, c->stream);
   c->end(h);
+}
+
+void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
+  SweepRhs r{};
+  r.rhs = rhs_f;
+  f_solve_sweeps(c, r, out);
 }
 
 // q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
 int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode) {
-  c->launches += 3;
+  c->launches += 1;
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
   if (c->sharded) {
@@ -696,14 +730,8 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
     r.ct = c->Ctf;   // Cᵀp fused into the forward sweep (a1)
     r.p = p;
   }
-  int h = c->begin(0);
-  trsv_forward(c->FF.d, r, c->xbuf, c->tgrid, c->stream);
-  sym_gemv(c, c->FF, c->xbuf, r.done_flag);
-  c->end(h);
-  h = c->begin(1);
-  trsv_backward(c->FF.d, c->xbuf, r.done_flag, c->tgrid, c->stream);
-  c->end(h);
-  h = c->begin(2);
+  f_solve_sweeps(c, r, c->xbuf);
+  int h = c->begin(2);
   kf_q(c->Cf, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
   c->end(h);
   if (c->sharded && pcg_mode) {
@@ -1311,6 +1339,46 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     }
     c->FF.sym_discrepancy = nn > 0 ? std::sqrt(dn / nn) : 0.0;
     c->FF.use_symmetric_roots(c->FF.sym_discrepancy <= 1e-10 && std::isfinite(c->FF.sym_discrepancy));
+    // flattened forest: M = L21 L11⁻¹ and L11⁻¹ column by column from forward sweeps on unit vectors
+    // (the sweep kernels already validated above), then the same accuracy guard against the sweeps
+    Factor& F = c->FF;
+    const char* fe = std::getenv("QPB_FLAT");
+    if (F.S.flat && F.sym_enabled && !(fe && fe[0] == '0')) {
+      cudaMemsetAsync(c->rhs2, 0, N * 8, st);
+      SweepRhs ur{};
+      ur.rhs = c->rhs2;
+      for (int64_t col = 0; col < F.S.fl_rc0; ++col) {
+        flat_set_unit(c->rhs2, col, st);
+        trsv_forward(F.d, ur, c->xbuf, c->tgrid, st);
+        flat_extract(F.d, col, c->xbuf, c->rhs2, col, st);
+      }
+      {
+        DeviceArena tmp;
+        const int32_t* src = tmp.upload(F.S.fl_mr_src, st);
+        flat_fill_rows(F.d, src, (int64_t)F.S.fl_mr_src.size(), st);
+        cudaStreamSynchronize(st);
+        tmp.release();
+      }
+      cudaMemsetAsync(F.d.acc, 0, N * 8, st);
+      rc = cuda_check(c, "flattened forest extraction");
+      if (rc) return rc;
+      cudaMemcpyAsync(c->rhs2, r.data(), N * 8, cudaMemcpyHostToDevice, st);
+      f_solve_dev(c, c->rhs2, c->xbuf);
+      cudaMemcpyAsync(y2.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+      F.d.flat = 1;
+      f_solve_dev(c, c->rhs2, c->xbuf);
+      cudaMemcpyAsync(y1.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+      rc = sync_check(c, "flattened-forest guard");
+      if (rc) return rc;
+      double fd = 0, fn = 0;
+      for (int64_t i = 0; i < N; ++i) {
+        fd += (y1[i] - y2[i]) * (y1[i] - y2[i]);
+        fn += y2[i] * y2[i];
+      }
+      F.flat_discrepancy = fn > 0 ? std::sqrt(fd / fn) : 0.0;
+      F.d.flat = (F.flat_discrepancy <= 1e-10 && std::isfinite(F.flat_discrepancy)) ? 1 : 0;
+      if (!F.d.flat) cudaMemsetAsync(F.d.acc, 0, N * 8, st);   // the sweeps expect zero accumulators
+    }
   }
   // ---- P_H: T = C diag(H)⁻¹ Cᵀ pattern (host) and values (device), symbolic of D + T
   if (p == QP_PREC_HIGH) {
@@ -1612,8 +1680,13 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->fsolve_bytes_F = c->FF.sym_enabled || !c->factored
                             ? 8.0 * (2.0 * (double)(S.nnz_L - S.sym_true) + (double)S.sym_lower)
                             : 16.0 * (double)S.nnz_L;
+    if (c->FF.d.flat)   // forest read as M (twice) and L11⁻¹ (twice) instead of L11, L21
+      s->fsolve_bytes_F = 8.0 * ((double)S.sym_lower + 2.0 * (double)S.fl_msize + 2.0 * (double)S.fl_ci.size());
     s->sym_discrepancy = c->FF.sym_discrepancy;
     s->sym_enabled = c->FF.sym_enabled ? 1.0 : 0.0;
+    s->flat_discrepancy = c->FF.flat_discrepancy;
+    s->flat_enabled = c->FF.d.flat ? 1.0 : 0.0;
+    s->flat_nnz_M = (double)S.fl_msize;
   }
   return QP_OK;
 }
@@ -1644,7 +1717,7 @@ int qp_profile(qp_ctx* c, int32_t enable) {
 int qp_profile_read(qp_ctx* c, double* ms, int64_t* count) {
   if (!c) return QP_EINVAL;
   c->harvest();
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 10; ++i) {
     if (ms) ms[i] = c->prof_ms[i];
     if (count) count[i] = c->prof_cnt[i];
   }

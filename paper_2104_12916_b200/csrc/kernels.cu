@@ -1222,7 +1222,7 @@ void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t m
 // x_J += S_J⁻¹ v_J over the chunks (I, K0..K0+nK) of every symmetric root, grid-stride, no flags.
 template <int U, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* x, int64_t c_begin, int64_t c_end,
-                                                           const int* done_flag) {
+                                                           const int* done_flag, const double* sub) {
   __shared__ double vK[512];
   __shared__ double vI[64];
   __shared__ double red[576];
@@ -1238,8 +1238,13 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
     const int ncol = (int)(F.blk_col0[bK + nK - 1] + F.blk_w[bK + nK - 1] - cK);
     const int ncol_t = (int)((rI < cK + ncol ? rI : cK + ncol) - cK);
     __syncthreads();
-    for (int c = tid; c < ncol; c += NT) vK[c] = F.vbuf[cK + c];
-    if (tid < Rn) vI[tid] = F.vbuf[rI + tid];
+    if (sub != nullptr) {
+      for (int c = tid; c < ncol; c += NT) vK[c] = F.vbuf[cK + c] - sub[cK + c];
+      if (tid < Rn) vI[tid] = F.vbuf[rI + tid] - sub[rI + tid];
+    } else {
+      for (int c = tid; c < ncol; c += NT) vK[c] = F.vbuf[cK + c];
+      if (tid < Rn) vI[tid] = F.vbuf[rI + tid];
+    }
     __syncthreads();
     const int64_t ldx = F.sn_ldx[J];
     schunk_gemv<U>(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
@@ -1249,20 +1254,175 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
 }
 
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
-                  cudaStream_t s) {
+                  cudaStream_t s, const double* sub) {
   if (c_end <= c_begin) return;
   static int variant = std::getenv("QPB_GEMV_VARIANT") ? std::atoi(std::getenv("QPB_GEMV_VARIANT")) : 1;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   switch (variant) {
-    case 1: k_symroot_gemv<8, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
-    case 2: k_symroot_gemv<16, 2><<<sms * 2, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
-    case 3: k_symroot_gemv<16, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
-    case 4: k_symroot_gemv<4, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
-    default: k_symroot_gemv<8, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag); break;
+    case 1: k_symroot_gemv<8, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
+    case 2: k_symroot_gemv<16, 2><<<sms * 2, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
+    case 3: k_symroot_gemv<16, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
+    case 4: k_symroot_gemv<4, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
+    default: k_symroot_gemv<8, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
   }
   (void)grid;
 }
+
+
+// ------------------------------------------------------------------------- flattened forest
+// Right-hand side of a flattened F-solve: b_c = (Cᵀp)_c or rhs_c (warp per column); forest columns
+// → acc[0, rc0) (b1), root columns → vbuf (the root GEMV's right-hand side before − M b1); x = 0.
+__global__ void __launch_bounds__(NT) k_flat_rhs(DevFactor F, SweepRhs R, double* x) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t rc0 = F.fl_rc0, N = F.N;
+  for (int64_t c = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 5; c < N; c += ((int64_t)gridDim.x * NT) >> 5) {
+    double v;
+    if (R.ct.p != nullptr) {
+      v = 0.0;
+      if (c < R.ct.nrows) {
+        const int64_t q0 = __ldg(R.ct.p + c), q1 = __ldg(R.ct.p + c + 1);
+        for (int64_t q = q0 + lane; q < q1; q += 32) v += __ldg(R.ct.v + q) * __ldg(R.p + __ldg(R.ct.i + q));
+        v = warp_sum(v);
+      }
+    } else {
+      v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+    }
+    if (lane == 0) {
+      if (c < rc0) {
+        F.acc[c] = v;
+        F.vbuf[c] = 0.0;   // y1 accumulator (k_flat_fwd)
+      } else {
+        F.vbuf[c] = v;
+      }
+      x[c] = 0.0;
+    }
+  }
+}
+
+// Forward product: tasks [0, nY) — 8 forest columns each (warp per column c), vbuf[rows of L11⁻¹(:,c)]
+// += L11⁻¹(:,c) b1_c (y1 = L11⁻¹ b1; vbuf[0, rc0) zeroed by k_flat_rhs); tasks [nY, nY + nRr) — 8 root
+// rows each (warp per row r): vbuf[r] = b2_r − M(r,:) b1, a fixed-order dot product (no atomics).
+__global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_flag, int64_t nY) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t rc0 = F.fl_rc0, wr = F.N - rc0;
+  const int64_t total = nY + (wr + 7) / 8;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    if (t < nY) {
+      const int64_t c = t * 8 + wid;
+      if (c < rc0) {
+        const double bc = F.acc[c];
+        for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32)
+          atomicAdd(F.vbuf + F.fl_ci[e], F.fl_nval[e] * bc);
+      }
+    } else {
+      const int64_t r = (t - nY) * 8 + wid;
+      if (r < wr) {
+        const int64_t e0 = F.fl_mr_ptr[r], e1 = F.fl_mr_ptr[r + 1];
+        double s = 0.0;
+        int64_t e = e0 + lane;
+        for (; e + 96 < e1; e += 128) {
+          const double v0 = __ldg(F.fl_mr_val + e), v1 = __ldg(F.fl_mr_val + e + 32);
+          const double v2 = __ldg(F.fl_mr_val + e + 64), v3 = __ldg(F.fl_mr_val + e + 96);
+          const int c0 = __ldg(F.fl_mr_col + e), c1 = __ldg(F.fl_mr_col + e + 32);
+          const int c2 = __ldg(F.fl_mr_col + e + 64), c3 = __ldg(F.fl_mr_col + e + 96);
+          s += v0 * F.acc[c0] + v1 * F.acc[c1] + v2 * F.acc[c2] + v3 * F.acc[c3];
+        }
+        for (; e < e1; e += 32) s += __ldg(F.fl_mr_val + e) * F.acc[__ldg(F.fl_mr_col + e)];
+        s = warp_sum(s);
+        if (lane == 0) F.vbuf[rc0 + r] -= s;
+      }
+    }
+  }
+}
+
+__global__ void k_flat_fill_rows(DevFactor F, const int32_t* src, int64_t nnz) {
+  for (int64_t k = blockIdx.x * (int64_t)NT + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * NT)
+    F.fl_mr_val[k] = F.fl_mval[src[k]];
+}
+void flat_fill_rows(const DevFactor& F, const int32_t* src, int64_t nnz, cudaStream_t s) {
+  k_flat_fill_rows<<<148 * 8, NT, 0, s>>>(F, src, nnz);
+}
+
+// Backward product: the M tiles — x[cols of J] −= M_J(tile)ᵀ x_root(tile rows) (root values gathered
+// once per tile into shared memory, warp per column); tasks [nmt, nmt + nX): 8 forest columns each,
+// x_c += Σ_i L11⁻¹(i,c) y1_i / d_i.  x[0, rc0) was zeroed by k_flat_rhs.
+__global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const int* done_flag, int64_t nX) {
+  __shared__ double xr[512];
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t rc0 = F.fl_rc0, N = F.N;
+  const int64_t total = F.fl_nmt + nX;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    if (t < F.fl_nmt) {
+      const int J = F.fl_mt_J[t], q0 = F.fl_mt_q0[t], nq = F.fl_mt_nq[t];
+      const int64_t c0 = F.sn_start[J];
+      const int w = (int)(F.sn_start[J + 1] - c0);
+      const int64_t nr = F.fl_roff[J + 1] - F.fl_roff[J];
+      const int32_t* rows = F.fl_rows + F.fl_roff[J] + q0;
+      __syncthreads();
+      for (int q = tid; q < nq; q += NT) xr[q] = x[rc0 + __ldg(rows + q)];   // nq ≤ 2·NT
+      __syncthreads();
+      const double* Mj = F.fl_mval + F.fl_moff[J] + q0;
+      for (int c = wid; c < w; c += NT / 32) {
+        const double* Mc = Mj + (int64_t)c * nr;
+        double s = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < nq; q += 32) s += __ldg(Mc + q) * xr[q];
+        s = warp_sum(s);
+        if (lane == 0) atomicAdd(x + c0 + c, -s);
+      }
+    } else {
+      const int64_t c = (t - F.fl_nmt) * 8 + wid;
+      if (c < rc0) {
+        double u = 0.0;
+        for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32) {
+          const int32_t i = F.fl_ci[e];
+          u += F.fl_nval[e] * F.vbuf[i] / F.Dpiv[i];
+        }
+        u = warp_sum(u);
+        if (lane == 0) atomicAdd(x + c, u);
+      }
+    }
+  }
+}
+
+// Extraction of forest column `col` after a forward sweep with rhs = e_col (symmetric-root mode):
+// vbuf[root] = −M e_col and x[forest] = L11⁻¹ e_col.  Also moves the unit entry: unit[prev] = 0.
+__global__ void k_flat_extract(DevFactor F, int64_t col, const double* x, double* unit, int64_t prev) {
+  const int tid = threadIdx.x;
+  const int64_t rc0 = F.fl_rc0;
+  const int J = F.fl_col2sn[col];
+  const int64_t nr = F.fl_roff[J + 1] - F.fl_roff[J];
+  double* Mc = F.fl_mval + F.fl_moff[J] + (col - F.sn_start[J]) * nr;
+  const int32_t* rows = F.fl_rows + F.fl_roff[J];
+  for (int64_t q = blockIdx.x * (int64_t)NT + tid; q < nr; q += (int64_t)gridDim.x * NT) Mc[q] = -F.vbuf[rc0 + rows[q]];
+  for (int64_t e = F.fl_cp[col] + blockIdx.x * (int64_t)NT + tid; e < F.fl_cp[col + 1]; e += (int64_t)gridDim.x * NT)
+    F.fl_nval[e] = x[F.fl_ci[e]];
+  if (blockIdx.x == 0 && tid == 0) {
+    if (prev >= 0) unit[prev] = 0.0;
+  }
+}
+__global__ void k_set_unit(double* unit, int64_t col) { unit[col] = 1.0; }
+
+void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
+  const int g0 = (int)std::max<int64_t>(1, std::min<int64_t>((F.N * 32 + NT - 1) / NT, (int64_t)sms * 8));
+  k_flat_rhs<<<g0, NT, 0, s>>>(F, r, x);
+  const int64_t nY = (F.fl_rc0 + 7) / 8, nRr = (F.N - F.fl_rc0 + 7) / 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nY + nRr, (int64_t)sms * 8));
+  k_flat_fwd<<<grid, NT, 0, s>>>(F, r.done_flag, nY);
+}
+void flat_backward(const DevFactor& F, double* x, const int* done_flag, int sms, cudaStream_t s) {
+  const int64_t nX = (F.fl_rc0 + 7) / 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(F.fl_nmt + nX, 1), (int64_t)sms * 8));
+  k_flat_bwd<<<grid, NT, 0, s>>>(F, x, done_flag, nX);
+}
+void flat_extract(const DevFactor& F, int64_t col, const double* x, double* unit, int64_t prev, cudaStream_t s) {
+  k_flat_extract<<<8, NT, 0, s>>>(F, col, x, unit, prev);
+}
+void flat_set_unit(double* unit, int64_t col, cudaStream_t s) { k_set_unit<<<1, 1, 0, s>>>(unit, col); }
 
 static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)TRSV_SMEM_DBL; }
 

@@ -92,6 +92,27 @@ struct DevFactor {
   const int64_t* pan_pref;
   const int64_t* upd_pref;
   int* status;        // pivot failures (device int)
+  // flattened forest (Symbolic::flat): M_J blocks, L11⁻¹ (column-ordered values + both index forms)
+  int flat;                       // 1: F-solves use k_flat_fwd / root GEMV / k_flat_bwd
+  int64_t fl_rc0;
+  const int64_t* fl_roff;
+  const int32_t* fl_rows;
+  const int64_t* fl_moff;
+  double* fl_mval;
+  const int64_t* fl_cp;
+  const int32_t* fl_ci;
+  const int64_t* fl_rp;
+  const int32_t* fl_rj;
+  const int64_t* fl_r2c;
+  double* fl_nval;                // L11⁻¹ values in column order (fl_cp / fl_ci)
+  const int32_t* fl_col2sn;
+  const int32_t* fl_mt_J;
+  const int32_t* fl_mt_q0;
+  const int32_t* fl_mt_nq;
+  int64_t fl_nmt;
+  const int64_t* fl_mr_ptr;       // M by root rows (forward product)
+  const int32_t* fl_mr_col;
+  double* fl_mr_val;
   unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][7 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
@@ -173,8 +194,16 @@ void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cu
 void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s);
 int trsv_grid(int device);
 // x_J += S_J⁻¹ v_J for the symmetric-root chunks [c_begin, c_end) (dedicated kernel)
+// sub != nullptr: the root's right-hand side is vbuf − sub (flattened forest: sub = acc = M b1)
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
-                  cudaStream_t s);
+                  cudaStream_t s, const double* sub = nullptr);
+// flattened forest F-solve halves (see Symbolic::flat) and the per-column extraction of M and L11⁻¹
+void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s);
+void flat_backward(const DevFactor& F, double* x, const int* done_flag, int sms, cudaStream_t s);
+void flat_extract(const DevFactor& F, int64_t col, const double* x, double* unit, int64_t prev, cudaStream_t s);
+void flat_set_unit(double* unit, int64_t col, cudaStream_t s);
+// after the extraction: row-form values of M gathered from the M_J blocks
+void flat_fill_rows(const DevFactor& F, const int32_t* src, int64_t nnz, cudaStream_t s);
 
 // ---- vector / SpMV kernels
 void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,

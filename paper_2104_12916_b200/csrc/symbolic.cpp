@@ -10,6 +10,8 @@
 #include "symbolic.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <iterator>
 #include <cmath>
 #include <numeric>
 #include <stdexcept>
@@ -684,7 +686,118 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   S.pivsign.assign(N, 1);
   for (int64_t c = 0; c < std::min(N, n_negative); ++c) S.pivsign[c] = -1;
   (void)tile_begin;
+  if (allow_symroot) plan_flat(S);
   return "";
+}
+
+void plan_flat(Symbolic& S, int64_t max_cols, double max_rel_root) {
+  S.flat = false;
+  const bool verbose = std::getenv("QPB_VERBOSE") != nullptr;
+  auto no = [&](const char* why) {
+    if (verbose) std::fprintf(stderr, "qpb: flattened forest not used: %s\n", why);
+  };
+  const int64_t ns = S.ns;
+  if (ns < 1) return no("empty");
+  const int64_t J0 = ns - 1;
+  if (S.sn_sinv[J0] < 0 || S.sn_parent[J0] >= 0) return no("last supernode is not a symmetric root");
+  const int64_t rc0 = S.sn_start[J0];
+  const int64_t wr = S.N - rc0;
+  if (rc0 > max_cols) return no("forest too wide");
+  for (int64_t J = 0; J < J0; ++J) {
+    if (S.sn_sinv[J] >= 0 || S.sn_start[J + 1] - S.sn_start[J] > BW) return no("forest supernode wider than 64");
+  }
+  // R_J = ∪ root rows of the supernodes on the path J → root (children before parents in index
+  // order, so the parent's set is complete when J is processed top-down)
+  std::vector<std::vector<int32_t>> R(J0);
+  for (int64_t J = J0 - 1; J >= 0; --J) {
+    std::vector<int32_t> own;
+    for (int64_t q = S.sn_rowptr[J]; q < S.sn_rowptr[J + 1]; ++q)
+      if (S.sn_rows[q] >= rc0) own.push_back((int32_t)(S.sn_rows[q] - rc0));
+    const int64_t P = S.sn_parent[J];   // −1: a separate tree (no root rows above it)
+    if (P >= 0 && P != J0) {
+      std::vector<int32_t> u;
+      std::set_union(own.begin(), own.end(), R[P].begin(), R[P].end(), std::back_inserter(u));
+      R[J].swap(u);
+    } else {
+      R[J].swap(own);
+    }
+  }
+  int64_t nnzM = 0;
+  for (int64_t J = 0; J < J0; ++J) nnzM += (int64_t)R[J].size() * (S.sn_start[J + 1] - S.sn_start[J]);
+  if ((double)nnzM > max_rel_root * (double)wr * (double)(wr + 1) / 2) return no("M too large");
+  if (verbose) std::fprintf(stderr, "qpb: flattened forest: %lld columns, nnz(M) = %lld\n", (long long)rc0,
+                            (long long)nnzM);
+  S.flat = true;
+  S.fl_rc0 = rc0;
+  S.fl_roff.assign(J0 + 1, 0);
+  S.fl_moff.assign(J0 + 1, 0);
+  S.fl_rows.clear();
+  for (int64_t J = 0; J < J0; ++J) {
+    S.fl_rows.insert(S.fl_rows.end(), R[J].begin(), R[J].end());
+    S.fl_roff[J + 1] = (int64_t)S.fl_rows.size();
+    S.fl_moff[J + 1] = S.fl_moff[J] + (int64_t)R[J].size() * (S.sn_start[J + 1] - S.sn_start[J]);
+  }
+  S.fl_msize = S.fl_moff[J0];
+  // L11⁻¹ column patterns: column c of supernode J → J's columns ≥ c, then every forest ancestor's columns
+  S.fl_col2sn.assign(rc0, 0);
+  S.fl_cp.assign(rc0 + 1, 0);
+  S.fl_ci.clear();
+  for (int64_t J = 0; J < J0; ++J)
+    for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) {
+      S.fl_col2sn[c] = (int32_t)J;
+      for (int64_t r = c; r < S.sn_start[J + 1]; ++r) S.fl_ci.push_back((int32_t)r);
+      for (int64_t K = S.sn_parent[J]; K >= 0 && K != J0; K = S.sn_parent[K])
+        for (int64_t r = S.sn_start[K]; r < S.sn_start[K + 1]; ++r) S.fl_ci.push_back((int32_t)r);
+      S.fl_cp[c + 1] = (int64_t)S.fl_ci.size();
+    }
+  // row form with the index of each entry in the column-ordered values
+  S.fl_rp.assign(rc0 + 1, 0);
+  for (int32_t r : S.fl_ci) S.fl_rp[r + 1]++;
+  for (int64_t r = 0; r < rc0; ++r) S.fl_rp[r + 1] += S.fl_rp[r];
+  S.fl_rj.assign(S.fl_ci.size(), 0);
+  S.fl_r2c.assign(S.fl_ci.size(), 0);
+  {
+    std::vector<int64_t> pos(S.fl_rp.begin(), S.fl_rp.end() - 1);
+    for (int64_t c = 0; c < rc0; ++c)
+      for (int64_t e = S.fl_cp[c]; e < S.fl_cp[c + 1]; ++e) {
+        const int64_t d = pos[S.fl_ci[e]]++;
+        S.fl_rj[d] = (int32_t)c;
+        S.fl_r2c[d] = e;
+      }
+  }
+  // row form of M for the forward product (no atomics: one dot product per root row)
+  S.fl_mr_ptr.assign(wr + 1, 0);
+  for (int64_t J = 0; J < J0; ++J)
+    for (int32_t r : R[J]) S.fl_mr_ptr[r + 1] += S.sn_start[J + 1] - S.sn_start[J];
+  for (int64_t r = 0; r < wr; ++r) S.fl_mr_ptr[r + 1] += S.fl_mr_ptr[r];
+  S.fl_mr_col.assign(S.fl_mr_ptr[wr], 0);
+  S.fl_mr_src.assign(S.fl_mr_ptr[wr], 0);
+  {
+    std::vector<int64_t> pos(S.fl_mr_ptr.begin(), S.fl_mr_ptr.end() - 1);
+    for (int64_t J = 0; J < J0; ++J) {
+      const int64_t w = S.sn_start[J + 1] - S.sn_start[J], nr = (int64_t)R[J].size();
+      for (int64_t t = 0; t < w; ++t)
+        for (int64_t q = 0; q < nr; ++q) {
+          const int64_t d = pos[R[J][q]]++;
+          S.fl_mr_col[d] = (int32_t)(S.sn_start[J] + t);
+          S.fl_mr_src[d] = (int32_t)(S.fl_moff[J] + t * nr + q);
+        }
+    }
+  }
+  // backward M tiles
+  S.fl_mt_J.clear();
+  S.fl_mt_q0.clear();
+  S.fl_mt_nq.clear();
+  for (int64_t J = 0; J < J0; ++J) {
+    const int64_t w = S.sn_start[J + 1] - S.sn_start[J], nr = (int64_t)R[J].size();
+    // ≤ 2 rows per thread of a 256-thread CTA: every load of a tile is in flight at once
+    const int64_t cap = std::min<int64_t>(512, std::max<int64_t>(1, TILE_ELEMS / std::max<int64_t>(1, w)));
+    for (int64_t q = 0; q < nr; q += cap) {
+      S.fl_mt_J.push_back((int32_t)J);
+      S.fl_mt_q0.push_back((int32_t)q);
+      S.fl_mt_nq.push_back((int32_t)std::min(cap, nr - q));
+    }
+  }
 }
 
 }  // namespace qpb

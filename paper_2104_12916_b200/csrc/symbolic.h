@@ -103,6 +103,27 @@ struct Symbolic {
   int64_t xtmp_size = 0;                 // doubles of the inversion scratch
   std::vector<int64_t> sn_xtmp;          // scratch offset per big supernode
 
+  // flattened forest (two-factor partitioned inverse, see plan_flat): with a symmetric root J0
+  // (columns [rc0, N)) the forest part L11 (columns [0, rc0)) and its coupling L21 enter every
+  // F-solve only through  y1 = L11⁻¹ b1,  v2 = b2 − M b1  (M = L21 L11⁻¹)  and
+  // x1 = L11⁻ᵀ D1⁻¹ y1 − Mᵀ x2: dependency-free products instead of level-by-level sweeps.
+  bool flat = false;
+  int64_t fl_rc0 = 0;                 // first root column (= number of forest columns)
+  std::vector<int64_t> fl_roff;       // per forest supernode J (ns_f + 1): offset into fl_rows
+  std::vector<int32_t> fl_rows;       // R_J: root-relative rows of M[:, J] (sorted)
+  std::vector<int64_t> fl_moff;       // per forest supernode: offset of M_J (|R_J| × w_J, column-major)
+  int64_t fl_msize = 0;               // doubles of all M_J
+  std::vector<int64_t> fl_cp;         // L11⁻¹ by columns (rc0 + 1)
+  std::vector<int32_t> fl_ci;         //   rows of each column (own supernode's columns ≥ c, then ancestors')
+  std::vector<int64_t> fl_rp;         // L11⁻¹ by rows (rc0 + 1)
+  std::vector<int32_t> fl_rj;         //   columns of each row
+  std::vector<int64_t> fl_r2c;        //   index of each row entry in the column-ordered values
+  std::vector<int32_t> fl_col2sn;     // forest column → supernode
+  std::vector<int32_t> fl_mt_J, fl_mt_q0, fl_mt_nq;   // M tiles (nq·w_J ≤ TILE_ELEMS) of the backward product
+  std::vector<int64_t> fl_mr_ptr;     // M by root rows (w_root + 1): the forward product's row form
+  std::vector<int32_t> fl_mr_col;     //   forest column of each entry
+  std::vector<int32_t> fl_mr_src;     //   index of each entry in the M_J blocks (values copied once)
+
   // multifrontal plan
   std::vector<int64_t> asm_dst;    // destination in workspace for each lower entry (+diag)
   std::vector<double> asm_val;     // F: values; P_H: T-values filled on device
@@ -142,5 +163,10 @@ std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr,
 // ancestor-closed top of the tree reordered to the end).
 std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot = true,
                     int64_t trailing_from = -1);
+
+// Decide and plan the flattened forest for a factor whose last supernode is a symmetric root
+// (sets S.flat; no-op otherwise).  Limits: forest supernodes ≤ BW wide, rc0 ≤ max_cols, and
+// nnz(M) ≤ max_rel_root · w_root(w_root+1)/2 (bytes bounded against the root GEMV).
+void plan_flat(Symbolic& S, int64_t max_cols = 16384, double max_rel_root = 0.1);
 
 }  // namespace qpb

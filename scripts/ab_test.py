@@ -20,7 +20,7 @@ s.pcg_solve(D, b, tol=0.0, maxit=5)
 s.profile(False); s.profile(True)
 t = time.time(); x, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=60); dt = time.time() - t
 pr = s.profile_read()
-print(mode, 'wall ms/it %.3f' % (1e3 * dt / it), 'fwd ms %.3f' % (pr['f_fwd'][0] / pr['f_fwd'][1]), 'bwd ms %.3f' % (pr['f_bwd'][0] / pr['f_bwd'][1]))
+print(mode, 'wall ms/it %.3f' % (1e3 * dt / it), 'fwd ms %.3f' % (pr['f_fwd'][0] / pr['f_fwd'][1]), 'root ms %.3f' % (pr['f_root'][0] / max(1, pr['f_root'][1])), 'bwd ms %.3f' % (pr['f_bwd'][0] / pr['f_bwd'][1]))
 s.profile(False)
 for _ in range(2):
     t = time.time(); x, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=200); dt = time.time() - t
