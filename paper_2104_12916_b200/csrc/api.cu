@@ -604,7 +604,7 @@ void plan_inverse(qp_ctx* c, Factor& F) {
       int64_t acc = 0;
       for (const GemmProb& p : v) {
         pref.push_back(acc);
-        acc += (int64_t)((p.M + 63) / 64) * ((p.N + 63) / 64);
+        acc += (int64_t)((p.M + 127) / 128) * ((p.N + 127) / 128);   // k_gemm128 tiles
         all.push_back(p);
       }
       pref.push_back(acc);
@@ -624,7 +624,7 @@ void plan_inverse(qp_ctx* c, Factor& F) {
     GemmProb g{F.d.xinv + S.sn_xtr[J], F.d.xinv + S.sn_xinv[J], F.d.xinv + S.sn_sinv[J], (int)w, (int)w, (int)w,
                (int)ldx, (int)ldx, (int)ldx, 1.0, 0.0, 2 | 4 | 8, 0};
     spref.push_back(acc);
-    acc += ((w + 63) / 64) * ((w + 63) / 64);
+    acc += ((w + 127) / 128) * ((w + 127) / 128);
     sp.push_back(g);
   }
   spref.push_back(acc);

@@ -1078,59 +1078,89 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
 }
 
 // ------------------------------------------------------------------------- partitioned inverse
-// Batched C = α·A·B + β·C (column-major), 64×64 C tile per CTA, K in chunks of 32.
-__global__ void __launch_bounds__(NT) k_gemm_batched(const GemmProb* probs, const int64_t* pref, int nprob) {
-  __shared__ double As[32 * 64];
-  __shared__ double Bs[32 * 64];
+// Batched C = α·A·B + β·C (column-major) on CUDA-core fp64: 128×128 C tile per 256-thread CTA,
+// 8×8 outputs per thread (rows ty·2 + {0,1} + {0,32,64,96}, columns likewise from tx) so every
+// shared-memory fragment load is a conflict-free 128-bit read, K in chunks of 8 staged by cp.async
+// into a double buffer (loads of chunk k+1 overlap the 64 DFMA per k-step of chunk k).
+constexpr int G_T = 128, G_K = 8, G_LD = G_T + 4;
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = ok ? 8 : 0;   // src-size 0 ⇒ zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__global__ void __launch_bounds__(256, 1) k_gemm128(const GemmProb* probs, const int64_t* pref, int nprob) {
+  __shared__ __align__(16) double As[2][G_K * G_LD];
+  __shared__ __align__(16) double Bs[2][G_K * G_LD];
   const int p = find_seg(pref, nprob + 1, blockIdx.x);
   const GemmProb P = probs[p];
   const int64_t t = blockIdx.x - pref[p];
-  const int tilesM = (P.M + 63) / 64;
+  const int tilesM = (P.M + G_T - 1) / G_T;
   const int ti = (int)(t % tilesM), tj = (int)(t / tilesM);
-  const int r0 = ti * 64, c0 = tj * 64;
   if ((P.flags & 8) && tj > ti) return;
+  const int r0 = ti * G_T, c0 = tj * G_T;
   int kmin = (P.flags & 2) ? c0 : 0;
   if (P.flags & 4) kmin = max(kmin, r0);
-  int kmax = (P.flags & 1) ? min(P.K, r0 + 64) : P.K;
+  const int kmax = (P.flags & 1) ? min(P.K, r0 + G_T) : P.K;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double acc[4][4];
+  double acc[8][8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int k0 = kmin; k0 < kmax; k0 += 32) {
-    const int kc = min(32, kmax - k0);
-    for (int idx = tid; idx < 32 * 64; idx += NT) {
-      int r = idx & 63, k = idx >> 6;
-      As[k * 64 + r] = (k < kc && r0 + r < P.M) ? P.A[(r0 + r) + (int64_t)(k0 + k) * P.lda] : 0.0;
-      int kk = idx & 31, c = idx >> 5;
-      Bs[kk * 64 + c] = (kk < kc && c0 + c < P.N) ? P.B[(k0 + kk) + (int64_t)(c0 + c) * P.ldb] : 0.0;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  // chunk loader: A(r0 + m, k0 + k) → As[k][m];  B(k0 + k, c0 + n) → Bs[k][n]  (4 + 4 per thread)
+  auto load = [&](int buf, int k0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + 256 * u;
+      const int m = idx & (G_T - 1), k = idx >> 7;
+      const bool ok = r0 + m < P.M && k0 + k < kmax;
+      cp_async8(&As[buf][k * G_LD + m], P.A + (ok ? (int64_t)(r0 + m) + (int64_t)(k0 + k) * P.lda : 0), ok);
+      const int kk = idx & (G_K - 1), n = idx >> 3;
+      const bool okb = c0 + n < P.N && k0 + kk < kmax;
+      cp_async8(&Bs[buf][kk * G_LD + n], P.B + (okb ? (int64_t)(k0 + kk) + (int64_t)(c0 + n) * P.ldb : 0), okb);
     }
+    cp_async_commit();
+  };
+  if (kmin < kmax) load(0, kmin);
+  int buf = 0;
+  for (int k0 = kmin; k0 < kmax; k0 += G_K) {
+    cp_async_wait_all();
     __syncthreads();
+    if (k0 + G_K < kmax) load(buf ^ 1, k0 + G_K);
+    const double* as = As[buf];
+    const double* bs = Bs[buf];
 #pragma unroll 4
-    for (int k = 0; k < 32; ++k) {
-      double a[4], b[4];
+    for (int k = 0; k < G_K; ++k) {
+      double a[8], b[8];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) a[x] = As[k * 64 + tx + 16 * x];
+      for (int g = 0; g < 4; ++g) {
+        const double2 va = *reinterpret_cast<const double2*>(as + k * G_LD + g * 32 + ty * 2);
+        const double2 vb = *reinterpret_cast<const double2*>(bs + k * G_LD + g * 32 + tx * 2);
+        a[2 * g] = va.x;
+        a[2 * g + 1] = va.y;
+        b[2 * g] = vb.x;
+        b[2 * g + 1] = vb.y;
+      }
 #pragma unroll
-      for (int y = 0; y < 4; ++y) b[y] = Bs[k * 64 + ty + 16 * y];
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
-    __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
-  for (int y = 0; y < 4; ++y) {
-    const int c = c0 + ty + 16 * y;
+  for (int j = 0; j < 8; ++j) {
+    const int c = c0 + (j >> 1) * 32 + tx * 2 + (j & 1);
     if (c >= P.N) continue;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int r = r0 + tx + 16 * x;
+    for (int i = 0; i < 8; ++i) {
+      const int r = r0 + (i >> 1) * 32 + ty * 2 + (i & 1);
       if (r >= P.M) continue;
       double* cp = P.C + r + (int64_t)c * P.ldc;
-      *cp = P.alpha * acc[x][y] + (P.beta != 0.0 ? P.beta * *cp : 0.0);
+      *cp = P.alpha * acc[i][j] + (P.beta != 0.0 ? P.beta * *cp : 0.0);
     }
   }
 }
@@ -1138,7 +1168,7 @@ __global__ void __launch_bounds__(NT) k_gemm_batched(const GemmProb* probs, cons
 void gemm_batched(const GemmProb* probs, const int64_t* tile_pref, int nprob, int64_t total_tiles,
                   cudaStream_t s) {
   if (total_tiles <= 0) return;
-  k_gemm_batched<<<(unsigned)total_tiles, NT, 0, s>>>(probs, tile_pref, nprob);
+  k_gemm128<<<(unsigned)total_tiles, 256, 0, s>>>(probs, tile_pref, nprob);   // tile_pref counts 128×128 tiles
 }
 
 // X_J := unit-lower L_JJ below the diagonal tiles, L_kk⁻¹ on the 64×64 diagonal tiles, 0 above.

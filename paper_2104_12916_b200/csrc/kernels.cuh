@@ -175,6 +175,7 @@ struct GemmProb {
               // 4: A upper-triangular (k >= row), 8: only tiles with tj <= ti (lower half, diagonal tiles full)
   int pad;
 };
+// tile_pref: per problem prefix of ⌈M/128⌉·⌈N/128⌉ tiles
 void gemm_batched(const GemmProb* probs, const int64_t* tile_pref, int nprob, int64_t total_tiles,
                   cudaStream_t s);
 void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t max_w2, cudaStream_t s);
