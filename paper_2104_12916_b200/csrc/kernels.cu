@@ -115,6 +115,15 @@ __device__ __forceinline__ int find_seg(const int64_t* pref, int n, int64_t x) {
   return lo;
 }
 
+// 8-byte global→shared asynchronous copies (zero fill when !ok)
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = ok ? 8 : 0;   // src-size 0 ⇒ zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 // ------------------------------------------------------------------------- multifrontal
 __global__ void k_mf_zero_fronts(DevFactor F, int64_t fr_off, int n_fr, int64_t total) {
   const int32_t* fr = F.lev_fronts + fr_off;
@@ -255,11 +264,18 @@ __global__ void __launch_bounds__(NT) k_mf_panel(DevFactor F, int k, int64_t act
 }
 
 // UPDATE: A_ij −= L_ik D_k L_jkᵀ on the trailing tiles (i ≥ j > k) of each front.
+// UPDATE A_ij −= L_ik D_k L_jkᵀ over the trailing lower triangle of each active front: one 64×64 tile
+// per 256-thread CTA, 4×4 outputs per thread (rows tx·2 + {0,1} + {0,32}: a warp's stores cover 32
+// consecutive rows of a column; columns likewise from ty) so
+// the fragments are conflict-free 128-bit shared loads (4 per 16 DFMA), the ≤ 64 pivot columns staged
+// by cp.async in double-buffered chunks of 16 (≈ 80 registers: 3 CTAs per SM overlap their epilogues),
+// D_k applied to the column operand in registers.
 __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t act_off, int n_act,
                                                   int64_t pref_off) {
-  extern __shared__ double dsm[];
-  double* Ls = dsm;
-  double* Rs = dsm + 64 * 68;
+  constexpr int KC = 16, LD = 64 + 4;
+  __shared__ __align__(16) double As[2][KC * LD];
+  __shared__ __align__(16) double Bs[2][KC * LD];
+  __shared__ double Dk[64];
   const int64_t* pref = F.upd_pref + pref_off;
   const int a = find_seg(pref, n_act + 1, blockIdx.x);
   const int J = F.act[act_off + a];
@@ -281,40 +297,57 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t ac
   const int Ri = (int)(ie - ib), Rj = (int)(je - jb);
   const int64_t noff = F.blk_noff[b];
   const double* L = F.fstore + F.blk_off[b] - (p0 + wk);  // index by front row
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < 64 * wk; idx += NT) {
-    int r = idx & 63, c = idx >> 6;
-    double d = F.Dpiv[c0 + p0 + c];
-    Ls[c * 68 + r] = r < Ri ? L[ib + r + (int64_t)c * noff] * d : 0.0;
-    Rs[c * 68 + r] = r < Rj ? L[jb + r + (int64_t)c * noff] : 0.0;
-  }
-  __syncthreads();
-  const int tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  if (tid < wk) Dk[tid] = F.Dpiv[c0 + p0 + tid];
+  auto load = [&](int buf, int k0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + NT * u;
+      const int r = idx & 63, c = idx >> 6;
+      const bool oka = r < Ri && k0 + c < wk, okb = r < Rj && k0 + c < wk;
+      cp_async8(&As[buf][c * LD + r], L + (oka ? ib + r + (int64_t)(k0 + c) * noff : 0), oka);
+      cp_async8(&Bs[buf][c * LD + r], L + (okb ? jb + r + (int64_t)(k0 + c) * noff : 0), okb);
+    }
+    cp_async_commit();
+  };
   double acc[4][4];
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-  for (int c = 0; c < wk; ++c) {
-    double lr[4], rs[4];
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  load(0, 0);
+  int buf = 0;
+  for (int k0 = 0; k0 < wk; k0 += KC) {
+    cp_async_wait_all();
+    __syncthreads();
+    if (k0 + KC < wk) load(buf ^ 1, k0 + KC);
+    const double* as = As[buf];
+    const double* bs = Bs[buf];
+#pragma unroll 8
+    for (int kk = 0; kk < KC; ++kk) {
+      const double d = (k0 + kk < wk) ? Dk[k0 + kk] : 0.0;
+      const double2 a0 = *reinterpret_cast<const double2*>(as + kk * LD + tx * 2);
+      const double2 a1 = *reinterpret_cast<const double2*>(as + kk * LD + 32 + tx * 2);
+      const double2 b0 = *reinterpret_cast<const double2*>(bs + kk * LD + ty * 2);
+      const double2 b1 = *reinterpret_cast<const double2*>(bs + kk * LD + 32 + ty * 2);
+      const double av[4] = {a0.x, a0.y, a1.x, a1.y};
+      const double bv[4] = {b0.x * d, b0.y * d, b1.x * d, b1.y * d};
 #pragma unroll
-    for (int x = 0; x < 4; ++x) lr[x] = Ls[c * 68 + tx + 16 * x];
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int y = 0; y < 4; ++y) rs[y] = Rs[c * 68 + ty + 16 * y];
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) acc[x][y] = fma(lr[x], rs[y], acc[x][y]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    buf ^= 1;
   }
 #pragma unroll
-  for (int y = 0; y < 4; ++y) {
-    int s = ty + 16 * y;
+  for (int j = 0; j < 4; ++j) {
+    const int s = (j >> 1) * 32 + ty * 2 + (j & 1);
     if (s >= Rj) continue;
     double* col = F.ws + fo + (jb + s) * m + ib;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      int r = tx + 16 * x;
-      if (r < Ri) col[r] -= acc[x][y];
+    for (int i = 0; i < 4; ++i) {
+      const int r = (i >> 1) * 32 + tx * 2 + (i & 1);
+      if (r < Ri) col[r] -= acc[i][j];
     }
   }
 }
@@ -339,16 +372,15 @@ void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref
              int64_t upd_total, cudaStream_t s) {
   if (n_act == 0) return;
   static bool attr = false;
-  const size_t sd = 2 * 64 * 65 * 8, sp = (2 * 64 * 65 + 64) * 8, su = 2 * 64 * 68 * 8;
+  const size_t sd = 2 * 64 * 65 * 8, sp = (2 * 64 * 65 + 64) * 8;
   if (!attr) {
     cudaFuncSetAttribute(k_mf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
     cudaFuncSetAttribute(k_mf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp);
-    cudaFuncSetAttribute(k_mf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)su);
     attr = true;
   }
   k_mf_diag<<<n_act, NT, sd, s>>>(F, k, act_off);
   if (pan_total > 0) k_mf_panel<<<(unsigned)pan_total, NT, sp, s>>>(F, k, act_off, n_act, pref_off);
-  if (upd_total > 0) k_mf_update<<<(unsigned)upd_total, NT, su, s>>>(F, k, act_off, n_act, pref_off);
+  if (upd_total > 0) k_mf_update<<<(unsigned)upd_total, NT, 0, s>>>(F, k, act_off, n_act, pref_off);
 }
 
 // ------------------------------------------------------------------------- triangular sweeps
@@ -1079,18 +1111,11 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
 
 // ------------------------------------------------------------------------- partitioned inverse
 // Batched C = α·A·B + β·C (column-major) on CUDA-core fp64: 128×128 C tile per 256-thread CTA,
-// 8×8 outputs per thread (rows ty·2 + {0,1} + {0,32,64,96}, columns likewise from tx) so every
+// 8×8 outputs per thread (rows tx·2 + {0,1} + {0,32,64,96}: coalesced column stores; columns likewise
+// from ty) so every
 // shared-memory fragment load is a conflict-free 128-bit read, K in chunks of 8 staged by cp.async
 // into a double buffer (loads of chunk k+1 overlap the 64 DFMA per k-step of chunk k).
 constexpr int G_T = 128, G_K = 8, G_LD = G_T + 4;
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool ok) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = ok ? 8 : 0;   // src-size 0 ⇒ zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
 __global__ void __launch_bounds__(256, 1) k_gemm128(const GemmProb* probs, const int64_t* pref, int nprob) {
   __shared__ __align__(16) double As[2][G_K * G_LD];
   __shared__ __align__(16) double Bs[2][G_K * G_LD];
@@ -1137,8 +1162,8 @@ __global__ void __launch_bounds__(256, 1) k_gemm128(const GemmProb* probs, const
       double a[8], b[8];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const double2 va = *reinterpret_cast<const double2*>(as + k * G_LD + g * 32 + ty * 2);
-        const double2 vb = *reinterpret_cast<const double2*>(bs + k * G_LD + g * 32 + tx * 2);
+        const double2 va = *reinterpret_cast<const double2*>(as + k * G_LD + g * 32 + tx * 2);
+        const double2 vb = *reinterpret_cast<const double2*>(bs + k * G_LD + g * 32 + ty * 2);
         a[2 * g] = va.x;
         a[2 * g + 1] = va.y;
         b[2 * g] = vb.x;
@@ -1153,11 +1178,11 @@ __global__ void __launch_bounds__(256, 1) k_gemm128(const GemmProb* probs, const
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const int c = c0 + (j >> 1) * 32 + tx * 2 + (j & 1);
+    const int c = c0 + (j >> 1) * 32 + ty * 2 + (j & 1);
     if (c >= P.N) continue;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int r = r0 + (i >> 1) * 32 + ty * 2 + (i & 1);
+      const int r = r0 + (i >> 1) * 32 + tx * 2 + (i & 1);
       if (r >= P.M) continue;
       double* cp = P.C + r + (int64_t)c * P.ldc;
       *cp = P.alpha * acc[i][j] + (P.beta != 0.0 ? P.beta * *cp : 0.0);
