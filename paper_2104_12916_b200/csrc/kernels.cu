@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t ac
   const double* L = F.fstore + F.blk_off[b] - (p0 + wk);  // index by front row
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   if (tid < wk) Dk[tid] = F.Dpiv[c0 + p0 + tid];
+  {   // pull the C tile into L2 now so the read-modify-write epilogue does not wait on HBM
+    const int cc = tid >> 2, seg = tid & 3;   // 64 columns × 4 lines of 16 doubles
+    if (cc < Rj && seg * 16 < Ri) prefetch_l2(F.ws + fo + (jb + cc) * m + ib + seg * 16);
+  }
   auto load = [&](int buf, int k0) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
