@@ -2,15 +2,14 @@
 
 Usage: python scripts/launch_summary.py gpurun_out/launches.csv "<command line>" > profiles/rN_launches_summary.txt
 
-Kernels are split into setup (factorization / inverses, run once per ipm_factor_once) and
-step (everything an IPM iteration launches), so the step-share of each kernel can be compared
-with bench.py's live `fsolve_share_of_step`.
+Launches are split by ORDER into setup (everything before the first IPM kernel, k_ipm_mu:
+factorization, inverses, accuracy guards, flattened-forest extraction) and step (the IPM
+iterations), so the step-share of each kernel can be compared with bench.py's live
+`fsolve_share_of_step`.
 """
 import csv
 import sys
 from collections import defaultdict
-
-SETUP = ("k_mf_", "k_gemm", "k_build_xinv", "k_transpose_xinv", "k_scale_xinv", "k_t_values")
 
 
 def main(path, cmd):
@@ -25,18 +24,18 @@ def main(path, cmd):
         val = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
         scale = {"ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "nsecond": 1.0}[unit]
-        rows.append((name, val * scale))
-    agg = defaultdict(lambda: [0, 0.0])
-    for n, t in rows:
-        agg[n][0] += 1
-        agg[n][1] += t
-    setup = {k: v for k, v in agg.items() if k.startswith(SETUP)}
-    step = {k: v for k, v in agg.items() if not k.startswith(SETUP)}
+        rows.append((int(r["ID"]), name, val * scale))
+    first_ipm = min((i for i, n, _ in rows if n.startswith("k_ipm_")), default=0)
+    setup, step = defaultdict(lambda: [0, 0.0]), defaultdict(lambda: [0, 0.0])
+    for i, n, t in rows:
+        d = setup if i < first_ipm else step
+        d[n][0] += 1
+        d[n][1] += t
     print(f"# ncu --metrics gpu__time_duration.sum --clock-control none: {cmd}")
     print("# (B200). Per-launch times are cold-cache and serialised: compare SHARES, not absolutes.")
     print(f"# {len(rows)} launches total; times in ns")
-    for title, d in (("STEP kernels (IPM iteration: residuals, F-solves, PCG, recovery, step)", step),
-                     ("SETUP kernels (ipm_factor_once: multifrontal LDL^T, partitioned inverses)", setup)):
+    for title, d in (("STEP kernels (IPM iterations: residuals, F-solves, PCG, recovery, step)", step),
+                     ("SETUP kernels (ipm_factor_once: LDL^T, inverses, guards, forest extraction)", setup)):
         tot = sum(v[1] for v in d.values()) or 1.0
         print(f"\n## {title}: {sum(v[0] for v in d.values())} launches, {tot / 1e6:.3f} ms")
         print(f"{'kernel':40s} {'launches':>9s} {'sum_ns':>14s} {'avg_ns':>11s} {'share':>7s}")
