@@ -57,3 +57,22 @@ def test_min_degree_reduces_fill():
     nat = P.Analysis(qp.H, qp.A, np.arange(qp.n)).stats()["nnz_LF"]
     md = P.Analysis(qp.H, qp.A).stats()["nnz_LF"]
     assert md < nat
+
+
+def test_setup_rejects_bad_inputs_before_touching_a_gpu():
+    """qp_setup validates shapes, CSR canonicality, symmetry and finiteness first (QP_EINVAL), so these
+    errors are reported identically with or without a GPU."""
+    import numpy as np
+    import scipy.sparse as sp
+    from paper_2104_12916_b200.binding import QPError, QPSolver
+    qp = qpgen.make("c0")
+    bad_g = qp.g.copy()
+    bad_g[0] = np.nan
+    H_asym = sp.csr_matrix(qp.H.toarray() + np.triu(np.ones((qp.n, qp.n)), 1) * 1e-3)
+    for args in ((qp.H, qp.A, qp.C, bad_g, qp.b, qp.d),
+                 (H_asym, qp.A, qp.C, qp.g, qp.b, qp.d),
+                 (qp.H, qp.A, sp.csr_matrix((0, qp.n)), qp.g, qp.b, np.zeros(0)),
+                 (qp.H, sp.csr_matrix((qp.n + 1, qp.n)), qp.C, qp.g, np.zeros(qp.n + 1), qp.d)):
+        with pytest.raises(QPError) as e:
+            QPSolver(*args)
+        assert e.value.code == -1, e.value

@@ -218,3 +218,89 @@ def test_ph_pcg_counts_along_oracle_trajectory():
     perm = s.structure("perm")[:qp.n]
     bad = _check_trajectory(qp, s, "high", [DenseF(qp.H, qp.A), SparseF(qp.H, qp.A, perm)])
     assert not bad, bad
+
+
+def test_ph_pcg_matches_oracle():
+    """PH-KF: P_H = D + C diag(H)⁻¹ Cᵀ refactored at D; counts ±2, solution 1e-8."""
+    qp = qpgen.scaled_random_qp(500, 120, 700, seed=12)
+    from paper_2104_12916_b200.binding import from_qp
+    s = from_qp(qp)
+    rng = np.random.default_rng(3)
+    D0 = rng.uniform(0.5, 2.0, qp.m2)
+    s.ipm_factor_once("high", D0=D0)
+    fs = DenseF(qp.H, qp.A)
+    T = kkt.T_matrix(qp)
+    for D in (D0, rng.uniform(0.05, 20.0, qp.m2)):        # second D forces a P_H refactor
+        b = rng.standard_normal(qp.m2)
+        x, it, rr, rc = s.pcg_solve(D, b, tol=1e-12, maxit=2000)
+        xr, itr, *_ = oracle_pcg(lambda v: kkt.KF_apply(qp, fs, D, v), b, kkt.PrecondH(qp, D, T=T), 1e-12, 2000)
+        assert abs(it - itr) <= 2
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def test_pl_one_iteration_when_m1_equals_n():
+    """m1 = n ⇒ K_F = D ⇒ PL-CG converges in exactly 1 iteration."""
+    qp = qpgen.make_syqp(32, 32)
+    s = solver(qp)
+    D = np.random.default_rng(4).uniform(0.5, 2.0, qp.m2)
+    b = np.random.default_rng(5).standard_normal(qp.m2)
+    x, it, rr, rc = s.pcg_solve(D, b, tol=1e-10, maxit=100)
+    assert it == 1
+
+
+def test_ph_one_iteration_m1_zero_diagonal_H():
+    """m1 = 0 and diagonal H ⇒ P_H = K_F ⇒ 1 iteration (Theorem 2 with m1 = 0)."""
+    import scipy.sparse as sp
+    n, m2 = 40, 60
+    rng = np.random.default_rng(6)
+    H = qpgen.canonical_csr(sp.diags(rng.uniform(0.5, 2.0, n)))
+    C = qpgen.canonical_csr(sp.random(m2, n, density=0.1, random_state=2) + sp.identity(n).tocsr()[[i % n for i in range(m2)]])
+    qp = qpgen.QP(H=H, A=qpgen.canonical_csr(sp.csr_matrix((0, n))), C=C, g=rng.standard_normal(n), b=np.zeros(0),
+                  d=np.zeros(m2))
+    from paper_2104_12916_b200.binding import from_qp
+    s = from_qp(qp)
+    D = rng.uniform(0.5, 2.0, m2)
+    s.ipm_factor_once("high", D0=D)
+    _, it, _, _ = s.pcg_solve(D, rng.standard_normal(m2), tol=1e-10, maxit=100)
+    assert it == 1
+
+
+def test_ph_ipm_matches_oracle():
+    qp = qpgen.make("c0")
+    from paper_2104_12916_b200.binding import from_qp
+    s = from_qp(qp)
+    s.ipm_factor_once("high")
+    got = s.ipm_solve(ipm_tol=1e-10)
+    ref = oracle_ipm(qp, precond="high", ipm_tol=1e-10)
+    assert got["converged"] and ref.converged
+    assert abs(got["objective"] - ref.objective) <= 1e-8 * abs(ref.objective)
+
+
+# ---------------------------------------------------------------- degenerate cases and call-order errors
+def test_pcg_zero_rhs_and_maxit():
+    """b = 0 ⇒ 0 iterations and Δν = 0 (oracle.pcg's convention); maxit reached ⇒ QP_MAXIT (status 1,
+    non-fatal) with exactly maxit iterations."""
+    qp = qpgen.make("c0")
+    s = solver(qp)
+    D = np.random.default_rng(8).uniform(0.5, 2.0, qp.m2)
+    x, it, rr, rc = s.pcg_solve(D, np.zeros(qp.m2), tol=1e-8, maxit=50)
+    assert it == 0 and rc == 0 and not np.any(x)
+    b = np.random.default_rng(9).standard_normal(qp.m2)
+    x, it, rr, rc = s.pcg_solve(D, b, tol=1e-30, maxit=7)
+    assert rc == 1 and it == 7 and rr > 0
+
+
+def test_call_order_and_bad_inputs():
+    from paper_2104_12916_b200.binding import QPError, from_qp
+    qp = qpgen.make("c0")
+    s = from_qp(qp)
+    with pytest.raises(QPError) as e:                       # pcg_solve before ipm_factor_once
+        s.pcg_solve(np.ones(qp.m2), np.ones(qp.m2))
+    assert e.value.code == -7
+    s.ipm_factor_once("low")
+    with pytest.raises(QPError) as e:                       # the factor of F is computed once
+        s.ipm_factor_once("low")
+    assert e.value.code == -7
+    with pytest.raises(QPError) as e:   # PCG breakdown: D = −10 I makes K_F negative definite, pᵀq < 0
+        s.pcg_solve(-10.0 * np.ones(qp.m2), np.random.default_rng(1).standard_normal(qp.m2), tol=1e-12, maxit=100)
+    assert e.value.code == -3

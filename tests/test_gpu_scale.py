@@ -100,3 +100,26 @@ def test_ipm_exact_recovery_decay(big):
         if qp.m1:
             assert np.abs(e1 - (1 - a) * e0).max() <= 1e-8 * (np.abs(e0).max() + 1e-9) + 1e-10
         g0, e0 = g1, e1
+
+
+def test_flattened_forest_c1():
+    """c1 uses the flattened forest: the factor-time guard agreed with the sweeps to 1e-12,
+    and a K_F product through it matches one through the sweeps (QPB_FLAT=0) to 1e-11."""
+    import os
+    from paper_2104_12916_b200.binding import from_qp
+    qp = qpgen.make("c1")
+    s = from_qp(qp)
+    s.ipm_factor_once("low")
+    st = s.stats()
+    assert st["flat_enabled"] == 1.0 and 0 <= st["flat_discrepancy"] <= 1e-12
+    os.environ["QPB_FLAT"] = "0"
+    try:
+        s0 = from_qp(qp)
+        s0.ipm_factor_once("low")
+    finally:
+        del os.environ["QPB_FLAT"]
+    assert s0.stats()["flat_enabled"] == 0.0
+    rng = np.random.default_rng(12)
+    D, p = rng.uniform(0.5, 2.0, qp.m2), rng.standard_normal(qp.m2)
+    q1, q0 = s.kf_apply(D, p), s0.kf_apply(D, p)
+    assert np.linalg.norm(q1 - q0) <= 1e-11 * np.linalg.norm(q0)
