@@ -27,7 +27,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from . import kkt
+from . import kkt, xspace
 from .fsolve import make_fsolver
 from .pcg import pcg
 
@@ -50,12 +50,15 @@ class IpmResult:
 def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 1e-8,
               max_ipm: int = 100, sigma: float = 0.1, tau: float = 0.995,
               pcg_maxit: Optional[int] = None, fs=None, x_perm=None, record: bool = False,
-              exact_ph: bool = False, direct: bool = False, forcing: bool = True) -> IpmResult:
+              exact_ph: bool = False, direct: bool = False, forcing: bool = True,
+              space: str = "nu") -> IpmResult:
     """Run the single-factorization inexact IPM.
 
     precond ∈ {"none" (U-KF), "low" (PL-KF), "high" (PH-KF)}.
     ``direct=True`` replaces PCG by a dense solve of K_F (trajectory reference).
     ``record=True`` stores (D_k, r_ν, Δν, PCG iterations) per IPM iteration.
+    ``space="x"``: the x-space twin — projected CG on the augmented system K_C with the constraint
+    preconditioner [H Aᵀ; A 0] = the F factor (oracle.xspace; `precond` is then ignored).
     """
     n, m1, m2 = qp.n, qp.m1, qp.m2
     t0 = time.perf_counter()
@@ -90,6 +93,16 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
         if k == max_ipm:
             break
         D = kkt.diag_D(s, nu)
+        if space == "x":
+            eps = min(pcg_tol, res["mu"]) if forcing else pcg_tol
+            f, e, W = xspace.x_rhs(qp, res, D)
+            dx, dlam, it, _, _, _ = xspace.ppcg(qp, fs, W, f, e, eps, pcg_maxit)
+            dnu, ds = xspace.newton_from_x(qp, res, D, nu, dx)
+            alpha, amax = kkt.step_length(s, ds, nu, dnu, tau)
+            trace.append(dict(k=k, mu=res["mu"], rg=rg_inf, re=re_inf, ri=ri_inf, pcg=it, alpha=alpha, eps=eps))
+            iters.append(it)
+            x, lam, nu, s = x + alpha * dx, lam + alpha * dlam, nu + alpha * dnu, s + alpha * ds
+            continue
         rnu = kkt.r_nu(qp, fs, res)
         if direct:
             KF = np.column_stack([kkt.KF_apply(qp, fs, D, e) for e in np.eye(m2)])
