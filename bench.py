@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=6, help="oracle PCG iterations per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--space", default="nu", choices=["nu", "x"],
+                    help="nu: PCG on K_F (the paper's PL-KF, default); x: the x-space twin (projected CG on K_C)")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
                     help="N > 1: independent replicas (weak) or one IPM with sharded rows (strong)")
     ap.add_argument("--profile-traffic", default=os.path.join(ROOT, "profiles", "traffic.json"))
@@ -253,7 +255,7 @@ def run_ours(args, rank, world, local, use_dist):
 
     # ---------------------------------------------------------------- device-resident value run
     # (no profiling events inside the timed region: they add ~40 µs per PCG iteration)
-    s.ipm_init()
+    s.ipm_init(space=args.space)
     s.ipm_iterate(W)
     torch.cuda.synchronize(dev)
     clocks = Clocks(local)
@@ -276,7 +278,7 @@ def run_ours(args, rank, world, local, use_dist):
 
     # ---------------------------------------------------------------- kernel durations (same steps, replayed
     # with CUDA events around every launch on the library stream) for the roofline
-    s.ipm_init()
+    s.ipm_init(space=args.space)
     s.ipm_iterate(W)
     s.profile(True)
     s.profile_read()
@@ -293,7 +295,7 @@ def run_ours(args, rank, world, local, use_dist):
 
     # ---------------------------------------------------------------- e2e replay through the C ABI
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.space == "nu":
         systems = []
         s.ipm_init()
         for k in range(W + K):
@@ -342,7 +344,9 @@ def run_ours(args, rank, world, local, use_dist):
     bwd_ms, bwd_n = prof["f_bwd"]
     root_ms, root_n = prof["f_root"]
     n_ipm_timed = max(0, min(K, r_prof["n_ipm"] - W))
-    real_solves = pcg_prof + 2 * n_ipm_timed          # K_F products + r_ν and recovery F-solves (profiled pass)
+    # F-solves in the profiled pass: ν-space — one per K_F product + r_ν and recovery per IPM step;
+    # x-space — one projection per PCG iteration + the first projection and the particular solution
+    real_solves = pcg_prof + 2 * n_ipm_timed
     solve_ms = fwd_ms + root_ms + bwd_ms
     ss = s.structure("sn_start")
     w_root = int(ss[-1] - ss[-2]) if st["sym_enabled"] else 0
@@ -388,9 +392,13 @@ def run_ours(args, rank, world, local, use_dist):
         "ms_per_step": ms_max / max(1, steps_done), "higher_is_better": True,
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} PL-KF: one IPM iteration per step (residuals, r_nu F-solve, "
-                               f"PCG to eps_k, recovery, step)" if args.precond == "low" else
-                   f"{args.config} {args.precond.upper()}-KF IPM iteration per step",
+        "config": {"workload": (f"{args.config} x-space twin: one IPM iteration per step (residuals, K_C rhs, "
+                                f"projected CG with the F factor as constraint preconditioner, step)"
+                                if args.space == "x" else
+                                f"{args.config} PL-KF: one IPM iteration per step (residuals, r_nu F-solve, "
+                                f"PCG to eps_k, recovery, step)" if args.precond == "low" else
+                                f"{args.config} {args.precond.upper()}-KF IPM iteration per step"),
+                   "space": args.space,
                    "n": qp.n, "m1": qp.m1, "m2": qp.m2, "nnz_LF": st["nnz_LF"], "precond": args.precond,
                    "ipm_steps_timed": steps_done, "pcg_iters_timed": pcg_timed,
                    "l2": "no flush: the factor read every sweep (%.2f GB) exceeds L2" % (st["factor_bytes"] / 1e9),

@@ -131,6 +131,20 @@ int ipm_factor_once(qp_ctx* ctx, const double* D0, qp_precond p);
 int pcg_solve(qp_ctx* ctx, const double* D_k, const double* rhs, double tol, int32_t maxit,
               double* dnu_out, int32_t* iters, double* relres);
 
+/* x-space twin of PL-KF: solve the augmented system K_C
+ *
+ *     G Δx − Aᵀ Δλ = f,   A Δx = e,   G = H + Cᵀ D_k⁻¹ C,
+ *
+ * by projected CG (Gould–Hribar–Nocedal, the paper's ref. gould2001solution, with the residual
+ * update) with the constraint preconditioner [H Aᵀ; A 0] applied through the F factor
+ * of ipm_factor_once — one F-solve per iteration — and the operator G p = H p + Cᵀ(D_k⁻¹∘(C p))
+ * applied matrix-free in one fused kernel.  Stops when √(rᵀg) ≤ tol·√(r₀ᵀg₀) (g the projected
+ * residual) or after maxit products (QP_MAXIT).  D_k: m2 values (> 0); f, dx_out: n values in the
+ * caller's x order; e, dlam_out: m1 values.  Host or device pointers per vectors_on_device.
+ * QP_EINVAL in sharded mode.  iters / relres may be NULL. */
+int pcg_solve_x(qp_ctx* ctx, const double* D_k, const double* f, const double* e, double tol, int32_t maxit,
+                double* dx_out, double* dlam_out, int32_t* iters, double* relres);
+
 typedef struct {
   double ipm_tol;      /* 1e-8 */
   double pcg_tol;      /* ε = 1e-3 */
@@ -139,6 +153,9 @@ typedef struct {
   int32_t max_ipm;     /* 100 */
   int32_t pcg_maxit;   /* 2000 */
   int32_t pcg_forcing; /* 1: ε_k = min(ε, μ_k) (reading R4); 0: fixed ε */
+  int32_t space;       /* 0: ν-space K_F with the chosen preconditioner (default); 1: the x-space
+                          twin — projected CG on the augmented system K_C (pcg_solve_x); not with
+                          sharded rows */
 } qp_ipm_opts;
 
 typedef struct {

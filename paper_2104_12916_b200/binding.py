@@ -52,7 +52,7 @@ class _SetupOpts(C.Structure):
 class _IpmOpts(C.Structure):
     _fields_ = [("ipm_tol", C.c_double), ("pcg_tol", C.c_double), ("sigma", C.c_double),
                 ("tau", C.c_double), ("max_ipm", C.c_int32), ("pcg_maxit", C.c_int32),
-                ("pcg_forcing", C.c_int32)]
+                ("pcg_forcing", C.c_int32), ("space", C.c_int32)]
 
 
 class _IpmResult(C.Structure):
@@ -98,6 +98,7 @@ def load_library(build: bool = True):
                              C.POINTER(_SetupOpts)]
     lib.ipm_factor_once.argtypes = [vp, vp, C.c_int]
     lib.pcg_solve.argtypes = [vp, vp, vp, dbl, i32, vp, C.POINTER(i32), C.POINTER(dbl)]
+    lib.pcg_solve_x.argtypes = [vp, vp, vp, vp, dbl, i32, vp, vp, C.POINTER(i32), C.POINTER(dbl)]
     lib.ipm_solve.argtypes = [vp, C.POINTER(_IpmOpts), C.POINTER(_IpmResult)]
     lib.qp_ipm_init.argtypes = [vp, C.POINTER(_IpmOpts)]
     lib.qp_ipm_iterate.argtypes = [vp, i32, C.POINTER(_IpmResult), C.POINTER(i32)]
@@ -256,8 +257,24 @@ class QPSolver:
         return ko, int(it.value), float(rr.value), rc
 
     def _opts(self, ipm_tol=1e-8, pcg_tol=1e-3, sigma=0.1, tau=0.995, max_ipm=100, pcg_maxit=2000,
-              pcg_forcing=True):
-        return _IpmOpts(ipm_tol, pcg_tol, sigma, tau, max_ipm, pcg_maxit, 1 if pcg_forcing else 0)
+              pcg_forcing=True, space="nu"):
+        return _IpmOpts(ipm_tol, pcg_tol, sigma, tau, max_ipm, pcg_maxit, 1 if pcg_forcing else 0,
+                        {"nu": 0, "x": 1}[space])
+
+    def pcg_solve_x(self, D, f, e, tol=1e-3, maxit=2000):
+        """x-space twin: G Δx − AᵀΔλ = f, AΔx = e, G = H + CᵀD⁻¹C (projected CG).
+        Returns (Δx, Δλ, iters, relres, status)."""
+        pD, kD = self._ptr(D, self.m2)
+        pf, kf = self._ptr(f, self.n)
+        pe, ke = self._ptr(e, self.m1) if self.m1 else (None, None)
+        if self.vectors_on_device:
+            raise NotImplementedError("device vectors: call the C ABI directly")
+        dx, dl = np.zeros(self.n), np.zeros(max(self.m1, 1))
+        it = C.c_int32()
+        rr = C.c_double()
+        rc = self._check(self.lib.pcg_solve_x(self.ctx, pD, pf, pe, float(tol), int(maxit), dx.ctypes.data,
+                                              dl.ctypes.data, C.byref(it), C.byref(rr)), ok=(0, 1))
+        return dx, dl[:self.m1], int(it.value), float(rr.value), rc
 
     def _result(self, with_vectors=True, max_ipm=100):
         r = _IpmResult()

@@ -265,7 +265,12 @@ struct qp_ctx {
   double t_factor_ph = 0;
   int64_t ph_refactors = 0;
   int64_t launches = 0;           // kernel launches issued by this context
-  cudaGraphExec_t pcg_graph[3] = {nullptr, nullptr, nullptr};   // GCH PCG iterations per preconditioner
+  cudaGraphExec_t pcg_graph[4] = {nullptr, nullptr, nullptr, nullptr};   // GCH PCG iterations per
+                                                                           // preconditioner; [3]: x-space
+  int graph_launches[4] = {0, 0, 0, 0};
+  // x-space twin buffers (n in factor order unless noted)
+  double *xs_W = nullptr, *xs_p = nullptr, *xs_q = nullptr, *xs_r = nullptr, *xs_x = nullptr;
+  double *xs_lam = nullptr /*m1*/, *xs_rhs = nullptr /*N, λ part zero*/;
   bool use_graphs = true;
   int graph_launches_per_chunk = 0;
   double last_eps = 0;            // PCG tolerance of the last IPM iteration
@@ -828,14 +833,14 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
       }
     }
     cudaGetLastError();
+    c->graph_launches[prec] = (int)(c->launches - l0);
     c->launches = l0;
-    c->graph_launches_per_chunk = 0;
   }
   int chunk = 2;
   for (int it = 0; it < maxit + 1;) {
     if (graphs && c->pcg_graph[prec] && it >= 2) {
       cudaGraphLaunch(c->pcg_graph[prec], st);
-      c->launches += (prec == 2 ? 11 : 6) * GCH;
+      c->launches += c->graph_launches[prec];
       it += GCH;
     } else {
       for (int k = 0; k < chunk; ++k)
@@ -853,6 +858,97 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   if (iters) *iters = c->h_pst->iter;
   if (relres) *relres = c->h_pst->bnorm2 > 0 ? std::sqrt(c->h_pst->rr / c->h_pst->bnorm2) : 0.0;
   if (c->h_pst->status == -3) return fail(c, QP_EBREAKDOWN, "PCG breakdown (pᵀq <= 0 or non-finite)");
+  return c->h_pst->status == 1 ? QP_MAXIT : QP_OK;
+}
+
+// x-space twin: projected CG on G Δx − AᵀΔλ = f, AΔx = e (oracle/xspace.py), G = H + CᵀD⁻¹C.
+// fe: [f; e] in factor order (N).  Result in c->xs_x (n) and c->xs_lam (m1).
+int pcg_x_dev(qp_ctx* c, const double* D, const double* fe, double tol, int maxit, int* iters, double* relres) {
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n, m1 = c->m1, N = n + m1;
+  const int g = c->vgrid;
+  int h = c->begin(3);
+  recip(c->m2, D, c->xs_W, g, st);
+  c->end(h);
+  // particular solution A x₀ = e: F [x₀; ·] = [0; e]
+  cudaMemsetAsync(c->xs_rhs, 0, N * 8, st);
+  if (m1 > 0) {
+    cudaMemcpyAsync(c->xs_rhs + n, fe + n, m1 * 8, cudaMemcpyDeviceToDevice, st);
+    f_solve_dev(c, c->xs_rhs, c->xbuf);
+    cudaMemcpyAsync(c->xs_x, c->xbuf, n * 8, cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(c->xs_rhs + n, 0, m1 * 8, st);
+  } else {
+    cudaMemsetAsync(c->xs_x, 0, n * 8, st);
+  }
+  // r = G x₀ − f, first projection, ρ₀, p = −g
+  g_apply(c->Hf, c->Cf, c->Ctf, c->xs_W, c->xs_x, c->xs_q, c->partial, c->pst, false, g, st);
+  xp_init_r(n, c->xs_q, fe, c->xs_r, c->xs_rhs, g, st);
+  c->launches += 3;
+  {
+    PcgState ps{};
+    ps.tol2 = tol * tol;
+    ps.maxit = maxit;
+    *c->h_pst = ps;
+    cudaMemcpyAsync(c->pst, c->h_pst, sizeof(PcgState), cudaMemcpyHostToDevice, st);
+  }
+  if (m1 > 0) cudaMemsetAsync(c->xs_lam, 0, m1 * 8, st);
+  f_solve_dev(c, c->xs_rhs, c->xbuf);
+  xp_update2(c->Atf, m1, c->xbuf, c->xs_r, c->xs_lam, c->xs_p, c->partial, c->pst, true, g, st);
+  c->launches += 1;
+  auto body = [&]() {
+    SweepRhs r{};
+    r.rhs = c->xs_rhs;
+    r.done_flag = &c->pst->done;
+    int hh = c->begin(2);
+    g_apply(c->Hf, c->Cf, c->Ctf, c->xs_W, c->xs_p, c->xs_q, c->partial, c->pst, true, g, st);
+    c->end(hh);
+    hh = c->begin(3);
+    xp_update1(n, c->xs_p, c->xs_q, c->xs_x, c->xs_r, c->xs_rhs, c->pst, g, st);
+    c->end(hh);
+    f_solve_sweeps(c, r, c->xbuf);
+    hh = c->begin(3);
+    xp_update2(c->Atf, m1, c->xbuf, c->xs_r, c->xs_lam, c->xs_p, c->partial, c->pst, false, g, st);
+    xp_update3(n, c->xbuf, c->xs_p, c->pst, g, st);
+    c->end(hh);
+    c->launches += 4;
+  };
+  constexpr int GCH = 8;
+  const bool graphs = c->use_graphs && !c->prof;
+  if (graphs && !c->pcg_graph[3]) {
+    int64_t l0 = c->launches;
+    cudaGraph_t gr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      for (int k = 0; k < GCH; ++k) body();
+      if (cudaStreamEndCapture(st, &gr) == cudaSuccess) {
+        if (cudaGraphInstantiate(&c->pcg_graph[3], gr, 0) != cudaSuccess) c->pcg_graph[3] = nullptr;
+        cudaGraphDestroy(gr);
+      }
+    }
+    cudaGetLastError();
+    c->graph_launches[3] = (int)(c->launches - l0);
+    c->launches = l0;
+  }
+  int chunk = 2;
+  for (int it = 0; it < maxit + 1;) {
+    if (graphs && c->pcg_graph[3] && it >= 2) {
+      cudaGraphLaunch(c->pcg_graph[3], st);
+      c->launches += c->graph_launches[3];
+      it += GCH;
+    } else {
+      for (int k = 0; k < chunk; ++k) body();
+      it += chunk;
+    }
+    cudaMemcpyAsync(c->h_pst, c->pst, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
+    int rc = sync_check(c, "pcg_x");
+    if (rc) return rc;
+    if (c->h_pst->done) break;
+    chunk = std::min(chunk * 2, 32);
+  }
+  c->harvest();
+  if (!c->h_pst->done) return fail(c, QP_ECUDA, "projected CG loop ended without completion (internal error)");
+  if (iters) *iters = c->h_pst->iter;
+  if (relres) *relres = c->h_pst->bnorm2 > 0 ? std::sqrt(c->h_pst->rr / c->h_pst->bnorm2) : 0.0;
+  if (c->h_pst->status == -3) return fail(c, QP_EBREAKDOWN, "projected CG breakdown (pᵀGp <= 0 or non-finite)");
   return c->h_pst->status == 1 ? QP_MAXIT : QP_OK;
 }
 
@@ -1000,6 +1096,28 @@ int ipm_iteration(qp_ctx* c, bool* converged) {
     return QP_OK;
   }
   *converged = false;
+  double eps_x = c->opts.pcg_forcing ? std::min(c->opts.pcg_tol, S.mu) : c->opts.pcg_tol;
+  if (c->opts.space == 1) {
+    // x-space twin: [f; e] = [r_g − CᵀD⁻¹r_a; −r_e] → projected CG → Δν = −D⁻¹(r_a + CΔx)
+    c->last_eps = eps_x;
+    h = c->begin(7);
+    x_rhs(c->Ctf, m1, c->rgre, c->ra, c->Dk, c->rhs2, c->vgrid, st);
+    c->end(h);
+    int itx = 0;
+    rc = pcg_x_dev(c, c->Dk, c->rhs2, eps_x, c->opts.pcg_maxit, &itx, nullptr);
+    if (rc != QP_OK && rc != QP_MAXIT) return rc;
+    c->pcg_hist.push_back(itx);
+    h = c->begin(7);
+    cudaMemcpyAsync(c->dxl, c->xs_x, n * 8, cudaMemcpyDeviceToDevice, st);
+    if (m1 > 0) cudaMemcpyAsync(c->dxl + n, c->xs_lam, m1 * 8, cudaMemcpyDeviceToDevice, st);
+    x_dnu(c->Cf, c->ra, c->Dk, c->xs_x, c->px, c->vgrid, st);
+    ipm_ds_alpha(m2, c->rc, c->nu, c->Dk, c->px, c->s, c->ds, c->partial, c->ist, c->vgrid, st);
+    ipm_update(N, m2, c->dxl, c->px, c->ds, c->xl, c->nu, c->s, c->ist, c->vgrid, st);
+    c->end(h);
+    c->launches += 5;
+    c->ipm_k++;
+    return cuda_check(c, "ipm iteration (x-space)");
+  }
   // r_ν = −r_a + [C 0] F⁻¹ (r_g; r_e)
   f_solve_dev(c, c->rgre, c->xbuf);
   h = c->begin(7);
@@ -1300,6 +1418,13 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     c->pst = c->mem.zeros<PcgState>(1, st);
     c->ist = c->mem.zeros<IpmState>(1, st);
     c->ubuf = c->mem.zeros<double>(N, st);
+    c->xs_W = c->mem.zeros<double>(m2, st);
+    c->xs_p = c->mem.zeros<double>(n, st);
+    c->xs_q = c->mem.zeros<double>(n, st);
+    c->xs_r = c->mem.zeros<double>(n, st);
+    c->xs_x = c->mem.zeros<double>(n, st);
+    c->xs_lam = c->mem.zeros<double>(std::max<int64_t>(m1, 1), st);
+    c->xs_rhs = c->mem.zeros<double>(N, st);
     PcgState ps{};
     ps.defer = c->sharded ? 1 : 0;
     cudaMemcpyAsync(c->pst, &ps, sizeof(PcgState), cudaMemcpyHostToDevice, st);
@@ -1521,11 +1646,41 @@ int pcg_solve(qp_ctx* c, const double* D_k, const double* rhs, double tol, int32
   return rc2 ? rc2 : rc;
 }
 
+int pcg_solve_x(qp_ctx* c, const double* D_k, const double* f, const double* e, double tol, int32_t maxit,
+                double* dx_out, double* dlam_out, int32_t* iters, double* relres) {
+  int rc = require(c, true);
+  if (rc) return rc;
+  if (c->sharded) return fail(c, QP_EINVAL, "the x-space twin is not available with sharded rows");
+  if (!D_k || !f || (c->m1 > 0 && !e)) return fail(c, QP_EINVAL, "NULL D_k / f / e");
+  const int64_t n = c->n, m1 = c->m1;
+  const double* Dd = in_vec(c, D_k, c->vin, c->m2);
+  cudaMemcpyAsync(c->Dk, Dd, c->m2 * 8, cudaMemcpyDeviceToDevice, c->stream);
+  const double* fd = in_vec(c, f, c->vin2, n);
+  gather(c->rhs2, fd, c->perm_dev, n, nullptr, c->stream);    // f into factor order
+  if (m1 > 0) {
+    const double* ed = in_vec(c, e, c->vin, m1);              // D_k already copied out of vin
+    cudaMemcpyAsync(c->rhs2 + n, ed, m1 * 8, cudaMemcpyDeviceToDevice, c->stream);
+  }
+  int it = 0;
+  double rr = 0;
+  rc = pcg_x_dev(c, c->Dk, c->rhs2, tol, maxit, &it, &rr);
+  if (iters) *iters = it;
+  if (relres) *relres = rr;
+  if (rc != QP_OK && rc != QP_MAXIT) return rc;
+  scatter(c->vout, c->xs_x, c->perm_dev, n, nullptr, c->stream);
+  out_vec(c, dx_out, c->vout, n);
+  if (m1 > 0) out_vec(c, dlam_out, c->xs_lam, m1);
+  int rc2 = sync_check(c, "pcg_solve_x");
+  return rc2 ? rc2 : rc;
+}
+
 int qp_ipm_init(qp_ctx* c, const qp_ipm_opts* o) {
   int rc = require(c, true);
   if (rc) return rc;
-  qp_ipm_opts d{1e-8, 1e-3, 0.1, 0.995, 100, 2000, 1};
+  qp_ipm_opts d{1e-8, 1e-3, 0.1, 0.995, 100, 2000, 1, 0};
   c->opts = o ? *o : d;
+  if (c->opts.space != 0 && c->opts.space != 1) return fail(c, QP_EINVAL, "qp_ipm_opts.space must be 0 or 1");
+  if (c->opts.space == 1 && c->sharded) return fail(c, QP_EINVAL, "the x-space twin is not available with sharded rows");
   if (c->opts.max_ipm <= 0) c->opts.max_ipm = 100;
   if (c->opts.pcg_maxit <= 0) c->opts.pcg_maxit = 2000;
   const int64_t n = c->n, m1 = c->m1, m2 = c->m2;

@@ -1794,6 +1794,163 @@ void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const
   k_scatter<<<grid, NT, 0, s>>>(out, in, idx, n, done);
 }
 
+
+// ------------------------------------------------------------------------- x-space twin (K_C, PPCG)
+// q = G p = H p + Cᵀ(W∘(C p)) in ONE kernel (the north_star's fused SpMV chain): warp per x-row i,
+// lanes over H's row, then over Cᵀ's row where each lane forms its (C p)_k on the fly (C rows are
+// short; the redundancy is nnz(C)·(column count of C) FMAs, all from L2).  Fused pᵀq reduction;
+// pcg_mode: the last block sets α = ρ / pᵀq (fin_pcg_pq).
+__global__ void __launch_bounds__(NT) k_g_apply(DevCSR Hf, DevCSR Cf, DevCSR Ctf, const double* W, const double* p,
+                                                double* q, double* partial, PcgState* st, int pcg_mode) {
+  __shared__ double sh[32];
+  if (pcg_mode && *((volatile int*)&st->done)) return;
+  const int lane = threadIdx.x & 31;
+  double loc = 0.0;
+  const int64_t nw = ((int64_t)gridDim.x * NT) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 5; i < Hf.nrows; i += nw) {
+    double s = 0.0;
+    for (int64_t e = Hf.p[i] + lane; e < Hf.p[i + 1]; e += 32) s += Hf.v[e] * __ldg(p + Hf.i[e]);
+    for (int64_t e = Ctf.p[i] + lane; e < Ctf.p[i + 1]; e += 32) {
+      const int32_t k = Ctf.i[e];
+      s += Ctf.v[e] * W[k] * csr_dot(Cf, k, p);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      q[i] = s;
+      loc += p[i] * s;
+    }
+  }
+  if (!pcg_mode) return;
+  const double v = block_reduce<0>(loc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  if (is_last_block(&st->arrive)) {
+    const double pq = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      fin_pcg_pq(st, pq);
+      st->arrive = 0;
+    }
+  }
+}
+
+// x += αp; r += αq; rhs[0, n) = −r (the projection's right-hand side; rhs[n, N) stays 0)
+__global__ void k_xp_update1(int64_t n, const double* p, const double* q, double* x, double* r, double* rhs,
+                             const PcgState* st) {
+  if (*((volatile const int*)&st->done)) return;
+  const double a = st->alpha;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+    x[i] += a * p[i];
+    const double ri = r[i] + a * q[i];
+    r[i] = ri;
+    rhs[i] = -ri;
+  }
+}
+
+// After the projection F [g; v] = [−r; 0] (so H g + Aᵀw = r with w = −v): r −= Aᵀw, λ += w, ρ' = rᵀg;
+// the last block applies the PCG decision of fin_pcg_upd1 with ‖·‖ = √(rᵀg) (stop: √(ρ'/ρ₀) ≤ ε).
+// init = 1: the first projection — ρ₀ = rᵀg, p = −g, iteration counter reset (fin_pcg_init).
+__global__ void __launch_bounds__(NT) k_xp_update2(DevCSR Atf, int64_t m1, const double* sol, double* r, double* lam,
+                                                   double* p, double* partial, PcgState* st, int init) {
+  __shared__ double sh[32];
+  if (!init && *((volatile int*)&st->done)) return;
+  const int64_t n = Atf.nrows;
+  const double* g = sol;
+  const double* v = sol + n;
+  double rg = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < n + m1; t += (int64_t)gridDim.x * NT) {
+    if (t < n) {
+      const double ri = r[t] + csr_dot(Atf, t, v);   // r − Aᵀw, w = −v
+      r[t] = ri;
+      rg += ri * g[t];
+      if (init) p[t] = -g[t];
+    } else {
+      lam[t - n] -= v[t - n];                        // λ += w
+    }
+  }
+  const double s = block_reduce<0>(rg, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  if (is_last_block(&st->arrive)) {
+    const double t = reduce_partials<0>(partial, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      if (init) {
+        st->iter = 0;
+        st->status = 0;
+        fin_pcg_init(st, fabs(t), t);
+        if (!(t > 0.0)) st->done = 1;
+      } else {
+        fin_pcg_upd1(st, fabs(t), t, 0);
+      }
+      st->arrive = 0;
+    }
+  }
+}
+
+// p = −g + βp
+__global__ void k_xp_update3(int64_t n, const double* g, double* p, const PcgState* st) {
+  if (*((volatile const int*)&st->done)) return;
+  const double b = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) p[i] = -g[i] + b * p[i];
+}
+
+// r = q − f;  rhs[0, n) = −r
+__global__ void k_xp_init_r(int64_t n, const double* q, const double* f, double* r, double* rhs) {
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+    const double ri = q[i] - f[i];
+    r[i] = ri;
+    rhs[i] = -ri;
+  }
+}
+
+// IPM x-space right-hand side: f = r_g − CᵀW r_a (factor order, n), e = −r_e (m1) → rhs_f = [f; e]
+__global__ void k_x_rhs(DevCSR Ctf, int64_t m1, const double* rg_re, const double* ra, const double* D, double* fe) {
+  const int64_t n = Ctf.nrows;
+  for (int64_t t = blockIdx.x * (int64_t)NT + threadIdx.x; t < n + m1; t += (int64_t)gridDim.x * NT) {
+    if (t < n) {
+      double s = 0.0;
+      for (int64_t e = Ctf.p[t]; e < Ctf.p[t + 1]; ++e) s += Ctf.v[e] * ra[Ctf.i[e]] / D[Ctf.i[e]];
+      fe[t] = rg_re[t] - s;
+    } else {
+      fe[t] = -rg_re[t];
+    }
+  }
+}
+
+// Δν = −D⁻¹(r_a + CΔx)
+__global__ void k_x_dnu(DevCSR Cf, const double* ra, const double* D, const double* dx, double* dnu) {
+  for (int64_t k = blockIdx.x * (int64_t)NT + threadIdx.x; k < Cf.nrows; k += (int64_t)gridDim.x * NT)
+    dnu[k] = -(ra[k] + csr_dot(Cf, k, dx)) / D[k];
+}
+__global__ void k_recip(int64_t m, const double* D, double* W) {
+  for (int64_t k = blockIdx.x * (int64_t)NT + threadIdx.x; k < m; k += (int64_t)gridDim.x * NT) W[k] = 1.0 / D[k];
+}
+
+void g_apply(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* W, const double* p, double* q,
+             double* partial, PcgState* st, bool pcg_mode, int grid, cudaStream_t s) {
+  k_g_apply<<<grid, NT, 0, s>>>(Hf, Cf, Ctf, W, p, q, partial, st, pcg_mode ? 1 : 0);
+}
+void xp_update1(int64_t n, const double* p, const double* q, double* x, double* r, double* rhs, const PcgState* st,
+                int grid, cudaStream_t s) {
+  k_xp_update1<<<grid, NT, 0, s>>>(n, p, q, x, r, rhs, st);
+}
+void xp_update2(const DevCSR& Atf, int64_t m1, const double* sol, double* r, double* lam, double* p, double* partial,
+                PcgState* st, bool init, int grid, cudaStream_t s) {
+  k_xp_update2<<<grid, NT, 0, s>>>(Atf, m1, sol, r, lam, p, partial, st, init ? 1 : 0);
+}
+void xp_update3(int64_t n, const double* g, double* p, const PcgState* st, int grid, cudaStream_t s) {
+  k_xp_update3<<<grid, NT, 0, s>>>(n, g, p, st);
+}
+void xp_init_r(int64_t n, const double* q, const double* f, double* r, double* rhs, int grid, cudaStream_t s) {
+  k_xp_init_r<<<grid, NT, 0, s>>>(n, q, f, r, rhs);
+}
+void x_rhs(const DevCSR& Ctf, int64_t m1, const double* rg_re, const double* ra, const double* D, double* fe,
+           int grid, cudaStream_t s) {
+  k_x_rhs<<<grid, NT, 0, s>>>(Ctf, m1, rg_re, ra, D, fe);
+}
+void x_dnu(const DevCSR& Cf, const double* ra, const double* D, const double* dx, double* dnu, int grid,
+           cudaStream_t s) {
+  k_x_dnu<<<grid, NT, 0, s>>>(Cf, ra, D, dx, dnu);
+}
+void recip(int64_t m, const double* D, double* W, int grid, cudaStream_t s) { k_recip<<<grid, NT, 0, s>>>(m, D, W); }
+
 // ------------------------------------------------------------------------- IPM kernels
 __global__ void __launch_bounds__(NT) k_ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial,
                                                IpmState* st) {

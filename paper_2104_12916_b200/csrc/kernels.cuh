@@ -222,6 +222,22 @@ void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid,
 void gather(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
 void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
 
+// ---- x-space twin (augmented system K_C, projected CG with the F factor as constraint
+//      preconditioner).  Vectors of length n in factor order; W = D⁻¹.
+void g_apply(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* W, const double* p, double* q,
+             double* partial, PcgState* st, bool pcg_mode, int grid, cudaStream_t s);
+void xp_update1(int64_t n, const double* p, const double* q, double* x, double* r, double* rhs, const PcgState* st,
+                int grid, cudaStream_t s);
+void xp_update2(const DevCSR& Atf, int64_t m1, const double* sol, double* r, double* lam, double* p, double* partial,
+                PcgState* st, bool init, int grid, cudaStream_t s);
+void xp_update3(int64_t n, const double* g, double* p, const PcgState* st, int grid, cudaStream_t s);
+void xp_init_r(int64_t n, const double* q, const double* f, double* r, double* rhs, int grid, cudaStream_t s);
+void x_rhs(const DevCSR& Ctf, int64_t m1, const double* rg_re, const double* ra, const double* D, double* fe,
+           int grid, cudaStream_t s);
+void x_dnu(const DevCSR& Cf, const double* ra, const double* D, const double* dx, double* dnu, int grid,
+           cudaStream_t s);
+void recip(int64_t m, const double* D, double* W, int grid, cudaStream_t s);
+
 // ---- IPM kernels (a9–a11)
 void ipm_mu(int64_t m2, const double* s_, const double* nu, double* partial, IpmState* st, int grid,
             cudaStream_t s);

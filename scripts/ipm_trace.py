@@ -6,10 +6,11 @@ from paper_2104_12916_b200.binding import from_qp
 name, prec = sys.argv[1], sys.argv[2]
 maxit = int(sys.argv[3]) if len(sys.argv) > 3 else 2000
 n_it = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+space = sys.argv[5] if len(sys.argv) > 5 else "nu"
 qp = qpgen.make(name)
 s = from_qp(qp)
 s.ipm_factor_once(prec)
-s.ipm_init(ipm_tol=1e-8, max_ipm=100, pcg_maxit=maxit)
+s.ipm_init(ipm_tol=1e-8, max_ipm=100, pcg_maxit=maxit, space=space)
 for k in range(n_it):
     r = s.ipm_iterate(1)
     D, rnu, eps = s.ipm_last_system()
