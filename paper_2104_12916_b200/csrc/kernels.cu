@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT) k_mf_panel(DevFactor F, int k, int64_t act
 // consecutive rows of a column; columns likewise from ty) so
 // the fragments are conflict-free 128-bit shared loads (4 per 16 DFMA), the ≤ 64 pivot columns staged
 // by cp.async in double-buffered chunks of 16 (≈ 80 registers: 3 CTAs per SM overlap their epilogues),
-// D_k applied to the column operand in registers.
+// D_k applied to the column operand once per landed chunk in shared memory.
 __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t act_off, int n_act,
                                                   int64_t pref_off) {
   constexpr int KC = 16, LD = 64 + 4;
@@ -324,18 +324,27 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int64_t ac
   for (int k0 = 0; k0 < wk; k0 += KC) {
     cp_async_wait_all();
     __syncthreads();
+    {   // B ← B·D_k on the landed chunk (4 DMUL per thread per chunk instead of 4 per k-step)
+      double* bw = Bs[buf];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = tid + NT * u;
+        const int r = idx & 63, c = idx >> 6;
+        bw[c * LD + r] *= (k0 + c < wk) ? Dk[k0 + c] : 0.0;
+      }
+    }
+    __syncthreads();
     if (k0 + KC < wk) load(buf ^ 1, k0 + KC);
     const double* as = As[buf];
     const double* bs = Bs[buf];
 #pragma unroll 8
     for (int kk = 0; kk < KC; ++kk) {
-      const double d = (k0 + kk < wk) ? Dk[k0 + kk] : 0.0;
       const double2 a0 = *reinterpret_cast<const double2*>(as + kk * LD + tx * 2);
       const double2 a1 = *reinterpret_cast<const double2*>(as + kk * LD + 32 + tx * 2);
       const double2 b0 = *reinterpret_cast<const double2*>(bs + kk * LD + ty * 2);
       const double2 b1 = *reinterpret_cast<const double2*>(bs + kk * LD + 32 + ty * 2);
       const double av[4] = {a0.x, a0.y, a1.x, a1.y};
-      const double bv[4] = {b0.x * d, b0.y * d, b1.x * d, b1.y * d};
+      const double bv[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
