@@ -1391,12 +1391,16 @@ __global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_fl
         const int64_t e0 = F.fl_mr_ptr[r], e1 = F.fl_mr_ptr[r + 1];
         double s = 0.0;
         int64_t e = e0 + lane;
-        for (; e + 96 < e1; e += 128) {
-          const double v0 = __ldg(F.fl_mr_val + e), v1 = __ldg(F.fl_mr_val + e + 32);
-          const double v2 = __ldg(F.fl_mr_val + e + 64), v3 = __ldg(F.fl_mr_val + e + 96);
-          const int c0 = __ldg(F.fl_mr_col + e), c1 = __ldg(F.fl_mr_col + e + 32);
-          const int c2 = __ldg(F.fl_mr_col + e + 64), c3 = __ldg(F.fl_mr_col + e + 96);
-          s += v0 * F.acc[c0] + v1 * F.acc[c1] + v2 * F.acc[c2] + v3 * F.acc[c3];
+        for (; e + 224 < e1; e += 256) {   // 8 entries per lane in flight
+          double v[8];
+          int cc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            v[u] = __ldg(F.fl_mr_val + e + 32 * u);
+            cc[u] = __ldg(F.fl_mr_col + e + 32 * u);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += v[u] * F.acc[cc[u]];
         }
         for (; e < e1; e += 32) s += __ldg(F.fl_mr_val + e) * F.acc[__ldg(F.fl_mr_col + e)];
         s = warp_sum(s);
@@ -1437,7 +1441,7 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
       for (int c = wid; c < w; c += NT / 32) {
         const double* Mc = Mj + (int64_t)c * nr;
         double s = 0.0;
-#pragma unroll 4
+#pragma unroll 8
         for (int q = lane; q < nq; q += 32) s += __ldg(Mc + q) * xr[q];
         s = warp_sum(s);
         if (lane == 0) atomicAdd(x + c0 + c, -s);
