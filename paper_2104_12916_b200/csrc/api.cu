@@ -670,7 +670,7 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
     mf_extend_add(F.d, S.level_ea[L].grp_off, S.level_ea[L].n_grp, st);
     while (si < S.steps.size() && S.steps[si].level == L) {
       const StepDesc& sd = S.steps[si];
-      mf_step(F.d, sd.k, sd.act_off, sd.n_act, S.pref_off[si], sd.pan_total, sd.upd_total, st);
+      mf_step(F.d, sd.k, sd.kind, sd.act_off, sd.n_act, S.pref_off[si], sd.pan_total, sd.upd_total, st);
       ++si;
     }
   }

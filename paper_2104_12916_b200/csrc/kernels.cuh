@@ -161,7 +161,8 @@ void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid
 void mf_assemble_level(const DevFactor& F, int64_t fr_off, int64_t n_fr, int64_t zero_total, int64_t asm_off,
                        int64_t n_asm, const double* src_vals, const double* D, const int64_t* perm, cudaStream_t s);
 void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s);
-void mf_step(const DevFactor& F, int k, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
+// kind: see StepDesc (0 DIAG+PANEL, 1–3 UPDATE modes)
+void mf_step(const DevFactor& F, int k, int kind, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
              int64_t upd_total, cudaStream_t s);
 
 // ---- partitioned inverse X_J = L_JJ⁻¹ of big supernodes (factor time)

@@ -656,10 +656,16 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
       int64_t w = S.sn_start[J + 1] - S.sn_start[J];
       max_nk = std::max(max_nk, (w + BW - 1) / BW);
     }
-    for (int64_t k = 0; k < max_nk; ++k) {
+    // Steps.  Pairs of pivot blocks (k, k+1): DIAG+PANEL(k); fronts ending at block k: UPDATE(k) on
+    // their trailing triangle; the others: UPDATE(k) on block column k+1 only, DIAG+PANEL(k+1), then
+    // one UPDATE with both blocks (128 pivot columns) on the triangle from k+2 — the trailing matrix
+    // is read and written once per two blocks.  QPB_PAIR=0: one block per step.
+    const bool pair = !(std::getenv("QPB_PAIR") && std::getenv("QPB_PAIR")[0] == '0');
+    auto add_step = [&](int64_t k, int kind, auto select) {
       StepDesc sd;
       sd.level = (int)L;
       sd.k = (int)k;
+      sd.kind = kind;
       sd.act_off = (int64_t)S.act.size();
       S.pref_off.push_back((int64_t)S.pan_pref.size());
       S.pan_pref.push_back(0);
@@ -669,18 +675,45 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
         const int64_t w = S.sn_start[J + 1] - S.sn_start[J];
         const int64_t m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
         const int64_t nk = (w + BW - 1) / BW;
-        if (nk <= k) continue;
+        if (!select(nk)) continue;
         const int64_t ntile = nk + (m - w + BW - 1) / BW;
-        const int64_t T = ntile - k - 1;
+        int64_t pan = 0, upd = 0;
+        if (kind == 0) {
+          pan = ntile - k - 1;
+        } else if (kind == 1) {
+          const int64_t T = ntile - k - 1;
+          upd = T * (T + 1) / 2;
+        } else if (kind == 2) {
+          upd = ntile - k - 1;
+        } else {
+          const int64_t T = ntile - k - 2;
+          upd = T * (T + 1) / 2;
+        }
         S.act.push_back(J);
-        S.pan_pref.push_back(S.pan_pref.back() + T);
-        S.upd_pref.push_back(S.upd_pref.back() + T * (T + 1) / 2);
+        S.pan_pref.push_back(S.pan_pref.back() + pan);
+        S.upd_pref.push_back(S.upd_pref.back() + upd);
         ++n_act;
       }
       sd.n_act = n_act;
       sd.pan_total = S.pan_pref.back();
       sd.upd_total = S.upd_pref.back();
-      S.steps.push_back(sd);
+      if (n_act > 0) S.steps.push_back(sd);
+      else {
+        S.pref_off.pop_back();
+        S.pan_pref.pop_back();
+        S.upd_pref.pop_back();
+      }
+    };
+    for (int64_t k = 0; k < max_nk; k += pair ? 2 : 1) {
+      add_step(k, 0, [&](int64_t nk) { return nk > k; });
+      if (!pair) {
+        add_step(k, 1, [&](int64_t nk) { return nk > k; });
+        continue;
+      }
+      add_step(k, 1, [&](int64_t nk) { return nk == k + 1; });
+      add_step(k, 2, [&](int64_t nk) { return nk > k + 1; });
+      add_step(k + 1, 0, [&](int64_t nk) { return nk > k + 1; });
+      add_step(k, 3, [&](int64_t nk) { return nk > k + 1; });
     }
   }
   S.pivsign.assign(N, 1);

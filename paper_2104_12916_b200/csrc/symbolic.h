@@ -31,6 +31,8 @@ struct LowerMatrix {
 
 struct StepDesc {
   int level, k;
+  int kind;           // 0 DIAG+PANEL(k); UPDATE with 1: block k on tiles i ≥ j ≥ k+1; 2: block k on the
+                      // column strip j = k+1; 3: blocks k and k+1 on tiles i ≥ j ≥ k+2
   int n_act;          // active fronts
   int64_t act_off;    // offset into act list
   int64_t pan_total;  // PANEL tiles
