@@ -1579,7 +1579,10 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
         }
       }
     }
-    e = analyse(PM, c->FP.S, 0, /*allow_symroot=*/false);   // P_H is refactored at every D: keep L-based sweeps
+    // P_H is refactored at every D: no symmetric root, and supernodes capped at 4096 columns so the
+    // partitioned inverses of its sweeps cost Σ B³/6 per refactor instead of w³/6 (QPB_PH_MAXW)
+    const int64_t ph_maxw = std::getenv("QPB_PH_MAXW") ? std::atoll(std::getenv("QPB_PH_MAXW")) : 4096;
+    e = analyse(PM, c->FP.S, 0, /*allow_symroot=*/false, -1, ph_maxw);
     if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of P_H: " + e);
     e = upload_factor(c, c->FP, c->ws_limit);
     if (!e.empty()) return fail(c, QP_ENOMEM, e);

@@ -883,7 +883,10 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       const int r0 = F.tile_r0[ti];
       const int64_t noff = F.blk_noff[b];
       const int64_t c0 = F.blk_col0[b];
-      load_tile(sm, F.fstore + F.blk_off[b] + r0, Rn, wk, noff);
+      const bool longt = Rn * wk > 4096;   // a long tile of a full-width block: straight from global memory
+      const double* Lt = F.fstore + F.blk_off[b] + r0;
+      if (longt) prefetch_block(Lt, Rn, wk, noff);
+      else load_tile(sm, Lt, Rn, wk, noff);
       if (tid == 0) {
         spin_u32(F.ready_f + b, E);
         if (F.tprof) t1 = gtime();
@@ -892,7 +895,22 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       if (tid < wk) S.y[tid] = __ldcg(x + c0 + tid);
       __syncthreads();
       const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
-      if (Rn <= 64) {
+      if (longt) {
+        // warp w: rows 64w + lane and 64w + 32 + lane; all 64 columns, 8 in flight
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int rb = wid * 64; rb < Rn; rb += NT * 2) {
+          const int ra = rb + lane, rc = rb + 32 + lane;
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < wk; ++c) {
+            const double yc = S.y[c];
+            if (ra < Rn) s0 += __ldg(Lt + ra + (int64_t)c * noff) * yc;
+            if (rc < Rn) s1 += __ldg(Lt + rc + (int64_t)c * noff) * yc;
+          }
+          if (ra < Rn) atomicAdd(F.acc + rows[ra], s0);
+          if (rc < Rn) atomicAdd(F.acc + rows[rc], s1);
+        }
+      } else if (Rn <= 64) {
         tile_gemv(sm, Rn, wk, S.y, S.red);
         if (tid < Rn) atomicAdd(F.acc + rows[tid], S.red[tid]);
       } else {
@@ -1117,18 +1135,37 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       const int r0 = F.tile_r0[ti];
       const int64_t noff = F.blk_noff[b];
       const int64_t c0 = F.blk_col0[b];
-      load_tile(sm, F.fstore + F.blk_off[b] + r0, Rn, wk, noff);
+      const double* Lt = F.fstore + F.blk_off[b] + r0;
+      const bool longt = Rn * wk > 4096;
+      if (longt) prefetch_block(Lt, Rn, wk, noff);
+      else load_tile(sm, Lt, Rn, wk, noff);
       if (tid == 0) {
         spin_u32(F.ready_sb + F.tile_dest[ti], E);
         if (F.tprof) t1 = gtime();
       }
       __syncthreads();
       const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
-      double* xr = sm + wk * (Rn + 1);
-      for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r]);
-      __syncthreads();
-      tile_gemv_t(sm, Rn, wk, xr, S.red);
-      if (tid < wk) atomicAdd(F.tacc + c0 + tid, S.red[tid]);
+      if (longt) {
+        // 64-row sub-tiles through shared memory, column sums accumulated by the first wk threads
+        double colsum = 0.0;
+        for (int s0 = 0; s0 < Rn; s0 += 64) {
+          const int Rs = Rn - s0 < 64 ? Rn - s0 : 64;
+          __syncthreads();
+          load_tile(sm, Lt + s0, Rs, wk, noff);
+          double* xr = sm + wk * (Rs + 1);
+          for (int r = tid; r < Rs; r += NT) xr[r] = __ldcg(x + rows[s0 + r]);
+          __syncthreads();
+          tile_gemv_t(sm, Rs, wk, xr, S.red);
+          if (tid < wk) colsum += S.red[tid];
+        }
+        if (tid < wk) atomicAdd(F.tacc + c0 + tid, colsum);
+      } else {
+        double* xr = sm + wk * (Rn + 1);
+        for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r]);
+        __syncthreads();
+        tile_gemv_t(sm, Rn, wk, xr, S.red);
+        if (tid < wk) atomicAdd(F.tacc + c0 + tid, S.red[tid]);
+      }
       __syncthreads();
       if (tid == 0) {
         __threadfence();

@@ -74,7 +74,8 @@ static inline int64_t tile_begin(int64_t t, int64_t nk, int64_t w, int64_t m) {
   return v < m ? v : m;
 }
 
-std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot, int64_t trailing_from) {
+std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot, int64_t trailing_from,
+                    int64_t max_sn_width) {
   const int64_t N = M.N;
   S.N = N;
   // ---------------------------------------------------------------- row form of the strict lower part
@@ -251,13 +252,22 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
       if (fb_ptr[last + 1] != fb_ptr[last]) return "trailing merge: last supernode has rows below (internal error)";
     }
   }
-  // relaxed partition (alive supernodes, in column order)
+  // relaxed partition (alive supernodes, in column order).  max_sn_width > 0 splits wider supernodes
+  // into a chain of pieces (multiples of BW columns): piece i keeps every later column of the original
+  // supernode as dense rows, so its parent is piece i+1 and the partitioned inverses of the sweeps
+  // are formed per piece (Σ B³/6 instead of w³/6 flops; used for P_H, refactored every IPM iteration).
   S.sn_start.clear();
-  std::vector<int64_t> rep;  // fundamental id that carries each relaxed supernode's below-rows
+  std::vector<int64_t> rep;       // fundamental id that carries each relaxed supernode's below-rows
+  std::vector<int64_t> sn_end;    // end column of the original relaxed supernode of each piece
+  const int64_t cap = max_sn_width > 0 ? std::max<int64_t>(BW, max_sn_width / BW * BW) : 0;
   for (int64_t J = 0; J < nf; ++J)
     if (alive[J]) {
-      S.sn_start.push_back(rc0[J]);
-      rep.push_back(J);
+      const int64_t a = rc0[J], e = rc0[J] + rw[J];
+      for (int64_t c = a; c < e; c += (cap > 0 ? cap : e - a)) {
+        S.sn_start.push_back(c);
+        rep.push_back(J);
+        sn_end.push_back(e);
+      }
     }
   S.sn_start.push_back(N);
   const int64_t ns = (int64_t)S.sn_start.size() - 1;
@@ -266,6 +276,10 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) col2sn[c] = J;
   S.sn_parent.assign(ns, -1);
   for (int64_t J = 0; J < ns; ++J) {
+    if (S.sn_start[J + 1] < sn_end[J]) {   // a piece: the next piece holds its first below-rows
+      S.sn_parent[J] = J + 1;
+      continue;
+    }
     int64_t p = S.parent[S.sn_start[J + 1] - 1];
     if (p >= 0) S.sn_parent[J] = col2sn[p];
   }
@@ -282,7 +296,7 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   S.sn_rowptr.assign(ns + 1, 0);
   S.sn_rows.clear();
   for (int64_t J = 0; J < ns; ++J) {
-    for (int64_t c = S.sn_start[J]; c < S.sn_start[J + 1]; ++c) S.sn_rows.push_back((int32_t)c);
+    for (int64_t c = S.sn_start[J]; c < sn_end[J]; ++c) S.sn_rows.push_back((int32_t)c);
     const int64_t F0 = rep[J];
     S.sn_rows.insert(S.sn_rows.end(), fb_rows.begin() + fb_ptr[F0], fb_rows.begin() + fb_ptr[F0 + 1]);
     S.sn_rowptr[J + 1] = (int64_t)S.sn_rows.size();
@@ -438,7 +452,9 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
       continue;
     }
     S.blk_dptr[b + 1] = (int64_t)S.blk_dest.size();
-    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(1024, TILE_ELEMS / wk));
+    // tiles fit the sweep's shared-memory staging (TILE_ELEMS); full-width blocks take long tiles of up to
+    // LONG_TILE rows instead, swept straight from global memory (fewer tasks, counters and atomics)
+    const int64_t cap = wk == BW ? LONG_TILE : std::max<int64_t>(1, std::min<int64_t>(1024, TILE_ELEMS / wk));
     // first off-diagonal row below the supernode's own columns
     int64_t r = S.blk_big[b] ? (S.sn_start[J + 1] - (S.blk_col0[b] + wk)) : 0;
     while (r < noff) {

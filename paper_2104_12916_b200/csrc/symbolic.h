@@ -16,6 +16,7 @@ constexpr int TILE_ELEMS = 4096; // max doubles in one trsv tile (32 KiB)
 constexpr int XCH = 8;           // column blocks per X chunk of a big supernode
 constexpr int FUSE_ELEMS = 2048;  // small supernodes with w·noff ≤ this are swept as one task
 constexpr int TASK_SHIFT = 28;   // task = (type << TASK_SHIFT) | index
+constexpr int LONG_TILE = 512;   // rows of a sweep tile of a full-width (BW) block
 
 // Lower-triangular (strict) pattern + values of a symmetric matrix already in
 // factor order, by columns, plus its diagonal.
@@ -163,8 +164,9 @@ std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr,
 // trailing_from ≥ 0: after amalgamation, every supernode reaching column trailing_from or beyond is merged
 // with the last supernode into one dense trailing supernode (requires that block to be closed: the
 // ancestor-closed top of the tree reordered to the end).
+// max_sn_width > 0: supernodes wider than that are split into a chain of pieces (P_H).
 std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool allow_symroot = true,
-                    int64_t trailing_from = -1);
+                    int64_t trailing_from = -1, int64_t max_sn_width = 0);
 
 // Decide and plan the flattened forest for a factor whose last supernode is a symmetric root
 // (sets S.flat; no-op otherwise).  Limits: forest supernodes ≤ BW wide, rc0 ≤ max_cols, and
