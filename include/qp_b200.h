@@ -245,8 +245,8 @@ int qp_profile(qp_ctx* ctx, int32_t enable);
 int qp_profile_read(qp_ctx* ctx, double* ms /*10*/, int64_t* count /*10*/);
 
 /* Debug instrumentation of the L_F sweeps: enable = 1 resets and enables;
- * enable = 0 disables and copies 70 int64 = [fwd, bwd] × [DIAG, TILE, PREP,
- * XCHUNK, SNF, SCHUNK, ROOTB] × [count, wait ns, busy ns, first start ns, last end ns]. */
+ * enable = 0 disables and copies 80 int64 = [fwd, bwd] × [DIAG, TILE, PREP,
+ * XCHUNK, SNF, SCHUNK, ROOTB, SNW] × [count, wait ns, busy ns, first start ns, last end ns]. */
 int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
 
 /* Debug: per-task trace of the sweeps profiled by the last enable/disable pair of

@@ -339,9 +339,9 @@ class QPSolver:
         return buf
 
     def debug_sweep_profile(self, enable):
-        out = np.zeros(70, dtype=np.int64)
+        out = np.zeros(80, dtype=np.int64)
         self._check(self.lib.qp_debug_sweep_profile(self.ctx, 1 if enable else 0, out.ctypes.data))
-        return out.reshape(2, 7, 5)
+        return out.reshape(2, 8, 5)
 
     def debug_sweep_trace(self, sweep, cap=1 << 20):
         out = np.zeros((cap, 6), dtype=np.int64)

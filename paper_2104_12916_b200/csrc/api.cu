@@ -475,6 +475,8 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.sn_nblk = m.upload(S.sn_nblk, st);
     d.blk_dptr = m.upload(S.blk_dptr, st);
     d.blk_dest = m.upload(S.blk_dest, st);
+    d.snw_fwd = m.upload(S.snw_fwd, st);
+    d.snw_bwd = m.upload(S.snw_bwd, st);
     d.flat = 0;
     if (S.flat) {
       d.fl_rc0 = S.fl_rc0;
@@ -556,7 +558,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     F.n_fwd_x = (int64_t)S.fwd_tasks_x.size();
     F.n_bwd_x = (int64_t)S.bwd_tasks_x.size();
     d.ttrace_cap = std::max<int64_t>(std::max(F.n_fwd_sym, F.n_bwd_sym), std::max(F.n_fwd_x, F.n_bwd_x));
-    F.tprof_buf = m.alloc<unsigned long long>(70 + 12 * d.ttrace_cap);
+    F.tprof_buf = m.alloc<unsigned long long>(80 + 12 * d.ttrace_cap);
     F.fs_bytes = S.fs_size * 8;
     F.ws_bytes = S.ws_size * 8;
   } catch (std::bad_alloc&) {
@@ -1883,17 +1885,17 @@ int qp_profile_read(qp_ctx* c, double* ms, int64_t* count) {
 }
 
 // Debug: sweep instrumentation of the F factor. enable=1 resets and turns it on;
-// enable=0 copies [2 sweeps][4 task types][count, wait ns, busy ns, first, last] into out (40 int64).
+// enable=0 copies [2 sweeps][8 task types][count, wait ns, busy ns, first, last] into out (80 int64).
 int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
   if (!c || !c->factored) return QP_ESTATE;
   Factor& F = c->FF;
   if (enable) {
-    std::vector<unsigned long long> init(70 + 12 * F.d.ttrace_cap, 0);
-    for (int i = 0; i < 14; ++i) init[i * 5 + 3] = ~0ull;
+    std::vector<unsigned long long> init(80 + 12 * F.d.ttrace_cap, 0);
+    for (int i = 0; i < 16; ++i) init[i * 5 + 3] = ~0ull;
     cudaMemcpyAsync(F.tprof_buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c->stream);
     F.d.tprof = F.tprof_buf;
   } else {
-    if (out) cudaMemcpyAsync(out, F.tprof_buf, 70 * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (out) cudaMemcpyAsync(out, F.tprof_buf, 80 * 8, cudaMemcpyDeviceToHost, c->stream);
     F.d.tprof = nullptr;
   }
   return sync_check(c, "qp_debug_sweep_profile");
@@ -1907,7 +1909,7 @@ int64_t qp_debug_sweep_trace(qp_ctx* c, int32_t sweep, int64_t* out, int64_t cap
   Factor& F = c->FF;
   const int64_t n = std::min<int64_t>(cap, sweep == 0 ? F.d.n_fwd_tasks : F.d.n_bwd_tasks);
   if (n > 0 && out)
-    cudaMemcpyAsync(out, F.tprof_buf + 70 + sweep * F.d.ttrace_cap * 6, n * 48, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(out, F.tprof_buf + 80 + sweep * F.d.ttrace_cap * 6, n * 48, cudaMemcpyDeviceToHost, c->stream);
   int st = sync_check(c, "qp_debug_sweep_trace");
   return st != QP_OK ? st : n;
 }

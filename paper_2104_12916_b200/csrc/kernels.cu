@@ -469,7 +469,7 @@ __device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int
                                           unsigned long long tb = 0) {
   if (tp == nullptr || threadIdx.x != 0) return;
   if ((int64_t)ticket < cap) {  // per-task trace: [task | smid<<32, t0, t1, ta, tb, t2]
-    unsigned long long* r = tp + 70 + ((int64_t)sweep * cap + ticket) * 6;
+    unsigned long long* r = tp + 80 + ((int64_t)sweep * cap + ticket) * 6;
     r[0] = (unsigned long long)(unsigned)task | ((unsigned long long)smid() << 32);
     r[1] = t0;
     r[2] = t1;
@@ -477,7 +477,7 @@ __device__ __forceinline__ void tprof_add(unsigned long long* tp, int sweep, int
     r[4] = tb;
     r[5] = t2;
   }
-  unsigned long long* q = tp + (sweep * 7 + type) * 5;
+  unsigned long long* q = tp + (sweep * 8 + type) * 5;
   atomicAdd(q + 0, 1ull);
   atomicAdd(q + 1, t1 - t0);
   atomicAdd(q + 2, t2 - t1);
@@ -668,6 +668,102 @@ __device__ __forceinline__ void sweep_rhs(const SweepRhs& R, int64_t c0, int wk,
   }
 }
 
+// ---- SNW: one tiny single-block supernode per warp (w ≤ 32, noff ≤ 256, w·noff ≤ 1024)
+// forward: y = L_bb⁻¹ (rhs − acc), acc[rows] += L_rows·y, then release the destination counters.
+__device__ __forceinline__ void snw_forward(const DevFactor& F, const SweepRhs& R, double* x, int b, unsigned E) {
+  const int lane = threadIdx.x & 31;
+  const int J = F.blk_sn[b];
+  const int wk = F.blk_w[b];
+  const int64_t c0 = F.blk_col0[b];
+  const int64_t noff = F.blk_noff[b];
+  const double* L = F.fstore + F.blk_off[b];
+  const double* inv = F.fstore + F.blk_inv[b];
+  const int32_t* rows = F.sn_rows + F.blk_rows[b];
+  // independent of the dependency: pull L_bb⁻¹, the L rows and their indices into L2
+  for (int64_t e = (int64_t)lane * 16; e < (int64_t)wk * wk; e += 32 * 16) prefetch_l2(inv + e);
+  for (int64_t e = (int64_t)lane * 16; e < noff * wk; e += 32 * 16) prefetch_l2(L + e);
+  if (lane * 32 < noff) prefetch_l2(rows + lane * 32);
+  double v = 0.0;
+  if (lane < wk) {
+    const int64_t c = c0 + lane;
+    if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+    else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+  }
+  if (lane == 0) spin_u64(F.cnt_f + J, (unsigned long long)E * (unsigned long long)F.fwd_expect[J]);
+  __syncwarp();
+  if (lane < wk) {
+    double* ap = F.acc + c0 + lane;
+    v -= __ldcg(ap);
+    *ap = 0.0;
+  }
+  double y = 0.0;   // y_i = Σ_{j ≤ i} L⁻¹(i, j) v_j,  L⁻¹(i, j) = inv[j·wk + i]
+#pragma unroll 8
+  for (int j = 0; j < wk; ++j) {
+    const double a = (lane < wk && j <= lane) ? __ldg(inv + j * wk + lane) : 0.0;
+    y += a * __shfl_sync(0xffffffffu, v, j);
+  }
+  if (lane < wk) x[c0 + lane] = y;
+  for (int r0 = 0; r0 < noff; r0 += 32) {
+    const int r = r0 + lane;
+    const bool ok = r < noff;
+    const int32_t row = ok ? __ldg(rows + r) : 0;
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < wk; ++c) {
+      const double l = ok ? __ldg(L + r + (int64_t)c * noff) : 0.0;
+      s += l * __shfl_sync(0xffffffffu, y, c);
+    }
+    if (ok) atomicAdd(F.acc + row, s);
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int64_t k = F.blk_dptr[b]; k < F.blk_dptr[b + 1]; ++k) {
+      __threadfence();
+      red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
+    }
+}
+// backward: t = L_rowsᵀ x_rows, x_b = L_bb⁻ᵀ (D⁻¹ y_b − t), publish the supernode.
+__device__ __forceinline__ void snw_backward(const DevFactor& F, double* x, int b, unsigned E) {
+  const int lane = threadIdx.x & 31;
+  const int J = F.blk_sn[b];
+  const int wk = F.blk_w[b];
+  const int64_t c0 = F.blk_col0[b];
+  const int64_t noff = F.blk_noff[b];
+  const double* L = F.fstore + F.blk_off[b];
+  const double* inv = F.fstore + F.blk_inv[b];
+  const int32_t* rows = F.sn_rows + F.blk_rows[b];
+  for (int64_t e = (int64_t)lane * 16; e < (int64_t)wk * wk; e += 32 * 16) prefetch_l2(inv + e);
+  for (int64_t e = (int64_t)lane * 16; e < noff * wk; e += 32 * 16) prefetch_l2(L + e);
+  const double dinv = lane < wk ? 1.0 / F.Dpiv[c0 + lane] : 0.0;
+  for (int64_t k = F.blk_dptr[b] + lane; k < F.blk_dptr[b + 1]; k += 32) spin_u32(F.ready_sb + F.blk_dest[k], E);
+  __syncwarp();
+  double t = 0.0;   // lane j < wk: t_j = Σ_r L(r, j) x_{rows[r]}
+  for (int r0 = 0; r0 < noff; r0 += 32) {
+    const int r = r0 + lane;
+    const double xr = r < noff ? __ldcg(x + __ldg(rows + r)) : 0.0;
+#pragma unroll 4
+    for (int j = 0; j < wk; ++j) {
+      double p = r < noff ? __ldg(L + r + (int64_t)j * noff) * xr : 0.0;
+      p = warp_sum(p);
+      if (lane == j) t += p;
+    }
+  }
+  double rhs = 0.0;
+  if (lane < wk) rhs = __ldcg(x + c0 + lane) * dinv - t;
+  double xi = 0.0;  // x_i = Σ_{j ≥ i} L⁻¹(j, i) rhs_j,  L⁻¹(j, i) = inv[i·wk + j]
+#pragma unroll 8
+  for (int j = 0; j < wk; ++j) {
+    const double a = (lane < wk && j >= lane) ? __ldg(inv + lane * wk + j) : 0.0;
+    xi += a * __shfl_sync(0xffffffffu, rhs, j);
+  }
+  if (lane < wk) x[c0 + lane] = xi;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    st_rel_u32(F.ready_sb + J, E);
+  }
+}
+
 // Forward sweep L y = b (unit lower L, factor order); y written to x.
 __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double* x) {
   extern __shared__ double sm[];
@@ -823,6 +919,10 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         __threadfence();
         red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
       }
+    } else if (type == 7) {
+      // ---------------- SNW: up to 8 tiny supernodes of one level, one warp each
+      const int bw = F.snw_fwd[idx * 8 + (tid >> 5)];
+      if (bw >= 0) snw_forward(F, R, x, bw, E);
     } else if (type == 5) {
       // ---------------- SCHUNK: symmetric root — x_I += S_IK v_K, x_K += S_IKᵀ v_I (K < I)
       const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
@@ -1086,6 +1186,10 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
         __threadfence();
         st_rel_u32(F.ready_sb + J, E);
       }
+    } else if (type == 7) {
+      // ---------------- SNW backward
+      const int bw = F.snw_bwd[idx * 8 + (tid >> 5)];
+      if (bw >= 0) snw_backward(F, x, bw, E);
     } else if (type == 6) {
       // ---------------- ROOTB: the symmetric root's x = S⁻¹ v was completed by the forward sweep
       const int J = idx;

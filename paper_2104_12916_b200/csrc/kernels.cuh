@@ -60,6 +60,8 @@ struct DevFactor {
   const int64_t* sn_ldx;
   const int64_t* sn_sinv;
   const int32_t* sn_nblk;
+  const int32_t* snw_fwd;         // SNW tasks: 8 block ids each (-1 padded), forward / backward grouping
+  const int32_t* snw_bwd;
   const int64_t* blk_dptr;        // fused small supernodes: destination supernode lists
   const int32_t* blk_dest;
   unsigned int* ready_sb;         // ns: backward — all of supernode J final
@@ -113,7 +115,7 @@ struct DevFactor {
   const int64_t* fl_mr_ptr;       // M by root rows (forward product)
   const int32_t* fl_mr_col;
   double* fl_mr_val;
-  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][7 types][5] + per-task trace
+  unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][8 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
 };

@@ -526,12 +526,50 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     std::stable_sort(bwd_order.begin(), bwd_order.end(),
                      [&](int32_t a, int32_t b) { return depth[a] < depth[b]; });
   }
+  // Tiny single-block supernodes (w ≤ 32, noff ≤ 256, w·noff ≤ 1024) are swept WARP-wide: groups of
+  // up to 8 from the same level (height forward, depth backward) form one task (type 7), one warp each.
+  std::vector<int32_t> tiny_f(ns, -1), tiny_b(ns, -1);   // group id of J, set on every member
+  std::vector<char> first_f(ns, 0), first_b(ns, 0);
+  {
+    auto tiny = [&](int64_t J) {
+      if (S.sn_blk0[J + 1] - S.sn_blk0[J] != 1) return false;
+      const int64_t b = S.sn_blk0[J];
+      const int64_t w = S.blk_w[b], noff = S.blk_noff[b];
+      return fused[b] && w <= 32 && noff <= 256 && w * noff <= 1024 && S.sn_xinv[J] < 0;
+    };
+    auto group = [&](const std::vector<int32_t>& order, const std::vector<int64_t>& key,
+                     std::vector<int32_t>& gid, std::vector<char>& first, std::vector<int32_t>& out) {
+      out.clear();
+      int64_t cur_key = -1, fill = 8;
+      for (int32_t J : order) {
+        if (!tiny(J)) continue;
+        if (key[J] != cur_key || fill == 8) {
+          out.resize(out.size() + 8, -1);
+          cur_key = key[J];
+          fill = 0;
+          first[J] = 1;
+        }
+        const int64_t g = (int64_t)out.size() / 8 - 1;
+        out[g * 8 + fill++] = S.sn_blk0[J];
+        gid[J] = (int32_t)g;
+      }
+    };
+    std::vector<int64_t> height(S.sn_level.begin(), S.sn_level.end()), depth(ns, 0);
+    for (int64_t J = ns - 1; J >= 0; --J)
+      if (S.sn_parent[J] >= 0) depth[J] = depth[S.sn_parent[J]] + 1;
+    group(fwd_order, height, tiny_f, first_f, S.snw_fwd);
+    group(bwd_order, depth, tiny_b, first_b, S.snw_bwd);
+  }
   auto build_queues = [&](bool use_sym, std::vector<int32_t>& fq, std::vector<int32_t>& bq) {
     fq.clear();
     bq.clear();
     for (int32_t J : fwd_order) {
       const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
       const bool sym = use_sym && S.sn_sinv[J] >= 0;
+      if (tiny_f[J] >= 0) {
+        if (first_f[J]) fq.push_back(enc(7, tiny_f[J]));
+        continue;
+      }
       if (S.sn_xinv[J] < 0) {
         for (int64_t b = b0; b < b1; ++b) {
           fq.push_back(enc(fused[b] ? 4 : 0, b));
@@ -548,6 +586,10 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     for (int32_t J : bwd_order) {
       const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
       const bool sym = use_sym && S.sn_sinv[J] >= 0;
+      if (tiny_b[J] >= 0) {
+        if (first_b[J]) bq.push_back(enc(7, tiny_b[J]));
+        continue;
+      }
       if (S.sn_xinv[J] < 0) {
         for (int64_t b = b1 - 1; b >= b0; --b) {
           for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) bq.push_back(enc(1, t));

@@ -84,7 +84,8 @@ struct Symbolic {
   // supernode), 3 XCHUNK(chunk of the inverse diagonal block of a big
   // supernode), 4 SNF(small supernode swept in one task: diagonal + all rows),
   // 5 SCHUNK(chunk of S_J⁻¹ of a symmetric root: x_I += S_IK v_K and x_K += S_IKᵀ v_I),
-  // 6 ROOTB(backward: the symmetric root's x is already final — publish it).
+  // 6 ROOTB(backward: the symmetric root's x is already final — publish it),
+  // 7 SNW(up to 8 tiny single-block supernodes of one level, one warp each).
   std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;   // tile_dest: destination SUPERNODE
   std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect /*per supernode*/, bwd_expect /*per block*/;
   std::vector<int32_t> fwd_tasks_x, bwd_tasks_x;   // same queues with symmetric roots swept through X/Xᵀ (fallback)
@@ -101,6 +102,7 @@ struct Symbolic {
   std::vector<int32_t> sn_nblk;          // blocks per supernode
   std::vector<int64_t> blk_dptr;         // per block: fused destination-supernode list (nb+1)
   std::vector<int32_t> blk_dest;
+  std::vector<int32_t> snw_fwd, snw_bwd; // warp-swept tiny supernodes: 8 block ids per task (type 7), -1 padded
   std::vector<int32_t> blk_big;          // 1 if the block belongs to a big supernode
   int64_t x_size = 0;                    // doubles of all X_J
   int64_t xtmp_size = 0;                 // doubles of the inversion scratch

@@ -17,7 +17,7 @@ D = rng.uniform(0.5, 2, qp.m2); p = rng.standard_normal(qp.m2)
 for rep in range(3):
     s.kf_apply(D, p)
 s.debug_sweep_profile(True); s.kf_apply(D, p); s.debug_sweep_profile(False)
-names = ['DIAG', 'TILE', 'PREP', 'XCHUNK', 'SNF', 'SCHUNK', 'ROOTB']
+names = ['DIAG', 'TILE', 'PREP', 'XCHUNK', 'SNF', 'SCHUNK', 'ROOTB', 'SNW']
 for sw in range(2):
     tr = s.debug_sweep_trace(sw)
     task = tr[:, 0] & 0xffffffff
