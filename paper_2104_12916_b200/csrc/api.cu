@@ -727,8 +727,10 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
   c->launches += 1;
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
-  if (c->sharded) {
-    // u = Σ_ranks C_gᵀ p_g, then the replicated F-solve on [u; 0]
+  static const bool pregather = !(std::getenv("QPB_PREGATHER") && std::getenv("QPB_PREGATHER")[0] == '0');
+  if (c->sharded || (pregather && !c->FF.d.flat)) {
+    // u = Σ_ranks C_gᵀ p_g (one coalesced SpMV before the sweeps: every sweep task then reads its
+    // right-hand side with one load), then the replicated F-solve on [u; 0]
     spmv(c->Ctf, p, c->ubuf, r.done_flag, c->vgrid, c->stream);
     c->launches += 1;
     if (int rc = c->allreduce(c->ubuf, c->n, 0)) return rc;
