@@ -360,12 +360,17 @@ def run_ours(args, rank, world, local, use_dist):
             traffic = json.load(open(args.profile_traffic)).get(args.config, {}).get("dram_bytes_per_fsolve")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "F-solve = k_trsv_fwd + k_symroot_gemv + k_trsv_bwd", "achieved": achieved,
+    flat = bool(st.get("flat_enabled", 0))
+    kname = ("F-solve = k_flat_rhs + k_flat_fwd + k_symroot_gemv + k_flat_bwd" if flat else
+             "F-solve = (C^T p SpMV +) k_trsv_fwd + k_symroot_gemv + k_trsv_bwd")
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_fsolve": fsolve_bytes,
-                "algorithmic_bytes_note": "8*(2*nnz(L_F) outside the symmetric root + w(w+1)/2 of the root's "
-                                          "S^-1, read once per F-solve)",
+                "algorithmic_bytes_note": ("8*(w(w+1)/2 of the root's S^-1 + 2*nnz(M) + 2*nnz(L11^-1)), the flattened "
+                                           "forest M = L21 L11^-1 read forward and backward" if flat else
+                                           "8*(2*nnz(L_F) outside the symmetric root + w(w+1)/2 of the root's "
+                                           "S^-1, read once per F-solve)"),
                 "paper_bytes_per_fsolve": paper_bytes,
                 "paper_formulation_GBps": real_solves * paper_bytes / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0,
                 "fsolve_ms_avg": solve_ms / max(1, real_solves),
