@@ -54,11 +54,12 @@ def main():
               f"{r['dram_pct']:8.1f} {gbs:8.0f} {r['l2_hit_pct']:7.1f} {r['regs']:5.0f} "
               f"{r['achieved_occ_pct']:6.1f} {r['issue_active']:6.2f}")
     if len(sys.argv) > 4:
-        # one F-solve = one forward sweep + (optional) root GEMV + one backward sweep, in launch order
+        # one F-solve = one launch of each F-solve kernel (sweeps or flattened products, root GEMV)
         one, seen = [], set()
         for r in recs:
             k = r["kernel"].split("<")[0].strip()
-            if k in ("k_trsv_fwd", "k_symroot_gemv", "k_trsv_bwd") and k not in seen:
+            if k in ("k_trsv_fwd", "k_symroot_gemv", "k_trsv_bwd", "k_flat_rhs", "k_flat_fwd", "k_flat_bwd") \
+                    and k not in seen:
                 seen.add(k)
                 one.append(r)
         path = sys.argv[4]
