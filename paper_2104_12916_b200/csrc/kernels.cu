@@ -615,14 +615,53 @@ __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_
       a1 = fma(q[u].y, vc, a1);
       t[u] = q[u].x * vi0 + q[u].y * vi1;
     }
+    if constexpr (U == 8) {
+      // transpose-reduce: 8 column partials over 32 lanes in 4+2+1+1+1 shuffles (not 5·8); lane bits
+      // 4,3,2 select the column a lane ends up holding, bits 1,0 finish the sum
+      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+      double a4[4], a2[2];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+      for (int i = 0; i < 4; ++i) {
+        const double recv = __shfl_xor_sync(0xffffffffu, h16 ? t[i] : t[i + 4], 16);
+        a4[i] = (h16 ? t[i + 4] : t[i]) + recv;
+      }
 #pragma unroll
-      for (int u = 0; u < U; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o);
-    if (lane == 0)
+      for (int i = 0; i < 2; ++i) {
+        const double recv = __shfl_xor_sync(0xffffffffu, h8 ? a4[i] : a4[i + 2], 8);
+        a2[i] = (h8 ? a4[i + 2] : a4[i]) + recv;
+      }
+      double a1 = (h4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? a2[0] : a2[1], 4);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      const int col = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+      if ((lane & 3) == 0 && c + 8 * col < ncol_t) colv[c + 8 * col] = a1;
+    } else if constexpr (U == 16) {
+      // the same transpose-reduce for 16 columns: 8+4+2+1 shuffles, bits 4..1 pick the column
+      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
+      double a8[8], a4[4], a2[2];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (c + 8 * u < ncol_t) colv[c + 8 * u] = t[u];
+      for (int i = 0; i < 8; ++i)
+        a8[i] = (h16 ? t[i + 8] : t[i]) + __shfl_xor_sync(0xffffffffu, h16 ? t[i] : t[i + 8], 16);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        a4[i] = (h8 ? a8[i + 4] : a8[i]) + __shfl_xor_sync(0xffffffffu, h8 ? a8[i] : a8[i + 4], 8);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        a2[i] = (h4 ? a4[i + 2] : a4[i]) + __shfl_xor_sync(0xffffffffu, h4 ? a4[i] : a4[i + 2], 4);
+      double a1 = (h2 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, h2 ? a2[0] : a2[1], 2);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      const int col = (h16 ? 8 : 0) + (h8 ? 4 : 0) + (h4 ? 2 : 0) + (h2 ? 1 : 0);
+      if ((lane & 1) == 0 && c + 8 * col < ncol_t) colv[c + 8 * col] = a1;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o);
+      if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c + 8 * u < ncol_t) colv[c + 8 * u] = t[u];
+    }
   }
   for (; c < ncol; c += 8) {
     const double2 q = ok ? __ldg(base + (int64_t)c * ld2) : make_double2(0.0, 0.0);
@@ -1491,7 +1530,7 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
                   cudaStream_t s, const double* sub) {
   if (c_end <= c_begin) return;
-  static int variant = std::getenv("QPB_GEMV_VARIANT") ? std::atoi(std::getenv("QPB_GEMV_VARIANT")) : 1;
+  static int variant = std::getenv("QPB_GEMV_VARIANT") ? std::atoi(std::getenv("QPB_GEMV_VARIANT")) : 3;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   switch (variant) {
