@@ -1596,19 +1596,18 @@ __global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_fl
       if (r < wr) {
         const int64_t e0 = F.fl_mr_ptr[r], e1 = F.fl_mr_ptr[r + 1];
         double s = 0.0;
-        int64_t e = e0 + lane;
-        for (; e + 224 < e1; e += 256) {   // 8 entries per lane in flight
+        for (int64_t e = e0 + lane; e < e1; e += 256) {   // 8 entries per lane in flight (predicated tail)
           double v[8];
           int cc[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            v[u] = __ldg(F.fl_mr_val + e + 32 * u);
-            cc[u] = __ldg(F.fl_mr_col + e + 32 * u);
+            const bool ok = e + 32 * u < e1;
+            v[u] = ok ? __ldg(F.fl_mr_val + e + 32 * u) : 0.0;
+            cc[u] = ok ? __ldg(F.fl_mr_col + e + 32 * u) : 0;
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) s += v[u] * F.acc[cc[u]];
         }
-        for (; e < e1; e += 32) s += __ldg(F.fl_mr_val + e) * F.acc[__ldg(F.fl_mr_col + e)];
         s = warp_sum(s);
         if (lane == 0) F.vbuf[rc0 + r] -= s;
       }
@@ -1647,8 +1646,13 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
       for (int c = wid; c < w; c += NT / 32) {
         const double* Mc = Mj + (int64_t)c * nr;
         double s = 0.0;
-#pragma unroll 8
-        for (int q = lane; q < nq; q += 32) s += __ldg(Mc + q) * xr[q];
+        for (int q0 = lane; q0 < nq; q0 += 256) {   // predicated batches of 8 loads per lane
+          double mv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mv[u] = q0 + 32 * u < nq ? __ldg(Mc + q0 + 32 * u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += q0 + 32 * u < nq ? mv[u] * xr[q0 + 32 * u] : 0.0;
+        }
         s = warp_sum(s);
         if (lane == 0) atomicAdd(x + c0 + c, -s);
       }
