@@ -96,9 +96,23 @@ __device__ double reduce_partials(const double* part, int n, double* sh) {
   }
   return block_reduce<OP>(v, sh);
 }
+// One row of a CSR product, 4 entries per batch so their index, value and gather loads overlap
+// (short rows — C has 4–6 entries per row — then cost one or two dependent load rounds, not six).
 __device__ __forceinline__ double csr_dot(const DevCSR& M, int64_t row, const double* x) {
   double s = 0.0;
-  for (int64_t q = M.p[row]; q < M.p[row + 1]; ++q) s += M.v[q] * __ldg(x + M.i[q]);
+  const int64_t q0 = M.p[row], q1 = M.p[row + 1];
+  for (int64_t q = q0; q < q1; q += 4) {
+    double v[4];
+    int32_t c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = q + u < q1;
+      v[u] = ok ? M.v[q + u] : 0.0;
+      c[u] = ok ? M.i[q + u] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += v[u] * __ldg(x + c[u]);
+  }
   return s;
 }
 // Front tile boundaries: pivot blocks of 64, then the update rows in tiles of 64.
