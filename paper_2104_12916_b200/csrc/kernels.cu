@@ -1303,19 +1303,34 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       __syncthreads();
       const int32_t* rows = F.sn_rows + F.blk_rows[b] + r0;
       if (longt) {
-        // 64-row sub-tiles through shared memory, column sums accumulated by the first wk threads
-        double colsum = 0.0;
-        for (int s0 = 0; s0 < Rn; s0 += 64) {
-          const int Rs = Rn - s0 < 64 ? Rn - s0 : 64;
-          __syncthreads();
-          load_tile(sm, Lt + s0, Rs, wk, noff);
-          double* xr = sm + wk * (Rs + 1);
-          for (int r = tid; r < Rs; r += NT) xr[r] = __ldcg(x + rows[s0 + r]);
-          __syncthreads();
-          tile_gemv_t(sm, Rs, wk, xr, S.red);
-          if (tid < wk) colsum += S.red[tid];
+        // straight from global memory: x of the tile's rows staged once in shared memory, warp w sums
+        // columns 8w..8w+7 over all rows (coalesced along rows, 8 loads in flight per row), then a
+        // transpose-reduce of the 8 column partials across the warp
+        for (int r = tid; r < Rn; r += NT) sm[r] = __ldcg(x + rows[r]);
+        __syncthreads();
+        const int lane = tid & 31, cw = (tid >> 5) * 8;
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = 0.0;
+        for (int r = lane; r < Rn; r += 32) {
+          const double xv = sm[r];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (cw + u < wk) t[u] += __ldg(Lt + r + (int64_t)(cw + u) * noff) * xv;
         }
-        if (tid < wk) atomicAdd(F.tacc + c0 + tid, colsum);
+        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+        double a4[4], a2[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          a4[i] = (h16 ? t[i + 4] : t[i]) + __shfl_xor_sync(0xffffffffu, h16 ? t[i] : t[i + 4], 16);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          a2[i] = (h8 ? a4[i + 2] : a4[i]) + __shfl_xor_sync(0xffffffffu, h8 ? a4[i] : a4[i + 2], 8);
+        double a1 = (h4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? a2[0] : a2[1], 4);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+        const int col = cw + (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+        if ((lane & 3) == 0 && col < wk) atomicAdd(F.tacc + c0 + col, a1);
       } else {
         double* xr = sm + wk * (Rn + 1);
         for (int r = tid; r < Rn; r += NT) xr[r] = __ldcg(x + rows[r]);
