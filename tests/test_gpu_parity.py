@@ -304,3 +304,29 @@ def test_call_order_and_bad_inputs():
     with pytest.raises(QPError) as e:   # PCG breakdown: D = −10 I makes K_F negative definite, pᵀq < 0
         s.pcg_solve(-10.0 * np.ones(qp.m2), np.random.default_rng(1).standard_normal(qp.m2), tol=1e-12, maxit=100)
     assert e.value.code == -3
+
+
+def test_ph_pieces_match_oracle(monkeypatch):
+    """P_H with its supernodes capped at 128 columns (a chain of pieces; the default cap of
+    4096 only bites at c1/c2 size) against the oracle: PCG solutions at fixed counts and at a tight
+    tolerance, and the PH-KF IPM objective."""
+    monkeypatch.setenv("QPB_PH_MAXW", "128")
+    qp = qpgen.scaled_random_qp(500, 120, 700, seed=12)
+    from paper_2104_12916_b200.binding import from_qp
+    s = from_qp(qp)
+    rng = np.random.default_rng(5)
+    D = rng.uniform(0.2, 5.0, qp.m2)
+    s.ipm_factor_once("high", D0=D)
+    assert s.stats()["n_supernodes_PH"] > 1
+    fs = DenseF(qp.H, qp.A)
+    T = kkt.T_matrix(qp)
+    b = rng.standard_normal(qp.m2)
+    for tol, maxit in ((0.0, 3), (1e-12, 2000)):
+        x, it, rr, rc = s.pcg_solve(D, b, tol=tol, maxit=maxit)
+        xr, itr, *_ = oracle_pcg(lambda v: kkt.KF_apply(qp, fs, D, v), b, kkt.PrecondH(qp, D, T=T), tol, maxit)
+        assert abs(it - itr) <= 2
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+    got = s.ipm_solve(ipm_tol=1e-10)
+    ref = oracle_ipm(qp, precond="high", ipm_tol=1e-10)
+    assert got["converged"] and ref.converged
+    assert abs(got["objective"] - ref.objective) <= 1e-8 * max(1.0, abs(ref.objective))
