@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=6, help="oracle PCG iterations per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ipm-solve", action="store_true",
+                    help="skip the full IPM solve timing (BJ metric 'IPM solve time'; c1 PH-KF, rank 0, ~1 min)")
     ap.add_argument("--space", default="nu", choices=["nu", "x"],
                     help="nu: PCG on K_F (the paper's PL-KF, default); x: the x-space twin (projected CG on K_C)")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
@@ -392,6 +394,25 @@ def run_ours(args, rank, world, local, use_dist):
         cpu = {"value": it / dt if dt > 0 else 0.0, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{it} PCG iterations of IPM step 0 on {args.config} (oracle F setup {t_or:.1f} s excluded)"}
 
+    # ---------------------------------------------------------------- IPM solve time (BJ metric, rank 0)
+    # c1 PL-KF does not converge, so the full solve is timed with P_H (PH-KF), the paper's
+    # other preconditioner, from the first P_H numeric factor to the 1e-8 KKT stop.
+    ipm = None
+    if rank == 0 and not args.no_ipm_solve and args.config == "c1" and not sharded:
+        del s
+        torch.cuda.synchronize(dev)
+        sp = from_qp(qp, device=local, stream=stream.cuda_stream)
+        t0 = time.perf_counter()
+        sp.ipm_factor_once("high")
+        t_set = time.perf_counter() - t0
+        r_ph = sp.ipm_solve(ipm_tol=1e-8, with_vectors=False)
+        stp = sp.stats()
+        ipm = {"config": args.config, "precond": "high", "converged": bool(r_ph["converged"]),
+               "n_ipm": r_ph["n_ipm"], "pcg_total": r_ph["pcg_total"], "solve_s": r_ph["t_solve_s"],
+               "setup_s": t_set, "p_h_refactor_s": stp["t_factor_ph_s"], "objective": r_ph["objective"],
+               "note": "full PH-KF IPM solve to the 1e-8 KKT test, setup (orderings, symbolic, factors) separate"}
+        sp.close()
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / max(1, steps_done), "higher_is_better": True,
@@ -410,6 +431,7 @@ def run_ours(args, rank, world, local, use_dist):
                    "parallelism": (f"sharded inequality rows x{world} (NCCL all-reduce, replicated F-solve)"
                                    if sharded else (f"replicas x{world}" if world > 1 else "single GPU"))},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
+        "ipm_solve": ipm,
         "setup_s": {"symbolic": st["t_symbolic_s"], "factor": st["t_factor_s"], "factor_once_total": t_setup},
     }
     if rank == 0:
