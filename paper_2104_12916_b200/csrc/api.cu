@@ -1511,6 +1511,8 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
   }
   // ---- P_H: T = C diag(H)⁻¹ Cᵀ pattern (host) and values (device), symbolic of D + T
   if (p == QP_PREC_HIGH) {
+    const bool verbose = std::getenv("QPB_VERBOSE") != nullptr;
+    double tph0 = now_s();
     HostCSR Ct = transpose(c->C);
     std::vector<int64_t> tp(m2 + 1, 0);
     std::vector<int32_t> ti;
@@ -1534,6 +1536,7 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     std::vector<int64_t> trow(c->nnz_t);
     for (int64_t i = 0; i < m2; ++i)
       for (int64_t q = tp[i]; q < tp[i + 1]; ++q) trow[q] = i;
+    if (verbose) std::fprintf(stderr, "qpb: P_H pattern of T (%lld entries) %.2f s\n", (long long)c->nnz_t, now_s() - tph0);
     // ordering of P_H: minimum degree on the pattern of T
     {
       std::vector<int64_t> ptr(m2 + 1, 0);
@@ -1544,8 +1547,12 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
           if (ti[q] != r) idx.push_back(ti[q]);
         ptr[r + 1] = (int64_t)idx.size();
       }
-      c->perm_ph = etree_postorder(m2, ptr, idx, min_degree_order(m2, ptr, idx));
+      // the tail of P_H's elimination is dense (C diag(H)⁻¹ Cᵀ couples rows through shared columns):
+      // stop the minimum-degree search once the minimum degree reaches half the remaining nodes
+      const double ds = std::getenv("QPB_PH_DENSE_STOP") ? std::atof(std::getenv("QPB_PH_DENSE_STOP")) : 0.5;
+      c->perm_ph = etree_postorder(m2, ptr, idx, min_degree_order(m2, ptr, idx, ds));
     }
+    if (verbose) std::fprintf(stderr, "qpb: P_H ordering %.2f s\n", now_s() - tph0);
     std::vector<int64_t> pinv_ph(m2);
     for (int64_t i = 0; i < m2; ++i) pinv_ph[c->perm_ph[i]] = i;
     LowerMatrix PM;
@@ -1588,6 +1595,7 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     const int64_t ph_maxw = std::getenv("QPB_PH_MAXW") ? std::atoll(std::getenv("QPB_PH_MAXW")) : 4096;
     e = analyse(PM, c->FP.S, 0, /*allow_symroot=*/false, -1, ph_maxw);
     if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of P_H: " + e);
+    if (verbose) std::fprintf(stderr, "qpb: P_H symbolic %.2f s\n", now_s() - tph0);
     e = upload_factor(c, c->FP, c->ws_limit);
     if (!e.empty()) return fail(c, QP_ENOMEM, e);
     plan_inverse(c, c->FP);

@@ -900,7 +900,8 @@ namespace qpb {
 // external degree bound d_i ≤ |A_i| + |L_p \ i| + Σ_{e∈E_i\p} |L_e \ L_p|).
 // A fill-reducing heuristic for the x block of F and for P_H; the paper does
 // not fix an ordering (it used dense SYTRF).  Deterministic.
-std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx) {
+std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
+                                      double dense_stop) {
   std::vector<std::vector<int32_t>> Av(n), Ev(n), Le(n);
   std::vector<int64_t> deg(n);
   for (int64_t i = 0; i < n; ++i) {
@@ -935,9 +936,11 @@ std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr
   for (int64_t k = 0; k < n; ++k) {
     while (mind <= n && head[mind] < 0) ++mind;
     if (mind > n) break;
-    if (mind >= n - k - 1 && n - k > 64) {
+    if (n - k > 64 && (mind >= n - k - 1 || (dense_stop < 1.0 && (double)mind >= dense_stop * (double)(n - k - 1)))) {
       // every remaining variable has (approximate) external degree n-k-1: the rest is a
-      // clique, its internal order does not change the fill — append in index order
+      // clique, its internal order does not change the fill — append in index order.  With
+      // dense_stop < 1 the same is done once the minimum degree reaches that fraction of the
+      // remaining nodes (the tail then factors as one dense block anyway)
       for (int64_t i = 0; i < n; ++i)
         if (state[i] == 0) order.push_back(i);
       break;

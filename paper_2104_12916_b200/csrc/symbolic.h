@@ -155,8 +155,9 @@ LowerMatrix build_F_lower(int64_t n, int64_t m1, const int64_t* Hp, const int32_
 
 // Symmetric pattern (full, both triangles, no diagonal) → approximate minimum
 // degree order (new→old).
+// dense_stop < 1: stop once the minimum degree reaches that fraction of the remaining nodes.
 std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr,
-                                      const std::vector<int32_t>& idx);
+                                      const std::vector<int32_t>& idx, double dense_stop = 1.0);
 
 // Equivalent reordering by an elimination-tree postorder (same fill), composed with `order`.
 std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
