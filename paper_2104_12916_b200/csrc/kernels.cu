@@ -723,7 +723,8 @@ __device__ __forceinline__ void sweep_rhs(const SweepRhs& R, int64_t c0, int wk,
 
 // ---- SNW: one tiny single-block supernode per warp (w ≤ 32, noff ≤ 256, w·noff ≤ 1024)
 // forward: y = L_bb⁻¹ (rhs − acc), acc[rows] += L_rows·y, then release the destination counters.
-__device__ __forceinline__ void snw_forward(const DevFactor& F, const SweepRhs& R, double* x, int b, unsigned E) {
+__device__ __forceinline__ void snw_forward(const DevFactor& F, const SweepRhs& R, double* x, int b, unsigned E,
+                                            unsigned long long& ta, unsigned long long& tb) {
   const int lane = threadIdx.x & 31;
   const int J = F.blk_sn[b];
   const int wk = F.blk_w[b];
@@ -756,6 +757,7 @@ __device__ __forceinline__ void snw_forward(const DevFactor& F, const SweepRhs& 
     y += a * __shfl_sync(0xffffffffu, v, j);
   }
   if (lane < wk) x[c0 + lane] = y;
+  if (F.tprof && threadIdx.x == 0) ta = gtime();
   for (int r0 = 0; r0 < noff; r0 += 32) {
     const int r = r0 + lane;
     const bool ok = r < noff;
@@ -769,6 +771,7 @@ __device__ __forceinline__ void snw_forward(const DevFactor& F, const SweepRhs& 
     if (ok) atomicAdd(F.acc + row, s);
   }
   __syncwarp();
+  if (F.tprof && threadIdx.x == 0) tb = gtime();
   if (lane == 0)
     for (int64_t k = F.blk_dptr[b]; k < F.blk_dptr[b + 1]; ++k) {
       __threadfence();
@@ -975,7 +978,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
     } else if (type == 7) {
       // ---------------- SNW: up to 8 tiny supernodes of one level, one warp each
       const int bw = F.snw_fwd[idx * 8 + (tid >> 5)];
-      if (bw >= 0) snw_forward(F, R, x, bw, E);
+      if (bw >= 0) snw_forward(F, R, x, bw, E, ta, tb);
     } else if (type == 5) {
       // ---------------- SCHUNK: symmetric root — x_I += S_IK v_K, x_K += S_IKᵀ v_I (K < I)
       const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];

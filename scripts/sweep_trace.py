@@ -44,4 +44,8 @@ for sw in range(2):
     if k.any() and (tr[k, 3] > 0).any():
         print('  SNF phases (us, median): dep->solved %.2f  solved->atomics done %.2f  atomics->end %.2f' % (
             np.median(ma[k] - b[k]), np.median(mb[k] - ma[k]), np.median(c[k] - mb[k])))
+    k7 = typ == 7
+    if k7.any() and (tr[k7, 3] > 0).any():
+        print('  SNW warp-0 phases (us, median): start->solved %.2f  solved->fan-out issued %.2f  ->end (fences) %.2f' % (
+            np.median(ma[k7] - a[k7]), np.median(mb[k7] - ma[k7]), np.median(c[k7] - mb[k7])))
     print('  SNF start quantiles', np.percentile(a[k], [10, 50, 90]).round(1), 'dep-start quantiles', np.percentile((b - a)[k], [10, 50, 90]).round(1))
