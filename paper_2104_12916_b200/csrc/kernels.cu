@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int mode, 
     if (k0 + KC < kt) load(buf ^ 1, k0 + KC);
     const double* as = As[buf];
     const double* bs = Bs[buf];
-#pragma unroll 8
+#pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
       const double2 a0 = *reinterpret_cast<const double2*>(as + kk * LD + tx * 2);
       const double2 a1 = *reinterpret_cast<const double2*>(as + kk * LD + 32 + tx * 2);
