@@ -475,6 +475,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.sn_nblk = m.upload(S.sn_nblk, st);
     d.blk_dptr = m.upload(S.blk_dptr, st);
     d.blk_dest = m.upload(S.blk_dest, st);
+    d.mf_group = S.mf_group;
     d.snw_fwd = m.upload(S.snw_fwd, st);
     d.snw_bwd = m.upload(S.snw_bwd, st);
     d.flat = 0;
@@ -672,7 +673,7 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
     mf_extend_add(F.d, S.level_ea[L].grp_off, S.level_ea[L].n_grp, st);
     while (si < S.steps.size() && S.steps[si].level == L) {
       const StepDesc& sd = S.steps[si];
-      mf_step(F.d, sd.k, sd.kind, sd.act_off, sd.n_act, S.pref_off[si], sd.pan_total, sd.upd_total, st);
+      mf_step(F.d, sd.k, sd.k0, sd.kind, sd.act_off, sd.n_act, S.pref_off[si], sd.pan_total, sd.upd_total, st);
       ++si;
     }
   }

@@ -286,12 +286,12 @@ __global__ void __launch_bounds__(NT) k_mf_panel(DevFactor F, int k, int64_t act
 // D_k applied to the column operand once per landed chunk in shared memory.
 // mode 1: block k on the tiles i ≥ j ≥ k+1; 2: block k on the column strip j = k+1 (i ≥ k+1);
 // 3: blocks k and k+1 (≤ 128 pivot columns) on the tiles i ≥ j ≥ k+2.
-__global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int mode, int64_t act_off, int n_act,
+__global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int k0g, int mode, int64_t act_off, int n_act,
                                                   int64_t pref_off) {
   constexpr int KC = 16, LD = 64 + 4;
   __shared__ __align__(16) double As[2][KC * LD];
   __shared__ __align__(16) double Bs[2][KC * LD];
-  __shared__ double Dk[128];
+  __shared__ double Dk[4 * MF_BW];
   const int64_t* pref = F.upd_pref + pref_off;
   const int a = find_seg(pref, n_act + 1, blockIdx.x);
   const int J = F.act[act_off + a];
@@ -299,46 +299,48 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int mode, 
   const int64_t m = F.sn_rowptr[J + 1] - F.sn_rowptr[J];
   const int64_t fo = F.front_off[J];
   const int64_t nk = (w + MF_BW - 1) / MF_BW;
-  const int64_t q = blockIdx.x - pref[a];
+  const int64_t ntile = nk + (m - w + MF_BW - 1) / MF_BW;
+  const int64_t e = min((int64_t)k0g + F.mf_group, nk) - 1;   // last pivot block of this front's group
+  int64_t q = blockIdx.x - pref[a];
   int64_t ti, tj;
-  if (mode == 2) {
-    ti = k + 1 + q;
+  int kfirst, nblk;   // pivot blocks kfirst .. kfirst + nblk − 1 are applied
+  if (mode == 2) {    // band: block k on block columns k+1 .. e, rows ≥ the column
     tj = k + 1;
-  } else {
+    while (q >= ntile - tj) {
+      q -= ntile - tj;
+      ++tj;
+    }
+    ti = tj + q;
+    kfirst = k;
+    nblk = 1;
+  } else {            // trailing triangle from block column e+1, all the group's blocks
     int64_t ii = (int64_t)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
     while (ii * (ii + 1) / 2 > q) --ii;
     while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
     const int64_t jj = q - ii * (ii + 1) / 2;
-    const int64_t t0 = mode == 3 ? k + 2 : k + 1;
-    ti = t0 + ii;
-    tj = t0 + jj;
+    ti = e + 1 + ii;
+    tj = e + 1 + jj;
+    kfirst = k0g;
+    nblk = (int)(e - k0g + 1);
   }
-  const int64_t p0 = (int64_t)MF_BW * k;
-  const int wk = (int)(w - p0 < MF_BW ? w - p0 : MF_BW);       // = 64 whenever block k+1 exists
-  const int b = F.sn_blk0[J] + k;
+  const int64_t p0 = (int64_t)MF_BW * kfirst;
+  const int kt = (int)(min((int64_t)MF_BW * (kfirst + nblk), w) - p0);   // pivot columns applied
+  const int b0 = F.sn_blk0[J] + kfirst;
   const int64_t ib = tile_begin(ti, nk, w, m), ie = tile_begin(ti + 1, nk, w, m);
   const int64_t jb = tile_begin(tj, nk, w, m), je = tile_begin(tj + 1, nk, w, m);
   const int Ri = (int)(ie - ib), Rj = (int)(je - jb);
-  const int64_t noff = F.blk_noff[b];
-  const double* L = F.fstore + F.blk_off[b] - (p0 + wk);  // index by front row
-  // second pivot block (mode 3)
-  const int64_t p1 = p0 + MF_BW;
-  const int wk1 = mode == 3 ? (int)(w - p1 < MF_BW ? w - p1 : MF_BW) : 0;
-  const int64_t noff1 = mode == 3 ? F.blk_noff[b + 1] : 0;
-  const double* L1 = mode == 3 ? F.fstore + F.blk_off[b + 1] - (p1 + wk1) : L;
-  const int kt = wk + wk1;                                  // pivot columns of this update
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  if (tid < wk) Dk[tid] = F.Dpiv[c0 + p0 + tid];
-  else if (tid < kt) Dk[tid] = F.Dpiv[c0 + p1 + (tid - wk)];
+  if (tid < kt) Dk[tid] = F.Dpiv[c0 + p0 + tid];
   {   // pull the C tile into L2 now so the read-modify-write epilogue does not wait on HBM
     const int cc = tid >> 2, seg = tid & 3;   // 64 columns × 4 lines of 16 doubles
     if (cc < Rj && seg * 16 < Ri) prefetch_l2(F.ws + fo + (jb + cc) * m + ib + seg * 16);
   }
-  auto load = [&](int buf, int k0) {   // chunks of block k, then of block k+1 (wk = 64 then)
-    const bool second = k0 >= wk;
-    const double* Ls = second ? L1 : L;
-    const int64_t ns = second ? noff1 : noff;
-    const int kb = second ? k0 - wk : k0, wl = second ? wk1 : wk;
+  auto load = [&](int buf, int kc0) {   // chunk of 16 pivot columns: block kfirst + kc0/64 (all but the last are 64 wide)
+    const int bi = kc0 / MF_BW, kb = kc0 - bi * MF_BW;
+    const int64_t pb = p0 + (int64_t)bi * MF_BW;
+    const int wl = (int)(min(pb + MF_BW, w) - pb);
+    const int64_t ns = F.blk_noff[b0 + bi];
+    const double* Ls = F.fstore + F.blk_off[b0 + bi] - (pb + wl);   // index by front row
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int idx = tid + NT * u;
@@ -366,8 +368,7 @@ __global__ void __launch_bounds__(NT) k_mf_update(DevFactor F, int k, int mode, 
         const int idx = tid + NT * u;
         const int r = idx & 63, c = idx >> 6;
         const int kc = k0 + c;
-        const bool ok = k0 >= wk ? kc - wk < wk1 : kc < wk;
-        bw[c * LD + r] *= ok ? Dk[kc] : 0.0;
+        bw[c * LD + r] *= kc < kt ? Dk[kc] : 0.0;
       }
     }
     __syncthreads();
@@ -418,8 +419,8 @@ void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStrea
   int64_t grid = (n_grp * 32 + NT - 1) / NT;
   k_mf_extend_add<<<(unsigned)grid, NT, 0, s>>>(F, grp_off, n_grp);
 }
-void mf_step(const DevFactor& F, int k, int kind, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
-             int64_t upd_total, cudaStream_t s) {
+void mf_step(const DevFactor& F, int k, int k0, int kind, int64_t act_off, int n_act, int64_t pref_off,
+             int64_t pan_total, int64_t upd_total, cudaStream_t s) {
   if (n_act == 0) return;
   static bool attr = false;
   const size_t sd = 2 * 64 * 65 * 8, sp = (2 * 64 * 65 + 64) * 8;
@@ -432,7 +433,7 @@ void mf_step(const DevFactor& F, int k, int kind, int64_t act_off, int n_act, in
     k_mf_diag<<<n_act, NT, sd, s>>>(F, k, act_off);
     if (pan_total > 0) k_mf_panel<<<(unsigned)pan_total, NT, sp, s>>>(F, k, act_off, n_act, pref_off);
   } else if (upd_total > 0) {
-    k_mf_update<<<(unsigned)upd_total, NT, 0, s>>>(F, k, kind, act_off, n_act, pref_off);
+    k_mf_update<<<(unsigned)upd_total, NT, 0, s>>>(F, k, k0, kind, act_off, n_act, pref_off);
   }
 }
 

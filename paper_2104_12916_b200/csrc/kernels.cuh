@@ -115,6 +115,7 @@ struct DevFactor {
   const int64_t* fl_mr_ptr;       // M by root rows (forward product)
   const int32_t* fl_mr_col;
   double* fl_mr_val;
+  int mf_group;                   // pivot blocks per trailing UPDATE (Symbolic::mf_group)
   unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][8 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
@@ -163,9 +164,9 @@ void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid
 void mf_assemble_level(const DevFactor& F, int64_t fr_off, int64_t n_fr, int64_t zero_total, int64_t asm_off,
                        int64_t n_asm, const double* src_vals, const double* D, const int64_t* perm, cudaStream_t s);
 void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStream_t s);
-// kind: see StepDesc (0 DIAG+PANEL, 1–3 UPDATE modes)
-void mf_step(const DevFactor& F, int k, int kind, int64_t act_off, int n_act, int64_t pref_off, int64_t pan_total,
-             int64_t upd_total, cudaStream_t s);
+// kind: see StepDesc (0 DIAG+PANEL, 2 band UPDATE, 3 trailing UPDATE); k0: the group's first block
+void mf_step(const DevFactor& F, int k, int k0, int kind, int64_t act_off, int n_act, int64_t pref_off,
+             int64_t pan_total, int64_t upd_total, cudaStream_t s);
 
 // ---- partitioned inverse X_J = L_JJ⁻¹ of big supernodes (factor time)
 struct GemmProb {

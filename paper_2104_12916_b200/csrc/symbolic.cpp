@@ -714,15 +714,19 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
       int64_t w = S.sn_start[J + 1] - S.sn_start[J];
       max_nk = std::max(max_nk, (w + BW - 1) / BW);
     }
-    // Steps.  Pairs of pivot blocks (k, k+1): DIAG+PANEL(k); fronts ending at block k: UPDATE(k) on
-    // their trailing triangle; the others: UPDATE(k) on block column k+1 only, DIAG+PANEL(k+1), then
-    // one UPDATE with both blocks (128 pivot columns) on the triangle from k+2 — the trailing matrix
-    // is read and written once per two blocks.  QPB_PAIR=0: one block per step.
-    const bool pair = !(std::getenv("QPB_PAIR") && std::getenv("QPB_PAIR")[0] == '0');
-    auto add_step = [&](int64_t k, int kind, auto select) {
+    // Steps, in groups of G pivot blocks k0 .. e (e = min(k0 + G, nk) − 1 per front): for each block g
+    // of the group, DIAG+PANEL(g), then (g < e) UPDATE of the group's remaining block columns g+1 .. e by
+    // block g (kind 2, a narrow band); after the group, ONE UPDATE of the trailing triangle (block columns
+    // > e) with all the group's pivot columns (kind 3, up to 64·G of them).  The trailing matrix is then
+    // read and written once per G blocks.  QPB_GROUP = G (default 4; 1 = one block per update).
+    const int64_t G = std::getenv("QPB_GROUP") ? std::max<int64_t>(1, std::min<int64_t>(4, std::atoll(std::getenv("QPB_GROUP"))))
+                                               : 4;
+    S.mf_group = (int32_t)G;
+    auto add_step = [&](int64_t k, int64_t k0, int kind, auto select) {
       StepDesc sd;
       sd.level = (int)L;
       sd.k = (int)k;
+      sd.k0 = (int)k0;
       sd.kind = kind;
       sd.act_off = (int64_t)S.act.size();
       S.pref_off.push_back((int64_t)S.pan_pref.size());
@@ -735,18 +739,17 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
         const int64_t nk = (w + BW - 1) / BW;
         if (!select(nk)) continue;
         const int64_t ntile = nk + (m - w + BW - 1) / BW;
+        const int64_t e = std::min(k0 + G, nk) - 1;   // last block of this front's group
         int64_t pan = 0, upd = 0;
         if (kind == 0) {
           pan = ntile - k - 1;
-        } else if (kind == 1) {
-          const int64_t T = ntile - k - 1;
-          upd = T * (T + 1) / 2;
         } else if (kind == 2) {
-          upd = ntile - k - 1;
+          for (int64_t tj = k + 1; tj <= e; ++tj) upd += ntile - tj;
         } else {
-          const int64_t T = ntile - k - 2;
+          const int64_t T = ntile - e - 1;
           upd = T * (T + 1) / 2;
         }
+        if (kind != 0 && upd == 0) continue;
         S.act.push_back(J);
         S.pan_pref.push_back(S.pan_pref.back() + pan);
         S.upd_pref.push_back(S.upd_pref.back() + upd);
@@ -762,16 +765,12 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
         S.upd_pref.pop_back();
       }
     };
-    for (int64_t k = 0; k < max_nk; k += pair ? 2 : 1) {
-      add_step(k, 0, [&](int64_t nk) { return nk > k; });
-      if (!pair) {
-        add_step(k, 1, [&](int64_t nk) { return nk > k; });
-        continue;
+    for (int64_t k0 = 0; k0 < max_nk; k0 += G) {
+      for (int64_t g = k0; g < std::min(k0 + G, max_nk); ++g) {
+        add_step(g, k0, 0, [&](int64_t nk) { return nk > g; });
+        add_step(g, k0, 2, [&](int64_t nk) { return nk > g + 1 && g + 1 < k0 + G; });
       }
-      add_step(k, 1, [&](int64_t nk) { return nk == k + 1; });
-      add_step(k, 2, [&](int64_t nk) { return nk > k + 1; });
-      add_step(k + 1, 0, [&](int64_t nk) { return nk > k + 1; });
-      add_step(k, 3, [&](int64_t nk) { return nk > k + 1; });
+      add_step(k0, k0, 3, [&](int64_t nk) { return nk > k0; });
     }
   }
   S.pivsign.assign(N, 1);

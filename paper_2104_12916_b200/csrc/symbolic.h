@@ -32,8 +32,9 @@ struct LowerMatrix {
 
 struct StepDesc {
   int level, k;
-  int kind;           // 0 DIAG+PANEL(k); UPDATE with 1: block k on tiles i ≥ j ≥ k+1; 2: block k on the
-                      // column strip j = k+1; 3: blocks k and k+1 on tiles i ≥ j ≥ k+2
+  int k0;             // first pivot block of the step's group
+  int kind;           // 0 DIAG+PANEL(k); UPDATE with 2: block k on the group's block columns k+1 .. e
+                      // (i ≥ j); 3: blocks k0 .. e on the trailing tiles i ≥ j > e (e per front)
   int n_act;          // active fronts
   int64_t act_off;    // offset into act list
   int64_t pan_total;  // PANEL tiles
@@ -130,6 +131,7 @@ struct Symbolic {
   std::vector<int32_t> fl_mr_src;     //   index of each entry in the M_J blocks (values copied once)
 
   // multifrontal plan
+  int32_t mf_group = 4;               // pivot blocks per trailing update (see the steps in analyse)
   std::vector<int64_t> asm_dst;    // destination in workspace for each lower entry (+diag)
   std::vector<double> asm_val;     // F: values; P_H: T-values filled on device
   std::vector<int64_t> asm_src;    // P_H: index into device T values (-1 = none)
