@@ -1042,8 +1042,8 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       const int64_t c0 = F.blk_col0[b];
       const bool longt = Rn * wk > 4096;   // a long tile of a full-width block: straight from global memory
       const double* Lt = F.fstore + F.blk_off[b] + r0;
-      if (longt) prefetch_block(Lt, Rn, wk, noff);
-      else load_tile(sm, Lt, Rn, wk, noff);
+      if (!longt) load_tile(sm, Lt, Rn, wk, noff);   // long tiles stream after the wait (an L2 prefetch of
+      // 256 KB per task was evicted before use and doubled the DRAM reads)
       if (tid == 0) {
         spin_u32(F.ready_f + b, E);
         if (F.tprof) t1 = gtime();
@@ -1298,8 +1298,8 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
       const int64_t c0 = F.blk_col0[b];
       const double* Lt = F.fstore + F.blk_off[b] + r0;
       const bool longt = Rn * wk > 4096;
-      if (longt) prefetch_block(Lt, Rn, wk, noff);
-      else load_tile(sm, Lt, Rn, wk, noff);
+      if (!longt) load_tile(sm, Lt, Rn, wk, noff);   // long tiles stream after the wait (an L2 prefetch of
+      // 256 KB per task was evicted before use and doubled the DRAM reads)
       if (tid == 0) {
         spin_u32(F.ready_sb + F.tile_dest[ti], E);
         if (F.tprof) t1 = gtime();
