@@ -83,9 +83,9 @@ def _solver(qp, rank, world, comm):
     return s
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_pcg_matches_oracle(world):
-    qp = qpgen.make("c0")
+@pytest.mark.parametrize("world,name", [(2, "c0"), (3, "c0"), (4, "ragged")])
+def test_sharded_pcg_matches_oracle(world, name):
+    qp = qpgen.make("c0") if name == "c0" else qpgen.scaled_random_qp(700, 130, 900, seed=3)
     rng = np.random.default_rng(11)
     D = rng.uniform(0.5, 2.0, qp.m2)
     b = rng.standard_normal(qp.m2)
