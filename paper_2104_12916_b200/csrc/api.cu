@@ -552,6 +552,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.status = m.zeros<int>(1, st);
     d.tprof = nullptr;
     d.use_sym = 0;
+    d.sweep_var = getenv("QPB_SWEEP_VAR") ? atoi(getenv("QPB_SWEEP_VAR")) : 1;
     F.fwd_sym = d.fwd_tasks;
     F.bwd_sym = d.bwd_tasks;
     F.n_fwd_sym = d.n_fwd_tasks;
@@ -1897,9 +1898,15 @@ int qp_profile_read(qp_ctx* c, double* ms, int64_t* count) {
 
 // Debug: sweep instrumentation of the F factor. enable=1 resets and turns it on;
 // enable=0 copies [2 sweeps][8 task types][count, wait ns, busy ns, first, last] into out (80 int64).
+// QPB_TRACE_PH=1 selects the P_H factor's sweeps instead of F's (debug only).
+static bool trace_ph(qp_ctx* c) {
+  const char* e = getenv("QPB_TRACE_PH");
+  return e && atoi(e) != 0 && c->FP.tprof_buf != nullptr;
+}
+
 int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
   if (!c || !c->factored) return QP_ESTATE;
-  Factor& F = c->FF;
+  Factor& F = trace_ph(c) ? c->FP : c->FF;
   if (enable) {
     std::vector<unsigned long long> init(80 + 12 * F.d.ttrace_cap, 0);
     for (int i = 0; i < 16; ++i) init[i * 5 + 3] = ~0ull;
@@ -1917,7 +1924,7 @@ int qp_debug_sweep_profile(qp_ctx* c, int32_t enable, int64_t* out) {
 // number of records written (the sweep's task count) or a negative status.
 int64_t qp_debug_sweep_trace(qp_ctx* c, int32_t sweep, int64_t* out, int64_t cap) {
   if (!c || !c->factored || sweep < 0 || sweep > 1) return QP_ESTATE;
-  Factor& F = c->FF;
+  Factor& F = trace_ph(c) ? c->FP : c->FF;
   const int64_t n = std::min<int64_t>(cap, sweep == 0 ? F.d.n_fwd_tasks : F.d.n_bwd_tasks);
   if (n > 0 && out)
     cudaMemcpyAsync(out, F.tprof_buf + 80 + sweep * F.d.ttrace_cap * 6, n * 48, cudaMemcpyDeviceToHost, c->stream);

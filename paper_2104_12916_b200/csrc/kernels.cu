@@ -1098,7 +1098,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
 }
 
 // Backward sweep Lᵀ x = D⁻¹ y (in place in x).
-__global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const int* done_flag) {
+__global__ void __launch_bounds__(NT, 4) k_trsv_bwd(DevFactor F, double* x, const int* done_flag) {
   extern __shared__ double sm[];
   __shared__ SweepShared S;
   const int tid = threadIdx.x;
@@ -1316,7 +1316,22 @@ __global__ void __launch_bounds__(NT) k_trsv_bwd(DevFactor F, double* x, const i
         double t[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) t[u] = 0.0;
-        for (int r = lane; r < Rn; r += 32) {
+        int r = lane;
+        if (wk == 64 && (F.sweep_var & 1)) {   // full-width block: two rows per lane in flight (16 loads)
+          const double* Lc = Lt + (int64_t)cw * noff;
+          for (; r + 32 < Rn; r += 64) {
+            const double xa = sm[r], xb = sm[r + 32];
+            double va[8], vb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              va[u] = __ldg(Lc + r + (int64_t)u * noff);
+              vb[u] = __ldg(Lc + r + 32 + (int64_t)u * noff);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] += va[u] * xa + vb[u] * xb;
+          }
+        }
+        for (; r < Rn; r += 32) {
           const double xv = sm[r];
 #pragma unroll
           for (int u = 0; u < 8; ++u)

@@ -118,6 +118,7 @@ struct DevFactor {
   int mf_group;                   // pivot blocks per trailing UPDATE (Symbolic::mf_group)
   unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][8 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
+  int sweep_var;      // A/B switch (QPB_SWEEP_VAR, default 1): bit 0 = backward long tiles two rows per lane
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
 };
 

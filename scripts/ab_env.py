@@ -11,7 +11,7 @@ sys.path.insert(0, '.')
 import qpgen
 from paper_2104_12916_b200.binding import from_qp
 qp = qpgen.make(sys.argv[1])
-s = from_qp(qp); s.ipm_factor_once('low')
+s = from_qp(qp); s.ipm_factor_once(sys.argv[2])
 rng = np.random.default_rng(0); D = rng.uniform(0.5, 2, qp.m2); b = rng.standard_normal(qp.m2)
 s.pcg_solve(D, b, tol=0.0, maxit=20)
 best = 1e9
@@ -26,12 +26,15 @@ def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     reps = 3
     cfg = "c1"
+    pre = "low"
     for i, a in enumerate(sys.argv):
         if a == "--reps":
             reps = int(sys.argv[i + 1])
         if a == "--config":
             cfg = sys.argv[i + 1]
-    variants = [a for a in args if a not in (str(reps), cfg)]
+        if a == "--precond":
+            pre = sys.argv[i + 1]
+    variants = [a for a in args if a not in (str(reps), cfg, pre)]
     res = {v: [] for v in variants}
     for _ in range(reps):
         for v in variants:
@@ -40,7 +43,7 @@ def main():
                 if "=" in kv:
                     k, val = kv.split("=", 1)
                     env[k] = val
-            out = subprocess.run([sys.executable, "-c", CHILD, cfg], env=env, capture_output=True, text=True)
+            out = subprocess.run([sys.executable, "-c", CHILD, cfg, pre], env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             res[v].append(json.loads(line[-1])["ms_per_it"] if line else float("nan"))
             if not line:

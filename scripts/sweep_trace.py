@@ -5,18 +5,27 @@ sys.path.insert(0, '.')
 import qpgen
 from paper_2104_12916_b200.binding import from_qp
 
+import os
 qp = qpgen.make(sys.argv[1] if len(sys.argv) > 1 else 'c1')
+PH = len(sys.argv) > 2 and sys.argv[2] == 'ph'      # trace the P_H factor's sweeps (QPB_TRACE_PH=1)
+if PH:
+    os.environ['QPB_TRACE_PH'] = '1'
 s = from_qp(qp)
-s.ipm_factor_once('low')
-ss = s.structure('sn_start'); lev = s.structure('sn_level')
+s.ipm_factor_once('high' if PH else 'low')
+ss = s.structure('sn_start', ph=PH); lev = s.structure('sn_level', ph=PH)
 w = np.diff(ss)
 nblk = (w + 63) // 64
 blk_sn = np.repeat(np.arange(len(w)), nblk)
 rng = np.random.default_rng(0)
 D = rng.uniform(0.5, 2, qp.m2); p = rng.standard_normal(qp.m2)
+def run():
+    if PH:   # one P_H apply per PCG iteration; the trace keeps the last sweep pair
+        s.pcg_solve(D, p, tol=1e-30, maxit=2)
+    else:
+        s.kf_apply(D, p)
 for rep in range(3):
-    s.kf_apply(D, p)
-s.debug_sweep_profile(True); s.kf_apply(D, p); s.debug_sweep_profile(False)
+    run()
+s.debug_sweep_profile(True); run(); s.debug_sweep_profile(False)
 names = ['DIAG', 'TILE', 'PREP', 'XCHUNK', 'SNF', 'SCHUNK', 'ROOTB', 'SNW']
 for sw in range(2):
     tr = s.debug_sweep_trace(sw)
@@ -40,6 +49,11 @@ for sw in range(2):
     print('  start time by ticket decile:', ['%.1f' % np.median(st[i:i + len(st) // 10]) for i in range(0, len(st), len(st) // 10)])
     print('  setup (dep-met - start) by type:', {names[t]: '%.2f' % np.median((b - a)[typ == t]) for t in np.unique(typ)})
     print('  tasks per SM: min %d max %d' % (np.bincount(sm).min(), np.bincount(sm).max()))
+    for ty in np.unique(typ):
+        k = typ == ty
+        print('  %-6s total busy %.1f us (%.1f%% of span x CTAs)  median busy %.2f us  median wait %.2f us' % (
+            names[ty], (c[k] - b[k]).sum(), 100 * (c[k] - b[k]).sum() / (c.max() * len(np.unique(sm)) * 4),
+            np.median(c[k] - b[k]), np.median(b[k] - a[k])))
     k = typ == 4
     if k.any() and (tr[k, 3] > 0).any():
         print('  SNF phases (us, median): dep->solved %.2f  solved->atomics done %.2f  atomics->end %.2f' % (
