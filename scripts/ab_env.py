@@ -21,6 +21,21 @@ for _ in range(3):
 print(json.dumps({"ms_per_it": best}))
 '''
 
+CHILD_REFACTOR = r'''
+import sys, time, json, numpy as np
+sys.path.insert(0, '.')
+import qpgen
+from paper_2104_12916_b200.binding import from_qp
+qp = qpgen.make(sys.argv[1])
+s = from_qp(qp); s.ipm_factor_once('high')
+rng = np.random.default_rng(0); b = rng.standard_normal(qp.m2)
+best = 1e9
+for _ in range(4):   # each new D forces one P_H numeric refactor inside pcg_solve
+    s.pcg_solve(rng.uniform(0.5, 2, qp.m2), b, tol=0.0, maxit=1)
+    best = min(best, 1e3 * s.stats()['t_factor_ph_s'])
+print(json.dumps({"ms_per_it": best}))
+'''
+
 
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
@@ -43,7 +58,8 @@ def main():
                 if "=" in kv:
                     k, val = kv.split("=", 1)
                     env[k] = val
-            out = subprocess.run([sys.executable, "-c", CHILD, cfg, pre], env=env, capture_output=True, text=True)
+            child = CHILD_REFACTOR if "--refactor" in sys.argv else CHILD
+            out = subprocess.run([sys.executable, "-c", child, cfg, pre], env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
             res[v].append(json.loads(line[-1])["ms_per_it"] if line else float("nan"))
             if not line:
