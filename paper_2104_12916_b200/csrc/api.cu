@@ -443,7 +443,8 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.tile_blk = m.upload(S.tile_blk, st);
     d.tile_r0 = m.upload(S.tile_r0, st);
     d.tile_nr = m.upload(S.tile_nr, st);
-    d.tile_dest = m.upload(S.tile_dest, st);
+    d.tile_dptr = m.upload(S.tile_dptr, st);
+    d.tile_dlist = m.upload(S.tile_dlist, st);
     d.fwd_tasks = m.upload(S.fwd_tasks, st);
     d.bwd_tasks = m.upload(S.bwd_tasks, st);
     F.fwd_x = m.upload(S.fwd_tasks_x, st);

@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
         }
       }
     } else {
-      // ---------------- TILE: acc[rows] += L_tile · y_b  (rows all in supernode tile_dest)
+      // ---------------- TILE: acc[rows] += L_tile · y_b  (rows in the supernodes tile_dlist[tile_dptr[ti] ..])
       const int ti = idx;
       const int b = F.tile_blk[ti];
       const int wk = F.blk_w[b];
@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       __syncthreads();
       if (tid == 0) {
         __threadfence();
-        atomicAdd(F.cnt_f + F.tile_dest[ti], 1ull);
+        for (int64_t q = F.tile_dptr[ti]; q < F.tile_dptr[ti + 1]; ++q) atomicAdd(F.cnt_f + F.tile_dlist[q], 1ull);
       }
     }
     if (F.tprof) tprof_add(F.tprof, 0, type, t0, t1, gtime(), task, S.ticket, F.ttrace_cap, ta, tb);
@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(NT, 4) k_trsv_bwd(DevFactor F, double* x, cons
       if (!longt) load_tile(sm, Lt, Rn, wk, noff);   // long tiles stream after the wait (an L2 prefetch of
       // 256 KB per task was evicted before use and doubled the DRAM reads)
       if (tid == 0) {
-        spin_u32(F.ready_sb + F.tile_dest[ti], E);
+        for (int64_t q = F.tile_dptr[ti]; q < F.tile_dptr[ti + 1]; ++q) spin_u32(F.ready_sb + F.tile_dlist[q], E);
         if (F.tprof) t1 = gtime();
       }
       __syncthreads();

@@ -29,7 +29,8 @@ struct DevFactor {
   const int32_t* tile_blk;
   const int32_t* tile_r0;
   const int32_t* tile_nr;
-  const int32_t* tile_dest;
+  const int64_t* tile_dptr;    // destination supernodes of tile t: tile_dlist[tile_dptr[t] .. tile_dptr[t+1])
+  const int32_t* tile_dlist;
   const int32_t* fwd_tasks;
   const int32_t* bwd_tasks;
   const int32_t* fwd_expect;

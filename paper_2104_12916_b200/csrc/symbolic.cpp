@@ -394,7 +394,9 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   // ---------------------------------------------------------------- trsv tiles and task queues
   // Big supernodes (more than one 64-column block) are swept through X_J = L_JJ⁻¹
   // (partitioned inverse): their intra-supernode rows are not tiled.
-  S.tile_blk.clear(); S.tile_r0.clear(); S.tile_nr.clear(); S.tile_dest.clear();
+  S.tile_blk.clear(); S.tile_r0.clear(); S.tile_nr.clear(); S.tile_dlist.clear();
+  S.tile_dptr.assign(1, 0);
+  const bool split_dest = std::getenv("QPB_TILE_SPLIT") && std::atoi(std::getenv("QPB_TILE_SPLIT")) != 0;
   S.fwd_expect.assign(ns, 0);
   S.bwd_expect.assign(S.nb, 0);
   S.blk_big.assign(S.nb, 0);
@@ -456,16 +458,32 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     // LONG_TILE rows instead, swept straight from global memory (fewer tasks, counters and atomics)
     const int64_t cap = wk == BW ? LONG_TILE : std::max<int64_t>(1, std::min<int64_t>(1024, TILE_ELEMS / wk));
     // first off-diagonal row below the supernode's own columns
+    // A tile may span several destination supernodes (rows are sorted, so they form runs): it bumps each
+    // destination's forward counter once and, backward, waits for each destination's ready flag.  Tiles
+    // split only by size, into equal parts: fewer tasks, so fewer CTAs parked on a dependency
+    // (QPB_TILE_SPLIT=1 restores one destination per tile).
     int64_t r = S.blk_big[b] ? (S.sn_start[J + 1] - (S.blk_col0[b] + wk)) : 0;
+    const int64_t ntl = (noff - r + cap - 1) / cap, per = ntl > 0 ? (noff - r + ntl - 1) / ntl : cap;
     while (r < noff) {
-      int32_t dest = (int32_t)col2sn[S.sn_rows[S.blk_rows[b] + r]];
-      int64_t e = r + 1;
-      while (e < noff && e - r < cap && col2sn[S.sn_rows[S.blk_rows[b] + e]] == dest) ++e;
+      int64_t e = std::min(noff, r + per);
+      if (split_dest) {
+        const int64_t d0 = col2sn[S.sn_rows[S.blk_rows[b] + r]];
+        e = r + 1;
+        while (e < noff && e - r < cap && col2sn[S.sn_rows[S.blk_rows[b] + e]] == d0) ++e;
+      }
       S.tile_blk.push_back((int32_t)b);
       S.tile_r0.push_back((int32_t)r);
       S.tile_nr.push_back((int32_t)(e - r));
-      S.tile_dest.push_back(dest);
-      S.fwd_expect[dest] += 1;
+      int64_t last = -1;
+      for (int64_t q = r; q < e; ++q) {
+        const int64_t dsn = col2sn[S.sn_rows[S.blk_rows[b] + q]];
+        if (dsn != last) {
+          S.tile_dlist.push_back((int32_t)dsn);
+          S.fwd_expect[dsn] += 1;
+          last = dsn;
+        }
+      }
+      S.tile_dptr.push_back((int64_t)S.tile_dlist.size());
       S.bwd_expect[b] += 1;
       r = e;
     }

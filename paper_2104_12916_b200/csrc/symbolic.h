@@ -87,7 +87,9 @@ struct Symbolic {
   // 5 SCHUNK(chunk of S_J⁻¹ of a symmetric root: x_I += S_IK v_K and x_K += S_IKᵀ v_I),
   // 6 ROOTB(backward: the symmetric root's x is already final — publish it),
   // 7 SNW(up to 8 tiny single-block supernodes of one level, one warp each).
-  std::vector<int32_t> tile_blk, tile_r0, tile_nr, tile_dest;   // tile_dest: destination SUPERNODE
+  std::vector<int32_t> tile_blk, tile_r0, tile_nr;
+  std::vector<int64_t> tile_dptr;    // tile t's destination SUPERNODES: tile_dlist[tile_dptr[t] .. tile_dptr[t+1])
+  std::vector<int32_t> tile_dlist;
   std::vector<int32_t> fwd_tasks, bwd_tasks, fwd_expect /*per supernode*/, bwd_expect /*per block*/;
   std::vector<int32_t> fwd_tasks_x, bwd_tasks_x;   // same queues with symmetric roots swept through X/Xᵀ (fallback)
   // partitioned inverse of multi-block ("big") supernodes
