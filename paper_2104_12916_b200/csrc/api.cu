@@ -554,6 +554,7 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.tprof = nullptr;
     d.use_sym = 0;
     d.sweep_var = getenv("QPB_SWEEP_VAR") ? atoi(getenv("QPB_SWEEP_VAR")) : 1;
+    d.l2hint = getenv("QPB_L2HINT") ? atoi(getenv("QPB_L2HINT")) : 0;
     F.fwd_sym = d.fwd_tasks;
     F.bwd_sym = d.bwd_tasks;
     F.n_fwd_sym = d.n_fwd_tasks;
@@ -726,8 +727,8 @@ void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
 }
 
 // q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
-int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode) {
-  c->launches += 1;
+int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode, bool fsolve_only = false) {
+  c->launches += fsolve_only ? 0 : 1;
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
   static const bool pregather = !(std::getenv("QPB_PREGATHER") && std::getenv("QPB_PREGATHER")[0] == '0');
@@ -743,6 +744,7 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
     r.p = p;
   }
   f_solve_sweeps(c, r, c->xbuf);
+  if (fsolve_only) return 0;   // q = D∘p − C w comes from the fused PCG step
   int h = c->begin(2);
   kf_q(c->Cf, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
   c->end(h);
@@ -805,7 +807,22 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
     pcg_init_ph(m2, c->pr, c->pz, c->pp, c->partial, c->pst, c->vgrid, st);
     c->launches += 1;
   }
+  // P_L / none on one GPU: a5 + a6 as one cooperative kernel (QPB_FUSED_PCG=0 restores k_kf_q,
+  // k_pcg_update1, k_pcg_update2 — bit-identical results)
+  static const bool fused_env = !(std::getenv("QPB_FUSED_PCG") && std::getenv("QPB_FUSED_PCG")[0] == '0');
+  const bool fused = fused_env && prec != 2 && !c->sharded;
   auto body = [&]() -> int {
+    if (fused) {
+      if (int rc = kf_apply_dev(c, D, c->pp, c->pq, true, true)) return rc;
+      int hh = c->begin(2);
+      const bool ok = pcg_step(c->Cf, prec, D, c->pp, c->xbuf, c->pq, c->px, c->pr, c->pz, c->partial, c->pst,
+                               c->vgrid, st);
+      c->end(hh);
+      c->launches += 1;
+      if (ok) return 0;
+      cudaGetLastError();
+      return fail(c, QP_ECUDA, "cooperative launch of k_pcg_step failed");
+    }
     if (int rc = kf_apply_dev(c, D, c->pp, c->pq, true)) return rc;
     int hh = c->begin(3);
     pcg_update1(prec, m2, D, c->pp, c->pq, c->px, c->pr, c->pz, c->partial, c->pst, c->vgrid, st);

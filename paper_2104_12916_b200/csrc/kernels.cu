@@ -14,6 +14,8 @@
 //    (P:L284–285);
 //  * IPM rhs / r_ν / recovery / Δs / step kernels (P:L65–69, P:L473–505,
 //    P:L727–752).
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 #include "kernels.cuh"
 
 #include <cfloat>
@@ -605,12 +607,52 @@ __device__ __forceinline__ void xchunk_gemv(const double* __restrict__ M, int64_
   __syncthreads();
 }
 
+// L2 eviction-priority hints (createpolicy + ld.global.nc.L2::cache_hint): the root GEMV's one-pass
+// stream of S⁻¹ (1.8 GB on c1) is marked evict_first so it does not push the flattened-forest arrays
+// (re-read by every F-solve, ≈0.1 GB) out of L2; those are marked evict_last.
+__device__ __forceinline__ uint64_t l2pol_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2pol_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2pol_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ldg_pol(const double2* a, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_pol(const double* a, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ldg_pol(const int32_t* a, uint64_t pol) {
+  int32_t v;
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ldg_pol(const int64_t* a, uint64_t pol) {
+  int64_t v;
+  asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 // Symmetric-root chunk: rows R ≤ 64 of block I, ncol columns of blocks K0..;
 // red[512 + r] = Σ_c S(r,c)·vK[c] (all columns) and colv[c] = Σ_r S(r,c)·vI[r] for c < ncol_t
 // (the columns strictly before block I).  One read of the chunk serves both products.
 template <int U = 8>
 __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_t ld, int R, int ncol, int ncol_t,
-                                            const double* vK, const double* vI, double* red, double* colv) {
+                                            const double* vK, const double* vI, double* red, double* colv,
+                                            uint64_t pol) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool ok = 2 * lane < R;
   const double2* base = reinterpret_cast<const double2*>(M + 2 * lane);
@@ -621,7 +663,7 @@ __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_
   for (; c + 8 * (U - 1) < ncol; c += 8 * U) {
     double2 q[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) q[u] = ok ? __ldg(base + (int64_t)(c + 8 * u) * ld2) : make_double2(0.0, 0.0);
+    for (int u = 0; u < U; ++u) q[u] = ok ? ldg_pol(base + (int64_t)(c + 8 * u) * ld2, pol) : make_double2(0.0, 0.0);
     double t[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -679,7 +721,7 @@ __device__ __forceinline__ void schunk_gemv(const double* __restrict__ M, int64_
     }
   }
   for (; c < ncol; c += 8) {
-    const double2 q = ok ? __ldg(base + (int64_t)c * ld2) : make_double2(0.0, 0.0);
+    const double2 q = ok ? ldg_pol(base + (int64_t)c * ld2, pol) : make_double2(0.0, 0.0);
     const double vc = vK[c];
     a0 = fma(q.x, vc, a0);
     a1 = fma(q.y, vc, a1);
@@ -1001,7 +1043,8 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       if (tid < Rn) vI[tid] = __ldcg(F.vbuf + rI + tid);
       __syncthreads();
       const int64_t ldx = F.sn_ldx[J];
-      schunk_gemv(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
+      schunk_gemv(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv,
+                  (F.l2hint & 1) ? l2pol_first() : l2pol_normal());
       if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
       for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
     } else if (type == 3) {
@@ -1551,6 +1594,7 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
   __shared__ double colv[512];
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
   const int tid = threadIdx.x;
+  const uint64_t pol = (F.l2hint & 1) ? l2pol_first() : l2pol_normal();
   for (int64_t idx = c_begin + blockIdx.x; idx < c_end; idx += gridDim.x) {
     const int bI = F.xt_bI[idx], bK = F.xt_bK[idx], nK = F.xt_nK[idx];
     const int J = F.blk_sn[bI];
@@ -1569,7 +1613,7 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
     }
     __syncthreads();
     const int64_t ldx = F.sn_ldx[J];
-    schunk_gemv<U>(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv);
+    schunk_gemv<U>(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
     if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
     for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
   }
@@ -1631,18 +1675,20 @@ __global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_fl
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rc0 = F.fl_rc0, wr = F.N - rc0;
   const int64_t total = nY + (wr + 7) / 8;
+  const uint64_t pol = (F.l2hint & 2) ? l2pol_last() : l2pol_normal();
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
     if (t < nY) {
       const int64_t c = t * 8 + wid;
       if (c < rc0) {
         const double bc = F.acc[c];
-        for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32)
-          atomicAdd(F.vbuf + F.fl_ci[e], F.fl_nval[e] * bc);
+        const int64_t e1 = ldg_pol(F.fl_cp + c + 1, pol);
+        for (int64_t e = ldg_pol(F.fl_cp + c, pol) + lane; e < e1; e += 32)
+          atomicAdd(F.vbuf + ldg_pol(F.fl_ci + e, pol), ldg_pol(F.fl_nval + e, pol) * bc);
       }
     } else {
       const int64_t r = (t - nY) * 8 + wid;
       if (r < wr) {
-        const int64_t e0 = F.fl_mr_ptr[r], e1 = F.fl_mr_ptr[r + 1];
+        const int64_t e0 = ldg_pol(F.fl_mr_ptr + r, pol), e1 = ldg_pol(F.fl_mr_ptr + r + 1, pol);
         double s = 0.0;
         for (int64_t e = e0 + lane; e < e1; e += 256) {   // 8 entries per lane in flight (predicated tail)
           double v[8];
@@ -1650,8 +1696,8 @@ __global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_fl
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const bool ok = e + 32 * u < e1;
-            v[u] = ok ? __ldg(F.fl_mr_val + e + 32 * u) : 0.0;
-            cc[u] = ok ? __ldg(F.fl_mr_col + e + 32 * u) : 0;
+            v[u] = ok ? ldg_pol(F.fl_mr_val + e + 32 * u, pol) : 0.0;
+            cc[u] = ok ? ldg_pol(F.fl_mr_col + e + 32 * u, pol) : 0;
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) s += v[u] * F.acc[cc[u]];
@@ -1680,6 +1726,7 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rc0 = F.fl_rc0, N = F.N;
   const int64_t total = F.fl_nmt + nX;
+  const uint64_t pol = (F.l2hint & 2) ? l2pol_last() : l2pol_normal();
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
     if (t < F.fl_nmt) {
       const int J = F.fl_mt_J[t], q0 = F.fl_mt_q0[t], nq = F.fl_mt_nq[t];
@@ -1688,7 +1735,7 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
       const int64_t nr = F.fl_roff[J + 1] - F.fl_roff[J];
       const int32_t* rows = F.fl_rows + F.fl_roff[J] + q0;
       __syncthreads();
-      for (int q = tid; q < nq; q += NT) xr[q] = x[rc0 + __ldg(rows + q)];   // nq ≤ 2·NT
+      for (int q = tid; q < nq; q += NT) xr[q] = x[rc0 + ldg_pol(rows + q, pol)];   // nq ≤ 2·NT
       __syncthreads();
       const double* Mj = F.fl_mval + F.fl_moff[J] + q0;
       for (int c = wid; c < w; c += NT / 32) {
@@ -1697,7 +1744,7 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
         for (int q0 = lane; q0 < nq; q0 += 256) {   // predicated batches of 8 loads per lane
           double mv[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) mv[u] = q0 + 32 * u < nq ? __ldg(Mc + q0 + 32 * u) : 0.0;
+          for (int u = 0; u < 8; ++u) mv[u] = q0 + 32 * u < nq ? ldg_pol(Mc + q0 + 32 * u, pol) : 0.0;
 #pragma unroll
           for (int u = 0; u < 8; ++u) s += q0 + 32 * u < nq ? mv[u] * xr[q0 + 32 * u] : 0.0;
         }
@@ -1708,9 +1755,10 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
       const int64_t c = (t - F.fl_nmt) * 8 + wid;
       if (c < rc0) {
         double u = 0.0;
-        for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32) {
-          const int32_t i = F.fl_ci[e];
-          u += F.fl_nval[e] * F.vbuf[i] / F.Dpiv[i];
+        const int64_t e1 = ldg_pol(F.fl_cp + c + 1, pol);
+        for (int64_t e = ldg_pol(F.fl_cp + c, pol) + lane; e < e1; e += 32) {
+          const int32_t i = ldg_pol(F.fl_ci + e, pol);
+          u += ldg_pol(F.fl_nval + e, pol) * F.vbuf[i] / F.Dpiv[i];
         }
         u = warp_sum(u);
         if (lane == 0) atomicAdd(x + c, u);
@@ -2020,6 +2068,81 @@ __global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z,
   const double beta = st->beta;
   for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < m2; i += (int64_t)gridDim.x * NT)
     p[i] = z[i] + beta * p[i];
+}
+
+// Fused PCG tail for P_L / no preconditioner on one GPU (a5 + a6 in one cooperative launch):
+//   q = D∘p − C·w, pᵀq  | grid sync |  α = ρ/pᵀq, x += αp, r −= αq, z = M⁻¹r, ‖r‖², rᵀz  | grid sync |
+//   convergence test, β = ρ'/ρ, p = z + βp.
+// The per-block partials are those of k_kf_q / k_pcg_update1 (same grid, same order), and every block
+// reduces them itself with reduce_partials, so all blocks take the same decision without another
+// round trip and the result is bit-identical to the three-kernel sequence; block 0 writes the state.
+// Phase A's partials live in partial[0, G), phase B's in partial[G, 3G), so no block overwrites a
+// partial another block is still reading.
+__global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const double* D, double* p, const double* w,
+                                                 double* q, double* x, double* r, double* z, double* partial,
+                                                 PcgState* st) {
+  __shared__ double sh[32];
+  if (*((volatile int*)&st->done)) return;   // every block reads the flag before the first grid sync
+  cg::grid_group grid = cg::this_grid();
+  const double rho = st->rho, tol2 = st->tol2, bnorm2 = st->bnorm2;
+  const int iter = st->iter, maxit = st->maxit;
+  const int64_t m2 = Cf.nrows, G = gridDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = G * NT;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  double loc = 0.0;
+  for (int64_t i = i0; i < m2; i += stride) {
+    const double pi = p[i];
+    const double qi = D[i] * pi - csr_dot(Cf, i, w);
+    q[i] = qi;
+    loc += pi * qi;
+  }
+  double v = block_reduce<0>(loc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  grid.sync();
+  const double pq = reduce_partials<0>(partial, (int)G, sh);
+  if (leader) fin_pcg_pq(st, pq);
+  if (!(pq > 0.0) || !isfinite(pq)) return;   // breakdown: fin_pcg_pq set status and done
+  const double alpha = rho / pq;
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = i0; i < m2; i += stride) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    rr += ri * ri;
+    const double zi = prec == 1 ? ri / D[i] : ri;
+    z[i] = zi;
+    rz += ri * zi;
+  }
+  const double v1 = block_reduce<0>(rr, sh);
+  const double v2 = block_reduce<0>(rz, sh);
+  if (threadIdx.x == 0) {
+    partial[G + blockIdx.x] = v1;
+    partial[2 * G + blockIdx.x] = v2;
+  }
+  grid.sync();
+  const double s1 = reduce_partials<0>(partial + G, (int)G, sh);
+  const double s2 = reduce_partials<0>(partial + 2 * G, (int)G, sh);
+  if (leader) fin_pcg_upd1(st, s1, s2, prec);
+  // the same decision as fin_pcg_upd1, from the values read at entry
+  if (!isfinite(s1) || s1 <= tol2 * bnorm2 || iter + 1 >= maxit) return;
+  const double beta = s2 / rho;
+  for (int64_t i = i0; i < m2; i += stride) p[i] = z[i] + beta * p[i];
+}
+
+bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const double* w, double* q, double* x,
+              double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s) {
+  static int max_grid = -1;
+  if (max_grid < 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_step, NT, 0);
+    max_grid = sms * occ;
+  }
+  if (grid > max_grid) return false;   // not co-resident: the caller runs the three-kernel sequence
+  DevCSR C = Cf;
+  void* args[] = {&C, &prec, &D, &p, &w, &q, &x, &r, &z, &partial, &st};
+  return cudaLaunchCooperativeKernel((const void*)k_pcg_step, grid, NT, args, 0, s) == cudaSuccess;
 }
 
 void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,

@@ -121,6 +121,8 @@ struct DevFactor {
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
   int sweep_var;      // A/B switch (QPB_SWEEP_VAR, default 1): bit 0 = backward long tiles two rows per lane
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
+  int l2hint;         // A/B switch (QPB_L2HINT, default 0 = measured best): bit 0 = root GEMV streams S⁻¹ with L2::evict_first,
+                      // bit 1 = flattened-forest arrays loaded with L2::evict_last (kept across F-solves)
 };
 
 // CSR on the device (int64 row pointers, int32 columns).
@@ -224,6 +226,9 @@ void pcg_update1(int prec, int64_t m2, const double* D, const double* p, const d
 void pcg_rz_ph(int64_t m2, const double* r, const double* z, double* partial, PcgState* st, int grid,
                cudaStream_t s);
 void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid, cudaStream_t s);
+// Fused a5 + a6 (P_L / none, unsharded): cooperative launch; false if it could not be launched.
+bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const double* w, double* q, double* x,
+              double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s);
 
 void gather(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
 void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
