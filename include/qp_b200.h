@@ -257,6 +257,15 @@ int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
  * Returns the number of records, or a negative qp_status. */
 int64_t qp_debug_sweep_trace(qp_ctx* ctx, int32_t sweep, int64_t* out, int64_t cap);
 
+/* Debug: launch timeline of the instrumented kernels (0 flat rhs, 1 flat forward, 2 root GEMV,
+ * 3 flat backward, 4 fused PCG step, 5 forward sweep, 6 backward sweep, 7 SpMV).  enable = 1
+ * resets the device buffer and turns recording on (kernels read the switch at run time, so
+ * captured CUDA graphs are recorded too); enable = 0 turns it off and copies
+ * min(cap, W) uint64 words to out (host, caller-owned), W = 2*8 + 2*8*256:
+ * [8 launch counters][8 scratch][8][256] earliest block start, [8][256] latest block end
+ * (globaltimer ns; ring slot = launch number mod 256).  Returns W or a negative qp_status. */
+int64_t qp_debug_timeline(qp_ctx* ctx, int32_t enable, int64_t* out, int64_t cap);
+
 /* Host-only: the contiguous split of m2 rows (CSR indptr, m2+1 entries) over
  * `world` ranks balancing nnz+1 per row; bounds (caller-owned, world+1 entries)
  * receives row offsets, bounds[0] = 0, bounds[world] = m2.  Deterministic. */

@@ -115,6 +115,8 @@ def load_library(build: bool = True):
     lib.qp_debug_sweep_profile.argtypes = [vp, i32, vp]
     lib.qp_debug_sweep_trace.argtypes = [vp, i32, vp, i64]
     lib.qp_debug_sweep_trace.restype = i64
+    lib.qp_debug_timeline.argtypes = [vp, i32, vp, i64]
+    lib.qp_debug_timeline.restype = i64
     lib.qp_ipm_last_system.argtypes = [vp, vp, vp, C.POINTER(dbl)]
     lib.qp_launch_count.argtypes = [vp]
     lib.qp_launch_count.restype = i64
@@ -349,6 +351,26 @@ class QPSolver:
         if n < 0:
             self._check(n)
         return out[:n]
+
+    def debug_timeline(self, enable):
+        """enable=True: start recording; enable=False: stop and return a list of (kernel, start_ns, end_ns)
+        per recorded launch, sorted by start (kernels: 0 flat rhs … 7 SpMV, include/qp_b200.h)."""
+        K, R = 8, 256
+        W = 2 * K + 2 * K * R
+        if enable:
+            rc = int(self.lib.qp_debug_timeline(self.ctx, 1, None, 0))
+            if rc < 0:
+                self._check(rc)
+            return None
+        out = np.zeros(W, dtype=np.uint64)
+        rc = int(self.lib.qp_debug_timeline(self.ctx, 0, out.ctypes.data, W))
+        if rc < 0:
+            self._check(rc)
+        st = out[2 * K:2 * K + K * R].reshape(K, R)
+        en = out[2 * K + K * R:].reshape(K, R)
+        ev = [(k, int(st[k, s]), int(en[k, s])) for k in range(K) for s in range(R)
+              if st[k, s] != np.uint64(2**64 - 1) and en[k, s] != 0]
+        return sorted(ev, key=lambda e: e[1])
 
     def ipm_last_system(self):
         D, r = np.zeros(self.m2), np.zeros(self.m2)

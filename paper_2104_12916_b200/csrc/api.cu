@@ -282,6 +282,7 @@ struct qp_ctx {
   double *px = nullptr, *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *xph = nullptr;
   double *vin = nullptr, *vin2 = nullptr, *vout = nullptr;  // staging for host I/O
   double* partial = nullptr;
+  unsigned long long* tl_buf = nullptr;   // qp_debug_timeline
   PcgState* pst = nullptr;
   IpmState* ist = nullptr;
   PcgState* h_pst = nullptr;  // pinned
@@ -361,6 +362,10 @@ struct qp_ctx {
       if (g) cudaGraphExecDestroy(g);
     for (auto e : pool) cudaEventDestroy(e);
     if (h_pst) cudaFreeHost(h_pst);
+    if (tl_buf) {
+      timeline_enable(nullptr);
+      cudaFree(tl_buf);
+    }
     if (h_ist) cudaFreeHost(h_ist);
     FF.mem.release();
     FP.mem.release();
@@ -500,6 +505,22 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
       d.fl_mr_ptr = m.upload(S.fl_mr_ptr, st);
       d.fl_mr_col = m.upload(S.fl_mr_col, st);
       d.fl_mr_val = m.zeros<double>(S.fl_mr_col.size(), st);
+      std::vector<int32_t> units;   // 8 int32 per unit: moff lo, moff hi, roff, col0, ld, rows | cols << 16, 0, 0
+      for (size_t t = 0; t < S.fl_mt_J.size(); ++t) {
+        const int64_t J = S.fl_mt_J[t], q0 = S.fl_mt_q0[t], nq = S.fl_mt_nq[t];
+        const int64_t c0 = S.sn_start[J], w = S.sn_start[J + 1] - c0, nr = S.fl_roff[J + 1] - S.fl_roff[J];
+        for (int64_t cg = 0; cg < w; cg += 8)
+          for (int64_t rg = 0; rg < nq; rg += 64) {
+            const int64_t mo = S.fl_moff[J] + cg * nr + q0 + rg;
+            units.insert(units.end(), {(int32_t)(uint32_t)(mo & 0xffffffffll), (int32_t)(mo >> 32),
+                                       (int32_t)(S.fl_roff[J] + q0 + rg), (int32_t)(c0 + cg), (int32_t)nr,
+                                       (int32_t)(std::min<int64_t>(64, nq - rg) | (std::min<int64_t>(8, w - cg) << 16)),
+                                       0, 0});
+          }
+      }
+      d.fl_nunits = (int64_t)units.size() / 8;
+      d.fl_units = reinterpret_cast<const int4*>(m.upload(units, st));
+      cudaStreamSynchronize(st);   // `units` is a local host buffer
     }
     d.ready_sb = m.zeros<unsigned int>(S.ns, st);
     d.sn_done_b = m.zeros<unsigned long long>(S.ns, st);
@@ -811,12 +832,17 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   // k_pcg_update1, k_pcg_update2 — bit-identical results)
   static const bool fused_env = !(std::getenv("QPB_FUSED_PCG") && std::getenv("QPB_FUSED_PCG")[0] == '0');
   const bool fused = fused_env && prec != 2 && !c->sharded;
+  // its grid: whole multiples of the SM count, about two rows of m2 per thread (fewer blocks make the two
+  // grid syncs and the per-block partial sums cheaper on small m2), at most the vector-kernel grid
+  const int step_grid = (int)std::min<int64_t>(
+      c->vgrid, (int64_t)c->sm_count * std::max<int64_t>(1, (m2 + (int64_t)c->sm_count * 512 - 1) /
+                                                                 ((int64_t)c->sm_count * 512)));
   auto body = [&]() -> int {
     if (fused) {
       if (int rc = kf_apply_dev(c, D, c->pp, c->pq, true, true)) return rc;
       int hh = c->begin(2);
       const bool ok = pcg_step(c->Cf, prec, D, c->pp, c->xbuf, c->pq, c->px, c->pr, c->pz, c->partial, c->pst,
-                               c->vgrid, st);
+                               step_grid, st);
       c->end(hh);
       c->launches += 1;
       if (ok) return 0;
@@ -1493,6 +1519,21 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     Factor& F = c->FF;
     const char* fe = std::getenv("QPB_FLAT");
     if (F.S.flat && F.sym_enabled && !(fe && fe[0] == '0')) {
+      if (std::getenv("QPB_VERBOSE")) {   // M-tile shape statistics
+        const auto& S = F.S;
+        int64_t ent = 0, warps = 0, hist[5] = {0, 0, 0, 0, 0};
+        for (size_t t = 0; t < S.fl_mt_J.size(); ++t) {
+          const int64_t J = S.fl_mt_J[t], w = S.sn_start[J + 1] - S.sn_start[J], nq = S.fl_mt_nq[t];
+          ent += w * nq;
+          warps += (nq + 63) / 64;
+          hist[w <= 2 ? 0 : w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 3 : 4]++;
+        }
+        std::fprintf(stderr, "qpb: flat %lld units; ", (long long)F.d.fl_nunits);
+        std::fprintf(stderr, "qpb: flat rc0 %lld, %zu M tiles, %lld entries, %.2f busy warps per tile, "
+                     "w<=2/8/16/32/64: %lld %lld %lld %lld %lld tiles\n", (long long)S.fl_rc0, S.fl_mt_J.size(),
+                     (long long)ent, S.fl_mt_J.empty() ? 0.0 : (double)warps / S.fl_mt_J.size(), (long long)hist[0],
+                     (long long)hist[1], (long long)hist[2], (long long)hist[3], (long long)hist[4]);
+      }
       cudaMemsetAsync(c->rhs2, 0, N * 8, st);
       SweepRhs ur{};
       ur.rhs = c->rhs2;
@@ -1948,6 +1989,32 @@ int64_t qp_debug_sweep_trace(qp_ctx* c, int32_t sweep, int64_t* out, int64_t cap
     cudaMemcpyAsync(out, F.tprof_buf + 80 + sweep * F.d.ttrace_cap * 6, n * 48, cudaMemcpyDeviceToHost, c->stream);
   int st = sync_check(c, "qp_debug_sweep_trace");
   return st != QP_OK ? st : n;
+}
+
+// Debug: launch timeline of the instrumented kernels (kernels.cuh TL_K / TL_RING).  enable = 1 allocates
+// (once), resets and turns it on; enable = 0 copies the buffer to out (host, 2·TL_K + 2·TL_K·TL_RING uint64)
+// and turns it off.  Returns the number of words, or a negative status.
+int64_t qp_debug_timeline(qp_ctx* c, int32_t enable, int64_t* out, int64_t cap) {
+  if (!c) return QP_EINVAL;
+  const int64_t words = 2 * TL_K + 2 * (int64_t)TL_K * TL_RING;
+  if (enable) {
+    if (!c->tl_buf) {
+      if (cudaMalloc(&c->tl_buf, words * 8) != cudaSuccess) return fail(c, QP_ENOMEM, "timeline buffer");
+    }
+    std::vector<unsigned long long> init(words, 0ull);
+    for (int64_t i = 2 * TL_K; i < 2 * TL_K + (int64_t)TL_K * TL_RING; ++i) init[i] = ~0ull;
+    cudaMemcpyAsync(c->tl_buf, init.data(), words * 8, cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);
+    timeline_enable(c->tl_buf);
+    int st = sync_check(c, "qp_debug_timeline");
+    return st != QP_OK ? st : words;
+  }
+  if (!c->tl_buf) return QP_ESTATE;
+  cudaStreamSynchronize(c->stream);
+  timeline_enable(nullptr);
+  if (out) cudaMemcpy(out, c->tl_buf, std::min(cap, words) * 8, cudaMemcpyDeviceToHost);
+  int st = sync_check(c, "qp_debug_timeline");
+  return st != QP_OK ? st : words;
 }
 
 int qp_partition_rows(const int64_t* indptr, int64_t m2, int32_t world, int64_t* bounds) {

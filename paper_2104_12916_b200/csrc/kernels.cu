@@ -474,6 +474,33 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Launch timeline (debug, qp_debug_timeline): for instrumented kernel k and ring slot s = its launch
+// number mod TL_RING, the earliest block start and the latest block end (globaltimer ns), so the host can
+// rebuild the per-launch durations AND the gaps between dependent launches (inside CUDA graphs too).
+// Layout of g_tl: [TL_K launch counters][TL_K arrival counters][TL_K][TL_RING] starts, [TL_K][TL_RING] ends.
+__device__ unsigned long long* g_tl = nullptr;
+__device__ __forceinline__ unsigned tl_begin(int k) {
+  unsigned long long* t = g_tl;
+  if (t == nullptr || threadIdx.x != 0) return 0;
+  const unsigned s = (unsigned)(*((volatile unsigned long long*)(t + k)) % TL_RING);
+  atomicMin(t + 2 * TL_K + k * TL_RING + s, gtime());
+  return s;
+}
+__device__ __forceinline__ void tl_end(int k, unsigned s) {
+  unsigned long long* t = g_tl;
+  if (t == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  atomicMax(t + 2 * TL_K + TL_K * TL_RING + k * TL_RING + s, gtime());
+  __threadfence();
+  if (atomicAdd(t + TL_K + k, 1ull) == gridDim.x - 1) {
+    t[TL_K + k] = 0;
+    __threadfence();
+    atomicAdd(t + k, 1ull);
+  }
+}
+void timeline_enable(unsigned long long* buf) { cudaMemcpyToSymbol(g_tl, &buf, sizeof(buf)); }
+
 // instrumentation: per sweep (0 fwd, 1 bwd) and task type: count, wait ns, busy ns, first start, last end
 __device__ __forceinline__ unsigned smid() {
   unsigned r;
@@ -872,6 +899,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
   if (tid == 0) S.epoch = *((volatile unsigned*)(F.sweep + 2)) + 1u;
   __syncthreads();
   const unsigned E = S.epoch;
+  const unsigned tls = tl_begin(5);
   while (true) {
     if (tid == 0) {
       unsigned t = atomicAdd(F.sweep + 0, 1u);
@@ -1138,6 +1166,7 @@ __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double
       __threadfence();
     }
   }
+  tl_end(5, tls);
 }
 
 // Backward sweep Lᵀ x = D⁻¹ y (in place in x).
@@ -1149,6 +1178,7 @@ __global__ void __launch_bounds__(NT, 4) k_trsv_bwd(DevFactor F, double* x, cons
   if (tid == 0) S.epoch = *((volatile unsigned*)(F.sweep + 3)) + 1u;
   __syncthreads();
   const unsigned E = S.epoch;
+  const unsigned tls = tl_begin(6);
   while (true) {
     if (tid == 0) {
       unsigned t = atomicAdd(F.sweep + 0, 1u);
@@ -1417,6 +1447,7 @@ __global__ void __launch_bounds__(NT, 4) k_trsv_bwd(DevFactor F, double* x, cons
       __threadfence();
     }
   }
+  tl_end(6, tls);
 }
 
 // ------------------------------------------------------------------------- partitioned inverse
@@ -1593,6 +1624,7 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
   __shared__ double red[576];
   __shared__ double colv[512];
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(2);
   const int tid = threadIdx.x;
   const uint64_t pol = (F.l2hint & 1) ? l2pol_first() : l2pol_normal();
   for (int64_t idx = c_begin + blockIdx.x; idx < c_end; idx += gridDim.x) {
@@ -1603,6 +1635,8 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
     const int Rn = F.blk_w[bI];
     const int ncol = (int)(F.blk_col0[bK + nK - 1] + F.blk_w[bK + nK - 1] - cK);
     const int ncol_t = (int)((rI < cK + ncol ? rI : cK + ncol) - cK);
+    const int64_t ldx = F.sn_ldx[J];
+    const double* Mc = F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx;
     __syncthreads();
     if (sub != nullptr) {
       for (int c = tid; c < ncol; c += NT) vK[c] = F.vbuf[cK + c] - sub[cK + c];
@@ -1612,11 +1646,11 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
       if (tid < Rn) vI[tid] = F.vbuf[rI + tid];
     }
     __syncthreads();
-    const int64_t ldx = F.sn_ldx[J];
-    schunk_gemv<U>(F.xinv + F.sn_sinv[J] + (rI - cJ) + (cK - cJ) * ldx, ldx, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
+    schunk_gemv<U>(Mc, ldx, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
     if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
     for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
   }
+  tl_end(2, tls);
 }
 
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
@@ -1641,6 +1675,7 @@ void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end,
 // → acc[0, rc0) (b1), root columns → vbuf (the root GEMV's right-hand side before − M b1); x = 0.
 __global__ void __launch_bounds__(NT) k_flat_rhs(DevFactor F, SweepRhs R, double* x) {
   if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const unsigned tls = tl_begin(0);
   const int lane = threadIdx.x & 31;
   const int64_t rc0 = F.fl_rc0, N = F.N;
   for (int64_t c = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 5; c < N; c += ((int64_t)gridDim.x * NT) >> 5) {
@@ -1665,16 +1700,17 @@ __global__ void __launch_bounds__(NT) k_flat_rhs(DevFactor F, SweepRhs R, double
       x[c] = 0.0;
     }
   }
+  tl_end(0, tls);
 }
 
 // Forward product: tasks [0, nY) — 8 forest columns each (warp per column c), vbuf[rows of L11⁻¹(:,c)]
 // += L11⁻¹(:,c) b1_c (y1 = L11⁻¹ b1; vbuf[0, rc0) zeroed by k_flat_rhs); tasks [nY, nY + nRr) — 8 root
 // rows each (warp per row r): vbuf[r] = b2_r − M(r,:) b1, a fixed-order dot product (no atomics).
-__global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_flag, int64_t nY) {
+__global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_flag, int64_t nY, int64_t total) {
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(1);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rc0 = F.fl_rc0, wr = F.N - rc0;
-  const int64_t total = nY + (wr + 7) / 8;
   const uint64_t pol = (F.l2hint & 2) ? l2pol_last() : l2pol_normal();
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
     if (t < nY) {
@@ -1707,6 +1743,127 @@ __global__ void __launch_bounds__(NT) k_flat_fwd(DevFactor F, const int* done_fl
       }
     }
   }
+  tl_end(1, tls);
+}
+
+// ---- M products by units (QPB_FLAT_TILES=1, default).  M_J (nr rows × w columns, column-major) is cut into
+// units of ≤ 64 rows × ≤ 8 columns, each described by 32 bytes built once at setup (fl_units: offset of
+// its first entry, offset of its row indices, first column, leading dimension, rows | columns << 16).
+// Warps take units grid-stride (about two per warp on c1), so a unit costs one descriptor load, one
+// round of matrix / row-index loads (two rows per lane, 8 columns in flight) and, backward, one gather.
+// Forward: s_r = Σ_c M(r,c) b1_c, one atomic per row into the root right-hand side.  Backward:
+// x_c −= Σ_r M(r,c) x_root(r): the 8 column partials combined by a transpose-reduce (4+2+1+1+1 shuffles),
+// one atomic per column and unit.  Forest columns (L11⁻¹ products) follow as warp-per-column units.
+// Transpose-reduce of 8 per-lane values over a warp: returns the warp sum of t[lane >> 2] in every lane
+// with (lane & 3) == 0.
+__device__ __forceinline__ double transpose_reduce8(const double (&t)[8], int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  double a4[4], a2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a4[i] = (h16 ? t[i + 4] : t[i]) + __shfl_xor_sync(0xffffffffu, h16 ? t[i] : t[i + 4], 16);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) a2[i] = (h8 ? a4[i + 2] : a4[i]) + __shfl_xor_sync(0xffffffffu, h8 ? a4[i] : a4[i + 2], 8);
+  double a1 = (h4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? a2[0] : a2[1], 4);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+  return a1;
+}
+
+struct FlatUnit {
+  int64_t moff;
+  int32_t roff, col0, ld, shape;
+};
+__device__ __forceinline__ FlatUnit load_unit(const int4* U, int64_t u) {
+  const int4 a = __ldg(U + 2 * u), b = __ldg(U + 2 * u + 1);
+  FlatUnit f;
+  f.moff = (int64_t)(uint32_t)a.x | ((int64_t)a.y << 32);
+  f.roff = a.z;
+  f.col0 = a.w;
+  f.ld = b.x;
+  f.shape = b.y;
+  return f;
+}
+
+__global__ void __launch_bounds__(NT) k_flat_fwd_t(DevFactor F, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(1);
+  const int lane = threadIdx.x & 31;
+  const int64_t rc0 = F.fl_rc0, nu = F.fl_nunits, total = nu + rc0;
+  const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+  for (int64_t u = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); u < total; u += nw) {
+    if (u < nu) {
+      const FlatUnit f = load_unit(F.fl_units, u);
+      const int nrows = f.shape & 0xffff, ncols = f.shape >> 16;
+      if (lane >= nrows) continue;
+      const bool okb = lane + 32 < nrows;
+      const int32_t ia = __ldg(F.fl_rows + f.roff + lane), ib = okb ? __ldg(F.fl_rows + f.roff + lane + 32) : 0;
+      const double* Mu = F.fl_mval + f.moff;
+      double ma[8], mb[8], bv[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const bool okc = c < ncols;
+        ma[c] = okc ? __ldg(Mu + (int64_t)c * f.ld + lane) : 0.0;
+        mb[c] = okc && okb ? __ldg(Mu + (int64_t)c * f.ld + lane + 32) : 0.0;
+        bv[c] = okc ? F.acc[f.col0 + c] : 0.0;
+      }
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        sa = fma(ma[c], bv[c], sa);
+        sb = fma(mb[c], bv[c], sb);
+      }
+      atomicAdd(F.vbuf + rc0 + ia, -sa);
+      if (okb) atomicAdd(F.vbuf + rc0 + ib, -sb);
+    } else {   // forest column c: y1[rows of L11⁻¹(:, c)] += L11⁻¹(:, c) b1_c
+      const int64_t c = u - nu;
+      const double bc = F.acc[c];
+      const int64_t e1 = F.fl_cp[c + 1];
+      for (int64_t e = F.fl_cp[c] + lane; e < e1; e += 32) atomicAdd(F.vbuf + F.fl_ci[e], F.fl_nval[e] * bc);
+    }
+  }
+  tl_end(1, tls);
+}
+
+__global__ void __launch_bounds__(NT) k_flat_bwd_t(DevFactor F, double* x, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(3);
+  const int lane = threadIdx.x & 31;
+  const int64_t rc0 = F.fl_rc0, nu = F.fl_nunits, total = nu + rc0;
+  const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+  for (int64_t u = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); u < total; u += nw) {
+    if (u < nu) {   // warp-uniform branch: the shuffles below need all 32 lanes
+      const FlatUnit f = load_unit(F.fl_units, u);
+      const int nrows = f.shape & 0xffff, ncols = f.shape >> 16;
+      const bool oka = lane < nrows, okb = lane + 32 < nrows;
+      const int32_t ia = oka ? __ldg(F.fl_rows + f.roff + lane) : 0;
+      const int32_t ib = okb ? __ldg(F.fl_rows + f.roff + lane + 32) : 0;
+      const double* Mu = F.fl_mval + f.moff;
+      double ma[8], mb[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const bool okc = c < ncols;
+        ma[c] = okc && oka ? __ldg(Mu + (int64_t)c * f.ld + lane) : 0.0;
+        mb[c] = okc && okb ? __ldg(Mu + (int64_t)c * f.ld + lane + 32) : 0.0;
+      }
+      const double xa = oka ? x[rc0 + ia] : 0.0, xb = okb ? x[rc0 + ib] : 0.0;
+      double tt[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tt[c] = ma[c] * xa + mb[c] * xb;
+      const double s = transpose_reduce8(tt, lane);
+      const int col = lane >> 2;
+      if ((lane & 3) == 0 && col < ncols) atomicAdd(x + f.col0 + col, -s);
+    } else {   // forest column c: x_c += Σ_i L11⁻¹(i, c) y1_i / d_i
+      const int64_t c = u - nu;
+      double v = 0.0;
+      for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32) {
+        const int32_t i = F.fl_ci[e];
+        v += F.fl_nval[e] * F.vbuf[i] / F.Dpiv[i];
+      }
+      v = warp_sum(v);
+      if (lane == 0) atomicAdd(x + c, v);
+    }
+  }
+  tl_end(3, tls);
 }
 
 __global__ void k_flat_fill_rows(DevFactor F, const int32_t* src, int64_t nnz) {
@@ -1720,14 +1877,15 @@ void flat_fill_rows(const DevFactor& F, const int32_t* src, int64_t nnz, cudaStr
 // Backward product: the M tiles — x[cols of J] −= M_J(tile)ᵀ x_root(tile rows) (root values gathered
 // once per tile into shared memory, warp per column); tasks [nmt, nmt + nX): 8 forest columns each,
 // x_c += Σ_i L11⁻¹(i,c) y1_i / d_i.  x[0, rc0) was zeroed by k_flat_rhs.
-__global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const int* done_flag, int64_t nX) {
+__global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const int* done_flag, int64_t nX, int64_t t0) {
   __shared__ double xr[512];
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(3);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rc0 = F.fl_rc0, N = F.N;
   const int64_t total = F.fl_nmt + nX;
   const uint64_t pol = (F.l2hint & 2) ? l2pol_last() : l2pol_normal();
-  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+  for (int64_t t = t0 + blockIdx.x; t < total; t += gridDim.x) {
     if (t < F.fl_nmt) {
       const int J = F.fl_mt_J[t], q0 = F.fl_mt_q0[t], nq = F.fl_mt_nq[t];
       const int64_t c0 = F.sn_start[J];
@@ -1765,6 +1923,7 @@ __global__ void __launch_bounds__(NT) k_flat_bwd(DevFactor F, double* x, const i
       }
     }
   }
+  tl_end(3, tls);
 }
 
 // Extraction of forest column `col` after a forward sweep with rhs = e_col (symmetric-root mode):
@@ -1788,14 +1947,34 @@ __global__ void k_set_unit(double* unit, int64_t col) { unit[col] = 1.0; }
 void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
   const int g0 = (int)std::max<int64_t>(1, std::min<int64_t>((F.N * 32 + NT - 1) / NT, (int64_t)sms * 8));
   k_flat_rhs<<<g0, NT, 0, s>>>(F, r, x);
-  const int64_t nY = (F.fl_rc0 + 7) / 8, nRr = (F.N - F.fl_rc0 + 7) / 8;
+  static const bool tiles = !(std::getenv("QPB_FLAT_TILES") && std::getenv("QPB_FLAT_TILES")[0] == '0');
+  if (tiles) {
+    const int64_t nwarps = F.fl_nunits + F.fl_rc0;
+    const int gt = (int)std::max<int64_t>(1, std::min<int64_t>((nwarps + 7) / 8, (int64_t)sms * 8));
+    k_flat_fwd_t<<<gt, NT, 0, s>>>(F, r.done_flag);
+    return;
+  }
+  const int skip = std::getenv("QPB_FLAT_SKIP") ? std::atoi(std::getenv("QPB_FLAT_SKIP")) : 0;  // TEMP
+  int64_t nY = (F.fl_rc0 + 7) / 8, nRr = (F.N - F.fl_rc0 + 7) / 8;
+  if (skip & 1) nY = 0;
+  if (skip & 2) nRr = 0;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nY + nRr, (int64_t)sms * 8));
-  k_flat_fwd<<<grid, NT, 0, s>>>(F, r.done_flag, nY);
+  if (nY + nRr > 0) k_flat_fwd<<<grid, NT, 0, s>>>(F, r.done_flag, nY, nY + nRr);
 }
 void flat_backward(const DevFactor& F, double* x, const int* done_flag, int sms, cudaStream_t s) {
-  const int64_t nX = (F.fl_rc0 + 7) / 8;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(F.fl_nmt + nX, 1), (int64_t)sms * 8));
-  k_flat_bwd<<<grid, NT, 0, s>>>(F, x, done_flag, nX);
+  static const bool tiles = !(std::getenv("QPB_FLAT_TILES") && std::getenv("QPB_FLAT_TILES")[0] == '0');
+  if (tiles) {
+    const int64_t nwarps = F.fl_nunits + F.fl_rc0;
+    const int gt = (int)std::max<int64_t>(1, std::min<int64_t>((nwarps + 7) / 8, (int64_t)sms * 8));
+    k_flat_bwd_t<<<gt, NT, 0, s>>>(F, x, done_flag);
+    return;
+  }
+  const int skip = std::getenv("QPB_FLAT_SKIP") ? std::atoi(std::getenv("QPB_FLAT_SKIP")) : 0;  // TEMP
+  int64_t nX = (F.fl_rc0 + 7) / 8;
+  if (skip & 4) nX = 0;
+  const int64_t t0 = (skip & 8) ? F.fl_nmt : 0;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(F.fl_nmt + nX - t0, 1), (int64_t)sms * 8));
+  if (F.fl_nmt + nX - t0 > 0) k_flat_bwd<<<grid, NT, 0, s>>>(F, x, done_flag, nX, t0);
 }
 void flat_extract(const DevFactor& F, int64_t col, const double* x, double* unit, int64_t prev, cudaStream_t s) {
   k_flat_extract<<<8, NT, 0, s>>>(F, col, x, unit, prev);
@@ -1904,8 +2083,10 @@ void finalize(int kind, PcgState* ps, IpmState* is, int prec, cudaStream_t s) {
 
 __global__ void k_spmv(DevCSR M, const double* x, double* y, const int* done) {
   if (done != nullptr && *((volatile const int*)done)) return;
+  const unsigned tls = tl_begin(7);
   for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < M.nrows; i += (int64_t)gridDim.x * NT)
     y[i] = csr_dot(M, i, x);
+  tl_end(7, tls);
 }
 void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid, cudaStream_t s) {
   k_spmv<<<grid, NT, 0, s>>>(M, x, y, done);
@@ -2084,6 +2265,7 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const doub
   __shared__ double sh[32];
   if (*((volatile int*)&st->done)) return;   // every block reads the flag before the first grid sync
   cg::grid_group grid = cg::this_grid();
+  const unsigned tls = tl_begin(4);
   const double rho = st->rho, tol2 = st->tol2, bnorm2 = st->bnorm2;
   const int iter = st->iter, maxit = st->maxit;
   const int64_t m2 = Cf.nrows, G = gridDim.x;
@@ -2101,7 +2283,10 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const doub
   grid.sync();
   const double pq = reduce_partials<0>(partial, (int)G, sh);
   if (leader) fin_pcg_pq(st, pq);
-  if (!(pq > 0.0) || !isfinite(pq)) return;   // breakdown: fin_pcg_pq set status and done
+  if (!(pq > 0.0) || !isfinite(pq)) {   // breakdown: fin_pcg_pq set status and done
+    tl_end(4, tls);
+    return;
+  }
   const double alpha = rho / pq;
   double rr = 0.0, rz = 0.0;
   for (int64_t i = i0; i < m2; i += stride) {
@@ -2124,9 +2309,13 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const doub
   const double s2 = reduce_partials<0>(partial + 2 * G, (int)G, sh);
   if (leader) fin_pcg_upd1(st, s1, s2, prec);
   // the same decision as fin_pcg_upd1, from the values read at entry
-  if (!isfinite(s1) || s1 <= tol2 * bnorm2 || iter + 1 >= maxit) return;
+  if (!isfinite(s1) || s1 <= tol2 * bnorm2 || iter + 1 >= maxit) {
+    tl_end(4, tls);
+    return;
+  }
   const double beta = s2 / rho;
   for (int64_t i = i0; i < m2; i += stride) p[i] = z[i] + beta * p[i];
+  tl_end(4, tls);
 }
 
 bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const double* w, double* q, double* x,

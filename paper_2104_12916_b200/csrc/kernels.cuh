@@ -116,6 +116,8 @@ struct DevFactor {
   const int64_t* fl_mr_ptr;       // M by root rows (forward product)
   const int32_t* fl_mr_col;
   double* fl_mr_val;
+  const int4* fl_units;           // M product units (≤ 64 rows × ≤ 8 columns), 2 × int4 each (k_flat_*_t)
+  int64_t fl_nunits;
   int mf_group;                   // pivot blocks per trailing UPDATE (Symbolic::mf_group)
   unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][8 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
@@ -226,6 +228,10 @@ void pcg_update1(int prec, int64_t m2, const double* D, const double* p, const d
 void pcg_rz_ph(int64_t m2, const double* r, const double* z, double* partial, PcgState* st, int grid,
                cudaStream_t s);
 void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid, cudaStream_t s);
+// Launch timeline instrumentation (debug): kernels 0 flat_rhs, 1 flat_fwd, 2 root GEMV, 3 flat_bwd,
+// 4 pcg_step, 5 trsv_fwd, 6 trsv_bwd, 7 spmv; buf = nullptr disables.
+constexpr int TL_K = 8, TL_RING = 256;
+void timeline_enable(unsigned long long* buf);
 // Fused a5 + a6 (P_L / none, unsharded): cooperative launch; false if it could not be launched.
 bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const double* w, double* q, double* x,
               double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s);
