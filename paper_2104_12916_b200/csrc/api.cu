@@ -283,6 +283,8 @@ struct qp_ctx {
   double *vin = nullptr, *vin2 = nullptr, *vout = nullptr;  // staging for host I/O
   double* partial = nullptr;
   unsigned long long* tl_buf = nullptr;   // qp_debug_timeline
+  const int32_t* long_c = nullptr;   // rows of C with > KF_LONG_ROW entries (k_pcg_step)
+  int64_t n_long_c = 0;
   PcgState* pst = nullptr;
   IpmState* ist = nullptr;
   PcgState* h_pst = nullptr;  // pinned
@@ -727,7 +729,7 @@ void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
 // forward product, root GEMV, backward product (three dependency-free kernels).
 void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
   Factor& F = c->FF;
-  c->launches += F.d.flat ? 3 : 2;
+  c->launches += F.d.flat ? (r.rhs_ready ? 2 : 3) : 2;
   int h = c->begin(0);
   if (F.d.flat) flat_forward(F.d, r, out, c->sm_count, c->stream);
   else trsv_forward(F.d, r, out, c->tgrid, c->stream);
@@ -748,12 +750,22 @@ void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
 }
 
 // q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
-int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode, bool fsolve_only = false) {
+static bool pregather_on() {
+  static const bool on = !(std::getenv("QPB_PREGATHER") && std::getenv("QPB_PREGATHER")[0] == '0');
+  return on;
+}
+
+// rhs_ready: the fused PCG step already prepared this F-solve's right-hand side (flat: acc / vbuf / xbuf;
+// pregather: ubuf).
+int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pcg_mode, bool fsolve_only = false,
+                 bool rhs_ready = false) {
   c->launches += fsolve_only ? 0 : 1;
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
-  static const bool pregather = !(std::getenv("QPB_PREGATHER") && std::getenv("QPB_PREGATHER")[0] == '0');
-  if (c->sharded || (pregather && !c->FF.d.flat)) {
+  r.rhs_ready = rhs_ready && c->FF.d.flat ? 1 : 0;
+  if (rhs_ready && !c->FF.d.flat) {
+    r.rhs = c->ubuf;
+  } else if (c->sharded || (pregather_on() && !c->FF.d.flat)) {
     // u = Σ_ranks C_gᵀ p_g (one coalesced SpMV before the sweeps: every sweep task then reads its
     // right-hand side with one load), then the replicated F-solve on [u; 0]
     spmv(c->Ctf, p, c->ubuf, r.done_flag, c->vgrid, c->stream);
@@ -767,7 +779,7 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
   f_solve_sweeps(c, r, c->xbuf);
   if (fsolve_only) return 0;   // q = D∘p − C w comes from the fused PCG step
   int h = c->begin(2);
-  kf_q(c->Cf, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
+  kf_q(c->Cf, c->long_c, c->n_long_c, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
   c->end(h);
   if (c->sharded && pcg_mode) {
     if (int rc = c->allreduce(pst_red(c), 1, 0)) return rc;
@@ -837,12 +849,26 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   const int step_grid = (int)std::min<int64_t>(
       c->vgrid, (int64_t)c->sm_count * std::max<int64_t>(1, (m2 + (int64_t)c->sm_count * 512 - 1) /
                                                                  ((int64_t)c->sm_count * 512)));
+  // phase D of the fused step prepares the next iteration's u = Cᵀp (flattened forest or pregathered
+  // sweeps); the first iteration's comes from the usual kernel
+  const int next_rhs = !fused ? 0 : c->FF.d.flat ? 1 : pregather_on() ? 2 : 0;
+  if (next_rhs == 1) {
+    SweepRhs r0{};
+    r0.ct = c->Ctf;
+    r0.p = c->pp;
+    r0.done_flag = &c->pst->done;
+    flat_rhs(c->FF.d, r0, c->xbuf, c->sm_count, st);
+    c->launches += 1;
+  } else if (next_rhs == 2) {
+    spmv(c->Ctf, c->pp, c->ubuf, &c->pst->done, c->vgrid, st);
+    c->launches += 1;
+  }
   auto body = [&]() -> int {
     if (fused) {
-      if (int rc = kf_apply_dev(c, D, c->pp, c->pq, true, true)) return rc;
+      if (int rc = kf_apply_dev(c, D, c->pp, c->pq, true, true, next_rhs != 0)) return rc;
       int hh = c->begin(2);
-      const bool ok = pcg_step(c->Cf, prec, D, c->pp, c->xbuf, c->pq, c->px, c->pr, c->pz, c->partial, c->pst,
-                               step_grid, st);
+      const bool ok = pcg_step(c->Cf, c->long_c, c->n_long_c, prec, D, c->pp, c->xbuf, c->pq, c->px, c->pr, c->pz,
+                               c->partial, c->pst, step_grid, st, next_rhs, &c->FF.d, &c->Ctf, c->xbuf, c->ubuf);
       c->end(hh);
       c->launches += 1;
       if (ok) return 0;
@@ -1432,6 +1458,14 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     c->Hf = upload_csr(c->mem, Hf, st);
     c->Af = upload_csr(c->mem, Af, st);
     c->Cf = upload_csr(c->mem, Cf, st);
+    {   // rows of C longer than 32 entries (power-law degrees, c3/c3s): warp per row in the fused PCG step
+      std::vector<int32_t> lr;
+      for (int64_t r = 0; r < Cf.nrows; ++r)
+        if (Cf.p[r + 1] - Cf.p[r] > KF_LONG_ROW) lr.push_back((int32_t)r);
+      c->n_long_c = (int64_t)lr.size();
+      c->long_c = c->mem.upload(lr, st);
+      cudaStreamSynchronize(st);
+    }
     c->Atf = upload_csr(c->mem, Atf, st);
     c->Ctf = upload_csr(c->mem, Ctf, st);
     std::vector<double> gf(n);

@@ -1944,9 +1944,12 @@ __global__ void k_flat_extract(DevFactor F, int64_t col, const double* x, double
 }
 __global__ void k_set_unit(double* unit, int64_t col) { unit[col] = 1.0; }
 
-void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
+void flat_rhs(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
   const int g0 = (int)std::max<int64_t>(1, std::min<int64_t>((F.N * 32 + NT - 1) / NT, (int64_t)sms * 8));
   k_flat_rhs<<<g0, NT, 0, s>>>(F, r, x);
+}
+void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
+  if (!r.rhs_ready) flat_rhs(F, r, x, sms, s);
   static const bool tiles = !(std::getenv("QPB_FLAT_TILES") && std::getenv("QPB_FLAT_TILES")[0] == '0');
   if (tiles) {
     const int64_t nwarps = F.fl_nunits + F.fl_rc0;
@@ -2094,17 +2097,54 @@ void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid
 
 // ------------------------------------------------------------------------- K_F product and PCG
 // q = D∘p − C_f·z (a5) with the pᵀq reduction; last block: α = ρ / pᵀq.
-__global__ void __launch_bounds__(NT) k_kf_q(DevCSR Cf, const double* D, const double* p, const double* z,
-                                             double* q, double* partial, PcgState* st, int pcg_mode) {
-  __shared__ double sh[32];
-  if (pcg_mode && *((volatile int*)&st->done)) return;
+// Row part of q = D∘p − C·z shared by k_kf_q and k_pcg_step: rows with ≤ KF_LONG_ROW entries thread per
+// row, the listed long rows (power-law degrees) warp per row with 4 loads in flight per lane; returns the
+// thread's share of pᵀq.
+__device__ __forceinline__ double kf_rows(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D,
+                                          const double* p, const double* z, double* q) {
+  const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = (int64_t)gridDim.x * NT;
   double loc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < Cf.nrows; i += (int64_t)gridDim.x * NT) {
+  for (int64_t i = i0; i < Cf.nrows; i += stride) {
+    if (nlong > 0 && Cf.p[i + 1] - Cf.p[i] > KF_LONG_ROW) continue;
     const double pi = p[i];
     const double qi = D[i] * pi - csr_dot(Cf, i, z);
     q[i] = qi;
     loc += pi * qi;
   }
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (i0 >> 5); j < nlong; j += stride >> 5) {
+    const int64_t i = longr[j];
+    const int64_t e0 = Cf.p[i], e1 = Cf.p[i + 1];
+    double s = 0.0;
+    for (int64_t e = e0 + lane; e < e1; e += 128) {
+      double v4[4];
+      int32_t c4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = e + 32 * u < e1;
+        v4[u] = ok ? Cf.v[e + 32 * u] : 0.0;
+        c4[u] = ok ? Cf.i[e + 32 * u] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s += v4[u] * __ldg(z + c4[u]);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const double pi = p[i];
+      const double qi = D[i] * pi - s;
+      q[i] = qi;
+      loc += pi * qi;
+    }
+  }
+  return loc;
+}
+
+__global__ void __launch_bounds__(NT) k_kf_q(DevCSR Cf, const int32_t* longr, int64_t nlong, const double* D,
+                                             const double* p, const double* z, double* q, double* partial,
+                                             PcgState* st, int pcg_mode) {
+  __shared__ double sh[32];
+  if (pcg_mode && *((volatile int*)&st->done)) return;
+  const double loc = kf_rows(Cf, longr, nlong, D, p, z, q);
   if (!pcg_mode) return;
   double v = block_reduce<0>(loc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = v;
@@ -2259,9 +2299,10 @@ __global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z,
 // round trip and the result is bit-identical to the three-kernel sequence; block 0 writes the state.
 // Phase A's partials live in partial[0, G), phase B's in partial[G, 3G), so no block overwrites a
 // partial another block is still reading.
-__global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const double* D, double* p, const double* w,
-                                                 double* q, double* x, double* r, double* z, double* partial,
-                                                 PcgState* st) {
+__global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, const int32_t* longr, int64_t nlong, int prec,
+                                                 const double* D, double* p, const double* w, double* q, double* x,
+                                                 double* r, double* z, double* partial, PcgState* st, int next_rhs,
+                                                 DevFactor F, DevCSR Ct, double* xout, double* ubuf) {
   __shared__ double sh[32];
   if (*((volatile int*)&st->done)) return;   // every block reads the flag before the first grid sync
   cg::grid_group grid = cg::this_grid();
@@ -2271,13 +2312,7 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const doub
   const int64_t m2 = Cf.nrows, G = gridDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = G * NT;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  double loc = 0.0;
-  for (int64_t i = i0; i < m2; i += stride) {
-    const double pi = p[i];
-    const double qi = D[i] * pi - csr_dot(Cf, i, w);
-    q[i] = qi;
-    loc += pi * qi;
-  }
+  const double loc = kf_rows(Cf, longr, nlong, D, p, w, q);
   double v = block_reduce<0>(loc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = v;
   grid.sync();
@@ -2315,11 +2350,30 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, int prec, const doub
   }
   const double beta = s2 / rho;
   for (int64_t i = i0; i < m2; i += stride) p[i] = z[i] + beta * p[i];
+  if (next_rhs) {   // phase D: the next F-solve's right-hand side u = Cᵀp (p complete after the sync)
+    grid.sync();
+    const int64_t N = next_rhs == 1 ? F.N : Ct.nrows, rc0 = F.fl_rc0;
+    for (int64_t cI = i0; cI < N; cI += stride) {
+      const double v = cI < Ct.nrows ? csr_dot(Ct, cI, p) : 0.0;
+      if (next_rhs == 2) {
+        ubuf[cI] = v;
+      } else {
+        if (cI < rc0) {
+          F.acc[cI] = v;
+          F.vbuf[cI] = 0.0;
+        } else {
+          F.vbuf[cI] = v;
+        }
+        xout[cI] = 0.0;
+      }
+    }
+  }
   tl_end(4, tls);
 }
 
-bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const double* w, double* q, double* x,
-              double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s) {
+bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, const double* D, double* p,
+              const double* w, double* q, double* x, double* r, double* z, double* partial, PcgState* st, int grid,
+              cudaStream_t s, int next_rhs, const DevFactor* Fp, const DevCSR* Ctp, double* xout, double* ubuf) {
   static int max_grid = -1;
   if (max_grid < 0) {
     int dev = 0, sms = 0, occ = 0;
@@ -2330,13 +2384,19 @@ bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const doub
   }
   if (grid > max_grid) return false;   // not co-resident: the caller runs the three-kernel sequence
   DevCSR C = Cf;
-  void* args[] = {&C, &prec, &D, &p, &w, &q, &x, &r, &z, &partial, &st};
+  DevFactor F{};
+  DevCSR Ct{};
+  if (Fp) F = *Fp;
+  if (Ctp) Ct = *Ctp;
+  if (next_rhs && (!Ctp || (next_rhs == 1 && !Fp))) next_rhs = 0;
+  void* args[] = {&C, &longr, &nlong, &prec, &D, &p, &w, &q, &x, &r, &z, &partial, &st, &next_rhs, &F, &Ct, &xout,
+                  &ubuf};
   return cudaLaunchCooperativeKernel((const void*)k_pcg_step, grid, NT, args, 0, s) == cudaSuccess;
 }
 
-void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,
-          PcgState* st, int grid, cudaStream_t s, bool pcg_mode) {
-  k_kf_q<<<grid, NT, 0, s>>>(Cf, D, p, z, q, partial, st, pcg_mode ? 1 : 0);
+void kf_q(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D, const double* p, const double* z,
+          double* q, double* partial, PcgState* st, int grid, cudaStream_t s, bool pcg_mode) {
+  k_kf_q<<<grid, NT, 0, s>>>(Cf, longr, nlong, D, p, z, q, partial, st, pcg_mode ? 1 : 0);
 }
 void pcg_init(int prec, int64_t m2, const double* b, const double* D, double* x, double* r, double* z,
               double* p, double* partial, PcgState* st, double tol, int maxit, int grid, cudaStream_t s) {

@@ -200,6 +200,7 @@ struct SweepRhs {
   DevCSR ct;                // optional: rhs[c] = Σ ct(c,:)·p for c < ct.nrows (K_F: Cᵀp fused)
   const double* p;
   const int* done_flag;     // early-exit flag (PCG converged) or nullptr
+  int rhs_ready;            // flattened forest: acc / vbuf / x already prepared (fused PCG step, phase D)
 };
 void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s);
 void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s);
@@ -217,8 +218,8 @@ void flat_set_unit(double* unit, int64_t col, cudaStream_t s);
 void flat_fill_rows(const DevFactor& F, const int32_t* src, int64_t nnz, cudaStream_t s);
 
 // ---- vector / SpMV kernels
-void kf_q(const DevCSR& Cf, const double* D, const double* p, const double* z, double* q, double* partial,
-          PcgState* st, int grid, cudaStream_t s, bool pcg_mode);
+void kf_q(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D, const double* p, const double* z,
+          double* q, double* partial, PcgState* st, int grid, cudaStream_t s, bool pcg_mode);
 void pcg_init(int prec, int64_t m2, const double* b, const double* D, double* x, double* r, double* z,
               double* p, double* partial, PcgState* st, double tol, int maxit, int grid, cudaStream_t s);
 void pcg_init_ph(int64_t m2, const double* r, const double* z, double* p, double* partial, PcgState* st,
@@ -233,8 +234,17 @@ void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid,
 constexpr int TL_K = 8, TL_RING = 256;
 void timeline_enable(unsigned long long* buf);
 // Fused a5 + a6 (P_L / none, unsharded): cooperative launch; false if it could not be launched.
-bool pcg_step(const DevCSR& Cf, int prec, const double* D, double* p, const double* w, double* q, double* x,
-              double* r, double* z, double* partial, PcgState* st, int grid, cudaStream_t s);
+// Rows of C with more than KF_LONG_ROW entries (listed in `longr`) are done warp per row, the rest thread per row.
+constexpr int KF_LONG_ROW = 32;
+// next_rhs (phase D, after p = z + βp and one more grid sync) prepares the next F-solve's right-hand side
+// u = Cᵀp, thread per row of Ct: 0 = none, 1 = flattened forest (acc / vbuf, xout = 0, as k_flat_rhs),
+// 2 = dense into ubuf (as the pregather SpMV).
+bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, const double* D, double* p,
+              const double* w, double* q, double* x, double* r, double* z, double* partial, PcgState* st, int grid,
+              cudaStream_t s, int next_rhs = 0, const DevFactor* F = nullptr, const DevCSR* Ct = nullptr,
+              double* xout = nullptr, double* ubuf = nullptr);
+// the flattened forest's right-hand side kernel alone (k_flat_rhs), for the first PCG iteration
+void flat_rhs(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s);
 
 void gather(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
 void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const int* done, cudaStream_t s);
