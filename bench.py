@@ -295,6 +295,39 @@ def run_ours(args, rank, world, local, use_dist):
     s.profile(False)
     pcg_prof = int(sum(r_prof["pcg_iters"][W:W + K]))
 
+    # ---------------------------------------------------------------- device launch timeline (third pass, the
+    # production path with CUDA graphs): per kernel the earliest block start and latest block end by
+    # %globaltimer, so launch durations and the idle gaps between dependent launches are both visible
+    TLN = ["flat_rhs", "flat_fwd", "root_gemv", "flat_bwd", "pcg_step", "trsv_fwd", "trsv_bwd", "spmv"]
+    s.ipm_init(space=args.space)
+    s.ipm_iterate(W)
+    torch.cuda.synchronize(dev)
+    s.debug_timeline(True)
+    s.ipm_iterate(1)
+    torch.cuda.synchronize(dev)
+    tl_ev = s.debug_timeline(False)
+    # the first 256 launches per kernel are recorded: keep the events before the first kernel's ring filled
+    if tl_ev:
+        last = {}
+        for k, a, b in tl_ev:
+            last[k] = last.get(k, 0) + 1
+        full = [k for k, c in last.items() if c >= 256]
+        if full:
+            cut = min(max(a for k, a, b in tl_ev if k == kk) for kk in full)
+            tl_ev = [e for e in tl_ev if e[1] <= cut]
+    tl = {}
+    if len(tl_ev) > 8:
+        span_us = (tl_ev[-1][2] - tl_ev[0][1]) / 1e3
+        busy = {}
+        for (k0, a0, b0), (k1, a1, b1) in zip(tl_ev, tl_ev[1:]):
+            d = busy.setdefault(TLN[k1], [0, 0.0, 0.0])
+            d[0] += 1
+            d[1] += (b1 - a1) / 1e3
+            d[2] += (a1 - b0) / 1e3
+        tl = {"span_us": span_us, "note": "first <=256 launches per kernel of one IPM step, graphs on",
+              "kernels": {k: {"n": v[0], "avg_us": v[1] / v[0], "avg_gap_before_us": v[2] / v[0],
+                              "share_of_span": v[1] / span_us} for k, v in busy.items()}}
+
     # ---------------------------------------------------------------- e2e replay through the C ABI
     e2e = None
     if not args.no_e2e and args.space == "nu":
@@ -363,7 +396,8 @@ def run_ours(args, rank, world, local, use_dist):
         except Exception:
             traffic = None
     flat = bool(st.get("flat_enabled", 0))
-    kname = ("F-solve = k_flat_rhs + k_flat_fwd + k_symroot_gemv + k_flat_bwd" if flat else
+    kname = ("F-solve = k_flat_fwd_t + k_symroot_gemv + k_flat_bwd_t (+ k_flat_rhs outside PCG; inside PCG the "
+             "fused step prepares C^T p)" if flat else
              "F-solve = (C^T p SpMV +) k_trsv_fwd + k_symroot_gemv + k_trsv_bwd")
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -384,7 +418,12 @@ def run_ours(args, rank, world, local, use_dist):
                 "flattened_forest": bool(st.get("flat_enabled", 0)),
                 "fsolve_share_of_step": solve_ms / ms_prof if ms_prof > 0 else None,
                 "timing": "kernel durations from a second pass over the same IPM steps with CUDA events "
-                          "around every launch (the headline pass runs without events)"}
+                          "around every launch (the headline pass runs without events)",
+                "device_timeline": tl}
+    if tl and "root_gemv" in tl.get("kernels", {}):
+        g_us = tl["kernels"]["root_gemv"]["avg_us"]
+        roofline["root_gemv"]["timeline_achieved"] = root_bytes / (g_us / 1e6) / 1e9
+        roofline["root_gemv"]["timeline_frac"] = root_bytes / (g_us / 1e6) / 1e9 / peak
 
     # ---------------------------------------------------------------- CPU baseline (rank 0)
     cpu = None

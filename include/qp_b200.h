@@ -263,7 +263,8 @@ int64_t qp_debug_sweep_trace(qp_ctx* ctx, int32_t sweep, int64_t* out, int64_t c
  * captured CUDA graphs are recorded too); enable = 0 turns it off and copies
  * min(cap, W) uint64 words to out (host, caller-owned), W = 2*8 + 2*8*256:
  * [8 launch counters][8 scratch][8][256] earliest block start, [8][256] latest block end
- * (globaltimer ns; ring slot = launch number mod 256).  Returns W or a negative qp_status. */
+ * (globaltimer ns; slot = launch number, the first 256 launches per kernel after enable).
+ * Returns W or a negative qp_status. */
 int64_t qp_debug_timeline(qp_ctx* ctx, int32_t enable, int64_t* out, int64_t cap);
 
 /* Host-only: the contiguous split of m2 rows (CSR indptr, m2+1 entries) over

@@ -354,7 +354,8 @@ class QPSolver:
 
     def debug_timeline(self, enable):
         """enable=True: start recording; enable=False: stop and return a list of (kernel, start_ns, end_ns)
-        per recorded launch, sorted by start (kernels: 0 flat rhs … 7 SpMV, include/qp_b200.h)."""
+        per recorded launch (the first 256 per kernel), sorted by start (kernels: 0 flat rhs … 7 SpMV,
+        include/qp_b200.h)."""
         K, R = 8, 256
         W = 2 * K + 2 * K * R
         if enable:

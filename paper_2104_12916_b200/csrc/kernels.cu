@@ -474,24 +474,26 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Launch timeline (debug, qp_debug_timeline): for instrumented kernel k and ring slot s = its launch
-// number mod TL_RING, the earliest block start and the latest block end (globaltimer ns), so the host can
+// Launch timeline (debug, qp_debug_timeline): for instrumented kernel k and its launch number s < TL_RING
+// (later launches are counted, not recorded), the earliest block start and the latest block end
+// (globaltimer ns), so the host can
 // rebuild the per-launch durations AND the gaps between dependent launches (inside CUDA graphs too).
 // Layout of g_tl: [TL_K launch counters][TL_K arrival counters][TL_K][TL_RING] starts, [TL_K][TL_RING] ends.
 __device__ unsigned long long* g_tl = nullptr;
 __device__ __forceinline__ unsigned tl_begin(int k) {
   unsigned long long* t = g_tl;
   if (t == nullptr || threadIdx.x != 0) return 0;
-  const unsigned s = (unsigned)(*((volatile unsigned long long*)(t + k)) % TL_RING);
-  atomicMin(t + 2 * TL_K + k * TL_RING + s, gtime());
-  return s;
+  const unsigned long long n = *((volatile unsigned long long*)(t + k));
+  if (n >= TL_RING) return TL_RING;   // ring full: only the first TL_RING launches are kept
+  atomicMin(t + 2 * TL_K + k * TL_RING + n, gtime());
+  return (unsigned)n;
 }
 __device__ __forceinline__ void tl_end(int k, unsigned s) {
   unsigned long long* t = g_tl;
   if (t == nullptr) return;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  atomicMax(t + 2 * TL_K + TL_K * TL_RING + k * TL_RING + s, gtime());
+  if (s < TL_RING) atomicMax(t + 2 * TL_K + TL_K * TL_RING + k * TL_RING + s, gtime());
   __threadfence();
   if (atomicAdd(t + TL_K + k, 1ull) == gridDim.x - 1) {
     t[TL_K + k] = 0;

@@ -58,7 +58,8 @@ def main():
         one, seen = [], set()
         for r in recs:
             k = r["kernel"].split("<")[0].strip()
-            if k in ("k_trsv_fwd", "k_symroot_gemv", "k_trsv_bwd", "k_flat_rhs", "k_flat_fwd", "k_flat_bwd") \
+            if k in ("k_trsv_fwd", "k_symroot_gemv", "k_trsv_bwd", "k_flat_rhs", "k_flat_fwd", "k_flat_bwd",
+                     "k_flat_fwd_t", "k_flat_bwd_t") \
                     and k not in seen:
                 seen.add(k)
                 one.append(r)
