@@ -231,6 +231,9 @@ typedef struct {
   double flat_discrepancy;           /* ‖y_flat − y_sweeps‖/‖y_sweeps‖ of the flattened-forest guard (−1: n/a) */
   double flat_enabled;               /* 1 if F-solves use the flattened forest (M = L21·L11⁻¹) */
   double flat_nnz_M;                 /* stored entries of M */
+  double dense_w_enabled;            /* 1 if PCG's K_F products use the explicit x-block W = (F⁻¹)₁₁ */
+  double dense_w_discrepancy;        /* ‖W·u − (F⁻¹[u; 0])ₓ‖/‖·‖ of its factor-time guard (−1: not built) */
+  double kf_bytes_W;                 /* bytes of W read per K_F product: 8·n(n+1)/2 (0 when not in use) */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 
@@ -240,7 +243,7 @@ int qp_get_stats(qp_ctx* ctx, qp_stats* s);
  *  0 F forward sweep (or flattened forward product), 1 F backward sweep (or
  *  flattened backward product), 2 K_F q-SpMV (a5), 3 PCG vector updates (a6),
  *  4 P_H sweeps (a7), 5 P_H refactor (a8), 6 IPM rhs (a9), 7 other,
- *  8 symmetric-root GEMV of the F-solve, 9 reserved (10 entries each). */
+ *  8 symmetric-root GEMV of the F-solve, 9 dense W GEMV of a PCG K_F product (10 entries each). */
 int qp_profile(qp_ctx* ctx, int32_t enable);
 int qp_profile_read(qp_ctx* ctx, double* ms /*10*/, int64_t* count /*10*/);
 

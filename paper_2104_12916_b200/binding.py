@@ -71,7 +71,8 @@ class _Stats(C.Structure):
                [(k, C.c_double) for k in ("c_fact_F", "c_fact_PH", "t_symbolic_s", "t_factor_s",
                                           "t_factor_ph_s", "pcg_bytes_per_iter", "pcg_flops_per_iter",
                                           "sweep_bytes_F", "fsolve_bytes_F", "sym_discrepancy", "sym_enabled",
-                                          "flat_discrepancy", "flat_enabled", "flat_nnz_M")]
+                                          "flat_discrepancy", "flat_enabled", "flat_nnz_M", "dense_w_enabled",
+                                          "dense_w_discrepancy", "kf_bytes_W")]
 
 
 _LIB = None
@@ -395,7 +396,7 @@ class QPSolver:
         cnt = np.zeros(10, dtype=np.int64)
         self._check(self.lib.qp_profile_read(self.ctx, ms.ctypes.data, cnt.ctypes.data))
         names = ["f_fwd", "f_bwd", "kf_q", "pcg_vec", "ph_sweeps", "ph_refactor", "ipm_rhs", "other", "f_root",
-                 "reserved"]
+                 "kf_W"]
         return {nm: (float(m), int(c)) for nm, m, c in zip(names, ms, cnt)}
 
 

@@ -17,6 +17,7 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <random>
 
 #include "../../include/qp_b200.h"
 #include "kernels.cuh"
@@ -283,6 +284,10 @@ struct qp_ctx {
   double *vin = nullptr, *vin2 = nullptr, *vout = nullptr;  // staging for host I/O
   double* partial = nullptr;
   unsigned long long* tl_buf = nullptr;   // qp_debug_timeline
+  double* dense_w = nullptr;         // explicit (F⁻¹)₁₁ (build_dense_w), column-major, leading dimension dw_ld
+  int64_t dw_ld = 0, dw_nch = 0;
+  const int2* dw_chunks = nullptr;
+  double dw_discrepancy = -1.0;
   const int32_t* long_c = nullptr;   // rows of C with > KF_LONG_ROW entries (k_pcg_step)
   int64_t n_long_c = 0;
   PcgState* pst = nullptr;
@@ -762,6 +767,14 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
   c->launches += fsolve_only ? 0 : 1;
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
+  if (rhs_ready && c->dense_w) {   // ubuf = Cᵀp and xbuf[0, n) = 0 from the fused step: w = W·Cᵀp
+    int h = c->begin(9);
+    dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks, c->dw_nch, c->ubuf, c->xbuf, r.done_flag, c->sm_count,
+               c->stream);
+    c->end(h);
+    c->launches += 1;
+    return 0;
+  }
   r.rhs_ready = rhs_ready && c->FF.d.flat ? 1 : 0;
   if (rhs_ready && !c->FF.d.flat) {
     r.rhs = c->ubuf;
@@ -851,8 +864,12 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
                                                                  ((int64_t)c->sm_count * 512)));
   // phase D of the fused step prepares the next iteration's u = Cᵀp (flattened forest or pregathered
   // sweeps); the first iteration's comes from the usual kernel
-  const int next_rhs = !fused ? 0 : c->FF.d.flat ? 1 : pregather_on() ? 2 : 0;
-  if (next_rhs == 1) {
+  const int next_rhs = !fused ? 0 : c->dense_w ? 3 : c->FF.d.flat ? 1 : pregather_on() ? 2 : 0;
+  if (next_rhs == 3) {
+    spmv(c->Ctf, c->pp, c->ubuf, &c->pst->done, c->vgrid, st);
+    cudaMemsetAsync(c->xbuf, 0, c->n * 8, st);
+    c->launches += 1;
+  } else if (next_rhs == 1) {
     SweepRhs r0{};
     r0.ct = c->Ctf;
     r0.p = c->pp;
@@ -1431,6 +1448,76 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
   return rc;
 }
 
+// Explicit x-block of F⁻¹ (DESIGN §5 "dense W"): W = (F⁻¹)₁₁ = −H⁻¹ + H⁻¹Aᵀ(AH⁻¹Aᵀ)⁻¹AH⁻¹ (n × n, factor
+// order, the block form of P:L757–787), so that the K_F product inside PCG is w = W·Cᵀp, one symmetric
+// GEMV reading 8·n(n+1)/2 bytes.  Used when that is fewer bytes than one F-solve (c0, c1) and W fits the
+// budget; built column by column from F-solves on unit vectors, then checked against an F-solve on a
+// random right-hand side (≤ 1e-10 relative) before it is used.  QPB_DENSE_W=0 disables it.
+int build_dense_w(qp_ctx* c) {
+  if (c->dense_w || c->sharded) return QP_OK;
+  const char* e = std::getenv("QPB_DENSE_W");
+  if (e && e[0] == '0') return QP_OK;
+  qp_stats s{};
+  qp_get_stats(c, &s);
+  const int64_t n = c->n, N = c->n + c->m1, ld = n + (n & 1);
+  const double wbytes = 8.0 * (double)n * (double)(n + 1) / 2.0;
+  if (n < 64 || !(wbytes < s.fsolve_bytes_F) || 8.0 * (double)ld * (double)n > 16e9) return QP_OK;
+  cudaStream_t st = c->stream;
+  double* W = nullptr;
+  try {
+    W = c->mem.zeros<double>((size_t)ld * (size_t)n, st);
+  } catch (std::bad_alloc&) {
+    cudaGetLastError();
+    return QP_OK;   // no room: keep the F-solve path
+  }
+  cudaMemsetAsync(c->rhs2, 0, N * 8, st);
+  for (int64_t j = 0; j < n; ++j) {
+    if (j > 0) cudaMemsetAsync(c->rhs2 + j - 1, 0, 8, st);
+    flat_set_unit(c->rhs2, j, st);
+    f_solve_dev(c, c->rhs2, c->xbuf);
+    cudaMemcpyAsync(W + (size_t)j * ld, c->xbuf, n * 8, cudaMemcpyDeviceToDevice, st);
+  }
+  cudaMemsetAsync(c->rhs2, 0, N * 8, st);
+  if (int rc = cuda_check(c, "dense W columns")) return rc;
+  // chunk list: row block I, first column block K0 (≤ 8 blocks of 64 columns up to the diagonal block)
+  std::vector<int32_t> ch;
+  const int64_t nb = (n + 63) / 64;
+  for (int64_t I = 0; I < nb; ++I)
+    for (int64_t K0 = 0; K0 <= I; K0 += 8) {
+      ch.push_back((int32_t)I);
+      ch.push_back((int32_t)K0);
+    }
+  c->dw_chunks = reinterpret_cast<const int2*>(c->mem.upload(ch, st));
+  c->dw_nch = (int64_t)ch.size() / 2;
+  cudaStreamSynchronize(st);
+  // accuracy guard: W·u against the x-part of an F-solve on [u; 0]
+  std::vector<double> u(N, 0.0), y1(n), y2(n);
+  std::mt19937_64 g(7);
+  std::normal_distribution<double> nd;
+  for (int64_t i = 0; i < n; ++i) u[i] = nd(g);
+  cudaMemcpyAsync(c->rhs2, u.data(), N * 8, cudaMemcpyHostToDevice, st);
+  f_solve_dev(c, c->rhs2, c->xbuf);
+  cudaMemcpyAsync(y2.data(), c->xbuf, n * 8, cudaMemcpyDeviceToHost, st);
+  cudaMemsetAsync(c->xbuf, 0, n * 8, st);
+  dense_symv(W, ld, n, c->dw_chunks, c->dw_nch, c->rhs2, c->xbuf, nullptr, c->sm_count, st);
+  cudaMemcpyAsync(y1.data(), c->xbuf, n * 8, cudaMemcpyDeviceToHost, st);
+  cudaMemsetAsync(c->rhs2, 0, N * 8, st);
+  if (int rc = sync_check(c, "dense W guard")) return rc;
+  double fd = 0, fn = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    fd += (y1[i] - y2[i]) * (y1[i] - y2[i]);
+    fn += y2[i] * y2[i];
+  }
+  c->dw_discrepancy = fn > 0 ? std::sqrt(fd / fn) : 0.0;
+  if (std::getenv("QPB_VERBOSE"))
+    std::fprintf(stderr, "qpb: dense W (n = %lld, %.3g GB read per product) guard %.2e\n", (long long)n,
+                 wbytes / 1e9, c->dw_discrepancy);
+  if (!(c->dw_discrepancy <= 1e-10)) return QP_OK;
+  c->dense_w = W;
+  c->dw_ld = ld;
+  return QP_OK;
+}
+
 int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
   int rc = require(c, false);
   if (rc) return rc;
@@ -1603,6 +1690,7 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
       F.d.flat = (F.flat_discrepancy <= 1e-10 && std::isfinite(F.flat_discrepancy)) ? 1 : 0;
       if (!F.d.flat) cudaMemsetAsync(F.d.acc, 0, N * 8, st);   // the sweeps expect zero accumulators
     }
+    if (int rc2 = build_dense_w(c)) return rc2;
   }
   // ---- P_H: T = C diag(H)⁻¹ Cᵀ pattern (host) and values (device), symbolic of D + T
   if (p == QP_PREC_HIGH) {
@@ -1952,6 +2040,9 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->flat_discrepancy = c->FF.flat_discrepancy;
     s->flat_enabled = c->FF.d.flat ? 1.0 : 0.0;
     s->flat_nnz_M = (double)S.fl_msize;
+    s->dense_w_enabled = c->dense_w ? 1.0 : 0.0;
+    s->dense_w_discrepancy = c->dw_discrepancy;
+    s->kf_bytes_W = c->dense_w ? 4.0 * (double)c->n * (double)(c->n + 1) : 0.0;
   }
   return QP_OK;
 }

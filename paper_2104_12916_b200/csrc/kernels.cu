@@ -1655,6 +1655,45 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
   tl_end(2, tls);
 }
 
+// Dense symmetric GEMV x += W v on the explicit x-block W = (F⁻¹)₁₁ (column-major, leading dimension ld,
+// full storage, lower triangle read): chunks (row block I, ≤ 8 column blocks from K0 up to the diagonal
+// block) through schunk_gemv, so each lower tile is read once for x_I += W_IK v_K and x_K += W_IKᵀ v_I.
+template <int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks,
+                                                         int64_t nch, const double* v, double* x,
+                                                         const int* done_flag) {
+  __shared__ double vK[512];
+  __shared__ double vI[64];
+  __shared__ double red[576];
+  __shared__ double colv[512];
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(2);
+  const int tid = threadIdx.x;
+  const uint64_t pol = l2pol_normal();
+  for (int64_t idx = blockIdx.x; idx < nch; idx += gridDim.x) {
+    const int2 ch = __ldg(chunks + idx);
+    const int64_t rI = 64 * (int64_t)ch.x, cK = 64 * (int64_t)ch.y;
+    const int Rn = (int)(n - rI < 64 ? n - rI : 64);
+    const int64_t cEnd = (cK + 512 < rI + Rn) ? cK + 512 : rI + Rn;
+    const int ncol = (int)(cEnd - cK);
+    const int ncol_t = (int)(rI - cK < ncol ? rI - cK : ncol);
+    __syncthreads();
+    for (int c = tid; c < ncol; c += NT) vK[c] = v[cK + c];
+    if (tid < Rn) vI[tid] = v[rI + tid];
+    __syncthreads();
+    schunk_gemv<U>(W + rI + cK * ld, ld, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
+    if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
+    for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
+  }
+  tl_end(2, tls);
+}
+
+void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const double* v, double* x,
+                const int* done_flag, int sms, cudaStream_t s) {
+  if (nch <= 0) return;
+  k_dense_symv<16, 3><<<sms * 3, NT, 0, s>>>(W, ld, n, chunks, nch, v, x, done_flag);
+}
+
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
                   cudaStream_t s, const double* sub) {
   if (c_end <= c_begin) return;
@@ -2357,8 +2396,9 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, const int32_t* longr
     const int64_t N = next_rhs == 1 ? F.N : Ct.nrows, rc0 = F.fl_rc0;
     for (int64_t cI = i0; cI < N; cI += stride) {
       const double v = cI < Ct.nrows ? csr_dot(Ct, cI, p) : 0.0;
-      if (next_rhs == 2) {
+      if (next_rhs >= 2) {
         ubuf[cI] = v;
+        if (next_rhs == 3) xout[cI] = 0.0;   // dense W: the GEMV accumulates into xout[0, n)
       } else {
         if (cI < rc0) {
           F.acc[cI] = v;
@@ -2390,7 +2430,7 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
   DevCSR Ct{};
   if (Fp) F = *Fp;
   if (Ctp) Ct = *Ctp;
-  if (next_rhs && (!Ctp || (next_rhs == 1 && !Fp))) next_rhs = 0;
+  if (next_rhs && (!Ctp || (next_rhs == 1 && !Fp) || (next_rhs == 3 && !xout))) next_rhs = 0;
   void* args[] = {&C, &longr, &nlong, &prec, &D, &p, &w, &q, &x, &r, &z, &partial, &st, &next_rhs, &F, &Ct, &xout,
                   &ubuf};
   return cudaLaunchCooperativeKernel((const void*)k_pcg_step, grid, NT, args, 0, s) == cudaSuccess;

@@ -238,11 +238,14 @@ void timeline_enable(unsigned long long* buf);
 constexpr int KF_LONG_ROW = 32;
 // next_rhs (phase D, after p = z + βp and one more grid sync) prepares the next F-solve's right-hand side
 // u = Cᵀp, thread per row of Ct: 0 = none, 1 = flattened forest (acc / vbuf, xout = 0, as k_flat_rhs),
-// 2 = dense into ubuf (as the pregather SpMV).
+// 2 = dense into ubuf (as the pregather SpMV), 3 = into ubuf with xout[0, n) = 0 (dense W GEMV next).
 bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, const double* D, double* p,
               const double* w, double* q, double* x, double* r, double* z, double* partial, PcgState* st, int grid,
               cudaStream_t s, int next_rhs = 0, const DevFactor* F = nullptr, const DevCSR* Ct = nullptr,
               double* xout = nullptr, double* ubuf = nullptr);
+// x += W v, W the explicit x-block of F⁻¹ (k_dense_symv; chunks = (row block, first column block) pairs)
+void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const double* v, double* x,
+                const int* done_flag, int sms, cudaStream_t s);
 // the flattened forest's right-hand side kernel alone (k_flat_rhs), for the first PCG iteration
 void flat_rhs(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s);
 
