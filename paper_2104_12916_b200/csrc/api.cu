@@ -767,12 +767,21 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
   c->launches += fsolve_only ? 0 : 1;
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
-  if (rhs_ready && c->dense_w) {   // ubuf = Cᵀp and xbuf[0, n) = 0 from the fused step: w = W·Cᵀp
+  if (c->dense_w && (rhs_ready || pcg_mode)) {   // w = W·Cᵀp
+    if (!rhs_ready) {   // (P_H PCG: not fused) Cᵀp into ubuf, w accumulator zeroed
+      spmv(c->Ctf, p, c->ubuf, r.done_flag, c->vgrid, c->stream);
+      cudaMemsetAsync(c->xbuf, 0, c->n * 8, c->stream);
+      c->launches += 1;
+    }   // else ubuf = Cᵀp and xbuf[0, n) = 0 come from the fused step's phase D
     int h = c->begin(9);
     dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks, c->dw_nch, c->ubuf, c->xbuf, r.done_flag, c->sm_count,
                c->stream);
     c->end(h);
     c->launches += 1;
+    if (fsolve_only) return 0;
+    h = c->begin(2);
+    kf_q(c->Cf, c->long_c, c->n_long_c, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
+    c->end(h);
     return 0;
   }
   r.rhs_ready = rhs_ready && c->FF.d.flat ? 1 : 0;
@@ -1452,7 +1461,8 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
 // order, the block form of P:L757–787), so that the K_F product inside PCG is w = W·Cᵀp, one symmetric
 // GEMV reading 8·n(n+1)/2 bytes.  Used when that is fewer bytes than one F-solve (c0, c1) and W fits the
 // budget; built column by column from F-solves on unit vectors, then checked against an F-solve on a
-// random right-hand side (≤ 1e-10 relative) before it is used.  QPB_DENSE_W=0 disables it.
+// random right-hand side (≤ 1e-10 relative) before it is used.  QPB_DENSE_W=0 disables it, =2 forces it
+// whenever it fits (tests).
 int build_dense_w(qp_ctx* c) {
   if (c->dense_w || c->sharded) return QP_OK;
   const char* e = std::getenv("QPB_DENSE_W");
@@ -1461,7 +1471,8 @@ int build_dense_w(qp_ctx* c) {
   qp_get_stats(c, &s);
   const int64_t n = c->n, N = c->n + c->m1, ld = n + (n & 1);
   const double wbytes = 8.0 * (double)n * (double)(n + 1) / 2.0;
-  if (n < 64 || !(wbytes < s.fsolve_bytes_F) || 8.0 * (double)ld * (double)n > 16e9) return QP_OK;
+  const bool force = e && e[0] == '2';   // QPB_DENSE_W=2: whenever it fits (tests)
+  if (n < 64 || !(force || wbytes < s.fsolve_bytes_F) || 8.0 * (double)ld * (double)n > 16e9) return QP_OK;
   cudaStream_t st = c->stream;
   double* W = nullptr;
   try {

@@ -1,0 +1,114 @@
+"""GPU parity of the alternative K_F / PCG paths, each against the CPU oracle.
+
+The library picks its K_F product path at setup (include/qp_b200.h qp_stats): the explicit x-block
+W = (F⁻¹)₁₁ when it reads fewer bytes than an F-solve, else the flattened forest or the sweeps; the
+P_L PCG runs as one fused cooperative step per iteration, with long rows of C (> 32 entries) warp per
+row.  The A/B switches QPB_DENSE_W=0 / QPB_FUSED_PCG=0 are read once per process, so every variant
+runs in its own subprocess; each must match the oracle on the same (D, rhs) at a fixed iteration count
+(reading c5#16: 1e-8 relative) and, on c0, reach the oracle's IPM objective (1e-8 relative).
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import qpgen
+from oracle import kkt
+from oracle.fsolve import DenseF
+from oracle.ipm import ipm_solve as oracle_ipm
+from oracle.pcg import pcg as oracle_pcg
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import qpgen
+from paper_2104_12916_b200.binding import from_qp
+qp = eval(sys.argv[2])
+s = from_qp(qp)
+s.ipm_factor_once('low')
+st = s.stats()
+rng = np.random.default_rng(8)
+D = rng.uniform(0.5, 2.0, qp.m2)
+b = rng.standard_normal(qp.m2)
+out = {"dense_w": st["dense_w_enabled"], "flat": st["flat_enabled"], "xs": {}}
+for k in (1, 3, 7):
+    x, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=k)
+    out["xs"][str(k)] = [it, x.tolist()]
+if sys.argv[3] == '1':
+    res = s.ipm_solve(ipm_tol=1e-10)
+    out["obj"] = res["objective"]
+    out["converged"] = bool(res["converged"])
+print("RESULT " + json.dumps(out))
+'''
+
+CASES = {
+    "c0": "qpgen.make('c0')",
+    "ragged": "qpgen.scaled_random_qp(700, 130, 900, seed=3)",
+    # every row of C has 40 entries: the fused step's warp-per-row branch
+    "long_rows": "qpgen.scaled_random_qp(300, 60, 400, seed=5, c_nnz=40)",
+    # dense F with a large λ block: W (n²/2 words) reads fewer bytes than an F-solve ((n+m1)²/2 words)
+    "dense_m1": "qpgen.scaled_random_qp(400, 200, 500, seed=6, g_nnz=8)",
+}
+VARIANTS = {"default": {}, "no_dense_w": {"QPB_DENSE_W": "0"}, "force_w": {"QPB_DENSE_W": "2"},
+            "unfused": {"QPB_FUSED_PCG": "0"}, "unfused_no_w": {"QPB_FUSED_PCG": "0", "QPB_DENSE_W": "0"},
+            "unfused_force_w": {"QPB_FUSED_PCG": "0", "QPB_DENSE_W": "2"}}
+
+
+def run_child(expr, env_extra, ipm):
+    env = dict(os.environ)
+    env.update(env_extra)
+    p = subprocess.run([sys.executable, "-c", CHILD, ROOT, expr, "1" if ipm else "0"], capture_output=True,
+                       text=True, env=env,
+                       timeout=600, cwd=ROOT)
+    line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
+    assert p.returncode == 0 and line, p.stderr[-2000:]
+    return json.loads(line[-1][7:])
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def oracle_case(request):
+    qp = eval(CASES[request.param])
+    fs = DenseF(qp.H, qp.A)
+    rng = np.random.default_rng(8)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    ref = {}
+    for k in (1, 3, 7):
+        xr, itr, *_ = oracle_pcg(lambda v: kkt.KF_apply(qp, fs, D, v), b, kkt.PrecondL(D), 0.0, k)
+        ref[k] = xr
+    obj = None
+    if request.param == "c0":   # PL-KF oracle IPMs at the other sizes take thousands of dense PCG steps
+        r = oracle_ipm(qp, precond="low", ipm_tol=1e-10, fs=fs)
+        assert r.converged
+        obj = r.objective
+    return request.param, qp, ref, obj
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_path_variant_matches_oracle(oracle_case, variant):
+    name, qp, ref, obj = oracle_case
+    out = run_child(CASES[name], VARIANTS[variant], obj is not None)
+    if name == "dense_m1" and variant in ("default", "unfused"):
+        assert out["dense_w"] == 1.0          # chosen by bytes
+    if name == "c0" and variant == "default":
+        assert out["dense_w"] == 0.0          # c0: one F-solve (150 KB) reads less than W (160 KB)
+    if VARIANTS[variant].get("QPB_DENSE_W") == "0":
+        assert out["dense_w"] == 0.0
+    if VARIANTS[variant].get("QPB_DENSE_W") == "2":
+        assert out["dense_w"] == 1.0
+    for k, xr in ref.items():
+        it, x = out["xs"][str(k)]
+        assert it == k
+        x = np.asarray(x)
+        assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr), (k, np.linalg.norm(x - xr) / np.linalg.norm(xr))
+    if obj is not None:
+        assert out["converged"]
+        assert abs(out["obj"] - obj) <= 1e-8 * max(1.0, abs(obj))
