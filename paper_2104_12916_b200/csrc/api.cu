@@ -1481,14 +1481,25 @@ int build_dense_w(qp_ctx* c) {
     cudaGetLastError();
     return QP_OK;   // no room: keep the F-solve path
   }
+  // Flattened forest with a symmetric root J0 = columns [r0, N): for a root column j the F-solve is
+  // x2 = S⁻¹e_j, so W's root block is S⁻¹'s x-part, copied from its lower storage; only the forest
+  // columns [0, r0) need F-solves (c1: 3 761 instead of 20 000).  The diagonal 64-blocks (the GEMV reads
+  // them full) are then completed from their lower triangles.
+  const Symbolic& S = c->FF.S;
+  const int64_t J0 = S.ns - 1;
+  const bool fast = c->FF.d.flat && c->FF.sym_enabled && J0 >= 0 && S.sn_sinv[J0] >= 0 &&
+                    S.sn_start[J0] == c->FF.d.fl_rc0 && S.sn_start[J0 + 1] == N && S.sn_start[J0] < n;
+  const int64_t r0 = fast ? S.sn_start[J0] : n;
   cudaMemsetAsync(c->rhs2, 0, N * 8, st);
-  for (int64_t j = 0; j < n; ++j) {
+  for (int64_t j = 0; j < r0; ++j) {
     if (j > 0) cudaMemsetAsync(c->rhs2 + j - 1, 0, 8, st);
     flat_set_unit(c->rhs2, j, st);
     f_solve_dev(c, c->rhs2, c->xbuf);
     cudaMemcpyAsync(W + (size_t)j * ld, c->xbuf, n * 8, cudaMemcpyDeviceToDevice, st);
   }
   cudaMemsetAsync(c->rhs2, 0, N * 8, st);
+  if (fast) w_copy_root(c->FF.d.xinv + S.sn_sinv[J0], S.sn_ldx[J0], W, ld, r0, n, st);
+  w_symmetrize_diag(W, ld, n, st);
   if (int rc = cuda_check(c, "dense W columns")) return rc;
   // chunk list: row block I, first column block K0 (≤ 8 blocks of 64 columns up to the diagonal block)
   std::vector<int32_t> ch;

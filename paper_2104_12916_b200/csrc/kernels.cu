@@ -1688,6 +1688,27 @@ __global__ void __launch_bounds__(NT, MINB) k_dense_symv(const double* W, int64_
   tl_end(2, tls);
 }
 
+// W[r0 + a, r0 + b] = S⁻¹(a, b) for a ≥ b (x-part of the symmetric root, lower storage Sinv with ldx).
+__global__ void k_w_copy_root(const double* Sinv, int64_t ldx, double* W, int64_t ld, int64_t r0, int64_t n) {
+  const int64_t m = n - r0;
+  for (int64_t b = blockIdx.x; b < m; b += gridDim.x)
+    for (int64_t a = b + threadIdx.x; a < m; a += NT) W[(r0 + a) + (r0 + b) * ld] = Sinv[a + b * ldx];
+}
+void w_copy_root(const double* Sinv, int64_t ldx, double* W, int64_t ld, int64_t r0, int64_t n, cudaStream_t s) {
+  if (n > r0) k_w_copy_root<<<148 * 8, NT, 0, s>>>(Sinv, ldx, W, ld, r0, n);
+}
+// Upper triangle of every diagonal 64-block from its lower triangle (k_dense_symv reads them full).
+__global__ void k_w_symmetrize_diag(double* W, int64_t ld, int64_t n) {
+  const int64_t c0 = 64 * (int64_t)blockIdx.x;
+  for (int t = threadIdx.x; t < 64 * 64; t += NT) {
+    const int64_t i = c0 + (t & 63), j = c0 + (t >> 6);
+    if (i < j && j < n) W[i + j * ld] = W[j + i * ld];
+  }
+}
+void w_symmetrize_diag(double* W, int64_t ld, int64_t n, cudaStream_t s) {
+  if (n > 0) k_w_symmetrize_diag<<<(unsigned)((n + 63) / 64), NT, 0, s>>>(W, ld, n);
+}
+
 void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const double* v, double* x,
                 const int* done_flag, int sms, cudaStream_t s) {
   if (nch <= 0) return;

@@ -243,6 +243,9 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
               const double* w, double* q, double* x, double* r, double* z, double* partial, PcgState* st, int grid,
               cudaStream_t s, int next_rhs = 0, const DevFactor* F = nullptr, const DevCSR* Ct = nullptr,
               double* xout = nullptr, double* ubuf = nullptr);
+// building W: the symmetric root's x-part from S⁻¹'s lower storage; diagonal 64-blocks completed
+void w_copy_root(const double* Sinv, int64_t ldx, double* W, int64_t ld, int64_t r0, int64_t n, cudaStream_t s);
+void w_symmetrize_diag(double* W, int64_t ld, int64_t n, cudaStream_t s);
 // x += W v, W the explicit x-block of F⁻¹ (k_dense_symv; chunks = (row block, first column block) pairs)
 void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const double* v, double* x,
                 const int* done_flag, int sms, cudaStream_t s);

@@ -68,11 +68,23 @@ def main():
             tj = json.load(open(path))
         except Exception:
             tj = {}
-        tj[cfg] = {"dram_bytes_per_fsolve": sum(r["dram_read"] + r["dram_write"] for r in one),
+        prev = tj.get(cfg, {})
+        w = [r for r in recs if r["kernel"].split("<")[0].strip() == "k_dense_symv"]
+        if w:   # explicit W: one launch per PCG K_F product (kept beside the F-solve numbers)
+            prev["dram_bytes_per_kf_W"] = w[0]["dram_read"] + w[0]["dram_write"]
+            prev["kf_W_launch"] = {"kernel": w[0]["kernel"], "duration_us": w[0]["duration"],
+                                   "dram_read_GB": w[0]["dram_read"] / 1e9, "dram_pct_of_peak": w[0]["dram_pct"],
+                                   "source": f"ncu --set full --clock-control none: {cmd}"}
+        if not one:
+            tj[cfg] = prev
+            json.dump(tj, open(path, "w"), indent=1)
+            return
+        prev.update({"dram_bytes_per_fsolve": sum(r["dram_read"] + r["dram_write"] for r in one),
                    "source": f"ncu --set full --clock-control none: {cmd}",
                    "launches": [{"kernel": r["kernel"], "duration_us": r["duration"],
                                  "dram_read_GB": r["dram_read"] / 1e9, "dram_write_MB": r["dram_write"] / 1e6,
-                                 "dram_pct_of_peak": r["dram_pct"]} for r in one]}
+                                 "dram_pct_of_peak": r["dram_pct"]} for r in one]})
+        tj[cfg] = prev
         json.dump(tj, open(path, "w"), indent=1)
 
 
