@@ -98,22 +98,23 @@ __device__ double reduce_partials(const double* part, int n, double* sh) {
   }
   return block_reduce<OP>(v, sh);
 }
-// One row of a CSR product, 4 entries per batch so their index, value and gather loads overlap
-// (short rows — C has 4–6 entries per row — then cost one or two dependent load rounds, not six).
+// One row of a CSR product, B entries per batch so their index, value and gather loads overlap
+// (short rows — C has 4–6 entries per row, Cᵀ about 12 — then cost one dependent load round).
+template <int B = 4>
 __device__ __forceinline__ double csr_dot(const DevCSR& M, int64_t row, const double* x) {
   double s = 0.0;
   const int64_t q0 = M.p[row], q1 = M.p[row + 1];
-  for (int64_t q = q0; q < q1; q += 4) {
-    double v[4];
-    int32_t c[4];
+  for (int64_t q = q0; q < q1; q += B) {
+    double v[B];
+    int32_t c[B];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < B; ++u) {
       const bool ok = q + u < q1;
       v[u] = ok ? M.v[q + u] : 0.0;
       c[u] = ok ? M.i[q + u] : 0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s += v[u] * __ldg(x + c[u]);
+    for (int u = 0; u < B; ++u) s += v[u] * __ldg(x + c[u]);
   }
   return s;
 }
@@ -2162,6 +2163,7 @@ void spmv(const DevCSR& M, const double* x, double* y, const int* done, int grid
 // Row part of q = D∘p − C·z shared by k_kf_q and k_pcg_step: rows with ≤ KF_LONG_ROW entries thread per
 // row, the listed long rows (power-law degrees) warp per row with 4 loads in flight per lane; returns the
 // thread's share of pᵀq.
+template <int B = 4>
 __device__ __forceinline__ double kf_rows(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D,
                                           const double* p, const double* z, double* q) {
   const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = (int64_t)gridDim.x * NT;
@@ -2169,7 +2171,7 @@ __device__ __forceinline__ double kf_rows(const DevCSR& Cf, const int32_t* longr
   for (int64_t i = i0; i < Cf.nrows; i += stride) {
     if (nlong > 0 && Cf.p[i + 1] - Cf.p[i] > KF_LONG_ROW) continue;
     const double pi = p[i];
-    const double qi = D[i] * pi - csr_dot(Cf, i, z);
+    const double qi = D[i] * pi - csr_dot<B>(Cf, i, z);
     q[i] = qi;
     loc += pi * qi;
   }
@@ -2361,7 +2363,7 @@ __global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z,
 // round trip and the result is bit-identical to the three-kernel sequence; block 0 writes the state.
 // Phase A's partials live in partial[0, G), phase B's in partial[G, 3G), so no block overwrites a
 // partial another block is still reading.
-__global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, const int32_t* longr, int64_t nlong, int prec,
+__global__ void __launch_bounds__(NT, 2) k_pcg_step(DevCSR Cf, const int32_t* longr, int64_t nlong, int prec,
                                                  const double* D, double* p, const double* w, double* q, double* x,
                                                  double* r, double* z, double* partial, PcgState* st, int next_rhs,
                                                  DevFactor F, DevCSR Ct, double* xout, double* ubuf) {
@@ -2374,7 +2376,7 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, const int32_t* longr
   const int64_t m2 = Cf.nrows, G = gridDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = G * NT;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  const double loc = kf_rows(Cf, longr, nlong, D, p, w, q);
+  const double loc = kf_rows<8>(Cf, longr, nlong, D, p, w, q);
   double v = block_reduce<0>(loc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = v;
   grid.sync();
@@ -2416,7 +2418,7 @@ __global__ void __launch_bounds__(NT) k_pcg_step(DevCSR Cf, const int32_t* longr
     grid.sync();
     const int64_t N = next_rhs == 1 ? F.N : Ct.nrows, rc0 = F.fl_rc0;
     for (int64_t cI = i0; cI < N; cI += stride) {
-      const double v = cI < Ct.nrows ? csr_dot(Ct, cI, p) : 0.0;
+      const double v = cI < Ct.nrows ? csr_dot<16>(Ct, cI, p) : 0.0;
       if (next_rhs >= 2) {
         ubuf[cI] = v;
         if (next_rhs == 3) xout[cI] = 0.0;   // dense W: the GEMV accumulates into xout[0, n)
@@ -2445,7 +2447,7 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_step, NT, 0);
     max_grid = sms * occ;
   }
-  if (grid > max_grid) return false;   // not co-resident: the caller runs the three-kernel sequence
+  if (grid > max_grid) grid = max_grid;   // co-residency bound of the cooperative launch (grid-stride loops)
   DevCSR C = Cf;
   DevFactor F{};
   DevCSR Ct{};
