@@ -2363,7 +2363,8 @@ __global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z,
 // round trip and the result is bit-identical to the three-kernel sequence; block 0 writes the state.
 // Phase A's partials live in partial[0, G), phase B's in partial[G, 3G), so no block overwrites a
 // partial another block is still reading.
-__global__ void __launch_bounds__(NT, 2) k_pcg_step(DevCSR Cf, const int32_t* longr, int64_t nlong, int prec,
+template <int BA, int BD, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_pcg_step(DevCSR Cf, const int32_t* longr, int64_t nlong, int prec,
                                                  const double* D, double* p, const double* w, double* q, double* x,
                                                  double* r, double* z, double* partial, PcgState* st, int next_rhs,
                                                  DevFactor F, DevCSR Ct, double* xout, double* ubuf) {
@@ -2376,7 +2377,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_step(DevCSR Cf, const int32_t* lo
   const int64_t m2 = Cf.nrows, G = gridDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = G * NT;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  const double loc = kf_rows<8>(Cf, longr, nlong, D, p, w, q);
+  const double loc = kf_rows<BA>(Cf, longr, nlong, D, p, w, q);
   double v = block_reduce<0>(loc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = v;
   grid.sync();
@@ -2418,7 +2419,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_step(DevCSR Cf, const int32_t* lo
     grid.sync();
     const int64_t N = next_rhs == 1 ? F.N : Ct.nrows, rc0 = F.fl_rc0;
     for (int64_t cI = i0; cI < N; cI += stride) {
-      const double v = cI < Ct.nrows ? csr_dot<16>(Ct, cI, p) : 0.0;
+      const double v = cI < Ct.nrows ? csr_dot<BD>(Ct, cI, p) : 0.0;
       if (next_rhs >= 2) {
         ubuf[cI] = v;
         if (next_rhs == 3) xout[cI] = 0.0;   // dense W: the GEMV accumulates into xout[0, n)
@@ -2439,14 +2440,20 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_step(DevCSR Cf, const int32_t* lo
 bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, const double* D, double* p,
               const double* w, double* q, double* x, double* r, double* z, double* partial, PcgState* st, int grid,
               cudaStream_t s, int next_rhs, const DevFactor* Fp, const DevCSR* Ctp, double* xout, double* ubuf) {
-  static int max_grid = -1;
-  if (max_grid < 0) {
-    int dev = 0, sms = 0, occ = 0;
+  // small m2 (grid ≤ 2 CTAs per SM): wide CSR batches (one load round per row of C and of Cᵀ, 94 registers);
+  // large m2: 4-entry batches at 4 CTAs per SM (more rows in flight)
+  static int sms = 0, max_wide = 0, max_narrow = 0;
+  if (!sms) {
+    int dev = 0, o1 = 0, o2 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_step, NT, 0);
-    max_grid = sms * occ;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_pcg_step<8, 16, 2>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_pcg_step<4, 4, 4>, NT, 0);
+    max_wide = sms * o1;
+    max_narrow = sms * o2;
   }
+  const bool wide = grid <= 2 * sms;
+  const int max_grid = wide ? max_wide : max_narrow;
   if (grid > max_grid) grid = max_grid;   // co-residency bound of the cooperative launch (grid-stride loops)
   DevCSR C = Cf;
   DevFactor F{};
@@ -2456,7 +2463,8 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
   if (next_rhs && (!Ctp || (next_rhs == 1 && !Fp) || (next_rhs == 3 && !xout))) next_rhs = 0;
   void* args[] = {&C, &longr, &nlong, &prec, &D, &p, &w, &q, &x, &r, &z, &partial, &st, &next_rhs, &F, &Ct, &xout,
                   &ubuf};
-  return cudaLaunchCooperativeKernel((const void*)k_pcg_step, grid, NT, args, 0, s) == cudaSuccess;
+  const void* fn = wide ? (const void*)k_pcg_step<8, 16, 2> : (const void*)k_pcg_step<4, 4, 4>;
+  return cudaLaunchCooperativeKernel(fn, grid, NT, args, 0, s) == cudaSuccess;
 }
 
 void kf_q(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D, const double* p, const double* z,
