@@ -123,3 +123,24 @@ def test_flattened_forest_c1():
     D, p = rng.uniform(0.5, 2.0, qp.m2), rng.standard_normal(qp.m2)
     q1, q0 = s.kf_apply(D, p), s0.kf_apply(D, p)
     assert np.linalg.norm(q1 - q0) <= 1e-11 * np.linalg.norm(q0)
+
+
+def test_dense_w_c1():
+    """c1's PCG K_F products use the explicit x-block W = (F⁻¹)₁₁: the setup guard agreed with
+    an F-solve to 1e-12, and one P_L PCG iteration (x₁ = ρ/(pᵀK_F p)·p, p = D⁻¹b), whose product goes
+    through W, matches the same formula with K_F p from the F-solve path (qp_kf_apply) to 1e-11."""
+    from paper_2104_12916_b200.binding import from_qp
+    qp = qpgen.make("c1")
+    s = from_qp(qp)
+    s.ipm_factor_once("low")
+    st = s.stats()
+    assert st["dense_w_enabled"] == 1.0 and 0 <= st["dense_w_discrepancy"] <= 1e-12
+    assert st["kf_bytes_W"] == 4.0 * qp.n * (qp.n + 1)
+    rng = np.random.default_rng(13)
+    D, b = rng.uniform(0.5, 2.0, qp.m2), rng.standard_normal(qp.m2)
+    x1, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=1)
+    p = b / D
+    Kp = s.kf_apply(D, p)
+    ref = (b @ p) / (p @ Kp) * p
+    assert it == 1
+    assert np.linalg.norm(x1 - ref) <= 1e-11 * np.linalg.norm(ref)
