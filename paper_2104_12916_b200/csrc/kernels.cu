@@ -2020,10 +2020,7 @@ void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cud
     k_flat_fwd_t<<<gt, NT, 0, s>>>(F, r.done_flag);
     return;
   }
-  const int skip = std::getenv("QPB_FLAT_SKIP") ? std::atoi(std::getenv("QPB_FLAT_SKIP")) : 0;  // TEMP
-  int64_t nY = (F.fl_rc0 + 7) / 8, nRr = (F.N - F.fl_rc0 + 7) / 8;
-  if (skip & 1) nY = 0;
-  if (skip & 2) nRr = 0;
+  const int64_t nY = (F.fl_rc0 + 7) / 8, nRr = (F.N - F.fl_rc0 + 7) / 8;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nY + nRr, (int64_t)sms * 8));
   if (nY + nRr > 0) k_flat_fwd<<<grid, NT, 0, s>>>(F, r.done_flag, nY, nY + nRr);
 }
@@ -2035,12 +2032,9 @@ void flat_backward(const DevFactor& F, double* x, const int* done_flag, int sms,
     k_flat_bwd_t<<<gt, NT, 0, s>>>(F, x, done_flag);
     return;
   }
-  const int skip = std::getenv("QPB_FLAT_SKIP") ? std::atoi(std::getenv("QPB_FLAT_SKIP")) : 0;  // TEMP
-  int64_t nX = (F.fl_rc0 + 7) / 8;
-  if (skip & 4) nX = 0;
-  const int64_t t0 = (skip & 8) ? F.fl_nmt : 0;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(F.fl_nmt + nX - t0, 1), (int64_t)sms * 8));
-  if (F.fl_nmt + nX - t0 > 0) k_flat_bwd<<<grid, NT, 0, s>>>(F, x, done_flag, nX, t0);
+  const int64_t nX = (F.fl_rc0 + 7) / 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(F.fl_nmt + nX, 1), (int64_t)sms * 8));
+  k_flat_bwd<<<grid, NT, 0, s>>>(F, x, done_flag, nX, 0);
 }
 void flat_extract(const DevFactor& F, int64_t col, const double* x, double* unit, int64_t prev, cudaStream_t s) {
   k_flat_extract<<<8, NT, 0, s>>>(F, col, x, unit, prev);

@@ -23,8 +23,6 @@ s.pcg_solve(D, b, tol=0.0, maxit=50)        # graphs captured, warm
 import os
 if os.environ.get('TL_PROFILE'):
     s.profile(True)                          # CUDA events around every section, no graphs
-if os.environ.get('TL_SKIP'):
-    os.environ['QPB_FLAT_SKIP'] = os.environ['TL_SKIP']   # timing-only switch, after the setup's guards
 s.debug_timeline(True)
 if os.environ.get('TL_KF'):                  # K_F products only (works with timing-only switches)
     for _ in range(iters):
