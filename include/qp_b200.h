@@ -233,7 +233,8 @@ typedef struct {
   double flat_nnz_M;                 /* stored entries of M */
   double dense_w_enabled;            /* 1 if PCG's K_F products use the explicit x-block W = (F⁻¹)₁₁ */
   double dense_w_discrepancy;        /* ‖W·u − (F⁻¹[u; 0])ₓ‖/‖·‖ of its factor-time guard (−1: not built) */
-  double kf_bytes_W;                 /* bytes of W read per K_F product: 8·n(n+1)/2 (0 when not in use) */
+  double kf_bytes_W;                 /* bytes of W this rank reads per K_F product: 8·n(n+1)/2, times the
+                                        rank's share of W's chunks in sharded mode (0 when not in use) */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 

@@ -286,6 +286,8 @@ struct qp_ctx {
   unsigned long long* tl_buf = nullptr;   // qp_debug_timeline
   double* dense_w = nullptr;         // explicit (F⁻¹)₁₁ (build_dense_w), column-major, leading dimension dw_ld
   int64_t dw_ld = 0, dw_nch = 0;
+  int64_t dw_c0 = 0, dw_c1 = 0;      // this rank's chunk range (all chunks unless sharded)
+  double dw_share = 1.0;             // its share of W's bytes
   const int2* dw_chunks = nullptr;
   double dw_discrepancy = -1.0;
   const int32_t* long_c = nullptr;   // rows of C with > KF_LONG_ROW entries (k_pcg_step)
@@ -768,20 +770,27 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
   SweepRhs r{};
   r.done_flag = pcg_mode ? &c->pst->done : nullptr;
   if (c->dense_w && (rhs_ready || pcg_mode)) {   // w = W·Cᵀp
-    if (!rhs_ready) {   // (P_H PCG: not fused) Cᵀp into ubuf, w accumulator zeroed
+    if (!rhs_ready) {   // (P_H or sharded PCG: not fused) Cᵀp into ubuf, w accumulator zeroed
       spmv(c->Ctf, p, c->ubuf, r.done_flag, c->vgrid, c->stream);
-      cudaMemsetAsync(c->xbuf, 0, c->n * 8, c->stream);
       c->launches += 1;
+      if (int rc = c->allreduce(c->ubuf, c->n, 0)) return rc;   // u = Σ_ranks C_gᵀ p_g
+      cudaMemsetAsync(c->xbuf, 0, c->n * 8, c->stream);
     }   // else ubuf = Cᵀp and xbuf[0, n) = 0 come from the fused step's phase D
     int h = c->begin(9);
-    dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks, c->dw_nch, c->ubuf, c->xbuf, r.done_flag, c->sm_count,
-               c->stream);
+    dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks + c->dw_c0, c->dw_c1 - c->dw_c0, c->ubuf, c->xbuf,
+               r.done_flag, c->sm_count, c->stream);
     c->end(h);
     c->launches += 1;
+    if (int rc = c->allreduce(c->xbuf, c->n, 0)) return rc;       // w = Σ_ranks (this rank's chunks)·u
     if (fsolve_only) return 0;
     h = c->begin(2);
     kf_q(c->Cf, c->long_c, c->n_long_c, D, p, c->xbuf, q, c->partial, c->pst, c->vgrid, c->stream, pcg_mode);
     c->end(h);
+    if (c->sharded && pcg_mode) {
+      if (int rc = c->allreduce(pst_red(c), 1, 0)) return rc;
+      finalize(FIN_PCG_PQ, c->pst, c->ist, c->precond, c->stream);
+      c->launches += 1;
+    }
     return 0;
   }
   r.rhs_ready = rhs_ready && c->FF.d.flat ? 1 : 0;
@@ -1464,7 +1473,7 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
 // random right-hand side (≤ 1e-10 relative) before it is used.  QPB_DENSE_W=0 disables it, =2 forces it
 // whenever it fits (tests).
 int build_dense_w(qp_ctx* c) {
-  if (c->dense_w || c->sharded) return QP_OK;
+  if (c->dense_w) return QP_OK;
   const char* e = std::getenv("QPB_DENSE_W");
   if (e && e[0] == '0') return QP_OK;
   qp_stats s{};
@@ -1503,14 +1512,47 @@ int build_dense_w(qp_ctx* c) {
   if (int rc = cuda_check(c, "dense W columns")) return rc;
   // chunk list: row block I, first column block K0 (≤ 8 blocks of 64 columns up to the diagonal block)
   std::vector<int32_t> ch;
+  std::vector<double> cb;   // bytes per chunk (rows × columns read), for the sharded split below
   const int64_t nb = (n + 63) / 64;
   for (int64_t I = 0; I < nb; ++I)
     for (int64_t K0 = 0; K0 <= I; K0 += 8) {
       ch.push_back((int32_t)I);
       ch.push_back((int32_t)K0);
+      const int64_t rows = std::min<int64_t>(64, n - 64 * I);
+      cb.push_back((double)rows * (double)(std::min<int64_t>(64 * K0 + 512, 64 * I + rows) - 64 * K0));
     }
   c->dw_chunks = reinterpret_cast<const int2*>(c->mem.upload(ch, st));
   c->dw_nch = (int64_t)ch.size() / 2;
+  // Sharded rows: W is replicated like the F factor, and rank g applies only the contiguous run of
+  // chunks [dw_c0, dw_c1) holding its 1/world of the lower triangle's bytes; its partial w (both the
+  // x_I and the transposed x_K contributions) is summed over ranks by one all-reduce of n doubles.
+  c->dw_c0 = 0;
+  c->dw_c1 = c->dw_nch;
+  if (c->sharded && c->world > 1) {
+    double tot = 0;
+    for (double v : cb) tot += v;
+    double acc = 0;
+    int64_t c0 = -1, c1 = c->dw_nch;
+    for (int64_t i = 0; i < c->dw_nch; ++i) {
+      const int owner = std::min<int>(c->world - 1, (int)(acc * c->world / tot));
+      if (owner == c->rank && c0 < 0) c0 = i;
+      if (owner > c->rank) {
+        c1 = i;
+        break;
+      }
+      acc += cb[i];
+    }
+    c->dw_c0 = c0 < 0 ? c1 : c0;
+    c->dw_c1 = c1;
+  }
+  {
+    double tot = 0, mine = 0;
+    for (int64_t i = 0; i < c->dw_nch; ++i) {
+      tot += cb[i];
+      if (i >= c->dw_c0 && i < c->dw_c1) mine += cb[i];
+    }
+    c->dw_share = tot > 0 ? mine / tot : 1.0;
+  }
   cudaStreamSynchronize(st);
   // accuracy guard: W·u against the x-part of an F-solve on [u; 0]
   std::vector<double> u(N, 0.0), y1(n), y2(n);
@@ -2064,7 +2106,7 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->flat_nnz_M = (double)S.fl_msize;
     s->dense_w_enabled = c->dense_w ? 1.0 : 0.0;
     s->dense_w_discrepancy = c->dw_discrepancy;
-    s->kf_bytes_W = c->dense_w ? 4.0 * (double)c->n * (double)(c->n + 1) : 0.0;
+    s->kf_bytes_W = c->dense_w ? 4.0 * (double)c->n * (double)(c->n + 1) * c->dw_share : 0.0;
   }
   return QP_OK;
 }

@@ -178,3 +178,52 @@ def test_nccl_world1_matches_unsharded():
     r2 = s2.ipm_solve(ipm_tol=1e-10)
     assert r1["converged"] and r2["converged"]
     assert abs(r1["objective"] - r2["objective"]) <= 1e-10 * max(1.0, abs(r1["objective"]))
+
+
+DENSE_M1 = dict(n=400, m1=200, m2=500, seed=6, g_nnz=8)   # W = (F⁻¹)₁₁ chosen by bytes (tests/test_gpu_paths.py)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_dense_w_pcg_matches_oracle(world):
+    """Sharded rows with the explicit W: every rank applies its contiguous run of W's lower-triangle
+    chunks and the partial w are summed by the all-reduce; the concatenated PCG solution matches the
+    oracle at fixed iterations (1e-8, reading R16) and every rank took the same decisions."""
+    d = dict(DENSE_M1)
+    qp = qpgen.scaled_random_qp(d.pop("n"), d.pop("m1"), d.pop("m2"), **d)
+    rng = np.random.default_rng(11)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    fs = make_fsolver(qp.H, qp.A)
+
+    def body(rank, comm):
+        s = _solver(qp, rank, world, comm)
+        assert s.stats()["dense_w_enabled"] == 1.0
+        sl = slice(s.row0, s.row0 + s.m2)
+        x, it, rr, rc = s.pcg_solve(D[sl], b[sl], tol=0.0, maxit=12)
+        s.close()
+        return s.row0, x, it
+    res = run_ranks(world, body)
+    xs = np.concatenate([r[1] for r in res])
+    assert {r[2] for r in res} == {12}
+    xo, ito, _, _, _ = pcg(lambda p: KF_apply(qp, fs, D, p), b, lambda r: r / D, 0.0, 12)
+    assert np.linalg.norm(xs - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_sharded_dense_w_ipm_matches_oracle(monkeypatch):
+    """c0 with W forced (QPB_DENSE_W=2) on two ranks: the sharded IPM reaches the oracle's objective."""
+    from oracle.ipm import ipm_solve as oracle_ipm
+    monkeypatch.setenv("QPB_DENSE_W", "2")
+    qp = qpgen.make("c0")
+    ref = oracle_ipm(qp, precond="low", ipm_tol=1e-10)
+
+    def body(rank, comm):
+        s = _solver(qp, rank, 2, comm)
+        assert s.stats()["dense_w_enabled"] == 1.0
+        r = s.ipm_solve(ipm_tol=1e-10, max_ipm=100)
+        s.close()
+        return r
+    res = run_ranks(2, body)
+    for r in res:
+        assert r["converged"]
+        assert abs(r["objective"] - ref.objective) <= 1e-8 * max(1.0, abs(ref.objective))
+    assert res[0]["pcg_iters"] == res[1]["pcg_iters"]
