@@ -502,8 +502,8 @@ def run_ours(args, rank, world, local, use_dist):
                    "space": args.space,
                    "n": qp.n, "m1": qp.m1, "m2": qp.m2, "nnz_LF": st["nnz_LF"], "precond": args.precond,
                    "ipm_steps_timed": steps_done, "pcg_iters_timed": pcg_timed,
-                   "l2": "no flush: the factor read every sweep (%.2f GB) exceeds L2" % (st["factor_bytes"] / 1e9),
-                   "parallelism": (f"sharded inequality rows x{world} (NCCL all-reduce, replicated F-solve)"
+                   "l2": ("no flush: every K_F product reads W (%.2f GB) and every full F-solve the factor (%.2f GB), both exceed L2" % (st["kf_bytes_W"] / 1e9, st["factor_bytes"] / 1e9)) if st.get("dense_w_enabled", 0) else ("no flush: the factor read every sweep (%.2f GB) exceeds L2" % (st["factor_bytes"] / 1e9)),
+                   "parallelism": (f"sharded inequality rows x{world} (NCCL all-reduce; " + ("W chunks split over ranks" if st.get("dense_w_enabled", 0) else "replicated F-solve") + ")"
                                    if sharded else (f"replicas x{world}" if world > 1 else "single GPU"))},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         "ipm_solve": ipm,
