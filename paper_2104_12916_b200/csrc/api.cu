@@ -757,6 +757,8 @@ void f_solve_dev(qp_ctx* c, const double* rhs_f, double* out) {
 }
 
 // q = K_F p (a1–a5): Cᵀp fused into the forward sweep, F-solve, q = D∘p − C w.
+constexpr int NT_HOST = 256;   // threads per CTA of the vector kernels (kernels.cuh NT)
+
 static bool pregather_on() {
   static const bool on = !(std::getenv("QPB_PREGATHER") && std::getenv("QPB_PREGATHER")[0] == '0');
   return on;
@@ -877,9 +879,10 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
   const bool fused = fused_env && prec != 2 && !c->sharded;
   // its grid: whole multiples of the SM count, about two rows of m2 per thread (fewer blocks make the two
   // grid syncs and the per-block partial sums cheaper on small m2), at most the vector-kernel grid
+  static const int rows_per_thread = std::getenv("QPB_STEP_RPT") ? std::max(1, std::atoi(std::getenv("QPB_STEP_RPT"))) : 2;
+  const int64_t per_wave = (int64_t)c->sm_count * NT_HOST * rows_per_thread;
   const int step_grid = (int)std::min<int64_t>(
-      c->vgrid, (int64_t)c->sm_count * std::max<int64_t>(1, (m2 + (int64_t)c->sm_count * 512 - 1) /
-                                                                 ((int64_t)c->sm_count * 512)));
+      c->vgrid, (int64_t)c->sm_count * std::max<int64_t>(1, (m2 + per_wave - 1) / per_wave));
   // phase D of the fused step prepares the next iteration's u = Cᵀp (flattened forest or pregathered
   // sweeps); the first iteration's comes from the usual kernel
   const int next_rhs = !fused ? 0 : c->dense_w ? 3 : c->FF.d.flat ? 1 : pregather_on() ? 2 : 0;

@@ -112,3 +112,26 @@ def test_path_variant_matches_oracle(oracle_case, variant):
     if obj is not None:
         assert out["converged"]
         assert abs(out["obj"] - obj) <= 1e-8 * max(1.0, abs(obj))
+
+
+def test_debug_timeline_records_pcg_launches():
+    """qp_debug_timeline: one fused PCG step per iteration (inside and outside the CUDA graph), every
+    recorded launch has start ≤ end, and launches of one kernel do not overlap (stream order)."""
+    from paper_2104_12916_b200.binding import from_qp
+    qp = qpgen.make("c0")
+    s = from_qp(qp)
+    s.ipm_factor_once("low")
+    rng = np.random.default_rng(3)
+    D, b = rng.uniform(0.5, 2.0, qp.m2), rng.standard_normal(qp.m2)
+    s.pcg_solve(D, b, tol=0.0, maxit=10)          # graph captured
+    s.debug_timeline(True)
+    x, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=10)
+    ev = s.debug_timeline(False)
+    assert it == 10
+    assert sum(1 for k, a, e in ev if k == 4) == 10     # k_pcg_step
+    assert sum(1 for k, a, e in ev if k == 2) >= 10     # the dense GEMV of every F-solve (S⁻¹ or W)
+    assert all(a <= e for k, a, e in ev)
+    for kk in {k for k, a, e in ev}:
+        spans = sorted((a, e) for k, a, e in ev if k == kk)
+        assert all(e0 <= a1 for (a0, e0), (a1, e1) in zip(spans, spans[1:]))
+    s.close()
