@@ -121,7 +121,10 @@ int qp_setup(qp_ctx** ctx, const qp_csr* H, const qp_csr* A, const qp_csr* C,
  * on the GPU with static 1×1 pivots and an inertia check (x pivots < 0,
  * λ pivots > 0) → QP_ENOTSPD on failure.  For QP_PREC_HIGH also
  * T = C·diag(H)⁻¹·Cᵀ and the symbolic analysis of D + T; D0 (m2
- * values, may be NULL = ones) gives the first numeric P_H factor. */
+ * values, may be NULL = ones) gives the first numeric P_H factor.  When it
+ * reads fewer bytes than one F-solve (and fits), the explicit x-block
+ * W = (F⁻¹)₁₁ is also formed here and guarded against an
+ * F-solve (≤ 1e-10); PCG's K_F products then use it (qp_stats.dense_w_*). */
 int ipm_factor_once(qp_ctx* ctx, const double* D0, qp_precond p);
 
 /* Solve K_F(D_k) Δν = rhs from Δν = 0 by PCG with the preconditioner chosen
