@@ -13,7 +13,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else 'c1'
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 qp = qpgen.make(name)
 s = from_qp(qp)
-s.ipm_factor_once('low')
+import os
+s.ipm_factor_once(os.environ.get('TL_PREC', 'low'))
 _st = s.stats()
 print('flat', _st['flat_enabled'], 'discrepancy %.2e' % _st['flat_discrepancy'])
 rng = np.random.default_rng(0)
