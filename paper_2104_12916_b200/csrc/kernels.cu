@@ -138,6 +138,17 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   const int n = ok ? 8 : 0;   // src-size 0 ⇒ zero fill
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
 }
+// 16-byte copy (two rows of one column) when the global address is 16-byte aligned and both rows are in
+// range; otherwise two 8-byte copies (zero fill for rows out of range)
+__device__ __forceinline__ void cp_async_pair(double* smem, const double* gmem, bool ok0, bool ok1) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (ok0 && ok1 && ((reinterpret_cast<uintptr_t>(gmem) & 15) == 0)) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(ok0 ? 8 : 0));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa + 8), "l"(ok1 ? gmem + 1 : gmem), "r"(ok1 ? 8 : 0));
+  }
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
@@ -536,6 +547,129 @@ __global__ void __launch_bounds__(128) k_mf_update8x4(DevFactor F, int k, int k0
   }
 }
 
+// Default UPDATE (QPB_UPD=4): k_mf_update8x4 with D_k applied to the B fragments in registers (4 DMUL per
+// k-step) instead of a shared-memory scaling pass and its barrier per chunk, and 16-byte cp.async for row
+// pairs where the column's address allows
+// (c1 P_H refactor 1.064 → 1.008 s; ncu had the scaling pass at 17 % and the cp.async at 22 % of the
+// instructions; 16-byte read-modify-writes in the epilogue were measured slower, 1.054 s).
+__global__ void __launch_bounds__(128) k_mf_update8x4r(DevFactor F, int k, int k0g, int mode, int64_t act_off, int n_act,
+                                                  int64_t pref_off) {
+  constexpr int KC = 16, LD = 64 + 4;
+  __shared__ __align__(16) double As[2][KC * LD];
+  __shared__ __align__(16) double Bs[2][KC * LD];
+  __shared__ double Dk[4 * MF_BW];
+  const int64_t* pref = F.upd_pref + pref_off;
+  const int a = find_seg(pref, n_act + 1, blockIdx.x);
+  const int J = F.act[act_off + a];
+  const int64_t c0 = F.sn_start[J], w = F.sn_start[J + 1] - c0;
+  const int64_t m = F.sn_rowptr[J + 1] - F.sn_rowptr[J];
+  const int64_t fo = F.front_off[J];
+  const int64_t nk = (w + MF_BW - 1) / MF_BW;
+  const int64_t ntile = nk + (m - w + MF_BW - 1) / MF_BW;
+  const int64_t e = min((int64_t)k0g + F.mf_group, nk) - 1;   // last pivot block of this front's group
+  int64_t q = blockIdx.x - pref[a];
+  int64_t ti, tj;
+  int kfirst, nblk;   // pivot blocks kfirst .. kfirst + nblk − 1 are applied
+  if (mode == 2) {    // band: block k on block columns k+1 .. e, rows ≥ the column
+    tj = k + 1;
+    while (q >= ntile - tj) {
+      q -= ntile - tj;
+      ++tj;
+    }
+    ti = tj + q;
+    kfirst = k;
+    nblk = 1;
+  } else {            // trailing triangle from block column e+1, all the group's blocks
+    int64_t ii = (int64_t)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+    while (ii * (ii + 1) / 2 > q) --ii;
+    while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+    const int64_t jj = q - ii * (ii + 1) / 2;
+    ti = e + 1 + ii;
+    tj = e + 1 + jj;
+    kfirst = k0g;
+    nblk = (int)(e - k0g + 1);
+  }
+  const int64_t p0 = (int64_t)MF_BW * kfirst;
+  const int kt = (int)(min((int64_t)MF_BW * (kfirst + nblk), w) - p0);   // pivot columns applied
+  const int b0 = F.sn_blk0[J] + kfirst;
+  const int64_t ib = tile_begin(ti, nk, w, m), ie = tile_begin(ti + 1, nk, w, m);
+  const int64_t jb = tile_begin(tj, nk, w, m), je = tile_begin(tj + 1, nk, w, m);
+  const int Ri = (int)(ie - ib), Rj = (int)(je - jb);
+  constexpr int UT = 128;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  for (int t = tid; t < kt; t += UT) Dk[t] = F.Dpiv[c0 + p0 + t];
+  {   // pull the C tile into L2 now so the read-modify-write epilogue does not wait on HBM
+    for (int t = tid; t < 256; t += UT) {   // 64 columns × 4 lines of 16 doubles
+      const int cc = t >> 2, seg = t & 3;
+      if (cc < Rj && seg * 16 < Ri) prefetch_l2(F.ws + fo + (jb + cc) * m + ib + seg * 16);
+    }
+  }
+  auto load = [&](int buf, int kc0) {   // chunk of 16 pivot columns: block kfirst + kc0/64 (all but the last are 64 wide)
+    const int bi = kc0 / MF_BW, kb = kc0 - bi * MF_BW;
+    const int64_t pb = p0 + (int64_t)bi * MF_BW;
+    const int wl = (int)(min(pb + MF_BW, w) - pb);
+    const int64_t ns = F.blk_noff[b0 + bi];
+    const double* Ls = F.fstore + F.blk_off[b0 + bi] - (pb + wl);   // index by front row
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {   // row pairs: 16-byte copies where the column's address allows
+      const int idx = tid + UT * u;
+      const int r = (idx & 31) * 2, c = idx >> 5;
+      const bool okc = kb + c < wl;
+      const int64_t co = (int64_t)(kb + c) * ns;
+      cp_async_pair(&As[buf][c * LD + r], Ls + (okc ? ib + r + co : 0), okc && r < Ri, okc && r + 1 < Ri);
+      cp_async_pair(&Bs[buf][c * LD + r], Ls + (okc ? jb + r + co : 0), okc && r < Rj, okc && r + 1 < Rj);
+    }
+    cp_async_commit();
+  };
+  double acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  load(0, 0);
+  int buf = 0;
+  for (int k0 = 0; k0 < kt; k0 += KC) {
+    cp_async_wait_all();
+    __syncthreads();
+    if (k0 + KC < kt) load(buf ^ 1, k0 + KC);
+    const double* as = As[buf];
+    const double* bs = Bs[buf];
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double av[8], bv[4];
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {   // rows 2tx + 16 i2 + {0, 1}
+        const double2 a = *reinterpret_cast<const double2*>(as + kk * LD + 16 * i2 + tx * 2);
+        av[2 * i2] = a.x;
+        av[2 * i2 + 1] = a.y;
+      }
+      const double dk = (k0 + kk < kt) ? Dk[k0 + kk] : 0.0;   // D_k applied in registers (no scaling pass)
+#pragma unroll
+      for (int j2 = 0; j2 < 2; ++j2) {   // columns 2ty + 32 j2 + {0, 1}
+        const double2 b = *reinterpret_cast<const double2*>(bs + kk * LD + 32 * j2 + ty * 2);
+        bv[2 * j2] = b.x * dk;
+        bv[2 * j2 + 1] = b.y * dk;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int s = (j >> 1) * 32 + ty * 2 + (j & 1);
+    if (s >= Rj) continue;
+    double* col = F.ws + fo + (jb + s) * m + ib;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = (i >> 1) * 16 + tx * 2 + (i & 1);
+      if (r < Ri) col[r] -= acc[i][j];
+    }
+  }
+}
+
 void mf_assemble_level(const DevFactor& F, int64_t fr_off, int64_t n_fr, int64_t zero_total, int64_t asm_off,
                        int64_t n_asm, const double* src_vals, const double* D, const int64_t* perm, cudaStream_t s) {
   if (zero_total > 0) {
@@ -566,8 +700,9 @@ void mf_step(const DevFactor& F, int k, int k0, int kind, int64_t act_off, int n
     k_mf_diag<<<n_act, NT, sd, s>>>(F, k, act_off);
     if (pan_total > 0) k_mf_panel<<<(unsigned)pan_total, NT, sp, s>>>(F, k, act_off, n_act, pref_off);
   } else if (upd_total > 0) {
-    static const int var = std::getenv("QPB_UPD") ? std::atoi(std::getenv("QPB_UPD")) : 2;
-    if (var == 2) k_mf_update8x4<<<(unsigned)upd_total, 128, 0, s>>>(F, k, k0, kind, act_off, n_act, pref_off);
+    static const int var = std::getenv("QPB_UPD") ? std::atoi(std::getenv("QPB_UPD")) : 4;
+    if (var == 4) k_mf_update8x4r<<<(unsigned)upd_total, 128, 0, s>>>(F, k, k0, kind, act_off, n_act, pref_off);
+    else if (var == 2) k_mf_update8x4<<<(unsigned)upd_total, 128, 0, s>>>(F, k, k0, kind, act_off, n_act, pref_off);
     else k_mf_update<<<(unsigned)upd_total, NT, 0, s>>>(F, k, k0, kind, act_off, n_act, pref_off);
   }
 }
