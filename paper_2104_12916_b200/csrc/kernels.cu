@@ -552,12 +552,12 @@ __global__ void __launch_bounds__(128) k_mf_update8x4(DevFactor F, int k, int k0
 // pairs where the column's address allows
 // (c1 P_H refactor 1.064 → 1.008 s; ncu had the scaling pass at 17 % and the cp.async at 22 % of the
 // instructions; 16-byte read-modify-writes in the epilogue were measured slower, 1.054 s).
-__global__ void __launch_bounds__(128) k_mf_update8x4r(DevFactor F, int k, int k0g, int mode, int64_t act_off, int n_act,
+__global__ void __launch_bounds__(128, 4) k_mf_update8x4r(DevFactor F, int k, int k0g, int mode, int64_t act_off, int n_act,
                                                   int64_t pref_off) {
   constexpr int KC = 16, LD = 64 + 4;
   __shared__ __align__(16) double As[2][KC * LD];
   __shared__ __align__(16) double Bs[2][KC * LD];
-  __shared__ double Dk[4 * MF_BW];
+  __shared__ __align__(16) double Dk[4 * MF_BW + KC];
   const int64_t* pref = F.upd_pref + pref_off;
   const int a = find_seg(pref, n_act + 1, blockIdx.x);
   const int J = F.act[act_off + a];
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(128) k_mf_update8x4r(DevFactor F, int k, int k
   const int Ri = (int)(ie - ib), Rj = (int)(je - jb);
   constexpr int UT = 128;
   const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
-  for (int t = tid; t < kt; t += UT) Dk[t] = F.Dpiv[c0 + p0 + t];
+  for (int t = tid; t < 4 * MF_BW + KC; t += UT) Dk[t] = t < kt ? F.Dpiv[c0 + p0 + t] : 0.0;   // zero past kt
   {   // pull the C tile into L2 now so the read-modify-write epilogue does not wait on HBM
     for (int t = tid; t < 256; t += UT) {   // 64 columns × 4 lines of 16 doubles
       const int cc = t >> 2, seg = t & 3;
@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(128) k_mf_update8x4r(DevFactor F, int k, int k
     if (k0 + KC < kt) load(buf ^ 1, k0 + KC);
     const double* as = As[buf];
     const double* bs = Bs[buf];
+    double2 dk2;   // D_k of k-steps kk, kk + 1 (one 16-byte shared load per two k-steps)
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
       double av[8], bv[4];
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(128) k_mf_update8x4r(DevFactor F, int k, int k
         av[2 * i2] = a.x;
         av[2 * i2 + 1] = a.y;
       }
-      const double dk = (k0 + kk < kt) ? Dk[k0 + kk] : 0.0;   // D_k applied in registers (no scaling pass)
+      const double dk = (kk & 1) ? dk2.y : (dk2 = *reinterpret_cast<const double2*>(Dk + k0 + kk)).x;   // D_k in registers
 #pragma unroll
       for (int j2 = 0; j2 < 2; ++j2) {   // columns 2ty + 32 j2 + {0, 1}
         const double2 b = *reinterpret_cast<const double2*>(bs + kk * LD + 32 * j2 + ty * 2);
