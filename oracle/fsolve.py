@@ -4,12 +4,14 @@ F = [−H Aᵀ; A 0]  (eq. f-def) is nonsingular for SPD 
 and full-row-rank A; its inertia is (n negative, m1 positive)
 (P:L714, Haynsworth).
 
-Two independent ways to apply F⁻¹:
+Three ways to apply F⁻¹:
 
 * ``DenseF``  — the explicit block inverse of P:L757–773 (eq. f-inv)
       F⁻¹ = [ −H⁻¹ + H⁻¹AᵀF_H⁻¹AH⁻¹ ,  H⁻¹AᵀF_H⁻¹ ]
             [        F_H⁻¹AH⁻¹        ,     F_H⁻¹   ],   F_H = AH⁻¹Aᵀ,
   applied with LAPACK Cholesky factors of H and of F_H (no LDLᵀ at all).
+* ``BlockF``  — the same block formula with SuperLU's LU of the SPD H and a
+  dense Cholesky of the m1 × m1 F_H: the full-size sparse configs;
 * ``SparseF`` — SuperLU LU of F permuted to the x-block order ``x_perm``
   with the λ block last, NATURAL column order and no pivoting
   (diag_pivot_thresh = 0), for the sparse configs.
@@ -93,8 +95,69 @@ class SparseF:
         return sol[:n], sol[n:]
 
 
+class BlockF:
+    """F⁻¹ through the block-inverse formula f-inv with a SPARSE factor of H.
+
+    Same algebra as ``DenseF`` — y = −H⁻¹r1 + H⁻¹Aᵀz, z = F_H⁻¹(AH⁻¹r1 + r2),
+    F_H = AH⁻¹Aᵀ — but H⁻¹ is applied through SuperLU's LU of the SPD H (no
+    pivoting needed: diag_pivot_thresh = 0) in a fill-reducing column order
+    (``x_perm`` when given, e.g. the generator's grid nested dissection, else
+    SuperLU's own minimum degree on H + Hᵀ, ``MMD_AT_PLUS_A``), and the small dense
+    F_H (m1 × m1) by LAPACK Cholesky.  No factor of F itself is formed, so this
+    route shares nothing with an LDLᵀ of F.  For the full-size configs
+    ("sparse" configs), where the dense H of ``DenseF`` does
+    not fit.
+    """
+
+    def __init__(self, H, A, x_perm=None, batch=256):
+        H = sp.csc_matrix(H)
+        A = sp.csr_matrix(A)
+        self.n, self.m1 = H.shape[0], A.shape[0]
+        self.A = A
+        if x_perm is not None:
+            p = np.asarray(x_perm, dtype=np.int64)
+            self.hp = p
+            Hp = H[p][:, p].tocsc()
+            self.lu = spla.splu(Hp, permc_spec="NATURAL", diag_pivot_thresh=0.0,
+                                options=dict(SymmetricMode=True))
+        else:
+            self.hp = None
+            self.lu = spla.splu(H, permc_spec="MMD_AT_PLUS_A", diag_pivot_thresh=0.0,
+                                options=dict(SymmetricMode=True))
+        if self.m1:
+            FH = np.empty((self.m1, self.m1))
+            At = A.T.tocsc()
+            for c0 in range(0, self.m1, batch):            # F_H = A (H⁻¹ Aᵀ), column batches
+                c1 = min(self.m1, c0 + batch)
+                HiAt = self.Hinv(At[:, c0:c1].toarray())
+                FH[:, c0:c1] = A @ HiAt
+            FH = 0.5 * (FH + FH.T)                            # exact symmetry of AH⁻¹Aᵀ (P:L773)
+            self.cFH = sla.cho_factor(FH, lower=True, overwrite_a=True)
+        else:
+            self.cFH = None
+
+    def Hinv(self, v):
+        v = np.asarray(v, dtype=float)
+        if self.hp is None:
+            return self.lu.solve(v)
+        out = np.empty_like(v)
+        out[self.hp] = self.lu.solve(v[self.hp])
+        return out
+
+    def solve(self, r1, r2=None):
+        """Return (y, z) = F⁻¹ (r1; r2), block by block as in f-inv."""
+        t = self.Hinv(r1)
+        if self.m1 == 0:
+            return -t, np.zeros((0,) + np.shape(r1)[1:])
+        if r2 is None:
+            r2 = np.zeros((self.m1,) + np.shape(r1)[1:])
+        z = sla.cho_solve(self.cFH, self.A @ t + r2)
+        y = -t + self.Hinv(self.A.T @ z)
+        return y, z
+
+
 def make_fsolver(H, A, x_perm=None, dense_limit=30000):
-    """Dense block formula up to ``dense_limit`` unknowns, SuperLU beyond."""
+    """Dense block formula up to ``dense_limit`` unknowns, the sparse-H block formula beyond."""
     if H.shape[0] + A.shape[0] <= dense_limit and x_perm is None:
         return DenseF(H, A)
-    return SparseF(H, A, x_perm)
+    return BlockF(H, A, x_perm)

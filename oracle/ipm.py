@@ -51,12 +51,14 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
               max_ipm: int = 100, sigma: float = 0.1, tau: float = 0.995,
               pcg_maxit: Optional[int] = None, fs=None, x_perm=None, record: bool = False,
               exact_ph: bool = False, direct: bool = False, forcing: bool = True,
-              space: str = "nu") -> IpmResult:
+              space: str = "nu", ph_opts: Optional[dict] = None) -> IpmResult:
     """Run the single-factorization inexact IPM.
 
     precond ∈ {"none" (U-KF), "low" (PL-KF), "high" (PH-KF)}.
     ``direct=True`` replaces PCG by a dense solve of K_F (trajectory reference).
     ``record=True`` stores (D_k, r_ν, Δν, PCG iterations) per IPM iteration.
+    ``ph_opts``: keyword options of ``kkt.PrecondH`` (sparse SuperLU factor / in-place dense factor
+    for the full-size configs).
     ``space="x"``: the x-space twin — projected CG on the augmented system K_C with the constraint
     preconditioner [H Aᵀ; A 0] = the F factor (oracle.xspace; `precond` is then ignored).
     """
@@ -112,7 +114,7 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
             if precond == "low":
                 M = kkt.PrecondL(D)
             elif precond == "high":
-                M = kkt.PrecondH(qp, D, T=T, exact=exact_ph)
+                M = kkt.PrecondH(qp, D, T=T, exact=exact_ph, **(ph_opts or {}))
             else:
                 M = kkt.PrecondNone()
             eps = min(pcg_tol, res["mu"]) if forcing else pcg_tol

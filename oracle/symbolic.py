@@ -19,8 +19,9 @@ same x-block permutation:
   the stored w·m − w(w−1)/2 entries (m = w_J + m_P rows);  a relaxed
   supernode's rows are its columns followed by the rows below its topmost
   fundamental supernode;
-* forced dense trailing supernode (input `trailing_from`, the library's choice like x_perm): after
-  amalgamation every supernode reaching that column merges with the last one;
+* forced dense trailing supernode (input `trailing_from`; ``analyse_auto`` derives it with
+  ``choose_trailing`` from the oracle's own structures): after amalgamation every supernode reaching
+  that column merges with the last one;
 * supernodal tree: parent of supernode J = supernode of parent(last col of J);
   level(J) = 0 for leaves, else 1 + max level(children);
 * row levels: lev(i) = 1 + max{lev(j) : j < i, L_ij ≠ 0}, 0 for rows with no
@@ -176,6 +177,46 @@ def row_levels(N, struct):
     return lev
 
 
+def choose_trailing(sn_start, sn_parent, sn_level, sn_rowptr, budget_frac=0.02, bw=64):
+    """Top-level absorption rule (DESIGN.md §4 "Top-level absorption"), decided from the oracle's
+    own supernodal structures: if the factor ends in a dense root R (no parent, width w_R > 64, no
+    rows below its columns) and the tree has more than 3 levels, take the lowest cut level L ≥ 1 such
+    that merging every supernode J ≠ R of level ≥ L into R adds at most 2 % of R's w_R(w_R+1)/2
+    entries as explicit zeros — Σ_J w_J·(w_R − (m_J − w_J)) for the rows of R each absorbed column
+    lacks, plus wsum²/2 for the triangle between the absorbed columns — and return the first column
+    of the absorbed block plus R (−1 when nothing is absorbed).  The absorbed columns must already be
+    contiguous before R (the library's reordering, an equivalent order with the same fill)."""
+    ns = len(sn_start) - 1
+    if ns < 2:
+        return -1
+    R = ns - 1
+    wR = int(sn_start[R + 1] - sn_start[R])
+    mR = int(sn_rowptr[R + 1] - sn_rowptr[R])
+    n_levels = int(np.max(sn_level)) + 1
+    if not (sn_parent[R] < 0 and wR > bw and mR == wR and n_levels > 3):
+        return -1
+    w = np.diff(np.asarray(sn_start, dtype=np.int64))[:R]
+    m = np.diff(np.asarray(sn_rowptr, dtype=np.int64))[:R]
+    lev = np.asarray(sn_level)[:R]
+    budget = budget_frac * wR * (wR + 1) / 2
+    best = n_levels - 1
+    for L in range(n_levels - 2, 0, -1):
+        sel = lev >= L
+        wsum = int(w[sel].sum())
+        zeros = float(np.sum(w[sel].astype(float) * (wR - (m[sel] - w[sel])))) + wsum * wsum / 2
+        if zeros > budget:
+            break
+        best = L
+    if best >= n_levels - 1:
+        return -1
+    sel = lev >= best
+    cols = np.concatenate([np.arange(sn_start[J], sn_start[J + 1]) for J in np.nonzero(sel)[0]] or [np.zeros(0, np.int64)])
+    first = int(sn_start[R]) - int(w[sel].sum())
+    if not np.array_equal(np.sort(cols), np.arange(first, int(sn_start[R]))):
+        return -1                                  # not contiguous before the root: no absorption in this order
+    return first
+
+
 def analyse(H, A, x_perm=None, trailing_from=-1):
     """All structures, as a dict of int64 arrays.  trailing_from: first column of a forced dense
     trailing supernode (the library's absorbed tree top, exported as structure 9), or -1."""
@@ -192,6 +233,7 @@ def analyse(H, A, x_perm=None, trailing_from=-1):
     m = np.diff(sn_rowptr)
     nnz_stored = int(np.sum(w * m - w * (w - 1) // 2))
     return dict(N=N, parent=parent, colcount=cc, sn_start=sn, fsn_start=fsn, nnz_stored=nnz_stored,
+                trailing_from=int(trailing_from) if 0 <= trailing_from < N else -1,
                 sn_parent=sparent,
                 sn_level=slevel, sn_rowptr=sn_rowptr, sn_rows=sn_rows, row_level=rlev,
                 nnz_L=int(cc.sum()), struct=struct)
@@ -204,3 +246,16 @@ def struct_hash(arr) -> str:
     h.update(np.int64(len(a)).tobytes())
     h.update(a.tobytes())
     return h.hexdigest()
+
+
+def analyse_auto(H, A, x_perm, absorb=True):
+    """``analyse`` with the trailing column chosen by the oracle itself (``choose_trailing`` on the
+    structures of the same order without a forced trailing supernode).  ``absorb`` = the library
+    chose the ordering itself (it never reorders a caller-supplied x_perm)."""
+    tf = -1
+    if absorb:
+        a0 = analyse(H, A, x_perm, trailing_from=-1)
+        tf = choose_trailing(a0["sn_start"], a0["sn_parent"], a0["sn_level"], a0["sn_rowptr"])
+        if tf < 0:
+            return a0
+    return analyse(H, A, x_perm, trailing_from=tf)

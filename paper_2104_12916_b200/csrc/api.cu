@@ -159,6 +159,15 @@ struct DeviceArena {
     cudaMemsetAsync(d, 0, std::max<size_t>(1, n) * sizeof(T), s);
     return d;
   }
+  // Free one allocation early (its size stays counted in `bytes`, an upper bound).
+  void free_ptr(void* p) {
+    for (size_t i = 0; i < ptrs.size(); ++i)
+      if (ptrs[i] == p) {
+        cudaFree(p);
+        ptrs.erase(ptrs.begin() + (long)i);
+        return;
+      }
+  }
 };
 
 struct Factor {
@@ -874,7 +883,7 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
     c->launches += 1;
   }
   // P_L / none on one GPU: a5 + a6 as one cooperative kernel (QPB_FUSED_PCG=0 restores k_kf_q,
-  // k_pcg_update1, k_pcg_update2 — bit-identical results)
+  // k_pcg_update1, k_pcg_update2 — equal up to the reduction order: they run on the vector grid)
   static const bool fused_env = !(std::getenv("QPB_FUSED_PCG") && std::getenv("QPB_FUSED_PCG")[0] == '0');
   const bool fused = fused_env && prec != 2 && !c->sharded;
   // its grid: whole multiples of the SM count, about two rows of m2 per thread (fewer blocks make the two
@@ -1469,6 +1478,18 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
   return rc;
 }
 
+// Sharded mode: turn a per-rank yes/no into one decision shared by every rank (min over ranks of 0/1),
+// through the same collective the PCG uses.  Uses xbuf[0] as device scratch (free at setup).
+static int agree_all(qp_ctx* c, bool& ok) {
+  double v = ok ? 1.0 : 0.0;
+  cudaMemcpyAsync(c->xbuf, &v, 8, cudaMemcpyHostToDevice, c->stream);
+  if (int rc = c->allreduce(c->xbuf, 1, 2)) return rc;
+  cudaMemcpyAsync(&v, c->xbuf, 8, cudaMemcpyDeviceToHost, c->stream);
+  if (int rc = sync_check(c, "rank agreement")) return rc;
+  ok = v > 0.5;
+  return QP_OK;
+}
+
 // Explicit x-block of F⁻¹ (DESIGN §5 "dense W"): W = (F⁻¹)₁₁ = −H⁻¹ + H⁻¹Aᵀ(AH⁻¹Aᵀ)⁻¹AH⁻¹ (n × n, factor
 // order, the block form of P:L757–787), so that the K_F product inside PCG is w = W·Cᵀp, one symmetric
 // GEMV reading 8·n(n+1)/2 bytes.  Used when that is fewer bytes than one F-solve (c0, c1) and W fits the
@@ -1491,7 +1512,19 @@ int build_dense_w(qp_ctx* c) {
     W = c->mem.zeros<double>((size_t)ld * (size_t)n, st);
   } catch (std::bad_alloc&) {
     cudaGetLastError();
-    return QP_OK;   // no room: keep the F-solve path
+    W = nullptr;    // no room: keep the F-solve path (sharded: every rank must agree, below)
+  }
+  if (c->sharded && c->world > 1) {
+    // The two K_F paths issue different collectives (W: all-reduce of u and of w; F-solve: of u only),
+    // so all ranks must take the same one: agree on the allocation first (min over ranks).
+    bool ok = W != nullptr;
+    if (int rc = agree_all(c, ok)) return rc;
+    if (!ok) {
+      if (W) c->mem.free_ptr(W);
+      return QP_OK;
+    }
+  } else if (!W) {
+    return QP_OK;
   }
   // Flattened forest with a symmetric root J0 = columns [r0, N): for a root column j the F-solve is
   // x2 = S⁻¹e_j, so W's root block is S⁻¹'s x-part, copied from its lower storage; only the forest
@@ -1579,7 +1612,14 @@ int build_dense_w(qp_ctx* c) {
   if (std::getenv("QPB_VERBOSE"))
     std::fprintf(stderr, "qpb: dense W (n = %lld, %.3g GB read per product) guard %.2e\n", (long long)n,
                  wbytes / 1e9, c->dw_discrepancy);
-  if (!(c->dw_discrepancy <= 1e-10)) return QP_OK;
+  bool ok = c->dw_discrepancy <= 1e-10;
+  if (c->sharded && c->world > 1)
+    if (int rc = agree_all(c, ok)) return rc;   // one decision for every rank (guard min over ranks)
+  if (!ok) {
+    cudaStreamSynchronize(st);
+    c->mem.free_ptr(W);
+    return QP_OK;
+  }
   c->dense_w = W;
   c->dw_ld = ld;
   return QP_OK;

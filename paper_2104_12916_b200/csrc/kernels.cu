@@ -14,6 +14,7 @@
 //    (P:L284–285);
 //  * IPM rhs / r_ν / recovery / Δs / step kernels (P:L65–69, P:L473–505,
 //    P:L727–752).
+#include <atomic>
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 #include "kernels.cuh"
@@ -690,12 +691,16 @@ void mf_extend_add(const DevFactor& F, int64_t grp_off, int64_t n_grp, cudaStrea
 void mf_step(const DevFactor& F, int k, int k0, int kind, int64_t act_off, int n_act, int64_t pref_off,
              int64_t pan_total, int64_t upd_total, cudaStream_t s) {
   if (n_act == 0) return;
-  static bool attr = false;
+  // The shared-memory attribute is per device: set it once per device (several contexts on several
+  // devices, or threads, may call this concurrently).
+  static std::atomic<uint8_t> attr[64];
   const size_t sd = 2 * 64 * 65 * 8, sp = (2 * 64 * 65 + 64) * 8;
-  if (!attr) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_acquire)) {
     cudaFuncSetAttribute(k_mf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
     cudaFuncSetAttribute(k_mf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp);
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev].store(1, std::memory_order_release);
   }
   if (kind == 0) {
     k_mf_diag<<<n_act, NT, sd, s>>>(F, k, act_off);
@@ -2312,8 +2317,8 @@ void flat_set_unit(double* unit, int64_t col, cudaStream_t s) { k_set_unit<<<1, 
 static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)TRSV_SMEM_DBL; }
 
 int trsv_grid(int device) {
-  static int cached[64] = {0};
-  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  static std::atomic<int> cached[64];
+  if (device >= 0 && device < 64 && cached[device].load()) return cached[device].load();
   int sms = 148, occ = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsv_smem_bytes());
@@ -2323,7 +2328,7 @@ int trsv_grid(int device) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_trsv_bwd, NT, trsv_smem_bytes());
   occ = std::max(1, std::min(o1, o2));
   int g = sms * occ;
-  if (device >= 0 && device < 64) cached[device] = g;
+  if (device >= 0 && device < 64) cached[device].store(g);
   return g;
 }
 
@@ -2622,7 +2627,8 @@ __global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z,
 //   convergence test, β = ρ'/ρ, p = z + βp.
 // The per-block partials are those of k_kf_q / k_pcg_update1 (same grid, same order), and every block
 // reduces them itself with reduce_partials, so all blocks take the same decision without another
-// round trip and the result is bit-identical to the three-kernel sequence; block 0 writes the state.
+// round trip; the result equals the three-kernel sequence's up to the reduction order (those kernels
+// run on the vector grid, this one on its own grid); block 0 writes the state.
 // Phase A's partials live in partial[0, G), phase B's in partial[G, 3G), so no block overwrites a
 // partial another block is still reading.
 template <int BA, int BD, int MINB>

@@ -342,3 +342,31 @@ def make(name: str, seed: int = 0) -> QP:
 def scaled_random_qp(n, m1, m2, seed=0, g_nnz=5, a_nnz=3, c_nnz=4, name=None):
     """Small random QPs of the config-0 family at other sizes (tests)."""
     return make_random_qp(n, m1, m2, g_nnz, a_nnz, c_nnz, seed, name or f"rand{n}_{m1}_{m2}")
+
+
+@dataclasses.dataclass
+class Probe:
+    """Seeded probe inputs for parity at full size (shared by the golden script and the GPU tests).
+
+    Data only — no method arithmetic.  Draw order (numpy PCG64, seed [seed, 7]): f (n+m1, N(0,1)),
+    D (m2, exp U(−4, 4): a six-decade spread like mid-IPM D = V⁻¹S), p (m2, N(0,1)), b (m2, N(0,1));
+    then the sample index sets (sorted, without replacement) for vectors of length n+m1 and m2.
+    """
+    f: np.ndarray
+    D: np.ndarray
+    p: np.ndarray
+    b: np.ndarray
+    idx_F: np.ndarray
+    idx_m2: np.ndarray
+
+
+def probe_inputs(qp: QP, seed: int = 0, nsample: int = 8192) -> Probe:
+    rng = np.random.default_rng([seed, 7])
+    N, m2 = qp.n + qp.m1, qp.m2
+    f = rng.standard_normal(N)
+    D = np.exp(rng.uniform(-4.0, 4.0, size=m2))
+    p = rng.standard_normal(m2)
+    b = rng.standard_normal(m2)
+    idx_F = np.sort(rng.choice(N, size=min(N, nsample), replace=False)).astype(np.int64)
+    idx_m2 = np.sort(rng.choice(m2, size=min(m2, nsample), replace=False)).astype(np.int64)
+    return Probe(f=f, D=D, p=p, b=b, idx_F=idx_F, idx_m2=idx_m2)

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import qpgen
-from oracle import symbolic
+from oracle import costs, symbolic
 
 P = pytest.importorskip("paper_2104_12916_b200")
 
@@ -32,7 +32,17 @@ def test_no_cpu_fallback():
     assert ei.value.code == -5     # QP_ECUDA
 
 
-@pytest.mark.parametrize("name", ["c0", "tiny", "m1_zero", "m1_eq_n", "ragged", "grid", "syqp"])
+def _path30():
+    import scipy.sparse as sp
+    n = 30
+    H = sp.diags([np.full(n - 1, -1.0), np.full(n, 4.0), np.full(n - 1, -1.0)], [-1, 0, 1], format="csr")
+    return qpgen.QP(H=qpgen.canonical_csr(H), A=qpgen.canonical_csr(sp.csr_matrix((0, n))),
+                    C=qpgen.canonical_csr(sp.identity(n, format="csr")), g=np.zeros(n), b=np.zeros(0),
+                    d=np.zeros(n), x_perm=np.arange(n))
+
+
+@pytest.mark.parametrize("name", ["c0", "tiny", "m1_zero", "m1_eq_n", "ragged", "grid", "syqp", "path30", "absorb",
+                                  "c3s"])
 def test_host_symbolic_matches_oracle(name):
     qp = {"c0": lambda: qpgen.make("c0"),
           "tiny": lambda: qpgen.scaled_random_qp(9, 4, 12, seed=1, g_nnz=3, a_nnz=3, c_nnz=3),
@@ -40,16 +50,28 @@ def test_host_symbolic_matches_oracle(name):
           "m1_eq_n": lambda: qpgen.make_syqp(24, 24),
           "ragged": lambda: qpgen.scaled_random_qp(700, 130, 900, seed=3),
           "grid": lambda: qpgen.make_grid_qp(24, 40, 60, seed=4, name="grid24"),
-          "syqp": lambda: qpgen.make_syqp(64, 20)}[name]()
+          "syqp": lambda: qpgen.make_syqp(64, 20),
+          "path30": _path30,                                                   # hand-worked relax example
+          "absorb": lambda: qpgen.scaled_random_qp(2000, 500, 3000, seed=5, g_nnz=8, a_nnz=4, c_nnz=6),
+          "c3s": lambda: qpgen.make("c3s")}[name]()
     a = P.Analysis(qp.H, qp.A, qp.x_perm)
     perm = a.structure("perm")
     assert sorted(perm[:qp.n].tolist()) == list(range(qp.n))
     assert perm[qp.n:].tolist() == list(range(qp.n, qp.n + qp.m1))      # λ block last, in row order
-    ref = symbolic.analyse(qp.H, qp.A, perm[:qp.n], trailing_from=int(a.structure("trailing_from")[0]))
+    # the oracle decides the forced trailing supernode itself (symbolic.choose_trailing); the library
+    # absorbs only under its own ordering (x_perm None)
+    ref = symbolic.analyse_auto(qp.H, qp.A, perm[:qp.n], absorb=qp.x_perm is None)
+    assert int(a.structure("trailing_from")[0]) == ref["trailing_from"]
     for k in KEYS:
         assert symbolic.struct_hash(a.structure(k)) == symbolic.struct_hash(ref[k]), k
     st = a.stats()
     assert st["nnz_LF"] == ref["nnz_L"] and st["nnz_LF_stored"] == ref["nnz_stored"]
+    # the paper's cost model: the library's c_fact(F) equals the oracle's Σ_j cc(j)² exactly
+    assert int(st["c_fact_F"]) == costs.c_fact(ref["colcount"])
+    if name == "path30":
+        assert a.structure("sn_start").tolist() == [0, 16, 30]
+    if name == "absorb":
+        assert ref["trailing_from"] > 0          # the case exercises the absorption rule
 
 
 def test_min_degree_reduces_fill():

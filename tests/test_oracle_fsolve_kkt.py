@@ -135,6 +135,19 @@ def test_spec_step_length():
     assert a1 == 1.0
 
 
+def test_step_length_nu_branch():
+    """The ν side of the fraction-to-boundary rule (reading R3), by hand: s + αΔs ≥ 0 never binds
+    (Δs ≥ 0); ν = (1, 4), Δν = (−2, −1) hits zero first at α = 1/2 (row 0) ⇒ α_max = 1/2,
+    α = 0.995/2.  Mixed: the s side binds at 1/4 (s = 1, Δs = −4) before ν's 1/2."""
+    a, amax = kkt.step_length(np.array([1.0, 2.0]), np.array([0.5, 1.0]), np.array([1.0, 4.0]),
+                              np.array([-2.0, -1.0]), 0.995)
+    assert amax == 0.5 and a == pytest.approx(0.4975, rel=1e-15)
+    a, amax = kkt.step_length(np.array([1.0]), np.array([-4.0]), np.array([1.0]), np.array([-2.0]), 0.995)
+    assert amax == 0.25 and a == pytest.approx(0.995 * 0.25, rel=1e-15)
+    a, amax = kkt.step_length(np.array([1.0]), np.array([-1.0]), np.array([3.0]), np.array([-12.0]), 0.5)
+    assert amax == 0.25 and a == 0.125
+
+
 def test_spec_build_ph():
     e = GOLD["build_ph"][0]
     n = e["n"]
@@ -161,3 +174,34 @@ def test_T_matrix_closed_form():
     Cd = qp.C.toarray()
     ref = Cd @ np.diag(1.0 / qp.H.diagonal()) @ Cd.T
     assert np.allclose(T, ref, rtol=1e-14, atol=1e-14)
+
+
+def test_chol_blocked_matches_lapack():
+    """The blocked Cholesky used for large dense P_H (c1) against LAPACK on a small SPD matrix with
+    ragged blocks: L Lᵀ = P, L equals numpy's factor, and the blocked solve inverts P."""
+    rng = np.random.default_rng(8)
+    n = 301
+    G = rng.standard_normal((n, n))
+    P = G @ G.T + n * np.eye(n)
+    L = kkt.chol_blocked(P.copy(), nb=64)
+    Lo = np.tril(L)
+    assert np.allclose(Lo @ Lo.T, P, rtol=1e-13, atol=1e-10)
+    assert np.allclose(Lo, np.linalg.cholesky(P), rtol=1e-12, atol=1e-12)
+    r = rng.standard_normal(n)
+    x = kkt.chol_blocked_solve(L, r, nb=64)
+    assert np.linalg.norm(P @ x - r) <= 1e-12 * np.linalg.norm(r) * np.linalg.cond(P)
+
+
+def test_blockf_matches_dense_block_inverse():
+    """BlockF (SuperLU of H + dense F_H) against numpy.linalg.inv(F) on small QPs, with and without x_perm."""
+    from oracle.fsolve import BlockF
+    for qp in (tiny(40, 9, 50, seed=31), qpgen.make_grid_qp(10, 12, 20, seed=5, name="g10")):
+        F = assemble_F(qp.H, qp.A).toarray()
+        rng = np.random.default_rng(2)
+        r = rng.standard_normal(qp.n + qp.m1)
+        ref = np.linalg.inv(F) @ r
+        for xp in (None, qp.x_perm):
+            if xp is None and qp.x_perm is not None:
+                continue
+            y, z = BlockF(qp.H, qp.A, xp).solve(r[:qp.n], r[qp.n:])
+            assert np.linalg.norm(np.concatenate([y, z]) - ref) <= 1e-11 * np.linalg.norm(ref)

@@ -211,3 +211,46 @@ def test_symbolic_trailing_merge(k):
     for j in range(s0, N):
         assert set(st["struct"][j].tolist()) <= set(rows.tolist())
     assert st["nnz_L"] == base["nnz_L"] and st["colcount"].tolist() == base["colcount"].tolist()
+
+
+def _path_qp(n):
+    """F = −H with H tridiagonal (a path graph), m1 = 0: etree is the path, cc(j) = 2 except cc(n−1) = 1."""
+    H = sp.diags([np.full(n - 1, -1.0), np.full(n, 4.0), np.full(n - 1, -1.0)], [-1, 0, 1], format="csr")
+    return qpgen.QP(H=qpgen.canonical_csr(H), A=qpgen.canonical_csr(sp.csr_matrix((0, n))),
+                    C=qpgen.canonical_csr(sp.identity(n, format="csr")), g=np.zeros(n), b=np.zeros(0), d=np.zeros(n))
+
+
+def test_relax_hand_example_path30():
+    """Relaxed amalgamation worked by hand on the path n = 30 (DESIGN.md §4 rule).
+
+    Fundamental supernodes: {0}, …, {27}, {28, 29} (only 28 joins 29: cc(28) = 2 = cc(29) + 1).
+    One pass in increasing order: block {0..k−1} (width k, true 2k entries, rows {0..k}) merging
+    with {k}: merged width k+1, rows k+2, stored (k+1)(k+4)/2, zeros k(k+1)/2, i.e. a zero fraction
+    k/(k+4): 15/19 ≤ 80 % still merges at width 16; at width 17 the 10 % rule refuses (16/20).
+    {16..27} (width 12, true 24) with {28, 29} (true 3): width 14, stored 105, zeros 78 (74 %) → merge.
+    {0..15} + {16..29}: width 30, stored 465, true 59 → 87 % > 10 % → refused.  Result [0, 16, 30]."""
+    qp = _path_qp(30)
+    a = symbolic.analyse(qp.H, qp.A)
+    assert a["fsn_start"].tolist() == list(range(29)) + [30]
+    assert a["sn_start"].tolist() == [0, 16, 30]
+    assert a["sn_parent"].tolist() == [1, -1] and a["sn_level"].tolist() == [0, 1]
+    # rows of {0..15}: its columns plus row 16; of {16..29}: its columns
+    assert a["sn_rows"].tolist() == list(range(17)) + list(range(16, 30))
+
+
+def test_choose_trailing_hand_example():
+    """The absorption rule (symbolic.choose_trailing) on hand-made supernodal trees.  Root R of width
+    100 (budget 0.02·100·101/2 = 101 zeros); four levels.  Level-2 child of width 2 with rows = its 2
+    columns + 90 of R's rows: zeros 2·(100 − 90) + 2²/2 = 22 ≤ 101 → absorbed; cutting at level 1 adds
+    the width-3 supernode with 60 of R's rows: 3·40 + 2·10 + 5²/2 = 152.5 > 101 → the cut stays at 2,
+    and the trailing block starts at column 9 − 2 = 7."""
+    # supernodes: 0 (leaf, level 0, w 4), 1 (level 1, w 3), 2 (level 2, w 2), 3 = R (level 3, w 100)
+    sn_start = np.array([0, 4, 7, 9, 109])
+    sn_parent = np.array([1, 2, 3, -1])
+    sn_level = np.array([0, 1, 2, 3])
+    sn_rowptr = np.cumsum([0, 4 + 5, 3 + 60, 2 + 90, 100])
+    assert symbolic.choose_trailing(sn_start, sn_parent, sn_level, sn_rowptr) == 7
+    # not a dense root (rows below): no absorption
+    assert symbolic.choose_trailing(sn_start, sn_parent, sn_level, sn_rowptr + np.array([0, 0, 0, 0, 1])) == -1
+    # too few levels
+    assert symbolic.choose_trailing(sn_start[1:] - 4, sn_parent[1:] - 1, sn_level[1:] - 1, sn_rowptr[1:] - 9) == -1
