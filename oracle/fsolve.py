@@ -35,18 +35,33 @@ def assemble_F(H, A) -> sp.csr_matrix:
 class DenseF:
     """F⁻¹ through the block-inverse formula f-inv."""
 
-    def __init__(self, H, A):
+    def __init__(self, H, A, explicit_w=False):
         Hd = H.toarray() if sp.issparse(H) else np.asarray(H, dtype=float)
         Ad = A.toarray() if sp.issparse(A) else np.asarray(A, dtype=float)
         self.n, self.m1 = Hd.shape[0], Ad.shape[0]
         self.A = Ad
         self.cH = sla.cho_factor(Hd, lower=True)           # H = L Lᵀ (H SPD, P:L711)
+        HiAt = None
         if self.m1:
             HiAt = sla.cho_solve(self.cH, Ad.T)              # H⁻¹Aᵀ
             FH = Ad @ HiAt                                   # F_H = A H⁻¹ Aᵀ (SPD, P:L773)
             self.cFH = sla.cho_factor(FH, lower=True)
         else:
             self.cFH = None
+        self.W = None
+        if explicit_w:
+            # the (1,1) block of f-inv written out: W = −H⁻¹ + H⁻¹Aᵀ F_H⁻¹ A H⁻¹ (P:L757–773), so that
+            # F⁻¹[u; 0] has x-part W u (one dense GEMV per K_F product on c1-size problems)
+            W = -sla.cho_solve(self.cH, np.eye(self.n))
+            if self.m1:
+                W += HiAt @ sla.cho_solve(self.cFH, HiAt.T)
+            self.W = 0.5 * (W + W.T)
+
+    def solve_x(self, r1):
+        """x-part of F⁻¹ (r1; 0) (row 1 of f-inv with r2 = 0)."""
+        if self.W is not None:
+            return self.W @ r1
+        return self.solve(r1, None)[0]
 
     def Hinv(self, v):
         return sla.cho_solve(self.cH, v)
@@ -143,6 +158,9 @@ class BlockF:
         out = np.empty_like(v)
         out[self.hp] = self.lu.solve(v[self.hp])
         return out
+
+    def solve_x(self, r1):
+        return self.solve(r1, None)[0]
 
     def solve(self, r1, r2=None):
         """Return (y, z) = F⁻¹ (r1; r2), block by block as in f-inv."""

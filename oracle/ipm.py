@@ -51,12 +51,15 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
               max_ipm: int = 100, sigma: float = 0.1, tau: float = 0.995,
               pcg_maxit: Optional[int] = None, fs=None, x_perm=None, record: bool = False,
               exact_ph: bool = False, direct: bool = False, forcing: bool = True,
-              space: str = "nu", ph_opts: Optional[dict] = None) -> IpmResult:
+              space: str = "nu", ph_opts: Optional[dict] = None,
+              rnu_perturb: Optional[int] = None) -> IpmResult:
     """Run the single-factorization inexact IPM.
 
     precond ∈ {"none" (U-KF), "low" (PL-KF), "high" (PH-KF)}.
     ``direct=True`` replaces PCG by a dense solve of K_F (trajectory reference).
     ``record=True`` stores (D_k, r_ν, Δν, PCG iterations) per IPM iteration.
+    ``rnu_perturb``: seed of a relative 1e-15 perturbation of every r_ν (a rounding-level variant of the
+    same trajectory, used to measure how far rounding alone moves the PCG counts; DESIGN reading R12).
     ``ph_opts``: keyword options of ``kkt.PrecondH`` (sparse SuperLU factor / in-place dense factor
     for the full-size configs).
     ``space="x"``: the x-space twin — projected CG on the augmented system K_C with the constraint
@@ -80,6 +83,7 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
     dmax = float(np.max(np.abs(qp.d))) if m2 else 0.0
 
     trace, iters = [], []
+    CWCt = None
     converged = False
     t1 = time.perf_counter()
     k = 0
@@ -106,9 +110,26 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
             x, lam, nu, s = x + alpha * dx, lam + alpha * dlam, nu + alpha * dnu, s + alpha * ds
             continue
         rnu = kkt.r_nu(qp, fs, res)
+        if rnu_perturb is not None:
+            prng = np.random.default_rng([rnu_perturb, k])
+            rnu = rnu * (1.0 + 1e-15 * prng.standard_normal(m2))
         if direct:
-            KF = np.column_stack([kkt.KF_apply(qp, fs, D, e) for e in np.eye(m2)])
-            dnu = np.linalg.solve(KF, rnu)
+            if getattr(fs, "W", None) is not None:
+                # K_F = D − C W Cᵀ with the written-out W = (F⁻¹)₁₁; C W Cᵀ is D-independent
+                if CWCt is None:
+                    Cd = qp.C.toarray() if m2 * n <= 4e8 else None
+                    CWCt = (qp.C @ (qp.C @ fs.W).T).T if Cd is None else Cd @ fs.W @ Cd.T
+                KF = -CWCt.copy() if m2 <= 8192 else np.negative(CWCt)
+                KF[np.diag_indices_from(KF)] += D
+                if m2 > 8192:
+                    L = kkt.chol_blocked(KF)
+                    dnu = kkt.chol_blocked_solve(L, rnu)
+                    del L, KF
+                else:
+                    dnu = np.linalg.solve(KF, rnu)
+            else:
+                KF = np.column_stack([kkt.KF_apply(qp, fs, D, e) for e in np.eye(m2)])
+                dnu = np.linalg.solve(KF, rnu)
             it = 0
         else:
             if precond == "low":

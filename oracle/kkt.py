@@ -50,7 +50,7 @@ def r_nu(qp, fs, res):
 def KF_apply(qp, fs, D, p):
     """K_F p = D∘p − [C 0] F⁻¹ [Cᵀp; 0], never forming K_F."""
     u = qp.C.T @ p
-    w, _ = fs.solve(u, None)
+    w = fs.solve_x(u) if hasattr(fs, "solve_x") else fs.solve(u, None)[0]
     return D * p - qp.C @ w
 
 

@@ -1116,13 +1116,14 @@ __device__ __forceinline__ void snw_forward(const DevFactor& F, const SweepRhs& 
     }
     if (ok) atomicAdd(F.acc + row, s);
   }
+  // publish: every lane fences its own atomics into acc (in parallel, one fence latency), then the lanes
+  // release the destination counters in parallel (the warp barrier orders all lanes' fenced writes
+  // before every release).  One fence per destination by lane 0 cost ~11 µs per task on c2's leaves.
+  if (F.blk_dptr[b + 1] > F.blk_dptr[b]) __threadfence();
   __syncwarp();
   if (F.tprof && threadIdx.x == 0) tb = gtime();
-  if (lane == 0)
-    for (int64_t k = F.blk_dptr[b]; k < F.blk_dptr[b + 1]; ++k) {
-      __threadfence();
-      red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
-    }
+  for (int64_t k = F.blk_dptr[b] + lane; k < F.blk_dptr[b + 1]; k += 32)
+    red_release_add_u64(F.cnt_f + F.blk_dest[k], 1ull);
 }
 // backward: t = L_rowsᵀ x_rows, x_b = L_bb⁻ᵀ (D⁻¹ y_b − t), publish the supernode.
 __device__ __forceinline__ void snw_backward(const DevFactor& F, double* x, int b, unsigned E) {

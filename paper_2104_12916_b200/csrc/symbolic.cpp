@@ -432,6 +432,19 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   }
   std::vector<int64_t> blk_tile0(S.nb + 1, 0);
   std::vector<char> fused(S.nb, 0);
+  // Root-row tiles: with a symmetric root R (the last supernode, columns [rc_split, N)), the rows of a
+  // forest block that lie in R only feed R's right-hand side, which nothing but R reads.  Those rows get
+  // tiles of their own.  Forward they are dispatched after every forest task, just before R, so the
+  // level-by-level forest sweep no longer shares its CTAs and dispatch order with them and they stream at
+  // the end with every dependency met (c2: 88 M of the forest's 145 M entries are root rows; forward sweep
+  // 888 → 740 µs).  Backward they keep their place before their block's DIAG: there they fill the CTAs the
+  // latency-bound top levels leave idle (all first: 680 → 745 µs; a quarter of the CTAs serving them from
+  // a second queue: 1 050 µs).  QPB_ROOT_TILES=0 keeps them in place in both sweeps.
+  const int64_t Jr = ns - 1;
+  const bool root_tiles = Jr >= 0 && S.sn_sinv[Jr] >= 0 &&
+                          !(std::getenv("QPB_ROOT_TILES") && std::getenv("QPB_ROOT_TILES")[0] == '0');
+  const int64_t rc_split = root_tiles ? S.sn_start[Jr] : N;
+  std::vector<char> tile_root;
   const int64_t fuse_elems = std::getenv("QPB_FUSE_ELEMS") ? std::atoll(std::getenv("QPB_FUSE_ELEMS")) : FUSE_ELEMS;
   S.blk_dptr.assign(S.nb + 1, 0);
   S.blk_dest.clear();
@@ -462,30 +475,40 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     // destination's forward counter once and, backward, waits for each destination's ready flag.  Tiles
     // split only by size, into equal parts: fewer tasks, so fewer CTAs parked on a dependency
     // (QPB_TILE_SPLIT=1 restores one destination per tile).
-    int64_t r = S.blk_big[b] ? (S.sn_start[J + 1] - (S.blk_col0[b] + wk)) : 0;
-    const int64_t ntl = (noff - r + cap - 1) / cap, per = ntl > 0 ? (noff - r + ntl - 1) / ntl : cap;
-    while (r < noff) {
-      int64_t e = std::min(noff, r + per);
-      if (split_dest) {
-        const int64_t d0 = col2sn[S.sn_rows[S.blk_rows[b] + r]];
-        e = r + 1;
-        while (e < noff && e - r < cap && col2sn[S.sn_rows[S.blk_rows[b] + e]] == d0) ++e;
-      }
-      S.tile_blk.push_back((int32_t)b);
-      S.tile_r0.push_back((int32_t)r);
-      S.tile_nr.push_back((int32_t)(e - r));
-      int64_t last = -1;
-      for (int64_t q = r; q < e; ++q) {
-        const int64_t dsn = col2sn[S.sn_rows[S.blk_rows[b] + q]];
-        if (dsn != last) {
-          S.tile_dlist.push_back((int32_t)dsn);
-          S.fwd_expect[dsn] += 1;
-          last = dsn;
+    const int64_t rstart = S.blk_big[b] ? (S.sn_start[J + 1] - (S.blk_col0[b] + wk)) : 0;
+    int64_t nx = noff;   // rows are sorted: [0, nx) below rc_split, [nx, noff) in the symmetric root
+    if (J != Jr)
+      while (nx > 0 && S.sn_rows[S.blk_rows[b] + nx - 1] >= rc_split) --nx;
+    const int64_t split = std::max(rstart, nx);
+    for (int part = 0; part < 2; ++part) {
+      int64_t r = part == 0 ? rstart : split;
+      const int64_t rend = part == 0 ? split : noff;
+      if (r >= rend) continue;
+      const int64_t ntl = (rend - r + cap - 1) / cap, per = ntl > 0 ? (rend - r + ntl - 1) / ntl : cap;
+      while (r < rend) {
+        int64_t e = std::min(rend, r + per);
+        if (split_dest) {
+          const int64_t d0 = col2sn[S.sn_rows[S.blk_rows[b] + r]];
+          e = r + 1;
+          while (e < rend && e - r < cap && col2sn[S.sn_rows[S.blk_rows[b] + e]] == d0) ++e;
         }
+        S.tile_blk.push_back((int32_t)b);
+        S.tile_r0.push_back((int32_t)r);
+        S.tile_nr.push_back((int32_t)(e - r));
+        tile_root.push_back((char)part);   // part 1 = rows of the symmetric root
+        int64_t last = -1;
+        for (int64_t q = r; q < e; ++q) {
+          const int64_t dsn = col2sn[S.sn_rows[S.blk_rows[b] + q]];
+          if (dsn != last) {
+            S.tile_dlist.push_back((int32_t)dsn);
+            S.fwd_expect[dsn] += 1;
+            last = dsn;
+          }
+        }
+        S.tile_dptr.push_back((int64_t)S.tile_dlist.size());
+        S.bwd_expect[b] += 1;
+        r = e;
       }
-      S.tile_dptr.push_back((int64_t)S.tile_dlist.size());
-      S.bwd_expect[b] += 1;
-      r = e;
     }
   }
   blk_tile0[S.nb] = (int64_t)S.tile_blk.size();
@@ -546,6 +569,9 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   }
   // Tiny single-block supernodes (w ≤ 32, noff ≤ 256, w·noff ≤ 1024) are swept WARP-wide: groups of
   // up to 8 from the same level (height forward, depth backward) form one task (type 7), one warp each.
+  // (Chaining a whole subtree of them through one warp, which needs no counters or fences between its
+  // members, was measured slower: c2 forward 740 → 810 µs, c4s 284 → 373 µs — the per-supernode latency,
+  // not the dependency hops, bounds this phase.)
   std::vector<int32_t> tiny_f(ns, -1), tiny_b(ns, -1);   // group id of J, set on every member
   std::vector<char> first_f(ns, 0), first_b(ns, 0);
   {
@@ -578,12 +604,18 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
     group(fwd_order, height, tiny_f, first_f, S.snw_fwd);
     group(bwd_order, depth, tiny_b, first_b, S.snw_bwd);
   }
+  // root-row tiles (see rc_split above), in block order
+  std::vector<int64_t> rtiles;
+  for (int64_t t = 0; t < (int64_t)tile_root.size(); ++t)
+    if (tile_root[t]) rtiles.push_back(t);
   auto build_queues = [&](bool use_sym, std::vector<int32_t>& fq, std::vector<int32_t>& bq) {
     fq.clear();
     bq.clear();
     for (int32_t J : fwd_order) {
       const int64_t b0 = S.sn_blk0[J], b1 = S.sn_blk0[J + 1];
       const bool sym = use_sym && S.sn_sinv[J] >= 0;
+      if (J == Jr)   // every forest task is dispatched: now the root-row tiles, then the root
+        for (int64_t t : rtiles) fq.push_back(enc(1, t));
       if (tiny_f[J] >= 0) {
         if (first_f[J]) fq.push_back(enc(7, tiny_f[J]));
         continue;
@@ -591,14 +623,16 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
       if (S.sn_xinv[J] < 0) {
         for (int64_t b = b0; b < b1; ++b) {
           fq.push_back(enc(fused[b] ? 4 : 0, b));
-          for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) fq.push_back(enc(1, t));
+          for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t)
+            if (!tile_root[t]) fq.push_back(enc(1, t));
         }
       } else {
         for (int64_t b = b0; b < b1; ++b) fq.push_back(enc(2, b));
         if (!sym)
           for (int64_t x = sn_xt0[J]; x < sn_xt0[J + 1]; ++x) fq.push_back(enc(3, x));
         for (int64_t b = b0; b < b1; ++b)
-          for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t) fq.push_back(enc(1, t));
+          for (int64_t t = blk_tile0[b]; t < blk_tile0[b + 1]; ++t)
+            if (!tile_root[t]) fq.push_back(enc(1, t));
       }
     }
     for (int32_t J : bwd_order) {
@@ -616,16 +650,17 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
       } else {
         if (sym) {
           bq.push_back(enc(6, J));
-          continue;
+        } else {
+          for (int64_t b = b1 - 1; b >= b0; --b)
+            for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) bq.push_back(enc(1, t));
+          for (int64_t b = b0; b < b1; ++b) bq.push_back(enc(2, b));
+          for (int64_t x = sn_xb0[J]; x < sn_xb0[J + 1]; ++x) bq.push_back(enc(3, x));
         }
-        for (int64_t b = b1 - 1; b >= b0; --b)
-          for (int64_t t = blk_tile0[b + 1] - 1; t >= blk_tile0[b]; --t) bq.push_back(enc(1, t));
-        for (int64_t b = b0; b < b1; ++b) bq.push_back(enc(2, b));
-        for (int64_t x = sn_xb0[J]; x < sn_xb0[J + 1]; ++x) bq.push_back(enc(3, x));
       }
     }
   };
   build_queues(true, S.fwd_tasks, S.bwd_tasks);
+
   S.sym_c0 = S.sym_c1 = 0;
   for (int64_t J = 0; J < ns; ++J)
     if (S.sn_sinv[J] >= 0) {   // symmetric roots are etree roots: at most one chunk range per root, roots last

@@ -11,7 +11,12 @@ inputs of ``qpgen.probe_inputs`` (D with a six-decade spread, N(0,1) vectors):
 * ``PH<k>``, ``PHeps``  the same with P_H = D + C diag(H)⁻¹Cᵀ where the oracle can
                factor P_H (c1 dense LAPACK, c4s SuperLU in the banded row order);
 * ``ipm_pl``   the oracle PL-KF IPM's first 15 iterations (μ, residual norms, α, PCG counts);
-* ``ipm_ph``   the oracle PH-KF IPM at ipm_tol 1e-10 (objective, counts, trace) — c1, c4s.
+* ``ipm_pl_var`` the same with r_ν perturbed by 1e-15 (two seeds): the rounding spread of the counts;
+* ``ipm_ph``   the oracle PH-KF IPM at ipm_tol 1e-10 (objective, counts, trace) — c4s;
+* ``ipm_direct`` c1: the oracle IPM with DIRECT K_F solves (K_F = D − C W Cᵀ formed densely with the
+               written-out W = (F⁻¹)₁₁ and Cholesky-factored) at ipm_tol 1e-10 — the optimum's objective,
+               which is unique (H SPD), for the GPU PH-KF objective parity; the oracle's own PH-KF IPM
+               on c1 would take ~7 h on the host (a 40 000² dense P_H factor and apply per step).
 
 Usage: python scripts/make_goldens.py CFG [stage ...]   (stages: F KF PL PH ipm_pl ipm_ph; default all)
 Each stage is saved as it finishes, so a long run can be resumed stage by stage.
@@ -34,6 +39,7 @@ from oracle.pcg import pcg  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "full")
 PH_OK = {"c1": dict(sparse=False, keep=False), "c4s": dict(sparse=True, order="natural")}
+IPM_PH = ("c4s",)
 KS = (1, 3, 7)
 
 
@@ -43,7 +49,7 @@ def log(*a):
 
 def fsolver(qp):
     if qp.name == "c1":
-        return DenseF(qp.H, qp.A)
+        return DenseF(qp.H, qp.A, explicit_w=True)     # K_F products through the written-out (F⁻¹)₁₁
     return BlockF(qp.H, qp.A, qp.x_perm)          # grid configs: the generator's ND order; c3s: SuperLU MMD
 
 
@@ -67,7 +73,7 @@ def flat(prefix, d):
 
 def main():
     cfg = sys.argv[1]
-    stages = sys.argv[2:] or ["F", "KF", "PL", "PH", "ipm_pl", "ipm_ph"]
+    stages = sys.argv[2:] or ["F", "KF", "PL", "PH", "ipm_pl", "ipm_pl_var", "ipm_ph", "ipm_direct"]
     qp = qpgen.make(cfg)
     pr = qpgen.probe_inputs(qp)
     log(cfg, "n", qp.n, "m1", qp.m1, "m2", qp.m2)
@@ -117,7 +123,25 @@ def main():
         save(cfg, "ipm_pl", dict(k=[d["k"] for d in tr], mu=[d["mu"] for d in tr], rg=[d["rg"] for d in tr],
                                  re=[d["re"] for d in tr], ri=[d["ri"] for d in tr], pcg=[d["pcg"] for d in tr],
                                  alpha=[d["alpha"] for d in tr], eps=[d["eps"] for d in tr]))
-    if "ipm_ph" in stages and cfg in PH_OK:
+    if "ipm_pl_var" in stages:
+        # rounding-level variants of the same trajectory (r_ν perturbed by 1e-15 relative): the spread of
+        # their PCG counts is what rounding alone does to the counts (DESIGN reading R12)
+        pay = {}
+        for v in (1, 2):
+            t = time.time()
+            r = ipm_solve(qp, precond="low", max_ipm=15, fs=fs, rnu_perturb=v)
+            meta[f"t_ipm_pl_var{v}_s"] = time.time() - t
+            pay[f"pcg_v{v}"] = [d["pcg"] for d in r.trace]
+            pay[f"mu_v{v}"] = [d["mu"] for d in r.trace]
+        save(cfg, "ipm_pl_var", pay)
+    if "ipm_direct" in stages and cfg == "c1":
+        t = time.time()
+        r = ipm_solve(qp, precond="low", ipm_tol=1e-10, fs=fs, direct=True)
+        meta["t_ipm_direct_s"] = time.time() - t
+        tr = r.trace
+        save(cfg, "ipm_direct", dict(objective=r.objective, n_ipm=r.n_ipm, converged=int(r.converged),
+                                     mu=[d["mu"] for d in tr], alpha=[d["alpha"] for d in tr]))
+    if "ipm_ph" in stages and cfg in IPM_PH:
         t = time.time()
         kw = {k: v for k, v in PH_OK[cfg].items()}
         r = ipm_solve(qp, precond="high", ipm_tol=1e-10, fs=fs, ph_opts=kw)

@@ -205,3 +205,25 @@ def test_blockf_matches_dense_block_inverse():
                 continue
             y, z = BlockF(qp.H, qp.A, xp).solve(r[:qp.n], r[qp.n:])
             assert np.linalg.norm(np.concatenate([y, z]) - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_dense_explicit_w_matches_solve():
+    """DenseF's written-out (F⁻¹)₁₁ (used for c1's K_F products) equals the x-part of F⁻¹[u; 0]
+    computed by numpy.linalg.inv(F)."""
+    qp = tiny(30, 7, 40, seed=41)
+    fs = DenseF(qp.H, qp.A, explicit_w=True)
+    Finv = np.linalg.inv(assemble_F(qp.H, qp.A).toarray())
+    assert np.allclose(fs.W, Finv[:qp.n, :qp.n], rtol=1e-10, atol=1e-12)
+    u = np.random.default_rng(3).standard_normal(qp.n)
+    assert np.allclose(fs.solve_x(u), fs.solve(u, None)[0], rtol=1e-11, atol=1e-12)
+
+
+def test_direct_ipm_dense_kf_route_matches_column_route():
+    """The oracle's direct IPM with K_F = D − C W Cᵀ (explicit W) follows the same iterates as the
+    column-by-column K_F route on a small QP (the c1 objective golden is made this way)."""
+    from oracle.ipm import ipm_solve
+    qp = tiny(40, 10, 60, seed=42)
+    a = ipm_solve(qp, precond="low", ipm_tol=1e-10, fs=DenseF(qp.H, qp.A), direct=True)
+    b = ipm_solve(qp, precond="low", ipm_tol=1e-10, fs=DenseF(qp.H, qp.A, explicit_w=True), direct=True)
+    assert a.converged and b.converged and a.n_ipm == b.n_ipm
+    assert abs(a.objective - b.objective) <= 1e-11 * abs(a.objective)
