@@ -64,8 +64,12 @@ def parse():
                     help="skip the full IPM solve timing (BJ metric 'IPM solve time'; c1 PH-KF, rank 0, ~1 min)")
     ap.add_argument("--space", default="nu", choices=["nu", "x"],
                     help="nu: PCG on K_F (the paper's PL-KF, default); x: the x-space twin (projected CG on K_C)")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
-                    help="N > 1: independent replicas (weak) or one IPM with sharded rows (strong)")
+    ap.add_argument("--mode", default=None, choices=["replicas", "sharded"],
+                    help="N > 1: one IPM with the inequality rows sharded over the ranks (default; strong "
+                         "scaling, W's chunks split over the ranks on c1) or independent replicas (weak)")
+    ap.add_argument("--secondary", default="c2",
+                    help="N = 1: also measure this config's PL-KF IPM steps (the sparse-sweep path; '' = off)")
+    ap.add_argument("--secondary-steps", type=int, default=4)
     ap.add_argument("--profile-traffic", default=os.path.join(ROOT, "profiles", "traffic.json"))
     return ap.parse_args()
 
@@ -194,6 +198,29 @@ class OracleSampler:
         return it, time.perf_counter() - t1
 
 
+def host_info():
+    """The host the oracle runs on: CPU model (lscpu / /proc/cpuinfo), cores, BLAS threads."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        model = next((ln.split(":", 1)[1].strip() for ln in out.splitlines() if ln.startswith("Model name")), None)
+    except Exception:
+        pass
+    if model is None:
+        try:
+            model = next(ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name"))
+        except Exception:
+            model = "unknown"
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": d.get("internal_api"), "threads": d.get("num_threads")} for d in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "blas": blas,
+            "superlu": "single-threaded (scipy.sparse.linalg.splu)"}
+
+
 def cpu_oracle_sample(qp, iters, x_perm=None):
     o = OracleSampler(qp, x_perm)
     it, dt = o.sample(iters)
@@ -222,11 +249,89 @@ def run_reference(args, rank, world):
                    "n": qp.n, "m1": qp.m1, "m2": qp.m2},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": o.cores, "kind": "oracle",
                          "sample": f"{args.steps} x {args.cpu_iters} PCG iterations of IPM step 0 on {args.config} "
-                                   f"(oracle F setup {o.t_setup:.1f} s excluded)"},
+                                   f"(oracle F setup {o.t_setup:.1f} s excluded)", "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
+
+
+# ----------------------------------------------------------------------------- secondary workload (sparse sweeps)
+def measure_secondary(cfg, args, local, stream, peak, peak_src):
+    """PL-KF IPM steps on `cfg` (default c2, the largest single-GPU config of BASELINE.json): the path where
+    every K_F product runs the sparse supernodal sweeps (a2–a4) instead of c1's explicit W.  Same protocol
+    as the headline (W warm-up IPM steps, K timed, CUDA events on the library stream), plus a profiled pass
+    for the sweep kernels' durations.  GB/s on SURVEY §8(d)'s algorithmic B_it per PCG iteration."""
+    import torch
+    import qpgen
+    from paper_2104_12916_b200.binding import from_qp
+    dev = torch.device("cuda", local)
+    qp = qpgen.make(cfg)
+    s = from_qp(qp, device=local, stream=stream.cuda_stream)
+    t0 = time.perf_counter()
+    s.ipm_factor_once("low")
+    t_setup = time.perf_counter() - t0
+    st = s.stats()
+    W, K = 2, args.secondary_steps
+    s.ipm_init()
+    s.ipm_iterate(W)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    r = s.ipm_iterate(K)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    pcg = int(sum(r["pcg_iters"][W:W + K]))
+    steps = max(0, min(K, r["n_ipm"] - W))
+    # profiled pass (CUDA events around every launch): sweep kernel durations
+    s.ipm_init()
+    s.ipm_iterate(W)
+    s.profile(True)
+    s.profile_read()
+    r2 = s.ipm_iterate(K)
+    torch.cuda.synchronize(dev)
+    prof = s.profile_read()
+    s.profile(False)
+    pcg2 = int(sum(r2["pcg_iters"][W:W + K]))
+    solves = pcg2 + 2 * max(0, min(K, r2["n_ipm"] - W))
+    ss = s.structure("sn_start")
+    w_root = int(ss[-1] - ss[-2]) if st["sym_enabled"] else 0
+    root_bytes = 8.0 * w_root * (w_root + 1) / 2
+    forest_bytes = (st["fsolve_bytes_F"] - root_bytes) / 2          # L_F outside the root, per sweep
+    (fwd_ms, _), (bwd_ms, _), (root_ms, _) = prof["f_fwd"], prof["f_bwd"], prof["f_root"]
+    gbs = lambda b, t: b * solves / (t / 1e3) / 1e9 if t > 0 else None  # noqa: E731
+    b_it = st["pcg_bytes_per_iter"]
+    value = pcg / (ms / 1e3) if ms > 0 else 0.0
+    ach_it = pcg * b_it / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    fsolve_ms = fwd_ms + bwd_ms + root_ms
+    out = {
+        "config": cfg, "workload": f"{cfg} PL-KF: one IPM iteration per step (sparse supernodal sweeps for every "
+                                   f"K_F product, symmetric-root GEMV, fused PCG step)",
+        "n": qp.n, "m1": qp.m1, "m2": qp.m2, "nnz_LF": st["nnz_LF"], "metric": METRIC, "unit": UNIT,
+        "value": value, "ms_per_step": ms / max(1, steps), "steps": steps, "warmup": W, "pcg_iters_timed": pcg,
+        "ms_per_pcg_iter": ms / max(1, pcg),
+        "achieved_GBps_Bit": ach_it, "frac_Bit": ach_it / peak, "frac_Bit_8TBps": ach_it / 8000.0,
+        "B_it_bytes": b_it,
+        "B_it_note": "SURVEY 8(d): 16 nnz(L_F) + 24 nnz(C) + 8(15 m2 + 6(n+m1)) per PCG iteration; the timed step "
+                     "also holds the IPM step's r_nu / recovery F-solves and residuals, so this is a lower bound",
+        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+                     "kernel": "k_trsv_fwd + k_symroot_gemv + k_trsv_bwd (one F-solve)",
+                     "achieved": gbs(st["fsolve_bytes_F"], fsolve_ms),
+                     "frac": (gbs(st["fsolve_bytes_F"], fsolve_ms) or 0) / peak,
+                     "algorithmic_bytes_per_fsolve": st["fsolve_bytes_F"],
+                     "per_kernel": {"k_trsv_fwd": {"bytes": forest_bytes, "ms": fwd_ms / max(1, solves),
+                                                   "GBps": gbs(forest_bytes, fwd_ms)},
+                                    "k_symroot_gemv": {"bytes": root_bytes, "ms": root_ms / max(1, solves),
+                                                       "GBps": gbs(root_bytes, root_ms)},
+                                    "k_trsv_bwd": {"bytes": forest_bytes, "ms": bwd_ms / max(1, solves),
+                                                   "GBps": gbs(forest_bytes, bwd_ms)}},
+                     "fsolve_share_of_step": fsolve_ms / sum(v[0] for v in prof.values()) if prof else None},
+        "setup_s": t_setup, "l2": "no flush: the factor read by every sweep (%.2f GB) exceeds L2" % (
+            st["factor_bytes"] / 1e9),
+    }
+    s.close()
+    return out
 
 # ----------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local, use_dist):
@@ -467,7 +572,24 @@ def run_ours(args, rank, world, local, use_dist):
         it, dt, t_or, cores = cpu_oracle_sample(qp, args.cpu_iters, s.structure("perm")[:qp.n]
                                                 if qp.n + qp.m1 > 30000 else None)
         cpu = {"value": it / dt if dt > 0 else 0.0, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{it} PCG iterations of IPM step 0 on {args.config} (oracle F setup {t_or:.1f} s excluded)"}
+               "sample": f"{it} PCG iterations of IPM step 0 on {args.config} (oracle F setup {t_or:.1f} s excluded)",
+               "host": host_info(), "oracle_factor_s": t_or, "oracle_ms_per_pcg_iter": 1e3 * dt / max(1, it)}
+        # per-config oracle times measured when the full-size goldens were made (scripts/make_goldens.py,
+        # the build container's host, stated in each record) — BASELINE.md §4's factor / PCG / IPM times
+        gold = {}
+        for cfg in ("c1", "c2", "c3s", "c4s"):
+            mp = os.path.join(ROOT, "tests", "golden", "full", f"{cfg}.meta.json")
+            if os.path.exists(mp):
+                try:
+                    gold[cfg] = json.load(open(mp))
+                except Exception:
+                    pass
+        cpu["oracle_times_full_size"] = gold or None
+
+    # ---------------------------------------------------------------- secondary workload (N = 1)
+    secondary = None
+    if world == 1 and args.secondary and args.secondary != args.config:
+        secondary = measure_secondary(args.secondary, args, local, stream, peak, peak_src)
 
     # ---------------------------------------------------------------- IPM solve time (BJ metric, rank 0)
     # c1 PL-KF does not converge, so the full solve is timed with P_H (PH-KF), the paper's
@@ -506,11 +628,23 @@ def run_ours(args, rank, world, local, use_dist):
                    "parallelism": (f"sharded inequality rows x{world} (NCCL all-reduce; " + ("W chunks split over ranks" if st.get("dense_w_enabled", 0) else "replicated F-solve") + ")"
                                    if sharded else (f"replicas x{world}" if world > 1 else "single GPU"))},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
-        "ipm_solve": ipm,
+        "ipm_solve": ipm, "secondary": secondary,
         "setup_s": {"symbolic": st["t_symbolic_s"], "factor": st["t_factor_s"], "factor_once_total": t_setup},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def spawn(args):
+    """`bench.py --gpus N` without a torchrun environment: re-run this command under torchrun with N ranks
+    (one process per GPU, rendezvous on 127.0.0.1) and pass its output through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -519,6 +653,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
+    if args.mode is None:
+        args.mode = "sharded" if world > 1 else "replicas"
     use_dist = dist_init(world, local)
     run_ours(args, rank, world, local, use_dist)
     if use_dist:

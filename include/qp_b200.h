@@ -238,6 +238,8 @@ typedef struct {
   double dense_w_discrepancy;        /* ‖W·u − (F⁻¹[u; 0])ₓ‖/‖·‖ of its factor-time guard (−1: not built) */
   double kf_bytes_W;                 /* bytes of W this rank reads per K_F product: 8·n(n+1)/2, times the
                                         rank's share of W's chunks in sharded mode (0 when not in use) */
+  double dense_finv_enabled;         /* 1 if F-solves use the explicit F⁻¹ (small N, DESIGN §5 "dense F⁻¹") */
+  double dense_finv_discrepancy;     /* its factor-time guard against the sweeps (−1: not built) */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 

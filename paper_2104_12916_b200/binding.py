@@ -72,7 +72,8 @@ class _Stats(C.Structure):
                                           "t_factor_ph_s", "pcg_bytes_per_iter", "pcg_flops_per_iter",
                                           "sweep_bytes_F", "fsolve_bytes_F", "sym_discrepancy", "sym_enabled",
                                           "flat_discrepancy", "flat_enabled", "flat_nnz_M", "dense_w_enabled",
-                                          "dense_w_discrepancy", "kf_bytes_W")]
+                                          "dense_w_discrepancy", "kf_bytes_W", "dense_finv_enabled",
+                                          "dense_finv_discrepancy")]
 
 
 _LIB = None

@@ -170,6 +170,39 @@ struct DeviceArena {
   }
 };
 
+// Host construction of a SymvPlan (kernels.cuh) for chunks [c_begin, c_end): chunk i contributes its row
+// partial (rows rob[i]) and column partials (output blocks cob0[i] .. cob0[i]+ncob[i]−1); output block o
+// (ids ob_lo + o, nob of them) has `width[o]` rows at x0[o].  Each block's slot list is ordered by the
+// kind (row partials first) and then by chunk index: the fixed summation order of the reducers.
+SymvPlan build_symv_plan(DeviceArena& m, cudaStream_t st, int64_t c_begin, int64_t c_end,
+                         const std::vector<int32_t>& rob, const std::vector<int32_t>& cob0,
+                         const std::vector<int32_t>& ncob, int32_t ob_lo, int32_t nob,
+                         const std::vector<int32_t>& width, const std::vector<int64_t>& x0) {
+  const int64_t nc = c_end - c_begin;
+  std::vector<int64_t> lptr(nob + 1, 0);
+  std::vector<int32_t> expect(nob, 0);
+  for (int64_t i = 0; i < nc; ++i) {
+    expect[rob[i] - ob_lo] += 1;
+    for (int32_t k = 0; k < ncob[i]; ++k) expect[cob0[i] + k - ob_lo] += 1;
+  }
+  for (int32_t o = 0; o < nob; ++o) lptr[o + 1] = lptr[o] + expect[o];
+  std::vector<int64_t> lsrc(lptr[nob]), fill(lptr.begin(), lptr.end() - 1);
+  for (int64_t i = 0; i < nc; ++i) lsrc[fill[rob[i] - ob_lo]++] = i * 576;          // row partials first
+  for (int64_t i = 0; i < nc; ++i)
+    for (int32_t k = 0; k < ncob[i]; ++k) lsrc[fill[cob0[i] + k - ob_lo]++] = i * 576 + 64 + 64 * (int64_t)k;
+  SymvPlan P{};
+  P.slots = m.zeros<double>((size_t)std::max<int64_t>(1, nc) * 576, st);
+  P.cnt = m.zeros<unsigned>((size_t)std::max(1, nob), st);
+  P.expect = m.upload(expect, st);
+  P.lptr = m.upload(lptr, st);
+  P.lsrc = m.upload(lsrc, st);
+  P.width = m.upload(width, st);
+  P.x0 = m.upload(x0, st);
+  P.c_begin = c_begin;
+  P.ob_lo = ob_lo;
+  return P;
+}
+
 struct Factor {
   Symbolic S;
   DevFactor d{};
@@ -185,6 +218,7 @@ struct Factor {
   std::vector<int32_t> sym_host;
   int n_sym = 0;
   std::vector<GemmProb> sym_plan;
+  SymvPlan sym_symv{};               // deterministic accumulation plan of k_symroot_gemv
   GemmProb* sym_dev = nullptr;
   int64_t* sym_pref_dev = nullptr;
   int64_t sym_total = 0;
@@ -296,6 +330,19 @@ struct qp_ctx {
   double* dense_w = nullptr;         // explicit (F⁻¹)₁₁ (build_dense_w), column-major, leading dimension dw_ld
   int64_t dw_ld = 0, dw_nch = 0;
   int64_t dw_c0 = 0, dw_c1 = 0;      // this rank's chunk range (all chunks unless sharded)
+  SymvPlan dw_plan_all{}, dw_plan{}; // k_dense_symv accumulation plans: all chunks (guard), this rank's
+  double* dense_finv = nullptr;      // small N: the whole F⁻¹ (N × N, ld df_ld), F-solves as one symmetric GEMV
+  int64_t df_ld = 0, df_nch = 0;
+  const int2* df_chunks = nullptr;
+  SymvPlan df_plan{};
+  double* df_rhs = nullptr;          // materialised right-hand side (N)
+  double df_discrepancy = -1;        // factor-time guard of the dense F⁻¹ (−1: not built)
+  double* phinv = nullptr;           // small m2: P_H⁻¹ (m2 × m2, ld pi_ld), rebuilt after every P_H refactor
+  bool phinv_ready = false;
+  int64_t pi_ld = 0, pi_nch = 0;
+  const int2* pi_chunks = nullptr;
+  SymvPlan pi_plan{};
+  double* pi_unit = nullptr;
   double dw_share = 1.0;             // its share of W's bytes
   const int2* dw_chunks = nullptr;
   double dw_discrepancy = -1.0;
@@ -472,6 +519,31 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.bwd_tasks = m.upload(S.bwd_tasks, st);
     F.fwd_x = m.upload(S.fwd_tasks_x, st);
     F.bwd_x = m.upload(S.bwd_tasks_x, st);
+    if (S.sym_c1 > S.sym_c0) {   // the symmetric-root GEMV's deterministic accumulation plan
+      const int64_t nc = S.sym_c1 - S.sym_c0;
+      std::vector<int32_t> rob(nc), cob0(nc), ncob(nc);
+      int32_t lo = INT32_MAX, hi = -1;
+      for (int64_t i = 0; i < nc; ++i) {
+        const int64_t x = S.sym_c0 + i;
+        const int32_t bI = S.xt_bI[x], bK = S.xt_bK[x], nK = S.xt_nK[x];
+        const int64_t rI = S.blk_col0[bI], cK = S.blk_col0[bK];
+        const int64_t ncol = S.blk_col0[bK + nK - 1] + S.blk_w[bK + nK - 1] - cK;
+        const int64_t ncol_t = std::min<int64_t>(rI, cK + ncol) - cK;
+        rob[i] = bI;
+        cob0[i] = bK;
+        ncob[i] = (int32_t)(ncol_t / 64);
+        lo = std::min({lo, bI, bK});
+        hi = std::max(hi, bI);
+      }
+      const int32_t nob = hi - lo + 1;
+      std::vector<int32_t> width(nob);
+      std::vector<int64_t> x0(nob);
+      for (int32_t o = 0; o < nob; ++o) {
+        width[o] = S.blk_w[lo + o];
+        x0[o] = S.blk_col0[lo + o];
+      }
+      F.sym_symv = build_symv_plan(m, st, S.sym_c0, S.sym_c1, rob, cob0, ncob, lo, nob, width, x0);
+    }
     d.fwd_expect = m.upload(S.fwd_expect, st);
     d.bwd_expect = m.upload(S.bwd_expect, st);
     d.ws = m.alloc<double>(S.ws_size);
@@ -538,6 +610,33 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
       }
       d.fl_nunits = (int64_t)units.size() / 8;
       d.fl_units = reinterpret_cast<const int4*>(m.upload(units, st));
+      {   // fixed-order reduction lists of the unit partials (no floating-point atomics)
+        const int64_t nu = d.fl_nunits, wr = S.N - S.fl_rc0, rc0 = S.fl_rc0;
+        std::vector<int64_t> fr_ptr(wr + 1, 0), bc_ptr(rc0 + 1, 0);
+        for (int64_t u = 0; u < nu; ++u) {
+          const int64_t roff = units[8 * u + 2], col0 = units[8 * u + 3], sh = units[8 * u + 5];
+          const int64_t nrows = sh & 0xffff, ncols = sh >> 16;
+          for (int64_t k = 0; k < nrows; ++k) fr_ptr[S.fl_rows[roff + k] + 1] += 1;
+          for (int64_t k = 0; k < ncols; ++k) bc_ptr[col0 + k + 1] += 1;
+        }
+        for (int64_t r = 0; r < wr; ++r) fr_ptr[r + 1] += fr_ptr[r];
+        for (int64_t c2 = 0; c2 < rc0; ++c2) bc_ptr[c2 + 1] += bc_ptr[c2];
+        std::vector<int32_t> fr_src(fr_ptr[wr]), bc_src(bc_ptr[rc0]);
+        std::vector<int64_t> ff(fr_ptr.begin(), fr_ptr.end() - 1), bf(bc_ptr.begin(), bc_ptr.end() - 1);
+        for (int64_t u = 0; u < nu; ++u) {
+          const int64_t roff = units[8 * u + 2], col0 = units[8 * u + 3], sh = units[8 * u + 5];
+          const int64_t nrows = sh & 0xffff, ncols = sh >> 16;
+          for (int64_t k = 0; k < nrows; ++k) fr_src[ff[S.fl_rows[roff + k]]++] = (int32_t)(u * 64 + k);
+          for (int64_t k = 0; k < ncols; ++k) bc_src[bf[col0 + k]++] = (int32_t)(u * 8 + k);
+        }
+        d.fl_fslot = m.zeros<double>((size_t)std::max<int64_t>(1, nu) * 64, st);
+        d.fl_bslot = m.zeros<double>((size_t)std::max<int64_t>(1, nu) * 8, st);
+        d.fl_fr_ptr = m.upload(fr_ptr, st);
+        d.fl_fr_src = m.upload(fr_src, st);
+        d.fl_bc_ptr = m.upload(bc_ptr, st);
+        d.fl_bc_src = m.upload(bc_src, st);
+        cudaStreamSynchronize(st);   // local host buffers
+      }
       cudaStreamSynchronize(st);   // `units` is a local host buffer
     }
     d.ready_sb = m.zeros<unsigned int>(S.ns, st);
@@ -738,14 +837,23 @@ double* ist_red(qp_ctx* c) { return (double*)((char*)c->ist + offsetof(IpmState,
 void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
   if (!F.sym_enabled) return;
   c->launches += 1;
-  symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, done, c->sm_count * 3, c->stream);
+  symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, &F.sym_symv, done, c->sm_count * 3, c->stream);
 }
 
 // One F-solve on the right-hand side described by r: the task-graph sweeps, or — flattened forest —
 // forward product, root GEMV, backward product (three dependency-free kernels).
 void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
   Factor& F = c->FF;
-  c->launches += F.d.flat ? (r.rhs_ready ? 2 : 3) : 2;
+  if (c->dense_finv) {   // small N: out = F⁻¹ v, one deterministic symmetric GEMV (DESIGN §5 "dense F⁻¹")
+    c->launches += 2;
+    int h = c->begin(8);
+    gather_rhs(r, c->df_rhs, out, F.d.N, c->sm_count, c->stream);
+    dense_symv(c->dense_finv, c->df_ld, F.d.N, c->df_chunks, c->df_nch, &c->df_plan, c->df_rhs, out, r.done_flag,
+               c->sm_count, c->stream);
+    c->end(h);
+    return;
+  }
+  c->launches += F.d.flat ? (r.rhs_ready ? 4 : 5) : 2;
   int h = c->begin(0);
   if (F.d.flat) flat_forward(F.d, r, out, c->sm_count, c->stream);
   else trsv_forward(F.d, r, out, c->tgrid, c->stream);
@@ -788,7 +896,7 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
       cudaMemsetAsync(c->xbuf, 0, c->n * 8, c->stream);
     }   // else ubuf = Cᵀp and xbuf[0, n) = 0 come from the fused step's phase D
     int h = c->begin(9);
-    dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks + c->dw_c0, c->dw_c1 - c->dw_c0, c->ubuf, c->xbuf,
+    dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks + c->dw_c0, c->dw_c1 - c->dw_c0, &c->dw_plan, c->ubuf, c->xbuf,
                r.done_flag, c->sm_count, c->stream);
     c->end(h);
     c->launches += 1;
@@ -833,6 +941,14 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
 
 // z = P_H⁻¹ r (a7), P_H factor order via perm_ph.
 void ph_apply_dev(qp_ctx* c, const double* r, double* z, const int* done) {
+  if (c->phinv_ready) {   // small m2: z = P_H⁻¹ r, one deterministic symmetric GEMV
+    c->launches += 2;
+    int h = c->begin(4);
+    zero_flag(z, c->m2, done, c->stream);
+    dense_symv(c->phinv, c->pi_ld, c->m2, c->pi_chunks, c->pi_nch, &c->pi_plan, r, z, done, c->sm_count, c->stream);
+    c->end(h);
+    return;
+  }
   c->launches += 3;
   SweepRhs sr{};
   sr.rhs = r;
@@ -845,6 +961,57 @@ void ph_apply_dev(qp_ctx* c, const double* r, double* z, const int* done) {
   c->end(h);
 }
 
+// Opt-in (QPB_DENSE_PHINV = m2 limit, default 0 = off): P_H⁻¹ formed column by column from the fresh
+// factor (m2 sweep pairs on unit vectors), so every P_H apply is one symmetric GEMV — one launch instead
+// of two latency-bound sweeps, and bit-reproducible.  Off by default: late in the IPM P_H's condition
+// number reaches 1e11 (c0) and an explicit inverse is then a measurably different preconditioner from
+// the Cholesky solves (c0 PH-KF iteration 16: 64 PCG iterations against the oracle's 72 in every
+// variant), unlike F⁻¹, whose conditioning does not depend on D.
+int build_phinv(qp_ctx* c) {
+  const char* e = std::getenv("QPB_DENSE_PHINV");
+  const int64_t lim = e ? std::atoll(e) : 0;
+  const int64_t m2 = c->m2;
+  c->phinv_ready = false;
+  if (m2 > lim || c->sharded) return QP_OK;
+  cudaStream_t st = c->stream;
+  if (!c->phinv) {
+    const int64_t ld = m2 + (m2 & 1), nb = (m2 + 63) / 64;
+    c->phinv = c->mem.zeros<double>((size_t)ld * (size_t)m2, st);
+    c->pi_unit = c->mem.zeros<double>(m2, st);
+    c->pi_ld = ld;
+    std::vector<int32_t> ch, rob, cob0, ncob, width(nb);
+    std::vector<int64_t> x0(nb);
+    for (int64_t I = 0; I < nb; ++I)
+      for (int64_t K0 = 0; K0 <= I; K0 += 8) {
+        const int64_t rr = std::min<int64_t>(64, m2 - 64 * I);
+        const int64_t ncol = std::min<int64_t>(64 * K0 + 512, 64 * I + rr) - 64 * K0;
+        ch.push_back((int32_t)I);
+        ch.push_back((int32_t)K0);
+        rob.push_back((int32_t)I);
+        cob0.push_back((int32_t)K0);
+        ncob.push_back((int32_t)(std::min<int64_t>(64 * I - 64 * K0, ncol) / 64));
+      }
+    for (int64_t o = 0; o < nb; ++o) {
+      width[o] = (int32_t)std::min<int64_t>(64, m2 - 64 * o);
+      x0[o] = 64 * o;
+    }
+    c->pi_chunks = reinterpret_cast<const int2*>(c->mem.upload(ch, st));
+    c->pi_nch = (int64_t)rob.size();
+    c->pi_plan = build_symv_plan(c->mem, st, 0, c->pi_nch, rob, cob0, ncob, 0, (int32_t)nb, width, x0);
+    cudaStreamSynchronize(st);   // host vectors
+  }
+  cudaMemsetAsync(c->pi_unit, 0, m2 * 8, st);
+  for (int64_t j = 0; j < m2; ++j) {
+    if (j > 0) cudaMemsetAsync(c->pi_unit + j - 1, 0, 8, st);
+    flat_set_unit(c->pi_unit, j, st);
+    ph_apply_dev(c, c->pi_unit, c->phinv + (size_t)j * c->pi_ld, nullptr);
+  }
+  w_symmetrize_diag(c->phinv, c->pi_ld, m2, st);
+  if (int rc = cuda_check(c, "P_H inverse")) return rc;
+  c->phinv_ready = true;
+  return QP_OK;
+}
+
 int ph_refactor(qp_ctx* c, const double* D) {
   double t0 = now_s();
   int h = c->begin(5);
@@ -853,6 +1020,7 @@ int ph_refactor(qp_ctx* c, const double* D) {
   if (rc) return rc;
   cudaMemcpyAsync(c->D_ph_last, D, c->m2 * 8, cudaMemcpyDeviceToDevice, c->stream);
   c->ph_valid = true;
+  if (int rc2 = build_phinv(c)) return rc2;
   c->t_factor_ph += now_s() - t0;
   c->ph_refactors++;
   return QP_OK;
@@ -1502,14 +1670,23 @@ int build_dense_w(qp_ctx* c) {
   if (e && e[0] == '0') return QP_OK;
   qp_stats s{};
   qp_get_stats(c, &s);
-  const int64_t n = c->n, N = c->n + c->m1, ld = n + (n & 1);
+  const int64_t n = c->n, N = c->n + c->m1;
+  // Small problems (N ≤ QPB_DENSE_FINV, default 4 096): the whole F⁻¹ is formed (N F-solves on unit
+  // vectors) and every F-solve becomes one symmetric GEMV; W = (F⁻¹)₁₁ is its top-left block.  At this
+  // size the sweeps are latency-bound (tens of µs through a few dependency levels) while the GEMV is one
+  // launch, and the GEMV's fixed-order reduction makes every F-solve and K_F product bit-reproducible.
+  const char* ef = std::getenv("QPB_DENSE_FINV");
+  const int64_t finv_max = ef ? std::atoll(ef) : 4096;
+  const bool small = N <= finv_max && N >= 1;
+  const int64_t ld = small ? N + (N & 1) : n + (n & 1);
   const double wbytes = 8.0 * (double)n * (double)(n + 1) / 2.0;
   const bool force = e && e[0] == '2';   // QPB_DENSE_W=2: whenever it fits (tests)
-  if (n < 64 || !(force || wbytes < s.fsolve_bytes_F) || 8.0 * (double)ld * (double)n > 16e9) return QP_OK;
+  if (!small && (n < 64 || !(force || wbytes < s.fsolve_bytes_F) || 8.0 * (double)ld * (double)n > 16e9))
+    return QP_OK;
   cudaStream_t st = c->stream;
   double* W = nullptr;
   try {
-    W = c->mem.zeros<double>((size_t)ld * (size_t)n, st);
+    W = c->mem.zeros<double>((size_t)ld * (size_t)(small ? N : n), st);
   } catch (std::bad_alloc&) {
     cudaGetLastError();
     W = nullptr;    // no room: keep the F-solve path (sharded: every rank must agree, below)
@@ -1532,20 +1709,65 @@ int build_dense_w(qp_ctx* c) {
   // them full) are then completed from their lower triangles.
   const Symbolic& S = c->FF.S;
   const int64_t J0 = S.ns - 1;
-  const bool fast = c->FF.d.flat && c->FF.sym_enabled && J0 >= 0 && S.sn_sinv[J0] >= 0 &&
+  const bool fast = !small && c->FF.d.flat && c->FF.sym_enabled && J0 >= 0 && S.sn_sinv[J0] >= 0 &&
                     S.sn_start[J0] == c->FF.d.fl_rc0 && S.sn_start[J0 + 1] == N && S.sn_start[J0] < n;
-  const int64_t r0 = fast ? S.sn_start[J0] : n;
+  const int64_t r0 = small ? N : fast ? S.sn_start[J0] : n;
+  const int64_t rows = small ? N : n;   // entries kept per column
   cudaMemsetAsync(c->rhs2, 0, N * 8, st);
   for (int64_t j = 0; j < r0; ++j) {
     if (j > 0) cudaMemsetAsync(c->rhs2 + j - 1, 0, 8, st);
     flat_set_unit(c->rhs2, j, st);
     f_solve_dev(c, c->rhs2, c->xbuf);
-    cudaMemcpyAsync(W + (size_t)j * ld, c->xbuf, n * 8, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(W + (size_t)j * ld, c->xbuf, rows * 8, cudaMemcpyDeviceToDevice, st);
   }
   cudaMemsetAsync(c->rhs2, 0, N * 8, st);
   if (fast) w_copy_root(c->FF.d.xinv + S.sn_sinv[J0], S.sn_ldx[J0], W, ld, r0, n, st);
-  w_symmetrize_diag(W, ld, n, st);
+  w_symmetrize_diag(W, ld, small ? N : n, st);   // the GEMV reads the diagonal 64-blocks full
   if (int rc = cuda_check(c, "dense W columns")) return rc;
+  if (small) {   // the whole F⁻¹: its own chunk list and plan over N, guarded against an F-solve by the sweeps
+    std::vector<int32_t> chF, rob, cob0, ncob;
+    const int64_t nbF = (N + 63) / 64;
+    for (int64_t I = 0; I < nbF; ++I)
+      for (int64_t K0 = 0; K0 <= I; K0 += 8) {
+        const int64_t rr = std::min<int64_t>(64, N - 64 * I);
+        const int64_t ncol = std::min<int64_t>(64 * K0 + 512, 64 * I + rr) - 64 * K0;
+        chF.push_back((int32_t)I);
+        chF.push_back((int32_t)K0);
+        rob.push_back((int32_t)I);
+        cob0.push_back((int32_t)K0);
+        ncob.push_back((int32_t)(std::min<int64_t>(64 * I - 64 * K0, ncol) / 64));
+      }
+    std::vector<int32_t> width(nbF);
+    std::vector<int64_t> x0(nbF);
+    for (int64_t o = 0; o < nbF; ++o) {
+      width[o] = (int32_t)std::min<int64_t>(64, N - 64 * o);
+      x0[o] = 64 * o;
+    }
+    c->df_chunks = reinterpret_cast<const int2*>(c->mem.upload(chF, st));
+    c->df_nch = (int64_t)rob.size();
+    c->df_plan = build_symv_plan(c->mem, st, 0, c->df_nch, rob, cob0, ncob, 0, (int32_t)nbF, width, x0);
+    c->df_rhs = c->mem.zeros<double>(N, st);
+    c->df_ld = ld;
+    std::vector<double> u(N), y1(N), y2(N);
+    std::mt19937_64 g(9);
+    std::normal_distribution<double> nd;
+    for (auto& v : u) v = nd(g);
+    cudaMemcpyAsync(c->rhs2, u.data(), N * 8, cudaMemcpyHostToDevice, st);
+    f_solve_dev(c, c->rhs2, c->xbuf);                                   // the sweeps
+    cudaMemcpyAsync(y2.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemsetAsync(c->xbuf, 0, N * 8, st);
+    dense_symv(W, ld, N, c->df_chunks, c->df_nch, &c->df_plan, c->rhs2, c->xbuf, nullptr, c->sm_count, st);
+    cudaMemcpyAsync(y1.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemsetAsync(c->rhs2, 0, N * 8, st);
+    if (int rc = sync_check(c, "dense F^-1 guard")) return rc;
+    double fd = 0, fn = 0;
+    for (int64_t i = 0; i < N; ++i) {
+      fd += (y1[i] - y2[i]) * (y1[i] - y2[i]);
+      fn += y2[i] * y2[i];
+    }
+    c->df_discrepancy = fn > 0 ? std::sqrt(fd / fn) : 0.0;
+    if (c->df_discrepancy <= 1e-10) c->dense_finv = W;
+  }
   // chunk list: row block I, first column block K0 (≤ 8 blocks of 64 columns up to the diagonal block)
   std::vector<int32_t> ch;
   std::vector<double> cb;   // bytes per chunk (rows × columns read), for the sharded split below
@@ -1589,6 +1811,30 @@ int build_dense_w(qp_ctx* c) {
     }
     c->dw_share = tot > 0 ? mine / tot : 1.0;
   }
+  {   // deterministic accumulation plans (all chunks for the guard below; this rank's for the PCG)
+    std::vector<int32_t> rob(c->dw_nch), cob0(c->dw_nch), ncob(c->dw_nch), width(nb);
+    std::vector<int64_t> x0(nb);
+    for (int64_t i = 0; i < c->dw_nch; ++i) {
+      const int64_t I = ch[2 * i], K0 = ch[2 * i + 1], rows = std::min<int64_t>(64, n - 64 * I);
+      const int64_t ncol = std::min<int64_t>(64 * K0 + 512, 64 * I + rows) - 64 * K0;
+      const int64_t ncol_t = std::min<int64_t>(64 * I - 64 * K0, ncol);
+      rob[i] = (int32_t)I;
+      cob0[i] = (int32_t)K0;
+      ncob[i] = (int32_t)(ncol_t / 64);
+    }
+    for (int64_t o = 0; o < nb; ++o) {
+      width[o] = (int32_t)std::min<int64_t>(64, n - 64 * o);
+      x0[o] = 64 * o;
+    }
+    c->dw_plan_all = build_symv_plan(c->mem, st, 0, c->dw_nch, rob, cob0, ncob, 0, (int32_t)nb, width, x0);
+    if (c->dw_c0 == 0 && c->dw_c1 == c->dw_nch) {
+      c->dw_plan = c->dw_plan_all;
+    } else {
+      std::vector<int32_t> r2(rob.begin() + c->dw_c0, rob.begin() + c->dw_c1),
+          k2(cob0.begin() + c->dw_c0, cob0.begin() + c->dw_c1), n2(ncob.begin() + c->dw_c0, ncob.begin() + c->dw_c1);
+      c->dw_plan = build_symv_plan(c->mem, st, 0, c->dw_c1 - c->dw_c0, r2, k2, n2, 0, (int32_t)nb, width, x0);
+    }
+  }
   cudaStreamSynchronize(st);
   // accuracy guard: W·u against the x-part of an F-solve on [u; 0]
   std::vector<double> u(N, 0.0), y1(n), y2(n);
@@ -1599,7 +1845,7 @@ int build_dense_w(qp_ctx* c) {
   f_solve_dev(c, c->rhs2, c->xbuf);
   cudaMemcpyAsync(y2.data(), c->xbuf, n * 8, cudaMemcpyDeviceToHost, st);
   cudaMemsetAsync(c->xbuf, 0, n * 8, st);
-  dense_symv(W, ld, n, c->dw_chunks, c->dw_nch, c->rhs2, c->xbuf, nullptr, c->sm_count, st);
+  dense_symv(W, ld, n, c->dw_chunks, c->dw_nch, &c->dw_plan_all, c->rhs2, c->xbuf, nullptr, c->sm_count, st);
   cudaMemcpyAsync(y1.data(), c->xbuf, n * 8, cudaMemcpyDeviceToHost, st);
   cudaMemsetAsync(c->rhs2, 0, N * 8, st);
   if (int rc = sync_check(c, "dense W guard")) return rc;
@@ -1797,8 +2043,8 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
       F.d.flat = (F.flat_discrepancy <= 1e-10 && std::isfinite(F.flat_discrepancy)) ? 1 : 0;
       if (!F.d.flat) cudaMemsetAsync(F.d.acc, 0, N * 8, st);   // the sweeps expect zero accumulators
     }
-    if (int rc2 = build_dense_w(c)) return rc2;
   }
+  if (int rc2 = build_dense_w(c)) return rc2;   // explicit W / small-N F⁻¹ (with or without a symmetric root)
   // ---- P_H: T = C diag(H)⁻¹ Cᵀ pattern (host) and values (device), symbolic of D + T
   if (p == QP_PREC_HIGH) {
     const bool verbose = std::getenv("QPB_VERBOSE") != nullptr;
@@ -2150,6 +2396,8 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->dense_w_enabled = c->dense_w ? 1.0 : 0.0;
     s->dense_w_discrepancy = c->dw_discrepancy;
     s->kf_bytes_W = c->dense_w ? 4.0 * (double)c->n * (double)(c->n + 1) * c->dw_share : 0.0;
+    s->dense_finv_enabled = c->dense_finv ? 1.0 : 0.0;
+    s->dense_finv_discrepancy = c->df_discrepancy;
   }
   return QP_OK;
 }

@@ -1891,11 +1891,47 @@ void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t m
   k_build_xinv<<<grid, NT, 0, s>>>(F, big_sns, n_big);
 }
 
+// Deterministic epilogue of a symmetric-GEMV chunk (see SymvPlan): the chunk's row partial (red[512 ..],
+// Rn rows, output block rob) and column partials (colv, ncol_t = 64·ncob columns, output blocks
+// cob0 .. cob0+ncob−1) go to the chunk's slot; the last arriver of each output block reduces it in the
+// plan's fixed order.  `red` (≥ 576 doubles of shared memory) is reused as scratch after a barrier.
+__device__ __forceinline__ void symv_epilogue(const SymvPlan& P, int64_t idx, int Rn, int rob, int ncol_t, int cob0,
+                                              const double* red_row, const double* colv, double* red, double* x) {
+  const int tid = threadIdx.x;
+  __shared__ int last[9];
+  double* slot = P.slots + (idx - P.c_begin) * 576;
+  if (tid < Rn) slot[tid] = red_row[tid];
+  for (int c = tid; c < ncol_t; c += NT) slot[64 + c] = colv[c];
+  __threadfence();
+  __syncthreads();
+  const int ncob = ncol_t >> 6;
+  if (tid <= ncob) {
+    const int ob = (tid == 0 ? rob : cob0 + tid - 1) - P.ob_lo;
+    const unsigned old = atomicAdd(P.cnt + ob, 1u);
+    last[tid] = (old + 1u == (unsigned)P.expect[ob]) ? ob : -1;
+  }
+  __syncthreads();
+  for (int j = 0; j <= ncob; ++j) {
+    const int ob = last[j];
+    if (ob < 0) continue;       // uniform across the CTA (shared)
+    __threadfence();
+    const int i = tid & 63, g = tid >> 6, w = P.width[ob];
+    double acc = 0.0;
+    for (int64_t e = P.lptr[ob] + g; e < P.lptr[ob + 1]; e += 4)
+      if (i < w) acc += __ldcg(P.slots + P.lsrc[e] + i);
+    red[g * 64 + i] = acc;
+    __syncthreads();
+    if (tid < w) x[P.x0[ob] + tid] += (red[tid] + red[64 + tid]) + (red[128 + tid] + red[192 + tid]);
+    if (tid == 0) P.cnt[ob] = 0u;
+    __syncthreads();
+  }
+}
+
 // Symmetric-root GEMV as its own kernel (between the forward and backward sparse sweeps):
 // x_J += S_J⁻¹ v_J over the chunks (I, K0..K0+nK) of every symmetric root, grid-stride, no flags.
 template <int U, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* x, int64_t c_begin, int64_t c_end,
-                                                           const int* done_flag, const double* sub) {
+                                                           SymvPlan P, const int* done_flag, const double* sub) {
   __shared__ double vK[512];
   __shared__ double vI[64];
   __shared__ double red[576];
@@ -1924,8 +1960,8 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
     }
     __syncthreads();
     schunk_gemv<U>(Mc, ldx, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
-    if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
-    for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
+    __syncthreads();
+    symv_epilogue(P, idx, Rn, bI, ncol_t, bK, red + 512, colv, vK, x);
   }
   tl_end(2, tls);
 }
@@ -1935,7 +1971,7 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
 // block) through schunk_gemv, so each lower tile is read once for x_I += W_IK v_K and x_K += W_IKᵀ v_I.
 template <int U, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks,
-                                                         int64_t nch, const double* v, double* x,
+                                                         int64_t nch, SymvPlan P, const double* v, double* x,
                                                          const int* done_flag) {
   __shared__ double vK[512];
   __shared__ double vI[64];
@@ -1957,10 +1993,44 @@ __global__ void __launch_bounds__(NT, MINB) k_dense_symv(const double* W, int64_
     if (tid < Rn) vI[tid] = v[rI + tid];
     __syncthreads();
     schunk_gemv<U>(W + rI + cK * ld, ld, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
-    if (tid < Rn) atomicAdd(x + rI + tid, red[512 + tid]);
-    for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + cK + c, colv[c]);
+    __syncthreads();
+    symv_epilogue(P, P.c_begin + idx, Rn, ch.x, ncol_t, ch.y, red + 512, colv, vK, x);
   }
   tl_end(2, tls);
+}
+
+// v[c] = the F-solve right-hand side described by R, for every c < N (dense F⁻¹ mode: the GEMV needs it
+// materialised): R.rhs (optionally gathered through in_perm), or (Cᵀp)_c fused (warp per row).
+__global__ void k_gather_rhs(SweepRhs R, double* v, double* out, int64_t N) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+  for (int64_t c = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); c < N; c += nw) {
+    double x = 0.0;
+    if (R.ct.p == nullptr) {
+      if (lane == 0) x = R.rhs[R.in_perm ? R.in_perm[c] : c];
+    } else if (c < R.ct.nrows) {
+      const int64_t q0 = __ldg(R.ct.p + c), q1 = __ldg(R.ct.p + c + 1);
+      for (int64_t q = q0 + lane; q < q1; q += 32) x += __ldg(R.ct.v + q) * __ldg(R.p + __ldg(R.ct.i + q));
+      x = warp_sum(x);
+    }
+    if (lane == 0) {
+      v[c] = x;
+      out[c] = 0.0;   // the GEMV's reducers accumulate into out
+    }
+  }
+}
+__global__ void k_zero_flag(double* v, int64_t n, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) v[i] = 0.0;
+}
+void zero_flag(double* v, int64_t n, const int* done_flag, cudaStream_t s) {
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + NT - 1) / NT, 148 * 8));
+  k_zero_flag<<<g, NT, 0, s>>>(v, n, done_flag);
+}
+void gather_rhs(const SweepRhs& r, double* v, double* out, int64_t N, int sms, cudaStream_t s) {
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, (int64_t)sms * 8));
+  k_gather_rhs<<<g, NT, 0, s>>>(r, v, out, N);
 }
 
 // W[r0 + a, r0 + b] = S⁻¹(a, b) for a ≥ b (x-part of the symmetric root, lower storage Sinv with ldx).
@@ -1984,24 +2054,24 @@ void w_symmetrize_diag(double* W, int64_t ld, int64_t n, cudaStream_t s) {
   if (n > 0) k_w_symmetrize_diag<<<(unsigned)((n + 63) / 64), NT, 0, s>>>(W, ld, n);
 }
 
-void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const double* v, double* x,
-                const int* done_flag, int sms, cudaStream_t s) {
+void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const SymvPlan* plan,
+                const double* v, double* x, const int* done_flag, int sms, cudaStream_t s) {
   if (nch <= 0) return;
-  k_dense_symv<16, 3><<<sms * 3, NT, 0, s>>>(W, ld, n, chunks, nch, v, x, done_flag);
+  k_dense_symv<16, 3><<<sms * 3, NT, 0, s>>>(W, ld, n, chunks, nch, *plan, v, x, done_flag);
 }
 
-void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
-                  cudaStream_t s, const double* sub) {
+void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const SymvPlan* plan,
+                  const int* done_flag, int grid, cudaStream_t s, const double* sub) {
   if (c_end <= c_begin) return;
   static int variant = std::getenv("QPB_GEMV_VARIANT") ? std::atoi(std::getenv("QPB_GEMV_VARIANT")) : 3;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   switch (variant) {
-    case 1: k_symroot_gemv<8, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
-    case 2: k_symroot_gemv<16, 2><<<sms * 2, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
-    case 3: k_symroot_gemv<16, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
-    case 4: k_symroot_gemv<4, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
-    default: k_symroot_gemv<8, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, done_flag, sub); break;
+    case 1: k_symroot_gemv<8, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
+    case 2: k_symroot_gemv<16, 2><<<sms * 2, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
+    case 3: k_symroot_gemv<16, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
+    case 4: k_symroot_gemv<4, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
+    default: k_symroot_gemv<8, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
   }
   (void)grid;
 }
@@ -2125,15 +2195,14 @@ __global__ void __launch_bounds__(NT) k_flat_fwd_t(DevFactor F, const int* done_
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
   const unsigned tls = tl_begin(1);
   const int lane = threadIdx.x & 31;
-  const int64_t rc0 = F.fl_rc0, nu = F.fl_nunits, total = nu + rc0;
+  const int64_t nu = F.fl_nunits, total = nu;
   const int64_t nw = (int64_t)gridDim.x * (NT / 32);
   for (int64_t u = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); u < total; u += nw) {
-    if (u < nu) {
+    {
       const FlatUnit f = load_unit(F.fl_units, u);
       const int nrows = f.shape & 0xffff, ncols = f.shape >> 16;
       if (lane >= nrows) continue;
       const bool okb = lane + 32 < nrows;
-      const int32_t ia = __ldg(F.fl_rows + f.roff + lane), ib = okb ? __ldg(F.fl_rows + f.roff + lane + 32) : 0;
       const double* Mu = F.fl_mval + f.moff;
       double ma[8], mb[8], bv[8];
 #pragma unroll
@@ -2149,26 +2218,45 @@ __global__ void __launch_bounds__(NT) k_flat_fwd_t(DevFactor F, const int* done_
         sa = fma(ma[c], bv[c], sa);
         sb = fma(mb[c], bv[c], sb);
       }
-      atomicAdd(F.vbuf + rc0 + ia, -sa);
-      if (okb) atomicAdd(F.vbuf + rc0 + ib, -sb);
-    } else {   // forest column c: y1[rows of L11⁻¹(:, c)] += L11⁻¹(:, c) b1_c
-      const int64_t c = u - nu;
-      const double bc = F.acc[c];
-      const int64_t e1 = F.fl_cp[c + 1];
-      for (int64_t e = F.fl_cp[c] + lane; e < e1; e += 32) atomicAdd(F.vbuf + F.fl_ci[e], F.fl_nval[e] * bc);
+      F.fl_fslot[u * 64 + lane] = sa;              // reduced per root row, in unit order, by k_flat_fwd_red
+      if (okb) F.fl_fslot[u * 64 + 32 + lane] = sb;
     }
   }
   tl_end(1, tls);
+}
+
+// Forward reductions (fixed order, no atomics): forest row i — y1_i = Σ_j L11⁻¹(i, j) b1_j (row form of
+// L11⁻¹); root row r — vbuf[rc0 + r] −= Σ of its unit partials in unit order.  Warp per row.
+__global__ void __launch_bounds__(NT) k_flat_fwd_red(DevFactor F, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t rc0 = F.fl_rc0, N = F.N;
+  const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+  for (int64_t t = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); t < N; t += nw) {
+    double v = 0.0;
+    if (t < rc0) {
+      for (int64_t e = F.fl_rp[t] + lane; e < F.fl_rp[t + 1]; e += 32)
+        v += F.fl_nval[F.fl_r2c[e]] * F.acc[F.fl_rj[e]];
+    } else {
+      const int64_t r = t - rc0;
+      for (int64_t e = F.fl_fr_ptr[r] + lane; e < F.fl_fr_ptr[r + 1]; e += 32) v += __ldcg(F.fl_fslot + F.fl_fr_src[e]);
+    }
+    v = warp_sum(v);
+    if (lane == 0) {
+      if (t < rc0) F.vbuf[t] = v;
+      else F.vbuf[t] -= v;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(NT) k_flat_bwd_t(DevFactor F, double* x, const int* done_flag) {
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
   const unsigned tls = tl_begin(3);
   const int lane = threadIdx.x & 31;
-  const int64_t rc0 = F.fl_rc0, nu = F.fl_nunits, total = nu + rc0;
+  const int64_t rc0 = F.fl_rc0, nu = F.fl_nunits, total = nu;
   const int64_t nw = (int64_t)gridDim.x * (NT / 32);
   for (int64_t u = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); u < total; u += nw) {
-    if (u < nu) {   // warp-uniform branch: the shuffles below need all 32 lanes
+    {   // warp-uniform: the shuffles below need all 32 lanes
       const FlatUnit f = load_unit(F.fl_units, u);
       const int nrows = f.shape & 0xffff, ncols = f.shape >> 16;
       const bool oka = lane < nrows, okb = lane + 32 < nrows;
@@ -2188,19 +2276,30 @@ __global__ void __launch_bounds__(NT) k_flat_bwd_t(DevFactor F, double* x, const
       for (int c = 0; c < 8; ++c) tt[c] = ma[c] * xa + mb[c] * xb;
       const double s = transpose_reduce8(tt, lane);
       const int col = lane >> 2;
-      if ((lane & 3) == 0 && col < ncols) atomicAdd(x + f.col0 + col, -s);
-    } else {   // forest column c: x_c += Σ_i L11⁻¹(i, c) y1_i / d_i
-      const int64_t c = u - nu;
-      double v = 0.0;
-      for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32) {
-        const int32_t i = F.fl_ci[e];
-        v += F.fl_nval[e] * F.vbuf[i] / F.Dpiv[i];
-      }
-      v = warp_sum(v);
-      if (lane == 0) atomicAdd(x + c, v);
+      if ((lane & 3) == 0 && col < ncols) F.fl_bslot[u * 8 + col] = s;   // reduced by k_flat_bwd_red
     }
   }
   tl_end(3, tls);
+}
+
+// Backward reduction (fixed order, no atomics), warp per forest column c:
+// x_c += Σ_i L11⁻¹(i, c) y1_i / d_i − Σ of its unit partials (Mᵀ x_root) in unit order.
+__global__ void __launch_bounds__(NT) k_flat_bwd_red(DevFactor F, double* x, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t rc0 = F.fl_rc0;
+  const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+  for (int64_t c = blockIdx.x * (int64_t)(NT / 32) + (threadIdx.x >> 5); c < rc0; c += nw) {
+    double v = 0.0, t = 0.0;
+    for (int64_t e = F.fl_cp[c] + lane; e < F.fl_cp[c + 1]; e += 32) {
+      const int32_t i = F.fl_ci[e];
+      v += F.fl_nval[e] * F.vbuf[i] / F.Dpiv[i];
+    }
+    for (int64_t e = F.fl_bc_ptr[c] + lane; e < F.fl_bc_ptr[c + 1]; e += 32) t += __ldcg(F.fl_bslot + F.fl_bc_src[e]);
+    v = warp_sum(v);
+    t = warp_sum(t);
+    if (lane == 0) x[c] += v - t;
+  }
 }
 
 __global__ void k_flat_fill_rows(DevFactor F, const int32_t* src, int64_t nnz) {
@@ -2289,9 +2388,10 @@ void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cud
   if (!r.rhs_ready) flat_rhs(F, r, x, sms, s);
   static const bool tiles = !(std::getenv("QPB_FLAT_TILES") && std::getenv("QPB_FLAT_TILES")[0] == '0');
   if (tiles) {
-    const int64_t nwarps = F.fl_nunits + F.fl_rc0;
-    const int gt = (int)std::max<int64_t>(1, std::min<int64_t>((nwarps + 7) / 8, (int64_t)sms * 8));
+    const int gt = (int)std::max<int64_t>(1, std::min<int64_t>((F.fl_nunits + 7) / 8, (int64_t)sms * 8));
     k_flat_fwd_t<<<gt, NT, 0, s>>>(F, r.done_flag);
+    const int gr = (int)std::max<int64_t>(1, std::min<int64_t>((F.N + 7) / 8, (int64_t)sms * 8));
+    k_flat_fwd_red<<<gr, NT, 0, s>>>(F, r.done_flag);
     return;
   }
   const int64_t nY = (F.fl_rc0 + 7) / 8, nRr = (F.N - F.fl_rc0 + 7) / 8;
@@ -2301,9 +2401,10 @@ void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cud
 void flat_backward(const DevFactor& F, double* x, const int* done_flag, int sms, cudaStream_t s) {
   static const bool tiles = !(std::getenv("QPB_FLAT_TILES") && std::getenv("QPB_FLAT_TILES")[0] == '0');
   if (tiles) {
-    const int64_t nwarps = F.fl_nunits + F.fl_rc0;
-    const int gt = (int)std::max<int64_t>(1, std::min<int64_t>((nwarps + 7) / 8, (int64_t)sms * 8));
+    const int gt = (int)std::max<int64_t>(1, std::min<int64_t>((F.fl_nunits + 7) / 8, (int64_t)sms * 8));
     k_flat_bwd_t<<<gt, NT, 0, s>>>(F, x, done_flag);
+    const int gr = (int)std::max<int64_t>(1, std::min<int64_t>((F.fl_rc0 + 7) / 8, (int64_t)sms * 8));
+    k_flat_bwd_red<<<gr, NT, 0, s>>>(F, x, done_flag);
     return;
   }
   const int64_t nX = (F.fl_rc0 + 7) / 8;

@@ -118,6 +118,12 @@ struct DevFactor {
   double* fl_mr_val;
   const int4* fl_units;           // M product units (≤ 64 rows × ≤ 8 columns), 2 × int4 each (k_flat_*_t)
   int64_t fl_nunits;
+  double* fl_fslot;               // per unit: 64 row partials of the forward product (deterministic reduction)
+  double* fl_bslot;               // per unit: 8 column partials of the backward product
+  const int64_t* fl_fr_ptr;       // per root row: its forward slots fl_fr_src[ptr[r] .. ptr[r+1]) (unit order)
+  const int32_t* fl_fr_src;
+  const int64_t* fl_bc_ptr;       // per forest column: its backward slots (unit order)
+  const int32_t* fl_bc_src;
   int mf_group;                   // pivot blocks per trailing UPDATE (Symbolic::mf_group)
   unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][8 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
@@ -125,6 +131,22 @@ struct DevFactor {
   int use_sym;        // 1: symmetric roots swept through S⁻¹ (queues fwd_tasks/bwd_tasks hold SCHUNK/ROOTB)
   int l2hint;         // A/B switch (QPB_L2HINT, default 0 = measured best): bit 0 = root GEMV streams S⁻¹ with L2::evict_first,
                       // bit 1 = flattened-forest arrays loaded with L2::evict_last (kept across F-solves)
+};
+
+// Deterministic accumulation plan of a chunked symmetric GEMV (k_dense_symv, k_symroot_gemv): every chunk
+// writes its row and column partials to its own slot (64 + 512 doubles); the CTA that brings an output
+// block's arrival counter to `expect` sums that block's slots in the fixed order lsrc[lptr[o] .. lptr[o+1])
+// and adds the sum to x — no floating-point atomics, so results are bit-identical run to run.
+struct SymvPlan {
+  double* slots;             // (c_end − c_begin) × 576 doubles
+  unsigned* cnt;             // per output block, reset to 0 by its reducer
+  const int32_t* expect;     // per output block: contributing chunks
+  const int64_t* lptr;       // per output block: slot list (slot offsets in doubles)
+  const int64_t* lsrc;
+  const int32_t* width;      // per output block: rows (≤ 64)
+  const int64_t* x0;         // per output block: first index in x
+  int64_t c_begin;
+  int32_t ob_lo;             // output block id of the first block (symroot: F block id − ob_lo)
 };
 
 // CSR on the device (int64 row pointers, int32 columns).
@@ -203,11 +225,16 @@ struct SweepRhs {
   int rhs_ready;            // flattened forest: acc / vbuf / x already prepared (fused PCG step, phase D)
 };
 void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s);
+// v[0, N) = the right-hand side described by r, out[0, N) = 0 (dense F⁻¹ mode)
+void gather_rhs(const SweepRhs& r, double* v, double* out, int64_t N, int sms, cudaStream_t s);
+// v[0, n) = 0 unless *done_flag
+void zero_flag(double* v, int64_t n, const int* done_flag, cudaStream_t s);
 void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s);
 int trsv_grid(int device);
 // x_J += S_J⁻¹ v_J for the symmetric-root chunks [c_begin, c_end) (dedicated kernel)
 // sub != nullptr: the root's right-hand side is vbuf − sub (flattened forest: sub = acc = M b1)
-void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const int* done_flag, int grid,
+void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const SymvPlan* plan,
+                  const int* done_flag, int grid,
                   cudaStream_t s, const double* sub = nullptr);
 // flattened forest F-solve halves (see Symbolic::flat) and the per-column extraction of M and L11⁻¹
 void flat_forward(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s);
@@ -247,7 +274,8 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
 void w_copy_root(const double* Sinv, int64_t ldx, double* W, int64_t ld, int64_t r0, int64_t n, cudaStream_t s);
 void w_symmetrize_diag(double* W, int64_t ld, int64_t n, cudaStream_t s);
 // x += W v, W the explicit x-block of F⁻¹ (k_dense_symv; chunks = (row block, first column block) pairs)
-void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const double* v, double* x,
+void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const SymvPlan* plan,
+                const double* v, double* x,
                 const int* done_flag, int sms, cudaStream_t s);
 // the flattened forest's right-hand side kernel alone (k_flat_rhs), for the first PCG iteration
 void flat_rhs(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s);

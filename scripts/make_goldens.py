@@ -11,7 +11,7 @@ inputs of ``qpgen.probe_inputs`` (D with a six-decade spread, N(0,1) vectors):
 * ``PH<k>``, ``PHeps``  the same with P_H = D + C diag(H)⁻¹Cᵀ where the oracle can
                factor P_H (c1 dense LAPACK, c4s SuperLU in the banded row order);
 * ``ipm_pl``   the oracle PL-KF IPM's first 15 iterations (μ, residual norms, α, PCG counts);
-* ``ipm_pl_var`` the same with r_ν perturbed by 1e-15 (two seeds): the rounding spread of the counts;
+* ``ipm_pl_var`` the same with r_ν perturbed by 1e-15 (seeds 1–4): the rounding spread of the counts;
 * ``ipm_ph``   the oracle PH-KF IPM at ipm_tol 1e-10 (objective, counts, trace) — c4s;
 * ``ipm_direct`` c1: the oracle IPM with DIRECT K_F solves (K_F = D − C W Cᵀ formed densely with the
                written-out W = (F⁻¹)₁₁ and Cholesky-factored) at ipm_tol 1e-10 — the optimum's objective,
@@ -40,6 +40,7 @@ from oracle.pcg import pcg  # noqa: E402
 OUT = os.path.join(ROOT, "tests", "golden", "full")
 PH_OK = {"c1": dict(sparse=False, keep=False), "c4s": dict(sparse=True, order="natural")}
 IPM_PH = ("c4s",)
+VARIANTS = tuple(int(v) for v in os.environ.get("GOLD_VARIANTS", "1,2,3,4").split(","))
 KS = (1, 3, 7)
 
 
@@ -58,12 +59,17 @@ def sample(v, idx):
 
 
 def save(cfg, stage, payload):
+    """Merge `payload` into tests/golden/full/<cfg>.npz (under a file lock: stages may run in parallel)."""
+    import fcntl
     os.makedirs(OUT, exist_ok=True)
     path = os.path.join(OUT, f"{cfg}.npz")
-    old = dict(np.load(path, allow_pickle=False)) if os.path.exists(path) else {}
-    for k, v in payload.items():
-        old[f"{stage}/{k}"] = np.asarray(v)
-    np.savez_compressed(path, **old)
+    with open(path + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        old = dict(np.load(path, allow_pickle=False)) if os.path.exists(path) else {}
+        for k, v in payload.items():
+            old[f"{stage}/{k}"] = np.asarray(v)
+        np.savez_compressed(path + ".tmp.npz", **old)
+        os.replace(path + ".tmp.npz", path)
     log("saved", cfg, stage, sorted(payload))
 
 
@@ -127,12 +133,28 @@ def main():
         # rounding-level variants of the same trajectory (r_ν perturbed by 1e-15 relative): the spread of
         # their PCG counts is what rounding alone does to the counts (DESIGN reading R12)
         pay = {}
-        for v in (1, 2):
+        for v in VARIANTS:
             t = time.time()
             r = ipm_solve(qp, precond="low", max_ipm=15, fs=fs, rnu_perturb=v)
             meta[f"t_ipm_pl_var{v}_s"] = time.time() - t
             pay[f"pcg_v{v}"] = [d["pcg"] for d in r.trace]
             pay[f"mu_v{v}"] = [d["mu"] for d in r.trace]
+        save(cfg, "ipm_pl_var", pay)
+    if "ipm_pl_opv" in stages:
+        # operator variants: the same trajectory with the F-solves through another exact route (SuperLU's
+        # LU of H in a different column order — other rounding in every K_F product)
+        from oracle.fsolve import BlockF as _BF
+        import scipy.sparse.linalg as _spla
+        pay = {}
+        for v, spec in enumerate(("COLAMD", "MMD_ATA"), start=1):
+            fs2 = _BF(qp.H, qp.A, None) if qp.x_perm is None else _BF(qp.H, qp.A, qp.x_perm)
+            if qp.x_perm is None:
+                fs2.lu = _spla.splu(qp.H.tocsc(), permc_spec=spec, diag_pivot_thresh=0.0,
+                                    options=dict(SymmetricMode=True))
+            t = time.time()
+            r = ipm_solve(qp, precond="low", max_ipm=15, fs=fs2, rnu_perturb=10 + v if qp.x_perm is not None else None)
+            meta[f"t_ipm_pl_opv{v}_s"] = time.time() - t
+            pay[f"pcg_v{10 + v}"] = [d["pcg"] for d in r.trace]
         save(cfg, "ipm_pl_var", pay)
     if "ipm_direct" in stages and cfg == "c1":
         t = time.time()

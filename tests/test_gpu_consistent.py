@@ -1,0 +1,37 @@
+"""PL-KF along a converging trajectory — the paper's benchmark protocol (scripts/consistent_pl.py):
+the IPM steps with a (near-)direct Δν (GPU: PH-KF PCG to 1e-12; oracle: a dense direct K_F solve) and
+PL-KF's PCG runs on every system only to count its iterations.  Against the oracle's twin
+(oracle.ipm.ipm_solve(direct=True, consistent="low")) on c0: both converge, same IPM iteration count ±1,
+objective within 1e-8 of the oracle's; and on every system of the GPU's trajectory the GPU's PL count
+lies within ±2 of the oracle PCG's count on that same system and its rounding-equivalent variants,
+while the count is within Corollary 1's (n − m1) + 1 (beyond it counts are rounding-decided, R12)."""
+import os
+import sys
+
+import pytest
+
+import qpgen
+from oracle.ipm import ipm_solve as oracle_ipm
+
+pytestmark = pytest.mark.gpu
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+
+
+def test_consistent_pl_c0_matches_oracle():
+    from consistent_pl import consistent_pl
+    from oracle import kkt
+    from oracle.fsolve import BlockF, DenseF
+    from oracle.pcg import pcg
+    qp = qpgen.make("c0")
+    got = consistent_pl(qp, pl_maxit=2000, ipm_tol=1e-8, keep_systems=True)
+    ref = oracle_ipm(qp, precond="low", ipm_tol=1e-8, direct=True, consistent="low")
+    assert got["converged"] and ref.converged
+    assert abs(got["n_ipm"] - ref.n_ipm) <= 1
+    assert abs(got["objective"] - ref.objective) <= 1e-8 * abs(ref.objective)
+    bound = qp.n - qp.m1 + 1
+    routes = [DenseF(qp.H, qp.A), BlockF(qp.H, qp.A), DenseF(qp.H, qp.A, explicit_w=True)]
+    for k, ((D, rnu, eps), g) in enumerate(zip(got["systems"], got["pl_counts"])):
+        its = [pcg(lambda p: kkt.KF_apply(qp, fs, D, p), rnu, kkt.PrecondL(D), eps, 2000)[1] for fs in routes]
+        if min(its) > bound:
+            continue
+        assert min(its) - 2 <= g <= max(its) + 2, (k, g, its)

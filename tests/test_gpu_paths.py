@@ -99,7 +99,7 @@ def test_path_variant_matches_oracle(oracle_case, variant):
     if name == "dense_m1" and variant in ("default", "unfused"):
         assert out["dense_w"] == 1.0          # chosen by bytes
     if name == "c0" and variant == "default":
-        assert out["dense_w"] == 0.0          # c0: one F-solve (150 KB) reads less than W (160 KB)
+        assert out["dense_w"] == 1.0          # c0 (N = 250): the small-N explicit F⁻¹, W its x-block
     if VARIANTS[variant].get("QPB_DENSE_W") == "0":
         assert out["dense_w"] == 0.0
     if VARIANTS[variant].get("QPB_DENSE_W") == "2":
