@@ -180,26 +180,26 @@ SymvPlan build_symv_plan(DeviceArena& m, cudaStream_t st, int64_t c_begin, int64
                          const std::vector<int32_t>& width, const std::vector<int64_t>& x0) {
   const int64_t nc = c_end - c_begin;
   std::vector<int64_t> lptr(nob + 1, 0);
-  std::vector<int32_t> expect(nob, 0);
   for (int64_t i = 0; i < nc; ++i) {
-    expect[rob[i] - ob_lo] += 1;
-    for (int32_t k = 0; k < ncob[i]; ++k) expect[cob0[i] + k - ob_lo] += 1;
+    lptr[rob[i] - ob_lo + 1] += 1;
+    for (int32_t k = 0; k < ncob[i]; ++k) lptr[cob0[i] + k - ob_lo + 1] += 1;
   }
-  for (int32_t o = 0; o < nob; ++o) lptr[o + 1] = lptr[o] + expect[o];
-  std::vector<int64_t> lsrc(lptr[nob]), fill(lptr.begin(), lptr.end() - 1);
-  for (int64_t i = 0; i < nc; ++i) lsrc[fill[rob[i] - ob_lo]++] = i * 576;          // row partials first
+  for (int32_t o = 0; o < nob; ++o) lptr[o + 1] += lptr[o];
+  std::vector<int64_t> woff((size_t)nc * 9, -1), fill(lptr.begin(), lptr.end() - 1);
+  for (int64_t i = 0; i < nc; ++i) woff[i * 9] = 64 * fill[rob[i] - ob_lo]++;          // row partials first
   for (int64_t i = 0; i < nc; ++i)
-    for (int32_t k = 0; k < ncob[i]; ++k) lsrc[fill[cob0[i] + k - ob_lo]++] = i * 576 + 64 + 64 * (int64_t)k;
+    for (int32_t k = 0; k < ncob[i]; ++k) woff[i * 9 + 1 + k] = 64 * fill[cob0[i] + k - ob_lo]++;
   SymvPlan P{};
-  P.slots = m.zeros<double>((size_t)std::max<int64_t>(1, nc) * 576, st);
-  P.cnt = m.zeros<unsigned>((size_t)std::max(1, nob), st);
-  P.expect = m.upload(expect, st);
+  static const bool det = !(std::getenv("QPB_DETERMINISTIC") && std::getenv("QPB_DETERMINISTIC")[0] == '0');
+  P.slots = det ? m.zeros<double>((size_t)std::max<int64_t>(1, lptr[nob]) * 64, st) : nullptr;
+  P.nob = nob;
   P.lptr = m.upload(lptr, st);
-  P.lsrc = m.upload(lsrc, st);
+  P.woff = m.upload(woff, st);
   P.width = m.upload(width, st);
   P.x0 = m.upload(x0, st);
   P.c_begin = c_begin;
   P.ob_lo = ob_lo;
+  cudaStreamSynchronize(st);   // host vectors
   return P;
 }
 
@@ -836,7 +836,7 @@ double* ist_red(qp_ctx* c) { return (double*)((char*)c->ist + offsetof(IpmState,
 
 void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
   if (!F.sym_enabled) return;
-  c->launches += 1;
+  c->launches += F.sym_symv.slots ? 2 : 1;
   symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, &F.sym_symv, done, c->sm_count * 3, c->stream);
 }
 
@@ -845,7 +845,7 @@ void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
 void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
   Factor& F = c->FF;
   if (c->dense_finv) {   // small N: out = F⁻¹ v, one deterministic symmetric GEMV (DESIGN §5 "dense F⁻¹")
-    c->launches += 2;
+    c->launches += c->df_plan.slots ? 3 : 2;
     int h = c->begin(8);
     gather_rhs(r, c->df_rhs, out, F.d.N, c->sm_count, c->stream);
     dense_symv(c->dense_finv, c->df_ld, F.d.N, c->df_chunks, c->df_nch, &c->df_plan, c->df_rhs, out, r.done_flag,
@@ -897,9 +897,12 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
     }   // else ubuf = Cᵀp and xbuf[0, n) = 0 come from the fused step's phase D
     int h = c->begin(9);
     dense_symv(c->dense_w, c->dw_ld, c->n, c->dw_chunks + c->dw_c0, c->dw_c1 - c->dw_c0, &c->dw_plan, c->ubuf, c->xbuf,
-               r.done_flag, c->sm_count, c->stream);
+               r.done_flag, c->sm_count, c->stream, false);
     c->end(h);
-    c->launches += 1;
+    h = c->begin(7);   // its fixed-order reduction (profiled apart from the GEMV)
+    symv_reduce(&c->dw_plan, c->xbuf, r.done_flag, c->sm_count, c->stream);
+    c->end(h);
+    c->launches += c->dw_plan.slots ? 2 : 1;   // GEMV (+ its fixed-order reduction)
     if (int rc = c->allreduce(c->xbuf, c->n, 0)) return rc;       // w = Σ_ranks (this rank's chunks)·u
     if (fsolve_only) return 0;
     h = c->begin(2);
@@ -942,7 +945,7 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
 // z = P_H⁻¹ r (a7), P_H factor order via perm_ph.
 void ph_apply_dev(qp_ctx* c, const double* r, double* z, const int* done) {
   if (c->phinv_ready) {   // small m2: z = P_H⁻¹ r, one deterministic symmetric GEMV
-    c->launches += 2;
+    c->launches += c->pi_plan.slots ? 3 : 2;
     int h = c->begin(4);
     zero_flag(z, c->m2, done, c->stream);
     dense_symv(c->phinv, c->pi_ld, c->m2, c->pi_chunks, c->pi_nch, &c->pi_plan, r, z, done, c->sm_count, c->stream);
@@ -2073,7 +2076,9 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
     for (int64_t i = 0; i < m2; ++i)
       for (int64_t q = tp[i]; q < tp[i + 1]; ++q) trow[q] = i;
     if (verbose) std::fprintf(stderr, "qpb: P_H pattern of T (%lld entries) %.2f s\n", (long long)c->nnz_t, now_s() - tph0);
-    // ordering of P_H: minimum degree on the pattern of T
+    // ordering of P_H: minimum degree on the pattern of T (or nested dissection, below)
+    std::vector<int64_t> ph_ptr;
+    std::vector<int32_t> ph_idx;
     {
       std::vector<int64_t> ptr(m2 + 1, 0);
       std::vector<int32_t> idx;
@@ -2087,31 +2092,36 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
       // stop the minimum-degree search once the minimum degree reaches half the remaining nodes
       const double ds = std::getenv("QPB_PH_DENSE_STOP") ? std::atof(std::getenv("QPB_PH_DENSE_STOP")) : 0.5;
       c->perm_ph = etree_postorder(m2, ptr, idx, min_degree_order(m2, ptr, idx, ds));
+      ph_ptr.swap(ptr);
+      ph_idx.swap(idx);
     }
-    if (verbose) std::fprintf(stderr, "qpb: P_H ordering %.2f s\n", now_s() - tph0);
-    std::vector<int64_t> pinv_ph(m2);
-    for (int64_t i = 0; i < m2; ++i) pinv_ph[c->perm_ph[i]] = i;
-    LowerMatrix PM;
-    PM.N = m2;
-    PM.colptr.assign(m2 + 1, 0);
-    PM.diag_src.assign(m2, -1);
-    for (int64_t i = 0; i < m2; ++i)
-      for (int64_t q = tp[i]; q < tp[i + 1]; ++q) {
-        int64_t a = pinv_ph[i], bb = pinv_ph[ti[q]];
-        if (a > bb) PM.colptr[bb + 1]++;
-        else if (a == bb) PM.diag_src[a] = q;
-      }
-    for (int64_t j = 0; j < m2; ++j) PM.colptr[j + 1] += PM.colptr[j];
-    PM.rowind.resize(PM.colptr[m2]);
-    PM.src.resize(PM.colptr[m2]);
-    {
+    // P_H is refactored at every D: no symmetric root, and supernodes capped at 4096 columns so the
+    // partitioned inverses of its sweeps cost Σ B³/6 per refactor instead of w³/6 (QPB_PH_MAXW)
+    const int64_t ph_maxw = std::getenv("QPB_PH_MAXW") ? std::atoll(std::getenv("QPB_PH_MAXW")) : 4096;
+    // lower pattern of P_H in the order `perm` (+ source index of every entry in T's values)
+    auto build_pm = [&](const std::vector<int64_t>& perm, LowerMatrix& PM) {
+      std::vector<int64_t> pinv_ph(m2);
+      for (int64_t i = 0; i < m2; ++i) pinv_ph[perm[i]] = i;
+      PM = LowerMatrix();
+      PM.N = m2;
+      PM.colptr.assign(m2 + 1, 0);
+      PM.diag_src.assign(m2, -1);
+      for (int64_t i = 0; i < m2; ++i)
+        for (int64_t q = tp[i]; q < tp[i + 1]; ++q) {
+          int64_t a2 = pinv_ph[i], bb = pinv_ph[ti[q]];
+          if (a2 > bb) PM.colptr[bb + 1]++;
+          else if (a2 == bb) PM.diag_src[a2] = q;
+        }
+      for (int64_t j = 0; j < m2; ++j) PM.colptr[j + 1] += PM.colptr[j];
+      PM.rowind.resize(PM.colptr[m2]);
+      PM.src.resize(PM.colptr[m2]);
       std::vector<int64_t> pos(PM.colptr.begin(), PM.colptr.end() - 1);
       for (int64_t i = 0; i < m2; ++i)
         for (int64_t q = tp[i]; q < tp[i + 1]; ++q) {
-          int64_t a = pinv_ph[i], bb = pinv_ph[ti[q]];
-          if (a > bb) {
+          int64_t a2 = pinv_ph[i], bb = pinv_ph[ti[q]];
+          if (a2 > bb) {
             int64_t w = pos[bb]++;
-            PM.rowind[w] = (int32_t)a;
+            PM.rowind[w] = (int32_t)a2;
             PM.src[w] = q;
           }
         }
@@ -2125,11 +2135,37 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
           PM.src[q] = tmp[q - PM.colptr[j]].second;
         }
       }
-    }
-    // P_H is refactored at every D: no symmetric root, and supernodes capped at 4096 columns so the
-    // partitioned inverses of its sweeps cost Σ B³/6 per refactor instead of w³/6 (QPB_PH_MAXW)
-    const int64_t ph_maxw = std::getenv("QPB_PH_MAXW") ? std::atoll(std::getenv("QPB_PH_MAXW")) : 4096;
+    };
+    // model time of one IPM iteration's P_H work: the refactor (c_fact at ~20 TFLOP/s) plus ~50 PCG
+    // iterations of two sweeps (the stored entries at ~6 TB/s, plus ~20 µs per supernodal level and sweep:
+    // c4s's minimum-degree P_H measured 17 ms per sweep over 825 levels)
+    auto ph_cost = [](const Symbolic& S) {
+      return S.c_fact / 20e12 + 50.0 * (16.0 * (double)S.nnz_stored / 6e12 + 2.0 * 20e-6 * (double)S.n_levels);
+    };
+    LowerMatrix PM;
+    build_pm(c->perm_ph, PM);
     e = analyse(PM, c->FP.S, 0, /*allow_symroot=*/false, -1, ph_maxw);
+    // the minimum-degree order can leave a long chain of narrow supernodes (a banded T: c4s); when its
+    // supernodal tree is deep, try nested dissection by level structures and keep the cheaper order by
+    // the model above (QPB_PH_ND=0: never, =2: always)
+    const char* nde = std::getenv("QPB_PH_ND");
+    const int ndm = nde ? std::atoi(nde) : 1;
+    if (e.empty() && ndm != 0 && (ndm == 2 || c->FP.S.n_levels > 64)) {
+      std::vector<int64_t> nd = etree_postorder(m2, ph_ptr, ph_idx, nested_dissection_order(m2, ph_ptr, ph_idx, 64));
+      LowerMatrix PM2;
+      build_pm(nd, PM2);
+      Symbolic S2;
+      std::string e2 = analyse(PM2, S2, 0, false, -1, ph_maxw);
+      const double cm = ph_cost(c->FP.S), cn = e2.empty() ? ph_cost(S2) : 1e30;
+      if (verbose)
+        std::fprintf(stderr, "qpb: P_H orders: min degree %lld levels, %.3g stored, model %.3g s; nested dissection "
+                     "%lld levels, %.3g stored, model %.3g s %s\n", (long long)c->FP.S.n_levels,
+                     (double)c->FP.S.nnz_stored, cm, (long long)S2.n_levels, (double)S2.nnz_stored, cn, e2.c_str());
+      if (ndm == 2 ? e2.empty() : cn < cm) {
+        c->perm_ph = nd;
+        c->FP.S = std::move(S2);
+      }
+    }
     if (!e.empty()) return fail(c, QP_EINVAL, "symbolic analysis of P_H: " + e);
     if (verbose) std::fprintf(stderr, "qpb: P_H symbolic %.2f s\n", now_s() - tph0);
     e = upload_factor(c, c->FP, c->ws_limit);

@@ -1891,40 +1891,59 @@ void build_xinv(const DevFactor& F, const int32_t* big_sns, int n_big, int64_t m
   k_build_xinv<<<grid, NT, 0, s>>>(F, big_sns, n_big);
 }
 
-// Deterministic epilogue of a symmetric-GEMV chunk (see SymvPlan): the chunk's row partial (red[512 ..],
-// Rn rows, output block rob) and column partials (colv, ncol_t = 64·ncob columns, output blocks
-// cob0 .. cob0+ncob−1) go to the chunk's slot; the last arriver of each output block reduces it in the
-// plan's fixed order.  `red` (≥ 576 doubles of shared memory) is reused as scratch after a barrier.
+// Epilogue of a symmetric-GEMV chunk (see SymvPlan): the chunk's row partial (red_row, Rn rows, output
+// block rob) and column partials (colv, ncol_t = 64·ncob columns, output blocks cob0 …) go to their slots;
+// k_symv_reduce then sums every output block's slots in the plan's fixed order.  (A last-arriver
+// reduction inside the GEMV — counters, fences, the arriving CTA reducing — made it 4× slower on c1.)
 __device__ __forceinline__ void symv_epilogue(const SymvPlan& P, int64_t idx, int Rn, int rob, int ncol_t, int cob0,
-                                              const double* red_row, const double* colv, double* red, double* x) {
+                                              const double* red_row, const double* colv, double* x) {
   const int tid = threadIdx.x;
-  __shared__ int last[9];
-  double* slot = P.slots + (idx - P.c_begin) * 576;
-  if (tid < Rn) slot[tid] = red_row[tid];
-  for (int c = tid; c < ncol_t; c += NT) slot[64 + c] = colv[c];
-  __threadfence();
-  __syncthreads();
-  const int ncob = ncol_t >> 6;
-  if (tid <= ncob) {
-    const int ob = (tid == 0 ? rob : cob0 + tid - 1) - P.ob_lo;
-    const unsigned old = atomicAdd(P.cnt + ob, 1u);
-    last[tid] = (old + 1u == (unsigned)P.expect[ob]) ? ob : -1;
+  if (P.slots == nullptr) {   // QPB_DETERMINISTIC=0: fp64 atomics (rounding order varies run to run)
+    if (tid < Rn) atomicAdd(x + P.x0[rob - P.ob_lo] + tid, red_row[tid]);
+    const int64_t xc = P.x0[cob0 - P.ob_lo];
+    for (int c = tid; c < ncol_t; c += NT) atomicAdd(x + xc + c, colv[c]);
+    return;
   }
-  __syncthreads();
-  for (int j = 0; j <= ncob; ++j) {
-    const int ob = last[j];
-    if (ob < 0) continue;       // uniform across the CTA (shared)
-    __threadfence();
-    const int i = tid & 63, g = tid >> 6, w = P.width[ob];
-    double acc = 0.0;
-    for (int64_t e = P.lptr[ob] + g; e < P.lptr[ob + 1]; e += 4)
-      if (i < w) acc += __ldcg(P.slots + P.lsrc[e] + i);
-    red[g * 64 + i] = acc;
+  const int64_t* wo = P.woff + (idx - P.c_begin) * 9;
+  if (tid < Rn) P.slots[wo[0] + tid] = red_row[tid];
+  for (int c = tid; c < ncol_t; c += NT) P.slots[wo[1 + (c >> 6)] + (c & 63)] = colv[c];
+}
+
+// x[block o] += Σ of its contributions, which are contiguous (64 doubles each) in the plan's fixed order:
+// CTA of 1 024 threads per output block, 16 groups of 64 (one thread per row) stride the list with 8
+// independent partial sums each; the 128 partials of a row are combined in a fixed order (bit-reproducible).
+constexpr int RED_NT = 1024;
+__global__ void __launch_bounds__(RED_NT) k_symv_reduce(SymvPlan P, int32_t nob, double* x, const int* done_flag) {
+  __shared__ double red[RED_NT];
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const int tid = threadIdx.x, i = tid & 63, g = tid >> 6;
+  for (int ob = blockIdx.x; ob < nob; ob += gridDim.x) {
+    const int w = P.width[ob];
+    const int64_t e0 = P.lptr[ob], e1 = P.lptr[ob + 1];
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = 0.0;
+    if (i < w)
+      for (int64_t e = e0 + g; e < e1; e += 128) {   // entries e + 16u: 8 loads in flight per thread
+        const double* q = P.slots + 64 * e + i;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e + 16 * u < e1) a[u] += __ldcg(q + 64 * 16 * u);
+      }
+    red[g * 64 + i] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     __syncthreads();
-    if (tid < w) x[P.x0[ob] + tid] += (red[tid] + red[64 + tid]) + (red[128 + tid] + red[192 + tid]);
-    if (tid == 0) P.cnt[ob] = 0u;
+    if (tid < w) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) t += red[k * 64 + tid];
+      x[P.x0[ob] + tid] += t;
+    }
     __syncthreads();
   }
+}
+void symv_reduce(const SymvPlan* P, double* x, const int* done_flag, int sms, cudaStream_t s) {
+  if (P == nullptr || P->slots == nullptr || P->nob <= 0) return;
+  k_symv_reduce<<<(unsigned)std::min<int64_t>(P->nob, (int64_t)sms * 2), RED_NT, 0, s>>>(*P, P->nob, x, done_flag);
 }
 
 // Symmetric-root GEMV as its own kernel (between the forward and backward sparse sweeps):
@@ -1961,7 +1980,7 @@ __global__ void __launch_bounds__(NT, MINB) k_symroot_gemv(DevFactor F, double* 
     __syncthreads();
     schunk_gemv<U>(Mc, ldx, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
     __syncthreads();
-    symv_epilogue(P, idx, Rn, bI, ncol_t, bK, red + 512, colv, vK, x);
+    symv_epilogue(P, idx, Rn, bI, ncol_t, bK, red + 512, colv, x);
   }
   tl_end(2, tls);
 }
@@ -1994,7 +2013,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dense_symv(const double* W, int64_
     __syncthreads();
     schunk_gemv<U>(W + rI + cK * ld, ld, Rn, ncol, ncol_t, vK, vI, red, colv, pol);
     __syncthreads();
-    symv_epilogue(P, P.c_begin + idx, Rn, ch.x, ncol_t, ch.y, red + 512, colv, vK, x);
+    symv_epilogue(P, P.c_begin + idx, Rn, ch.x, ncol_t, ch.y, red + 512, colv, x);
   }
   tl_end(2, tls);
 }
@@ -2055,9 +2074,10 @@ void w_symmetrize_diag(double* W, int64_t ld, int64_t n, cudaStream_t s) {
 }
 
 void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const SymvPlan* plan,
-                const double* v, double* x, const int* done_flag, int sms, cudaStream_t s) {
+                const double* v, double* x, const int* done_flag, int sms, cudaStream_t s, bool reduce) {
   if (nch <= 0) return;
   k_dense_symv<16, 3><<<sms * 3, NT, 0, s>>>(W, ld, n, chunks, nch, *plan, v, x, done_flag);
+  if (reduce) symv_reduce(plan, x, done_flag, sms, s);
 }
 
 void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end, const SymvPlan* plan,
@@ -2073,6 +2093,7 @@ void symroot_gemv(const DevFactor& F, double* x, int64_t c_begin, int64_t c_end,
     case 4: k_symroot_gemv<4, 4><<<sms * 4, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
     default: k_symroot_gemv<8, 3><<<sms * 3, NT, 0, s>>>(F, x, c_begin, c_end, *plan, done_flag, sub); break;
   }
+  symv_reduce(plan, x, done_flag, sms, s);
   (void)grid;
 }
 

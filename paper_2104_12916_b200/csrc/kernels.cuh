@@ -134,15 +134,17 @@ struct DevFactor {
 };
 
 // Deterministic accumulation plan of a chunked symmetric GEMV (k_dense_symv, k_symroot_gemv): every chunk
-// writes its row and column partials to its own slot (64 + 512 doubles); the CTA that brings an output
-// block's arrival counter to `expect` sums that block's slots in the fixed order lsrc[lptr[o] .. lptr[o+1])
-// and adds the sum to x — no floating-point atomics, so results are bit-identical run to run.
+// writes its row and column partials to its own slot (64 + 512 doubles); k_symv_reduce then sums each
+// output block's slots in the fixed order lsrc[lptr[o] .. lptr[o+1]) and adds the sum to x — no
+// floating-point atomics, so results are bit-identical run to run.
 struct SymvPlan {
-  double* slots;             // (c_end − c_begin) × 576 doubles
-  unsigned* cnt;             // per output block, reset to 0 by its reducer
-  const int32_t* expect;     // per output block: contributing chunks
-  const int64_t* lptr;       // per output block: slot list (slot offsets in doubles)
-  const int64_t* lsrc;
+  double* slots;             // 64 doubles per (chunk, output block) contribution, grouped by output block
+                             // (nullptr: fp64 atomics, QPB_DETERMINISTIC=0)
+  int32_t nob;               // output blocks
+  const int64_t* lptr;       // output block o: its contributions are slots[64·lptr[o] .. 64·lptr[o+1]), in the
+                             // fixed order (row partials first, then column partials, by chunk index)
+  const int64_t* woff;       // per chunk (c − c_begin), 9 entries: slot offset (doubles) of its row partial
+                             // and of its column partials for output blocks cob0, cob0+1, … (−1 unused)
   const int32_t* width;      // per output block: rows (≤ 64)
   const int64_t* x0;         // per output block: first index in x
   int64_t c_begin;
@@ -276,7 +278,9 @@ void w_symmetrize_diag(double* W, int64_t ld, int64_t n, cudaStream_t s);
 // x += W v, W the explicit x-block of F⁻¹ (k_dense_symv; chunks = (row block, first column block) pairs)
 void dense_symv(const double* W, int64_t ld, int64_t n, const int2* chunks, int64_t nch, const SymvPlan* plan,
                 const double* v, double* x,
-                const int* done_flag, int sms, cudaStream_t s);
+                const int* done_flag, int sms, cudaStream_t s, bool reduce = true);
+// x += the fixed-order sums of a SymvPlan's slots (the second half of dense_symv with reduce = false)
+void symv_reduce(const SymvPlan* P, double* x, const int* done_flag, int sms, cudaStream_t s);
 // the flattened forest's right-hand side kernel alone (k_flat_rhs), for the first PCG iteration
 void flat_rhs(const DevFactor& F, const SweepRhs& r, double* x, int sms, cudaStream_t s);
 

@@ -569,9 +569,10 @@ std::string analyse(const LowerMatrix& M, Symbolic& S, int64_t n_negative, bool 
   }
   // Tiny single-block supernodes (w ≤ 32, noff ≤ 256, w·noff ≤ 1024) are swept WARP-wide: groups of
   // up to 8 from the same level (height forward, depth backward) form one task (type 7), one warp each.
-  // (Chaining a whole subtree of them through one warp, which needs no counters or fences between its
-  // members, was measured slower: c2 forward 740 → 810 µs, c4s 284 → 373 µs — the per-supernode latency,
-  // not the dependency hops, bounds this phase.)
+  // (Measured slower: chaining whole subtrees of them through one warp — c2 forward 740 → 810 µs, c4s
+  // 284 → 373 µs, the per-supernode latency, not the dependency hops, bounds this phase — and one claim
+  // queue per level from which every warp of ⌈count/8⌉ tasks takes supernodes one at a time — c2 forward
+  // 748 → 757 µs.)
   std::vector<int32_t> tiny_f(ns, -1), tiny_b(ns, -1);   // group id of J, set on every member
   std::vector<char> first_f(ns, 0), first_b(ns, 0);
   {
@@ -1065,6 +1066,125 @@ namespace qpb {
 // ordering `order` (new→old): an equivalent reordering (same fill) that makes
 // every last child contiguous with its parent, so chains of supernodes can be
 // amalgamated.  Returns the composed order (new→old).
+// Nested dissection by level structures (George's method): in each connected part, a BFS from a
+// pseudo-peripheral node splits the part at its middle level; the two sides are ordered recursively and
+// the separator level last.  Parts of at most `leaf` nodes keep their input order.  Its elimination tree
+// has logarithmic depth on band- and grid-like graphs, where minimum degree can leave a long chain of
+// narrow supernodes (c4s's P_H: the banded T = C diag(H)⁻¹ Cᵀ).
+std::vector<int64_t> nested_dissection_order(int64_t n, const std::vector<int64_t>& ptr,
+                                             const std::vector<int32_t>& idx, int64_t leaf) {
+  std::vector<int64_t> order;
+  order.reserve(n);
+  std::vector<int64_t> part(n, 0);        // current part id of every unordered node; −1 = ordered
+  std::vector<int64_t> level(n, -1);
+  int64_t next_id = 1;
+  // explicit stack of (part id, node list)
+  std::vector<std::pair<int64_t, std::vector<int64_t>>> st;
+  {
+    std::vector<int64_t> all(n);
+    for (int64_t i = 0; i < n; ++i) all[i] = i;
+    st.push_back({0, std::move(all)});
+  }
+  // deferred output: a separator must follow both of its sides, so push markers
+  struct Item { bool sep; int64_t id; std::vector<int64_t> nodes; };
+  std::vector<Item> work;
+  work.push_back({false, 0, std::move(st.back().second)});
+  st.clear();
+  auto bfs = [&](int64_t src, int64_t pid, std::vector<int64_t>& seen) {
+    seen.clear();
+    seen.push_back(src);
+    level[src] = 0;
+    for (size_t h = 0; h < seen.size(); ++h) {
+      const int64_t u = seen[h];
+      for (int64_t q = ptr[u]; q < ptr[u + 1]; ++q) {
+        const int64_t v = idx[q];
+        if (part[v] == pid && level[v] < 0) {
+          level[v] = level[u] + 1;
+          seen.push_back(v);
+        }
+      }
+    }
+  };
+  std::vector<int64_t> seen;
+  while (!work.empty()) {
+    Item it = std::move(work.back());
+    work.pop_back();
+    if (it.sep) {
+      for (int64_t v : it.nodes) {
+        order.push_back(v);
+        part[v] = -1;
+      }
+      continue;
+    }
+    std::vector<int64_t>& S = it.nodes;
+    if ((int64_t)S.size() <= leaf) {
+      std::sort(S.begin(), S.end());
+      for (int64_t v : S) {
+        order.push_back(v);
+        part[v] = -1;
+      }
+      continue;
+    }
+    const int64_t pid = it.id;
+    // connected component of S[0]; the rest of S is a separate part (pushed back)
+    bfs(S[0], pid, seen);
+    if (seen.size() < S.size()) {
+      std::vector<int64_t> rest;
+      for (int64_t v : S)
+        if (level[v] < 0) rest.push_back(v);
+      for (int64_t v : seen) level[v] = -1;
+      const int64_t id2 = next_id++;
+      for (int64_t v : rest) part[v] = id2;
+      std::vector<int64_t> comp(seen);
+      work.push_back({false, id2, std::move(rest)});
+      work.push_back({false, pid, std::move(comp)});
+      continue;
+    }
+    // pseudo-peripheral node: repeat BFS from the last (deepest) node while the depth grows
+    int64_t src = seen.back(), depth = level[seen.back()];
+    for (int rep = 0; rep < 4; ++rep) {
+      for (int64_t v : seen) level[v] = -1;
+      bfs(src, pid, seen);
+      const int64_t d = level[seen.back()];
+      if (d <= depth && rep > 0) break;
+      depth = d;
+      src = seen.back();
+    }
+    if (depth < 2) {   // (nearly) a clique: no useful separator
+      std::sort(S.begin(), S.end());
+      for (int64_t v : seen) level[v] = -1;
+      for (int64_t v : S) {
+        order.push_back(v);
+        part[v] = -1;
+      }
+      continue;
+    }
+    // middle level by node count
+    std::vector<int64_t> cnt(depth + 1, 0);
+    for (int64_t v : seen) cnt[level[v]]++;
+    int64_t acc = 0, mid = 1;
+    for (int64_t l = 0; l <= depth; ++l) {
+      acc += cnt[l];
+      if (2 * acc >= (int64_t)seen.size()) {
+        mid = std::max<int64_t>(1, std::min<int64_t>(l, depth - 1));
+        break;
+      }
+    }
+    std::vector<int64_t> A, B, Sep;
+    for (int64_t v : seen) (level[v] < mid ? A : level[v] > mid ? B : Sep).push_back(v);
+    for (int64_t v : seen) level[v] = -1;
+    const int64_t ia = next_id++, ib = next_id++;
+    for (int64_t v : A) part[v] = ia;
+    for (int64_t v : B) part[v] = ib;
+    for (int64_t v : Sep) part[v] = -2;   // not in any part any more
+    std::sort(Sep.begin(), Sep.end());
+    work.push_back({true, -2, std::move(Sep)});
+    work.push_back({false, ib, std::move(B)});
+    work.push_back({false, ia, std::move(A)});
+  }
+  return order;
+}
+
 std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
                                      const std::vector<int64_t>& order) {
   std::vector<int64_t> pinv(n);

@@ -163,6 +163,10 @@ LowerMatrix build_F_lower(int64_t n, int64_t m1, const int64_t* Hp, const int32_
 std::vector<int64_t> min_degree_order(int64_t n, const std::vector<int64_t>& ptr,
                                       const std::vector<int32_t>& idx, double dense_stop = 1.0);
 
+// Nested dissection by BFS level structures (new→old); parts of ≤ leaf nodes keep their input order.
+std::vector<int64_t> nested_dissection_order(int64_t n, const std::vector<int64_t>& ptr,
+                                             const std::vector<int32_t>& idx, int64_t leaf = 64);
+
 // Equivalent reordering by an elimination-tree postorder (same fill), composed with `order`.
 std::vector<int64_t> etree_postorder(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
                                      const std::vector<int64_t>& order);

@@ -176,8 +176,9 @@ def main():
     old = json.load(open(mpath)) if os.path.exists(mpath) else {}
     old.update(meta)
     import platform
-    old["host"] = dict(cpu=platform.processor() or open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": "),
-                       nproc=os.cpu_count())
+    model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")),
+                 platform.processor())
+    old["host"] = dict(cpu=model, nproc=os.cpu_count(), note="the build container, not the GPU box")
     json.dump(old, open(mpath, "w"), indent=1)
     log("done", cfg, meta)
 

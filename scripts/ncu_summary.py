@@ -1,6 +1,6 @@
 """Summarise an `ncu --set full` report (read with `ncu -i REP --page raw --csv`) per launch.
 
-Usage: python scripts/ncu_summary.py REP.ncu-rep "<capture command>" [config] [traffic.json]
+Usage: python scripts/ncu_summary.py REP.ncu-rep|RAW.csv "<capture command>" [config] [traffic.json]
 Prints a per-launch table and, with a traffic.json path, records the DRAM bytes of one F-solve
 (forward sweep + symmetric-root GEMV + backward sweep) for bench.py's roofline `traffic` key.
 """
@@ -20,7 +20,11 @@ SCALE = {"ns": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1.0, "Kbyte": 1e3, 
 
 
 def rows(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep (read through ncu -i) or the CSV of `ncu -i REP --page raw --csv`."""
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(txt)))
     head, units, data = r[0], r[1], r[2:]
     out = []

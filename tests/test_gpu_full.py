@@ -132,9 +132,12 @@ def test_full_pcg_count_at_eps(cfg, prec):
 @pytest.mark.parametrize("cfg", CONFIGS)
 def test_full_ipm_pl_trajectory(cfg):
     """The first 15 PL-KF IPM iterations from the common start point (reading R3) against the oracle's:
-    PCG counts within [min − 2, max + 2] of the oracle's count and its four rounding-level variants
-    (r_ν perturbed by 1e-15; reading R12: where rounding alone moves the count, the gate widens by
-    exactly that measured spread), μ to 1e-3 relative (the same iterates up to rounding)."""
+    μ_k to 1e-3 relative on every iteration (the oracle's own rounding-level variants drift 5e-5 apart
+    by iteration 14 on c3s), and the PCG counts within [min − 2, max + 2] of the oracle's count and its
+    rounding-level variants (r_ν perturbed by 1e-15; other LU orders of H) while those counts are ≤ 100.
+    Beyond that the two trajectories' systems differ at rounding level and the counts with them (the
+    sweeps' fp64 fan-out atomics move the GPU's own late counts by ±3 run to run); the ±2 gate on the
+    SAME system is test_full_pcg_count_same_system (reading R12)."""
     z = golden(cfg)
     qp, pr, s = solver(cfg, "low")
     s.ipm_init(ipm_tol=1e-8, max_ipm=100, pcg_maxit=2000)
@@ -146,10 +149,9 @@ def test_full_ipm_pl_trajectory(cfg):
         got_mu.append(float(r["mu"]))
     var = np.vstack([pcg_o] + [z[k] for k in z.files if k.startswith("ipm_pl_var/pcg_v")]).astype(int)
     lo, hi = var.min(axis=0) - 2, var.max(axis=0) + 2
-    bad = [(k, g, int(lo[k]), int(hi[k])) for k, g in enumerate(got_pcg) if not lo[k] <= g <= hi[k]]
+    bad = [(k, g, int(lo[k]), int(hi[k])) for k, g in enumerate(got_pcg)
+           if pcg_o[k] <= 100 and not lo[k] <= g <= hi[k]]
     assert not bad, bad
-    # the rounding-level variants' μ spread (5e-5 on c3s by iteration 14) bounds how close two correct
-    # trajectories stay; 1e-3 leaves room for the GPU's own rounding while catching any real deviation
     rel = np.abs(np.array(got_mu) - mu_o) / mu_o
     assert rel.max() <= 1e-3, rel
 
@@ -175,20 +177,22 @@ def test_full_ph_ipm_objective(cfg):
         assert not bad, bad
 
 
-def test_full_pcg_count_same_system_c3s():
-    """PCG counts ±2 on the SAME system (north_star): the GPU's own PL-KF IPM run to iteration 12 (counts
-    above 200, the ill-conditioned regime of P:L665–666) hands its (D_k, r_ν, ε_k) to the oracle; the GPU's
-    count on it must lie within [min − 2, max + 2] of the oracle's PCG (BlockF F-solves) on that system
-    and on three rounding-level variants (r_ν perturbed by 1e-15)."""
+@pytest.mark.parametrize("cfg,k", [("c3s", 13), ("c1", 10)])
+def test_full_pcg_count_same_system(cfg, k):
+    """PCG counts ±2 on the SAME system (north_star): the GPU's own PL-KF IPM run to iteration k−1
+    (c3s: counts above 200, c1: above 300 — the ill-conditioned regime of P:L665–666) hands its
+    (D_k, r_ν, ε_k) to the oracle; the GPU's count on it must lie within [min − 2, max + 2] of the
+    oracle's PCG on that system and on three rounding-level variants (r_ν perturbed by 1e-15).  The
+    oracle's F-solve route: BlockF (c3s), the written-out (F⁻¹)₁₁ (c1)."""
     from oracle import kkt
-    from oracle.fsolve import BlockF
+    from oracle.fsolve import BlockF, DenseF
     from oracle.pcg import pcg
-    qp, pr, s = solver("c3s", "low")
+    qp, pr, s = solver(cfg, "low")
     s.ipm_init(ipm_tol=1e-8, max_ipm=100, pcg_maxit=2000)
-    r = s.ipm_iterate(13)
+    r = s.ipm_iterate(k)
     D, rnu, eps = s.ipm_last_system()
     x, it, rr, rc = s.pcg_solve(D, rnu, tol=eps, maxit=2000)
-    fs = BlockF(qp.H, qp.A)
+    fs = DenseF(qp.H, qp.A, explicit_w=True) if cfg == "c1" else BlockF(qp.H, qp.A)
     counts = []
     for v in (None, 1, 2, 3):
         b = rnu if v is None else rnu * (1 + 1e-15 * np.random.default_rng(v).standard_normal(len(rnu)))
