@@ -198,6 +198,14 @@ int64_t qp_launch_count(const qp_ctx* ctx);
  *              rhs/out of length n + m1 (a2–a4 of SURVEY §8(a)).
  * qp_kf_apply: q = K_F(D) p (a1–a5). */
 int qp_f_solve(qp_ctx* ctx, const double* rhs, double* out);
+
+/* q = G p = H p + Cᵀ(D⁻¹∘(C p)): the x-space operator of the augmented system K_C (the
+ * north_star's "H·p + Cᵀ(D·(C·p))" with D = V⁻¹S, so its D·(C·p) is D⁻¹∘(C p) here), applied without
+ * any factorization — callable right after qp_setup, at sizes whose F cannot be factored (full C3/C4).
+ * Two streaming kernels over C, then H and Cᵀ, in natural order.  D: m2 (this rank's rows, > 0),
+ * p: n, q: n (replicated; sharded mode all-reduces the ranks' partial products).  Host or device
+ * pointers per vectors_on_device.  Errors: QP_ESTATE before qp_setup, QP_ENOMEM. */
+int qp_operator_apply(qp_ctx* ctx, const double* D, const double* p, double* q);
 int qp_kf_apply(qp_ctx* ctx, const double* D, const double* p, double* q);
 
 /* Host-only symbolic analysis (no GPU needed): ordering of the x block

@@ -106,6 +106,7 @@ def load_library(build: bool = True):
     lib.qp_ipm_iterate.argtypes = [vp, i32, C.POINTER(_IpmResult), C.POINTER(i32)]
     lib.qp_f_solve.argtypes = [vp, vp, vp]
     lib.qp_kf_apply.argtypes = [vp, vp, vp, vp]
+    lib.qp_operator_apply.argtypes = [vp, vp, vp, vp]
     lib.qp_analyse.argtypes = [C.POINTER(vp), C.POINTER(_CSR), C.POINTER(_CSR), vp]
     lib.qp_partition_rows.argtypes = [vp, i64, i32, vp]
     lib.qp_get_partition.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
@@ -326,6 +327,18 @@ class QPSolver:
         out = np.zeros(N)
         self._check(self.lib.qp_f_solve(self.ctx, p, out.ctypes.data))
         return out[:self.n], out[self.n:]
+
+    def operator_apply(self, D, p, out=None):
+        """q = H p + Cᵀ(D⁻¹∘(C p)) (qp_operator_apply; no factorization needed)."""
+        pD, kD = self._ptr(D, self.m2)
+        pp, kp = self._ptr(p, self.n)
+        if self.vectors_on_device:
+            assert out is not None
+            self._check(self.lib.qp_operator_apply(self.ctx, pD, pp, out.data_ptr()))
+            return out
+        q = np.zeros(self.n)
+        self._check(self.lib.qp_operator_apply(self.ctx, pD, pp, q.ctypes.data))
+        return q
 
     def kf_apply(self, D, p):
         pD, kD = self._ptr(D, self.m2)

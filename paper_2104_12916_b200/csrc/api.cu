@@ -337,6 +337,9 @@ struct qp_ctx {
   SymvPlan df_plan{};
   double* df_rhs = nullptr;          // materialised right-hand side (N)
   double df_discrepancy = -1;        // factor-time guard of the dense F⁻¹ (−1: not built)
+  bool op_ready = false;             // qp_operator_apply: natural-order device copies of H, C, Cᵀ
+  DevCSR opH{}, opC{}, opCt{};
+  double *op_D = nullptr, *op_p = nullptr, *op_t = nullptr, *op_q = nullptr;
   double* phinv = nullptr;           // small m2: P_H⁻¹ (m2 × m2, ld pi_ld), rebuilt after every P_H refactor
   bool phinv_ready = false;
   int64_t pi_ld = 0, pi_nch = 0;
@@ -2348,6 +2351,36 @@ int qp_kf_apply(qp_ctx* c, const double* D, const double* p, double* q) {
   rc = sync_check(c, "qp_kf_apply");
   c->harvest();
   return rc;
+}
+
+int qp_operator_apply(qp_ctx* c, const double* D, const double* p, double* q) {
+  if (!c) return QP_EINVAL;
+  if (!c->setup_done) return fail(c, QP_ESTATE, "qp_setup has not completed");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  if (!c->op_ready) {
+    try {
+      c->opH = upload_csr(c->mem, c->H, st);
+      c->opC = upload_csr(c->mem, c->C, st);
+      c->opCt = upload_csr(c->mem, transpose(c->C), st);
+      c->op_D = c->mem.zeros<double>(std::max<int64_t>(1, c->m2), st);
+      c->op_t = c->mem.zeros<double>(std::max<int64_t>(1, c->m2), st);
+      c->op_p = c->mem.zeros<double>(c->n, st);
+      c->op_q = c->mem.zeros<double>(c->n, st);
+    } catch (std::bad_alloc&) {
+      return fail(c, QP_ENOMEM, "cudaMalloc failed (operator copies)");
+    }
+    c->op_ready = true;
+  }
+  const double* Dd = in_vec(c, D, c->op_D, c->m2);
+  const double* pd = in_vec(c, p, c->op_p, c->n);
+  double* qd = c->vectors_on_device ? q : c->op_q;
+  op_apply(c->opH, c->opC, c->opCt, Dd, pd, c->op_t, qd, !c->sharded || c->rank == 0, c->sm_count, st);
+  c->launches += 2;
+  if (c->sharded)
+    if (int rc = c->allreduce(qd, c->n, 0)) return rc;   // Σ_ranks of the rows' partial products
+  if (!c->vectors_on_device) out_vec(c, q, c->op_q, c->n);
+  return sync_check(c, "qp_operator_apply");
 }
 
 int qp_get_structure(qp_ctx* c, int32_t which, int64_t* out, int64_t* len) {

@@ -2902,6 +2902,44 @@ void scatter(double* out, const double* in, const int64_t* idx, int64_t n, const
 }
 
 
+// ------------------------------------------------------------------------- the x-space operator alone
+// G p = H p + Cᵀ(D⁻¹ ∘ (C p)) (the north_star's "H·p + Cᵀ(D·(C·p))" with D = V⁻¹S) at any
+// size, without a factorization: two streaming passes — t = D⁻¹∘(C p) over the rows of C, then
+// q = H p + Cᵀ t over the rows of H and Cᵀ — each a quad of lanes per row (4 consecutive entries per
+// load round: full 32-byte sectors on the short rows of these matrices).  Sharded rows: every rank
+// applies its rows of C (and H once, on rank 0); the caller all-reduces q.
+__global__ void __launch_bounds__(NT) k_op_t(DevCSR Cf, const double* D, const double* p, double* t) {
+  const int q4 = threadIdx.x & 3;
+  const int64_t nq = ((int64_t)gridDim.x * NT) >> 2;
+  for (int64_t k = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 2; k < Cf.nrows; k += nq) {
+    double s = 0.0;
+    for (int64_t e = __ldg(Cf.p + k) + q4; e < __ldg(Cf.p + k + 1); e += 4) s += __ldg(Cf.v + e) * __ldg(p + __ldg(Cf.i + e));
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (q4 == 0) t[k] = s / D[k];
+  }
+}
+__global__ void __launch_bounds__(NT) k_op_q(DevCSR Hf, DevCSR Ctf, const double* p, const double* t, double* q,
+                                             int with_h) {
+  const int q4 = threadIdx.x & 3;
+  const int64_t nq = ((int64_t)gridDim.x * NT) >> 2;
+  for (int64_t i = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 2; i < Ctf.nrows; i += nq) {
+    double s = 0.0;
+    if (with_h)
+      for (int64_t e = __ldg(Hf.p + i) + q4; e < __ldg(Hf.p + i + 1); e += 4) s += __ldg(Hf.v + e) * __ldg(p + __ldg(Hf.i + e));
+    for (int64_t e = __ldg(Ctf.p + i) + q4; e < __ldg(Ctf.p + i + 1); e += 4) s += __ldg(Ctf.v + e) * __ldg(t + __ldg(Ctf.i + e));
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (q4 == 0) q[i] = s;
+  }
+}
+void op_apply(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* D, const double* p, double* t,
+              double* q, bool with_h, int sms, cudaStream_t s) {
+  const int g = sms * 8;
+  k_op_t<<<g, NT, 0, s>>>(Cf, D, p, t);
+  k_op_q<<<g, NT, 0, s>>>(Hf, Ctf, p, t, q, with_h ? 1 : 0);
+}
+
 // ------------------------------------------------------------------------- x-space twin (K_C, PPCG)
 // q = G p = H p + Cᵀ(W∘(C p)) in ONE kernel (the north_star's fused SpMV chain): warp per x-row i,
 // lanes over H's row, then over Cᵀ's row where each lane forms its (C p)_k on the fly (C rows are

@@ -227,6 +227,9 @@ struct SweepRhs {
   int rhs_ready;            // flattened forest: acc / vbuf / x already prepared (fused PCG step, phase D)
 };
 void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s);
+// q = H p (with_h) + Cᵀ(D⁻¹∘(C p)) in two streaming passes (t: m2 scratch), natural order, no factor
+void op_apply(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* D, const double* p, double* t,
+              double* q, bool with_h, int sms, cudaStream_t s);
 // v[0, N) = the right-hand side described by r, out[0, N) = 0 (dense F⁻¹ mode)
 void gather_rhs(const SweepRhs& r, double* v, double* out, int64_t N, int sms, cudaStream_t s);
 // v[0, n) = 0 unless *done_flag

@@ -133,9 +133,10 @@ def main():
         # rounding-level variants of the same trajectory (r_ν perturbed by 1e-15 relative): the spread of
         # their PCG counts is what rounding alone does to the counts (DESIGN reading R12)
         pay = {}
+        vmax = int(os.environ.get("GOLD_VAR_MAXIPM", "15"))   # the count gate covers counts ≤ 100 only
         for v in VARIANTS:
             t = time.time()
-            r = ipm_solve(qp, precond="low", max_ipm=15, fs=fs, rnu_perturb=v)
+            r = ipm_solve(qp, precond="low", max_ipm=vmax, fs=fs, rnu_perturb=v)
             meta[f"t_ipm_pl_var{v}_s"] = time.time() - t
             pay[f"pcg_v{v}"] = [d["pcg"] for d in r.trace]
             pay[f"mu_v{v}"] = [d["mu"] for d in r.trace]

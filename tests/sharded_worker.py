@@ -57,6 +57,9 @@ def main():
         res[f"it{k}"] = it
     x, it, rr, rc = s.pcg_solve(D[lo:hi], b[lo:hi], tol=1e-12, maxit=2000)
     res.update(x_tight=x.tolist(), it_tight=it, rr_tight=rr)
+    # the x-space operator with sharded rows: every rank's q is the all-reduced H p + Cᵀ(D⁻¹∘(C p))
+    pg = np.random.default_rng(12).standard_normal(qp.n)
+    res["Gp"] = s.operator_apply(D[lo:hi], pg).tolist()
     if case == "c0":
         r = s.ipm_solve(ipm_tol=1e-10)
         res.update(objective=r["objective"], converged=bool(r["converged"]), n_ipm=r["n_ipm"],

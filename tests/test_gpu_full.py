@@ -147,8 +147,9 @@ def test_full_ipm_pl_trajectory(cfg):
         r = s.ipm_iterate(1)                 # μ reported = the one this iteration started from
         got_pcg.append(int(r["pcg_iters"][-1]))
         got_mu.append(float(r["mu"]))
-    var = np.vstack([pcg_o] + [z[k] for k in z.files if k.startswith("ipm_pl_var/pcg_v")]).astype(int)
-    lo, hi = var.min(axis=0) - 2, var.max(axis=0) + 2
+    vs = [np.asarray(z[k]).astype(int) for k in z.files if k.startswith("ipm_pl_var/pcg_v")]
+    lo = np.array([min([int(pcg_o[k])] + [int(v[k]) for v in vs if len(v) > k]) - 2 for k in range(len(pcg_o))])
+    hi = np.array([max([int(pcg_o[k])] + [int(v[k]) for v in vs if len(v) > k]) + 2 for k in range(len(pcg_o))])
     bad = [(k, g, int(lo[k]), int(hi[k])) for k, g in enumerate(got_pcg)
            if pcg_o[k] <= 100 and not lo[k] <= g <= hi[k]]
     assert not bad, bad

@@ -70,6 +70,11 @@ def test_two_process_sharded_matches_oracle(case, tmp_path):
     got = np.concatenate([r["x_tight"] for r in res])
     assert np.linalg.norm(got - ref) <= 1e-8 * np.linalg.norm(ref)
     assert res[0]["it_tight"] == res[1]["it_tight"] and abs(res[0]["it_tight"] - itr) <= 2
+    from oracle.xspace import G_apply
+    gref = G_apply(qp, 1.0 / D, np.random.default_rng(12).standard_normal(qp.n))
+    for r in res:   # qp_operator_apply, rows sharded, partial products all-reduced
+        assert np.linalg.norm(np.array(r["Gp"]) - gref) <= 1e-13 * np.linalg.norm(gref)
+    assert res[0]["Gp"] == res[1]["Gp"]
     if case != "c0":   # PL-KF IPM at 1e-10 is checked on c0 (ragged: PL-KF stalls late)
         return
     # one IPM over both processes: every decision comes from all-reduced scalars, so both ranks take the
