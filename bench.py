@@ -408,7 +408,7 @@ def run_ours(args, rank, world, local, use_dist):
     # ---------------------------------------------------------------- device launch timeline (third pass, the
     # production path with CUDA graphs): per kernel the earliest block start and latest block end by
     # %globaltimer, so launch durations and the idle gaps between dependent launches are both visible
-    TLN = ["flat_rhs", "flat_fwd", "root_gemv", "flat_bwd", "pcg_step", "trsv_fwd", "trsv_bwd", "spmv"]
+    TLN = ["flat_rhs", "flat_fwd", "root_gemv", "flat_bwd", "pcg_step", "trsv_fwd", "trsv_bwd", "spmv", "lvl_fwd", "lvl_bwd"]
     s.ipm_init(space=args.space)
     s.ipm_iterate(W)
     torch.cuda.synchronize(dev)

@@ -248,6 +248,9 @@ typedef struct {
                                         rank's share of W's chunks in sharded mode (0 when not in use) */
   double dense_finv_enabled;         /* 1 if F-solves use the explicit F⁻¹ (small N, DESIGN §5 "dense F⁻¹") */
   double dense_finv_discrepancy;     /* its factor-time guard against the sweeps (−1: not built) */
+  double lvl_levels_F, lvl_levels_PH;  /* leaf phase: bottom levels of L_F / L_PH swept level-synchronously
+                                          (one launch per level, DESIGN §5 "leaf phase"); 0 = none */
+  double lvl_supernodes_F, lvl_supernodes_PH;  /* supernodes in those levels */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 
@@ -275,11 +278,12 @@ int qp_debug_sweep_profile(qp_ctx* ctx, int32_t enable, int64_t* out);
 int64_t qp_debug_sweep_trace(qp_ctx* ctx, int32_t sweep, int64_t* out, int64_t cap);
 
 /* Debug: launch timeline of the instrumented kernels (0 flat rhs, 1 flat forward, 2 root GEMV,
- * 3 flat backward, 4 fused PCG step, 5 forward sweep, 6 backward sweep, 7 SpMV).  enable = 1
+ * 3 flat backward, 4 fused PCG step, 5 forward sweep, 6 backward sweep, 7 SpMV, 8 / 9 leaf-phase
+ * level kernels forward / backward).  enable = 1
  * resets the device buffer and turns recording on (kernels read the switch at run time, so
  * captured CUDA graphs are recorded too); enable = 0 turns it off and copies
- * min(cap, W) uint64 words to out (host, caller-owned), W = 2*8 + 2*8*256:
- * [8 launch counters][8 scratch][8][256] earliest block start, [8][256] latest block end
+ * min(cap, W) uint64 words to out (host, caller-owned), W = 2*10 + 2*10*256:
+ * [10 launch counters][10 scratch][10][256] earliest block start, [10][256] latest block end
  * (globaltimer ns; slot = launch number, the first 256 launches per kernel after enable).
  * Returns W or a negative qp_status. */
 int64_t qp_debug_timeline(qp_ctx* ctx, int32_t enable, int64_t* out, int64_t cap);

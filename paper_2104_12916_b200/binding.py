@@ -73,7 +73,8 @@ class _Stats(C.Structure):
                                           "sweep_bytes_F", "fsolve_bytes_F", "sym_discrepancy", "sym_enabled",
                                           "flat_discrepancy", "flat_enabled", "flat_nnz_M", "dense_w_enabled",
                                           "dense_w_discrepancy", "kf_bytes_W", "dense_finv_enabled",
-                                          "dense_finv_discrepancy")]
+                                          "dense_finv_discrepancy", "lvl_levels_F", "lvl_levels_PH",
+                                          "lvl_supernodes_F", "lvl_supernodes_PH")]
 
 
 _LIB = None
@@ -369,9 +370,9 @@ class QPSolver:
 
     def debug_timeline(self, enable):
         """enable=True: start recording; enable=False: stop and return a list of (kernel, start_ns, end_ns)
-        per recorded launch (the first 256 per kernel), sorted by start (kernels: 0 flat rhs … 7 SpMV,
+        per recorded launch (the first 256 per kernel), sorted by start (kernels: 0 flat rhs … 7 SpMV, 8/9 leaf-phase levels fwd/bwd,
         include/qp_b200.h)."""
-        K, R = 8, 256
+        K, R = 10, 256
         W = 2 * K + 2 * K * R
         if enable:
             rc = int(self.lib.qp_debug_timeline(self.ctx, 1, None, 0))

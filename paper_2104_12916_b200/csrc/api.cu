@@ -577,6 +577,22 @@ std::string upload_factor(qp_ctx* c, Factor& F, int64_t ws_limit) {
     d.mf_group = S.mf_group;
     d.snw_fwd = m.upload(S.snw_fwd, st);
     d.snw_bwd = m.upload(S.snw_bwd, st);
+    {
+      std::vector<int32_t> desc;
+      desc.reserve(S.lvl_blk.size() * 8);
+      for (int32_t b : S.lvl_blk) {
+        const int64_t lo = S.blk_off[b], io = S.blk_inv[b], ro = S.blk_rows[b];
+        desc.insert(desc.end(), {(int32_t)(uint32_t)(lo & 0xffffffffll), (int32_t)(lo >> 32),
+                                 (int32_t)(uint32_t)(io & 0xffffffffll), (int32_t)(io >> 32),
+                                 (int32_t)(uint32_t)(ro & 0xffffffffll), (int32_t)(ro >> 32), S.blk_col0[b],
+                                 (int32_t)(S.blk_w[b] | (S.blk_noff[b] << 6))});
+      }
+      d.lvl_desc = reinterpret_cast<const int4*>(m.upload(desc, st));
+    }
+    d.lvl_cut = S.lvl_cut;
+    d.lvl_cut = (int32_t)std::min<size_t>(S.lvl_g.size(), (size_t)std::min<int32_t>(S.lvl_cut, LVL_MAX));
+    for (int L = 0; L <= d.lvl_cut; ++L) d.lvl_ptr_h[L] = L < (int)S.lvl_ptr.size() ? S.lvl_ptr[L] : 0;
+    for (int L = 0; L < d.lvl_cut; ++L) d.lvl_g_h[L] = (int8_t)S.lvl_g[L];
     d.flat = 0;
     if (S.flat) {
       d.fl_rc0 = S.fl_rc0;
@@ -856,7 +872,7 @@ void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
     c->end(h);
     return;
   }
-  c->launches += F.d.flat ? (r.rhs_ready ? 4 : 5) : 2;
+  c->launches += F.d.flat ? (r.rhs_ready ? 4 : 5) : 2 + 2 * F.d.lvl_cut;
   int h = c->begin(0);
   if (F.d.flat) flat_forward(F.d, r, out, c->sm_count, c->stream);
   else trsv_forward(F.d, r, out, c->tgrid, c->stream);
@@ -955,7 +971,7 @@ void ph_apply_dev(qp_ctx* c, const double* r, double* z, const int* done) {
     c->end(h);
     return;
   }
-  c->launches += 3;
+  c->launches += 3 + 2 * c->FP.d.lvl_cut;
   SweepRhs sr{};
   sr.rhs = r;
   sr.in_perm = c->perm_ph_dev;
@@ -2458,6 +2474,10 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     if (c->FF.d.flat)   // forest read as M (twice) and L11⁻¹ (twice) instead of L11, L21
       s->fsolve_bytes_F = 8.0 * ((double)S.sym_lower + 2.0 * (double)S.fl_msize + 2.0 * (double)S.fl_ci.size());
     s->sym_discrepancy = c->FF.sym_discrepancy;
+    s->lvl_levels_F = S.lvl_cut;
+    s->lvl_supernodes_F = S.lvl_blk.size();
+    s->lvl_levels_PH = c->FP.S.lvl_cut;
+    s->lvl_supernodes_PH = c->FP.S.lvl_blk.size();
     s->sym_enabled = c->FF.sym_enabled ? 1.0 : 0.0;
     s->flat_discrepancy = c->FF.flat_discrepancy;
     s->flat_enabled = c->FF.d.flat ? 1.0 : 0.0;

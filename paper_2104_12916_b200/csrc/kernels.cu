@@ -1167,6 +1167,134 @@ __device__ __forceinline__ void snw_backward(const DevFactor& F, double* x, int 
   }
 }
 
+// ---- leaf phase: one level of single-block supernodes (≤ G columns), a group of G lanes per supernode.
+// Every load that does not depend on the solve — the right-hand side, the accumulator, the group's column of
+// L_bb⁻¹ and the first G rows of L_rows with their indices — is issued before any arithmetic, so a supernode
+// costs about one memory round trip.  Forward: y = L_bb⁻¹ (b − acc), acc[rows] += L_rows·y (the level below
+// has finished: kernel order replaces the task graph's counters).
+template <int G>
+__device__ __forceinline__ unsigned lvl_mask() {
+  return G == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+}
+template <int G>
+__global__ void __launch_bounds__(NT, G == 16 ? 3 : 2) k_lvl_fwd(DevFactor F, SweepRhs R, double* x, int64_t i0,
+                                                                 int64_t i1) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const unsigned tls = tl_begin(8);
+  const int64_t i = i0 + ((int64_t)blockIdx.x * NT + threadIdx.x) / G;
+  if (i < i1) {   // whole groups take the same branch
+    const unsigned gm = lvl_mask<G>();
+    const int lane = threadIdx.x & (G - 1);
+    const int4 d0 = __ldg(F.lvl_desc + 2 * i), d1 = __ldg(F.lvl_desc + 2 * i + 1);   // one round trip
+    const double* L = F.fstore + ((int64_t)(uint32_t)d0.x | ((int64_t)d0.y << 32));
+    const double* inv = F.fstore + ((int64_t)(uint32_t)d0.z | ((int64_t)d0.w << 32));
+    const int32_t* rows = F.sn_rows + ((int64_t)(uint32_t)d1.x | ((int64_t)d1.y << 32));
+    const int64_t c0 = d1.z;
+    const int wk = d1.w & 63, noff = (int)((unsigned)d1.w >> 6);
+    if (noff > G)
+      for (int64_t e = (int64_t)lane * 16; e < (int64_t)noff * wk; e += G * 16) prefetch_l2(L + e);
+    double v = 0.0, a = 0.0;
+    if (lane < wk) {
+      const int64_t c = c0 + lane;
+      if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+      else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+      a = __ldcg(F.acc + c);
+    }
+    double iv[G];   // lane i: L_bb⁻¹(i, j) = inv[j·wk + i], j ≤ i
+#pragma unroll
+    for (int j = 0; j < G; ++j) iv[j] = (j < wk && j <= lane && lane < wk) ? __ldg(inv + j * wk + lane) : 0.0;
+    const bool rok = lane < noff;
+    const int32_t row = rok ? __ldg(rows + lane) : 0;
+    double lr[G];   // lane r: L(r, c)
+#pragma unroll
+    for (int c = 0; c < G; ++c) lr[c] = (c < wk && rok) ? __ldg(L + lane + (int64_t)c * noff) : 0.0;
+    if (lane < wk) F.acc[c0 + lane] = 0.0;
+    v -= a;
+    double y = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) y += iv[j] * __shfl_sync(gm, v, j, G);
+    if (lane < wk) x[c0 + lane] = y;
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < G; ++c) s += lr[c] * __shfl_sync(gm, y, c, G);
+    if (rok) atomicAdd(F.acc + row, s);
+    for (int r0 = G; r0 < noff; r0 += G) {
+      const int r = r0 + lane;
+      const bool ok = r < noff;
+      const int32_t rw = ok ? __ldg(rows + r) : 0;
+      double s2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        const double l = (c < wk && ok) ? __ldg(L + r + (int64_t)c * noff) : 0.0;
+        s2 += l * __shfl_sync(gm, y, c, G);
+      }
+      if (ok) atomicAdd(F.acc + rw, s2);
+    }
+  }
+  tl_end(8, tls);
+}
+// Transpose-reduce over a group of G lanes: lane l ends with Σ_lanes t[l] (G−1 shuffles for G columns).
+template <int G>
+__device__ __forceinline__ double group_treduce(double (&t)[G], int lane, unsigned gm) {
+#pragma unroll
+  for (int h = G / 2; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? t[k] : t[k + h];
+      const double keep = up ? t[k + h] : t[k];
+      t[k] = keep + __shfl_xor_sync(gm, send, h, G);
+    }
+  }
+  return t[0];
+}
+// Backward: t = L_rowsᵀ x_rows (the rows belong to higher levels, already final), x_b = L_bb⁻ᵀ (D⁻¹y_b − t).
+// Fixed-order arithmetic (no atomics): bit-reproducible.
+template <int G>
+__global__ void __launch_bounds__(NT, G == 16 ? 3 : 2) k_lvl_bwd(DevFactor F, double* x, const int* done_flag,
+                                                                 int64_t i0, int64_t i1) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(9);
+  const int64_t i = i0 + ((int64_t)blockIdx.x * NT + threadIdx.x) / G;
+  if (i < i1) {
+    const unsigned gm = lvl_mask<G>();
+    const int lane = threadIdx.x & (G - 1);
+    const int4 d0 = __ldg(F.lvl_desc + 2 * i), d1 = __ldg(F.lvl_desc + 2 * i + 1);
+    const double* L = F.fstore + ((int64_t)(uint32_t)d0.x | ((int64_t)d0.y << 32));
+    const double* inv = F.fstore + ((int64_t)(uint32_t)d0.z | ((int64_t)d0.w << 32));
+    const int32_t* rows = F.sn_rows + ((int64_t)(uint32_t)d1.x | ((int64_t)d1.y << 32));
+    const int64_t c0 = d1.z;
+    const int wk = d1.w & 63, noff = (int)((unsigned)d1.w >> 6);
+    if (noff > G)
+      for (int64_t e = (int64_t)lane * 16; e < (int64_t)noff * wk; e += G * 16) prefetch_l2(L + e);
+    double yv = 0.0, dinv = 0.0;
+    if (lane < wk) {
+      yv = __ldcg(x + c0 + lane);
+      dinv = 1.0 / __ldg(F.Dpiv + c0 + lane);
+    }
+    double ivt[G];   // lane i: L_bb⁻¹(j, i) = inv[i·wk + j], j ≥ i (one contiguous run per lane)
+#pragma unroll
+    for (int j = 0; j < G; ++j) ivt[j] = (j < wk && j >= lane && lane < wk) ? __ldg(inv + lane * wk + j) : 0.0;
+    double t[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) t[c] = 0.0;
+    for (int r0 = 0; r0 < noff; r0 += G) {
+      const int r = r0 + lane;
+      const bool ok = r < noff;
+      const double xr = ok ? __ldcg(x + __ldg(rows + r)) : 0.0;
+#pragma unroll
+      for (int c = 0; c < G; ++c) t[c] += ((c < wk && ok) ? __ldg(L + r + (int64_t)c * noff) : 0.0) * xr;
+    }
+    const double tc = group_treduce<G>(t, lane, gm);
+    const double rhs = lane < wk ? yv * dinv - tc : 0.0;
+    double xi = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) xi += ivt[j] * __shfl_sync(gm, rhs, j, G);
+    if (lane < wk) x[c0 + lane] = xi;
+  }
+  tl_end(9, tls);
+}
+
 // Forward sweep L y = b (unit lower L, factor order); y written to x.
 __global__ void __launch_bounds__(NT) k_trsv_fwd(DevFactor F, SweepRhs R, double* x) {
   extern __shared__ double sm[];
@@ -2456,10 +2584,24 @@ int trsv_grid(int device) {
 }
 
 void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s) {
+  for (int L = 0; L < F.lvl_cut; ++L) {   // leaf phase, bottom level first
+    const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
+    const int G = F.lvl_g_h[L];
+    const int g = (int)((i1 - i0) * G + NT - 1) / NT;
+    if (G == 16) k_lvl_fwd<16><<<g, NT, 0, s>>>(F, r, x, i0, i1);
+    else k_lvl_fwd<32><<<g, NT, 0, s>>>(F, r, x, i0, i1);
+  }
   k_trsv_fwd<<<grid, NT, trsv_smem_bytes(), s>>>(F, r, x);
 }
 void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid, cudaStream_t s) {
   k_trsv_bwd<<<grid, NT, trsv_smem_bytes(), s>>>(F, x, done_flag);
+  for (int L = F.lvl_cut - 1; L >= 0; --L) {   // leaf phase, top level first
+    const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
+    const int G = F.lvl_g_h[L];
+    const int g = (int)((i1 - i0) * G + NT - 1) / NT;
+    if (G == 16) k_lvl_bwd<16><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
+    else k_lvl_bwd<32><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
+  }
 }
 
 // ------------------------------------------------------------------------- reduction finalizers

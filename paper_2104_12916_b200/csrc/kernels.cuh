@@ -125,6 +125,12 @@ struct DevFactor {
   const int64_t* fl_bc_ptr;       // per forest column: its backward slots (unit order)
   const int32_t* fl_bc_src;
   int mf_group;                   // pivot blocks per trailing UPDATE (Symbolic::mf_group)
+  // leaf phase (Symbolic::lvl_*): trsv_forward / trsv_backward launch one level kernel per level
+  const int4* lvl_desc;           // per leaf-phase supernode (level order), 2 × int4: L offset, L_bb⁻¹ offset,
+                                  // row-list offset (int64 each, lo/hi), first column, w | noff << 6
+  int32_t lvl_cut;
+  int64_t lvl_ptr_h[25];          // host copy: blocks of level L are lvl_blk[lvl_ptr_h[L] .. lvl_ptr_h[L+1])
+  int8_t lvl_g_h[24];             // host copy: lanes per supernode (16 or 32) of each level
   unsigned long long* tprof;  // optional sweep instrumentation [2 sweeps][8 types][5] + per-task trace
   int64_t ttrace_cap;         // per-sweep trace capacity (tasks) after the 70 summary words
   int sweep_var;      // A/B switch (QPB_SWEEP_VAR, default 1): bit 0 = backward long tiles two rows per lane
@@ -263,7 +269,7 @@ void pcg_rz_ph(int64_t m2, const double* r, const double* z, double* partial, Pc
 void pcg_update2(int64_t m2, const double* z, double* p, PcgState* st, int grid, cudaStream_t s);
 // Launch timeline instrumentation (debug): kernels 0 flat_rhs, 1 flat_fwd, 2 root GEMV, 3 flat_bwd,
 // 4 pcg_step, 5 trsv_fwd, 6 trsv_bwd, 7 spmv; buf = nullptr disables.
-constexpr int TL_K = 8, TL_RING = 256;
+constexpr int TL_K = 10, TL_RING = 256;
 void timeline_enable(unsigned long long* buf);
 // Fused a5 + a6 (P_L / none, unsharded): cooperative launch; false if it could not be launched.
 // Rows of C with more than KF_LONG_ROW entries (listed in `longr`) are done warp per row, the rest thread per row.

@@ -17,6 +17,8 @@ constexpr int XCH = 8;           // column blocks per X chunk of a big supernode
 constexpr int FUSE_ELEMS = 2048;  // small supernodes with w·noff ≤ this are swept as one task
 constexpr int TASK_SHIFT = 28;   // task = (type << TASK_SHIFT) | index
 constexpr int LONG_TILE = 512;   // rows of a sweep tile of a full-width (BW) block
+constexpr int LVL_MAX = 24;      // most elimination-tree levels swept level-synchronously (leaf phase)
+constexpr int LVL_MIN = 1024;    // a level joins the leaf phase only with at least this many supernodes
 
 // Lower-triangular (strict) pattern + values of a symmetric matrix already in
 // factor order, by columns, plus its diagonal.
@@ -106,6 +108,14 @@ struct Symbolic {
   std::vector<int64_t> blk_dptr;         // per block: fused destination-supernode list (nb+1)
   std::vector<int32_t> blk_dest;
   std::vector<int32_t> snw_fwd, snw_bwd; // warp-swept tiny supernodes: 8 block ids per task (type 7), -1 padded
+  // leaf phase: the lowest lvl_cut levels of the supernodal elimination tree (all single-block supernodes
+  // ≤ 32 columns, ≥ LVL_MIN of them per level) are swept level by level, one kernel per level and a group of
+  // 16 or 32 lanes per supernode (k_lvl_fwd / k_lvl_bwd), before (forward) / after (backward) the task graph;
+  // they take no part in its counters.  lvl_blk: their blocks, level by level (lvl_ptr); lvl_g: lanes per
+  // supernode of each level.
+  int32_t lvl_cut = 0;
+  std::vector<int64_t> lvl_ptr;
+  std::vector<int32_t> lvl_blk, lvl_g;
   std::vector<int32_t> blk_big;          // 1 if the block belongs to a big supernode
   int64_t x_size = 0;                    // doubles of all X_J
   int64_t xtmp_size = 0;                 // doubles of the inversion scratch

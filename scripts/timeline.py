@@ -8,7 +8,7 @@ import numpy as np
 sys.path.insert(0, '.')
 import qpgen
 from paper_2104_12916_b200.binding import from_qp
-NAMES = ["flat_rhs", "flat_fwd", "root_gemv", "flat_bwd", "pcg_step", "trsv_fwd", "trsv_bwd", "spmv"]
+NAMES = ["flat_rhs", "flat_fwd", "root_gemv", "flat_bwd", "pcg_step", "trsv_fwd", "trsv_bwd", "spmv", "lvl_fwd", "lvl_bwd"]
 name = sys.argv[1] if len(sys.argv) > 1 else 'c1'
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 qp = qpgen.make(name)
