@@ -251,6 +251,10 @@ typedef struct {
   double lvl_levels_F, lvl_levels_PH;  /* leaf phase: bottom levels of L_F / L_PH swept level-synchronously
                                           (one launch per level, DESIGN §5 "leaf phase"); 0 = none */
   double lvl_supernodes_F, lvl_supernodes_PH;  /* supernodes in those levels */
+  double pi_enabled;                 /* 1 if F-solves sweep the levels above the leaf phase as level products
+                                        (Z_J = [L_JJ⁻¹; L_ext,J L_JJ⁻¹], one kernel per level) */
+  double pi_discrepancy;             /* their factor-time guard against the task-graph sweeps (−1: not built) */
+  double pi_levels;                  /* levels swept that way */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 

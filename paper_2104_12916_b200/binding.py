@@ -74,7 +74,8 @@ class _Stats(C.Structure):
                                           "flat_discrepancy", "flat_enabled", "flat_nnz_M", "dense_w_enabled",
                                           "dense_w_discrepancy", "kf_bytes_W", "dense_finv_enabled",
                                           "dense_finv_discrepancy", "lvl_levels_F", "lvl_levels_PH",
-                                          "lvl_supernodes_F", "lvl_supernodes_PH")]
+                                          "lvl_supernodes_F", "lvl_supernodes_PH", "pi_enabled", "pi_discrepancy",
+                                          "pi_levels")]
 
 
 _LIB = None

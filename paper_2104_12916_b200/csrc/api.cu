@@ -235,6 +235,8 @@ struct Factor {
   double sym_discrepancy = 0.0;  // ‖y_sym − y_X‖ / ‖y_X‖ measured at factor time
   bool sym_enabled = false;
   double flat_discrepancy = -1.0;  // ‖y_flat − y_sweep‖ / ‖y_sweep‖ at factor time (−1: not tried)
+  PiSweep pi{};                    // level products (partitioned inverse by levels)
+  double pi_discrepancy = -1.0;    // ‖y_levels − y_sweeps‖ / ‖y_sweeps‖ at factor time (−1: not tried)
   const int32_t* fwd_sym = nullptr;
   const int32_t* bwd_sym = nullptr;
   int64_t n_fwd_sym = 0, n_bwd_sym = 0, n_fwd_x = 0, n_bwd_x = 0;
@@ -853,10 +855,10 @@ int numeric_factor(qp_ctx* c, Factor& F, const double* src_vals, const double* D
 double* pst_red(qp_ctx* c) { return (double*)((char*)c->pst + offsetof(PcgState, red)); }
 double* ist_red(qp_ctx* c) { return (double*)((char*)c->ist + offsetof(IpmState, red)); }
 
-void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done) {
+void sym_gemv(qp_ctx* c, Factor& F, double* x, const int* done, const double* sub = nullptr) {
   if (!F.sym_enabled) return;
   c->launches += F.sym_symv.slots ? 2 : 1;
-  symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, &F.sym_symv, done, c->sm_count * 3, c->stream);
+  symroot_gemv(F.d, x, F.S.sym_c0, F.S.sym_c1, &F.sym_symv, done, c->sm_count * 3, c->stream, sub);
 }
 
 // One F-solve on the right-hand side described by r: the task-graph sweeps, or — flattened forest —
@@ -869,6 +871,21 @@ void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
     gather_rhs(r, c->df_rhs, out, F.d.N, c->sm_count, c->stream);
     dense_symv(c->dense_finv, c->df_ld, F.d.N, c->df_chunks, c->df_nch, &c->df_plan, c->df_rhs, out, r.done_flag,
                c->sm_count, c->stream);
+    c->end(h);
+    return;
+  }
+  if (F.pi.enabled) {   // level products: leaf levels, one product kernel per upper level, root GEMV, and back
+    int nl = 0;
+    for (int L = 0; L < F.pi.nlev; ++L) nl += F.pi.lev_ptr[L + 1] > F.pi.lev_ptr[L] ? 1 : 0;
+    c->launches += 1 + 2 * F.d.lvl_cut + 2 * nl;
+    int h = c->begin(0);
+    pi_forward(F.d, F.pi, r, out, c->sm_count, c->stream);
+    c->end(h);
+    h = c->begin(8);
+    sym_gemv(c, F, out, r.done_flag, F.d.acc);
+    c->end(h);
+    h = c->begin(1);
+    pi_backward(F.d, F.pi, out, r.done_flag, c->stream);
     c->end(h);
     return;
   }
@@ -1668,6 +1685,87 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
   return rc;
 }
 
+// Level products: plan and build Z_J = [X_J; L_ext,J X_J] for every supernode of F between the
+// leaf phase and the symmetric root, level by level (tiles of ≤ 512 rows × ≤ 64 columns, larger first).
+// Leaves F.pi.enabled = 0; the caller enables it after the accuracy guard.
+int build_pi(qp_ctx* c) {
+  Factor& F = c->FF;
+  const Symbolic& S = F.S;
+  const int64_t ns = S.ns, Jr = ns - 1;
+  F.pi = PiSweep{};
+  const int64_t min_n = std::getenv("QPB_PI_MINN") ? std::atoll(std::getenv("QPB_PI_MINN")) : 4096;   // tests: 0
+  if (Jr < 1 || S.sn_sinv[Jr] < 0 || F.n_sym != 1 || S.N <= min_n) return QP_OK;
+  const int lcut = F.d.lvl_cut;
+  int64_t top = -1;
+  for (int64_t J = 0; J < Jr; ++J)
+    if (S.sn_level[J] >= lcut) top = std::max<int64_t>(top, S.sn_level[J]);
+  if (top < lcut || top - lcut + 1 > PI_MAXLEV) return QP_OK;
+  const int nlev = (int)(top - lcut + 1);
+  std::vector<std::vector<int32_t>> by(nlev);
+  for (int64_t J = 0; J < Jr; ++J)
+    if (S.sn_level[J] >= lcut) by[S.sn_level[J] - lcut].push_back((int32_t)J);
+  std::vector<int64_t> zoffJ(ns, -1);
+  std::vector<PiTile> tiles;
+  std::vector<int32_t> tile_J;
+  int64_t zs = 0;
+  F.pi.lev_ptr[0] = 0;
+  for (int L = 0; L < nlev; ++L) {
+    std::vector<std::pair<PiTile, int32_t>> lt;
+    for (int32_t J : by[L]) {
+      const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+      const int64_t ld = (m + 1) & ~int64_t(1);
+      if (ld > INT32_MAX) return QP_OK;
+      zoffJ[J] = zs;
+      for (int64_t c0 = 0; c0 < w; c0 += 64) {
+        const int64_t nc = std::min<int64_t>(64, w - c0);
+        for (int64_t r0 = c0; r0 < m; r0 += 512) {
+          const int64_t nr = std::min<int64_t>(512, m - r0);
+          PiTile t{};
+          t.zoff = zs + r0 + c0 * ld;
+          t.roff = S.sn_rowptr[J] + r0;
+          t.ld = (int32_t)ld;
+          t.col0 = (int32_t)(S.sn_start[J] + c0);
+          t.nr = (int16_t)nr;
+          t.nc = (int16_t)nc;
+          t.wx = (int16_t)std::max<int64_t>(0, std::min<int64_t>(nr, w - r0));
+          lt.push_back({t, J});
+        }
+      }
+      zs += ld * w;
+    }
+    std::stable_sort(lt.begin(), lt.end(), [](const std::pair<PiTile, int32_t>& a, const std::pair<PiTile, int32_t>& b) {
+      return (int)a.first.nr * a.first.nc > (int)b.first.nr * b.first.nc;
+    });
+    for (auto& q : lt) {
+      tiles.push_back(q.first);
+      tile_J.push_back(q.second);
+    }
+    F.pi.lev_ptr[L + 1] = (int64_t)tiles.size();
+  }
+  if (tiles.empty()) return QP_OK;
+  cudaStream_t st = c->stream;
+  int64_t* zoff_dev = nullptr;
+  try {
+    F.pi.Z = F.mem.alloc<double>((size_t)zs);
+    F.pi.tiles = F.mem.upload(tiles, st);
+    F.pi.tile_J = F.mem.upload(tile_J, st);
+    zoff_dev = F.mem.upload(zoffJ, st);
+  } catch (std::bad_alloc&) {
+    cudaGetLastError();
+    F.pi = PiSweep{};
+    return QP_OK;   // not enough memory for Z: keep the sweeps
+  }
+  F.pi.nlev = nlev;
+  F.pi.z_size = zs;
+  F.pi.root0 = S.sn_start[Jr];
+  pi_build(F.d, F.pi, zoff_dev, st);
+  int rc = sync_check(c, "level-product build");   // host vectors
+  if (std::getenv("QPB_VERBOSE"))
+    std::fprintf(stderr, "qpb: level products: %d levels above the %d leaf levels, %zu tiles, Z %.1f MB\n", nlev, lcut,
+                 tiles.size(), zs * 8e-6);
+  return rc;
+}
+
 // Sharded mode: turn a per-rank yes/no into one decision shared by every rank (min over ranks of 0/1),
 // through the same collective the PCG uses.  Uses xbuf[0] as device scratch (free at setup).
 static int agree_all(qp_ctx* c, bool& ok) {
@@ -2064,6 +2162,35 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
       F.flat_discrepancy = fn > 0 ? std::sqrt(fd / fn) : 0.0;
       F.d.flat = (F.flat_discrepancy <= 1e-10 && std::isfinite(F.flat_discrepancy)) ? 1 : 0;
       if (!F.d.flat) cudaMemsetAsync(F.d.acc, 0, N * 8, st);   // the sweeps expect zero accumulators
+    }
+    // level products (deep forests: c2, c3s, c4s): same guard against the sweeps
+    const char* pe = std::getenv("QPB_PI");
+    if (F.sym_enabled && !F.d.flat && !(pe && pe[0] == '0')) {
+      rc = build_pi(c);
+      if (rc) return rc;
+      if (F.pi.nlev > 0) {
+        cudaMemcpyAsync(c->rhs2, r.data(), N * 8, cudaMemcpyHostToDevice, st);
+        f_solve_dev(c, c->rhs2, c->xbuf);
+        cudaMemcpyAsync(y2.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+        F.pi.enabled = 1;
+        f_solve_dev(c, c->rhs2, c->xbuf);
+        cudaMemcpyAsync(y1.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+        rc = sync_check(c, "level-product guard");
+        if (rc) return rc;
+        double fd = 0, fn = 0;
+        for (int64_t i = 0; i < N; ++i) {
+          fd += (y1[i] - y2[i]) * (y1[i] - y2[i]);
+          fn += y2[i] * y2[i];
+        }
+        F.pi_discrepancy = fn > 0 ? std::sqrt(fd / fn) : 0.0;
+        F.pi.enabled = (F.pi_discrepancy <= 1e-10 && std::isfinite(F.pi_discrepancy)) ? 1 : 0;
+        if (std::getenv("QPB_VERBOSE"))
+          std::fprintf(stderr, "qpb: level-product guard %.3e -> %s\n", F.pi_discrepancy, F.pi.enabled ? "on" : "off");
+        if (!F.pi.enabled) {   // the sweeps expect zero accumulators
+          cudaMemsetAsync(F.d.acc, 0, N * 8, st);
+          cudaMemsetAsync(F.d.tacc, 0, N * 8, st);
+        }
+      }
     }
   }
   if (int rc2 = build_dense_w(c)) return rc2;   // explicit W / small-N F⁻¹ (with or without a symmetric root)
@@ -2478,6 +2605,9 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->lvl_supernodes_F = S.lvl_blk.size();
     s->lvl_levels_PH = c->FP.S.lvl_cut;
     s->lvl_supernodes_PH = c->FP.S.lvl_blk.size();
+    s->pi_enabled = c->FF.pi.enabled ? 1.0 : 0.0;
+    s->pi_discrepancy = c->FF.pi_discrepancy;
+    s->pi_levels = c->FF.pi.enabled ? c->FF.pi.nlev : 0;
     s->sym_enabled = c->FF.sym_enabled ? 1.0 : 0.0;
     s->flat_discrepancy = c->FF.flat_discrepancy;
     s->flat_enabled = c->FF.d.flat ? 1.0 : 0.0;

@@ -2604,6 +2604,211 @@ void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid
   }
 }
 
+// ------------------------------------------------------------------------- level products (PiSweep)
+// Z_J = [X_J; L_ext,J X_J] per supernode; one kernel per elimination-tree level, a CTA per tile.
+__device__ __forceinline__ PiTile pi_load_tile(const PiTile* t) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(t)), b = __ldg(reinterpret_cast<const int4*>(t) + 1);
+  PiTile T;
+  T.zoff = (int64_t)(uint32_t)a.x | ((int64_t)a.y << 32);
+  T.roff = (int64_t)(uint32_t)a.z | ((int64_t)a.w << 32);
+  T.ld = b.x;
+  T.col0 = b.y;
+  T.nr = (int16_t)(b.z & 0xffff);
+  T.nc = (int16_t)((unsigned)b.z >> 16);
+  T.wx = (int16_t)(b.w & 0xffff);
+  T.pad = 0;
+  return T;
+}
+// X part of Z_J: rows [0, w) of the tile's columns, copied from L_bb⁻¹ (single block) or X_J (big supernode).
+__global__ void __launch_bounds__(NT) k_pi_build_x(DevFactor F, const PiTile* tiles, const int32_t* tile_J, double* Z,
+                                                   int64_t ntiles) {
+  const int64_t ti = blockIdx.x;
+  if (ti >= ntiles) return;
+  const PiTile T = pi_load_tile(tiles + ti);
+  if (T.wx <= 0) return;
+  const int J = tile_J[ti];
+  const int64_t cJ = F.sn_start[J], w = F.sn_start[J + 1] - cJ;
+  const int64_t r0 = T.roff - F.sn_rowptr[J], c0 = T.col0 - cJ;
+  const bool big = F.sn_xinv[J] >= 0;
+  const double* X = big ? F.xinv + F.sn_xinv[J] : F.fstore + F.blk_inv[F.sn_blk0[J]];
+  const int64_t ldx = big ? F.sn_ldx[J] : w;
+  for (int i = threadIdx.x; i < (int)T.wx * T.nc; i += NT) {
+    const int c = i / T.wx, r = i - c * T.wx;
+    const int64_t gr = r0 + r, gc = c0 + c;
+    Z[T.zoff + r + (int64_t)c * T.ld] = gr >= gc ? X[gr + gc * ldx] : 0.0;
+  }
+}
+// Y part: Y(e, c) = Σ_{k ≥ c} L_ext(e, k) X(k, c), a thread per external row, the tile's columns in registers.
+__global__ void __launch_bounds__(NT) k_pi_build_y(DevFactor F, const PiTile* tiles, const int32_t* tile_J, double* Z,
+                                                   const int64_t* zoffJ, int64_t ntiles) {
+  const int64_t ti = blockIdx.x;
+  if (ti >= ntiles) return;
+  const PiTile T = pi_load_tile(tiles + ti);
+  if (T.wx >= T.nr) return;
+  const int J = tile_J[ti];
+  const int64_t cJ = F.sn_start[J], w = F.sn_start[J + 1] - cJ;
+  const int64_t r0 = T.roff - F.sn_rowptr[J], c0 = T.col0 - cJ;
+  const int b0 = F.sn_blk0[J];
+  const double* Zx = Z + zoffJ[J];   // X_J: rows [0, w), leading dimension T.ld
+  for (int r = T.wx + threadIdx.x; r < T.nr; r += NT) {
+    const int64_t e = r0 + r - w;    // external row
+    double a[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) a[c] = 0.0;
+    for (int64_t k = c0; k < w; ++k) {
+      const int b = b0 + (int)(k >> 6), kk = (int)(k & 63);
+      const int64_t noff = F.blk_noff[b];
+      const int64_t local = w + e - (((k >> 6) << 6) + F.blk_w[b]);
+      const double l = F.fstore[F.blk_off[b] + local + (int64_t)kk * noff];
+      const double* xr = Zx + k;
+#pragma unroll
+      for (int c = 0; c < 64; ++c)
+        if (c < T.nc && c0 + c <= k) a[c] += l * xr[(c0 + c) * (int64_t)T.ld];
+    }
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      if (c < T.nc) Z[T.zoff + r + (int64_t)c * T.ld] = a[c];
+  }
+}
+// Start of a level-product F-solve: acc = tacc = x = 0; the root's right-hand side into vbuf.
+__global__ void __launch_bounds__(NT) k_pi_init(DevFactor F, SweepRhs R, double* x, int64_t root0) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  for (int64_t c = blockIdx.x * (int64_t)NT + threadIdx.x; c < F.N; c += (int64_t)gridDim.x * NT) {
+    F.acc[c] = 0.0;
+    F.tacc[c] = 0.0;
+    x[c] = 0.0;
+    if (c >= root0) {
+      double v;
+      if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+      else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+      F.vbuf[c] = v;
+    }
+  }
+}
+// Forward, one level: v = b − acc on the tile's columns; [y; u] += Z_tile v (y into tacc, u into acc).
+__global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const PiTile* tiles, const double* Z) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const unsigned tls = tl_begin(5);
+  __shared__ double v[64];
+  const PiTile T = pi_load_tile(tiles + blockIdx.x);
+  const int tid = threadIdx.x;
+  if (tid < T.nc) {
+    const int64_t c = (int64_t)T.col0 + tid;
+    double b;
+    if (R.ct.p != nullptr) b = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+    else b = R.rhs[R.in_perm ? R.in_perm[c] : c];
+    v[tid] = b - __ldcg(F.acc + c);
+  }
+  __syncthreads();
+  const int r = 2 * tid;
+  if (r < T.nr) {
+    const double* zp = Z + T.zoff + r;
+    const int32_t* rows = F.sn_rows + T.roff + r;
+    const bool two = r + 1 < T.nr;
+    const int32_t g0 = __ldg(rows), g1 = two ? __ldg(rows + 1) : 0;
+    double s0 = 0.0, s1 = 0.0;
+    const int64_t ld = T.ld;
+#pragma unroll 8
+    for (int c = 0; c < T.nc; ++c) {
+      const double2 z = __ldg(reinterpret_cast<const double2*>(zp + c * ld));
+      const double vc = v[c];
+      s0 += z.x * vc;
+      s1 += z.y * vc;
+    }
+    atomicAdd((r < T.wx ? F.tacc : F.acc) + g0, s0);
+    if (two) atomicAdd((r + 1 < T.wx ? F.tacc : F.acc) + g1, s1);
+  }
+  tl_end(5, tls);
+}
+// Backward, one level: s = D⁻¹y on the tile's own rows, −x on its external rows; x_cols += Z_tileᵀ s.
+__global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* tiles, const double* Z, double* x,
+                                                  const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(6);
+  __shared__ double s[512 + 2];
+  const PiTile T = pi_load_tile(tiles + blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int r = tid; r < ((T.nr + 1) & ~1); r += NT) {
+    double sv = 0.0;
+    if (r < T.nr) {
+      const int32_t g = __ldg(F.sn_rows + T.roff + r);
+      sv = r < T.wx ? __ldcg(F.tacc + g) / __ldg(F.Dpiv + g) : -__ldcg(x + g);
+    }
+    s[r] = sv;
+  }
+  __syncthreads();
+  double t[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t[k] = 0.0;
+  const int64_t ld = T.ld;
+  const double* zp = Z + T.zoff + (int64_t)wid * ld;
+  for (int rb = 2 * lane; rb < T.nr; rb += 64) {
+    const double s0 = s[rb], s1 = s[rb + 1];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (wid + 8 * k < T.nc) {
+        const double2 z = __ldg(reinterpret_cast<const double2*>(zp + rb + 8 * k * ld));
+        t[k] += z.x * s0 + z.y * s1;
+      }
+    }
+  }
+  // 8 column sums over 32 lanes: fold 8 → 1 values over xor 16, 8, 4, then two plain stages
+#pragma unroll
+  for (int h = 4, m = 16; h >= 1; h >>= 1, m >>= 1) {
+    const bool up = lane & m;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? t[k] : t[k + h];
+      const double keep = up ? t[k + h] : t[k];
+      t[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  double r0 = t[0];
+  r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+  r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+  // lane bits (16, 8, 4) select k = 4·b16 + 2·b8 + b4
+  if ((lane & 3) == 0) {
+    const int k = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    const int c = wid + 8 * k;
+    if (c < T.nc) atomicAdd(x + T.col0 + c, r0);
+  }
+  tl_end(6, tls);
+}
+void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaStream_t s) {
+  const int64_t nt = P.lev_ptr[P.nlev];
+  if (nt <= 0) return;
+  cudaMemsetAsync(P.Z, 0, (size_t)P.z_size * sizeof(double), s);
+  k_pi_build_x<<<(unsigned)nt, NT, 0, s>>>(F, P.tiles, P.tile_J, P.Z, nt);
+  k_pi_build_y<<<(unsigned)nt, NT, 0, s>>>(F, P.tiles, P.tile_J, P.Z, zoffJ, nt);
+}
+void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
+  k_pi_init<<<sms * 4, NT, 0, s>>>(F, r, x, P.root0);
+  for (int L = 0; L < F.lvl_cut; ++L) {   // leaf phase, bottom level first
+    const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
+    const int G = F.lvl_g_h[L];
+    const int g = (int)((i1 - i0) * G + NT - 1) / NT;
+    if (G == 16) k_lvl_fwd<16><<<g, NT, 0, s>>>(F, r, x, i0, i1);
+    else k_lvl_fwd<32><<<g, NT, 0, s>>>(F, r, x, i0, i1);
+  }
+  for (int L = 0; L < P.nlev; ++L) {
+    const int64_t n = P.lev_ptr[L + 1] - P.lev_ptr[L];
+    if (n > 0) k_pi_fwd<<<(unsigned)n, NT, 0, s>>>(F, r, P.tiles + P.lev_ptr[L], P.Z);
+  }
+}
+void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* done_flag, cudaStream_t s) {
+  for (int L = P.nlev - 1; L >= 0; --L) {
+    const int64_t n = P.lev_ptr[L + 1] - P.lev_ptr[L];
+    if (n > 0) k_pi_bwd<<<(unsigned)n, NT, 0, s>>>(F, P.tiles + P.lev_ptr[L], P.Z, x, done_flag);
+  }
+  for (int L = F.lvl_cut - 1; L >= 0; --L) {   // leaf phase, top level first
+    const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
+    const int G = F.lvl_g_h[L];
+    const int g = (int)((i1 - i0) * G + NT - 1) / NT;
+    if (G == 16) k_lvl_bwd<16><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
+    else k_lvl_bwd<32><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
+  }
+}
+
 // ------------------------------------------------------------------------- reduction finalizers
 // Each takes the GLOBAL reduced values (local ones when not sharded) and updates the state.
 __device__ void fin_pcg_init(PcgState* st, double bb, double rz) {

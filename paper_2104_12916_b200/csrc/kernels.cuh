@@ -255,6 +255,39 @@ void flat_set_unit(double* unit, int64_t col, cudaStream_t s);
 // after the extraction: row-form values of M gathered from the M_J blocks
 void flat_fill_rows(const DevFactor& F, const int32_t* src, int64_t nnz, cudaStream_t s);
 
+// ---- level products (partitioned inverse by elimination-tree levels, F only; DESIGN §5 "level products")
+// Every supernode J above the leaf phase and below the symmetric root stores the panel
+//   Z_J = [X_J; Y_J],  X_J = L_JJ⁻¹ (w×w, lower),  Y_J = L_ext,J · X_J (noff×w),
+// column-major with an even leading dimension.  With v_J = b_J − acc_J the forward step of J is the one
+// product [y_J; u] = Z_J v_J (u added to acc[rows]); backward x_J = X_Jᵀ D_J⁻¹ y_J − Y_Jᵀ x_rows = Z_Jᵀ s.
+// Neither has a dependency inside the supernode, so one level of the tree is one dependency-free kernel
+// over tiles of ≤ 512 rows × ≤ 64 columns (the classical no-fill partitioned inverse with the
+// elimination-tree levels as partitions).
+struct PiTile {          // 32 bytes, read as two int4
+  int64_t zoff;          // first entry of the tile in Z (even)
+  int64_t roff;          // first row of the tile in sn_rows
+  int32_t ld;            // leading dimension of Z_J (even)
+  int32_t col0;          // factor column of the tile's first column
+  int16_t nr, nc;        // rows (≤ 512), columns (≤ 64)
+  int16_t wx;            // rows of the tile that lie in X_J (the supernode's own columns): 0 … nr
+  int16_t pad;
+};
+constexpr int PI_MAXLEV = 64;
+struct PiSweep {
+  int enabled = 0;
+  int nlev = 0;                        // levels lvl_cut … top−1 (the symmetric root excluded)
+  const PiTile* tiles = nullptr;       // level-major
+  const int32_t* tile_J = nullptr;     // supernode of each tile (build only)
+  double* Z = nullptr;
+  int64_t z_size = 0;
+  int64_t root0 = 0;                   // first column of the symmetric root
+  int64_t lev_ptr[PI_MAXLEV + 1] = {0};
+};
+// Z from the factor storage (after the numeric factorization and the X_J inverses); zoffJ: per supernode offset of Z_J (device)
+void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaStream_t s);
+void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s);
+void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* done_flag, cudaStream_t s);
+
 // ---- vector / SpMV kernels
 void kf_q(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D, const double* p, const double* z,
           double* q, double* partial, PcgState* st, int grid, cudaStream_t s, bool pcg_mode);

@@ -38,7 +38,11 @@ st = s.stats()
 rng = np.random.default_rng(8)
 D = rng.uniform(0.5, 2.0, qp.m2)
 b = rng.standard_normal(qp.m2)
-out = {"dense_w": st["dense_w_enabled"], "flat": st["flat_enabled"], "xs": {}}
+out = {"dense_w": st["dense_w_enabled"], "flat": st["flat_enabled"], "pi": st["pi_enabled"],
+       "pi_levels": st["pi_levels"], "lvl": st["lvl_levels_F"], "xs": {}}
+if len(sys.argv) > 4 and sys.argv[4] == 'fsolve':
+    f = np.random.default_rng(12).standard_normal(qp.n + qp.m1)
+    out["fsolve"] = np.concatenate(s.f_solve(f)).tolist()
 for k in (1, 3, 7):
     x, it, rr, rc = s.pcg_solve(D, b, tol=0.0, maxit=k)
     out["xs"][str(k)] = [it, x.tolist()]
@@ -62,10 +66,10 @@ VARIANTS = {"default": {}, "no_dense_w": {"QPB_DENSE_W": "0"}, "force_w": {"QPB_
             "unfused_force_w": {"QPB_FUSED_PCG": "0", "QPB_DENSE_W": "2"}}
 
 
-def run_child(expr, env_extra, ipm):
+def run_child(expr, env_extra, ipm, extra=()):
     env = dict(os.environ)
     env.update(env_extra)
-    p = subprocess.run([sys.executable, "-c", CHILD, ROOT, expr, "1" if ipm else "0"], capture_output=True,
+    p = subprocess.run([sys.executable, "-c", CHILD, ROOT, expr, "1" if ipm else "0", *extra], capture_output=True,
                        text=True, env=env,
                        timeout=600, cwd=ROOT)
     line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
@@ -112,6 +116,40 @@ def test_path_variant_matches_oracle(oracle_case, variant):
     if obj is not None:
         assert out["converged"]
         assert abs(out["obj"] - obj) <= 1e-8 * max(1.0, abs(obj))
+
+
+PI_ENV = {"QPB_PI_MINN": "0", "QPB_DENSE_FINV": "0", "QPB_DENSE_W": "0", "QPB_FLAT": "0"}
+
+
+@pytest.mark.parametrize("variant", ["leaf_phase", "all_levels", "off"])
+def test_level_products_match_oracle(variant):
+    """Level products (Z_J = [L_JJ⁻¹; L_ext L_JJ⁻¹], one kernel per elimination-tree level) on a
+    grid QP small enough for the dense oracle: the F-solve and the P_L PCG iterates against the oracle with
+    (a) the leaf phase below them, (b) every level swept as a product, (c) switched off (the task graph)."""
+    expr = "qpgen.make_grid_qp(48, 80, 200, seed=9, name='grid48')"
+    qp = eval(expr)
+    env = dict(PI_ENV)
+    env.update({"leaf_phase": {"QPB_LVL_MIN": "16"}, "all_levels": {"QPB_LVL": "0"}, "off": {"QPB_PI": "0"}}[variant])
+    out = run_child(expr, env, False, extra=("fsolve",))
+    assert out["dense_w"] == 0.0 and out["flat"] == 0.0
+    if variant == "off":
+        assert out["pi"] == 0.0
+    else:
+        assert out["pi"] == 1.0 and out["pi_levels"] >= 2
+        assert (out["lvl"] > 0) == (variant == "leaf_phase")
+    fs = DenseF(qp.H, qp.A)
+    f = np.random.default_rng(12).standard_normal(qp.n + qp.m1)
+    yr = np.concatenate(fs.solve(f[:qp.n], f[qp.n:]))
+    y = np.asarray(out["fsolve"])
+    assert np.linalg.norm(y - yr) <= 1e-9 * np.linalg.norm(yr), np.linalg.norm(y - yr) / np.linalg.norm(yr)
+    rng = np.random.default_rng(8)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    b = rng.standard_normal(qp.m2)
+    for k in (1, 3, 7):
+        xr, itr, *_ = oracle_pcg(lambda v: kkt.KF_apply(qp, fs, D, v), b, kkt.PrecondL(D), 0.0, k)
+        it, x = out["xs"][str(k)]
+        assert it == k
+        assert np.linalg.norm(np.asarray(x) - xr) <= 1e-8 * np.linalg.norm(xr)
 
 
 def test_debug_timeline_records_pcg_launches():
