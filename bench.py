@@ -305,9 +305,16 @@ def measure_secondary(cfg, args, local, stream, peak, peak_src):
     value = pcg / (ms / 1e3) if ms > 0 else 0.0
     ach_it = pcg * b_it / (ms / 1e3) / 1e9 if ms > 0 else 0.0
     fsolve_ms = fwd_ms + bwd_ms + root_ms
+    if st.get("pi_enabled"):   # level products: leaf levels / subtrees, then one product kernel per level
+        leaf = "k_st_fwd" if st.get("pi_subtrees") else "k_lvl_fwd x%d" % int(st["lvl_levels_F"])
+        kf = "k_pi_init + %s + k_pi_fwd x%d levels" % (leaf, int(st["pi_levels"]))
+        kb = "k_pi_bwd x%d levels + %s" % (int(st["pi_levels"]), leaf.replace("fwd", "bwd"))
+    else:
+        kf, kb = "k_trsv_fwd", "k_trsv_bwd"
     out = {
         "config": cfg, "workload": f"{cfg} PL-KF: one IPM iteration per step (sparse supernodal sweeps for every "
                                    f"K_F product, symmetric-root GEMV, fused PCG step)",
+        "sweep_path": "level products" if st.get("pi_enabled") else "task graph",
         "n": qp.n, "m1": qp.m1, "m2": qp.m2, "nnz_LF": st["nnz_LF"], "metric": METRIC, "unit": UNIT,
         "value": value, "ms_per_step": ms / max(1, steps), "steps": steps, "warmup": W, "pcg_iters_timed": pcg,
         "ms_per_pcg_iter": ms / max(1, pcg),
@@ -316,16 +323,16 @@ def measure_secondary(cfg, args, local, stream, peak, peak_src):
         "B_it_note": "SURVEY 8(d): 16 nnz(L_F) + 24 nnz(C) + 8(15 m2 + 6(n+m1)) per PCG iteration; the timed step "
                      "also holds the IPM step's r_nu / recovery F-solves and residuals, so this is a lower bound",
         "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
-                     "kernel": "k_trsv_fwd + k_symroot_gemv + k_trsv_bwd (one F-solve)",
+                     "kernel": f"[{kf}] + k_symroot_gemv + [{kb}] (one F-solve)",
                      "achieved": gbs(st["fsolve_bytes_F"], fsolve_ms),
                      "frac": (gbs(st["fsolve_bytes_F"], fsolve_ms) or 0) / peak,
                      "algorithmic_bytes_per_fsolve": st["fsolve_bytes_F"],
-                     "per_kernel": {"k_trsv_fwd": {"bytes": forest_bytes, "ms": fwd_ms / max(1, solves),
-                                                   "GBps": gbs(forest_bytes, fwd_ms)},
+                     "per_kernel": {"forward": {"kernels": kf, "bytes": forest_bytes, "ms": fwd_ms / max(1, solves),
+                                                "GBps": gbs(forest_bytes, fwd_ms)},
                                     "k_symroot_gemv": {"bytes": root_bytes, "ms": root_ms / max(1, solves),
                                                        "GBps": gbs(root_bytes, root_ms)},
-                                    "k_trsv_bwd": {"bytes": forest_bytes, "ms": bwd_ms / max(1, solves),
-                                                   "GBps": gbs(forest_bytes, bwd_ms)}},
+                                    "backward": {"kernels": kb, "bytes": forest_bytes, "ms": bwd_ms / max(1, solves),
+                                                 "GBps": gbs(forest_bytes, bwd_ms)}},
                      "fsolve_share_of_step": fsolve_ms / sum(v[0] for v in prof.values()) if prof else None},
         "setup_s": t_setup, "l2": "no flush: the factor read by every sweep (%.2f GB) exceeds L2" % (
             st["factor_bytes"] / 1e9),
@@ -508,6 +515,8 @@ def run_ours(args, rank, world, local, use_dist):
     flat = bool(st.get("flat_enabled", 0))
     kname = ("F-solve = k_flat_fwd_t + k_symroot_gemv + k_flat_bwd_t (+ k_flat_rhs outside PCG; inside PCG the "
              "fused step prepares C^T p)" if flat else
+             "F-solve = k_pi_init + leaf levels / subtrees + k_pi_fwd per level + k_symroot_gemv + k_pi_bwd per "
+             "level + leaf levels / subtrees (level products)" if st.get("pi_enabled") else
              "F-solve = (C^T p SpMV +) k_trsv_fwd + k_symroot_gemv + k_trsv_bwd")
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

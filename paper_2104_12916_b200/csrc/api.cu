@@ -877,7 +877,7 @@ void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
   if (F.pi.enabled) {   // level products: leaf levels, one product kernel per upper level, root GEMV, and back
     int nl = 0;
     for (int L = 0; L < F.pi.nlev; ++L) nl += F.pi.lev_ptr[L + 1] > F.pi.lev_ptr[L] ? 1 : 0;
-    c->launches += 1 + 2 * F.d.lvl_cut + 2 * nl;
+    c->launches += 1 + (F.pi.st_n > 0 ? 2 : 2 * F.d.lvl_cut) + 2 * nl;
     int h = c->begin(0);
     pi_forward(F.d, F.pi, r, out, c->sm_count, c->stream);
     c->end(h);
@@ -1695,15 +1695,108 @@ int build_pi(qp_ctx* c) {
   F.pi = PiSweep{};
   const int64_t min_n = std::getenv("QPB_PI_MINN") ? std::atoll(std::getenv("QPB_PI_MINN")) : 4096;   // tests: 0
   if (Jr < 1 || S.sn_sinv[Jr] < 0 || F.n_sym != 1 || S.N <= min_n) return QP_OK;
-  const int lcut = F.d.lvl_cut;
+  // ---- subtrees below the level products (kernels.cuh StHdr): maximal subtrees of single-block supernodes of
+  // ≤ 32 columns whose entries fit QPB_ST_KB (default 96 KB) and whose frame fits ST_FRAME
+  std::vector<char> in_st(ns, 0);
+  std::vector<StHdr> hdr;
+  std::vector<int32_t> sdesc, slptr, sloc;
+  int st_g = 16;
+  {
+    const char* se = std::getenv("QPB_ST");
+    const int64_t budget = (std::getenv("QPB_ST_KB") ? std::atoll(std::getenv("QPB_ST_KB")) : 96) * 128;   // doubles
+    std::vector<int64_t> sub(ns, 0), cols(ns, 0), cnt(ns, 0);
+    std::vector<char> ok(ns, 1), fits(ns, 0);
+    bool post = true;
+    for (int64_t J = 0; J < ns && post; ++J) post = S.sn_parent[J] < 0 || S.sn_parent[J] > J;
+    for (int64_t J = 0; post && !(se && se[0] == '0') && J < ns; ++J) {
+      const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J], noff = m - w;
+      const bool elig = J != Jr && S.sn_blk0[J + 1] - S.sn_blk0[J] == 1 && w <= 32 && S.sn_xinv[J] < 0 &&
+                        noff < (int64_t(1) << 25);
+      sub[J] += w * w + noff * w;
+      cols[J] += w;
+      cnt[J] += 1;
+      ok[J] = ok[J] && elig;
+      bool f = ok[J] && sub[J] <= budget && cols[J] + noff <= ST_FRAME && S.sn_level[J] < 30 && cnt[J] <= J + 1 &&
+               cnt[J] <= ST_MAXSN;
+      if (f) {   // the subtree's supernodes and columns are the contiguous ranges ending at J (postorder)
+        const int64_t K0 = J - cnt[J] + 1;
+        f = S.sn_start[J + 1] - cols[J] == S.sn_start[K0];
+        for (int64_t K = K0; f && K < J; ++K) f = S.sn_parent[K] > K && S.sn_parent[K] <= J;
+      }
+      fits[J] = f;
+      const int64_t p = S.sn_parent[J];
+      if (p >= 0) {
+        sub[p] += sub[J];
+        cols[p] += cols[J];
+        cnt[p] += cnt[J];
+        if (!ok[J]) ok[p] = 0;
+      }
+    }
+    std::vector<int32_t> roots;
+    for (int64_t J = 0; J < ns; ++J)
+      if (fits[J] && (S.sn_parent[J] < 0 || !fits[S.sn_parent[J]])) roots.push_back((int32_t)J);
+    const int64_t st_min = std::getenv("QPB_ST_MIN") ? std::atoll(std::getenv("QPB_ST_MIN")) : 64;
+    if ((int64_t)roots.size() < st_min) roots.clear();   // too few to fill the GPU: keep the leaf phase
+    std::stable_sort(roots.begin(), roots.end(), [&](int32_t a, int32_t b) { return sub[a] > sub[b]; });
+    for (int32_t Jt : roots) {
+      const int64_t K0 = Jt - cnt[Jt] + 1;
+      const int64_t c_lo = S.sn_start[K0], c_hi = S.sn_start[Jt + 1];
+      const int64_t wt = S.sn_start[Jt + 1] - S.sn_start[Jt];
+      const int32_t* rr = S.sn_rows.data() + S.sn_rowptr[Jt] + wt;
+      const int64_t next = S.sn_rowptr[Jt + 1] - S.sn_rowptr[Jt] - wt;
+      std::vector<int32_t> mem;
+      for (int64_t K = K0; K <= Jt; ++K) mem.push_back((int32_t)K);
+      std::stable_sort(mem.begin(), mem.end(), [&](int32_t a, int32_t b) { return S.sn_level[a] < S.sn_level[b]; });
+      StHdr h{};
+      h.d0 = (int32_t)(sdesc.size() / 8);
+      h.nlev = (int32_t)S.sn_level[Jt] + 1;
+      h.c_lo = (int32_t)c_lo;
+      h.ncols = (int32_t)(c_hi - c_lo);
+      h.next = (int32_t)next;
+      h.lptr = (int32_t)slptr.size();
+      h.rootrows = S.sn_rowptr[Jt] + wt;
+      h.fslo = S.blk_inv[S.sn_blk0[K0]];
+      h.fslen = (int32_t)(S.blk_off[S.sn_blk0[Jt]] + next * wt - h.fslo);
+      size_t q = 0;
+      for (int32_t l = 0; l <= h.nlev; ++l) {
+        while (l < h.nlev && q < mem.size() && S.sn_level[mem[q]] < l) ++q;
+        slptr.push_back(l < h.nlev ? (int32_t)q : (int32_t)mem.size());
+      }
+      for (int32_t K : mem) {
+        in_st[K] = 1;
+        const int64_t w = S.sn_start[K + 1] - S.sn_start[K], m = S.sn_rowptr[K + 1] - S.sn_rowptr[K], noff = m - w;
+        if (w > 16) st_g = 32;
+        const int32_t b = S.sn_blk0[K];
+        const int64_t lo = S.blk_off[b], io = S.blk_inv[b], ro = (int64_t)sloc.size();
+        for (int64_t e = 0; e < noff; ++e) {
+          const int32_t g = S.sn_rows[S.sn_rowptr[K] + w + e];
+          if (g < c_hi) {
+            sloc.push_back((int32_t)(g - c_lo));
+          } else {
+            const int32_t* it = std::lower_bound(rr, rr + next, g);
+            if (it == rr + next || *it != g) return fail(c, QP_EINVAL, "subtree plan: row outside the root's row list");
+            sloc.push_back((int32_t)(h.ncols + (it - rr)));
+          }
+        }
+        sdesc.insert(sdesc.end(), {(int32_t)(uint32_t)(lo & 0xffffffffll), (int32_t)(lo >> 32),
+                                   (int32_t)(uint32_t)(io & 0xffffffffll), (int32_t)(io >> 32),
+                                   (int32_t)(uint32_t)(ro & 0xffffffffll), (int32_t)(ro >> 32), (int32_t)S.sn_start[K],
+                                   (int32_t)(w | (noff << 6))});
+      }
+      hdr.push_back(h);
+    }
+  }
+  const bool use_st = !hdr.empty();
+  const int lcut = use_st ? 0 : F.d.lvl_cut;
+  auto in_pi = [&](int64_t J) { return J < Jr && (use_st ? !in_st[J] : S.sn_level[J] >= lcut); };
   int64_t top = -1;
   for (int64_t J = 0; J < Jr; ++J)
-    if (S.sn_level[J] >= lcut) top = std::max<int64_t>(top, S.sn_level[J]);
+    if (in_pi(J)) top = std::max<int64_t>(top, S.sn_level[J]);
   if (top < lcut || top - lcut + 1 > PI_MAXLEV) return QP_OK;
   const int nlev = (int)(top - lcut + 1);
   std::vector<std::vector<int32_t>> by(nlev);
   for (int64_t J = 0; J < Jr; ++J)
-    if (S.sn_level[J] >= lcut) by[S.sn_level[J] - lcut].push_back((int32_t)J);
+    if (in_pi(J)) by[S.sn_level[J] - lcut].push_back((int32_t)J);
   std::vector<int64_t> zoffJ(ns, -1);
   std::vector<PiTile> tiles;
   std::vector<int32_t> tile_J;
@@ -1750,6 +1843,14 @@ int build_pi(qp_ctx* c) {
     F.pi.tiles = F.mem.upload(tiles, st);
     F.pi.tile_J = F.mem.upload(tile_J, st);
     zoff_dev = F.mem.upload(zoffJ, st);
+    if (use_st) {
+      F.pi.st_hdr = F.mem.upload(hdr, st);
+      F.pi.st_desc = reinterpret_cast<const int4*>(F.mem.upload(sdesc, st));
+      F.pi.st_lptr = F.mem.upload(slptr, st);
+      F.pi.st_loc = F.mem.upload(sloc, st);
+      F.pi.st_n = (int64_t)hdr.size();
+      F.pi.st_g = st_g;
+    }
   } catch (std::bad_alloc&) {
     cudaGetLastError();
     F.pi = PiSweep{};
@@ -1761,8 +1862,8 @@ int build_pi(qp_ctx* c) {
   pi_build(F.d, F.pi, zoff_dev, st);
   int rc = sync_check(c, "level-product build");   // host vectors
   if (std::getenv("QPB_VERBOSE"))
-    std::fprintf(stderr, "qpb: level products: %d levels above the %d leaf levels, %zu tiles, Z %.1f MB\n", nlev, lcut,
-                 tiles.size(), zs * 8e-6);
+    std::fprintf(stderr, "qpb: level products: %d levels above %s (%d / %zu), %zu tiles, Z %.1f MB\n", nlev,
+                 use_st ? "the subtrees" : "the leaf levels", lcut, hdr.size(), tiles.size(), zs * 8e-6);
   return rc;
 }
 
@@ -2608,6 +2709,7 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->pi_enabled = c->FF.pi.enabled ? 1.0 : 0.0;
     s->pi_discrepancy = c->FF.pi_discrepancy;
     s->pi_levels = c->FF.pi.enabled ? c->FF.pi.nlev : 0;
+    s->pi_subtrees = c->FF.pi.enabled ? (double)c->FF.pi.st_n : 0.0;
     s->sym_enabled = c->FF.sym_enabled ? 1.0 : 0.0;
     s->flat_discrepancy = c->FF.flat_discrepancy;
     s->flat_enabled = c->FF.d.flat ? 1.0 : 0.0;

@@ -2565,6 +2565,13 @@ void flat_extract(const DevFactor& F, int64_t col, const double* x, double* unit
 }
 void flat_set_unit(double* unit, int64_t col, cudaStream_t s) { k_set_unit<<<1, 1, 0, s>>>(unit, col); }
 
+__global__ void k_lvl16_fwd(DevFactor F, SweepRhs R, double* x, int64_t i0, int64_t i1);
+__global__ void k_lvl16_bwd(DevFactor F, double* x, const int* done_flag, int64_t i0, int64_t i1);
+// QPB_LVL16=0: the 16-lane level kernels instead of the warp-per-supernode ones (A/B)
+static bool lvl16_on() {
+  static const bool on = !(std::getenv("QPB_LVL16") && std::getenv("QPB_LVL16")[0] == '0');
+  return on;
+}
 static size_t trsv_smem_bytes() { return sizeof(double) * (size_t)TRSV_SMEM_DBL; }
 
 int trsv_grid(int device) {
@@ -2588,7 +2595,8 @@ void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cu
     const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
     const int G = F.lvl_g_h[L];
     const int g = (int)((i1 - i0) * G + NT - 1) / NT;
-    if (G == 16) k_lvl_fwd<16><<<g, NT, 0, s>>>(F, r, x, i0, i1);
+    if (G == 16 && lvl16_on()) k_lvl16_fwd<<<(unsigned)(((i1 - i0) * 32 + NT - 1) / NT), NT, 0, s>>>(F, r, x, i0, i1);
+    else if (G == 16) k_lvl_fwd<16><<<g, NT, 0, s>>>(F, r, x, i0, i1);
     else k_lvl_fwd<32><<<g, NT, 0, s>>>(F, r, x, i0, i1);
   }
   k_trsv_fwd<<<grid, NT, trsv_smem_bytes(), s>>>(F, r, x);
@@ -2599,7 +2607,8 @@ void trsv_backward(const DevFactor& F, double* x, const int* done_flag, int grid
     const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
     const int G = F.lvl_g_h[L];
     const int g = (int)((i1 - i0) * G + NT - 1) / NT;
-    if (G == 16) k_lvl_bwd<16><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
+    if (G == 16 && lvl16_on()) k_lvl16_bwd<<<(unsigned)(((i1 - i0) * 32 + NT - 1) / NT), NT, 0, s>>>(F, x, done_flag, i0, i1);
+    else if (G == 16) k_lvl_bwd<16><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
     else k_lvl_bwd<32><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
   }
 }
@@ -2774,6 +2783,426 @@ __global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* til
   }
   tl_end(6, tls);
 }
+
+// ---- small supernodes (≤ 16 columns), one WARP per supernode, every load issued before any arithmetic.
+// The 16-lane kernels above (k_lvl_fwd / k_lvl_bwd) load the first 16 rows of L_rows up front and the rest in
+// passes of 16 after the solve: with 40–90 rows per supernode that is 4–6 dependent memory round trips, and
+// the round trips, not the bytes, set the time of a level (c2: 23 µs forward / 30 µs backward per level for
+// 47 MB).  Here lane ↔ row (two passes of 32 rows in registers, further passes looped), the two half-warps
+// split the columns of L_bb⁻¹, and a supernode costs one round trip.
+// LOCAL: accumulators / x of the rows live in a shared-memory frame (subtrees), rows are frame indices.
+constexpr int SNW_P = 2;   // row passes held in registers
+template <bool LOCAL>
+__device__ __forceinline__ void sn16_fwd(const double* __restrict__ L, const double* __restrict__ inv,
+                                         const int32_t* __restrict__ rows, int wk, int noff, double b,
+                                         const double* accp /* this supernode's accumulators (lane & 15) */,
+                                         double* accw /* base for the row updates */, double* xdst) {
+  const int wl = threadIdx.x & 31, i = wl & 15, h = wl >> 4;
+  double a = 0.0;
+  if (i < wk) a = LOCAL ? accp[i] : __ldcg(accp + i);
+  double iv[8];   // half h: L_bb⁻¹(i, j), j = 8h + k
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int j = 8 * h + k;
+    iv[k] = (j < wk && j <= i && i < wk) ? __ldg(inv + j * wk + i) : 0.0;
+  }
+  double lr[SNW_P][16];
+  int32_t rw[SNW_P];
+#pragma unroll
+  for (int p = 0; p < SNW_P; ++p) {
+    const int r = wl + 32 * p;
+    const bool ok = r < noff;
+    rw[p] = ok ? __ldg(rows + r) : 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) lr[p][c] = (ok && c < wk) ? __ldg(L + r + (int64_t)c * noff) : 0.0;
+  }
+  const double v = b - a;
+  double y = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) y += iv[k] * __shfl_sync(0xffffffffu, v, 8 * h + k);
+  y += __shfl_xor_sync(0xffffffffu, y, 16);
+  if (wl < wk) xdst[wl] = y;
+  double yc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) yc[c] = __shfl_sync(0xffffffffu, y, c);
+#pragma unroll
+  for (int p = 0; p < SNW_P; ++p) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) sacc = fma(lr[p][c], yc[c], sacc);
+    if (wl + 32 * p < noff) atomicAdd(accw + rw[p], sacc);
+  }
+  for (int r0 = 32 * SNW_P; r0 < noff; r0 += 32) {
+    const int r = r0 + wl;
+    const bool ok = r < noff;
+    const int32_t g = ok ? __ldg(rows + r) : 0;
+    double s2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) s2 += ((ok && c < wk) ? __ldg(L + r + (int64_t)c * noff) : 0.0) * yc[c];
+    if (ok) atomicAdd(accw + g, s2);
+  }
+}
+template <bool LOCAL>
+__device__ __forceinline__ double sn16_bwd(const double* __restrict__ L, const double* __restrict__ inv,
+                                           const int32_t* __restrict__ rows, int wk, int noff, double yv, double dpiv,
+                                           const double* xr_base) {
+  const int wl = threadIdx.x & 31, i = wl & 15, h = wl >> 4;
+  double ivt[8];   // half h: L_bb⁻¹(j, i), j = 8h + k ≥ i
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int j = 8 * h + k;
+    ivt[k] = (j < wk && j >= i && i < wk) ? __ldg(inv + i * wk + j) : 0.0;
+  }
+  double lr[SNW_P][16];
+  double xr[SNW_P];
+#pragma unroll
+  for (int p = 0; p < SNW_P; ++p) {
+    const int r = wl + 32 * p;
+    const bool ok = r < noff;
+    const int32_t g = ok ? __ldg(rows + r) : 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) lr[p][c] = (ok && c < wk) ? __ldg(L + r + (int64_t)c * noff) : 0.0;
+    xr[p] = ok ? (LOCAL ? xr_base[g] : __ldcg(xr_base + g)) : 0.0;
+  }
+  double t[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    t[c] = 0.0;
+#pragma unroll
+    for (int p = 0; p < SNW_P; ++p) t[c] = fma(lr[p][c], xr[p], t[c]);
+  }
+  for (int r0 = 32 * SNW_P; r0 < noff; r0 += 32) {
+    const int r = r0 + wl;
+    const bool ok = r < noff;
+    const int32_t g = ok ? __ldg(rows + r) : 0;
+    const double xv = ok ? (LOCAL ? xr_base[g] : __ldcg(xr_base + g)) : 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) t[c] += ((ok && c < wk) ? __ldg(L + r + (int64_t)c * noff) : 0.0) * xv;
+  }
+  // 16 column sums over 32 lanes: halves added, then the transpose-reduce inside each half
+#pragma unroll
+  for (int c = 0; c < 16; ++c) t[c] += __shfl_xor_sync(0xffffffffu, t[c], 16);
+  const double tc = group_treduce<16>(t, i, 0xffffffffu);
+  const double rhs = i < wk ? yv / dpiv - tc : 0.0;
+  double xi = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) xi += ivt[k] * __shfl_sync(0xffffffffu, rhs, 8 * h + k);
+  xi += __shfl_xor_sync(0xffffffffu, xi, 16);
+  return xi;   // x_i in lanes i and i + 16
+}
+// One level of the leaf phase, warp per supernode (levels whose supernodes have ≤ 16 columns).
+__global__ void __launch_bounds__(NT, 2) k_lvl16_fwd(DevFactor F, SweepRhs R, double* x, int64_t i0, int64_t i1) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const unsigned tls = tl_begin(8);
+  const int64_t i = i0 + ((int64_t)blockIdx.x * NT + threadIdx.x) / 32;
+  if (i < i1) {
+    const int4 d0 = __ldg(F.lvl_desc + 2 * i), d1 = __ldg(F.lvl_desc + 2 * i + 1);
+    const double* L = F.fstore + ((int64_t)(uint32_t)d0.x | ((int64_t)d0.y << 32));
+    const double* inv = F.fstore + ((int64_t)(uint32_t)d0.z | ((int64_t)d0.w << 32));
+    const int32_t* rows = F.sn_rows + ((int64_t)(uint32_t)d1.x | ((int64_t)d1.y << 32));
+    const int64_t c0 = d1.z;
+    const int wk = d1.w & 63, noff = (int)((unsigned)d1.w >> 6);
+    const int li = threadIdx.x & 15;
+    double b = 0.0;
+    if (li < wk) {
+      const int64_t c = c0 + li;
+      if (R.ct.p != nullptr) b = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+      else b = R.rhs[R.in_perm ? R.in_perm[c] : c];
+    }
+    sn16_fwd<false>(L, inv, rows, wk, noff, b, F.acc + c0, F.acc, x + c0);
+    __syncwarp();
+    if ((threadIdx.x & 31) < wk) F.acc[c0 + (threadIdx.x & 31)] = 0.0;
+  }
+  tl_end(8, tls);
+}
+__global__ void __launch_bounds__(NT, 2) k_lvl16_bwd(DevFactor F, double* x, const int* done_flag, int64_t i0,
+                                                     int64_t i1) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(9);
+  const int64_t i = i0 + ((int64_t)blockIdx.x * NT + threadIdx.x) / 32;
+  if (i < i1) {
+    const int4 d0 = __ldg(F.lvl_desc + 2 * i), d1 = __ldg(F.lvl_desc + 2 * i + 1);
+    const double* L = F.fstore + ((int64_t)(uint32_t)d0.x | ((int64_t)d0.y << 32));
+    const double* inv = F.fstore + ((int64_t)(uint32_t)d0.z | ((int64_t)d0.w << 32));
+    const int32_t* rows = F.sn_rows + ((int64_t)(uint32_t)d1.x | ((int64_t)d1.y << 32));
+    const int64_t c0 = d1.z;
+    const int wk = d1.w & 63, noff = (int)((unsigned)d1.w >> 6);
+    const int li = threadIdx.x & 15;
+    double yv = 0.0, dp = 1.0;
+    if (li < wk) {
+      yv = __ldcg(x + c0 + li);
+      dp = __ldg(F.Dpiv + c0 + li);
+    }
+    const double xi = sn16_bwd<false>(L, inv, rows, wk, noff, yv, dp, x);
+    if ((threadIdx.x & 31) < wk) x[c0 + (threadIdx.x & 31)] = xi;
+  }
+  tl_end(9, tls);
+}
+
+// ---- subtrees: one WARP per subtree (StHdr), groups of G lanes per supernode, the frame in shared memory.
+// A CTA-wide version (a CTA per subtree, __syncthreads between local levels) left most of its threads idle
+// above the subtree's leaves and took 37 µs per subtree (c2: 357 µs forward against 163 µs for the level
+// kernels); with a warp per subtree nearly every subtree is resident at once and the per-subtree latency
+// overlaps across warps.
+constexpr int ST_WPB = NT / 32;   // subtrees per CTA
+template <int G>
+__global__ void __launch_bounds__(NT, G == 16 ? 3 : 2) k_st_fwd(DevFactor F, SweepRhs R, PiSweep P, double* x) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const unsigned tls = tl_begin(8);
+  __shared__ double frs[ST_WPB][ST_FRAME];
+  __shared__ int4 sds[ST_WPB][2 * ST_MAXSN];
+  const int tid = threadIdx.x, wl = tid & 31, wid = tid >> 5;
+  const int64_t t = (int64_t)blockIdx.x * ST_WPB + wid;
+  if (t < P.st_n) {
+    double* fr = frs[wid];
+    const StHdr* hp = P.st_hdr + t;
+    const int d0 = __ldg(&hp->d0), nlev = __ldg(&hp->nlev), c_lo = __ldg(&hp->c_lo), ncols = __ldg(&hp->ncols);
+    const int next = __ldg(&hp->next), lp = __ldg(&hp->lptr), fslen = __ldg(&hp->fslen);
+    const int64_t fslo = __ldg(&hp->fslo);
+    for (int64_t e = (int64_t)wl * 16; e < fslen; e += 32 * 16) prefetch_l2(F.fstore + fslo + e);
+    // the subtree's descriptors and level pointers staged once (one round trip instead of one per supernode)
+    int4* sd = sds[wid];
+    const int lpv = wl <= nlev ? __ldg(P.st_lptr + lp + wl) : 0;
+    const int nsn = __shfl_sync(0xffffffffu, lpv, nlev);
+    for (int i = wl; i < 2 * nsn; i += 32) sd[i] = __ldg(P.st_desc + 2 * (int64_t)d0 + i);
+    for (int i = wl; i < ncols + next; i += 32) fr[i] = 0.0;
+    __syncwarp();
+    {
+      const int4 f1 = sd[1], l1 = sd[2 * nsn - 1];
+      const int64_t lo0 = (int64_t)(uint32_t)f1.x | ((int64_t)f1.y << 32);
+      const int64_t lo1 = ((int64_t)(uint32_t)l1.x | ((int64_t)l1.y << 32)) + (int64_t)((unsigned)l1.w >> 6);
+      for (int64_t e = lo0 + (int64_t)wl * 32; e < lo1; e += 32 * 32) prefetch_l2(P.st_loc + e);
+    }
+    const unsigned gm = lvl_mask<G>();
+    const int lane = tid & (G - 1), grp = wl / G;
+    for (int l = 0; l < nlev; ++l) {
+      const int i0 = __shfl_sync(0xffffffffu, lpv, l), i1 = __shfl_sync(0xffffffffu, lpv, l + 1);
+      for (int i = i0 + grp; i < i1; i += 32 / G) {
+        const int4 a0 = sd[2 * i], a1 = sd[2 * i + 1];
+        const double* L = F.fstore + ((int64_t)(uint32_t)a0.x | ((int64_t)a0.y << 32));
+        const double* inv = F.fstore + ((int64_t)(uint32_t)a0.z | ((int64_t)a0.w << 32));
+        const int32_t* loc = P.st_loc + ((int64_t)(uint32_t)a1.x | ((int64_t)a1.y << 32));
+        const int c0 = a1.z;
+        const int wk = a1.w & 63, noff = (int)((unsigned)a1.w >> 6);
+        double v = 0.0;
+        if (lane < wk) {
+          const int64_t c = (int64_t)c0 + lane;
+          if (R.ct.p != nullptr) v = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+          else v = R.rhs[R.in_perm ? R.in_perm[c] : c];
+        }
+        double iv[G];   // lane i: L_bb⁻¹(i, j) = inv[j·wk + i], j ≤ i
+#pragma unroll
+        for (int j = 0; j < G; ++j) iv[j] = (j < wk && j <= lane && lane < wk) ? __ldg(inv + j * wk + lane) : 0.0;
+        const bool rok = lane < noff;
+        const int32_t row = rok ? __ldg(loc + lane) : 0;
+        double lr[G];   // lane r: L(r, c)
+#pragma unroll
+        for (int c = 0; c < G; ++c) lr[c] = (c < wk && rok) ? __ldg(L + lane + (int64_t)c * noff) : 0.0;
+        if (lane < wk) v -= fr[c0 - c_lo + lane];
+        double y = 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) y += iv[j] * __shfl_sync(gm, v, j, G);
+        if (lane < wk) x[c0 + lane] = y;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < G; ++c) s += lr[c] * __shfl_sync(gm, y, c, G);
+        if (rok) atomicAdd(fr + row, s);
+        for (int r0 = G; r0 < noff; r0 += G) {
+          const int r = r0 + lane;
+          const bool ok = r < noff;
+          const int32_t rw = ok ? __ldg(loc + r) : 0;
+          double s2 = 0.0;
+#pragma unroll
+          for (int c = 0; c < G; ++c) {
+            const double lv = (c < wk && ok) ? __ldg(L + r + (int64_t)c * noff) : 0.0;
+            s2 += lv * __shfl_sync(gm, y, c, G);
+          }
+          if (ok) atomicAdd(fr + rw, s2);
+        }
+      }
+      __syncwarp();
+    }
+    const int32_t* rr = F.sn_rows + __ldg(&hp->rootrows);
+    for (int e = wl; e < next; e += 32) atomicAdd(F.acc + __ldg(rr + e), fr[ncols + e]);
+  }
+  tl_end(8, tls);
+}
+template <int G>
+__global__ void __launch_bounds__(NT, G == 16 ? 3 : 2) k_st_bwd(DevFactor F, PiSweep P, double* x, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(9);
+  __shared__ double frs[ST_WPB][ST_FRAME];
+  __shared__ int4 sds[ST_WPB][2 * ST_MAXSN];
+  const int tid = threadIdx.x, wl = tid & 31, wid = tid >> 5;
+  const int64_t t = (int64_t)blockIdx.x * ST_WPB + wid;
+  if (t < P.st_n) {
+    double* fr = frs[wid];
+    const StHdr* hp = P.st_hdr + t;
+    const int d0 = __ldg(&hp->d0), nlev = __ldg(&hp->nlev), c_lo = __ldg(&hp->c_lo), ncols = __ldg(&hp->ncols);
+    const int next = __ldg(&hp->next), lp = __ldg(&hp->lptr), fslen = __ldg(&hp->fslen);
+    const int64_t fslo = __ldg(&hp->fslo);
+    for (int64_t e = (int64_t)wl * 16; e < fslen; e += 32 * 16) prefetch_l2(F.fstore + fslo + e);
+    int4* sd = sds[wid];
+    const int lpv = wl <= nlev ? __ldg(P.st_lptr + lp + wl) : 0;
+    const int nsn = __shfl_sync(0xffffffffu, lpv, nlev);
+    for (int i = wl; i < 2 * nsn; i += 32) sd[i] = __ldg(P.st_desc + 2 * (int64_t)d0 + i);
+    const int32_t* rr = F.sn_rows + __ldg(&hp->rootrows);
+    for (int e = wl; e < next; e += 32) fr[ncols + e] = __ldcg(x + __ldg(rr + e));
+    __syncwarp();
+    {
+      const int4 f1 = sd[1], l1 = sd[2 * nsn - 1];
+      const int64_t lo0 = (int64_t)(uint32_t)f1.x | ((int64_t)f1.y << 32);
+      const int64_t lo1 = ((int64_t)(uint32_t)l1.x | ((int64_t)l1.y << 32)) + (int64_t)((unsigned)l1.w >> 6);
+      for (int64_t e = lo0 + (int64_t)wl * 32; e < lo1; e += 32 * 32) prefetch_l2(P.st_loc + e);
+    }
+    const unsigned gm = lvl_mask<G>();
+    const int lane = tid & (G - 1), grp = wl / G;
+    for (int l = nlev - 1; l >= 0; --l) {
+      const int i0 = __shfl_sync(0xffffffffu, lpv, l), i1 = __shfl_sync(0xffffffffu, lpv, l + 1);
+      for (int i = i0 + grp; i < i1; i += 32 / G) {
+        const int4 a0 = sd[2 * i], a1 = sd[2 * i + 1];
+        const double* L = F.fstore + ((int64_t)(uint32_t)a0.x | ((int64_t)a0.y << 32));
+        const double* inv = F.fstore + ((int64_t)(uint32_t)a0.z | ((int64_t)a0.w << 32));
+        const int32_t* loc = P.st_loc + ((int64_t)(uint32_t)a1.x | ((int64_t)a1.y << 32));
+        const int c0 = a1.z;
+        const int wk = a1.w & 63, noff = (int)((unsigned)a1.w >> 6);
+        double yv = 0.0, dinv = 0.0;
+        if (lane < wk) {
+          yv = __ldcg(x + c0 + lane);
+          dinv = 1.0 / __ldg(F.Dpiv + c0 + lane);
+        }
+        double ivt[G];   // lane i: L_bb⁻¹(j, i) = inv[i·wk + j], j ≥ i
+#pragma unroll
+        for (int j = 0; j < G; ++j) ivt[j] = (j < wk && j >= lane && lane < wk) ? __ldg(inv + lane * wk + j) : 0.0;
+        double tt[G];
+#pragma unroll
+        for (int c = 0; c < G; ++c) tt[c] = 0.0;
+        for (int r0 = 0; r0 < noff; r0 += G) {
+          const int r = r0 + lane;
+          const bool ok = r < noff;
+          const double xr = ok ? fr[__ldg(loc + r)] : 0.0;
+#pragma unroll
+          for (int c = 0; c < G; ++c) tt[c] += ((c < wk && ok) ? __ldg(L + r + (int64_t)c * noff) : 0.0) * xr;
+        }
+        const double tc = group_treduce<G>(tt, lane, gm);
+        const double rhs = lane < wk ? yv * dinv - tc : 0.0;
+        double xi = 0.0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) xi += ivt[j] * __shfl_sync(gm, rhs, j, G);
+        if (lane < wk) {
+          x[c0 + lane] = xi;
+          fr[c0 - c_lo + lane] = xi;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  tl_end(9, tls);
+}
+// Subtrees of ≤ 16-column supernodes: a warp per subtree, the whole warp on one supernode at a time
+// (sn16_fwd / sn16_bwd: one round trip per supernode, served by L2 after the subtree's prefetch).
+__global__ void __launch_bounds__(NT, 2) k_st16_fwd(DevFactor F, SweepRhs R, PiSweep P, double* x) {
+  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+  const unsigned tls = tl_begin(8);
+  __shared__ double frs[ST_WPB][ST_FRAME];
+  __shared__ int4 sds[ST_WPB][2 * ST_MAXSN];
+  const int tid = threadIdx.x, wl = tid & 31, wid = tid >> 5;
+  const int64_t t = (int64_t)blockIdx.x * ST_WPB + wid;
+  if (t < P.st_n) {
+    double* fr = frs[wid];
+    const StHdr* hp = P.st_hdr + t;
+    const int d0 = __ldg(&hp->d0), nlev = __ldg(&hp->nlev), c_lo = __ldg(&hp->c_lo), ncols = __ldg(&hp->ncols);
+    const int next = __ldg(&hp->next), lp = __ldg(&hp->lptr), fslen = __ldg(&hp->fslen);
+    const int64_t fslo = __ldg(&hp->fslo);
+    for (int64_t e = (int64_t)wl * 16; e < fslen; e += 32 * 16) prefetch_l2(F.fstore + fslo + e);
+    int4* sd = sds[wid];
+    const int lpv = wl <= nlev ? __ldg(P.st_lptr + lp + wl) : 0;
+    const int nsn = __shfl_sync(0xffffffffu, lpv, nlev);
+    for (int i = wl; i < 2 * nsn; i += 32) sd[i] = __ldg(P.st_desc + 2 * (int64_t)d0 + i);
+    for (int i = wl; i < ncols + next; i += 32) fr[i] = 0.0;
+    __syncwarp();
+    {
+      const int4 f1 = sd[1], l1 = sd[2 * nsn - 1];
+      const int64_t lo0 = (int64_t)(uint32_t)f1.x | ((int64_t)f1.y << 32);
+      const int64_t lo1 = ((int64_t)(uint32_t)l1.x | ((int64_t)l1.y << 32)) + (int64_t)((unsigned)l1.w >> 6);
+      for (int64_t e = lo0 + (int64_t)wl * 32; e < lo1; e += 32 * 32) prefetch_l2(P.st_loc + e);
+    }
+    for (int l = 0; l < nlev; ++l) {
+      const int i0 = __shfl_sync(0xffffffffu, lpv, l), i1 = __shfl_sync(0xffffffffu, lpv, l + 1);
+      for (int i = i0; i < i1; ++i) {
+        const int4 a0 = sd[2 * i], a1 = sd[2 * i + 1];
+        const double* L = F.fstore + ((int64_t)(uint32_t)a0.x | ((int64_t)a0.y << 32));
+        const double* inv = F.fstore + ((int64_t)(uint32_t)a0.z | ((int64_t)a0.w << 32));
+        const int32_t* loc = P.st_loc + ((int64_t)(uint32_t)a1.x | ((int64_t)a1.y << 32));
+        const int c0 = a1.z;
+        const int wk = a1.w & 63, noff = (int)((unsigned)a1.w >> 6);
+        double b = 0.0;
+        if ((wl & 15) < wk) {
+          const int64_t c = (int64_t)c0 + (wl & 15);
+          if (R.ct.p != nullptr) b = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+          else b = R.rhs[R.in_perm ? R.in_perm[c] : c];
+        }
+        sn16_fwd<true>(L, inv, loc, wk, noff, b, fr + (c0 - c_lo), fr, x + c0);
+      }
+      __syncwarp();
+    }
+    const int32_t* rr = F.sn_rows + __ldg(&hp->rootrows);
+    for (int e = wl; e < next; e += 32) atomicAdd(F.acc + __ldg(rr + e), fr[ncols + e]);
+  }
+  tl_end(8, tls);
+}
+__global__ void __launch_bounds__(NT, 2) k_st16_bwd(DevFactor F, PiSweep P, double* x, const int* done_flag) {
+  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+  const unsigned tls = tl_begin(9);
+  __shared__ double frs[ST_WPB][ST_FRAME];
+  __shared__ int4 sds[ST_WPB][2 * ST_MAXSN];
+  const int tid = threadIdx.x, wl = tid & 31, wid = tid >> 5;
+  const int64_t t = (int64_t)blockIdx.x * ST_WPB + wid;
+  if (t < P.st_n) {
+    double* fr = frs[wid];
+    const StHdr* hp = P.st_hdr + t;
+    const int d0 = __ldg(&hp->d0), nlev = __ldg(&hp->nlev), c_lo = __ldg(&hp->c_lo), ncols = __ldg(&hp->ncols);
+    const int next = __ldg(&hp->next), lp = __ldg(&hp->lptr), fslen = __ldg(&hp->fslen);
+    const int64_t fslo = __ldg(&hp->fslo);
+    for (int64_t e = (int64_t)wl * 16; e < fslen; e += 32 * 16) prefetch_l2(F.fstore + fslo + e);
+    int4* sd = sds[wid];
+    const int lpv = wl <= nlev ? __ldg(P.st_lptr + lp + wl) : 0;
+    const int nsn = __shfl_sync(0xffffffffu, lpv, nlev);
+    for (int i = wl; i < 2 * nsn; i += 32) sd[i] = __ldg(P.st_desc + 2 * (int64_t)d0 + i);
+    const int32_t* rr = F.sn_rows + __ldg(&hp->rootrows);
+    for (int e = wl; e < next; e += 32) fr[ncols + e] = __ldcg(x + __ldg(rr + e));
+    __syncwarp();
+    {
+      const int4 f1 = sd[1], l1 = sd[2 * nsn - 1];
+      const int64_t lo0 = (int64_t)(uint32_t)f1.x | ((int64_t)f1.y << 32);
+      const int64_t lo1 = ((int64_t)(uint32_t)l1.x | ((int64_t)l1.y << 32)) + (int64_t)((unsigned)l1.w >> 6);
+      for (int64_t e = lo0 + (int64_t)wl * 32; e < lo1; e += 32 * 32) prefetch_l2(P.st_loc + e);
+    }
+    for (int l = nlev - 1; l >= 0; --l) {
+      const int i0 = __shfl_sync(0xffffffffu, lpv, l), i1 = __shfl_sync(0xffffffffu, lpv, l + 1);
+      for (int i = i0; i < i1; ++i) {
+        const int4 a0 = sd[2 * i], a1 = sd[2 * i + 1];
+        const double* L = F.fstore + ((int64_t)(uint32_t)a0.x | ((int64_t)a0.y << 32));
+        const double* inv = F.fstore + ((int64_t)(uint32_t)a0.z | ((int64_t)a0.w << 32));
+        const int32_t* loc = P.st_loc + ((int64_t)(uint32_t)a1.x | ((int64_t)a1.y << 32));
+        const int c0 = a1.z;
+        const int wk = a1.w & 63, noff = (int)((unsigned)a1.w >> 6);
+        double yv = 0.0, dp = 1.0;
+        if ((wl & 15) < wk) {
+          yv = __ldcg(x + c0 + (wl & 15));
+          dp = __ldg(F.Dpiv + c0 + (wl & 15));
+        }
+        const double xi = sn16_bwd<true>(L, inv, loc, wk, noff, yv, dp, fr);
+        if (wl < wk) {
+          x[c0 + wl] = xi;
+          fr[c0 - c_lo + wl] = xi;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  tl_end(9, tls);
+}
 void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaStream_t s) {
   const int64_t nt = P.lev_ptr[P.nlev];
   if (nt <= 0) return;
@@ -2783,11 +3212,17 @@ void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaSt
 }
 void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
   k_pi_init<<<sms * 4, NT, 0, s>>>(F, r, x, P.root0);
-  for (int L = 0; L < F.lvl_cut; ++L) {   // leaf phase, bottom level first
+  if (P.st_n > 0) {
+    if (P.st_g == 16 && lvl16_on()) k_st16_fwd<<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
+    else if (P.st_g == 16) k_st_fwd<16><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
+    else k_st_fwd<32><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
+  }
+  for (int L = 0; P.st_n == 0 && L < F.lvl_cut; ++L) {   // leaf phase, bottom level first
     const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
     const int G = F.lvl_g_h[L];
     const int g = (int)((i1 - i0) * G + NT - 1) / NT;
-    if (G == 16) k_lvl_fwd<16><<<g, NT, 0, s>>>(F, r, x, i0, i1);
+    if (G == 16 && lvl16_on()) k_lvl16_fwd<<<(unsigned)(((i1 - i0) * 32 + NT - 1) / NT), NT, 0, s>>>(F, r, x, i0, i1);
+    else if (G == 16) k_lvl_fwd<16><<<g, NT, 0, s>>>(F, r, x, i0, i1);
     else k_lvl_fwd<32><<<g, NT, 0, s>>>(F, r, x, i0, i1);
   }
   for (int L = 0; L < P.nlev; ++L) {
@@ -2800,11 +3235,17 @@ void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* don
     const int64_t n = P.lev_ptr[L + 1] - P.lev_ptr[L];
     if (n > 0) k_pi_bwd<<<(unsigned)n, NT, 0, s>>>(F, P.tiles + P.lev_ptr[L], P.Z, x, done_flag);
   }
-  for (int L = F.lvl_cut - 1; L >= 0; --L) {   // leaf phase, top level first
+  if (P.st_n > 0) {
+    if (P.st_g == 16 && lvl16_on()) k_st16_bwd<<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);
+    else if (P.st_g == 16) k_st_bwd<16><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);
+    else k_st_bwd<32><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);
+  }
+  for (int L = P.st_n > 0 ? -1 : F.lvl_cut - 1; L >= 0; --L) {   // leaf phase, top level first
     const int64_t i0 = F.lvl_ptr_h[L], i1 = F.lvl_ptr_h[L + 1];
     const int G = F.lvl_g_h[L];
     const int g = (int)((i1 - i0) * G + NT - 1) / NT;
-    if (G == 16) k_lvl_bwd<16><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
+    if (G == 16 && lvl16_on()) k_lvl16_bwd<<<(unsigned)(((i1 - i0) * 32 + NT - 1) / NT), NT, 0, s>>>(F, x, done_flag, i0, i1);
+    else if (G == 16) k_lvl_bwd<16><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
     else k_lvl_bwd<32><<<g, NT, 0, s>>>(F, x, done_flag, i0, i1);
   }
 }

@@ -273,6 +273,24 @@ struct PiTile {          // 32 bytes, read as two int4
   int16_t pad;
 };
 constexpr int PI_MAXLEV = 64;
+// Subtrees (below the level products): a maximal subtree of small supernodes whose factor entries fit a byte
+// budget is swept by ONE WARP, bottom-up (forward) / top-down (backward) with the subtree's part of the
+// vector in shared memory — __syncwarp between its local levels replaces kernel boundaries, updates
+// inside the subtree never touch global memory, and its rows above the subtree (all contained in the root's
+// row list) are flushed / gathered once.  The subtree's factor entries are one contiguous range of fstore
+// (postorder), prefetched into L2 when the CTA starts.
+constexpr int ST_FRAME = 512;
+constexpr int ST_MAXSN = 48;    // most supernodes of a subtree (its descriptors are staged in shared memory); local levels ≤ 31   // most doubles of a subtree's frame (its columns + the root's external rows)
+struct StHdr {           // 48 bytes
+  int32_t d0;            // first descriptor (st_desc, 2 × int4 each, local-level order)
+  int32_t nlev;          // local levels
+  int32_t c_lo, ncols;   // the subtree's columns [c_lo, c_lo + ncols)
+  int32_t next;          // external rows of the subtree's root
+  int32_t lptr;          // st_lptr[lptr .. lptr + nlev]: descriptor ranges of the local levels (relative to d0)
+  int64_t rootrows;      // offset into sn_rows of the root's external rows
+  int64_t fslo;          // the subtree's entries: fstore[fslo, fslo + fslen)
+  int32_t fslen, pad;
+};
 struct PiSweep {
   int enabled = 0;
   int nlev = 0;                        // levels lvl_cut … top−1 (the symmetric root excluded)
@@ -282,6 +300,13 @@ struct PiSweep {
   int64_t z_size = 0;
   int64_t root0 = 0;                   // first column of the symmetric root
   int64_t lev_ptr[PI_MAXLEV + 1] = {0};
+  // subtrees (st_n = 0: the leaf phase's level kernels run instead)
+  int64_t st_n = 0;
+  int st_g = 16;                       // lanes per supernode (16: every subtree supernode has ≤ 16 columns)
+  const StHdr* st_hdr = nullptr;
+  const int4* st_desc = nullptr;       // as DevFactor::lvl_desc, the row-list offset pointing into st_loc
+  const int32_t* st_lptr = nullptr;
+  const int32_t* st_loc = nullptr;     // per off-diagonal row of a subtree supernode: its index in the frame
 };
 // Z from the factor storage (after the numeric factorization and the X_J inverses); zoffJ: per supernode offset of Z_J (device)
 void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaStream_t s);

@@ -44,3 +44,11 @@ out = {NAMES[k]: {"n": cnt[k], "dur_us": round(dur[k] / cnt[k], 2), "gap_before_
 print(json.dumps({"config": name, "us_per_iteration": round(per_it, 2), "kernels": out}))
 if os.environ.get('TL_SERIES'):
     print('gemv series', [round((e - s0) / 1e3, 1) for k, s0, e in ev if k == 2])
+if _st.get('pi_enabled'):
+    # level products: per-level durations (launch order within a sweep), averaged over the recorded sweeps
+    for kk, nm in ((5, 'level fwd'), (6, 'level bwd'), (8, 'leaf fwd'), (9, 'leaf bwd')):
+        e = [(s0, e0) for k, s0, e0 in ev if k == kk]
+        nl = max(1, round(len(e) / max(1, cnt[2])))
+        e = e[:len(e) // nl * nl]
+        d = np.array([(b - a) / 1e3 for a, b in e]).reshape(-1, nl)
+        print(nm, 'levels per sweep', nl, 'us per level', d.mean(0).round(1).tolist(), 'sum', round(float(d.mean(0).sum()), 1))

@@ -39,7 +39,7 @@ rng = np.random.default_rng(8)
 D = rng.uniform(0.5, 2.0, qp.m2)
 b = rng.standard_normal(qp.m2)
 out = {"dense_w": st["dense_w_enabled"], "flat": st["flat_enabled"], "pi": st["pi_enabled"],
-       "pi_levels": st["pi_levels"], "lvl": st["lvl_levels_F"], "xs": {}}
+       "pi_levels": st["pi_levels"], "lvl": st["lvl_levels_F"], "st": st["pi_subtrees"], "xs": {}}
 if len(sys.argv) > 4 and sys.argv[4] == 'fsolve':
     f = np.random.default_rng(12).standard_normal(qp.n + qp.m1)
     out["fsolve"] = np.concatenate(s.f_solve(f)).tolist()
@@ -121,22 +121,27 @@ def test_path_variant_matches_oracle(oracle_case, variant):
 PI_ENV = {"QPB_PI_MINN": "0", "QPB_DENSE_FINV": "0", "QPB_DENSE_W": "0", "QPB_FLAT": "0"}
 
 
-@pytest.mark.parametrize("variant", ["leaf_phase", "all_levels", "off"])
+@pytest.mark.parametrize("variant", ["subtrees", "subtrees32", "leaf_phase", "all_levels", "off"])
 def test_level_products_match_oracle(variant):
     """Level products (Z_J = [L_JJ⁻¹; L_ext L_JJ⁻¹], one kernel per elimination-tree level) on a
     grid QP small enough for the dense oracle: the F-solve and the P_L PCG iterates against the oracle with
-    (a) the leaf phase below them, (b) every level swept as a product, (c) switched off (the task graph)."""
+    (a) subtrees swept by one CTA each below them (16 and 32 lanes per supernode), (b) the leaf phase below
+    them, (c) every level swept as a product, (d) switched off (the task graph)."""
     expr = "qpgen.make_grid_qp(48, 80, 200, seed=9, name='grid48')"
     qp = eval(expr)
     env = dict(PI_ENV)
-    env.update({"leaf_phase": {"QPB_LVL_MIN": "16"}, "all_levels": {"QPB_LVL": "0"}, "off": {"QPB_PI": "0"}}[variant])
+    env.update({"subtrees": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8"},
+                "subtrees32": {"QPB_ST_MIN": "1", "QPB_ST_KB": "40"},
+                "leaf_phase": {"QPB_LVL_MIN": "16", "QPB_ST": "0"}, "all_levels": {"QPB_LVL": "0", "QPB_ST": "0"},
+                "off": {"QPB_PI": "0"}}[variant])
     out = run_child(expr, env, False, extra=("fsolve",))
     assert out["dense_w"] == 0.0 and out["flat"] == 0.0
     if variant == "off":
         assert out["pi"] == 0.0
     else:
         assert out["pi"] == 1.0 and out["pi_levels"] >= 2
-        assert (out["lvl"] > 0) == (variant == "leaf_phase")
+        assert (out["lvl"] > 0) == (variant == "leaf_phase") or variant.startswith("subtrees")
+        assert (out["st"] > 0) == variant.startswith("subtrees")
     fs = DenseF(qp.H, qp.A)
     f = np.random.default_rng(12).standard_normal(qp.n + qp.m1)
     yr = np.concatenate(fs.solve(f[:qp.n], f[qp.n:]))
