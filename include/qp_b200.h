@@ -255,7 +255,9 @@ typedef struct {
                                         (Z_J = [L_JJ⁻¹; L_ext,J L_JJ⁻¹], one kernel per level) */
   double pi_discrepancy;             /* their factor-time guard against the task-graph sweeps (−1: not built) */
   double pi_levels;                  /* levels swept that way */
-  double pi_subtrees;                /* subtrees below them swept by one CTA each (0: the leaf phase instead) */
+  double pi_subtrees;                /* subtrees below them swept by one warp each (0: the leaf phase instead) */
+  double pi_fsolve_ms, sweep_fsolve_ms; /* factor-time medians of one F-solve through the level products / the
+                                        task-graph sweeps: the faster path is kept (0: not timed) */
 } qp_stats;
 int qp_get_stats(qp_ctx* ctx, qp_stats* s);
 

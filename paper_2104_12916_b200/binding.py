@@ -75,7 +75,7 @@ class _Stats(C.Structure):
                                           "dense_w_discrepancy", "kf_bytes_W", "dense_finv_enabled",
                                           "dense_finv_discrepancy", "lvl_levels_F", "lvl_levels_PH",
                                           "lvl_supernodes_F", "lvl_supernodes_PH", "pi_enabled", "pi_discrepancy",
-                                          "pi_levels", "pi_subtrees")]
+                                          "pi_levels", "pi_subtrees", "pi_fsolve_ms", "sweep_fsolve_ms")]
 
 
 _LIB = None

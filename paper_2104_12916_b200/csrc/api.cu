@@ -237,6 +237,7 @@ struct Factor {
   double flat_discrepancy = -1.0;  // ‖y_flat − y_sweep‖ / ‖y_sweep‖ at factor time (−1: not tried)
   PiSweep pi{};                    // level products (partitioned inverse by levels)
   double pi_discrepancy = -1.0;    // ‖y_levels − y_sweeps‖ / ‖y_sweeps‖ at factor time (−1: not tried)
+  double pi_ms[2] = {0, 0};        // factor-time F-solve medians: [0] task graph, [1] level products
   const int32_t* fwd_sym = nullptr;
   const int32_t* bwd_sym = nullptr;
   int64_t n_fwd_sym = 0, n_bwd_sym = 0, n_fwd_x = 0, n_bwd_x = 0;
@@ -1802,39 +1803,70 @@ int build_pi(qp_ctx* c) {
   std::vector<int32_t> tile_J;
   int64_t zs = 0;
   F.pi.lev_ptr[0] = 0;
-  for (int L = 0; L < nlev; ++L) {
-    std::vector<std::pair<PiTile, int32_t>> lt;
-    for (int32_t J : by[L]) {
-      const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
-      const int64_t ld = (m + 1) & ~int64_t(1);
-      if (ld > INT32_MAX) return QP_OK;
-      zoffJ[J] = zs;
-      for (int64_t c0 = 0; c0 < w; c0 += 64) {
-        const int64_t nc = std::min<int64_t>(64, w - c0);
-        for (int64_t r0 = c0; r0 < m; r0 += 512) {
-          const int64_t nr = std::min<int64_t>(512, m - r0);
-          PiTile t{};
-          t.zoff = zs + r0 + c0 * ld;
-          t.roff = S.sn_rowptr[J] + r0;
-          t.ld = (int32_t)ld;
-          t.col0 = (int32_t)(S.sn_start[J] + c0);
-          t.nr = (int16_t)nr;
-          t.nc = (int16_t)nc;
-          t.wx = (int16_t)std::max<int64_t>(0, std::min<int64_t>(nr, w - r0));
-          lt.push_back({t, J});
+  // Tile shapes: a supernode with ≤ `short` rows is cut into strips of 64 rows (a warp each, 8 per CTA); taller
+  // ones into CTA tiles of 512 rows × 64 columns.  The backward product takes strips up to 640 rows (a CTA
+  // tile there first gathers its 512 inputs, then streams), the forward product up to 320 (measured on c2).
+  // QPB_PI_NC < 64 narrows the CTA tiles (measured slower: more tiles re-gather their inputs).
+  const int64_t short_f = std::getenv("QPB_PI_SHORT") ? std::atoll(std::getenv("QPB_PI_SHORT")) : 320;
+  const int64_t short_b = std::getenv("QPB_PI_SHORT_B") ? std::atoll(std::getenv("QPB_PI_SHORT_B")) : 640;
+  const int64_t ncw = std::getenv("QPB_PI_NC") ? std::max<int64_t>(16, std::min<int64_t>(64, std::atoll(std::getenv("QPB_PI_NC")))) : 64;
+  std::vector<PiTile> btiles;
+  bool too_big = false;
+  auto plan = [&](int64_t pi_short, std::vector<PiTile>& out, std::vector<int32_t>* outJ, int64_t* ptr, int64_t* sptr,
+                  bool set_z) {
+    int64_t z = 0;
+    ptr[0] = 0;
+    for (int L = 0; L < nlev; ++L) {
+      std::vector<std::pair<PiTile, int32_t>> lt, ls;
+      for (int32_t J : by[L]) {
+        const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+        const int64_t ld = (m + 1) & ~int64_t(1);
+        if (ld > INT32_MAX) too_big = true;
+        if (set_z) zoffJ[J] = z;
+        const bool strip = m <= pi_short;
+        const int64_t cw = strip ? 64 : ncw, rh = strip ? 64 : 512;
+        for (int64_t c0 = 0; c0 < w; c0 += cw) {
+          const int64_t nc = std::min<int64_t>(cw, w - c0);
+          for (int64_t r0 = c0 & ~int64_t(63); r0 < m; r0 += rh) {   // rows above the diagonal block are zero
+            const int64_t nr = std::min<int64_t>(rh, m - r0);
+            PiTile t{};
+            t.zoff = z + r0 + c0 * ld;
+            t.roff = S.sn_rowptr[J] + r0;
+            t.ld = (int32_t)ld;
+            t.col0 = (int32_t)(S.sn_start[J] + c0);
+            t.nr = (int16_t)nr;
+            t.nc = (int16_t)nc;
+            t.wx = (int16_t)std::max<int64_t>(0, std::min<int64_t>(nr, w - r0));
+            (strip ? ls : lt).push_back({t, J});
+          }
         }
+        z += ld * w;
       }
-      zs += ld * w;
+      auto bigger = [](const std::pair<PiTile, int32_t>& a, const std::pair<PiTile, int32_t>& b) {
+        return (int)a.first.nr * a.first.nc > (int)b.first.nr * b.first.nc;
+      };
+      std::stable_sort(lt.begin(), lt.end(), bigger);
+      std::stable_sort(ls.begin(), ls.end(), bigger);
+      for (auto& q : lt) {
+        out.push_back(q.first);
+        if (outJ) outJ->push_back(q.second);
+      }
+      sptr[L] = (int64_t)out.size();
+      for (auto& q : ls) {
+        out.push_back(q.first);
+        if (outJ) outJ->push_back(q.second);
+      }
+      ptr[L + 1] = (int64_t)out.size();
     }
-    std::stable_sort(lt.begin(), lt.end(), [](const std::pair<PiTile, int32_t>& a, const std::pair<PiTile, int32_t>& b) {
-      return (int)a.first.nr * a.first.nc > (int)b.first.nr * b.first.nc;
-    });
-    for (auto& q : lt) {
-      tiles.push_back(q.first);
-      tile_J.push_back(q.second);
-    }
-    F.pi.lev_ptr[L + 1] = (int64_t)tiles.size();
+    return z;
+  };
+  zs = plan(short_f, tiles, &tile_J, F.pi.lev_ptr, F.pi.lev_sptr, true);
+  plan(short_b, btiles, nullptr, F.pi.blev_ptr, F.pi.blev_sptr, false);
+  if (too_big) {
+    F.pi = PiSweep{};
+    return QP_OK;
   }
+  F.pi.prefetch = std::getenv("QPB_PI_PF") && std::getenv("QPB_PI_PF")[0] == '1';   // measured slower on c2 (0.984 -> 1.009 ms per PCG iteration)
   if (tiles.empty()) return QP_OK;
   cudaStream_t st = c->stream;
   int64_t* zoff_dev = nullptr;
@@ -1842,6 +1874,7 @@ int build_pi(qp_ctx* c) {
     F.pi.Z = F.mem.alloc<double>((size_t)zs);
     F.pi.tiles = F.mem.upload(tiles, st);
     F.pi.tile_J = F.mem.upload(tile_J, st);
+    F.pi.btiles = F.mem.upload(btiles, st);
     zoff_dev = F.mem.upload(zoffJ, st);
     if (use_st) {
       F.pi.st_hdr = F.mem.upload(hdr, st);
@@ -2287,6 +2320,47 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
         F.pi.enabled = (F.pi_discrepancy <= 1e-10 && std::isfinite(F.pi_discrepancy)) ? 1 : 0;
         if (std::getenv("QPB_VERBOSE"))
           std::fprintf(stderr, "qpb: level-product guard %.3e -> %s\n", F.pi_discrepancy, F.pi.enabled ? "on" : "off");
+        // Which path is faster depends on the tree (c2: deep nested dissection, 1.45 → 0.87 ms per F-solve;
+        // c3s: a shallow minimum-degree forest under a dominant root, 0.19 → 0.26 ms), so time both on this
+        // factor: the median of 5 F-solves each after 2 warm-ups (QPB_PI=2 forces the level products).
+        if (F.pi.enabled && !(pe && pe[0] == '2')) {
+          cudaEvent_t e0, e1;
+          cudaEventCreate(&e0);
+          cudaEventCreate(&e1);
+          double med[2] = {0, 0};
+          for (int mode = 1; mode >= 0; --mode) {
+            F.pi.enabled = mode;
+            if (!mode) {   // the sweeps expect zero accumulators
+              cudaMemsetAsync(F.d.acc, 0, N * 8, st);
+              cudaMemsetAsync(F.d.tacc, 0, N * 8, st);
+            }
+            std::vector<float> ts;
+            for (int rep = 0; rep < 7; ++rep) {
+              cudaEventRecord(e0, st);
+              f_solve_dev(c, c->rhs2, c->xbuf);
+              cudaEventRecord(e1, st);
+              cudaEventSynchronize(e1);
+              float ms = 0;
+              cudaEventElapsedTime(&ms, e0, e1);
+              if (rep >= 2) ts.push_back(ms);
+            }
+            std::sort(ts.begin(), ts.end());
+            med[mode] = ts[ts.size() / 2];
+          }
+          cudaEventDestroy(e0);
+          cudaEventDestroy(e1);
+          rc = cuda_check(c, "level-product timing");
+          if (rc) return rc;
+          F.pi_ms[0] = med[0];
+          F.pi_ms[1] = med[1];
+          bool faster = med[1] < med[0];
+          if (c->sharded)
+            if (int rc3 = agree_all(c, faster)) return rc3;
+          F.pi.enabled = faster ? 1 : 0;   // acc / tacc are zero here (the sweeps ran last)
+          if (std::getenv("QPB_VERBOSE"))
+            std::fprintf(stderr, "qpb: F-solve %.3f ms with level products, %.3f ms with the task graph -> %s\n", med[1],
+                         med[0], F.pi.enabled ? "level products" : "task graph");
+        }
         if (!F.pi.enabled) {   // the sweeps expect zero accumulators
           cudaMemsetAsync(F.d.acc, 0, N * 8, st);
           cudaMemsetAsync(F.d.tacc, 0, N * 8, st);
@@ -2710,6 +2784,8 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->pi_discrepancy = c->FF.pi_discrepancy;
     s->pi_levels = c->FF.pi.enabled ? c->FF.pi.nlev : 0;
     s->pi_subtrees = c->FF.pi.enabled ? (double)c->FF.pi.st_n : 0.0;
+    s->pi_fsolve_ms = c->FF.pi_ms[1];
+    s->sweep_fsolve_ms = c->FF.pi_ms[0];
     s->sym_enabled = c->FF.sym_enabled ? 1.0 : 0.0;
     s->flat_discrepancy = c->FF.flat_discrepancy;
     s->flat_enabled = c->FF.d.flat ? 1.0 : 0.0;

@@ -2695,95 +2695,176 @@ __global__ void __launch_bounds__(NT) k_pi_init(DevFactor F, SweepRhs R, double*
   }
 }
 // Forward, one level: v = b − acc on the tile's columns; [y; u] += Z_tile v (y into tacc, u into acc).
-__global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const PiTile* tiles, const double* Z) {
+// Blocks [0, nbig) take one CTA tile each (≤ 512 rows, two per thread); the remaining blocks take 8 strips
+// each (≤ 64 rows of a short supernode, a warp per strip, v in registers): a short supernode no longer
+// occupies a CTA with most of its threads idle.
+// A CTA tile's part of Z into L2 (one 128-byte line per lane and column, 8 columns per warp), issued before
+// the loads the tile's input depends on: the DRAM fetch then overlaps the gather of v / s.
+__device__ __forceinline__ void pi_prefetch(const double* Z, const PiTile& T) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = wid; c < T.nc; c += NT / 32)
+    for (int r = lane * 16; r < T.nr; r += 32 * 16) prefetch_l2(Z + T.zoff + r + (int64_t)c * T.ld);
+}
+__device__ __forceinline__ double pi_rhs(const SweepRhs& R, int64_t c) {
+  if (R.ct.p != nullptr) return c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
+  return R.rhs[R.in_perm ? R.in_perm[c] : c];
+}
+__global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const PiTile* tiles, int nbig, int nstrip,
+                                                  const double* Z, int pf) {
   if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
   const unsigned tls = tl_begin(5);
   __shared__ double v[64];
-  const PiTile T = pi_load_tile(tiles + blockIdx.x);
   const int tid = threadIdx.x;
-  if (tid < T.nc) {
-    const int64_t c = (int64_t)T.col0 + tid;
-    double b;
-    if (R.ct.p != nullptr) b = c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
-    else b = R.rhs[R.in_perm ? R.in_perm[c] : c];
-    v[tid] = b - __ldcg(F.acc + c);
-  }
-  __syncthreads();
-  const int r = 2 * tid;
-  if (r < T.nr) {
-    const double* zp = Z + T.zoff + r;
-    const int32_t* rows = F.sn_rows + T.roff + r;
-    const bool two = r + 1 < T.nr;
-    const int32_t g0 = __ldg(rows), g1 = two ? __ldg(rows + 1) : 0;
-    double s0 = 0.0, s1 = 0.0;
-    const int64_t ld = T.ld;
-#pragma unroll 8
-    for (int c = 0; c < T.nc; ++c) {
-      const double2 z = __ldg(reinterpret_cast<const double2*>(zp + c * ld));
-      const double vc = v[c];
-      s0 += z.x * vc;
-      s1 += z.y * vc;
+  if ((int)blockIdx.x < nbig) {
+    const PiTile T = pi_load_tile(tiles + blockIdx.x);
+    if (pf) pi_prefetch(Z, T);
+    if (tid < T.nc) {
+      const int64_t c = (int64_t)T.col0 + tid;
+      v[tid] = pi_rhs(R, c) - __ldcg(F.acc + c);
     }
-    atomicAdd((r < T.wx ? F.tacc : F.acc) + g0, s0);
-    if (two) atomicAdd((r + 1 < T.wx ? F.tacc : F.acc) + g1, s1);
+    __syncthreads();
+    const int r = 2 * tid;
+    if (r < T.nr) {
+      const double* zp = Z + T.zoff + r;
+      const int32_t* rows = F.sn_rows + T.roff + r;
+      const bool two = r + 1 < T.nr;
+      const int32_t g0 = __ldg(rows), g1 = two ? __ldg(rows + 1) : 0;
+      double s0 = 0.0, s1 = 0.0;
+      const int64_t ld = T.ld;
+#pragma unroll 8
+      for (int c = 0; c < T.nc; ++c) {
+        const double2 z = __ldg(reinterpret_cast<const double2*>(zp + c * ld));
+        const double vc = v[c];
+        s0 += z.x * vc;
+        s1 += z.y * vc;
+      }
+      atomicAdd((r < T.wx ? F.tacc : F.acc) + g0, s0);
+      if (two) atomicAdd((r + 1 < T.wx ? F.tacc : F.acc) + g1, s1);
+    }
+  } else {
+    const int lane = tid & 31;
+    const int si = ((int)blockIdx.x - nbig) * (NT / 32) + (tid >> 5);
+    if (si < nstrip) {
+      const PiTile T = pi_load_tile(tiles + nbig + si);
+      const int64_t c = (int64_t)T.col0 + lane;
+      const double vlo = lane < T.nc ? pi_rhs(R, c) - __ldcg(F.acc + c) : 0.0;
+      const double vhi = lane + 32 < T.nc ? pi_rhs(R, c + 32) - __ldcg(F.acc + c + 32) : 0.0;
+      const int r = 2 * lane;
+      const bool ok = r < T.nr, two = r + 1 < T.nr;
+      const double* zp = Z + T.zoff + (ok ? r : 0);
+      const int32_t* rows = F.sn_rows + T.roff + r;
+      const int32_t g0 = ok ? __ldg(rows) : 0, g1 = two ? __ldg(rows + 1) : 0;
+      double s0 = 0.0, s1 = 0.0;
+      const int64_t ld = T.ld;
+#pragma unroll 8
+      for (int cc = 0; cc < T.nc; ++cc) {
+        const double vc = __shfl_sync(0xffffffffu, cc < 32 ? vlo : vhi, cc & 31);
+        if (ok) {
+          const double2 z = __ldg(reinterpret_cast<const double2*>(zp + cc * ld));
+          s0 += z.x * vc;
+          s1 += z.y * vc;
+        }
+      }
+      if (ok) atomicAdd((r < T.wx ? F.tacc : F.acc) + g0, s0);
+      if (two) atomicAdd((r + 1 < T.wx ? F.tacc : F.acc) + g1, s1);
+    }
   }
   tl_end(5, tls);
 }
 // Backward, one level: s = D⁻¹y on the tile's own rows, −x on its external rows; x_cols += Z_tileᵀ s.
-__global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* tiles, const double* Z, double* x,
-                                                  const int* done_flag) {
+__device__ __forceinline__ double pi_sval(const DevFactor& F, const PiTile& T, const double* x, int r) {
+  const int32_t g = __ldg(F.sn_rows + T.roff + r);
+  return r < T.wx ? __ldcg(F.tacc + g) / __ldg(F.Dpiv + g) : -__ldcg(x + g);
+}
+__global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* tiles, int nbig, int nstrip, const double* Z,
+                                                  double* x, const int* done_flag, int pf) {
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
   const unsigned tls = tl_begin(6);
   __shared__ double s[512 + 2];
-  const PiTile T = pi_load_tile(tiles + blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int r = tid; r < ((T.nr + 1) & ~1); r += NT) {
-    double sv = 0.0;
-    if (r < T.nr) {
-      const int32_t g = __ldg(F.sn_rows + T.roff + r);
-      sv = r < T.wx ? __ldcg(F.tacc + g) / __ldg(F.Dpiv + g) : -__ldcg(x + g);
+  if ((int)blockIdx.x < nbig) {
+    const PiTile T = pi_load_tile(tiles + blockIdx.x);
+    if (pf) pi_prefetch(Z, T);
+    for (int r = tid; r < ((T.nr + 1) & ~1); r += NT) s[r] = r < T.nr ? pi_sval(F, T, x, r) : 0.0;
+    __syncthreads();
+    double t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = 0.0;
+    const int64_t ld = T.ld;
+    const double* zp = Z + T.zoff + (int64_t)wid * ld;
+    for (int rb = 2 * lane; rb < T.nr; rb += 64) {
+      const double s0 = s[rb], s1 = s[rb + 1];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (wid + 8 * k < T.nc) {
+          const double2 z = __ldg(reinterpret_cast<const double2*>(zp + rb + 8 * k * ld));
+          t[k] += z.x * s0 + z.y * s1;
+        }
+      }
     }
-    s[r] = sv;
-  }
-  __syncthreads();
-  double t[8];
+    // 8 column sums over 32 lanes: fold 8 → 1 values over xor 16, 8, 4, then two plain stages
 #pragma unroll
-  for (int k = 0; k < 8; ++k) t[k] = 0.0;
-  const int64_t ld = T.ld;
-  const double* zp = Z + T.zoff + (int64_t)wid * ld;
-  for (int rb = 2 * lane; rb < T.nr; rb += 64) {
-    const double s0 = s[rb], s1 = s[rb + 1];
+    for (int h = 4, m = 16; h >= 1; h >>= 1, m >>= 1) {
+      const bool up = lane & m;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (wid + 8 * k < T.nc) {
-        const double2 z = __ldg(reinterpret_cast<const double2*>(zp + rb + 8 * k * ld));
-        t[k] += z.x * s0 + z.y * s1;
+      for (int k = 0; k < h; ++k) {
+        const double send = up ? t[k] : t[k + h];
+        const double keep = up ? t[k + h] : t[k];
+        t[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    double r0 = t[0];
+    r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+    r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+    // lane bits (16, 8, 4) select k = 4·b16 + 2·b8 + b4
+    if ((lane & 3) == 0) {
+      const int k = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      const int c = wid + 8 * k;
+      if (c < T.nc) atomicAdd(x + T.col0 + c, r0);
+    }
+  } else {
+    const int si = ((int)blockIdx.x - nbig) * (NT / 32) + wid;
+    if (si < nstrip) {
+      const PiTile T = pi_load_tile(tiles + nbig + si);
+      const int r = 2 * lane;
+      const bool ok = r < T.nr;
+      const double s0 = ok ? pi_sval(F, T, x, r) : 0.0;
+      const double s1 = r + 1 < T.nr ? pi_sval(F, T, x, r + 1) : 0.0;
+      const double* zp = Z + T.zoff + (ok ? r : 0);
+      const int64_t ld = T.ld;
+      for (int cb = 0; cb < T.nc; cb += 16) {
+        double t[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          double tv = 0.0;
+          if (ok && cb + k < T.nc) {
+            const double2 z = __ldg(reinterpret_cast<const double2*>(zp + (cb + k) * ld));
+            tv = z.x * s0 + z.y * s1;
+          }
+          t[k] = tv;
+        }
+        // 16 column sums over 32 lanes: fold 16 → 1 values over xor 16, 8, 4, 2, then one plain stage
+#pragma unroll
+        for (int h = 8, m = 16; h >= 1; h >>= 1, m >>= 1) {
+          const bool up = lane & m;
+#pragma unroll
+          for (int k = 0; k < h; ++k) {
+            const double send = up ? t[k] : t[k + h];
+            const double keep = up ? t[k + h] : t[k];
+            t[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+          }
+        }
+        double r0 = t[0];
+        r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+        if ((lane & 1) == 0) {   // lane bits (16, 8, 4, 2) select k = 8·b16 + 4·b8 + 2·b4 + b2
+          const int k = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+          if (cb + k < T.nc) atomicAdd(x + T.col0 + cb + k, r0);
+        }
       }
     }
   }
-  // 8 column sums over 32 lanes: fold 8 → 1 values over xor 16, 8, 4, then two plain stages
-#pragma unroll
-  for (int h = 4, m = 16; h >= 1; h >>= 1, m >>= 1) {
-    const bool up = lane & m;
-#pragma unroll
-    for (int k = 0; k < h; ++k) {
-      const double send = up ? t[k] : t[k + h];
-      const double keep = up ? t[k + h] : t[k];
-      t[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-    }
-  }
-  double r0 = t[0];
-  r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
-  r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
-  // lane bits (16, 8, 4) select k = 4·b16 + 2·b8 + b4
-  if ((lane & 3) == 0) {
-    const int k = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    const int c = wid + 8 * k;
-    if (c < T.nc) atomicAdd(x + T.col0 + c, r0);
-  }
   tl_end(6, tls);
 }
-
 // ---- small supernodes (≤ 16 columns), one WARP per supernode, every load issued before any arithmetic.
 // The 16-lane kernels above (k_lvl_fwd / k_lvl_bwd) load the first 16 rows of L_rows up front and the rest in
 // passes of 16 after the solve: with 40–90 rows per supernode that is 4–6 dependent memory round trips, and
@@ -3226,14 +3307,18 @@ void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double*
     else k_lvl_fwd<32><<<g, NT, 0, s>>>(F, r, x, i0, i1);
   }
   for (int L = 0; L < P.nlev; ++L) {
-    const int64_t n = P.lev_ptr[L + 1] - P.lev_ptr[L];
-    if (n > 0) k_pi_fwd<<<(unsigned)n, NT, 0, s>>>(F, r, P.tiles + P.lev_ptr[L], P.Z);
+    const int64_t nbig = P.lev_sptr[L] - P.lev_ptr[L], nstrip = P.lev_ptr[L + 1] - P.lev_sptr[L];
+    const int64_t n = nbig + (nstrip + NT / 32 - 1) / (NT / 32);
+    if (n > 0) k_pi_fwd<<<(unsigned)n, NT, 0, s>>>(F, r, P.tiles + P.lev_ptr[L], (int)nbig, (int)nstrip, P.Z, P.prefetch);
   }
 }
 void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* done_flag, cudaStream_t s) {
   for (int L = P.nlev - 1; L >= 0; --L) {
-    const int64_t n = P.lev_ptr[L + 1] - P.lev_ptr[L];
-    if (n > 0) k_pi_bwd<<<(unsigned)n, NT, 0, s>>>(F, P.tiles + P.lev_ptr[L], P.Z, x, done_flag);
+    const int64_t nbig = P.blev_sptr[L] - P.blev_ptr[L], nstrip = P.blev_ptr[L + 1] - P.blev_sptr[L];
+    const int64_t n = nbig + (nstrip + NT / 32 - 1) / (NT / 32);
+    if (n > 0)
+      k_pi_bwd<<<(unsigned)n, NT, 0, s>>>(F, P.btiles + P.blev_ptr[L], (int)nbig, (int)nstrip, P.Z, x, done_flag,
+                                          P.prefetch);
   }
   if (P.st_n > 0) {
     if (P.st_g == 16 && lvl16_on()) k_st16_bwd<<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);

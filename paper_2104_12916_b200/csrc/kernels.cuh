@@ -294,12 +294,18 @@ struct StHdr {           // 48 bytes
 struct PiSweep {
   int enabled = 0;
   int nlev = 0;                        // levels lvl_cut … top−1 (the symmetric root excluded)
-  const PiTile* tiles = nullptr;       // level-major
-  const int32_t* tile_J = nullptr;     // supernode of each tile (build only)
+  const PiTile* tiles = nullptr;       // forward tiles, level-major
+  const int32_t* tile_J = nullptr;     // supernode of each forward tile (build only)
+  const PiTile* btiles = nullptr;      // backward tiles (same Z, strips for taller supernodes than forward)
+  int64_t blev_ptr[PI_MAXLEV + 1] = {0};
+  int64_t blev_sptr[PI_MAXLEV] = {0};
+  int prefetch = 1;                    // CTA tiles prefetch their part of Z into L2 before the dependent loads
   double* Z = nullptr;
   int64_t z_size = 0;
   int64_t root0 = 0;                   // first column of the symmetric root
   int64_t lev_ptr[PI_MAXLEV + 1] = {0};
+  int64_t lev_sptr[PI_MAXLEV] = {0};   // level L: CTA tiles [lev_ptr[L], lev_sptr[L]), then strips (≤ 64 rows, a warp
+                                       // each, 8 per CTA) [lev_sptr[L], lev_ptr[L + 1])
   // subtrees (st_n = 0: the leaf phase's level kernels run instead)
   int64_t st_n = 0;
   int st_g = 16;                       // lanes per supernode (16: every subtree supernode has ≤ 16 columns)

@@ -1,15 +1,18 @@
 #!/bin/bash
-# Subtrees with the warp-wide supernode code: path tests, c2 bench A/B, timeline.
+# 4 CTAs/SM level-product kernels: path tests, c2/c4s/c3s bench, timeline, full parity.
 set -u
 O=gpurun_out/pi${1:-}
 mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_paths.py -m gpu -x -q -k "level_products" > $O/pytest_paths.log 2>&1
 echo "paths rc=$?" >> $O/status.txt
-B="python bench.py --config c2 --steps 4 --warmup 3 --no-cpu-baseline --no-ipm-solve --secondary= --no-e2e"
-for kb in 96 48 200; do
-QPB_ST_KB=$kb timeout 900 $B > $O/bench_c2_kb$kb.json 2> $O/bench_c2_kb$kb.err
-echo "bench c2 kb$kb rc=$?" >> $O/status.txt
-done
+B="python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-ipm-solve --secondary= --no-e2e"
+QPB_VERBOSE=1 timeout 900 $B --config c2 > $O/bench_c2.json 2> $O/bench_c2.err
+echo "bench c2 rc=$?" >> $O/status.txt
 timeout 600 python scripts/timeline.py c2 12 > $O/timeline_c2.txt 2>&1
-QPB_ST=0 timeout 600 python scripts/timeline.py c2 12 > $O/timeline_c2_nost.txt 2>&1
-echo "timeline rc=$?" >> $O/status.txt
+for cfg in c4s c3s; do
+QPB_VERBOSE=1 timeout 900 $B --config $cfg > $O/bench_$cfg.json 2> $O/bench_$cfg.err
+QPB_PI=0 timeout 900 $B --config $cfg > $O/bench_${cfg}_off.json 2> $O/bench_${cfg}_off.err
+done
+echo "bench c4s c3s rc=$?" >> $O/status.txt
+timeout 2400 python -m pytest tests/test_gpu_full.py tests/test_gpu_scale.py -m gpu -x -q --deselect "tests/test_gpu_full.py::test_full_ph_ipm_objective" > $O/pytest_full.log 2>&1
+echo "full rc=$?" >> $O/status.txt

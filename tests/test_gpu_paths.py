@@ -118,7 +118,7 @@ def test_path_variant_matches_oracle(oracle_case, variant):
         assert abs(out["obj"] - obj) <= 1e-8 * max(1.0, abs(obj))
 
 
-PI_ENV = {"QPB_PI_MINN": "0", "QPB_DENSE_FINV": "0", "QPB_DENSE_W": "0", "QPB_FLAT": "0"}
+PI_ENV = {"QPB_PI_MINN": "0", "QPB_DENSE_FINV": "0", "QPB_DENSE_W": "0", "QPB_FLAT": "0", "QPB_PI": "2"}
 
 
 @pytest.mark.parametrize("variant", ["subtrees", "subtrees32", "leaf_phase", "all_levels", "off"])
