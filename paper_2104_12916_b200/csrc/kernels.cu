@@ -48,6 +48,11 @@ __device__ __forceinline__ unsigned long long atom_acqrel_add_u64(unsigned long 
   asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   return old;
 }
+// Programmatic dependent launch (the level-product chain): wait for the previous grid in the stream to
+// complete and flush, then let the next grid's CTAs be scheduled as this grid's CTAs drain (they block in
+// their own grid_dep_wait).  Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -2711,6 +2716,8 @@ __device__ __forceinline__ double pi_rhs(const SweepRhs& R, int64_t c) {
 }
 __global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const PiTile* tiles, int nbig, int nstrip,
                                                   const double* Z, int pf) {
+  grid_dep_wait();
+  grid_dep_launch();
   if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
   const unsigned tls = tl_begin(5);
   __shared__ double v[64];
@@ -2778,6 +2785,8 @@ __device__ __forceinline__ double pi_sval(const DevFactor& F, const PiTile& T, c
 }
 __global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* tiles, int nbig, int nstrip, const double* Z,
                                                   double* x, const int* done_flag, int pf) {
+  grid_dep_wait();
+  grid_dep_launch();
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
   const unsigned tls = tl_begin(6);
   __shared__ double s[512 + 2];
@@ -3183,6 +3192,8 @@ __global__ void __launch_bounds__(NT, G == 16 ? 3 : 2) k_st_bwd(DevFactor F, PiS
 // Subtrees of ≤ 16-column supernodes: a warp per subtree, the whole warp on one supernode at a time
 // (sn16_fwd / sn16_bwd: one round trip per supernode, served by L2 after the subtree's prefetch).
 __global__ void __launch_bounds__(NT, 2) k_st16_fwd(DevFactor F, SweepRhs R, PiSweep P, double* x) {
+  grid_dep_wait();
+  grid_dep_launch();
   if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
   const unsigned tls = tl_begin(8);
   __shared__ double frs[ST_WPB][ST_FRAME];
@@ -3233,6 +3244,8 @@ __global__ void __launch_bounds__(NT, 2) k_st16_fwd(DevFactor F, SweepRhs R, PiS
   tl_end(8, tls);
 }
 __global__ void __launch_bounds__(NT, 2) k_st16_bwd(DevFactor F, PiSweep P, double* x, const int* done_flag) {
+  grid_dep_wait();
+  grid_dep_launch();
   if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
   const unsigned tls = tl_begin(9);
   __shared__ double frs[ST_WPB][ST_FRAME];
@@ -3284,6 +3297,26 @@ __global__ void __launch_bounds__(NT, 2) k_st16_bwd(DevFactor F, PiSweep P, doub
   }
   tl_end(9, tls);
 }
+// Launch with programmatic stream serialization (QPB_PDL=0: a plain launch): the kernel must start with
+// grid_dep_wait().
+static bool pdl_on() {
+  static const bool on = !(std::getenv("QPB_PDL") && std::getenv("QPB_PDL")[0] == '0');
+  return on;
+}
+template <class... KA, class... A>
+static void launch_dep(void (*k)(KA...), unsigned grid, cudaStream_t s, A... a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, a...);
+}
 void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaStream_t s) {
   const int64_t nt = P.lev_ptr[P.nlev];
   if (nt <= 0) return;
@@ -3294,7 +3327,7 @@ void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaSt
 void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
   k_pi_init<<<sms * 4, NT, 0, s>>>(F, r, x, P.root0);
   if (P.st_n > 0) {
-    if (P.st_g == 16 && lvl16_on()) k_st16_fwd<<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
+    if (P.st_g == 16 && lvl16_on()) launch_dep(k_st16_fwd, (unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), s, F, r, P, x);
     else if (P.st_g == 16) k_st_fwd<16><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
     else k_st_fwd<32><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
   }
@@ -3309,7 +3342,7 @@ void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double*
   for (int L = 0; L < P.nlev; ++L) {
     const int64_t nbig = P.lev_sptr[L] - P.lev_ptr[L], nstrip = P.lev_ptr[L + 1] - P.lev_sptr[L];
     const int64_t n = nbig + (nstrip + NT / 32 - 1) / (NT / 32);
-    if (n > 0) k_pi_fwd<<<(unsigned)n, NT, 0, s>>>(F, r, P.tiles + P.lev_ptr[L], (int)nbig, (int)nstrip, P.Z, P.prefetch);
+    if (n > 0) launch_dep(k_pi_fwd, (unsigned)n, s, F, r, P.tiles + P.lev_ptr[L], (int)nbig, (int)nstrip, (const double*)P.Z, P.prefetch);
   }
 }
 void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* done_flag, cudaStream_t s) {
@@ -3317,11 +3350,11 @@ void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* don
     const int64_t nbig = P.blev_sptr[L] - P.blev_ptr[L], nstrip = P.blev_ptr[L + 1] - P.blev_sptr[L];
     const int64_t n = nbig + (nstrip + NT / 32 - 1) / (NT / 32);
     if (n > 0)
-      k_pi_bwd<<<(unsigned)n, NT, 0, s>>>(F, P.btiles + P.blev_ptr[L], (int)nbig, (int)nstrip, P.Z, x, done_flag,
-                                          P.prefetch);
+      launch_dep(k_pi_bwd, (unsigned)n, s, F, P.btiles + P.blev_ptr[L], (int)nbig, (int)nstrip, (const double*)P.Z, x,
+                 done_flag, P.prefetch);
   }
   if (P.st_n > 0) {
-    if (P.st_g == 16 && lvl16_on()) k_st16_bwd<<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);
+    if (P.st_g == 16 && lvl16_on()) launch_dep(k_st16_bwd, (unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), s, F, P, x, done_flag);
     else if (P.st_g == 16) k_st_bwd<16><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);
     else k_st_bwd<32><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, P, x, done_flag);
   }
