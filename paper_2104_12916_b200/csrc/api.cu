@@ -878,7 +878,7 @@ void f_solve_sweeps(qp_ctx* c, const SweepRhs& r, double* out) {
   if (F.pi.enabled) {   // level products: leaf levels, one product kernel per upper level, root GEMV, and back
     int nl = 0;
     for (int L = 0; L < F.pi.nlev; ++L) nl += F.pi.lev_ptr[L + 1] > F.pi.lev_ptr[L] ? 1 : 0;
-    c->launches += 1 + (F.pi.st_n > 0 ? 2 : 2 * F.d.lvl_cut) + 2 * nl;
+    c->launches += (r.rhs_ready ? 0 : 1) + (F.pi.st_n > 0 ? 2 : 2 * F.d.lvl_cut) + 2 * nl;
     int h = c->begin(0);
     pi_forward(F.d, F.pi, r, out, c->sm_count, c->stream);
     c->end(h);
@@ -952,7 +952,7 @@ int kf_apply_dev(qp_ctx* c, const double* D, const double* p, double* q, bool pc
     }
     return 0;
   }
-  r.rhs_ready = rhs_ready && c->FF.d.flat ? 1 : 0;
+  r.rhs_ready = rhs_ready && (c->FF.d.flat || (c->FF.pi.enabled && !c->dense_finv)) ? 1 : 0;
   if (rhs_ready && !c->FF.d.flat) {
     r.rhs = c->ubuf;
   } else if (c->sharded || (pregather_on() && !c->FF.d.flat)) {
@@ -1102,7 +1102,7 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
       c->vgrid, (int64_t)c->sm_count * std::max<int64_t>(1, (m2 + per_wave - 1) / per_wave));
   // phase D of the fused step prepares the next iteration's u = Cᵀp (flattened forest or pregathered
   // sweeps); the first iteration's comes from the usual kernel
-  const int next_rhs = !fused ? 0 : c->dense_w ? 3 : c->FF.d.flat ? 1 : pregather_on() ? 2 : 0;
+  const int next_rhs = !fused ? 0 : c->dense_w ? 3 : c->FF.d.flat ? 1 : !pregather_on() ? 0 : c->FF.pi.enabled ? 4 : 2;
   if (next_rhs == 3) {
     spmv(c->Ctf, c->pp, c->ubuf, &c->pst->done, c->vgrid, st);
     cudaMemsetAsync(c->xbuf, 0, c->n * 8, st);
@@ -1114,9 +1114,16 @@ int pcg_dev(qp_ctx* c, const double* D, const double* b, double tol, int maxit, 
     r0.done_flag = &c->pst->done;
     flat_rhs(c->FF.d, r0, c->xbuf, c->sm_count, st);
     c->launches += 1;
-  } else if (next_rhs == 2) {
+  } else if (next_rhs == 2 || next_rhs == 4) {
     spmv(c->Ctf, c->pp, c->ubuf, &c->pst->done, c->vgrid, st);
     c->launches += 1;
+    if (next_rhs == 4) {   // level products: accumulators zeroed and the root's right-hand side staged
+      SweepRhs r0{};
+      r0.rhs = c->ubuf;
+      r0.done_flag = &c->pst->done;
+      pi_init(c->FF.d, c->FF.pi, r0, c->xbuf, c->sm_count, st);
+      c->launches += 1;
+    }
   }
   auto body = [&]() -> int {
     if (fused) {
@@ -1892,6 +1899,7 @@ int build_pi(qp_ctx* c) {
   F.pi.nlev = nlev;
   F.pi.z_size = zs;
   F.pi.root0 = S.sn_start[Jr];
+  if (!F.d.flat) F.d.fl_rc0 = F.pi.root0;   // the fused PCG step's phase D (next_rhs = 4) stages vbuf from here
   pi_build(F.d, F.pi, zoff_dev, st);
   int rc = sync_check(c, "level-product build");   // host vectors
   if (std::getenv("QPB_VERBOSE"))

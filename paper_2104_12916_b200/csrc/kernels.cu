@@ -3324,8 +3324,11 @@ void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaSt
   k_pi_build_x<<<(unsigned)nt, NT, 0, s>>>(F, P.tiles, P.tile_J, P.Z, nt);
   k_pi_build_y<<<(unsigned)nt, NT, 0, s>>>(F, P.tiles, P.tile_J, P.Z, zoffJ, nt);
 }
-void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
+void pi_init(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
   k_pi_init<<<sms * 4, NT, 0, s>>>(F, r, x, P.root0);
+}
+void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s) {
+  if (!r.rhs_ready) k_pi_init<<<sms * 4, NT, 0, s>>>(F, r, x, P.root0);
   if (P.st_n > 0) {
     if (P.st_g == 16 && lvl16_on()) launch_dep(k_st16_fwd, (unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), s, F, r, P, x);
     else if (P.st_g == 16) k_st_fwd<16><<<(unsigned)((P.st_n + ST_WPB - 1) / ST_WPB), NT, 0, s>>>(F, r, P, x);
@@ -3660,6 +3663,91 @@ __global__ void __launch_bounds__(NT) k_pcg_update2(int64_t m2, const double* z,
 // run on the vector grid, this one on its own grid); block 0 writes the state.
 // Phase A's partials live in partial[0, G), phase B's in partial[G, 3G), so no block overwrites a
 // partial another block is still reading.
+// QPB_STEP_B4=0: the large-m2 fused step one row per loop trip (A/B)
+__device__ int g_step_b4 = 1;
+__device__ __forceinline__ bool step_batch4() { return g_step_b4 != 0; }
+// Four rows of a CSR product at once (rows r[u], valid where ok[u]): the four rows' pointer, entry and gather
+// loads are issued together, so a thread that owns many rows of a grid-stride loop pays one dependent round
+// trip per FOUR rows instead of per row (the large-m2 fused step was bound by exactly these round trips).
+__device__ __forceinline__ void csr_dot4(const DevCSR& M, const int64_t (&r)[4], const bool (&ok)[4], const double* x,
+                                         double (&s)[4]) {
+  int64_t q0[4], q1[4];
+  int64_t len = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    q0[u] = ok[u] ? M.p[r[u]] : 0;
+    q1[u] = ok[u] ? M.p[r[u] + 1] : 0;
+    s[u] = 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) len = q1[u] - q0[u] > len ? q1[u] - q0[u] : len;
+  for (int64_t k = 0; k < len; ++k) {
+    double v[4];
+    int32_t c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = q0[u] + k < q1[u];
+      v[u] = in ? M.v[q0[u] + k] : 0.0;
+      c[u] = in ? M.i[q0[u] + k] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] += v[u] * __ldg(x + c[u]);
+  }
+}
+// kf_rows with the short rows taken four at a time (see csr_dot4); the long rows as in kf_rows.
+__device__ __forceinline__ double kf_rows4(const DevCSR& Cf, const int32_t* longr, int64_t nlong, const double* D,
+                                           const double* p, const double* z, double* q) {
+  const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = (int64_t)gridDim.x * NT;
+  double loc = 0.0;
+  for (int64_t i = i0; i < Cf.nrows; i += 4 * stride) {
+    int64_t r[4];
+    bool ok[4];
+    double pv[4], dv[4], s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      r[u] = i + u * stride;
+      ok[u] = r[u] < Cf.nrows;
+      if (ok[u] && nlong > 0 && Cf.p[r[u] + 1] - Cf.p[r[u]] > KF_LONG_ROW) ok[u] = false;
+      pv[u] = ok[u] ? p[r[u]] : 0.0;
+      dv[u] = ok[u] ? D[r[u]] : 0.0;
+    }
+    csr_dot4(Cf, r, ok, z, s);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (ok[u]) {
+        const double qi = dv[u] * pv[u] - s[u];
+        q[r[u]] = qi;
+        loc += pv[u] * qi;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (i0 >> 5); j < nlong; j += stride >> 5) {
+    const int64_t i = longr[j];
+    const int64_t e0 = Cf.p[i], e1 = Cf.p[i + 1];
+    double s = 0.0;
+    for (int64_t e = e0 + lane; e < e1; e += 128) {
+      double v4[4];
+      int32_t c4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool in = e + 32 * u < e1;
+        v4[u] = in ? Cf.v[e + 32 * u] : 0.0;
+        c4[u] = in ? Cf.i[e + 32 * u] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s += v4[u] * __ldg(z + c4[u]);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const double pi = p[i];
+      const double qi = D[i] * pi - s;
+      q[i] = qi;
+      loc += pi * qi;
+    }
+  }
+  return loc;
+}
 template <int BA, int BD, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_pcg_step(DevCSR Cf, const int32_t* longr, int64_t nlong, int prec,
                                                  const double* D, double* p, const double* w, double* q, double* x,
@@ -3674,7 +3762,8 @@ __global__ void __launch_bounds__(NT, MINB) k_pcg_step(DevCSR Cf, const int32_t*
   const int64_t m2 = Cf.nrows, G = gridDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)NT + threadIdx.x, stride = G * NT;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  const double loc = kf_rows<BA>(Cf, longr, nlong, D, p, w, q);
+  const bool b4 = BA == 4 && step_batch4();   // large-m2 variant: four rows per loop trip in every phase
+  const double loc = b4 ? kf_rows4(Cf, longr, nlong, D, p, w, q) : kf_rows<BA>(Cf, longr, nlong, D, p, w, q);
   double v = block_reduce<0>(loc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = v;
   grid.sync();
@@ -3686,14 +3775,43 @@ __global__ void __launch_bounds__(NT, MINB) k_pcg_step(DevCSR Cf, const int32_t*
   }
   const double alpha = rho / pq;
   double rr = 0.0, rz = 0.0;
-  for (int64_t i = i0; i < m2; i += stride) {
-    x[i] += alpha * p[i];
-    const double ri = r[i] - alpha * q[i];
-    r[i] = ri;
-    rr += ri * ri;
-    const double zi = prec == 1 ? ri / D[i] : ri;
-    z[i] = zi;
-    rz += ri * zi;
+  if (b4) {
+    for (int64_t i = i0; i < m2; i += 4 * stride) {
+      double xv[4], pv[4], rv[4], qv[4], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = i + u * stride;
+        const bool ok = j < m2;
+        xv[u] = ok ? x[j] : 0.0;
+        pv[u] = ok ? p[j] : 0.0;
+        rv[u] = ok ? r[j] : 0.0;
+        qv[u] = ok ? q[j] : 0.0;
+        dv[u] = ok && prec == 1 ? D[j] : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = i + u * stride;
+        if (j < m2) {
+          x[j] = xv[u] + alpha * pv[u];
+          const double ri = rv[u] - alpha * qv[u];
+          r[j] = ri;
+          rr += ri * ri;
+          const double zi = prec == 1 ? ri / dv[u] : ri;
+          z[j] = zi;
+          rz += ri * zi;
+        }
+      }
+    }
+  } else {
+    for (int64_t i = i0; i < m2; i += stride) {
+      x[i] += alpha * p[i];
+      const double ri = r[i] - alpha * q[i];
+      r[i] = ri;
+      rr += ri * ri;
+      const double zi = prec == 1 ? ri / D[i] : ri;
+      z[i] = zi;
+      rz += ri * zi;
+    }
   }
   const double v1 = block_reduce<0>(rr, sh);
   const double v2 = block_reduce<0>(rz, sh);
@@ -3711,13 +3829,65 @@ __global__ void __launch_bounds__(NT, MINB) k_pcg_step(DevCSR Cf, const int32_t*
     return;
   }
   const double beta = s2 / rho;
-  for (int64_t i = i0; i < m2; i += stride) p[i] = z[i] + beta * p[i];
+  if (b4) {
+    for (int64_t i = i0; i < m2; i += 4 * stride) {
+      double zv[4], pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = i + u * stride;
+        zv[u] = j < m2 ? z[j] : 0.0;
+        pv[u] = j < m2 ? p[j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = i + u * stride;
+        if (j < m2) p[j] = zv[u] + beta * pv[u];
+      }
+    }
+  } else {
+    for (int64_t i = i0; i < m2; i += stride) p[i] = z[i] + beta * p[i];
+  }
   if (next_rhs) {   // phase D: the next F-solve's right-hand side u = Cᵀp (p complete after the sync)
     grid.sync();
-    const int64_t N = next_rhs == 1 ? F.N : Ct.nrows, rc0 = F.fl_rc0;
+    const int64_t N = (next_rhs == 1 || next_rhs == 4) ? F.N : Ct.nrows, rc0 = F.fl_rc0;
+    if (b4 && (next_rhs == 2 || next_rhs == 4)) {
+      for (int64_t cI = i0; cI < N; cI += 4 * stride) {
+        int64_t rr4[4];
+        bool ok[4];
+        double s4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          rr4[u] = cI + u * stride;
+          ok[u] = rr4[u] < Ct.nrows;
+        }
+        csr_dot4(Ct, rr4, ok, p, s4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = rr4[u];
+          if (j < N) {
+            const double v = ok[u] ? s4[u] : 0.0;
+            ubuf[j] = v;
+            if (next_rhs == 4) {
+              F.acc[j] = 0.0;
+              F.tacc[j] = 0.0;
+              xout[j] = 0.0;
+              if (j >= rc0) F.vbuf[j] = v;
+            }
+          }
+        }
+      }
+      tl_end(4, tls);
+      return;
+    }
     for (int64_t cI = i0; cI < N; cI += stride) {
       const double v = cI < Ct.nrows ? csr_dot<BD>(Ct, cI, p) : 0.0;
-      if (next_rhs >= 2) {
+      if (next_rhs == 4) {   // level products: what k_pi_init does, with u = Cᵀp as the right-hand side
+        ubuf[cI] = v;
+        F.acc[cI] = 0.0;
+        F.tacc[cI] = 0.0;
+        xout[cI] = 0.0;
+        if (cI >= rc0) F.vbuf[cI] = v;
+      } else if (next_rhs >= 2) {
         ubuf[cI] = v;
         if (next_rhs == 3) xout[cI] = 0.0;   // dense W: the GEMV accumulates into xout[0, n)
       } else {
@@ -3741,11 +3911,15 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
   // large m2: 4-entry batches at 4 CTAs per SM (more rows in flight)
   static int sms = 0, max_wide = 0, max_narrow = 0;
   if (!sms) {
+    if (std::getenv("QPB_STEP_B4") && std::getenv("QPB_STEP_B4")[0] == '0') {
+      const int zero = 0;
+      cudaMemcpyToSymbol(g_step_b4, &zero, sizeof(int));
+    }
     int dev = 0, o1 = 0, o2 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_pcg_step<8, 16, 2>, NT, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_pcg_step<4, 4, 4>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_pcg_step<4, 4, 3>, NT, 0);
     max_wide = sms * o1;
     max_narrow = sms * o2;
   }
@@ -3757,10 +3931,10 @@ bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, c
   DevCSR Ct{};
   if (Fp) F = *Fp;
   if (Ctp) Ct = *Ctp;
-  if (next_rhs && (!Ctp || (next_rhs == 1 && !Fp) || (next_rhs == 3 && !xout))) next_rhs = 0;
+  if (next_rhs && (!Ctp || ((next_rhs == 1 || next_rhs == 4) && !Fp) || (next_rhs >= 3 && !xout))) next_rhs = 0;
   void* args[] = {&C, &longr, &nlong, &prec, &D, &p, &w, &q, &x, &r, &z, &partial, &st, &next_rhs, &F, &Ct, &xout,
                   &ubuf};
-  const void* fn = wide ? (const void*)k_pcg_step<8, 16, 2> : (const void*)k_pcg_step<4, 4, 4>;
+  const void* fn = wide ? (const void*)k_pcg_step<8, 16, 2> : (const void*)k_pcg_step<4, 4, 3>;
   return cudaLaunchCooperativeKernel(fn, grid, NT, args, 0, s) == cudaSuccess;
 }
 

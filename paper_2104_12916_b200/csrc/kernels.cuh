@@ -230,7 +230,7 @@ struct SweepRhs {
   DevCSR ct;                // optional: rhs[c] = Σ ct(c,:)·p for c < ct.nrows (K_F: Cᵀp fused)
   const double* p;
   const int* done_flag;     // early-exit flag (PCG converged) or nullptr
-  int rhs_ready;            // flattened forest: acc / vbuf / x already prepared (fused PCG step, phase D)
+  int rhs_ready;            // flattened forest / level products: acc / vbuf / x already prepared (fused PCG step, phase D)
 };
 void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cudaStream_t s);
 // q = H p (with_h) + Cᵀ(D⁻¹∘(C p)) in two streaming passes (t: m2 scratch), natural order, no factor
@@ -316,6 +316,8 @@ struct PiSweep {
 };
 // Z from the factor storage (after the numeric factorization and the X_J inverses); zoffJ: per supernode offset of Z_J (device)
 void pi_build(const DevFactor& F, const PiSweep& P, const int64_t* zoffJ, cudaStream_t s);
+// pi_forward starts with pi_init unless r.rhs_ready (the fused PCG step's phase D, next_rhs = 4, did the same)
+void pi_init(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s);
 void pi_forward(const DevFactor& F, const PiSweep& P, const SweepRhs& r, double* x, int sms, cudaStream_t s);
 void pi_backward(const DevFactor& F, const PiSweep& P, double* x, const int* done_flag, cudaStream_t s);
 
@@ -340,7 +342,8 @@ void timeline_enable(unsigned long long* buf);
 constexpr int KF_LONG_ROW = 32;
 // next_rhs (phase D, after p = z + βp and one more grid sync) prepares the next F-solve's right-hand side
 // u = Cᵀp, thread per row of Ct: 0 = none, 1 = flattened forest (acc / vbuf, xout = 0, as k_flat_rhs),
-// 2 = dense into ubuf (as the pregather SpMV), 3 = into ubuf with xout[0, n) = 0 (dense W GEMV next).
+// 2 = dense into ubuf (as the pregather SpMV), 3 = into ubuf with xout[0, n) = 0 (dense W GEMV next),
+// 4 = level products: into ubuf, acc = tacc = xout = 0 on [0, N), vbuf = u on the root's columns (as k_pi_init).
 bool pcg_step(const DevCSR& Cf, const int32_t* longr, int64_t nlong, int prec, const double* D, double* p,
               const double* w, double* q, double* x, double* r, double* z, double* partial, PcgState* st, int grid,
               cudaStream_t s, int next_rhs = 0, const DevFactor* F = nullptr, const DevCSR* Ct = nullptr,

@@ -12,7 +12,7 @@ Paths exercised here that the small parity cases never reach:
 * c1: the explicit W = (F⁻¹)₁₁ built with its root block copied from S⁻¹ (the "root-copy" build) for
   every PCG K_F product, the flattened forest for the F-solves; P_H with its dense tail cut into
   4 096-column pieces;
-* c2 / c4s: the fused PCG step's large-m2 variant k_pcg_step<4,4,4> (chosen when the step grid
+* c2 / c4s: the fused PCG step's large-m2 variant k_pcg_step<4,4,3> (chosen when the step grid
   exceeds 2 CTAs per SM: m2 > 2·148·256·2 rows);
 * c2 / c4s / c3s: the task-graph sweeps over deep supernodal trees (21 / 19 / 8 levels).
 """
