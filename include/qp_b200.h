@@ -82,6 +82,15 @@ typedef enum {
  * Every rank must produce bit-identical results.  Return 0 on success. */
 typedef int (*qp_allreduce_fn)(void* user, double* buf, int64_t count, int32_t op, void* stream);
 
+/* Neighbour exchange used by the halo mode of the sharded operator instead of NCCL send/recv (optional;
+ * needed for that mode when `allreduce` is set).  Sends n_to_prev doubles at DEVICE pointer to_prev to
+ * rank − 1 and n_to_next doubles at to_next to rank + 1; receives n_from_prev doubles from rank − 1 into
+ * from_prev and n_from_next from rank + 1 into from_next (a count of 0: no transfer; the first rank has
+ * no previous, the last no next).  Ordered on `stream` (the call may synchronise it).  0 on success. */
+typedef int (*qp_halo_fn)(void* user, const double* to_prev, int64_t n_to_prev, const double* to_next,
+                          int64_t n_to_next, double* from_prev, int64_t n_from_prev, double* from_next,
+                          int64_t n_from_next, void* stream);
+
 typedef struct {
   int device;              /* CUDA device ordinal */
   void* stream;            /* cudaStream_t or NULL */
@@ -94,6 +103,8 @@ typedef struct {
   int64_t workspace_limit_bytes; /* multifrontal workspace cap; 0 = 120 GiB */
   qp_allreduce_fn allreduce;     /* optional collective provider (sharded mode), else NULL */
   void* allreduce_user;          /* passed to allreduce */
+  qp_halo_fn halo;               /* optional neighbour exchange (halo mode of the sharded operator), else NULL */
+  void* halo_user;               /* passed to halo */
 } qp_setup_opts;
 
 /* Sharded mode (enabled when world > 1, nccl_uid != NULL or
@@ -206,6 +217,25 @@ int qp_f_solve(qp_ctx* ctx, const double* rhs, double* out);
  * p: n, q: n (replicated; sharded mode all-reduces the ranks' partial products).  Host or device
  * pointers per vectors_on_device.  Errors: QP_ESTATE before qp_setup, QP_ENOMEM. */
 int qp_operator_apply(qp_ctx* ctx, const double* D, const double* p, double* q);
+
+/* Halo mode of the sharded operator (BJ configs[4]: "rows are partitioned across 2/4/8 GPUs with a halo
+ * exchange"; north_star: "boundary entries of p are exchanged with NCCL").  When every rank's rows of C and
+ * of H reach only into the two neighbouring ranks' parts of x (band-local C, grid H), x is split into
+ * contiguous OWNED ranges [own_lo, own_hi), one per rank, and one product exchanges two halos with the
+ * neighbours instead of all-reducing n doubles:
+ *   1. p on the rank's window [p_lo, p_hi) ⊇ owned range: the entries outside it are received from the
+ *      neighbours that own them (ncclSend/ncclRecv in one group, or opts.halo);
+ *   2. t = D⁻¹∘(C_g p) on the rank's rows, q = (H p on the owned rows) + C_gᵀ t on [q_lo, q_hi);
+ *   3. the parts of q outside the owned range are sent to their owners and added there.
+ * qp_operator_halo_plan (collective, after qp_setup) derives the plan from the rank's rows with the rule
+ * "owned boundary b_g = midpoint between the last column rank g − 1 touches and the first column rank g
+ * touches" and writes info[0..8) = {enabled (0/1, agreed by all ranks), own_lo, own_hi, p_lo, p_hi, q_lo,
+ * q_hi, doubles this rank sends per product}.  qp_operator_apply_halo: D = the rank's m2 rows (> 0); p and
+ * q full-length (n) buffers; on entry p must hold the rank's OWNED entries, on return p also holds its
+ * window and q holds G p on the OWNED range (other entries unspecified).  Errors: QP_ESTATE if the plan
+ * is absent or not enabled, QP_ENCCL from the exchange. */
+int qp_operator_halo_plan(qp_ctx* ctx, int64_t* info);
+int qp_operator_apply_halo(qp_ctx* ctx, const double* D, double* p, double* q);
 int qp_kf_apply(qp_ctx* ctx, const double* D, const double* p, double* q);
 
 /* Host-only symbolic analysis (no GPU needed): ordering of the x block

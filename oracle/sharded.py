@@ -69,3 +69,77 @@ def sharded_pcg(C_g, fs, D_g, b_g, Minv_g, tol, maxit, allreduce):
         p = z + (rho_new / rho) * p
         rho = rho_new
     return x, maxit, rn / bnorm, False
+
+
+# ---------------------------------------------------------------- halo mode of the x-space operator
+def halo_plan(H, C, row_bounds, world):
+    """Owned x-ranges and windows of the halo mode (include/qp_b200.h qp_operator_halo_plan; BJ configs[4]:
+    "rows are partitioned … with a halo exchange"; north_star: "boundary entries of p are exchanged").
+
+    Written out from the definition:
+    * cmin_g, cmax_g: the first / last column any of rank g's rows of C (rows row_bounds[g]..row_bounds[g+1]) touches;
+    * owned boundaries b_0 = 0, b_W = n, b_g = ⌊(cmax_{g−1} + 1 + cmin_g)/2⌋ made monotone: rank g owns x[b_g : b_{g+1}];
+    * q window of g = hull(owned range, [cmin_g, cmax_g]); p window = hull(q window, columns of H's owned rows);
+    * enabled iff every owned range is non-empty and every window lies in [b_{g−1}, b_{g+2}] (only the two
+      neighbours' parts of x are reached).
+    Returns dict(enabled, b, p_lo, p_hi, q_lo, q_hi) with numpy int64 arrays."""
+    H = H.tocsr()
+    C = C.tocsr()
+    n = H.shape[0]
+    W = world
+    cmin, cmax = np.zeros(W, dtype=np.int64), np.zeros(W, dtype=np.int64)
+    ok = W >= 2 and n >= 4 * W
+    for g in range(W):
+        idx = C.indices[C.indptr[row_bounds[g]]:C.indptr[row_bounds[g + 1]]]
+        if len(idx) == 0:
+            return dict(enabled=False)
+        cmin[g], cmax[g] = idx.min(), idx.max()
+    b = np.zeros(W + 1, dtype=np.int64)
+    b[W] = n
+    for g in range(1, W):
+        mid = int(np.floor((float(cmax[g - 1]) + 1.0 + float(cmin[g])) / 2.0))
+        b[g] = max(b[g - 1], min(n, max(0, mid)))
+    ok = ok and bool(np.all(np.diff(b) > 0))
+    p_lo, p_hi, q_lo, q_hi = (np.zeros(W, dtype=np.int64) for _ in range(4))
+    for g in range(W):
+        q_lo[g], q_hi[g] = min(b[g], cmin[g]), max(b[g + 1], cmax[g] + 1)
+        p_lo[g], p_hi[g] = q_lo[g], q_hi[g]
+        if ok:
+            cols = H.indices[H.indptr[b[g]]:H.indptr[b[g + 1]]]
+            if len(cols):
+                p_lo[g], p_hi[g] = min(p_lo[g], cols.min()), max(p_hi[g], cols.max() + 1)
+    for g in range(W):
+        left, right = b[max(0, g - 1)], b[min(W, g + 2)]
+        ok = ok and p_lo[g] >= left and p_hi[g] <= right and q_lo[g] >= left and q_hi[g] <= right
+    return dict(enabled=bool(ok), b=b, p_lo=p_lo, p_hi=p_hi, q_lo=q_lo, q_hi=q_hi)
+
+
+def halo_operator(rank, plan, H, C_g, D_g, p, exchange):
+    """One product q = H p + Cᵀ(D⁻¹∘(C p)) in halo mode on `rank`.  p: length-n array whose owned
+    entries are valid; exchange(to_prev, to_next, n_from_prev, n_from_next) -> (from_prev, from_next) moves
+    arrays between neighbouring ranks.  Returns (q, p): q valid on the owned range, p with the window filled."""
+    b, W = plan["b"], len(plan["b"]) - 1
+    g = rank
+    lo, hi = int(b[g]), int(b[g + 1])
+    p = np.array(p, dtype=float, copy=True)
+    # 1. boundary entries of p
+    tp = p[lo:int(plan["p_hi"][g - 1])] if g > 0 else p[:0]
+    tn = p[int(plan["p_lo"][g + 1]):hi] if g + 1 < W else p[:0]
+    fp, fn = exchange(tp, tn, lo - int(plan["p_lo"][g]), int(plan["p_hi"][g]) - hi)
+    p[int(plan["p_lo"][g]):lo] = fp
+    p[hi:int(plan["p_hi"][g])] = fn
+    # 2. local products: C_g reaches only the q window, H's owned rows only the p window
+    pw = np.zeros_like(p)
+    pw[int(plan["p_lo"][g]):int(plan["p_hi"][g])] = p[int(plan["p_lo"][g]):int(plan["p_hi"][g])]
+    t = (C_g @ pw) / D_g
+    q = np.asarray(C_g.T @ t, dtype=float)
+    q[lo:hi] += (H.tocsr()[lo:hi] @ pw)
+    # 3. q outside the owned range goes to its owner
+    qtp = q[int(plan["q_lo"][g]):lo]
+    qtn = q[hi:int(plan["q_hi"][g])]
+    nfp = int(plan["q_hi"][g - 1]) - lo if g > 0 else 0
+    nfn = hi - int(plan["q_lo"][g + 1]) if g + 1 < W else 0
+    fp, fn = exchange(qtp, qtn, max(0, nfp), max(0, nfn))
+    q[lo:lo + len(fp)] += fp
+    q[hi - len(fn):hi] += fn
+    return q, p

@@ -40,13 +40,17 @@ class _CSR(C.Structure):
 
 # int (*)(void* user, double* buf, int64_t count, int32_t op, void* stream)
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+# int (*)(void* user, const double* to_prev, int64_t, const double* to_next, int64_t,
+#         double* from_prev, int64_t, double* from_next, int64_t, void* stream)
+HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                      C.c_void_p, C.c_int64, C.c_void_p)
 
 
 class _SetupOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_uid", C.c_void_p), ("x_perm", C.c_void_p), ("vectors_on_device", C.c_int),
                 ("workspace_limit_bytes", C.c_int64), ("allreduce", ALLREDUCE_FN),
-                ("allreduce_user", C.c_void_p)]
+                ("allreduce_user", C.c_void_p), ("halo", HALO_FN), ("halo_user", C.c_void_p)]
 
 
 class _IpmOpts(C.Structure):
@@ -109,6 +113,8 @@ def load_library(build: bool = True):
     lib.qp_f_solve.argtypes = [vp, vp, vp]
     lib.qp_kf_apply.argtypes = [vp, vp, vp, vp]
     lib.qp_operator_apply.argtypes = [vp, vp, vp, vp]
+    lib.qp_operator_halo_plan.argtypes = [vp, vp]
+    lib.qp_operator_apply_halo.argtypes = [vp, vp, vp, vp]
     lib.qp_analyse.argtypes = [C.POINTER(vp), C.POINTER(_CSR), C.POINTER(_CSR), vp]
     lib.qp_partition_rows.argtypes = [vp, i64, i32, vp]
     lib.qp_get_partition.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
@@ -168,11 +174,12 @@ class QPSolver:
     """One qp_ctx: ``qp_setup`` on construction, ``qp_free`` on close."""
 
     def __init__(self, H, A, Cm, g, b, d, x_perm=None, device=0, stream=None, vectors_on_device=False,
-                 workspace_limit_bytes=0, rank=0, world=1, nccl_uid=None, allreduce=None):
+                 workspace_limit_bytes=0, rank=0, world=1, nccl_uid=None, allreduce=None, halo=None):
         """rank / world / nccl_uid / allreduce select the sharded mode (qp_b200.h): every rank passes
         the same global problem; m2-length vectors are then this rank's row slice
         (``self.row0 : self.row0 + self.m2`` of ``self.m2_global``).  ``allreduce`` is a Python
-        callable ``f(buf_ptr, count, op, stream_ptr) -> int`` used instead of NCCL."""
+        callable ``f(buf_ptr, count, op, stream_ptr) -> int`` used instead of NCCL; ``halo`` a callable
+        ``f(to_prev, n, to_next, n, from_prev, n, from_next, n, stream_ptr) -> int`` (qp_halo_fn)."""
         import scipy.sparse as sp
         self.lib = load_library()
         self.vectors_on_device = bool(vectors_on_device)
@@ -201,6 +208,9 @@ class QPSolver:
         if allreduce is not None:
             self._ar = ALLREDUCE_FN(lambda user, buf, cnt, op, st: int(allreduce(buf, cnt, op, st)))
             opts.allreduce = self._ar
+        if halo is not None:
+            self._halo = HALO_FN(lambda user, a, na, b, nb, c_, nc, d_, nd, st: int(halo(a, na, b, nb, c_, nc, d_, nd, st)))
+            opts.halo = self._halo
         opts.vectors_on_device = 1 if vectors_on_device else 0
         opts.workspace_limit_bytes = workspace_limit_bytes
         if x_perm is not None:
@@ -341,6 +351,23 @@ class QPSolver:
         q = np.zeros(self.n)
         self._check(self.lib.qp_operator_apply(self.ctx, pD, pp, q.ctypes.data))
         return q
+
+    def operator_halo_plan(self):
+        """qp_operator_halo_plan (collective): dict(enabled, own=(lo, hi), p_window, q_window, sent_doubles)."""
+        info = np.zeros(8, dtype=np.int64)
+        self._check(self.lib.qp_operator_halo_plan(self.ctx, info.ctypes.data))
+        return dict(enabled=bool(info[0]), own=(int(info[1]), int(info[2])), p_window=(int(info[3]), int(info[4])),
+                    q_window=(int(info[5]), int(info[6])), sent_doubles=int(info[7]))
+
+    def operator_apply_halo(self, D, p):
+        """qp_operator_apply_halo with host vectors: p full length with this rank's owned entries valid;
+        returns q (full length; valid on the owned range) and p with the rank's window filled in."""
+        assert not self.vectors_on_device
+        D = _f64(D)
+        p = np.array(p, dtype=np.float64, copy=True)
+        q = np.zeros(self.n)
+        self._check(self.lib.qp_operator_apply_halo(self.ctx, D.ctypes.data, p.ctypes.data, q.ctypes.data))
+        return q, p
 
     def kf_apply(self, D, p):
         pD, kD = self._ptr(D, self.m2)

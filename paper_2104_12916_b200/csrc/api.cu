@@ -41,6 +41,11 @@ struct NcclApi {
                              cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  // halo mode of the sharded operator (optional symbols: present in every NCCL ≥ 2.7)
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
 };
 NcclApi& nccl_api() {
   static NcclApi api;
@@ -58,6 +63,10 @@ NcclApi& nccl_api() {
   api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
   api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
   api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+  api.send = (decltype(api.send))dlsym(h, "ncclSend");
+  api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+  api.group_start = (decltype(api.group_start))dlsym(h, "ncclGroupStart");
+  api.group_end = (decltype(api.group_end))dlsym(h, "ncclGroupEnd");
   api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy && api.error_string;
   if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
   return api;
@@ -279,6 +288,15 @@ struct qp_ctx {
   ncclComm_t nccl = nullptr;
   qp_allreduce_fn ar_fn = nullptr;
   void* ar_user = nullptr;
+  qp_halo_fn halo_fn = nullptr;
+  void* halo_user = nullptr;
+  // halo plan of the sharded operator (qp_operator_halo_plan): owned boundaries b[0..world], the ranks'
+  // windows of p and q, receive scratch
+  struct HaloPlan {
+    bool planned = false, enabled = false;
+    std::vector<int64_t> b, plo, phi, qlo, qhi;
+    double *from_prev = nullptr, *from_next = nullptr;
+  } halo;
   double* ubuf = nullptr;        // N: all-reduced Cᵀ(·) in factor order (λ part zero)
   int64_t ws_limit = 0;
   int64_t n = 0, m1 = 0, m2 = 0;
@@ -422,6 +440,32 @@ struct qp_ctx {
     ncclResult_t r = nccl_api().all_reduce(buf, buf, (size_t)cnt, ncclFloat64, o, nccl, stream);
     if (r != ncclSuccess) {
       err = std::string("ncclAllReduce: ") + nccl_api().error_string(r);
+      return QP_ENCCL;
+    }
+    return 0;
+  }
+  // Neighbour exchange on this context's stream (see qp_halo_fn); counts of 0 are skipped.
+  int exchange(const double* to_prev, int64_t n_tp, const double* to_next, int64_t n_tn, double* from_prev, int64_t n_fp,
+               double* from_next, int64_t n_fn) {
+    if (halo_fn) {
+      int rc = halo_fn(halo_user, to_prev, n_tp, to_next, n_tn, from_prev, n_fp, from_next, n_fn, (void*)stream);
+      if (rc != 0) err = "qp_halo_fn returned " + std::to_string(rc);
+      return rc != 0 ? QP_ENCCL : 0;
+    }
+    NcclApi& api = nccl_api();
+    if (!nccl || !api.send || !api.recv || !api.group_start || !api.group_end) {
+      err = "halo exchange needs NCCL send/recv or opts.halo";
+      return QP_ENCCL;
+    }
+    ncclResult_t r = api.group_start();
+    if (r == ncclSuccess && n_tp > 0) r = api.send(to_prev, (size_t)n_tp, ncclFloat64, rank - 1, nccl, stream);
+    if (r == ncclSuccess && n_tn > 0) r = api.send(to_next, (size_t)n_tn, ncclFloat64, rank + 1, nccl, stream);
+    if (r == ncclSuccess && n_fp > 0) r = api.recv(from_prev, (size_t)n_fp, ncclFloat64, rank - 1, nccl, stream);
+    if (r == ncclSuccess && n_fn > 0) r = api.recv(from_next, (size_t)n_fn, ncclFloat64, rank + 1, nccl, stream);
+    ncclResult_t r2 = api.group_end();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) {
+      err = std::string("ncclSend/ncclRecv: ") + api.error_string(r);
       return QP_ENCCL;
     }
     return 0;
@@ -1686,6 +1730,8 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
       c->ar_fn = o.allreduce;
       c->ar_user = o.allreduce_user;
     }
+    c->halo_fn = o.halo;
+    c->halo_user = o.halo_user;
   }
   int rc = cuda_check(c.get(), "qp_setup");
   c->setup_done = rc == QP_OK;
@@ -2679,25 +2725,30 @@ int qp_kf_apply(qp_ctx* c, const double* D, const double* p, double* q) {
   return rc;
 }
 
+static int ensure_op(qp_ctx* c) {
+  if (c->op_ready) return QP_OK;
+  cudaStream_t st = c->stream;
+  try {
+    c->opH = upload_csr(c->mem, c->H, st);
+    c->opC = upload_csr(c->mem, c->C, st);
+    c->opCt = upload_csr(c->mem, transpose(c->C), st);
+    c->op_D = c->mem.zeros<double>(std::max<int64_t>(1, c->m2), st);
+    c->op_t = c->mem.zeros<double>(std::max<int64_t>(1, c->m2), st);
+    c->op_p = c->mem.zeros<double>(c->n, st);
+    c->op_q = c->mem.zeros<double>(c->n, st);
+  } catch (std::bad_alloc&) {
+    return fail(c, QP_ENOMEM, "cudaMalloc failed (operator copies)");
+  }
+  c->op_ready = true;
+  return QP_OK;
+}
+
 int qp_operator_apply(qp_ctx* c, const double* D, const double* p, double* q) {
   if (!c) return QP_EINVAL;
   if (!c->setup_done) return fail(c, QP_ESTATE, "qp_setup has not completed");
   cudaSetDevice(c->device);
   cudaStream_t st = c->stream;
-  if (!c->op_ready) {
-    try {
-      c->opH = upload_csr(c->mem, c->H, st);
-      c->opC = upload_csr(c->mem, c->C, st);
-      c->opCt = upload_csr(c->mem, transpose(c->C), st);
-      c->op_D = c->mem.zeros<double>(std::max<int64_t>(1, c->m2), st);
-      c->op_t = c->mem.zeros<double>(std::max<int64_t>(1, c->m2), st);
-      c->op_p = c->mem.zeros<double>(c->n, st);
-      c->op_q = c->mem.zeros<double>(c->n, st);
-    } catch (std::bad_alloc&) {
-      return fail(c, QP_ENOMEM, "cudaMalloc failed (operator copies)");
-    }
-    c->op_ready = true;
-  }
+  if (int rc = ensure_op(c)) return rc;
   const double* Dd = in_vec(c, D, c->op_D, c->m2);
   const double* pd = in_vec(c, p, c->op_p, c->n);
   double* qd = c->vectors_on_device ? q : c->op_q;
@@ -2707,6 +2758,141 @@ int qp_operator_apply(qp_ctx* c, const double* D, const double* p, double* q) {
     if (int rc = c->allreduce(qd, c->n, 0)) return rc;   // Σ_ranks of the rows' partial products
   if (!c->vectors_on_device) out_vec(c, q, c->op_q, c->n);
   return sync_check(c, "qp_operator_apply");
+}
+
+// Small all-gather through the all-reduce: every rank contributes `per` values at its own offset.
+static int gather_small(qp_ctx* c, const std::vector<double>& mine, std::vector<double>& all) {
+  const int64_t per = (int64_t)mine.size(), tot = per * c->world;
+  all.assign(tot, 0.0);
+  for (int64_t k = 0; k < per; ++k) all[c->rank * per + k] = mine[k];
+  cudaMemcpyAsync(c->op_q, all.data(), tot * 8, cudaMemcpyHostToDevice, c->stream);
+  if (int rc = c->allreduce(c->op_q, tot, 0)) return rc;
+  cudaMemcpyAsync(all.data(), c->op_q, tot * 8, cudaMemcpyDeviceToHost, c->stream);
+  return sync_check(c, "halo plan gather");
+}
+
+int qp_operator_halo_plan(qp_ctx* c, int64_t* info) {
+  if (!c || !info) return QP_EINVAL;
+  if (!c->setup_done) return fail(c, QP_ESTATE, "qp_setup has not completed");
+  cudaSetDevice(c->device);
+  if (int rc = ensure_op(c)) return rc;
+  auto& P = c->halo;
+  const int W = c->world, g = c->rank;
+  const int64_t n = c->n;
+  if (!P.planned) {
+    P.enabled = false;
+    if (c->sharded && W >= 2 && n >= 4 * (int64_t)W) {
+      // columns this rank's rows of C touch
+      double cmin = (double)n, cmax = -1.0;
+      for (int32_t j : c->C.i) {
+        cmin = std::min(cmin, (double)j);
+        cmax = std::max(cmax, (double)j);
+      }
+      std::vector<double> all;
+      if (int rc = gather_small(c, {cmin, cmax}, all)) return rc;
+      // owned boundaries: b_0 = 0, b_W = n, b_g = the midpoint between the last column rank g − 1 touches
+      // and the first column rank g touches (rounded down), made monotone
+      P.b.assign(W + 1, 0);
+      P.b[W] = n;
+      bool ok = true;
+      for (int r = 1; r < W; ++r) {
+        const double hi_prev = all[2 * (r - 1) + 1], lo_here = all[2 * r];
+        if (hi_prev < 0 || lo_here >= (double)n) ok = false;   // a rank without entries
+        int64_t mid = (int64_t)std::floor((hi_prev + 1.0 + lo_here) / 2.0);
+        P.b[r] = std::max<int64_t>(P.b[r - 1], std::min<int64_t>(n, std::max<int64_t>(0, mid)));
+      }
+      for (int r = 0; r < W; ++r) ok = ok && P.b[r + 1] > P.b[r];
+      // this rank's windows: q = owned ∪ C's columns; p = q ∪ the columns of H's owned rows
+      int64_t qlo = std::min<int64_t>(P.b[g], (int64_t)cmin), qhi = std::max<int64_t>(P.b[g + 1], (int64_t)cmax + 1);
+      int64_t plo = qlo, phi = qhi;
+      for (int64_t i = P.b[g]; ok && i < P.b[g + 1]; ++i)
+        for (int64_t e = c->H.p[i]; e < c->H.p[i + 1]; ++e) {
+          plo = std::min<int64_t>(plo, c->H.i[e]);
+          phi = std::max<int64_t>(phi, (int64_t)c->H.i[e] + 1);
+        }
+      std::vector<double> wall;
+      if (int rc = gather_small(c, {(double)plo, (double)phi, (double)qlo, (double)qhi}, wall)) return rc;
+      P.plo.resize(W); P.phi.resize(W); P.qlo.resize(W); P.qhi.resize(W);
+      for (int r = 0; r < W; ++r) {
+        P.plo[r] = (int64_t)wall[4 * r];
+        P.phi[r] = (int64_t)wall[4 * r + 1];
+        P.qlo[r] = (int64_t)wall[4 * r + 2];
+        P.qhi[r] = (int64_t)wall[4 * r + 3];
+        // only the two neighbours' owned ranges may be reached
+        const int64_t left = P.b[std::max(0, r - 1)], right = P.b[std::min(W, r + 2)];
+        ok = ok && P.plo[r] >= left && P.phi[r] <= right && P.qlo[r] >= left && P.qhi[r] <= right;
+      }
+      {   // one decision for every rank (xbuf may not exist yet: through the small gather)
+        std::vector<double> oks;
+        if (int rc = gather_small(c, {ok ? 1.0 : 0.0}, oks)) return rc;
+        for (double v : oks) ok = ok && v > 0.5;
+      }
+      if (ok) {
+        const int64_t nfp = g > 0 ? std::max<int64_t>(0, P.qhi[g - 1] - P.b[g]) : 0;
+        const int64_t nfn = g + 1 < W ? std::max<int64_t>(0, P.b[g + 1] - P.qlo[g + 1]) : 0;
+        try {
+          P.from_prev = c->mem.zeros<double>((size_t)std::max<int64_t>(1, nfp), c->stream);
+          P.from_next = c->mem.zeros<double>((size_t)std::max<int64_t>(1, nfn), c->stream);
+        } catch (std::bad_alloc&) {
+          return fail(c, QP_ENOMEM, "cudaMalloc failed (halo buffers)");
+        }
+      }
+      P.enabled = ok;
+    }
+    P.planned = true;
+  }
+  for (int k = 0; k < 8; ++k) info[k] = 0;
+  info[0] = P.enabled ? 1 : 0;
+  if (P.enabled) {
+    info[1] = P.b[g];
+    info[2] = P.b[g + 1];
+    info[3] = P.plo[g];
+    info[4] = P.phi[g];
+    info[5] = P.qlo[g];
+    info[6] = P.qhi[g];
+    int64_t sent = 0;
+    if (g > 0) sent += std::max<int64_t>(0, P.phi[g - 1] - P.b[g]) + std::max<int64_t>(0, P.b[g] - P.qlo[g]);
+    if (g + 1 < W) sent += std::max<int64_t>(0, P.b[g + 1] - P.plo[g + 1]) + std::max<int64_t>(0, P.qhi[g] - P.b[g + 1]);
+    info[7] = sent;
+  }
+  return QP_OK;
+}
+
+int qp_operator_apply_halo(qp_ctx* c, const double* D, double* p, double* q) {
+  if (!c) return QP_EINVAL;
+  if (!c->setup_done) return fail(c, QP_ESTATE, "qp_setup has not completed");
+  auto& P = c->halo;
+  if (!P.planned || !P.enabled) return fail(c, QP_ESTATE, "no halo plan (qp_operator_halo_plan) or not band-local");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  const int W = c->world, g = c->rank;
+  const double* Dd = in_vec(c, D, c->op_D, c->m2);
+  double* pd = c->vectors_on_device ? p : c->op_p;
+  double* qd = c->vectors_on_device ? q : c->op_q;
+  if (!c->vectors_on_device)
+    cudaMemcpyAsync(pd + P.b[g], p + P.b[g], (P.b[g + 1] - P.b[g]) * 8, cudaMemcpyHostToDevice, st);
+  // 1. boundary entries of p: my owned entries inside the neighbours' windows go out, my window's
+  //    entries outside my owned range come in (in place: all ranges are contiguous)
+  const int64_t tp = g > 0 ? std::max<int64_t>(0, P.phi[g - 1] - P.b[g]) : 0;
+  const int64_t tn = g + 1 < W ? std::max<int64_t>(0, P.b[g + 1] - P.plo[g + 1]) : 0;
+  const int64_t fp = std::max<int64_t>(0, P.b[g] - P.plo[g]), fn = std::max<int64_t>(0, P.phi[g] - P.b[g + 1]);
+  if (int rc = c->exchange(pd + P.b[g], tp, pd + (P.b[g + 1] - tn), tn, pd + P.plo[g], fp, pd + P.b[g + 1], fn)) return rc;
+  // 2. local products on the windows
+  op_apply_range(c->opH, c->opC, c->opCt, Dd, pd, c->op_t, qd, P.qlo[g], P.qhi[g], P.b[g], P.b[g + 1], c->sm_count, st);
+  c->launches += 2;
+  // 3. q outside the owned range goes to its owner and is added there
+  const int64_t qtp = std::max<int64_t>(0, P.b[g] - P.qlo[g]), qtn = std::max<int64_t>(0, P.qhi[g] - P.b[g + 1]);
+  const int64_t qfp = g > 0 ? std::max<int64_t>(0, P.qhi[g - 1] - P.b[g]) : 0;
+  const int64_t qfn = g + 1 < W ? std::max<int64_t>(0, P.b[g + 1] - P.qlo[g + 1]) : 0;
+  if (int rc = c->exchange(qd + P.qlo[g], qtp, qd + P.b[g + 1], qtn, P.from_prev, qfp, P.from_next, qfn)) return rc;
+  add_range(qd + P.b[g], P.from_prev, qfp, st);
+  add_range(qd + (P.b[g + 1] - qfn), P.from_next, qfn, st);
+  c->launches += (qfp > 0) + (qfn > 0);
+  if (!c->vectors_on_device) {
+    cudaMemcpyAsync(p + P.plo[g], pd + P.plo[g], (P.phi[g] - P.plo[g]) * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(q + P.b[g], qd + P.b[g], (P.b[g + 1] - P.b[g]) * 8, cudaMemcpyDeviceToHost, st);
+  }
+  return sync_check(c, "qp_operator_apply_halo");
 }
 
 int qp_get_structure(qp_ctx* c, int32_t which, int64_t* out, int64_t* len) {

@@ -4013,6 +4013,34 @@ __global__ void __launch_bounds__(NT) k_op_q(DevCSR Hf, DevCSR Ctf, const double
     if (q4 == 0) q[i] = s;
   }
 }
+__global__ void __launch_bounds__(NT) k_op_q_range(DevCSR Hf, DevCSR Ctf, const double* p, const double* t, double* q,
+                                                   int64_t q_lo, int64_t q_hi, int64_t h_lo, int64_t h_hi) {
+  const int q4 = threadIdx.x & 3;
+  const int64_t nq = ((int64_t)gridDim.x * NT) >> 2;
+  for (int64_t i = q_lo + ((blockIdx.x * (int64_t)NT + threadIdx.x) >> 2); i < q_hi; i += nq) {
+    double s = 0.0;
+    if (i >= h_lo && i < h_hi)
+      for (int64_t e = __ldg(Hf.p + i) + q4; e < __ldg(Hf.p + i + 1); e += 4) s += __ldg(Hf.v + e) * __ldg(p + __ldg(Hf.i + e));
+    for (int64_t e = __ldg(Ctf.p + i) + q4; e < __ldg(Ctf.p + i + 1); e += 4) s += __ldg(Ctf.v + e) * __ldg(t + __ldg(Ctf.i + e));
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (q4 == 0) q[i] = s;
+  }
+}
+__global__ void __launch_bounds__(NT) k_add_range(double* dst, const double* src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) dst[i] += src[i];
+}
+void op_apply_range(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* D, const double* p, double* t,
+                    double* q, int64_t q_lo, int64_t q_hi, int64_t h_lo, int64_t h_hi, int sms, cudaStream_t s) {
+  const int g = sms * 8;
+  k_op_t<<<g, NT, 0, s>>>(Cf, D, p, t);
+  k_op_q_range<<<g, NT, 0, s>>>(Hf, Ctf, p, t, q, q_lo, q_hi, h_lo, h_hi);
+}
+void add_range(double* dst, const double* src, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + NT - 1) / NT, 148 * 8));
+  k_add_range<<<g, NT, 0, s>>>(dst, src, n);
+}
 void op_apply(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* D, const double* p, double* t,
               double* q, bool with_h, int sms, cudaStream_t s) {
   const int g = sms * 8;

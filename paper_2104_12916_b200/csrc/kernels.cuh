@@ -236,6 +236,11 @@ void trsv_forward(const DevFactor& F, const SweepRhs& r, double* x, int grid, cu
 // q = H p (with_h) + Cᵀ(D⁻¹∘(C p)) in two streaming passes (t: m2 scratch), natural order, no factor
 void op_apply(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* D, const double* p, double* t,
               double* q, bool with_h, int sms, cudaStream_t s);
+// halo mode: q[i] = (H p)_i for i in [h_lo, h_hi) (else 0) + (Cᵀ t)_i, rows [q_lo, q_hi) only
+void op_apply_range(const DevCSR& Hf, const DevCSR& Cf, const DevCSR& Ctf, const double* D, const double* p, double* t,
+                    double* q, int64_t q_lo, int64_t q_hi, int64_t h_lo, int64_t h_hi, int sms, cudaStream_t s);
+// dst[0, n) += src[0, n)
+void add_range(double* dst, const double* src, int64_t n, cudaStream_t s);
 // v[0, N) = the right-hand side described by r, out[0, N) = 0 (dense F⁻¹ mode)
 void gather_rhs(const SweepRhs& r, double* v, double* out, int64_t N, int sms, cudaStream_t s);
 // v[0, n) = 0 unless *done_flag

@@ -53,6 +53,36 @@ class ThreadComm:
             return int(err)
         return allreduce
 
+    def halo(self, rank):
+        """qp_halo_fn for threads: every rank posts what it sends, then reads what its neighbours posted."""
+        from cuda.bindings import runtime as rt
+
+        def d2h(ptr, n):
+            host = np.empty(n)
+            if n:
+                (err,) = rt.cudaMemcpy(host.ctypes.data, ptr, n * 8, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+                assert int(err) == 0, err
+            return host
+
+        def exchange(to_prev, n_tp, to_next, n_tn, from_prev, n_fp, from_next, n_fn, stream):
+            (err,) = rt.cudaStreamSynchronize(stream)
+            assert int(err) == 0, err
+            self.slots[rank] = (d2h(to_prev, n_tp), d2h(to_next, n_tn))
+            self.bar.wait()
+            if n_fp:
+                src = self.slots[rank - 1][1]
+                assert len(src) == n_fp
+                (err,) = rt.cudaMemcpy(from_prev, src.ctypes.data, n_fp * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+                assert int(err) == 0, err
+            if n_fn:
+                src = self.slots[rank + 1][0]
+                assert len(src) == n_fn
+                (err,) = rt.cudaMemcpy(from_next, src.ctypes.data, n_fn * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+                assert int(err) == 0, err
+            self.bar.wait()
+            return 0
+        return exchange
+
 
 def run_ranks(world, body):
     """body(rank, comm) in `world` threads; returns the per-rank results (re-raises errors)."""
@@ -227,3 +257,60 @@ def test_sharded_dense_w_ipm_matches_oracle(monkeypatch):
         assert r["converged"]
         assert abs(r["objective"] - ref.objective) <= 1e-8 * max(1.0, abs(ref.objective))
     assert res[0]["pcg_iters"] == res[1]["pcg_iters"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_operator_halo_mode_matches_oracle(world):
+    """Halo mode of the sharded operator (qp_operator_apply_halo; BJ configs[4], north_star "boundary entries
+    of p are exchanged"): on a band-local grid QP every rank plans the same owned ranges and windows as the
+    oracle's definition (oracle.sharded.halo_plan, bit-exact), its product equals H p + Cᵀ D⁻¹ C p on the
+    owned range (1e-12), only the owned entries of p are read, and it sends far fewer than n doubles."""
+    from oracle.sharded import halo_plan, partition_rows
+    from paper_2104_12916_b200.binding import from_qp
+    qp = qpgen.make_grid_qp(24, 16, 0, seed=5, name="band24", band=8, m2_band=1500)
+    C = qp.C.tocsr()
+    rng = np.random.default_rng(3)
+    D = rng.uniform(0.5, 2.0, qp.m2)
+    p = rng.standard_normal(qp.n)
+    ref = qp.H @ p + C.T @ ((C @ p) / D)
+    oplan = halo_plan(qp.H, C, partition_rows(C.indptr, qp.m2, world), world)
+    assert oplan["enabled"]
+
+    def body(rank, comm):
+        s = from_qp(qp, rank=rank, world=world, allreduce=comm.fn(rank), halo=comm.halo(rank))
+        plan = s.operator_halo_plan()
+        lo, hi = plan["own"]
+        pin = np.full(qp.n, 1e300)         # poison: only the owned entries may be used as given
+        pin[lo:hi] = p[lo:hi]
+        q, pw = s.operator_apply_halo(D[s.row0:s.row0 + s.m2], pin)
+        q_ar = s.operator_apply(D[s.row0:s.row0 + s.m2], p)     # the all-reduce path, same context
+        s.close()
+        return plan, q[lo:hi], pw, q_ar
+    res = run_ranks(world, body)
+    for g, (plan, qg, pw, q_ar) in enumerate(res):
+        assert plan["enabled"]
+        assert plan["own"] == (int(oplan["b"][g]), int(oplan["b"][g + 1]))
+        assert plan["p_window"] == (int(oplan["p_lo"][g]), int(oplan["p_hi"][g]))
+        assert plan["q_window"] == (int(oplan["q_lo"][g]), int(oplan["q_hi"][g]))
+        a, b = plan["p_window"]
+        assert np.array_equal(pw[a:b], p[a:b])                   # the window of p was filled exactly
+        assert plan["sent_doubles"] < qp.n // 2
+        assert np.linalg.norm(q_ar - ref) <= 1e-12 * np.linalg.norm(ref)
+    got = np.concatenate([r[1] for r in res])
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_operator_halo_mode_rejected_for_random_rows():
+    """c0's rows of C reach all of x: with 4 ranks the plan is disabled on every rank and the halo call
+    returns QP_ESTATE; the all-reduce path still serves."""
+    from paper_2104_12916_b200.binding import QPError, from_qp
+    qp = qpgen.make("c0")
+
+    def body(rank, comm):
+        s = from_qp(qp, rank=rank, world=4, allreduce=comm.fn(rank), halo=comm.halo(rank))
+        plan = s.operator_halo_plan()
+        with pytest.raises(QPError):
+            s.operator_apply_halo(np.ones(s.m2), np.zeros(qp.n))
+        s.close()
+        return plan["enabled"]
+    assert run_ranks(4, body) == [False] * 4
