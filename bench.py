@@ -306,7 +306,7 @@ def measure_secondary(cfg, args, local, stream, peak, peak_src):
     ach_it = pcg * b_it / (ms / 1e3) / 1e9 if ms > 0 else 0.0
     fsolve_ms = fwd_ms + bwd_ms + root_ms
     if st.get("pi_enabled"):   # level products: leaf levels / subtrees, then one product kernel per level
-        leaf = "k_st_fwd" if st.get("pi_subtrees") else "k_lvl_fwd x%d" % int(st["lvl_levels_F"])
+        leaf = "k_st16_fwd" if st.get("pi_subtrees") else "k_lvl_fwd x%d" % int(st["lvl_levels_F"])
         kf = "k_pi_init + %s + k_pi_fwd x%d levels" % (leaf, int(st["pi_levels"]))
         kb = "k_pi_bwd x%d levels + %s" % (int(st["pi_levels"]), leaf.replace("fwd", "bwd"))
     else:

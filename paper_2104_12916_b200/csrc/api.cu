@@ -2976,7 +2976,9 @@ int qp_get_stats(qp_ctx* c, qp_stats* s) {
     s->lvl_supernodes_PH = c->FP.S.lvl_blk.size();
     s->pi_enabled = c->FF.pi.enabled ? 1.0 : 0.0;
     s->pi_discrepancy = c->FF.pi_discrepancy;
-    s->pi_levels = c->FF.pi.enabled ? c->FF.pi.nlev : 0;
+    s->pi_levels = 0;
+    for (int L = 0; c->FF.pi.enabled && L < c->FF.pi.nlev; ++L)
+      s->pi_levels += c->FF.pi.lev_ptr[L + 1] > c->FF.pi.lev_ptr[L] ? 1 : 0;   // non-empty levels = launches per sweep
     s->pi_subtrees = c->FF.pi.enabled ? (double)c->FF.pi.st_n : 0.0;
     s->pi_fsolve_ms = c->FF.pi_ms[1];
     s->sweep_fsolve_ms = c->FF.pi_ms[0];

@@ -2714,28 +2714,38 @@ __device__ __forceinline__ double pi_rhs(const SweepRhs& R, int64_t c) {
   if (R.ct.p != nullptr) return c < R.ct.nrows ? csr_dot(R.ct, c, R.p) : 0.0;
   return R.rhs[R.in_perm ? R.in_perm[c] : c];
 }
+__device__ __forceinline__ void pi_prefetch_strip(const double* Z, const PiTile& T) {
+  const int lane = threadIdx.x & 31;   // 64 rows = 4 lines per column
+  for (int i = lane; i < T.nc * 4; i += 32)
+    if ((i & 3) * 16 < T.nr) prefetch_l2(Z + T.zoff + (int64_t)(i >> 2) * T.ld + (i & 3) * 16);
+}
+// Everything that does not depend on the previous level — the tile descriptor, the row indices and (pf) an
+// L2 prefetch of the tile's part of Z — happens BEFORE griddepcontrol.wait: with programmatic dependent
+// launch the next level's CTAs are already resident while the current level drains, and what remains after
+// the wait is the dependent gather and a stream from L2.
 __global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const PiTile* tiles, int nbig, int nstrip,
                                                   const double* Z, int pf) {
-  grid_dep_wait();
   grid_dep_launch();
-  if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
-  const unsigned tls = tl_begin(5);
   __shared__ double v[64];
   const int tid = threadIdx.x;
+  unsigned tls = 0;
   if ((int)blockIdx.x < nbig) {
     const PiTile T = pi_load_tile(tiles + blockIdx.x);
+    const int r = 2 * tid;
+    const bool ok = r < T.nr, two = r + 1 < T.nr;
+    const int32_t* rows = F.sn_rows + T.roff + r;
+    const int32_t g0 = ok ? __ldg(rows) : 0, g1 = two ? __ldg(rows + 1) : 0;
     if (pf) pi_prefetch(Z, T);
+    grid_dep_wait();
+    if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+    tls = tl_begin(5);
     if (tid < T.nc) {
       const int64_t c = (int64_t)T.col0 + tid;
       v[tid] = pi_rhs(R, c) - __ldcg(F.acc + c);
     }
     __syncthreads();
-    const int r = 2 * tid;
-    if (r < T.nr) {
+    if (ok) {
       const double* zp = Z + T.zoff + r;
-      const int32_t* rows = F.sn_rows + T.roff + r;
-      const bool two = r + 1 < T.nr;
-      const int32_t g0 = __ldg(rows), g1 = two ? __ldg(rows + 1) : 0;
       double s0 = 0.0, s1 = 0.0;
       const int64_t ld = T.ld;
 #pragma unroll 8
@@ -2751,16 +2761,26 @@ __global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const
   } else {
     const int lane = tid & 31;
     const int si = ((int)blockIdx.x - nbig) * (NT / 32) + (tid >> 5);
-    if (si < nstrip) {
-      const PiTile T = pi_load_tile(tiles + nbig + si);
+    const bool live = si < nstrip;
+    PiTile T{};
+    int32_t g0 = 0, g1 = 0;
+    if (live) {
+      T = pi_load_tile(tiles + nbig + si);
+      const int32_t* rows = F.sn_rows + T.roff + 2 * lane;
+      g0 = 2 * lane < T.nr ? __ldg(rows) : 0;
+      g1 = 2 * lane + 1 < T.nr ? __ldg(rows + 1) : 0;
+      if (pf) pi_prefetch_strip(Z, T);
+    }
+    grid_dep_wait();
+    if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
+    tls = tl_begin(5);
+    if (live) {
       const int64_t c = (int64_t)T.col0 + lane;
       const double vlo = lane < T.nc ? pi_rhs(R, c) - __ldcg(F.acc + c) : 0.0;
       const double vhi = lane + 32 < T.nc ? pi_rhs(R, c + 32) - __ldcg(F.acc + c + 32) : 0.0;
       const int r = 2 * lane;
       const bool ok = r < T.nr, two = r + 1 < T.nr;
       const double* zp = Z + T.zoff + (ok ? r : 0);
-      const int32_t* rows = F.sn_rows + T.roff + r;
-      const int32_t g0 = ok ? __ldg(rows) : 0, g1 = two ? __ldg(rows + 1) : 0;
       double s0 = 0.0, s1 = 0.0;
       const int64_t ld = T.ld;
 #pragma unroll 8
@@ -2779,22 +2799,25 @@ __global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const
   tl_end(5, tls);
 }
 // Backward, one level: s = D⁻¹y on the tile's own rows, −x on its external rows; x_cols += Z_tileᵀ s.
-__device__ __forceinline__ double pi_sval(const DevFactor& F, const PiTile& T, const double* x, int r) {
-  const int32_t g = __ldg(F.sn_rows + T.roff + r);
+__device__ __forceinline__ double pi_sval_g(const DevFactor& F, const PiTile& T, const double* x, int r, int32_t g) {
   return r < T.wx ? __ldcg(F.tacc + g) / __ldg(F.Dpiv + g) : -__ldcg(x + g);
 }
 __global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* tiles, int nbig, int nstrip, const double* Z,
                                                   double* x, const int* done_flag, int pf) {
-  grid_dep_wait();
   grid_dep_launch();
-  if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
-  const unsigned tls = tl_begin(6);
   __shared__ double s[512 + 2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned tls = 0;
   if ((int)blockIdx.x < nbig) {
     const PiTile T = pi_load_tile(tiles + blockIdx.x);
+    const int32_t ga = tid < T.nr ? __ldg(F.sn_rows + T.roff + tid) : 0;
+    const int32_t gb = tid + NT < T.nr ? __ldg(F.sn_rows + T.roff + tid + NT) : 0;
     if (pf) pi_prefetch(Z, T);
-    for (int r = tid; r < ((T.nr + 1) & ~1); r += NT) s[r] = r < T.nr ? pi_sval(F, T, x, r) : 0.0;
+    grid_dep_wait();
+    if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+    tls = tl_begin(6);
+    s[tid] = tid < T.nr ? pi_sval_g(F, T, x, tid, ga) : 0.0;
+    s[tid + NT] = tid + NT < T.nr ? pi_sval_g(F, T, x, tid + NT, gb) : 0.0;
     __syncthreads();
     double t[8];
 #pragma unroll
@@ -2833,12 +2856,23 @@ __global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* til
     }
   } else {
     const int si = ((int)blockIdx.x - nbig) * (NT / 32) + wid;
-    if (si < nstrip) {
-      const PiTile T = pi_load_tile(tiles + nbig + si);
+    const bool live = si < nstrip;
+    PiTile T{};
+    int32_t g0 = 0, g1 = 0;
+    if (live) {
+      T = pi_load_tile(tiles + nbig + si);
+      g0 = 2 * lane < T.nr ? __ldg(F.sn_rows + T.roff + 2 * lane) : 0;
+      g1 = 2 * lane + 1 < T.nr ? __ldg(F.sn_rows + T.roff + 2 * lane + 1) : 0;
+      if (pf) pi_prefetch_strip(Z, T);
+    }
+    grid_dep_wait();
+    if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
+    tls = tl_begin(6);
+    if (live) {
       const int r = 2 * lane;
       const bool ok = r < T.nr;
-      const double s0 = ok ? pi_sval(F, T, x, r) : 0.0;
-      const double s1 = r + 1 < T.nr ? pi_sval(F, T, x, r + 1) : 0.0;
+      const double s0 = ok ? pi_sval_g(F, T, x, r, g0) : 0.0;
+      const double s1 = r + 1 < T.nr ? pi_sval_g(F, T, x, r + 1, g1) : 0.0;
       const double* zp = Z + T.zoff + (ok ? r : 0);
       const int64_t ld = T.ld;
       for (int cb = 0; cb < T.nc; cb += 16) {
