@@ -1859,10 +1859,14 @@ int build_pi(qp_ctx* c) {
   // Tile shapes: a supernode with ≤ `short` rows is cut into strips of 64 rows (a warp each, 8 per CTA); taller
   // ones into CTA tiles of 512 rows × 64 columns.  The backward product takes strips up to 640 rows (a CTA
   // tile there first gathers its 512 inputs, then streams), the forward product up to 320 (measured on c2).
-  // QPB_PI_NC < 64 narrows the CTA tiles (measured slower: more tiles re-gather their inputs).
   const int64_t short_f = std::getenv("QPB_PI_SHORT") ? std::atoll(std::getenv("QPB_PI_SHORT")) : 320;
   const int64_t short_b = std::getenv("QPB_PI_SHORT_B") ? std::atoll(std::getenv("QPB_PI_SHORT_B")) : 640;
-  const int64_t ncw = std::getenv("QPB_PI_NC") ? std::max<int64_t>(16, std::min<int64_t>(64, std::atoll(std::getenv("QPB_PI_NC")))) : 64;
+  // CTA-tile width: 64 columns, halved (to ≥ 16) while a level has fewer than 2 CTA tiles per SM: a lone CTA
+  // keeps only 32 KB in flight, so a level of one or two wide supernodes (the top of the tree) is bound by
+  // per-CTA memory parallelism, not bandwidth (c4s: 13 → 7 µs per top level, 0.59 → 0.49 ms per PCG
+  // iteration; c2's levels 18–19 11.7 → 9.4 µs forward, 18.8 → 13.5 µs backward).  Levels that already fill
+  // the GPU get slower with narrower tiles (every tile re-gathers its inputs).  QPB_PI_NC forces a width.
+  const int64_t nc_force = std::getenv("QPB_PI_NC") ? std::max<int64_t>(16, std::min<int64_t>(64, std::atoll(std::getenv("QPB_PI_NC")))) : 0;
   std::vector<PiTile> btiles;
   bool too_big = false;
   auto plan = [&](int64_t pi_short, std::vector<PiTile>& out, std::vector<int32_t>* outJ, int64_t* ptr, int64_t* sptr,
@@ -1871,6 +1875,16 @@ int build_pi(qp_ctx* c) {
     ptr[0] = 0;
     for (int L = 0; L < nlev; ++L) {
       std::vector<std::pair<PiTile, int32_t>> lt, ls;
+      int64_t ncw = nc_force > 0 ? nc_force : 64;
+      for (; nc_force == 0 && ncw > 16; ncw /= 2) {
+        int64_t nt = 0;
+        for (int32_t J : by[L]) {
+          const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
+          if (m <= pi_short) continue;
+          for (int64_t c0 = 0; c0 < w; c0 += ncw) nt += (m - (c0 & ~int64_t(63)) + 511) / 512;
+        }
+        if (nt == 0 || nt >= 2 * (int64_t)c->sm_count) break;
+      }
       for (int32_t J : by[L]) {
         const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J];
         const int64_t ld = (m + 1) & ~int64_t(1);
