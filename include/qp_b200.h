@@ -79,7 +79,10 @@ typedef enum {
 /* Cross-rank collective used by the sharded mode instead of NCCL (optional).
  * In-place all-reduce of `count` doubles at DEVICE pointer buf, ordered on the
  * cudaStream_t `stream` (the call may synchronise it); op: 0 sum, 1 max, 2 min.
- * Every rank must produce bit-identical results.  Return 0 on success. */
+ * Every rank must produce bit-identical results.  The reduced values must be visible to work enqueued on
+ * `stream` after the call returns: write them with cudaMemcpyAsync on `stream` (and synchronise it), not
+ * with a plain cudaMemcpy from pageable memory — that may return before its DMA lands and is not ordered
+ * with a non-blocking stream.  Return 0 on success. */
 typedef int (*qp_allreduce_fn)(void* user, double* buf, int64_t count, int32_t op, void* stream);
 
 /* Neighbour exchange used by the halo mode of the sharded operator instead of NCCL send/recv (optional;

@@ -1933,7 +1933,9 @@ int build_pi(qp_ctx* c) {
     F.pi = PiSweep{};
     return QP_OK;
   }
-  F.pi.prefetch = std::getenv("QPB_PI_PF") && std::getenv("QPB_PI_PF")[0] == '1';   // measured slower on c2 (0.984 -> 1.009 ms per PCG iteration)
+  // before the wait: 2 (default) = the lines of each thread's first batch of loads and whole strips into L2 (c4s 0.489 -> 0.472 ms,
+  // c2 0.898 -> 0.896 ms); 1 = the whole CTA tile (c2 0.917 -> 0.981 ms: it floods L2 ahead of the streaming loads); 0 = none
+  F.pi.prefetch = std::getenv("QPB_PI_PF") ? std::atoi(std::getenv("QPB_PI_PF")) : 2;
   if (tiles.empty()) return QP_OK;
   cudaStream_t st = c->stream;
   int64_t* zoff_dev = nullptr;

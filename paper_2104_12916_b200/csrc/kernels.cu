@@ -2735,7 +2735,12 @@ __global__ void __launch_bounds__(NT, 4) k_pi_fwd(DevFactor F, SweepRhs R, const
     const bool ok = r < T.nr, two = r + 1 < T.nr;
     const int32_t* rows = F.sn_rows + T.roff + r;
     const int32_t g0 = ok ? __ldg(rows) : 0, g1 = two ? __ldg(rows + 1) : 0;
-    if (pf) pi_prefetch(Z, T);
+    if (pf == 1) pi_prefetch(Z, T);
+    if (pf == 2 && ok && (tid & 7) == 0) {   // the lines of the first batch of loads only (one lane per 128-byte line)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < T.nc) prefetch_l2(Z + T.zoff + r + (int64_t)c * T.ld);
+    }
     grid_dep_wait();
     if (R.done_flag != nullptr && *((volatile const int*)R.done_flag)) return;
     tls = tl_begin(5);
@@ -2812,7 +2817,12 @@ __global__ void __launch_bounds__(NT, 4) k_pi_bwd(DevFactor F, const PiTile* til
     const PiTile T = pi_load_tile(tiles + blockIdx.x);
     const int32_t ga = tid < T.nr ? __ldg(F.sn_rows + T.roff + tid) : 0;
     const int32_t gb = tid + NT < T.nr ? __ldg(F.sn_rows + T.roff + tid + NT) : 0;
-    if (pf) pi_prefetch(Z, T);
+    if (pf == 1) pi_prefetch(Z, T);
+    if (pf == 2 && (lane & 7) == 0 && 2 * lane < T.nr) {   // first batch: rows 2·lane.., columns wid + 8k
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (wid + 8 * k < T.nc) prefetch_l2(Z + T.zoff + 2 * lane + (int64_t)(wid + 8 * k) * T.ld);
+    }
     grid_dep_wait();
     if (done_flag != nullptr && *((volatile const int*)done_flag)) return;
     tls = tl_begin(6);

@@ -10,6 +10,7 @@ inputs of ``qpgen.probe_inputs`` (D with a six-decade spread, N(0,1) vectors):
 * ``PLeps``    the P_L PCG iteration count at ε = 1e-3 and its solution's samples;
 * ``PH<k>``, ``PHeps``  the same with P_H = D + C diag(H)⁻¹Cᵀ where the oracle can
                factor P_H (c1 dense LAPACK, c4s SuperLU in the banded row order);
+* ``PLeps_var`` the ε = 1e-3 P_L count with b perturbed by 1e-15 relative (seeds 1–4): the rounding spread;
 * ``ipm_pl``   the oracle PL-KF IPM's first 15 iterations (μ, residual norms, α, PCG counts);
 * ``ipm_pl_var`` the same with r_ν perturbed by 1e-15 (seeds 1–4): the rounding spread of the counts;
 * ``ipm_ph``   the oracle PH-KF IPM at ipm_tol 1e-10 (objective, counts, trace) — c4s;
@@ -121,6 +122,19 @@ def main():
         pay.update(eps_iters=it, eps_relres=rr, eps_converged=int(ok))
         log(name, "eps count", it, "relres", rr)
         save(cfg, name, pay)
+    if "PLeps_var" in stages:
+        # rounding-level variants of the ε-count solve: b perturbed by 1e-15 relative (seeds 1..4), the same
+        # perturbation the IPM variants apply to r_ν — what rounding alone does to the count (reading R12)
+        pay = {}
+        M = kkt.PrecondL(pr.D)
+        for v in VARIANTS:
+            bv = pr.b * (1.0 + 1e-15 * np.random.default_rng([v, 0]).standard_normal(len(pr.b)))
+            t = time.time()
+            x, it, rr, ok, _ = pcg(Kop, bv, M, 1e-3, 2000)
+            meta[f"t_PLeps_var{v}_s"] = time.time() - t
+            pay[f"eps_iters_v{v}"] = it
+            log("PLeps variant", v, "count", it)
+        save(cfg, "PLeps_var", pay)
     if "ipm_pl" in stages:
         t = time.time()
         r = ipm_solve(qp, precond="low", max_ipm=15, fs=fs)

@@ -40,7 +40,13 @@ def main():
             return int(err)
         t = torch.from_numpy(host)
         dist.all_reduce(t, op=ops[op])
-        (err,) = rt.cudaMemcpy(buf, t.numpy().ctypes.data, count * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+        # back on the caller's stream, and complete before returning: a plain cudaMemcpy from pageable memory
+        # may return before its DMA lands and is not ordered with the library's non-blocking stream
+        (err,) = rt.cudaMemcpyAsync(buf, t.numpy().ctypes.data, count * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice,
+                                    stream)
+        if int(err):
+            return int(err)
+        (err,) = rt.cudaStreamSynchronize(stream)
         return int(err)
 
     qp = qpgen.make("c0") if case == "c0" else qpgen.scaled_random_qp(700, 130, 900, seed=3)

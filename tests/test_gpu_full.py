@@ -123,7 +123,10 @@ def test_full_pcg_count_at_eps(cfg, prec):
     stage = "PL" if prec == "low" else "PH"
     x, it, rr, rc = s.pcg_solve(pr.D, pr.b, tol=1e-3, maxit=2000)
     ito = int(z[f"{stage}/eps_iters"])
-    assert abs(it - ito) <= 2, (it, ito)
+    # the band of the oracle's own rounding-level variants (b perturbed by 1e-15 relative; reading R12),
+    # where the golden holds them: counts of a few hundred steps move by ±3 with the summation order alone
+    vs = [int(z[k]) for k in z.files if prec == "low" and k.startswith("PLeps_var/eps_iters_v")]
+    assert min([ito] + vs) - 2 <= it <= max([ito] + vs) + 2, (it, ito, vs)
     assert rr <= 1e-3
     if it == ito:
         _cmp(x, z, stage, pr.idx_m2, "eps", tol=1e-4)

@@ -49,7 +49,12 @@ class ThreadComm:
                 res = res + self.slots[r] if op == 0 else (np.maximum(res, self.slots[r]) if op == 1
                                                            else np.minimum(res, self.slots[r]))
             self.bar.wait()
-            (err,) = rt.cudaMemcpy(buf, res.ctypes.data, count * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+            # on the caller's stream and complete before returning (a plain cudaMemcpy from pageable memory may
+            # return before its DMA lands and is not ordered with the library's non-blocking stream)
+            (err,) = rt.cudaMemcpyAsync(buf, res.ctypes.data, count * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice,
+                                        stream)
+            assert int(err) == 0, err
+            (err,) = rt.cudaStreamSynchronize(stream)
             return int(err)
         return allreduce
 
@@ -72,13 +77,17 @@ class ThreadComm:
             if n_fp:
                 src = self.slots[rank - 1][1]
                 assert len(src) == n_fp
-                (err,) = rt.cudaMemcpy(from_prev, src.ctypes.data, n_fp * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+                (err,) = rt.cudaMemcpyAsync(from_prev, src.ctypes.data, n_fp * 8,
+                                            rt.cudaMemcpyKind.cudaMemcpyHostToDevice, stream)
                 assert int(err) == 0, err
             if n_fn:
                 src = self.slots[rank + 1][0]
                 assert len(src) == n_fn
-                (err,) = rt.cudaMemcpy(from_next, src.ctypes.data, n_fn * 8, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+                (err,) = rt.cudaMemcpyAsync(from_next, src.ctypes.data, n_fn * 8,
+                                            rt.cudaMemcpyKind.cudaMemcpyHostToDevice, stream)
                 assert int(err) == 0, err
+            (err,) = rt.cudaStreamSynchronize(stream)
+            assert int(err) == 0, err
             self.bar.wait()
             return 0
         return exchange
