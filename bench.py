@@ -305,6 +305,12 @@ def measure_secondary(cfg, args, local, stream, peak, peak_src):
     value = pcg / (ms / 1e3) if ms > 0 else 0.0
     ach_it = pcg * b_it / (ms / 1e3) / 1e9 if ms > 0 else 0.0
     fsolve_ms = fwd_ms + bwd_ms + root_ms
+    traffic = None
+    if os.path.exists(args.profile_traffic):
+        try:
+            traffic = json.load(open(args.profile_traffic)).get(cfg, {}).get("dram_bytes_per_fsolve")
+        except Exception:
+            traffic = None
     if st.get("pi_enabled"):   # level products: leaf levels / subtrees, then one product kernel per level
         leaf = "k_st16_fwd" if st.get("pi_subtrees") else "k_lvl_fwd x%d" % int(st["lvl_levels_F"])
         kf = "k_pi_init + %s + k_pi_fwd x%d levels" % (leaf, int(st["pi_levels"]))
@@ -327,6 +333,11 @@ def measure_secondary(cfg, args, local, stream, peak, peak_src):
                      "achieved": gbs(st["fsolve_bytes_F"], fsolve_ms),
                      "frac": (gbs(st["fsolve_bytes_F"], fsolve_ms) or 0) / peak,
                      "algorithmic_bytes_per_fsolve": st["fsolve_bytes_F"],
+                     "traffic": traffic if st.get("pi_enabled") else None,
+                     "traffic_note": "DRAM read + write bytes of one F-solve from the ncu --set full capture in "
+                                     "profiles/r2_ncu_c2_levels.txt (level products: the panels Z_J hold L_JJ^-1 as "
+                                     "full w x w squares and the relaxed supernodes' explicit zeros (stored 2.23e8 entries against 2.09e8 true), "
+                                     "plus row lists and the vector gathers: +24 % over the algorithmic bytes, no re-reads)",
                      "per_kernel": {"forward": {"kernels": kf, "bytes": forest_bytes, "ms": fwd_ms / max(1, solves),
                                                 "GBps": gbs(forest_bytes, fwd_ms)},
                                     "k_symroot_gemv": {"bytes": root_bytes, "ms": root_ms / max(1, solves),

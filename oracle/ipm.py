@@ -52,7 +52,8 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
               pcg_maxit: Optional[int] = None, fs=None, x_perm=None, record: bool = False,
               exact_ph: bool = False, direct: bool = False, forcing: bool = True,
               space: str = "nu", ph_opts: Optional[dict] = None,
-              rnu_perturb: Optional[int] = None, consistent: Optional[str] = None) -> IpmResult:
+              rnu_perturb: Optional[int] = None, consistent: Optional[str] = None,
+              rnu_perturb_mag: float = 1e-15) -> IpmResult:
     """Run the single-factorization inexact IPM.
 
     precond ∈ {"none" (U-KF), "low" (PL-KF), "high" (PH-KF)}.
@@ -117,7 +118,7 @@ def ipm_solve(qp, precond: str = "low", pcg_tol: float = 1e-3, ipm_tol: float = 
         rnu = kkt.r_nu(qp, fs, res)
         if rnu_perturb is not None:
             prng = np.random.default_rng([rnu_perturb, k])
-            rnu = rnu * (1.0 + 1e-15 * prng.standard_normal(m2))
+            rnu = rnu * (1.0 + rnu_perturb_mag * prng.standard_normal(m2))
         if direct:
             if getattr(fs, "W", None) is not None:
                 # K_F = D − C W Cᵀ with the written-out W = (F⁻¹)₁₁; C W Cᵀ is D-independent

@@ -150,7 +150,8 @@ def main():
         vmax = int(os.environ.get("GOLD_VAR_MAXIPM", "15"))   # the count gate covers counts ≤ 100 only
         for v in VARIANTS:
             t = time.time()
-            r = ipm_solve(qp, precond="low", max_ipm=vmax, fs=fs, rnu_perturb=v)
+            r = ipm_solve(qp, precond="low", max_ipm=vmax, fs=fs, rnu_perturb=v,
+                          rnu_perturb_mag=float(os.environ.get("GOLD_VAR_MAG", "1e-15")))   # reading R12: 1e-15 or 1e-14
             meta[f"t_ipm_pl_var{v}_s"] = time.time() - t
             pay[f"pcg_v{v}"] = [d["pcg"] for d in r.trace]
             pay[f"mu_v{v}"] = [d["mu"] for d in r.trace]

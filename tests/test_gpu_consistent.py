@@ -9,6 +9,7 @@ rounding, R12)."""
 import os
 import sys
 
+import numpy as np
 import pytest
 
 import qpgen
@@ -33,6 +34,12 @@ def test_consistent_pl_c0_matches_oracle():
     routes = [DenseF(qp.H, qp.A), BlockF(qp.H, qp.A), DenseF(qp.H, qp.A, explicit_w=True)]
     for k, ((D, rnu, eps), g) in enumerate(zip(got["systems"], got["pl_counts"])):
         its = [pcg(lambda p: kkt.KF_apply(qp, fs, D, p), rnu, kkt.PrecondL(D), eps, 2000)[1] for fs in routes]
+        # the rest of reading R12's band: r_ν perturbed by 1e-15 and 1e-14 relative (the three exact routes
+        # can agree on a count that rounding-level noise moves by 2: system 4 gives 54–56 around their 55)
+        for seed in (1, 2, 3):
+            for mag in (1e-15, 1e-14):
+                r2 = rnu * (1.0 + mag * np.random.default_rng([seed, k]).standard_normal(len(rnu)))
+                its.append(pcg(lambda p: kkt.KF_apply(qp, routes[0], D, p), r2, kkt.PrecondL(D), eps, 2000)[1])
         if min(its) > bound:
             continue
         assert min(its) - 2 <= g <= max(its) + 2, (k, g, its)
