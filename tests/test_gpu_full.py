@@ -205,3 +205,34 @@ def test_full_pcg_count_same_system(cfg, k):
     assert it > 150, it
     assert min(counts) - 2 <= it <= max(counts) + 2, (it, counts)
     assert min(counts) - 2 <= r["pcg_iters"][-1] <= max(counts) + 2, (r["pcg_iters"][-1], counts)
+
+
+@pytest.mark.parametrize("mode", ["2", "0"])
+@pytest.mark.parametrize("cfg", ["c3s", "c4s", "c2"])
+def test_full_sweep_paths_both_match_oracle(cfg, mode, monkeypatch):
+    """The two F-solve paths of deep sparse factors — level products with subtrees (QPB_PI=2, forced) and the
+    task-graph sweeps (QPB_PI=0) — each against the oracle's F-solve and K_F product at full size, whichever
+    of them the factor-time timing would pick on this box (DESIGN §5 "level products")."""
+    from paper_2104_12916_b200.binding import from_qp
+    for k in list(_CACHE):
+        _CACHE.pop(k)[2].close()
+    monkeypatch.setenv("QPB_PI", mode)
+    z = golden(cfg)
+    qp = qpgen.make(cfg)
+    pr = qpgen.probe_inputs(qp)
+    s = from_qp(qp)
+    try:
+        s.ipm_factor_once("low")
+        st = s.stats()
+        assert st["pi_enabled"] == (1.0 if mode == "2" else 0.0)
+        if mode == "2":
+            assert st["pi_discrepancy"] <= 1e-10 and st["pi_levels"] >= 2
+        y, zz = s.f_solve(pr.f)
+        _cmp(np.concatenate([y, zz]), z, "F", pr.idx_F)
+        q = s.kf_apply(pr.D, pr.p)
+        _cmp(q, z, "KF", pr.idx_m2)
+        x, it, rr, rc = s.pcg_solve(pr.D, pr.b, tol=0.0, maxit=7)      # the fused step's phase D (next_rhs = 4 / 2)
+        assert it == 7
+        _cmp(x, z, "PL", pr.idx_m2, "k7")
+    finally:
+        s.close()
