@@ -121,7 +121,7 @@ def test_path_variant_matches_oracle(oracle_case, variant):
 PI_ENV = {"QPB_PI_MINN": "0", "QPB_DENSE_FINV": "0", "QPB_DENSE_W": "0", "QPB_FLAT": "0", "QPB_PI": "2"}
 
 
-@pytest.mark.parametrize("variant", ["subtrees", "subtrees32", "leaf_phase", "all_levels", "off"])
+@pytest.mark.parametrize("variant", ["subtrees", "subtrees32", "subtrees_fused_rhs", "leaf_phase", "all_levels", "off"])
 def test_level_products_match_oracle(variant):
     """Level products (Z_J = [L_JJ⁻¹; L_ext L_JJ⁻¹], one kernel per elimination-tree level) on a
     grid QP small enough for the dense oracle: the F-solve and the P_L PCG iterates against the oracle with
@@ -132,6 +132,8 @@ def test_level_products_match_oracle(variant):
     env = dict(PI_ENV)
     env.update({"subtrees": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8"},
                 "subtrees32": {"QPB_ST_MIN": "1", "QPB_ST_KB": "40"},
+                # Cᵀp gathered inside the sweep kernels (no pregather SpMV, no phase D in the fused step)
+                "subtrees_fused_rhs": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8", "QPB_PREGATHER": "0"},
                 "leaf_phase": {"QPB_LVL_MIN": "16", "QPB_ST": "0"}, "all_levels": {"QPB_LVL": "0", "QPB_ST": "0"},
                 "off": {"QPB_PI": "0"}}[variant])
     out = run_child(expr, env, False, extra=("fsolve",))
