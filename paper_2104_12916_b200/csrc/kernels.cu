@@ -2956,23 +2956,26 @@ __device__ __forceinline__ void sn16_fwd(const double* __restrict__ L, const dou
   for (int k = 0; k < 8; ++k) y += iv[k] * __shfl_sync(0xffffffffu, v, 8 * h + k);
   y += __shfl_xor_sync(0xffffffffu, y, 16);
   if (wl < wk) xdst[wl] = y;
-  double yc[16];
+  double sacc[SNW_P];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) yc[c] = __shfl_sync(0xffffffffu, y, c);
+  for (int p = 0; p < SNW_P; ++p) sacc[p] = 0.0;
 #pragma unroll
-  for (int p = 0; p < SNW_P; ++p) {
-    double sacc = 0.0;
+  for (int c = 0; c < 16; ++c) {   // y_c broadcast once per column, used by every pass (no y array in registers)
+    const double yc = __shfl_sync(0xffffffffu, y, c);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) sacc = fma(lr[p][c], yc[c], sacc);
-    if (wl + 32 * p < noff) atomicAdd(accw + rw[p], sacc);
+    for (int p = 0; p < SNW_P; ++p) sacc[p] = fma(lr[p][c], yc, sacc[p]);
   }
+#pragma unroll
+  for (int p = 0; p < SNW_P; ++p)
+    if (wl + 32 * p < noff) atomicAdd(accw + rw[p], sacc[p]);
   for (int r0 = 32 * SNW_P; r0 < noff; r0 += 32) {
     const int r = r0 + wl;
     const bool ok = r < noff;
     const int32_t g = ok ? __ldg(rows + r) : 0;
     double s2 = 0.0;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) s2 += ((ok && c < wk) ? __ldg(L + r + (int64_t)c * noff) : 0.0) * yc[c];
+    for (int c = 0; c < 16; ++c)
+      s2 += ((ok && c < wk) ? __ldg(L + r + (int64_t)c * noff) : 0.0) * __shfl_sync(0xffffffffu, y, c);
     if (ok) atomicAdd(accw + g, s2);
   }
 }
@@ -3234,7 +3237,9 @@ __global__ void __launch_bounds__(NT, G == 16 ? 3 : 2) k_st_bwd(DevFactor F, PiS
   tl_end(9, tls);
 }
 // Subtrees of ≤ 16-column supernodes: a warp per subtree, the whole warp on one supernode at a time
-// (sn16_fwd / sn16_bwd: one round trip per supernode, served by L2 after the subtree's prefetch).
+// (sn16_fwd / sn16_bwd: one round trip per supernode, served by L2 after the subtree's prefetch).  128 registers,
+// 2 CTAs per SM: at 3 CTAs per SM (80 registers, 152 bytes of spills) the kernels took 208 / 179 µs on c2 instead of
+// 110 / 111 µs.
 __global__ void __launch_bounds__(NT, 2) k_st16_fwd(DevFactor F, SweepRhs R, PiSweep P, double* x) {
   grid_dep_wait();
   grid_dep_launch();
