@@ -1742,7 +1742,7 @@ int qp_setup(qp_ctx** out, const qp_csr* H, const qp_csr* A, const qp_csr* C, co
 // Level products: plan and build Z_J = [X_J; L_ext,J X_J] for every supernode of F between the
 // leaf phase and the symmetric root, level by level (tiles of ≤ 512 rows × ≤ 64 columns, larger first).
 // Leaves F.pi.enabled = 0; the caller enables it after the accuracy guard.
-int build_pi(qp_ctx* c) {
+int build_pi(qp_ctx* c, bool allow_subtrees = true) {
   Factor& F = c->FF;
   const Symbolic& S = F.S;
   const int64_t ns = S.ns, Jr = ns - 1;
@@ -1762,7 +1762,7 @@ int build_pi(qp_ctx* c) {
     std::vector<char> ok(ns, 1), fits(ns, 0);
     bool post = true;
     for (int64_t J = 0; J < ns && post; ++J) post = S.sn_parent[J] < 0 || S.sn_parent[J] > J;
-    for (int64_t J = 0; post && !(se && se[0] == '0') && J < ns; ++J) {
+    for (int64_t J = 0; post && allow_subtrees && !(se && se[0] == '0') && J < ns; ++J) {
       const int64_t w = S.sn_start[J + 1] - S.sn_start[J], m = S.sn_rowptr[J + 1] - S.sn_rowptr[J], noff = m - w;
       const bool elig = J != Jr && S.sn_blk0[J + 1] - S.sn_blk0[J] == 1 && w <= 32 && S.sn_xinv[J] < 0 &&
                         noff < (int64_t(1) << 25);
@@ -2367,15 +2367,58 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
       F.d.flat = (F.flat_discrepancy <= 1e-10 && std::isfinite(F.flat_discrepancy)) ? 1 : 0;
       if (!F.d.flat) cudaMemsetAsync(F.d.acc, 0, N * 8, st);   // the sweeps expect zero accumulators
     }
-    // level products (deep forests: c2, c3s, c4s): same guard against the sweeps
+    // level products (deep forests: c2, c3s, c4s): the same guard against the sweeps, then the fastest of up
+    // to three paths is kept by TIMING them on this factor (median of 5 F-solves after 2 warm-ups each): the
+    // task graph, the level products over subtrees, and the level products over the leaf phase's level
+    // kernels.  Which wins depends on the tree — c2 (deep nested dissection): 1.34 / 0.81 / 0.88 ms; c3s (a
+    // shallow, unbalanced minimum-degree forest under a dominant root: its 8 291 subtrees are long chains
+    // of supernodes, 65 µs per sweep in one warp each): 0.166 / 0.210 / ≈ 0.12 ms.  QPB_PI=2 skips the task
+    // graph, QPB_ST=0 the subtrees, QPB_ST=2 the leaf-phase variant.
     const char* pe = std::getenv("QPB_PI");
     if (F.sym_enabled && !F.d.flat && !(pe && pe[0] == '0')) {
-      rc = build_pi(c);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      auto time_path = [&]() -> double {
+        std::vector<float> ts;
+        for (int rep = 0; rep < 7; ++rep) {
+          cudaEventRecord(e0, st);
+          f_solve_dev(c, c->rhs2, c->xbuf);
+          cudaEventRecord(e1, st);
+          cudaEventSynchronize(e1);
+          float ms = 0;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (rep >= 2) ts.push_back(ms);
+        }
+        std::sort(ts.begin(), ts.end());
+        return ts[ts.size() / 2];
+      };
+      auto zero_acc = [&]() {   // the sweeps expect zero accumulators
+        cudaMemsetAsync(F.d.acc, 0, N * 8, st);
+        cudaMemsetAsync(F.d.tacc, 0, N * 8, st);
+      };
+      // reference: the task graph
+      F.pi = PiSweep{};
+      cudaMemcpyAsync(c->rhs2, r.data(), N * 8, cudaMemcpyHostToDevice, st);
+      f_solve_dev(c, c->rhs2, c->xbuf);
+      cudaMemcpyAsync(y2.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+      rc = sync_check(c, "level-product reference");
       if (rc) return rc;
-      if (F.pi.nlev > 0) {
-        cudaMemcpyAsync(c->rhs2, r.data(), N * 8, cudaMemcpyHostToDevice, st);
-        f_solve_dev(c, c->rhs2, c->xbuf);
-        cudaMemcpyAsync(y2.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
+      const bool force = pe && pe[0] == '2';
+      const bool only_st = std::getenv("QPB_ST") && std::getenv("QPB_ST")[0] == '2';   // tests: subtrees or nothing
+      double best_ms = force ? 1e30 : time_path();
+      F.pi_ms[0] = force ? 0.0 : best_ms;
+      PiSweep best{};
+      double best_disc = -1.0;
+      for (int cand = 0; cand < 2; ++cand) {   // 0: over subtrees, 1: over the leaf phase
+        rc = build_pi(c, cand == 0);
+        if (rc) return rc;
+        PiSweep P = F.pi;
+        if (P.nlev <= 0 || (cand == 1 && best.nlev > 0 && best.st_n == 0)) {   // nothing built / same plan as candidate 0
+          F.pi = best;
+          if (cand == 0) continue;
+          break;
+        }
         F.pi.enabled = 1;
         f_solve_dev(c, c->rhs2, c->xbuf);
         cudaMemcpyAsync(y1.data(), c->xbuf, N * 8, cudaMemcpyDeviceToHost, st);
@@ -2386,56 +2429,42 @@ int ipm_factor_once(qp_ctx* c, const double* D0, qp_precond p) {
           fd += (y1[i] - y2[i]) * (y1[i] - y2[i]);
           fn += y2[i] * y2[i];
         }
-        F.pi_discrepancy = fn > 0 ? std::sqrt(fd / fn) : 0.0;
-        F.pi.enabled = (F.pi_discrepancy <= 1e-10 && std::isfinite(F.pi_discrepancy)) ? 1 : 0;
+        const double disc = fn > 0 ? std::sqrt(fd / fn) : 0.0;
+        const bool ok = disc <= 1e-10 && std::isfinite(disc);
+        const double ms = ok ? time_path() : 1e30;
+        if (ok && (F.pi_ms[1] == 0.0 || ms < F.pi_ms[1])) F.pi_ms[1] = ms;   // the faster level-product variant
+        rc = cuda_check(c, "level-product timing");
+        if (rc) return rc;
         if (std::getenv("QPB_VERBOSE"))
-          std::fprintf(stderr, "qpb: level-product guard %.3e -> %s\n", F.pi_discrepancy, F.pi.enabled ? "on" : "off");
-        // Which path is faster depends on the tree (c2: deep nested dissection, 1.45 → 0.87 ms per F-solve;
-        // c3s: a shallow minimum-degree forest under a dominant root, 0.19 → 0.26 ms), so time both on this
-        // factor: the median of 5 F-solves each after 2 warm-ups (QPB_PI=2 forces the level products).
-        if (F.pi.enabled && !(pe && pe[0] == '2')) {
-          cudaEvent_t e0, e1;
-          cudaEventCreate(&e0);
-          cudaEventCreate(&e1);
-          double med[2] = {0, 0};
-          for (int mode = 1; mode >= 0; --mode) {
-            F.pi.enabled = mode;
-            if (!mode) {   // the sweeps expect zero accumulators
-              cudaMemsetAsync(F.d.acc, 0, N * 8, st);
-              cudaMemsetAsync(F.d.tacc, 0, N * 8, st);
-            }
-            std::vector<float> ts;
-            for (int rep = 0; rep < 7; ++rep) {
-              cudaEventRecord(e0, st);
-              f_solve_dev(c, c->rhs2, c->xbuf);
-              cudaEventRecord(e1, st);
-              cudaEventSynchronize(e1);
-              float ms = 0;
-              cudaEventElapsedTime(&ms, e0, e1);
-              if (rep >= 2) ts.push_back(ms);
-            }
-            std::sort(ts.begin(), ts.end());
-            med[mode] = ts[ts.size() / 2];
-          }
-          cudaEventDestroy(e0);
-          cudaEventDestroy(e1);
-          rc = cuda_check(c, "level-product timing");
-          if (rc) return rc;
-          F.pi_ms[0] = med[0];
-          F.pi_ms[1] = med[1];
-          bool faster = med[1] < med[0];
-          if (c->sharded)
-            if (int rc3 = agree_all(c, faster)) return rc3;
-          F.pi.enabled = faster ? 1 : 0;   // acc / tacc are zero here (the sweeps ran last)
-          if (std::getenv("QPB_VERBOSE"))
-            std::fprintf(stderr, "qpb: F-solve %.3f ms with level products, %.3f ms with the task graph -> %s\n", med[1],
-                         med[0], F.pi.enabled ? "level products" : "task graph");
+          std::fprintf(stderr, "qpb: level products over %s: guard %.3e, F-solve %.3f ms (task graph %.3f ms)\n",
+                       P.st_n > 0 ? "subtrees" : "the leaf phase", disc, ok ? ms : -1.0, F.pi_ms[0]);
+        if (cand == 0 || best.nlev == 0) F.pi_discrepancy = disc;
+        bool better = ok && ms < best_ms;
+        if (c->sharded)
+          if (int rc3 = agree_all(c, better)) return rc3;
+        if (better) {
+          if (best.Z) F.mem.free_ptr(best.Z);
+          best = F.pi;
+          best.enabled = 1;
+          best_ms = ms;
+          best_disc = disc;
+        } else if (P.Z) {
+          F.mem.free_ptr(P.Z);
         }
-        if (!F.pi.enabled) {   // the sweeps expect zero accumulators
-          cudaMemsetAsync(F.d.acc, 0, N * 8, st);
-          cudaMemsetAsync(F.d.tacc, 0, N * 8, st);
-        }
+        F.pi = PiSweep{};
+        if (cand == 0 && (P.st_n == 0 || only_st)) break;   // no subtrees planned (the second candidate is the same plan) / QPB_ST=2
       }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      F.pi = best;
+      if (best.enabled) {
+        F.pi_discrepancy = best_disc;
+        if (!F.d.flat) F.d.fl_rc0 = F.pi.root0;
+      }
+      zero_acc();
+      if (std::getenv("QPB_VERBOSE"))
+        std::fprintf(stderr, "qpb: F-solve path: %s\n", !F.pi.enabled ? "task graph" : F.pi.st_n > 0
+                     ? "level products over subtrees" : "level products over the leaf phase");
     }
   }
   if (int rc2 = build_dense_w(c)) return rc2;   // explicit W / small-N F⁻¹ (with or without a symmetric root)

@@ -130,10 +130,10 @@ def test_level_products_match_oracle(variant):
     expr = "qpgen.make_grid_qp(48, 80, 200, seed=9, name='grid48')"
     qp = eval(expr)
     env = dict(PI_ENV)
-    env.update({"subtrees": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8"},
-                "subtrees32": {"QPB_ST_MIN": "1", "QPB_ST_KB": "40"},
+    env.update({"subtrees": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8", "QPB_ST": "2"},
+                "subtrees32": {"QPB_ST_MIN": "1", "QPB_ST_KB": "40", "QPB_ST": "2"},
                 # Cᵀp gathered inside the sweep kernels (no pregather SpMV, no phase D in the fused step)
-                "subtrees_fused_rhs": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8", "QPB_PREGATHER": "0"},
+                "subtrees_fused_rhs": {"QPB_ST_MIN": "1", "QPB_ST_KB": "8", "QPB_PREGATHER": "0", "QPB_ST": "2"},
                 "leaf_phase": {"QPB_LVL_MIN": "16", "QPB_ST": "0"}, "all_levels": {"QPB_LVL": "0", "QPB_ST": "0"},
                 "off": {"QPB_PI": "0"}}[variant])
     out = run_child(expr, env, False, extra=("fsolve",))
