@@ -234,10 +234,13 @@ def run_reference(args, rank, world):
     import qpgen
     qp = qpgen.make(args.config)
     o = OracleSampler(qp, qp.x_perm)
-    o.sample(1)                                   # warm-up
+    _, t_it = o.sample(1)                         # warm-up; also sizes the per-step sample
+    # bounded sample: at most --cpu-iters PCG iterations per step, fewer when K steps of them would take
+    # more than about three minutes on this host (the metric, iterations/s, does not depend on the count)
+    per_step = max(1, min(args.cpu_iters, int(180.0 / max(args.steps * t_it, 1e-9))))
     its, dts = 0, 0.0
     for k in range(args.steps):
-        it, dt = o.sample(args.cpu_iters)
+        it, dt = o.sample(per_step)
         its += it
         dts += dt
     value = its / dts if dts > 0 else 0.0
@@ -248,7 +251,7 @@ def run_reference(args, rank, world):
         "config": {"workload": f"{args.config} PL-KF (CPU oracle: dense block-inverse F-solve, textbook PCG)",
                    "n": qp.n, "m1": qp.m1, "m2": qp.m2},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": o.cores, "kind": "oracle",
-                         "sample": f"{args.steps} x {args.cpu_iters} PCG iterations of IPM step 0 on {args.config} "
+                         "sample": f"{args.steps} x {per_step} PCG iterations of IPM step 0 on {args.config} "
                                    f"(oracle F setup {o.t_setup:.1f} s excluded)", "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
